@@ -1,0 +1,233 @@
+/*
+ * bigmac.h -- C ABI of the B200-native BigMac nested-pipeline step.
+ *
+ * Paper: "BigMac" (arxiv 2605.25451), PAPER.md line numbers cited as P:<line>.
+ * The paper's statement of the problem is
+ *     train_step(data_iter, pp_size, microbatch_num, warmup_bound)
+ *       = get_llm_schedule -> build_schedule -> insert_comm_ops
+ *         -> deadlock_check -> create_executor -> load_schedule -> execute
+ * This header exposes exactly those steps:
+ *     bm_build_schedule       get_llm_schedule + build_schedule + insert_comm_ops
+ *                             + deadlock_check (+ receive-ring sizing)
+ *     bm_ctx_create/_bind     create_executor + load_schedule
+ *     bm_step                 execute (one training step of the nested pipeline) P:323
+ *
+ * Conventions
+ *   - Every function returns bm_status; on failure bm_last_error() returns a
+ *     thread-local message valid until the next bm_* call on that thread.
+ *   - No C++ exceptions cross this boundary.  No torch types appear here.
+ *   - "device pointer" = CUDA global memory of the calling process's current
+ *     device; "host pointer" = ordinary (preferably pinned) host memory.
+ *   - The library owns bm_schedule and bm_ctx objects; it never frees memory
+ *     it did not allocate.  All large device buffers (weights, grads,
+ *     workspace, receive arena) are allocated by the caller and bound with
+ *     bm_ctx_bind.
+ */
+#ifndef BIGMAC_H
+#define BIGMAC_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  BM_OK = 0,
+  BM_E_INVALID = 1,     /* bad ranges / inconsistent arguments                       */
+  BM_E_REMAINDER = 2,   /* M % P != 0: units of pp_size micro-batches */
+  BM_E_WARMUP = 3,      /* W < W*: some F_u precedes EncFwd(u)         */
+  BM_E_DEPENDENCY = 4,  /* verification failed (should be unreachable)               */
+  BM_E_DEADLOCK = 5,    /* happens-before graph incl. credit edges is cyclic */
+  BM_E_CUDA = 6,
+  BM_E_NCCL = 7,
+  BM_E_OOM = 8,         /* a bound buffer is smaller than required                   */
+  BM_E_STATE = 9,       /* call out of order (e.g. bm_step before bm_ctx_bind)      */
+  BM_E_TIMEOUT = 10
+} bm_status;
+
+typedef enum { BM_LLM_1F1B = 0, BM_LLM_INTERLEAVED = 1 } bm_llm_sched;
+typedef enum { BM_ENC_NONE = 0, BM_ENC_DP_UNIT = 1 } bm_enc_place;
+typedef enum { BM_GEN_NONE = 0, BM_GEN_DP_SHARD = 1, BM_GEN_LAST_STAGE = 2 } bm_gen_place;
+
+typedef enum {
+  BM_OP_ENC_FWD = 0, BM_OP_ENC_BWD = 1, BM_OP_LLM_FWD = 2, BM_OP_LLM_BWD = 3,
+  BM_OP_GEN_FWD = 4, BM_OP_GEN_BWD = 5, BM_OP_SEND = 6, BM_OP_RECV = 7
+} bm_op_kind;   /* compute vs communication operators */
+
+typedef enum {
+  BM_PAY_NONE = -1,
+  BM_PAY_ACT = 0,      /* LLM stage-boundary activation, stage s -> s+1  */
+  BM_PAY_GRAD = 1,     /* LLM stage-boundary gradient, s -> s-1              */
+  BM_PAY_EMB = 2,      /* encoder output gathered to the entry stage          */
+  BM_PAY_EMBGRAD = 3,  /* input-embedding gradient scattered to the encoder rank */
+  BM_PAY_GENIN = 4,    /* last stage scatters generator inputs                */
+  BM_PAY_GENGRAD = 5   /* generator input-gradients gathered back             */
+} bm_payload;
+
+/* Scheduler configuration (pp_size, microbatch_num, warmup_bound).
+ * warmup_units == 0 selects W* (the minimal dependency-safe warmup, R4).
+ * cost_fwd:cost_bwd is the cut-timeline cost ratio that defines "columns"
+ * (R1), default 1:2.  ring_slack adds receive slots
+ * above the minimal deadlock-free ring size. */
+typedef struct {
+  int32_t stages;        /* P >= 1                       */
+  int32_t microbatches;  /* M >= 1, M % P == 0           */
+  int32_t vchunks;       /* V >= 1 (V >= 2 iff interleaved) */
+  int32_t warmup_units;  /* W >= 0; 0 => W*              */
+  int32_t llm_sched;     /* bm_llm_sched                 */
+  int32_t enc_place;     /* bm_enc_place                 */
+  int32_t gen_place;     /* bm_gen_place                 */
+  int32_t cost_fwd;      /* >= 1                         */
+  int32_t cost_bwd;      /* >= 1                         */
+  int32_t ring_slack;    /* >= 0                         */
+  int32_t reserved[6];   /* must be zero                 */
+} bm_sched_cfg;
+
+/* One operator of a rank's list.  -1 marks an absent field.
+ *   EncFwd/EncBwd: mb = unit*P + rank, unit
+ *   LlmFwd/LlmBwd: mb, chunk
+ *   GenFwd/GenBwd: mb (row shard = rank under BM_GEN_DP_SHARD)
+ *   Send/Recv:     mb, chunk (act/grad), unit (emb/embgrad), peer, payload,
+ *                  slot (= seq mod ring size), seq (per-channel message index) */
+typedef struct {
+  int32_t kind, mb, chunk, unit, peer, payload, slot, seq;
+} bm_op;
+
+typedef struct {
+  int32_t w_star;             /* minimal warmup (P:216 analysis)                  */
+  int32_t warmup_units;       /* W used                                            */
+  int32_t peak_enc_units;     /* max live EncFwd-EncBwd on this rank (<= W) */
+  int32_t peak_gen_shards;    /* max live GenFwd-GenBwd (1)                */
+  int32_t peak_llm_inflight;  /* max live LLM F-B (unchanged LLM schedule)  */
+  int32_t n_ops;              /* ops incl. comm on this rank                       */
+  int64_t llm_idle_cost_units;/* makespan - busy in the cut-timeline DES           */
+  int64_t makespan_cost_units;
+  int32_t ring_slots[6];      /* max receive ring size per payload on this rank   */
+} bm_sched_stats;
+
+typedef struct bm_schedule bm_schedule;
+
+/* Build, nest, insert comm ops, size rings and verify.  *out is owned by the
+ * library; free with bm_schedule_free.  Pure and reentrant. */
+bm_status bm_build_schedule(const bm_sched_cfg* cfg, bm_schedule** out);
+/* Borrowed view of rank's op list; valid until bm_schedule_free. */
+bm_status bm_schedule_rank_ops(const bm_schedule* s, int32_t rank, const bm_op** ops, int64_t* n);
+bm_status bm_schedule_stats(const bm_schedule* s, int32_t rank, bm_sched_stats* out);
+/* Ring size K and message count of channel (src -> dst, payload); K = nmsg = 0 if absent. */
+bm_status bm_schedule_ring(const bm_schedule* s, int32_t src, int32_t dst, int32_t payload,
+                           int32_t* K, int32_t* nmsg);
+/* Text serialization "rank\tindex\tkind\tmb\tchunk\tunit\tpeer\tpayload\tslot\tseq\n"
+ * ('-' = absent).  Call with cap = 0 to get *needed (bytes incl. the NUL). */
+bm_status bm_schedule_serialize(const bm_schedule* s, char* buf, size_t cap, size_t* needed);
+void bm_schedule_free(bm_schedule* s);
+const char* bm_last_error(void);
+
+/* ------------------------------------------------------------------------ */
+/* Synthetic MLLM model: encoder + projector (DP),      */
+/* LLM (pipeline stages), generator (DP row shards).                        */
+/* ------------------------------------------------------------------------ */
+typedef enum { BM_BF16 = 0, BM_F32 = 1 } bm_dtype;
+
+typedef struct {
+  int32_t S;                      /* LLM sequence length                      */
+  int32_t d_in, d_e, f_e, L_e;    /* encoder                                  */
+  int32_t d, f, L, vocab;         /* LLM (d is also the projector width)      */
+  int32_t d_g, f_g, L_g, d_t;     /* generator                                */
+  int32_t dtype;                  /* bm_dtype of weights/activations           */
+  int32_t max_n_mod, max_n_gen;   /* upper bounds on per-sample row counts     */
+  int32_t reserved[8];
+} bm_model_cfg;
+
+/* Parameter kinds: DP parameters (encoder, projector, generator) are summed
+ * over ranks at step end; LLM parameters belong to one stage. */
+typedef enum { BM_PARAM_DP = 0, BM_PARAM_LLM = 1 } bm_param_kind;
+
+typedef struct {
+  char name[48];      /* synth.param_specs name, e.g. "llm.layer3.gate_up" */
+  int32_t rows, cols; /* [out, in]; norm gains: rows = n, cols = 1          */
+  int64_t offset;     /* element offset into the weight and grad buffers    */
+  int32_t kind;       /* bm_param_kind                                      */
+  int32_t reserved;
+} bm_param_info;
+
+/* Parameters held by `rank` under `sc` (layers of its virtual stages; the
+ * text table on rank 0, final norm + head on rank P-1; DP params everywhere).
+ * DP parameters occupy the prefix [0, *dp_elems) of the buffers. */
+bm_status bm_param_count(const bm_model_cfg* mc, const bm_sched_cfg* sc, int32_t rank,
+                         int32_t* n, int64_t* total_elems, int64_t* dp_elems);
+bm_status bm_param_info_get(const bm_model_cfg* mc, const bm_sched_cfg* sc, int32_t rank,
+                            int32_t idx, bm_param_info* out);
+
+/* ------------------------------------------------------------------------ */
+/* Executor                                                     */
+/* ------------------------------------------------------------------------ */
+typedef struct bm_ctx bm_ctx;
+
+typedef struct {
+  int64_t weight_bytes;  /* total_elems * sizeof(dtype)                          */
+  int64_t grad_bytes;    /* total_elems * 4 (fp32 accumulation)                  */
+  int64_t work_bytes;    /* activations stash, scratch, per-step batch staging   */
+  int64_t comm_bytes;    /* receive slots + flags, exported to peers via IPC     */
+} bm_ctx_sizes;
+
+typedef struct {
+  void* weights;   /* device, weight_bytes, filled by the caller                 */
+  void* grads;     /* device, grad_bytes (zeroed by bm_step)                     */
+  void* work;      /* device, work_bytes                                         */
+  void* comm;      /* device, comm_bytes (zeroed by the caller before binding)   */
+} bm_buffers;
+
+/* Create the per-rank executor for `rank` of schedule s (s must outlive ctx). */
+bm_status bm_ctx_create(const bm_model_cfg* mc, const bm_schedule* s, int32_t rank, bm_ctx** out);
+bm_status bm_ctx_sizes_get(const bm_ctx* c, bm_ctx_sizes* out);
+bm_status bm_ctx_bind(bm_ctx* c, const bm_buffers* b);
+
+/* Peer memory (CUDA IPC over NVLink).  Export any device pointer as a 64-byte
+ * handle + byte offset into its allocation; peers import it with
+ * bm_ctx_open_peer (their `comm` buffer).  Exchange is done by the caller. */
+bm_status bm_ipc_export(const void* dptr, uint8_t handle[64], int64_t* offset);
+bm_status bm_ctx_open_peer(bm_ctx* c, int32_t peer, const uint8_t handle[64], int64_t offset);
+
+/* Data-parallel gradient sum over the P ranks (NCCL).  Rank 0 creates
+ * the id, the caller broadcasts it. */
+bm_status bm_nccl_unique_id(uint8_t id[128]);
+bm_status bm_ctx_init_nccl(bm_ctx* c, const uint8_t id[128], int32_t nranks, int32_t rank);
+
+/* One step's inputs.  If on_host != 0 the array pointers are host pointers
+ * and bm_step copies them to the device inside the step (end-to-end path).
+ * Row counts are always host arrays.  All ranks receive the full batch. */
+typedef struct {
+  int32_t M;
+  const int32_t* n_mod;     /* host [M]                                            */
+  const int32_t* n_gen;     /* host [M]                                            */
+  const void* patches;      /* [sum n_mod, ld_patch] dtype, microbatch-major       */
+  int32_t ld_patch;         /* >= d_in, multiple of 8                              */
+  const int32_t* ids;       /* [M, S]                                              */
+  const int32_t* labels;    /* [M, S]                                              */
+  const void* targets;      /* [sum n_gen, d_t] dtype                              */
+  int32_t on_host;
+  int32_t reserved[7];
+} bm_batch;
+
+/* Enqueue one training step on `stream` (cudaStream_t; 0 = legacy default).
+ * Asynchronous.  Zeroes grads, runs the rank's op list, allreduces DP grads
+ * and the loss terms, and leaves the results in the bound buffers. */
+bm_status bm_step(bm_ctx* c, const bm_batch* batch, void* stream);
+
+/* Device pointer to float[2*M + 1]: per-mb CE, per-mb MSE (sums over ranks
+ * after bm_step), and the step loss L = (1/M) sum (CE_m + MSE_m). */
+bm_status bm_ctx_loss_ptr(const bm_ctx* c, const float** dptr);
+
+/* Number of kernels this rank launched in its last bm_step (kernel census). */
+bm_status bm_ctx_launch_count(const bm_ctx* c, int64_t* n);
+/* Peak bytes of stash memory live during the last step, per module
+ * (0 encoder, 1 LLM, 2 generator) -- the schedule's activation footprint. */
+bm_status bm_ctx_stash_peak(const bm_ctx* c, int64_t out[3]);
+void bm_ctx_destroy(bm_ctx* c);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BIGMAC_H */

@@ -1,0 +1,92 @@
+/*
+ * bigmac_kernels.h -- C ABI of the individual sm_100a kernels the executor
+ * uses for the model's compute (one entry point per device op on the hot path).
+ * They exist so parity tests can check each kernel against the oracle; the
+ * executor calls the same launchers internally.
+ *
+ * All pointers are device pointers unless noted; `stream` is a cudaStream_t
+ * (0 = legacy default).  dtype is bm_dtype (0 bf16, 1 fp32).  Errors are
+ * reported as bm_status with bm_last_error() (bigmac.h).  Launches are
+ * asynchronous; argument errors are detected on the host before launch.
+ */
+#ifndef BIGMAC_KERNELS_H
+#define BIGMAC_KERNELS_H
+
+#include "bigmac.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* GEMM epilogues */
+typedef enum {
+  BM_EPI_STORE = 0,   /* C = alpha*acc            (C dtype = c_dtype)           */
+  BM_EPI_ACCUM = 1,   /* C += alpha*acc           (C must be fp32; wgrad, β = 1) */
+  BM_EPI_ADD = 2      /* C = alpha*acc + R        (R has c_dtype; residual add)  */
+} bm_epilogue;
+
+/* C[m, n] = sum_k A(m, k) * B(n, k), fp32 accumulation.
+ *   A(m, k) = A[m*lda + k] if a_major == 0 (K-major) else A[k*lda + m] (MN-major)
+ *   B(n, k) = B[n*ldb + k] if b_major == 0 (K-major) else B[k*ldb + n] (MN-major)
+ *   C[m*ldc + n], R[m*ldr + n].
+ * dtype of A/B: BM_BF16 -> tcgen05.mma kind::f16 tiles fed by TMA (TMEM
+ * accumulators); BM_F32 -> exact fp32 FFMA kernel (no TF32; parity mode).
+ * Requirements (bf16): lda, ldb multiples of 8 elements, A/B 16-byte aligned.
+ * The dense block contractions of the model (Linear layers of the
+ * encoder, LLM and generator) are all instances: forward X W^T (A, B K-major),
+ * data-grad dY W (B MN-major), weight-grad dY^T X (A, B MN-major, ACCUM). */
+bm_status bm_k_gemm(int32_t dtype, int32_t M, int32_t N, int32_t K,
+                    const void* A, int64_t lda, int32_t a_major,
+                    const void* B, int64_t ldb, int32_t b_major,
+                    void* C, int64_t ldc, int32_t c_dtype, int32_t epilogue,
+                    const void* R, int64_t ldr, float alpha, void* stream);
+
+/* RMSNorm y = x * rstd * g, rstd = 1/sqrt(mean(x^2) + 1e-5); rstd saved (fp32 [rows]). */
+bm_status bm_k_rmsnorm_fwd(int32_t dtype, int32_t rows, int32_t cols, const void* x,
+                           const void* g, void* y, float* rstd, void* stream);
+/* dx = rstd*(dy*g - xhat*mean(dy*g*xhat)) [+ dres];  dg += sum_rows dy*xhat (fp32).
+ * dres may be NULL; dx may alias dres.  `partial` is fp32 scratch of
+ * bm_k_rmsnorm_bwd_scratch(rows, cols) floats. */
+bm_status bm_k_rmsnorm_bwd(int32_t dtype, int32_t rows, int32_t cols, const void* dy,
+                           const void* x, const void* g, const float* rstd, const void* dres,
+                           void* dx, float* dg, float* partial, void* stream);
+int64_t bm_k_rmsnorm_bwd_scratch(int32_t rows, int32_t cols);
+
+/* h[i, j] = silu(gu[i, j]) * gu[i, f + j]   (gu: [rows, 2f], h: [rows, f]) */
+bm_status bm_k_swiglu_fwd(int32_t dtype, int32_t rows, int32_t f, const void* gu, void* h, void* stream);
+/* dgu = [dh*u*s*(1 + g(1-s)), dh*g*s],  s = sigmoid(g) */
+bm_status bm_k_swiglu_bwd(int32_t dtype, int32_t rows, int32_t f, const void* dh, const void* gu,
+                          void* dgu, void* stream);
+/* z = gelu_tanh(a);  da = dz * gelu_tanh'(a)  (n elements) */
+bm_status bm_k_gelu_fwd(int32_t dtype, int64_t n, const void* a, void* z, void* stream);
+bm_status bm_k_gelu_bwd(int32_t dtype, int64_t n, const void* dz, const void* a, void* da, void* stream);
+
+/* embed_preprocess: X[i] = emb[i] for i < n_mod, else table[ids[i]] */
+bm_status bm_k_embed_fwd(int32_t dtype, int32_t S, int32_t d, int32_t n_mod, const int32_t* ids,
+                         const void* table, const void* emb, void* X, void* stream);
+/* text-table gradient: dT[ids[i]] += dX[i] for i in [n_mod, S), deterministic
+ * (sorted segmented sum).  dT fp32.  scratch: bm_k_embed_bwd_scratch(S) bytes. */
+bm_status bm_k_embed_bwd(int32_t dtype, int32_t S, int32_t d, int32_t n_mod, const int32_t* ids,
+                         const void* dX, float* dT, void* scratch, void* stream);
+int64_t bm_k_embed_bwd_scratch(int32_t S);
+
+/* Cross-entropy over rows of logits [n, V]: loss_out[0] (+)= scale_loss * mean_i
+ * (lse_i - z[i, label_i]); logits overwritten with dz = (softmax - onehot) * scale_grad.
+ * accumulate != 0 adds into *loss_out.  scratch: n floats. */
+bm_status bm_k_ce_fwd_bwd(int32_t dtype, int32_t n, int32_t V, void* logits, const int32_t* labels,
+                          float scale_grad, float* loss_out, float scale_loss, int32_t accumulate,
+                          float* scratch, void* stream);
+/* MSE shard: loss_out[0] += sum((out - t)^2) / denom * scale_loss;
+ * dout = 2 (out - t) / denom * scale_grad  (out, t, dout: [n, dt]) */
+bm_status bm_k_mse_fwd_bwd(int32_t dtype, int32_t n, int32_t dt, const void* out, const void* t,
+                           float denom, float scale_grad, float scale_loss, float* loss_out,
+                           void* dout, void* stream);
+
+/* Elementwise helpers used by the executor. */
+bm_status bm_k_add(int32_t dtype, int64_t n, const void* a, const void* b, void* out, void* stream);
+bm_status bm_k_cast(int32_t src_dtype, int32_t dst_dtype, int64_t n, const void* src, void* dst, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BIGMAC_KERNELS_H */

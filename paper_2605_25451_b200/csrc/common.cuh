@@ -1,0 +1,74 @@
+// common.cuh -- shared helpers for the sm_100a kernels and the executor.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdio>
+#include <string>
+
+#include "../../include/bigmac.h"
+#include "../../include/bigmac_kernels.h"
+
+namespace bm {
+
+// thread-local error message (bm_last_error)
+void set_error(const std::string& msg);
+const char* get_error();
+
+struct Err {
+  bm_status code;
+  std::string msg;
+};
+
+#define BM_CUDA_TRY(expr)                                                          \
+  do {                                                                             \
+    cudaError_t _e = (expr);                                                       \
+    if (_e != cudaSuccess) {                                                       \
+      ::bm::set_error(std::string(#expr) + ": " + cudaGetErrorString(_e) + " @" +  \
+                      __FILE__ + ":" + std::to_string(__LINE__));                  \
+      return BM_E_CUDA;                                                            \
+    }                                                                              \
+  } while (0)
+
+#define BM_TRY(expr)                 \
+  do {                               \
+    bm_status _s = (expr);           \
+    if (_s != BM_OK) return _s;      \
+  } while (0)
+
+#define BM_CHECK_ARG(cond, msg)                      \
+  do {                                               \
+    if (!(cond)) {                                   \
+      ::bm::set_error(std::string("invalid argument: ") + (msg)); \
+      return BM_E_INVALID;                           \
+    }                                                \
+  } while (0)
+
+typedef __nv_bfloat16 bf16;
+
+template <typename T> struct DT;
+template <> struct DT<bf16> { static constexpr int id = BM_BF16; };
+template <> struct DT<float> { static constexpr int id = BM_F32; };
+
+__device__ __forceinline__ float to_f(bf16 v) { return __bfloat162float(v); }
+__device__ __forceinline__ float to_f(float v) { return v; }
+template <typename T> __device__ __forceinline__ T from_f(float v);
+template <> __device__ __forceinline__ bf16 from_f<bf16>(float v) { return __float2bfloat16_rn(v); }
+template <> __device__ __forceinline__ float from_f<float>(float v) { return v; }
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+inline int ceil_div(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
+
+int num_sms();
+
+// launch census (kernels launched through the library)
+void count_launch(int n = 1);
+int64_t launch_count();
+
+}  // namespace bm

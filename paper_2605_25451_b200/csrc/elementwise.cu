@@ -1,0 +1,552 @@
+// elementwise.cu -- HBM-bound kernels of the step: RMSNorm fwd/bwd, SwiGLU,
+// GELU, embed_preprocess fwd/bwd, cross-entropy and MSE losses.
+//
+// All kernels move 16-byte vectors (8 bf16 / 4 fp32 per access), keep
+// reductions in fp32 with fixed (deterministic) shuffle/shared-memory trees,
+// and accumulate weight-like gradients (RMSNorm gains, text table) through
+// deterministic two-pass reductions so reruns are bitwise identical.
+#include <cfloat>
+
+#include "common.cuh"
+
+namespace bm {
+
+// ------------------------------------------------------------------ vectors
+template <typename T> struct V16;
+template <> struct V16<bf16> {
+  static constexpr int N = 8;
+  uint4 raw;
+  __device__ __forceinline__ float get(int i) const { return __bfloat162float(reinterpret_cast<const bf16*>(&raw)[i]); }
+  __device__ __forceinline__ void set(int i, float v) { reinterpret_cast<bf16*>(&raw)[i] = __float2bfloat16_rn(v); }
+};
+template <> struct V16<float> {
+  static constexpr int N = 4;
+  float4 raw;
+  __device__ __forceinline__ float get(int i) const { return reinterpret_cast<const float*>(&raw)[i]; }
+  __device__ __forceinline__ void set(int i, float v) { reinterpret_cast<float*>(&raw)[i] = v; }
+};
+template <typename T> __device__ __forceinline__ V16<T> vload(const T* p) {
+  V16<T> v;
+  v.raw = *reinterpret_cast<const decltype(v.raw)*>(p);
+  return v;
+}
+template <typename T> __device__ __forceinline__ void vstore(T* p, const V16<T>& v) {
+  *reinterpret_cast<decltype(v.raw)*>(p) = v.raw;
+}
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+// deterministic block reduction (blockDim.x multiple of 32, <= 1024)
+__device__ __forceinline__ float block_sum(float v, float* sh) {
+  v = warp_sum(v);
+  const int w = threadIdx.x / 32, l = threadIdx.x % 32;
+  __syncthreads();
+  if (l == 0) sh[w] = v;
+  __syncthreads();
+  const int nw = blockDim.x / 32;
+  float r = (threadIdx.x < nw) ? sh[threadIdx.x] : 0.f;
+  if (w == 0) r = warp_sum(r);
+  if (threadIdx.x == 0) sh[0] = r;
+  __syncthreads();
+  r = sh[0];
+  __syncthreads();
+  return r;
+}
+__device__ __forceinline__ float block_max(float v, float* sh) {
+  v = warp_max(v);
+  const int w = threadIdx.x / 32, l = threadIdx.x % 32;
+  __syncthreads();
+  if (l == 0) sh[w] = v;
+  __syncthreads();
+  const int nw = blockDim.x / 32;
+  float r = (threadIdx.x < nw) ? sh[threadIdx.x] : -FLT_MAX;
+  if (w == 0) r = warp_max(r);
+  if (threadIdx.x == 0) sh[0] = r;
+  __syncthreads();
+  r = sh[0];
+  __syncthreads();
+  return r;
+}
+
+constexpr float RMS_EPS = 1e-5f;
+constexpr float GELU_C = 0.7978845608028654f;  // sqrt(2/pi)
+
+__device__ __forceinline__ float gelu_f(float a) {
+  return 0.5f * a * (1.f + tanhf(GELU_C * (a + 0.044715f * a * a * a)));
+}
+__device__ __forceinline__ float gelu_grad(float a) {
+  const float t = tanhf(GELU_C * (a + 0.044715f * a * a * a));
+  return 0.5f * (1.f + t) + 0.5f * a * (1.f - t * t) * GELU_C * (1.f + 3.f * 0.044715f * a * a);
+}
+
+// ------------------------------------------------------------------ RMSNorm
+template <typename T>
+__global__ void rmsnorm_fwd_kernel(int rows, int cols, const T* __restrict__ x, const T* __restrict__ g,
+                                   T* __restrict__ y, float* __restrict__ rstd) {
+  constexpr int N = V16<T>::N;
+  const int warps = blockDim.x / 32;
+  const int row = blockIdx.x * warps + threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  if (row >= rows) return;
+  const T* xr = x + (int64_t)row * cols;
+  float ss = 0.f;
+  for (int c = lane * N; c < cols; c += 32 * N) {
+    V16<T> v = vload(xr + c);
+#pragma unroll
+    for (int i = 0; i < N; ++i) { float f = v.get(i); ss += f * f; }
+  }
+  ss = warp_sum(ss);
+  const float r = rsqrtf(ss / cols + RMS_EPS);
+  if (lane == 0) rstd[row] = r;
+  T* yr = y + (int64_t)row * cols;
+  for (int c = lane * N; c < cols; c += 32 * N) {
+    V16<T> v = vload(xr + c), gv = vload(g + c), o;
+#pragma unroll
+    for (int i = 0; i < N; ++i) o.set(i, v.get(i) * r * gv.get(i));
+    vstore(yr + c, o);
+  }
+}
+
+template <typename T>
+__global__ void rmsnorm_bwd_kernel(int rows, int cols, const T* __restrict__ dy, const T* __restrict__ x,
+                                   const T* __restrict__ g, const float* __restrict__ rstd, const T* dres, T* dx) {
+  constexpr int N = V16<T>::N;
+  const int warps = blockDim.x / 32;
+  const int row = blockIdx.x * warps + threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  if (row >= rows) return;
+  const int64_t off = (int64_t)row * cols;
+  const float r = rstd[row];
+  float dot = 0.f;
+  for (int c = lane * N; c < cols; c += 32 * N) {
+    V16<T> dv = vload(dy + off + c), xv = vload(x + off + c), gv = vload(g + c);
+#pragma unroll
+    for (int i = 0; i < N; ++i) dot += dv.get(i) * gv.get(i) * xv.get(i) * r;
+  }
+  dot = warp_sum(dot) / cols;
+  for (int c = lane * N; c < cols; c += 32 * N) {
+    V16<T> dv = vload(dy + off + c), xv = vload(x + off + c), gv = vload(g + c), o;
+    V16<T> rv;
+    if (dres) rv = vload(dres + off + c);
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      float v = r * (dv.get(i) * gv.get(i) - xv.get(i) * r * dot);
+      if (dres) v += rv.get(i);
+      o.set(i, v);
+    }
+    vstore(dx + off + c, o);
+  }
+}
+
+// partial[chunk][col] = sum_{rows in chunk} dy * x * rstd
+template <typename T>
+__global__ void rmsnorm_dg_partial_kernel(int rows, int cols, int nchunk, const T* __restrict__ dy,
+                                          const T* __restrict__ x, const float* __restrict__ rstd,
+                                          float* __restrict__ partial) {
+  const int col = blockIdx.x * blockDim.x + threadIdx.x;
+  const int chunk = blockIdx.y;
+  if (col >= cols) return;
+  const int per = (rows + nchunk - 1) / nchunk;
+  const int r0 = chunk * per, r1 = min(rows, r0 + per);
+  float acc = 0.f;
+  for (int r = r0; r < r1; ++r) {
+    const int64_t o = (int64_t)r * cols + col;
+    acc += to_f(dy[o]) * to_f(x[o]) * rstd[r];
+  }
+  partial[(int64_t)chunk * cols + col] = acc;
+}
+__global__ void colsum_accum_kernel(int nchunk, int cols, const float* __restrict__ partial, float* __restrict__ out) {
+  const int col = blockIdx.x * blockDim.x + threadIdx.x;
+  if (col >= cols) return;
+  float acc = 0.f;
+  for (int k = 0; k < nchunk; ++k) acc += partial[(int64_t)k * cols + col];
+  out[col] += acc;
+}
+
+static int dg_chunks(int rows) { return rows < 64 ? (rows > 0 ? rows : 1) : 64; }
+
+// ------------------------------------------------------------------ SwiGLU / GELU
+template <typename T>
+__global__ void swiglu_fwd_kernel(int64_t total, int f, const T* __restrict__ gu, T* __restrict__ h) {
+  constexpr int N = V16<T>::N;
+  const int64_t nv = total / N;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nv; v += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = v * N;
+    const int64_t i = e / f;
+    const int j = (int)(e % f);
+    const T* row = gu + i * 2 * (int64_t)f;
+    V16<T> gv = vload(row + j), uv = vload(row + f + j), o;
+#pragma unroll
+    for (int q = 0; q < N; ++q) {
+      const float gg = gv.get(q);
+      const float s = 1.f / (1.f + __expf(-gg));
+      o.set(q, gg * s * uv.get(q));
+    }
+    vstore(h + e, o);
+  }
+}
+template <typename T>
+__global__ void swiglu_bwd_kernel(int64_t total, int f, const T* __restrict__ dh, const T* __restrict__ gu,
+                                  T* __restrict__ dgu) {
+  constexpr int N = V16<T>::N;
+  const int64_t nv = total / N;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nv; v += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = v * N;
+    const int64_t i = e / f;
+    const int j = (int)(e % f);
+    const T* row = gu + i * 2 * (int64_t)f;
+    T* orow = dgu + i * 2 * (int64_t)f;
+    V16<T> gv = vload(row + j), uv = vload(row + f + j), dv = vload(dh + e), og, ou;
+#pragma unroll
+    for (int q = 0; q < N; ++q) {
+      const float gg = gv.get(q), uu = uv.get(q), d = dv.get(q);
+      const float s = 1.f / (1.f + __expf(-gg));
+      og.set(q, d * uu * s * (1.f + gg * (1.f - s)));
+      ou.set(q, d * gg * s);
+    }
+    vstore(orow + j, og);
+    vstore(orow + f + j, ou);
+  }
+}
+template <typename T>
+__global__ void gelu_fwd_kernel(int64_t n, const T* __restrict__ a, T* __restrict__ z) {
+  constexpr int N = V16<T>::N;
+  const int64_t nv = n / N;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nv; v += (int64_t)gridDim.x * blockDim.x) {
+    V16<T> av = vload(a + v * N), o;
+#pragma unroll
+    for (int q = 0; q < N; ++q) o.set(q, gelu_f(av.get(q)));
+    vstore(z + v * N, o);
+  }
+  for (int64_t e = nv * N + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
+    z[e] = from_f<T>(gelu_f(to_f(a[e])));
+}
+template <typename T>
+__global__ void gelu_bwd_kernel(int64_t n, const T* __restrict__ dz, const T* __restrict__ a, T* __restrict__ da) {
+  constexpr int N = V16<T>::N;
+  const int64_t nv = n / N;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nv; v += (int64_t)gridDim.x * blockDim.x) {
+    V16<T> av = vload(a + v * N), dv = vload(dz + v * N), o;
+#pragma unroll
+    for (int q = 0; q < N; ++q) o.set(q, dv.get(q) * gelu_grad(av.get(q)));
+    vstore(da + v * N, o);
+  }
+  for (int64_t e = nv * N + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
+    da[e] = from_f<T>(to_f(dz[e]) * gelu_grad(to_f(a[e])));
+}
+template <typename T>
+__global__ void add_kernel(int64_t n, const T* __restrict__ a, const T* __restrict__ b, T* __restrict__ o) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
+    o[e] = from_f<T>(to_f(a[e]) + to_f(b[e]));
+}
+template <typename S, typename D>
+__global__ void cast_kernel(int64_t n, const S* __restrict__ a, D* __restrict__ o) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
+    o[e] = from_f<D>(to_f(a[e]));
+}
+
+// ------------------------------------------------------------------ embed_preprocess
+template <typename T>
+__global__ void embed_fwd_kernel(int S, int d, int n_mod, const int32_t* __restrict__ ids, const T* __restrict__ table,
+                                 const T* __restrict__ emb, T* __restrict__ X) {
+  constexpr int N = V16<T>::N;
+  const int warps = blockDim.x / 32;
+  const int row = blockIdx.x * warps + threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  if (row >= S) return;
+  const T* src = (row < n_mod) ? emb + (int64_t)row * d : table + (int64_t)ids[row] * d;
+  T* dst = X + (int64_t)row * d;
+  for (int c = lane * N; c < d; c += 32 * N) vstore(dst + c, vload(src + c));
+}
+
+// Sort (id, position) for positions [n_mod, S) in one CTA (bitonic, smem),
+// emit positions in sorted order and segment starts.
+// scratch layout (int32): [0] nseg | order[S] | seg_start[S+1]
+__global__ void embed_sort_kernel(int S, int n_mod, const int32_t* __restrict__ ids, int32_t* __restrict__ scratch) {
+  extern __shared__ unsigned long long keys[];
+  __shared__ int wsum[32];
+  const int cnt = S - n_mod;
+  int n2 = 1;
+  while (n2 < cnt) n2 <<= 1;
+  for (int i = threadIdx.x; i < n2; i += blockDim.x)
+    keys[i] = (i < cnt) ? (((unsigned long long)(unsigned)ids[n_mod + i] << 32) | (unsigned)(n_mod + i)) : ~0ull;
+  __syncthreads();
+  for (int k = 2; k <= n2; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < n2; i += blockDim.x) {
+        const int ixj = i ^ j;
+        if (ixj > i) {
+          const bool up = (i & k) == 0;
+          unsigned long long a = keys[i], b = keys[ixj];
+          if ((a > b) == up) { keys[i] = b; keys[ixj] = a; }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  int32_t* order = scratch + 1;
+  int32_t* seg = scratch + 1 + S;
+  // heads + exclusive scan (each thread owns a contiguous span)
+  const int per = (cnt + blockDim.x - 1) / blockDim.x;
+  const int b0 = threadIdx.x * per, b1 = min(cnt, b0 + per);
+  int local = 0;
+  for (int i = b0; i < b1; ++i) {
+    order[i] = (int32_t)(keys[i] & 0xffffffffu);
+    if (i == 0 || (keys[i] >> 32) != (keys[i - 1] >> 32)) ++local;
+  }
+  // block exclusive scan of `local`
+  const int lane = threadIdx.x % 32, w = threadIdx.x / 32;
+  int v = local;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int t = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += t;
+  }
+  if (lane == 31) wsum[w] = v;
+  __syncthreads();
+  if (w == 0) {
+    int s = (lane < (int)(blockDim.x / 32)) ? wsum[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int t = __shfl_up_sync(0xffffffffu, s, o);
+      if (lane >= o) s += t;
+    }
+    wsum[lane] = s;
+  }
+  __syncthreads();
+  int base = v - local + (w > 0 ? wsum[w - 1] : 0);
+  for (int i = b0; i < b1; ++i) {
+    if (i == 0 || (keys[i] >> 32) != (keys[i - 1] >> 32)) seg[base++] = i;
+  }
+  if (threadIdx.x == blockDim.x - 1) {
+    const int total = v + (w > 0 ? wsum[w - 1] : 0);
+    scratch[0] = total;
+    seg[total] = cnt;
+  }
+}
+
+template <typename T>
+__global__ void embed_segsum_kernel(int S, int d, const int32_t* __restrict__ ids, const T* __restrict__ dX,
+                                    const int32_t* __restrict__ scratch, float* __restrict__ dT) {
+  const int nseg = scratch[0];
+  const int32_t* order = scratch + 1;
+  const int32_t* seg = scratch + 1 + S;
+  const int warps = blockDim.x / 32;
+  const int lane = threadIdx.x % 32;
+  for (int s = blockIdx.x * warps + threadIdx.x / 32; s < nseg; s += gridDim.x * warps) {
+    const int i0 = seg[s], i1 = seg[s + 1];
+    const int id = ids[order[i0]];
+    float* dst = dT + (int64_t)id * d;
+    for (int c = lane; c < d; c += 32) {
+      float acc = 0.f;
+      for (int i = i0; i < i1; ++i) acc += to_f(dX[(int64_t)order[i] * d + c]);
+      dst[c] += acc;
+    }
+  }
+}
+
+// ------------------------------------------------------------------ losses
+template <typename T>
+__global__ void ce_row_kernel(int V, T* __restrict__ logits, const int32_t* __restrict__ labels, float scale_grad,
+                              float* __restrict__ row_loss) {
+  __shared__ float sh[32];
+  const int row = blockIdx.x;
+  T* z = logits + (int64_t)row * V;
+  float mx = -FLT_MAX;
+  for (int j = threadIdx.x; j < V; j += blockDim.x) mx = fmaxf(mx, to_f(z[j]));
+  mx = block_max(mx, sh);
+  float s = 0.f;
+  for (int j = threadIdx.x; j < V; j += blockDim.x) s += __expf(to_f(z[j]) - mx);
+  s = block_sum(s, sh);
+  const float lse = mx + __logf(s);
+  const int lab = labels[row];
+  const float zl = to_f(z[lab]);
+  __syncthreads();
+  if (threadIdx.x == 0) row_loss[row] = lse - zl;
+  for (int j = threadIdx.x; j < V; j += blockDim.x) {
+    const float p = __expf(to_f(z[j]) - lse);
+    z[j] = from_f<T>((p - (j == lab ? 1.f : 0.f)) * scale_grad);
+  }
+}
+__global__ void sum_scale_kernel(int n, const float* __restrict__ v, float scale, int accumulate, float* out) {
+  __shared__ float sh[32];
+  float s = 0.f;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) s += v[i];
+  s = block_sum(s, sh);
+  if (threadIdx.x == 0) out[0] = (accumulate ? out[0] : 0.f) + s * scale;
+}
+template <typename T>
+__global__ void mse_kernel(int64_t n, const T* __restrict__ out, const T* __restrict__ t, float inv_denom,
+                           float scale_grad, float scale_loss, float* loss, T* __restrict__ dout) {
+  __shared__ float sh[32];
+  float s = 0.f;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    const float df = to_f(out[i]) - to_f(t[i]);
+    s += df * df;
+    dout[i] = from_f<T>(2.f * df * inv_denom * scale_grad);
+  }
+  s = block_sum(s, sh);
+  if (threadIdx.x == 0) loss[0] += s * inv_denom * scale_loss;
+}
+
+// ================================================================== launchers
+static int ew_grid(int64_t work_items) {
+  int64_t g = (work_items + 255) / 256;
+  const int64_t cap = (int64_t)num_sms() * 8;
+  if (g > cap) g = cap;
+  return (int)(g < 1 ? 1 : g);
+}
+
+template <typename T>
+bm_status rmsnorm_fwd(int rows, int cols, const T* x, const T* g, T* y, float* rstd, cudaStream_t st) {
+  if (rows <= 0) return BM_OK;
+  BM_CHECK_ARG(cols % V16<T>::N == 0, "rmsnorm cols must be a multiple of the vector width");
+  rmsnorm_fwd_kernel<T><<<ceil_div(rows, 8), 256, 0, st>>>(rows, cols, x, g, y, rstd);
+  count_launch();
+  BM_CUDA_TRY(cudaGetLastError());
+  return BM_OK;
+}
+template <typename T>
+bm_status rmsnorm_bwd(int rows, int cols, const T* dy, const T* x, const T* g, const float* rstd, const T* dres,
+                      T* dx, float* dg, float* partial, cudaStream_t st) {
+  if (rows <= 0) return BM_OK;
+  BM_CHECK_ARG(cols % V16<T>::N == 0, "rmsnorm cols must be a multiple of the vector width");
+  // gain gradient first (dx may alias dy's residual buffer)
+  const int nch = dg_chunks(rows);
+  rmsnorm_dg_partial_kernel<T><<<dim3(ceil_div(cols, 256), nch), 256, 0, st>>>(rows, cols, nch, dy, x, rstd, partial);
+  colsum_accum_kernel<<<ceil_div(cols, 256), 256, 0, st>>>(nch, cols, partial, dg);
+  rmsnorm_bwd_kernel<T><<<ceil_div(rows, 8), 256, 0, st>>>(rows, cols, dy, x, g, rstd, dres, dx);
+  count_launch(3);
+  BM_CUDA_TRY(cudaGetLastError());
+  return BM_OK;
+}
+template <typename T>
+bm_status swiglu_fwd(int rows, int f, const T* gu, T* h, cudaStream_t st) {
+  const int64_t total = (int64_t)rows * f;
+  if (total == 0) return BM_OK;
+  BM_CHECK_ARG(f % V16<T>::N == 0, "swiglu f must be a multiple of the vector width");
+  swiglu_fwd_kernel<T><<<ew_grid(total / V16<T>::N), 256, 0, st>>>(total, f, gu, h);
+  count_launch();
+  BM_CUDA_TRY(cudaGetLastError());
+  return BM_OK;
+}
+template <typename T>
+bm_status swiglu_bwd(int rows, int f, const T* dh, const T* gu, T* dgu, cudaStream_t st) {
+  const int64_t total = (int64_t)rows * f;
+  if (total == 0) return BM_OK;
+  BM_CHECK_ARG(f % V16<T>::N == 0, "swiglu f must be a multiple of the vector width");
+  swiglu_bwd_kernel<T><<<ew_grid(total / V16<T>::N), 256, 0, st>>>(total, f, dh, gu, dgu);
+  count_launch();
+  BM_CUDA_TRY(cudaGetLastError());
+  return BM_OK;
+}
+template <typename T>
+bm_status gelu_fwd(int64_t n, const T* a, T* z, cudaStream_t st) {
+  if (n == 0) return BM_OK;
+  gelu_fwd_kernel<T><<<ew_grid(n / V16<T>::N + 1), 256, 0, st>>>(n, a, z);
+  count_launch();
+  BM_CUDA_TRY(cudaGetLastError());
+  return BM_OK;
+}
+template <typename T>
+bm_status gelu_bwd(int64_t n, const T* dz, const T* a, T* da, cudaStream_t st) {
+  if (n == 0) return BM_OK;
+  gelu_bwd_kernel<T><<<ew_grid(n / V16<T>::N + 1), 256, 0, st>>>(n, dz, a, da);
+  count_launch();
+  BM_CUDA_TRY(cudaGetLastError());
+  return BM_OK;
+}
+template <typename T>
+bm_status embed_fwd(int S, int d, int n_mod, const int32_t* ids, const T* table, const T* emb, T* X, cudaStream_t st) {
+  BM_CHECK_ARG(d % V16<T>::N == 0, "embed width must be a multiple of the vector width");
+  embed_fwd_kernel<T><<<ceil_div(S, 8), 256, 0, st>>>(S, d, n_mod, ids, table, emb, X);
+  count_launch();
+  BM_CUDA_TRY(cudaGetLastError());
+  return BM_OK;
+}
+int64_t embed_bwd_scratch_bytes(int S) { return (int64_t)(2 * S + 2) * 4; }
+
+template <typename T>
+bm_status embed_bwd(int S, int d, int n_mod, const int32_t* ids, const T* dX, float* dT, void* scratch, cudaStream_t st) {
+  const int cnt = S - n_mod;
+  if (cnt <= 0) return BM_OK;
+  BM_CHECK_ARG(S <= 16384, "embed_bwd supports S <= 16384");
+  int n2 = 1;
+  while (n2 < cnt) n2 <<= 1;
+  const int smem = n2 * 8;
+  static bool attr = false;
+  if (!attr) {
+    BM_CUDA_TRY(cudaFuncSetAttribute(embed_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 16384 * 8));
+    attr = true;
+  }
+  embed_sort_kernel<<<1, 1024, smem, st>>>(S, n_mod, ids, reinterpret_cast<int32_t*>(scratch));
+  embed_segsum_kernel<T><<<ceil_div(cnt, 8), 256, 0, st>>>(S, d, ids, dX, reinterpret_cast<int32_t*>(scratch), dT);
+  count_launch(2);
+  BM_CUDA_TRY(cudaGetLastError());
+  return BM_OK;
+}
+template <typename T>
+bm_status ce_fwd_bwd(int n, int V, T* logits, const int32_t* labels, float scale_grad, float* loss_out,
+                     float scale_loss, int accumulate, float* scratch, cudaStream_t st) {
+  if (n <= 0) return BM_OK;
+  ce_row_kernel<T><<<n, 256, 0, st>>>(V, logits, labels, scale_grad, scratch);
+  sum_scale_kernel<<<1, 1024, 0, st>>>(n, scratch, scale_loss / n, accumulate, loss_out);
+  count_launch(2);
+  BM_CUDA_TRY(cudaGetLastError());
+  return BM_OK;
+}
+template <typename T>
+bm_status mse_fwd_bwd(int n, int dt, const T* out, const T* t, float denom, float scale_grad, float scale_loss,
+                      float* loss_out, T* dout, cudaStream_t st) {
+  if (n <= 0) return BM_OK;
+  mse_kernel<T><<<1, 1024, 0, st>>>((int64_t)n * dt, out, t, 1.f / denom, scale_grad, scale_loss, loss_out, dout);
+  count_launch();
+  BM_CUDA_TRY(cudaGetLastError());
+  return BM_OK;
+}
+template <typename T>
+bm_status add(int64_t n, const T* a, const T* b, T* o, cudaStream_t st) {
+  if (n == 0) return BM_OK;
+  add_kernel<T><<<ew_grid(n), 256, 0, st>>>(n, a, b, o);
+  count_launch();
+  BM_CUDA_TRY(cudaGetLastError());
+  return BM_OK;
+}
+bm_status cast(int sd, int dd, int64_t n, const void* s, void* d, cudaStream_t st) {
+  if (n == 0) return BM_OK;
+  if (sd == BM_F32 && dd == BM_BF16) cast_kernel<float, bf16><<<ew_grid(n), 256, 0, st>>>(n, (const float*)s, (bf16*)d);
+  else if (sd == BM_BF16 && dd == BM_F32) cast_kernel<bf16, float><<<ew_grid(n), 256, 0, st>>>(n, (const bf16*)s, (float*)d);
+  else if (sd == BM_F32 && dd == BM_F32) cast_kernel<float, float><<<ew_grid(n), 256, 0, st>>>(n, (const float*)s, (float*)d);
+  else cast_kernel<bf16, bf16><<<ew_grid(n), 256, 0, st>>>(n, (const bf16*)s, (bf16*)d);
+  count_launch();
+  BM_CUDA_TRY(cudaGetLastError());
+  return BM_OK;
+}
+
+#define BM_INST(T)                                                                                              \
+  template bm_status rmsnorm_fwd<T>(int, int, const T*, const T*, T*, float*, cudaStream_t);                    \
+  template bm_status rmsnorm_bwd<T>(int, int, const T*, const T*, const T*, const float*, const T*, T*, float*, \
+                                    float*, cudaStream_t);                                                      \
+  template bm_status swiglu_fwd<T>(int, int, const T*, T*, cudaStream_t);                                       \
+  template bm_status swiglu_bwd<T>(int, int, const T*, const T*, T*, cudaStream_t);                             \
+  template bm_status gelu_fwd<T>(int64_t, const T*, T*, cudaStream_t);                                          \
+  template bm_status gelu_bwd<T>(int64_t, const T*, const T*, T*, cudaStream_t);                                \
+  template bm_status embed_fwd<T>(int, int, int, const int32_t*, const T*, const T*, T*, cudaStream_t);         \
+  template bm_status embed_bwd<T>(int, int, int, const int32_t*, const T*, float*, void*, cudaStream_t);        \
+  template bm_status ce_fwd_bwd<T>(int, int, T*, const int32_t*, float, float*, float, int, float*, cudaStream_t); \
+  template bm_status mse_fwd_bwd<T>(int, int, const T*, const T*, float, float, float, float*, T*, cudaStream_t); \
+  template bm_status add<T>(int64_t, const T*, const T*, T*, cudaStream_t);
+BM_INST(bf16)
+BM_INST(float)
+
+int64_t rmsnorm_bwd_scratch_floats(int rows, int cols) { return (int64_t)dg_chunks(rows) * cols; }
+
+}  // namespace bm

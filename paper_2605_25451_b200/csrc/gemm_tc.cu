@@ -1,0 +1,484 @@
+// gemm_tc.cu -- bf16 GEMM on the 5th-gen tensor cores (sm_100a).
+//
+// C[m, n] = sum_k A(m, k) B(n, k) with fp32 accumulation in TMEM, for the
+// dense block contractions of the synthetic MLLM (every Linear layer's
+// forward, data-grad and weight-grad; PAPER P:290-304 gives the model
+// functions, DESIGN.md "Kernels" the shapes).
+//
+// Design (sm_100a, one CTA per SM, persistent):
+//   warp 0      TMA producer: cp.async.bulk.tensor 2D tiles, 128B swizzle,
+//               STAGES-deep smem ring guarded by full/empty mbarriers
+//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer
+//               (kind::f16, M=128, N=BN, K=16 per instruction); commits free
+//               smem stages and publish finished accumulators
+//   warps 2..5  epilogue: tcgen05.ld 32x32b.x32 -> registers -> fused
+//               epilogue (store / fp32 accumulate / residual add) -> global
+//   TMEM holds two BN-column accumulators so the epilogue of tile i overlaps
+//   the MMAs of tile i+1.
+// A and B may each be K-major or MN-major; the UMMA smem descriptors and the
+// instruction descriptor's major bits express the transpose, so forward,
+// dgrad and wgrad need no transposed copies.
+#include <unordered_map>
+#include <mutex>
+#include <vector>
+
+#include "common.cuh"
+
+namespace bm {
+namespace tc {
+
+constexpr int BM = 128;
+constexpr int BK = 64;                  // 64 bf16 = 128 B = one swizzle row
+constexpr int NUM_THREADS = 192;
+
+template <int BN> struct Cfg {
+  static constexpr int A_BYTES = BM * BK * 2;          // 16 KB
+  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGES = (BN == 256) ? 4 : (BN == 128 ? 6 : 8);
+  static constexpr int TMEM_COLS = 2 * BN;             // double-buffered accumulators
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+};
+
+struct EpiArgs {
+  int M, N, K;
+  void* C;
+  int64_t ldc;
+  int c_f32;       // C is fp32
+  int epi;         // bm_epilogue
+  const void* R;
+  int64_t ldr;
+  float alpha;
+};
+
+// ---------------------------------------------------------------- PTX helpers
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void tma_prefetch(const CUtensorMap* map) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+__device__ __forceinline__ void umma_f16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                         uint32_t accum) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum));
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+// UMMA shared-memory descriptor, SWIZZLE_128B, version 1 (sm_100).
+//   K-major : LBO unused (1), SBO = 1024 B (8 rows x 128 B)
+//   MN-major: LBO = byte stride between 64-element MN chunks, SBO = 1024 B
+__device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_bytes) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo_bytes >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo_bytes >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;   // version (sm_100)
+  d |= (uint64_t)2 << 61;   // SWIZZLE_128B
+  return d;
+}
+
+// Instruction descriptor for kind::f16: bf16 x bf16 -> fp32, M = 128, N = BN.
+__host__ __device__ constexpr uint32_t make_idesc(int N, bool a_mn, bool b_mn) {
+  return (1u << 4)                     // D format fp32
+         | (1u << 7)                   // A bf16
+         | (1u << 10)                  // B bf16
+         | ((a_mn ? 1u : 0u) << 15)    // A major
+         | ((b_mn ? 1u : 0u) << 16)    // B major
+         | ((uint32_t)(N >> 3) << 17)  // N / 8
+         | ((uint32_t)(BM >> 4) << 24);// M / 16
+}
+
+__device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int& mb, int& nb) {
+  // grouped raster: 8 m-tiles share each n sweep for L2 reuse of B
+  const int G = 8;
+  int per_group = G * tiles_n;
+  int group = t / per_group;
+  int first_m = group * G;
+  int gm = min(G, tiles_m - first_m);
+  int r = t % per_group;
+  mb = first_m + r % gm;
+  nb = r / gm;
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ void epilogue_row(const EpiArgs& a, int row, int col0, const float* v) {
+  // one thread writes up to 32 consecutive columns of one row
+  const int ncols = min(32, a.N - col0);
+  if (ncols <= 0) return;
+  const float alpha = a.alpha;
+  if (a.c_f32) {
+    float* c = reinterpret_cast<float*>(a.C) + (int64_t)row * a.ldc + col0;
+    const bool vec = (ncols == 32) && ((reinterpret_cast<uintptr_t>(c) & 15) == 0);
+    if (a.epi == BM_EPI_ACCUM) {
+      if (vec) {
+#pragma unroll
+        for (int j = 0; j < 32; j += 4) {
+          float4 o = *reinterpret_cast<float4*>(c + j);
+          o.x += alpha * v[j]; o.y += alpha * v[j + 1]; o.z += alpha * v[j + 2]; o.w += alpha * v[j + 3];
+          *reinterpret_cast<float4*>(c + j) = o;
+        }
+      } else {
+        for (int j = 0; j < ncols; ++j) c[j] += alpha * v[j];
+      }
+    } else {
+      const float* r = (a.epi == BM_EPI_ADD) ? reinterpret_cast<const float*>(a.R) + (int64_t)row * a.ldr + col0 : nullptr;
+      if (vec && (r == nullptr || (reinterpret_cast<uintptr_t>(r) & 15) == 0)) {
+#pragma unroll
+        for (int j = 0; j < 32; j += 4) {
+          float4 o = make_float4(alpha * v[j], alpha * v[j + 1], alpha * v[j + 2], alpha * v[j + 3]);
+          if (r) {
+            float4 q = *reinterpret_cast<const float4*>(r + j);
+            o.x += q.x; o.y += q.y; o.z += q.z; o.w += q.w;
+          }
+          *reinterpret_cast<float4*>(c + j) = o;
+        }
+      } else {
+        for (int j = 0; j < ncols; ++j) c[j] = alpha * v[j] + (r ? r[j] : 0.f);
+      }
+    }
+  } else {
+    bf16* c = reinterpret_cast<bf16*>(a.C) + (int64_t)row * a.ldc + col0;
+    const bf16* r = (a.epi == BM_EPI_ADD) ? reinterpret_cast<const bf16*>(a.R) + (int64_t)row * a.ldr + col0 : nullptr;
+    const bool vec = (ncols == 32) && ((reinterpret_cast<uintptr_t>(c) & 15) == 0) &&
+                     (r == nullptr || (reinterpret_cast<uintptr_t>(r) & 15) == 0);
+    if (vec) {
+#pragma unroll
+      for (int j = 0; j < 32; j += 8) {
+        float w[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) w[q] = alpha * v[j + q];
+        if (r) {
+          uint4 rv = *reinterpret_cast<const uint4*>(r + j);
+          const bf16* rb = reinterpret_cast<const bf16*>(&rv);
+#pragma unroll
+          for (int q = 0; q < 8; ++q) w[q] += __bfloat162float(rb[q]);
+        }
+        uint4 ov;
+        bf16* ob = reinterpret_cast<bf16*>(&ov);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) ob[q] = __float2bfloat16_rn(w[q]);
+        *reinterpret_cast<uint4*>(c + j) = ov;
+      }
+    } else {
+      for (int j = 0; j < ncols; ++j) {
+        float w = alpha * v[j] + (r ? __bfloat162float(r[j]) : 0.f);
+        c[j] = __float2bfloat16_rn(w);
+      }
+    }
+  }
+}
+
+template <int BN, bool A_MN, bool B_MN>
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, EpiArgs args) {
+  using C = Cfg<BN>;
+  constexpr int STAGES = C::STAGES;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smA = smem;
+  uint8_t* smB = smem + STAGES * C::A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * C::STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  const int tiles_m = (args.M + BM - 1) / BM;
+  const int tiles_n = (args.N + BN - 1) / BN;
+  const int num_tiles = tiles_m * tiles_n;
+  const int nk = (args.K + BK - 1) / BK;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull[s], 1);
+      mbar_init(&tempty[s], 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    tma_prefetch(&tmA);
+    tma_prefetch(&tmB);
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"((uint32_t)C::TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        int mb, nb;
+        tile_coords(t, tiles_m, tiles_n, mb, nb);
+        const int m0 = mb * BM, n0 = nb * BN;
+        for (int kb = 0; kb < nk; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_expect_tx(&full[stage], C::STAGE_BYTES);
+          uint8_t* a_dst = smA + stage * C::A_BYTES;
+          uint8_t* b_dst = smB + stage * C::B_BYTES;
+          const int k0 = kb * BK;
+          if (A_MN) {
+#pragma unroll
+            for (int j = 0; j < BM / 64; ++j) tma_load_2d(a_dst + j * (BK * 128), &tmA, &full[stage], m0 + 64 * j, k0);
+          } else {
+            tma_load_2d(a_dst, &tmA, &full[stage], k0, m0);
+          }
+          if (B_MN) {
+#pragma unroll
+            for (int j = 0; j < BN / 64; ++j) tma_load_2d(b_dst + j * (BK * 128), &tmB, &full[stage], n0 + 64 * j, k0);
+          } else {
+            tma_load_2d(b_dst, &tmB, &full[stage], k0, n0);
+          }
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---------------- MMA issuer
+      constexpr uint32_t idesc = make_idesc(BN, A_MN, B_MN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int local = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++local) {
+        const int acc = local & 1;
+        const uint32_t acc_phase = (local >> 1) & 1;
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t tmem_d = tmem_base + acc * BN;
+        for (int kb = 0; kb < nk; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a_base = smem_u32(smA + stage * C::A_BYTES);
+          const uint32_t b_base = smem_u32(smB + stage * C::B_BYTES);
+#pragma unroll
+          for (int kk = 0; kk < BK / 16; ++kk) {
+            uint64_t ad = A_MN ? make_desc(a_base + kk * 2048, BK * 128, 1024) : make_desc(a_base + kk * 32, 16, 1024);
+            uint64_t bd = B_MN ? make_desc(b_base + kk * 2048, BK * 128, 1024) : make_desc(b_base + kk * 32, 16, 1024);
+            umma_f16(tmem_d, ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
+          }
+          umma_commit(&empty[stage]);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+        umma_commit(&tfull[acc]);
+      }
+    }
+  } else {
+    // ---------------- epilogue warps 2..5 (TMEM lane quadrant = warp % 4)
+    const int quad = warp & 3;
+    int local = 0;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++local) {
+      int mb, nb;
+      tile_coords(t, tiles_m, tiles_n, mb, nb);
+      const int acc = local & 1;
+      const uint32_t acc_phase = (local >> 1) & 1;
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const int row = mb * BM + quad * 32 + lane;
+      const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + acc * BN;
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 32) {
+        float v[32];
+        tmem_ld32(taddr + c, v);
+        if (row < args.M) epilogue_row(args, row, nb * BN + c, v);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"((uint32_t)C::TMEM_COLS));
+  }
+}
+
+// ---------------------------------------------------------------- host side
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn get_encode() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  return fn;
+}
+
+struct MapKey {
+  const void* p;
+  uint64_t inner, outer, stride;
+  uint32_t box_outer;
+  bool operator==(const MapKey& o) const {
+    return p == o.p && inner == o.inner && outer == o.outer && stride == o.stride && box_outer == o.box_outer;
+  }
+};
+struct MapKeyHash {
+  size_t operator()(const MapKey& k) const {
+    size_t h = reinterpret_cast<size_t>(k.p);
+    h = h * 1000003u ^ k.inner;
+    h = h * 1000003u ^ k.outer;
+    h = h * 1000003u ^ k.stride;
+    h = h * 1000003u ^ k.box_outer;
+    return h;
+  }
+};
+
+static std::mutex g_map_mu;
+static std::unordered_map<MapKey, CUtensorMap, MapKeyHash> g_maps;
+
+// 2D bf16 tensor [outer][inner] with row stride `ld` elements; box = 64 x box_outer.
+static bm_status make_map(const void* p, uint64_t inner, uint64_t outer, uint64_t ld, uint32_t box_outer,
+                          CUtensorMap* out) {
+  MapKey key{p, inner, outer, ld, box_outer};
+  {
+    std::lock_guard<std::mutex> g(g_map_mu);
+    auto it = g_maps.find(key);
+    if (it != g_maps.end()) {
+      *out = it->second;
+      return BM_OK;
+    }
+  }
+  EncodeTiledFn enc = get_encode();
+  if (!enc) {
+    set_error("cuTensorMapEncodeTiled unavailable");
+    return BM_E_CUDA;
+  }
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {ld * 2};
+  cuuint32_t box[2] = {64, box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(p), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ") inner=" + std::to_string(inner) +
+              " outer=" + std::to_string(outer) + " ld=" + std::to_string(ld));
+    return BM_E_CUDA;
+  }
+  std::lock_guard<std::mutex> g(g_map_mu);
+  if (g_maps.size() > 65536) g_maps.clear();
+  g_maps.emplace(key, *out);
+  return BM_OK;
+}
+
+template <int BN, bool A_MN, bool B_MN>
+static bm_status launch(const CUtensorMap& ma, const CUtensorMap& mb, const EpiArgs& ea, cudaStream_t st) {
+  using C = Cfg<BN>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    BM_CUDA_TRY(cudaFuncSetAttribute(gemm_kernel<BN, A_MN, B_MN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    attr_set = true;
+  }
+  const int tiles = ceil_div(ea.M, BM) * ceil_div(ea.N, BN);
+  const int grid = tiles < num_sms() ? tiles : num_sms();
+  gemm_kernel<BN, A_MN, B_MN><<<grid, NUM_THREADS, C::SMEM, st>>>(ma, mb, ea);
+  count_launch();
+  BM_CUDA_TRY(cudaGetLastError());
+  return BM_OK;
+}
+
+template <int BN>
+static bm_status dispatch_majors(bool a_mn, bool b_mn, const CUtensorMap& ma, const CUtensorMap& mb,
+                                 const EpiArgs& ea, cudaStream_t st) {
+  if (!a_mn && !b_mn) return launch<BN, false, false>(ma, mb, ea, st);
+  if (!a_mn && b_mn) return launch<BN, false, true>(ma, mb, ea, st);
+  if (a_mn && b_mn) return launch<BN, true, true>(ma, mb, ea, st);
+  return launch<BN, true, false>(ma, mb, ea, st);
+}
+
+}  // namespace tc
+
+bm_status gemm_bf16_tc(int M, int N, int K, const void* A, int64_t lda, int a_major, const void* B, int64_t ldb,
+                       int b_major, void* Cp, int64_t ldc, int c_dtype, int epi, const void* R, int64_t ldr,
+                       float alpha, cudaStream_t st) {
+  using namespace tc;
+  BM_CHECK_ARG(lda % 8 == 0 && ldb % 8 == 0, "lda/ldb must be multiples of 8 (16-byte TMA strides)");
+  BM_CHECK_ARG((reinterpret_cast<uintptr_t>(A) & 15) == 0 && (reinterpret_cast<uintptr_t>(B) & 15) == 0,
+               "A/B must be 16-byte aligned");
+  const int BN = (N <= 64) ? 64 : (N <= 128 ? 128 : 256);
+  CUtensorMap ma, mb;
+  if (a_major == 0) BM_TRY(make_map(A, K, M, lda, BM, &ma));
+  else BM_TRY(make_map(A, M, K, lda, BK, &ma));
+  if (b_major == 0) BM_TRY(make_map(B, K, N, ldb, BN, &mb));
+  else BM_TRY(make_map(B, N, K, ldb, BK, &mb));
+  EpiArgs ea{M, N, K, Cp, ldc, c_dtype == BM_F32 ? 1 : 0, epi, R, ldr, alpha};
+  const bool amn = a_major != 0, bmn = b_major != 0;
+  if (BN == 64) return dispatch_majors<64>(amn, bmn, ma, mb, ea, st);
+  if (BN == 128) return dispatch_majors<128>(amn, bmn, ma, mb, ea, st);
+  return dispatch_majors<256>(amn, bmn, ma, mb, ea, st);
+}
+
+}  // namespace bm

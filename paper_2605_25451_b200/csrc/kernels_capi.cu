@@ -1,0 +1,146 @@
+// kernels_capi.cu -- extern "C" entry points of include/bigmac_kernels.h and
+// the library-wide helpers (error string, SM count, launch census).
+#include <atomic>
+#include <mutex>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace bm {
+
+static thread_local std::string g_err;
+void set_error(const std::string& msg) { g_err = msg; }
+const char* get_error() { return g_err.c_str(); }
+
+int num_sms() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int v = 0;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) v = 148;
+    n = v;
+  }
+  return n;
+}
+
+static std::atomic<int64_t> g_launches{0};
+void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+int64_t launch_count() { return g_launches.load(std::memory_order_relaxed); }
+
+bm_status gemm(int dtype, int M, int N, int K, const void* A, int64_t lda, int a_major, const void* B, int64_t ldb,
+               int b_major, void* C, int64_t ldc, int c_dtype, int epi, const void* R, int64_t ldr, float alpha,
+               cudaStream_t st) {
+  if (M <= 0 || N <= 0) return BM_OK;
+  BM_CHECK_ARG(epi != BM_EPI_ACCUM || c_dtype == BM_F32, "ACCUM epilogue requires an fp32 C");
+  if (K <= 0) {
+    // empty contraction: C = 0 (STORE) / C = R (ADD) / unchanged (ACCUM)
+    if (epi == BM_EPI_ACCUM) return BM_OK;
+    const size_t es = c_dtype == BM_F32 ? 4 : 2;
+    if (epi == BM_EPI_STORE) {
+      BM_CUDA_TRY(cudaMemset2DAsync(C, ldc * es, 0, (size_t)N * es, M, st));
+    } else {
+      BM_CUDA_TRY(cudaMemcpy2DAsync(C, ldc * es, R, ldr * es, (size_t)N * es, M, cudaMemcpyDeviceToDevice, st));
+    }
+    return BM_OK;
+  }
+  if (dtype == BM_BF16) {
+    return gemm_bf16_tc(M, N, K, A, lda, a_major, B, ldb, b_major, C, ldc, c_dtype, epi, R, ldr, alpha, st);
+  }
+  BM_CHECK_ARG(c_dtype == BM_F32, "fp32 GEMM writes fp32 C");
+  return gemm_f32_simt(M, N, K, (const float*)A, lda, a_major, (const float*)B, ldb, b_major, (float*)C, ldc, epi,
+                       (const float*)R, ldr, alpha, st);
+}
+
+}  // namespace bm
+
+using namespace bm;
+
+#define ST(s) reinterpret_cast<cudaStream_t>(s)
+#define DISPATCH(dtype, call_bf16, call_f32)                  \
+  do {                                                        \
+    if ((dtype) == BM_BF16) return call_bf16;                 \
+    if ((dtype) == BM_F32) return call_f32;                   \
+    set_error("unknown dtype");                               \
+    return BM_E_INVALID;                                      \
+  } while (0)
+
+extern "C" {
+
+const char* bm_last_error(void) { return get_error(); }
+
+bm_status bm_k_gemm(int32_t dtype, int32_t M, int32_t N, int32_t K, const void* A, int64_t lda, int32_t a_major,
+                    const void* B, int64_t ldb, int32_t b_major, void* C, int64_t ldc, int32_t c_dtype,
+                    int32_t epilogue, const void* R, int64_t ldr, float alpha, void* stream) {
+  return gemm(dtype, M, N, K, A, lda, a_major, B, ldb, b_major, C, ldc, c_dtype, epilogue, R, ldr, alpha, ST(stream));
+}
+
+bm_status bm_k_rmsnorm_fwd(int32_t dtype, int32_t rows, int32_t cols, const void* x, const void* g, void* y,
+                           float* rstd, void* stream) {
+  DISPATCH(dtype, rmsnorm_fwd<bf16>(rows, cols, (const bf16*)x, (const bf16*)g, (bf16*)y, rstd, ST(stream)),
+           rmsnorm_fwd<float>(rows, cols, (const float*)x, (const float*)g, (float*)y, rstd, ST(stream)));
+}
+bm_status bm_k_rmsnorm_bwd(int32_t dtype, int32_t rows, int32_t cols, const void* dy, const void* x, const void* g,
+                           const float* rstd, const void* dres, void* dx, float* dg, float* partial, void* stream) {
+  DISPATCH(dtype,
+           rmsnorm_bwd<bf16>(rows, cols, (const bf16*)dy, (const bf16*)x, (const bf16*)g, rstd, (const bf16*)dres,
+                             (bf16*)dx, dg, partial, ST(stream)),
+           rmsnorm_bwd<float>(rows, cols, (const float*)dy, (const float*)x, (const float*)g, rstd,
+                              (const float*)dres, (float*)dx, dg, partial, ST(stream)));
+}
+int64_t bm_k_rmsnorm_bwd_scratch(int32_t rows, int32_t cols) { return rmsnorm_bwd_scratch_floats(rows, cols); }
+
+bm_status bm_k_swiglu_fwd(int32_t dtype, int32_t rows, int32_t f, const void* gu, void* h, void* stream) {
+  DISPATCH(dtype, swiglu_fwd<bf16>(rows, f, (const bf16*)gu, (bf16*)h, ST(stream)),
+           swiglu_fwd<float>(rows, f, (const float*)gu, (float*)h, ST(stream)));
+}
+bm_status bm_k_swiglu_bwd(int32_t dtype, int32_t rows, int32_t f, const void* dh, const void* gu, void* dgu,
+                          void* stream) {
+  DISPATCH(dtype, swiglu_bwd<bf16>(rows, f, (const bf16*)dh, (const bf16*)gu, (bf16*)dgu, ST(stream)),
+           swiglu_bwd<float>(rows, f, (const float*)dh, (const float*)gu, (float*)dgu, ST(stream)));
+}
+bm_status bm_k_gelu_fwd(int32_t dtype, int64_t n, const void* a, void* z, void* stream) {
+  DISPATCH(dtype, gelu_fwd<bf16>(n, (const bf16*)a, (bf16*)z, ST(stream)),
+           gelu_fwd<float>(n, (const float*)a, (float*)z, ST(stream)));
+}
+bm_status bm_k_gelu_bwd(int32_t dtype, int64_t n, const void* dz, const void* a, void* da, void* stream) {
+  DISPATCH(dtype, gelu_bwd<bf16>(n, (const bf16*)dz, (const bf16*)a, (bf16*)da, ST(stream)),
+           gelu_bwd<float>(n, (const float*)dz, (const float*)a, (float*)da, ST(stream)));
+}
+bm_status bm_k_embed_fwd(int32_t dtype, int32_t S, int32_t d, int32_t n_mod, const int32_t* ids, const void* table,
+                         const void* emb, void* X, void* stream) {
+  DISPATCH(dtype, embed_fwd<bf16>(S, d, n_mod, ids, (const bf16*)table, (const bf16*)emb, (bf16*)X, ST(stream)),
+           embed_fwd<float>(S, d, n_mod, ids, (const float*)table, (const float*)emb, (float*)X, ST(stream)));
+}
+bm_status bm_k_embed_bwd(int32_t dtype, int32_t S, int32_t d, int32_t n_mod, const int32_t* ids, const void* dX,
+                         float* dT, void* scratch, void* stream) {
+  DISPATCH(dtype, embed_bwd<bf16>(S, d, n_mod, ids, (const bf16*)dX, dT, scratch, ST(stream)),
+           embed_bwd<float>(S, d, n_mod, ids, (const float*)dX, dT, scratch, ST(stream)));
+}
+int64_t bm_k_embed_bwd_scratch(int32_t S) { return embed_bwd_scratch_bytes(S); }
+
+bm_status bm_k_ce_fwd_bwd(int32_t dtype, int32_t n, int32_t V, void* logits, const int32_t* labels, float scale_grad,
+                          float* loss_out, float scale_loss, int32_t accumulate, float* scratch, void* stream) {
+  DISPATCH(dtype,
+           ce_fwd_bwd<bf16>(n, V, (bf16*)logits, labels, scale_grad, loss_out, scale_loss, accumulate, scratch,
+                            ST(stream)),
+           ce_fwd_bwd<float>(n, V, (float*)logits, labels, scale_grad, loss_out, scale_loss, accumulate, scratch,
+                             ST(stream)));
+}
+bm_status bm_k_mse_fwd_bwd(int32_t dtype, int32_t n, int32_t dt, const void* out, const void* t, float denom,
+                           float scale_grad, float scale_loss, float* loss_out, void* dout, void* stream) {
+  DISPATCH(dtype,
+           mse_fwd_bwd<bf16>(n, dt, (const bf16*)out, (const bf16*)t, denom, scale_grad, scale_loss, loss_out,
+                             (bf16*)dout, ST(stream)),
+           mse_fwd_bwd<float>(n, dt, (const float*)out, (const float*)t, denom, scale_grad, scale_loss, loss_out,
+                              (float*)dout, ST(stream)));
+}
+bm_status bm_k_add(int32_t dtype, int64_t n, const void* a, const void* b, void* out, void* stream) {
+  DISPATCH(dtype, add<bf16>(n, (const bf16*)a, (const bf16*)b, (bf16*)out, ST(stream)),
+           add<float>(n, (const float*)a, (const float*)b, (float*)out, ST(stream)));
+}
+bm_status bm_k_cast(int32_t src_dtype, int32_t dst_dtype, int64_t n, const void* src, void* dst, void* stream) {
+  return cast(src_dtype, dst_dtype, n, src, dst, ST(stream));
+}
+
+}  // extern "C"

@@ -1,0 +1,589 @@
+// sched.cpp -- host schedule builder: BigMac's pipeline scheduler.
+//
+//   get_llm_schedule   Megatron-style 1F1B / interleaved 1F1B lists
+//   columns            cut timeline = integer DES of the LLM lists with the
+//                      cost_fwd:cost_bwd ratio (R1)
+//   build_schedule     W warmup encoder units, then a sweep over LLM op starts
+//                      and trigger events: GEN(m) at the end of F(m, V-1) on
+//                      the last rank (llm_output_ready), ENC(u) at the
+//                      end of G_u = B(uP+P-1, 0) on rank 0 (encoder_grad_ready,
+//                      P:265) -> EncBwd(u) + EncFwd(next)
+//   insert_comm_ops    Recv right before each consumer, Send right after each
+//                      producer; act/grad, emb/embgrad gather and
+//                      scatter, genin/gengrad
+//   deadlock_check     happens-before graph (program order, per-peer send
+//                      chains, data edges, credit edges of the receive rings)
+//                      must be acyclic; rings sized minimal + slack
+// Output is bit-identical to oracle/schedule.py (tests/test_sched_parity.py).
+#include <algorithm>
+#include <cstring>
+#include <map>
+#include <set>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "../../include/bigmac.h"
+
+namespace bm {
+void set_error(const std::string& msg);
+}
+
+struct bm_schedule {
+  bm_sched_cfg cfg;
+  std::vector<std::vector<bm_op>> ranks;
+  std::vector<bm_sched_stats> stats;
+  std::map<std::tuple<int, int, int>, std::pair<int, int>> rings;  // (src,dst,payload) -> (K, nmsg)
+};
+
+namespace bm {
+namespace sched {
+
+struct Fail {
+  bm_status code;
+  std::string msg;
+};
+
+struct LOp {
+  bool bwd;
+  int mb, chunk;
+};
+
+static bm_op mk(int kind, int mb = -1, int chunk = -1, int unit = -1, int peer = -1, int payload = -1) {
+  bm_op o;
+  o.kind = kind; o.mb = mb; o.chunk = chunk; o.unit = unit; o.peer = peer; o.payload = payload;
+  o.slot = -1; o.seq = -1;
+  return o;
+}
+
+static void validate(const bm_sched_cfg& c) {
+  const int P = c.stages, M = c.microbatches, V = c.vchunks;
+  if (P < 1 || M < 1 || V < 1 || c.warmup_units < 0) throw Fail{BM_E_INVALID, "P, M, V must be >= 1 and W >= 0"};
+  if (c.cost_fwd < 1 || c.cost_bwd < 1 || c.ring_slack < 0)
+    throw Fail{BM_E_INVALID, "costs must be >= 1 and ring_slack >= 0"};
+  if (c.llm_sched == BM_LLM_1F1B && V != 1) throw Fail{BM_E_INVALID, "1F1B requires V == 1"};
+  if (c.llm_sched == BM_LLM_INTERLEAVED && V < 2) throw Fail{BM_E_INVALID, "interleaved 1F1B requires V >= 2"};
+  if (c.llm_sched != BM_LLM_1F1B && c.llm_sched != BM_LLM_INTERLEAVED) throw Fail{BM_E_INVALID, "unknown llm_sched"};
+  if (c.enc_place != BM_ENC_NONE && c.enc_place != BM_ENC_DP_UNIT) throw Fail{BM_E_INVALID, "unknown enc_place"};
+  if (c.gen_place != BM_GEN_NONE && c.gen_place != BM_GEN_DP_SHARD && c.gen_place != BM_GEN_LAST_STAGE)
+    throw Fail{BM_E_INVALID, "unknown gen_place"};
+  for (int i = 0; i < 6; ++i)
+    if (c.reserved[i] != 0) throw Fail{BM_E_INVALID, "reserved fields must be zero"};
+  if (M % P != 0) throw Fail{BM_E_REMAINDER, "M=" + std::to_string(M) + " is not a multiple of P=" + std::to_string(P)};
+}
+
+// ---------------------------------------------------------------- LLM base lists
+static std::vector<std::vector<LOp>> base_lists(int P, int M, int V) {
+  std::vector<std::vector<LOp>> out(P);
+  for (int r = 0; r < P; ++r) {
+    std::vector<LOp> fwd, bwd;
+    int w;
+    if (V == 1) {
+      w = std::min(P - r - 1, M);
+      for (int m = 0; m < M; ++m) { fwd.push_back({false, m, 0}); bwd.push_back({true, m, 0}); }
+    } else {
+      w = std::min(2 * (P - r - 1) + (V - 1) * P, M * V);
+      for (int k = 0; k < M * V; ++k) {
+        const int g = k / (P * V), j = k % (P * V);
+        const int c = j / P, m = g * P + (j % P);
+        fwd.push_back({false, m, c});
+        bwd.push_back({true, m, V - 1 - c});
+      }
+    }
+    const int total = (int)fwd.size();
+    auto& ops = out[r];
+    for (int k = 0; k < w; ++k) ops.push_back(fwd[k]);
+    for (int i = 0; i < total - w; ++i) { ops.push_back(fwd[w + i]); ops.push_back(bwd[i]); }
+    for (int i = total - w; i < total; ++i) ops.push_back(bwd[i]);
+  }
+  return out;
+}
+
+struct Times {
+  int P, M, V;
+  std::vector<int64_t> st, en;  // index(r, bwd, m, c)
+  size_t idx(int r, bool b, int m, int c) const { return (((size_t)r * 2 + (b ? 1 : 0)) * M + m) * V + c; }
+};
+
+static Times des_llm(const std::vector<std::vector<LOp>>& base, int P, int M, int V, int cf, int cb) {
+  Times T{P, M, V, {}, {}};
+  T.st.assign((size_t)P * 2 * M * V, -1);
+  T.en.assign((size_t)P * 2 * M * V, -1);
+  std::vector<size_t> ptr(P, 0);
+  std::vector<int64_t> freet(P, 0);
+  size_t remaining = 0;
+  for (auto& l : base) remaining += l.size();
+  while (remaining) {
+    bool prog = false;
+    for (int r = 0; r < P; ++r) {
+      while (ptr[r] < base[r].size()) {
+        const LOp& o = base[r][ptr[r]];
+        const int s = o.chunk * P + r;
+        int64_t dep_end = 0;
+        bool has = false;
+        if (!o.bwd && s > 0) {
+          const size_t d = T.idx((s - 1) % P, false, o.mb, (s - 1) / P);
+          if (T.en[d] < 0) break;
+          dep_end = T.en[d]; has = true;
+        }
+        if (o.bwd && s < P * V - 1) {
+          const size_t d = T.idx((s + 1) % P, true, o.mb, (s + 1) / P);
+          if (T.en[d] < 0) break;
+          dep_end = T.en[d]; has = true;
+        }
+        const int64_t start = std::max(freet[r], has ? dep_end : (int64_t)0);
+        const int64_t end = start + (o.bwd ? cb : cf);
+        const size_t me = T.idx(r, o.bwd, o.mb, o.chunk);
+        T.st[me] = start; T.en[me] = end;
+        freet[r] = end;
+        ++ptr[r]; --remaining; prog = true;
+      }
+    }
+    if (!prog) throw Fail{BM_E_DEPENDENCY, "LLM base schedule stalls"};
+  }
+  return T;
+}
+
+static int w_star(const std::vector<LOp>& base0, int P, int M) {
+  std::map<std::tuple<bool, int, int>, int> pos;
+  for (int i = 0; i < (int)base0.size(); ++i) pos[{base0[i].bwd, base0[i].mb, base0[i].chunk}] = i;
+  const int n_u = M / P;
+  int best = 1;
+  for (int i = 0; i < n_u; ++i) {
+    const int g = pos[{true, i * P + P - 1, 0}];
+    int cnt = 0;
+    for (int j = i; j < n_u; ++j)
+      if (pos[{false, j * P, 0}] < g) ++cnt;
+    best = std::max(best, cnt);
+  }
+  return best;
+}
+
+// ---------------------------------------------------------------- nesting
+static std::vector<std::vector<bm_op>> nest(const bm_sched_cfg& c, const std::vector<std::vector<LOp>>& base,
+                                            const Times& T, int& W_out) {
+  const int P = c.stages, M = c.microbatches, V = c.vchunks;
+  const int n_u = M / P;
+  const int W = c.warmup_units > 0 ? c.warmup_units : w_star(base[0], P, M);
+  W_out = W;
+  const bool enc = c.enc_place != BM_ENC_NONE;
+  struct Ev {
+    int64_t t;
+    int cls, tb;
+    int r, idx;  // LLM: rank, index in base[r]; GEN: m; ENC: u
+  };
+  std::vector<Ev> ev;
+  for (int r = 0; r < P; ++r)
+    for (int i = 0; i < (int)base[r].size(); ++i) {
+      const LOp& o = base[r][i];
+      ev.push_back({T.st[T.idx(r, o.bwd, o.mb, o.chunk)], 2, r, r, i});
+    }
+  if (c.gen_place != BM_GEN_NONE)
+    for (int m = 0; m < M; ++m) ev.push_back({T.en[T.idx(P - 1, false, m, V - 1)], 0, m, 0, m});
+  if (enc)
+    for (int u = 0; u < n_u; ++u) ev.push_back({T.en[T.idx(0, true, u * P + P - 1, 0)], 1, u, 0, u});
+  std::sort(ev.begin(), ev.end(), [](const Ev& a, const Ev& b) {
+    if (a.t != b.t) return a.t < b.t;
+    if (a.cls != b.cls) return a.cls < b.cls;
+    return a.tb < b.tb;
+  });
+  std::vector<std::vector<bm_op>> lists(P);
+  int nxt = 0;
+  if (enc) {
+    for (int u = 0; u < std::min(W, n_u); ++u)
+      for (int r = 0; r < P; ++r) lists[r].push_back(mk(BM_OP_ENC_FWD, u * P + r, -1, u));
+    nxt = std::min(W, n_u);
+  }
+  for (const Ev& e : ev) {
+    if (e.cls == 2) {
+      const LOp& o = base[e.r][e.idx];
+      if (enc && !o.bwd && e.r == 0 && o.chunk == 0 && o.mb / P >= nxt)
+        throw Fail{BM_E_WARMUP, "W=" + std::to_string(W) + " too small: F(" + std::to_string(o.mb) +
+                                    ",0)@0 precedes EncFwd(" + std::to_string(o.mb / P) + ")"};
+      lists[e.r].push_back(mk(o.bwd ? BM_OP_LLM_BWD : BM_OP_LLM_FWD, o.mb, o.chunk));
+    } else if (e.cls == 0) {
+      const int m = e.idx;
+      if (c.gen_place == BM_GEN_DP_SHARD) {
+        for (int r = 0; r < P; ++r) {
+          lists[r].push_back(mk(BM_OP_GEN_FWD, m));
+          lists[r].push_back(mk(BM_OP_GEN_BWD, m));
+        }
+      } else {
+        lists[P - 1].push_back(mk(BM_OP_GEN_FWD, m));
+        lists[P - 1].push_back(mk(BM_OP_GEN_BWD, m));
+      }
+    } else {
+      const int u = e.idx;
+      for (int r = 0; r < P; ++r) lists[r].push_back(mk(BM_OP_ENC_BWD, u * P + r, -1, u));
+      if (nxt < n_u) {
+        for (int r = 0; r < P; ++r) lists[r].push_back(mk(BM_OP_ENC_FWD, nxt * P + r, -1, nxt));
+        ++nxt;
+      }
+    }
+  }
+  return lists;
+}
+
+// ---------------------------------------------------------------- comm insertion
+static bool is_compute(int k) { return k <= BM_OP_GEN_BWD; }
+
+static void recvs_before(const bm_sched_cfg& c, int r, const bm_op& o, std::vector<bm_op>& out) {
+  const int P = c.stages, V = c.vchunks;
+  if (o.kind == BM_OP_LLM_FWD) {
+    const int s = o.chunk * P + r;
+    if (s > 0 && (s - 1) % P != r) out.push_back(mk(BM_OP_RECV, o.mb, o.chunk, -1, (s - 1) % P, BM_PAY_ACT));
+    if (s == 0 && c.enc_place != BM_ENC_NONE && o.mb % P != 0)
+      out.push_back(mk(BM_OP_RECV, o.mb, -1, o.mb / P, o.mb % P, BM_PAY_EMB));
+  } else if (o.kind == BM_OP_LLM_BWD) {
+    const int s = o.chunk * P + r;
+    if (s < P * V - 1 && (s + 1) % P != r) out.push_back(mk(BM_OP_RECV, o.mb, o.chunk, -1, (s + 1) % P, BM_PAY_GRAD));
+    if (s == P * V - 1 && c.gen_place == BM_GEN_DP_SHARD)
+      for (int q = 0; q < P; ++q)
+        if (q != r) out.push_back(mk(BM_OP_RECV, o.mb, -1, -1, q, BM_PAY_GENGRAD));
+  } else if (o.kind == BM_OP_ENC_BWD && r != 0) {
+    out.push_back(mk(BM_OP_RECV, o.mb, -1, o.unit, 0, BM_PAY_EMBGRAD));
+  } else if (o.kind == BM_OP_GEN_FWD && c.gen_place == BM_GEN_DP_SHARD && r != P - 1) {
+    out.push_back(mk(BM_OP_RECV, o.mb, -1, -1, P - 1, BM_PAY_GENIN));
+  }
+}
+
+static void sends_after(const bm_sched_cfg& c, int r, const bm_op& o, std::vector<bm_op>& out) {
+  const int P = c.stages, V = c.vchunks;
+  if (o.kind == BM_OP_LLM_FWD) {
+    const int s = o.chunk * P + r;
+    if (s < P * V - 1 && (s + 1) % P != r) out.push_back(mk(BM_OP_SEND, o.mb, o.chunk, -1, (s + 1) % P, BM_PAY_ACT));
+    if (s == P * V - 1 && c.gen_place == BM_GEN_DP_SHARD)
+      for (int q = 0; q < P; ++q)
+        if (q != r) out.push_back(mk(BM_OP_SEND, o.mb, -1, -1, q, BM_PAY_GENIN));
+  } else if (o.kind == BM_OP_LLM_BWD) {
+    const int s = o.chunk * P + r;
+    if (s > 0 && (s - 1) % P != r) out.push_back(mk(BM_OP_SEND, o.mb, o.chunk, -1, (s - 1) % P, BM_PAY_GRAD));
+    if (s == 0 && c.enc_place != BM_ENC_NONE && o.mb % P != 0)
+      out.push_back(mk(BM_OP_SEND, o.mb, -1, o.mb / P, o.mb % P, BM_PAY_EMBGRAD));
+  } else if (o.kind == BM_OP_ENC_FWD && r != 0) {
+    out.push_back(mk(BM_OP_SEND, o.mb, -1, o.unit, 0, BM_PAY_EMB));
+  } else if (o.kind == BM_OP_GEN_BWD && c.gen_place == BM_GEN_DP_SHARD && r != P - 1) {
+    out.push_back(mk(BM_OP_SEND, o.mb, -1, -1, P - 1, BM_PAY_GENGRAD));
+  }
+}
+
+typedef std::tuple<int, int, int> Chan;  // src, dst, payload
+
+// ---------------------------------------------------------------- deadlock graph
+struct Graph {
+  int n = 0;
+  std::vector<int> rank_base;
+  std::map<std::pair<Chan, int>, int> send_at, recv_at, release_at;  // -> node id
+  std::vector<std::pair<int, int>> base_edges;
+};
+
+static Graph build_graph(const std::vector<std::vector<bm_op>>& L) {
+  Graph g;
+  const int P = (int)L.size();
+  g.rank_base.resize(P);
+  for (int r = 0; r < P; ++r) { g.rank_base[r] = g.n; g.n += (int)L[r].size(); }
+  for (int r = 0; r < P; ++r) {
+    const auto& ops = L[r];
+    for (int i = 0; i < (int)ops.size(); ++i) {
+      const bm_op& o = ops[i];
+      if (o.kind == BM_OP_SEND) {
+        g.send_at[{Chan{r, o.peer, o.payload}, o.seq}] = g.rank_base[r] + i;
+      } else if (o.kind == BM_OP_RECV) {
+        Chan ch{o.peer, r, o.payload};
+        g.recv_at[{ch, o.seq}] = g.rank_base[r] + i;
+        int j = i + 1;
+        while (!is_compute(ops[j].kind)) ++j;
+        if (o.payload == BM_PAY_GENIN)
+          while (ops[j].kind != BM_OP_GEN_BWD) ++j;
+        g.release_at[{ch, o.seq}] = g.rank_base[r] + j;
+      }
+    }
+    int prev = -1;
+    std::map<int, int> last_send;
+    for (int i = 0; i < (int)ops.size(); ++i) {
+      const int id = g.rank_base[r] + i;
+      if (ops[i].kind == BM_OP_SEND) {
+        if (prev >= 0) g.base_edges.push_back({g.rank_base[r] + prev, id});
+        auto it = last_send.find(ops[i].peer);
+        if (it != last_send.end()) g.base_edges.push_back({g.rank_base[r] + it->second, id});
+        last_send[ops[i].peer] = i;
+      } else {
+        if (prev >= 0) g.base_edges.push_back({g.rank_base[r] + prev, id});
+        prev = i;
+      }
+    }
+  }
+  for (auto& kv : g.send_at) g.base_edges.push_back({kv.second, g.recv_at.at(kv.first)});
+  return g;
+}
+
+static void credit_edges(const Graph& g, const Chan& ch, int K, int nmsg, std::vector<std::pair<int, int>>& out) {
+  for (int j = K; j < nmsg; ++j) out.push_back({g.release_at.at({ch, j - K}), g.send_at.at({ch, j})});
+}
+
+static bool acyclic(int n, const std::vector<std::pair<int, int>>& e1, const std::vector<std::pair<int, int>>& e2) {
+  std::vector<int> indeg(n, 0), head(n, -1), nxt(e1.size() + e2.size()), to(e1.size() + e2.size());
+  int k = 0;
+  auto add = [&](const std::pair<int, int>& e) {
+    to[k] = e.second; nxt[k] = head[e.first]; head[e.first] = k; ++indeg[e.second]; ++k;
+  };
+  for (auto& e : e1) add(e);
+  for (auto& e : e2) add(e);
+  std::vector<int> q;
+  q.reserve(n);
+  for (int i = 0; i < n; ++i)
+    if (!indeg[i]) q.push_back(i);
+  size_t qi = 0;
+  while (qi < q.size()) {
+    const int x = q[qi++];
+    for (int e = head[x]; e >= 0; e = nxt[e])
+      if (--indeg[to[e]] == 0) q.push_back(to[e]);
+  }
+  return (int)q.size() == n;
+}
+
+// ---------------------------------------------------------------- verification
+static void verify_deps(const bm_sched_cfg& c, const std::vector<std::vector<bm_op>>& lists) {
+  const int P = c.stages, V = c.vchunks;
+  std::map<std::tuple<int, int, int, int>, int> nid;  // (rank, kind, mb, chunk)
+  auto key = [](int r, const bm_op& o) {
+    return std::make_tuple(r, o.kind, o.mb, (o.kind == BM_OP_LLM_FWD || o.kind == BM_OP_LLM_BWD) ? o.chunk : -1);
+  };
+  int n = 0;
+  for (int r = 0; r < P; ++r)
+    for (auto& o : lists[r]) {
+      auto k = key(r, o);
+      if (nid.count(k)) throw Fail{BM_E_DEPENDENCY, "duplicate compute op"};
+      nid[k] = n++;
+    }
+  std::vector<std::pair<int, int>> edges;
+  auto dep = [&](int r, int kind, int mb, int chunk, int to) {
+    auto it = nid.find(std::make_tuple(r, kind, mb, chunk));
+    if (it == nid.end()) throw Fail{BM_E_DEPENDENCY, "missing producer"};
+    edges.push_back({it->second, to});
+  };
+  for (int r = 0; r < P; ++r) {
+    for (size_t i = 0; i < lists[r].size(); ++i) {
+      const bm_op& o = lists[r][i];
+      const int me = nid[key(r, o)];
+      if (i) edges.push_back({nid[key(r, lists[r][i - 1])], me});
+      if (o.kind == BM_OP_LLM_FWD) {
+        const int s = o.chunk * P + r;
+        if (s > 0) dep((s - 1) % P, BM_OP_LLM_FWD, o.mb, (s - 1) / P, me);
+        else if (c.enc_place != BM_ENC_NONE) dep(o.mb % P, BM_OP_ENC_FWD, o.mb, -1, me);
+      } else if (o.kind == BM_OP_LLM_BWD) {
+        const int s = o.chunk * P + r;
+        dep(r, BM_OP_LLM_FWD, o.mb, o.chunk, me);
+        if (s < P * V - 1) dep((s + 1) % P, BM_OP_LLM_BWD, o.mb, (s + 1) / P, me);
+        else if (c.gen_place == BM_GEN_DP_SHARD) for (int q = 0; q < P; ++q) dep(q, BM_OP_GEN_BWD, o.mb, -1, me);
+        else if (c.gen_place == BM_GEN_LAST_STAGE) dep(P - 1, BM_OP_GEN_BWD, o.mb, -1, me);
+      } else if (o.kind == BM_OP_ENC_BWD) {
+        dep(r, BM_OP_ENC_FWD, o.mb, -1, me);
+        dep(0, BM_OP_LLM_BWD, o.mb, 0, me);
+      } else if (o.kind == BM_OP_GEN_FWD) {
+        dep(P - 1, BM_OP_LLM_FWD, o.mb, V - 1, me);
+      } else if (o.kind == BM_OP_GEN_BWD) {
+        dep(r, BM_OP_GEN_FWD, o.mb, -1, me);
+      }
+    }
+  }
+  if (!acyclic(n, edges, {})) throw Fail{BM_E_DEPENDENCY, "dependency cycle in the nested schedule"};
+}
+
+static int peak_window(const std::vector<bm_op>& ops, int open_k, int close_k) {
+  int cur = 0, best = 0;
+  for (auto& o : ops) {
+    if (o.kind == open_k) best = std::max(best, ++cur);
+    else if (o.kind == close_k) --cur;
+  }
+  return best;
+}
+
+// ---------------------------------------------------------------- driver
+static bm_schedule* build(const bm_sched_cfg& c) {
+  validate(c);
+  const int P = c.stages, M = c.microbatches, V = c.vchunks;
+  auto base = base_lists(P, M, V);
+  Times T = des_llm(base, P, M, V, c.cost_fwd, c.cost_bwd);
+  int W = 0;
+  auto lists = nest(c, base, T, W);
+  verify_deps(c, lists);
+  for (int r = 0; r < P; ++r) {  // LLM order preserved
+    size_t k = 0;
+    for (auto& o : lists[r]) {
+      if (o.kind != BM_OP_LLM_FWD && o.kind != BM_OP_LLM_BWD) continue;
+      if (k >= base[r].size() || base[r][k].bwd != (o.kind == BM_OP_LLM_BWD) || base[r][k].mb != o.mb ||
+          base[r][k].chunk != o.chunk)
+        throw Fail{BM_E_DEPENDENCY, "LLM order changed"};
+      ++k;
+    }
+  }
+  // comm insertion + sequence numbers
+  std::vector<std::vector<bm_op>> full(P);
+  for (int r = 0; r < P; ++r)
+    for (auto& o : lists[r]) {
+      recvs_before(c, r, o, full[r]);
+      full[r].push_back(o);
+      sends_after(c, r, o, full[r]);
+    }
+  std::map<Chan, int> scnt, rcnt;
+  for (int r = 0; r < P; ++r)
+    for (auto& o : full[r]) {
+      if (o.kind == BM_OP_SEND) o.seq = scnt[Chan{r, o.peer, o.payload}]++;
+      else if (o.kind == BM_OP_RECV) o.seq = rcnt[Chan{o.peer, r, o.payload}]++;
+    }
+  if (scnt != rcnt) throw Fail{BM_E_DEPENDENCY, "unmatched send/recv counts"};
+  // ring sizing
+  Graph g = build_graph(full);
+  if (!acyclic(g.n, g.base_edges, {})) throw Fail{BM_E_DEADLOCK, "schedule deadlocks even with unbounded slots"};
+  std::map<Chan, int> K;
+  for (auto& kv : scnt) {
+    const int nmsg = kv.second;
+    int k = 1;
+    while (k < nmsg) {
+      std::vector<std::pair<int, int>> ce;
+      credit_edges(g, kv.first, k, nmsg, ce);
+      if (acyclic(g.n, g.base_edges, ce)) break;
+      ++k;
+    }
+    K[kv.first] = std::min(k + c.ring_slack, nmsg);
+  }
+  for (;;) {
+    std::vector<std::pair<int, int>> ce;
+    for (auto& kv : scnt) credit_edges(g, kv.first, K[kv.first], kv.second, ce);
+    if (acyclic(g.n, g.base_edges, ce)) break;
+    bool grew = false;
+    for (auto& kv : scnt)
+      if (K[kv.first] < kv.second) { ++K[kv.first]; grew = true; }
+    if (!grew) throw Fail{BM_E_DEADLOCK, "credit rings cannot be sized"};
+  }
+  for (int r = 0; r < P; ++r)
+    for (auto& o : full[r]) {
+      if (o.kind == BM_OP_SEND) o.slot = o.seq % K[Chan{r, o.peer, o.payload}];
+      else if (o.kind == BM_OP_RECV) o.slot = o.seq % K[Chan{o.peer, r, o.payload}];
+    }
+  // stats
+  auto* s = new bm_schedule();
+  s->cfg = c;
+  s->ranks = std::move(full);
+  for (auto& kv : scnt) s->rings[kv.first] = {K[kv.first], kv.second};
+  int64_t makespan = 0;
+  for (auto e : T.en) makespan = std::max(makespan, e);
+  const bool enc = c.enc_place != BM_ENC_NONE;
+  const int ws = enc ? w_star(base[0], P, M) : 0;
+  for (int r = 0; r < P; ++r) {
+    bm_sched_stats st;
+    std::memset(&st, 0, sizeof(st));
+    st.w_star = ws;
+    st.warmup_units = enc ? W : 0;
+    st.peak_enc_units = peak_window(lists[r], BM_OP_ENC_FWD, BM_OP_ENC_BWD);
+    st.peak_gen_shards = peak_window(lists[r], BM_OP_GEN_FWD, BM_OP_GEN_BWD);
+    st.peak_llm_inflight = peak_window(lists[r], BM_OP_LLM_FWD, BM_OP_LLM_BWD);
+    st.n_ops = (int)s->ranks[r].size();
+    int64_t busy = 0;
+    for (auto& o : base[r]) busy += o.bwd ? c.cost_bwd : c.cost_fwd;
+    st.llm_idle_cost_units = makespan - busy;
+    st.makespan_cost_units = makespan;
+    for (auto& kv : s->rings)
+      if (std::get<1>(kv.first) == r) {
+        int p = std::get<2>(kv.first);
+        st.ring_slots[p] = std::max(st.ring_slots[p], kv.second.first);
+      }
+    s->stats.push_back(st);
+  }
+  return s;
+}
+
+}  // namespace sched
+}  // namespace bm
+
+// ================================================================ C ABI
+static const char* KIND_NAMES[] = {"EncFwd", "EncBwd", "LlmFwd", "LlmBwd", "GenFwd", "GenBwd", "Send", "Recv"};
+static const char* PAY_NAMES[] = {"act", "grad", "emb", "embgrad", "genin", "gengrad"};
+
+extern "C" {
+
+bm_status bm_build_schedule(const bm_sched_cfg* cfg, bm_schedule** out) {
+  if (!cfg || !out) {
+    bm::set_error("null argument");
+    return BM_E_INVALID;
+  }
+  try {
+    *out = bm::sched::build(*cfg);
+    return BM_OK;
+  } catch (const bm::sched::Fail& f) {
+    bm::set_error(f.msg);
+    *out = nullptr;
+    return f.code;
+  } catch (const std::exception& e) {
+    bm::set_error(std::string("internal error: ") + e.what());
+    *out = nullptr;
+    return BM_E_DEPENDENCY;
+  }
+}
+
+bm_status bm_schedule_rank_ops(const bm_schedule* s, int32_t rank, const bm_op** ops, int64_t* n) {
+  if (!s || !ops || !n || rank < 0 || rank >= (int)s->ranks.size()) {
+    bm::set_error("bad schedule/rank");
+    return BM_E_INVALID;
+  }
+  *ops = s->ranks[rank].data();
+  *n = (int64_t)s->ranks[rank].size();
+  return BM_OK;
+}
+
+bm_status bm_schedule_stats(const bm_schedule* s, int32_t rank, bm_sched_stats* out) {
+  if (!s || !out || rank < 0 || rank >= (int)s->stats.size()) {
+    bm::set_error("bad schedule/rank");
+    return BM_E_INVALID;
+  }
+  *out = s->stats[rank];
+  return BM_OK;
+}
+
+bm_status bm_schedule_ring(const bm_schedule* s, int32_t src, int32_t dst, int32_t payload, int32_t* K,
+                           int32_t* nmsg) {
+  if (!s || !K || !nmsg) {
+    bm::set_error("null argument");
+    return BM_E_INVALID;
+  }
+  auto it = s->rings.find(std::make_tuple(src, dst, payload));
+  *K = it == s->rings.end() ? 0 : it->second.first;
+  *nmsg = it == s->rings.end() ? 0 : it->second.second;
+  return BM_OK;
+}
+
+bm_status bm_schedule_serialize(const bm_schedule* s, char* buf, size_t cap, size_t* needed) {
+  if (!s || !needed) {
+    bm::set_error("null argument");
+    return BM_E_INVALID;
+  }
+  std::string out;
+  auto f = [&](int v) { out += (v < 0) ? std::string("-") : std::to_string(v); };
+  for (size_t r = 0; r < s->ranks.size(); ++r)
+    for (size_t i = 0; i < s->ranks[r].size(); ++i) {
+      const bm_op& o = s->ranks[r][i];
+      out += std::to_string(r); out += '\t';
+      out += std::to_string(i); out += '\t';
+      out += KIND_NAMES[o.kind]; out += '\t';
+      f(o.mb); out += '\t';
+      f(o.chunk); out += '\t';
+      f(o.unit); out += '\t';
+      f(o.peer); out += '\t';
+      out += (o.payload < 0) ? "-" : PAY_NAMES[o.payload]; out += '\t';
+      f(o.slot); out += '\t';
+      f(o.seq); out += '\n';
+    }
+  *needed = out.size() + 1;
+  if (cap == 0 || !buf) return BM_OK;
+  if (cap < out.size() + 1) {
+    bm::set_error("buffer too small");
+    return BM_E_INVALID;
+  }
+  std::memcpy(buf, out.c_str(), out.size() + 1);
+  return BM_OK;
+}
+
+void bm_schedule_free(bm_schedule* s) { delete s; }
+
+}  // extern "C"

@@ -1,0 +1,86 @@
+"""Time the tcgen05 GEMM on the model's shapes (CUDA events, warm, L2-flushed
+between iterations) next to cuBLAS (torch.matmul) for context.
+
+    python scripts/gemm_bench.py [--json out.json]
+"""
+import json
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2605_25451_b200 import _lib as L  # noqa: E402
+
+PEAK = 1664.4  # MEASURED_PEAKS bf16_tflops (burst)
+
+
+def bench(fn, iters=10, flush=None):
+    for _ in range(3):
+        fn()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(iters):
+        if flush is not None:
+            flush.zero_()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        fn()
+        e.record()
+        e.synchronize()
+        ts.append(s.elapsed_time(e))
+    ts.sort()
+    return ts[len(ts) // 2]
+
+
+def main():
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
+    shapes = [
+        # name, M, N, K, a_mn, b_mn, epi
+        ("C2 gate_up fwd", 4096, 16384, 2048, 0, 0, "store"),
+        ("C2 down fwd+res", 4096, 2048, 8192, 0, 0, "add"),
+        ("C2 down dgrad", 4096, 8192, 2048, 0, 1, "store"),
+        ("C2 gate_up wgrad", 16384, 2048, 4096, 1, 1, "accum"),
+        ("C2 head fwd", 3500, 32000, 2048, 0, 0, "store"),
+        ("8192^3", 8192, 8192, 8192, 0, 0, "store"),
+        ("C4 gate_up fwd", 8192, 22016, 4096, 0, 0, "store"),
+        ("enc fc1 n=554", 554, 1536, 384, 0, 0, "store"),
+    ]
+    out = []
+    for name, M, N, K, amn, bmn, epi in shapes:
+        A = torch.randn((K, M) if amn else (M, K), device="cuda").to(torch.bfloat16)
+        B = torch.randn((K, N) if bmn else (N, K), device="cuda").to(torch.bfloat16)
+        lda = M if amn else K
+        ldb = N if bmn else K
+        if epi == "accum":
+            C = torch.zeros((M, N), device="cuda", dtype=torch.float32)
+            cdt, e, R = 1, 1, None
+        else:
+            C = torch.zeros((M, N), device="cuda", dtype=torch.bfloat16)
+            cdt, e = 0, (2 if epi == "add" else 0)
+            R = torch.zeros((M, N), device="cuda", dtype=torch.bfloat16) if epi == "add" else None
+
+        def ours():
+            L.call("bm_k_gemm", 0, M, N, K, A.data_ptr(), lda, amn, B.data_ptr(), ldb, bmn, C.data_ptr(), N, cdt, e,
+                   R.data_ptr() if R is not None else None, N, 1.0, None)
+
+        a2 = A.t() if amn else A
+        b2 = B if bmn else B.t()
+
+        def cublas():
+            torch.matmul(a2, b2)
+
+        t = bench(ours, flush=flush)
+        tc = bench(cublas, flush=flush)
+        fl = 2.0 * M * N * K
+        row = dict(name=name, M=M, N=N, K=K, ms=t, tflops=fl / t / 1e9, frac=fl / t / 1e9 / PEAK,
+                   cublas_ms=tc, cublas_tflops=fl / tc / 1e9)
+        print(json.dumps(row))
+        out.append(row)
+    if "--json" in sys.argv:
+        with open(sys.argv[sys.argv.index("--json") + 1], "w") as f:
+            json.dump(out, f, indent=1)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,223 @@
+"""GPU parity of the individual sm_100a kernels (called through the C ABI of
+include/bigmac_kernels.h) against the oracle's fp64 definitions.
+
+Inputs are bf16-representable, so the only differences are the kernels'
+fp32 accumulation order and bf16 output rounding (tolerances stated per test).
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from oracle import model as om  # noqa: E402
+from synth import bf16_round  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+BF16, F32 = 0, 1
+
+
+@pytest.fixture(scope="module")
+def L():
+    from paper_2605_25451_b200 import _lib
+    return _lib
+
+
+def dev(x, dtype):
+    t = torch.tensor(np.asarray(x, np.float32), device="cuda")
+    return t.to(torch.bfloat16 if dtype == BF16 else torch.float32).contiguous()
+
+
+def host(t):
+    return t.float().cpu().numpy().astype(np.float64)
+
+
+def rnd(rng, *shape, scale=1.0):
+    return bf16_round(rng.standard_normal(shape).astype(np.float32) * scale).astype(np.float64)
+
+
+GEMM_SHAPES = [(128, 256, 64), (300, 200, 100), (1, 16, 48), (257, 513, 130), (64, 64, 16),
+               (129, 1000, 640), (2048, 2048, 1024), (40, 4096, 16)]
+
+
+@pytest.mark.parametrize("M,N,K", GEMM_SHAPES)
+@pytest.mark.parametrize("a_mn,b_mn", [(0, 0), (0, 1), (1, 1), (1, 0)])
+@pytest.mark.parametrize("dtype", [BF16, F32])
+def test_gemm_store_f32(L, M, N, K, a_mn, b_mn, dtype):
+    rng = np.random.default_rng(M * 7 + N * 3 + K + 11 * a_mn + 5 * b_mn)
+    A = rnd(rng, M, K)
+    B = rnd(rng, N, K)
+    Ad = dev(A.T.copy() if a_mn else A, dtype)
+    Bd = dev(B.T.copy() if b_mn else B, dtype)
+    lda = M if a_mn else K
+    ldb = N if b_mn else K
+    if dtype == BF16 and (lda % 8 or ldb % 8):
+        pytest.skip("bf16 TMA needs 16-byte strides")
+    C = torch.full((M, N), 7.0, device="cuda", dtype=torch.float32)
+    L.call("bm_k_gemm", dtype, M, N, K, Ad.data_ptr(), lda, a_mn, Bd.data_ptr(), ldb, b_mn,
+           C.data_ptr(), N, F32, 0, None, 0, 1.0, None)
+    torch.cuda.synchronize()
+    ref = A @ B.T
+    err = np.abs(host(C) - ref).max()
+    tol = 1e-5 * np.sqrt(K) * max(1.0, np.abs(ref).max()) if dtype == BF16 else 2e-6 * np.sqrt(K) * max(1.0, np.abs(ref).max())
+    assert err <= tol, (err, tol)
+
+
+@pytest.mark.parametrize("M,N,K", [(300, 200, 100), (257, 513, 130), (1024, 768, 512)])
+@pytest.mark.parametrize("epi", ["bf16_store", "bf16_add", "f32_accum"])
+def test_gemm_epilogues(L, M, N, K, epi):
+    rng = np.random.default_rng(1)
+    A, B = rnd(rng, M, K), rnd(rng, N, K)
+    R = rnd(rng, M, N)
+    Ad, Bd = dev(A, BF16), dev(B, BF16)
+    ref = A @ B.T * 0.5
+    if epi == "bf16_store":
+        C = torch.zeros((M, N), device="cuda", dtype=torch.bfloat16)
+        L.call("bm_k_gemm", BF16, M, N, K, Ad.data_ptr(), K, 0, Bd.data_ptr(), K, 0, C.data_ptr(), N, BF16, 0,
+               None, 0, 0.5, None)
+    elif epi == "bf16_add":
+        C = torch.zeros((M, N), device="cuda", dtype=torch.bfloat16)
+        Rd = dev(R, BF16)
+        L.call("bm_k_gemm", BF16, M, N, K, Ad.data_ptr(), K, 0, Bd.data_ptr(), K, 0, C.data_ptr(), N, BF16, 2,
+               Rd.data_ptr(), N, 0.5, None)
+        ref = ref + R
+    else:
+        C = dev(R, F32)
+        L.call("bm_k_gemm", BF16, M, N, K, Ad.data_ptr(), K, 0, Bd.data_ptr(), K, 0, C.data_ptr(), N, F32, 1,
+               None, 0, 0.5, None)
+        ref = ref + R
+    torch.cuda.synchronize()
+    out = host(C)
+    if epi.startswith("bf16"):
+        assert np.all(np.abs(out - ref) <= 2.0 ** -8 * np.abs(ref) + 1e-4 * np.sqrt(K))
+    else:
+        assert np.abs(out - ref).max() <= 1e-5 * np.sqrt(K)
+
+
+@pytest.mark.parametrize("dtype", [BF16, F32])
+@pytest.mark.parametrize("rows,cols", [(1, 64), (37, 128), (300, 2048)])
+def test_rmsnorm(L, dtype, rows, cols):
+    rng = np.random.default_rng(2)
+    x = rnd(rng, rows, cols, scale=2.0)
+    g = rnd(rng, cols, scale=0.5) + 1.0
+    g = bf16_round(g.astype(np.float32)).astype(np.float64)
+    dy = rnd(rng, rows, cols)
+    dres = rnd(rng, rows, cols)
+    xd, gd, dyd, dresd = dev(x, dtype), dev(g, dtype), dev(dy, dtype), dev(dres, dtype)
+    y = torch.empty_like(xd)
+    rstd = torch.empty(rows, device="cuda", dtype=torch.float32)
+    L.call("bm_k_rmsnorm_fwd", dtype, rows, cols, xd.data_ptr(), gd.data_ptr(), y.data_ptr(), rstd.data_ptr(), None)
+    dx = torch.empty_like(xd)
+    dg = torch.full((cols,), 0.25, device="cuda", dtype=torch.float32)
+    part = torch.empty(L.lib().bm_k_rmsnorm_bwd_scratch(rows, cols), device="cuda", dtype=torch.float32)
+    L.call("bm_k_rmsnorm_bwd", dtype, rows, cols, dyd.data_ptr(), xd.data_ptr(), gd.data_ptr(), rstd.data_ptr(),
+           dresd.data_ptr(), dx.data_ptr(), dg.data_ptr(), part.data_ptr(), None)
+    torch.cuda.synchronize()
+    yr, rs = om.rmsnorm(x, g)
+    dxr, dgr = om.rmsnorm_bwd(dy, x, g, rs)
+    tol = 1e-2 if dtype == BF16 else 1e-5
+    assert np.abs(host(y) - yr).max() <= tol * np.abs(yr).max()
+    assert np.abs(host(rstd) - rs[:, 0]).max() <= 1e-5 * np.abs(rs).max()
+    assert np.abs(host(dx) - (dxr + dres)).max() <= tol * np.abs(dxr + dres).max()
+    assert np.abs(host(dg) - (dgr + 0.25)).max() <= 1e-4 * max(1, np.abs(dgr).max())
+
+
+@pytest.mark.parametrize("dtype", [BF16, F32])
+def test_swiglu_gelu(L, dtype):
+    rng = np.random.default_rng(3)
+    rows, f = 77, 384
+    gu = rnd(rng, rows, 2 * f, scale=2.0)
+    dh = rnd(rng, rows, f)
+    gud, dhd = dev(gu, dtype), dev(dh, dtype)
+    h = torch.empty((rows, f), device="cuda", dtype=gud.dtype)
+    dgu = torch.empty_like(gud)
+    L.call("bm_k_swiglu_fwd", dtype, rows, f, gud.data_ptr(), h.data_ptr(), None)
+    L.call("bm_k_swiglu_bwd", dtype, rows, f, dhd.data_ptr(), gud.data_ptr(), dgu.data_ptr(), None)
+    a = rnd(rng, 1001, scale=3.0)
+    ad, dz = dev(a, dtype), dev(np.ones(1001), dtype)
+    z = torch.empty_like(ad)
+    da = torch.empty_like(ad)
+    L.call("bm_k_gelu_fwd", dtype, 1001, ad.data_ptr(), z.data_ptr(), None)
+    L.call("bm_k_gelu_bwd", dtype, 1001, dz.data_ptr(), ad.data_ptr(), da.data_ptr(), None)
+    torch.cuda.synchronize()
+    tol = 1e-2 if dtype == BF16 else 1e-5
+    hr = om.swiglu(gu, f)
+    assert np.abs(host(h) - hr).max() <= tol * np.abs(hr).max()
+    dgur = om.swiglu_bwd(dh, gu, f)
+    assert np.abs(host(dgu) - dgur).max() <= tol * np.abs(dgur).max()
+    assert np.abs(host(z) - om.gelu(a)).max() <= tol * np.abs(om.gelu(a)).max()
+    assert np.abs(host(da) - om.gelu_bwd(np.ones(1001), a)).max() <= tol * 1.2
+
+
+@pytest.mark.parametrize("dtype", [BF16, F32])
+@pytest.mark.parametrize("S,d,n_mod,vocab", [(128, 128, 40, 256), (4096, 256, 700, 1000), (64, 64, 64, 50)])
+def test_embed(L, dtype, S, d, n_mod, vocab):
+    rng = np.random.default_rng(4)
+    table = rnd(rng, vocab, d)
+    emb = rnd(rng, n_mod, d)
+    ids = rng.integers(0, vocab, size=S).astype(np.int32)
+    dX = rnd(rng, S, d)
+    td, ed, dXd = dev(table, dtype), dev(emb, dtype), dev(dX, dtype)
+    idd = torch.tensor(ids, device="cuda")
+    X = torch.empty((S, d), device="cuda", dtype=td.dtype)
+    L.call("bm_k_embed_fwd", dtype, S, d, n_mod, idd.data_ptr(), td.data_ptr(), ed.data_ptr(), X.data_ptr(), None)
+    dT = torch.zeros((vocab, d), device="cuda", dtype=torch.float32)
+    scratch = torch.empty(L.lib().bm_k_embed_bwd_scratch(S), device="cuda", dtype=torch.uint8)
+    L.call("bm_k_embed_bwd", dtype, S, d, n_mod, idd.data_ptr(), dXd.data_ptr(), dT.data_ptr(), scratch.data_ptr(),
+           None)
+    dT2 = torch.zeros_like(dT)
+    L.call("bm_k_embed_bwd", dtype, S, d, n_mod, idd.data_ptr(), dXd.data_ptr(), dT2.data_ptr(), scratch.data_ptr(),
+           None)
+    torch.cuda.synchronize()
+    Xr = om.embed_fwd({"llm.embed": table}, ids, emb, n_mod)
+    assert np.array_equal(host(X), Xr)   # pure data movement: bit exact
+    G = {}
+
+    class Cfg:
+        pass
+    c = Cfg()
+    c.vocab, c.d = vocab, d
+    om.embed_bwd(c, dX, ids, n_mod, G)
+    assert np.abs(host(dT) - G["llm.embed"]).max() <= 1e-5 * max(1, np.abs(G["llm.embed"]).max())
+    assert torch.equal(dT, dT2)          # deterministic
+
+
+@pytest.mark.parametrize("dtype", [BF16, F32])
+@pytest.mark.parametrize("n,V", [(88, 256), (300, 32000), (1, 50)])
+def test_cross_entropy(L, dtype, n, V):
+    rng = np.random.default_rng(5)
+    z = rnd(rng, n, V, scale=2.0)
+    lab = rng.integers(0, V, size=n).astype(np.int32)
+    zd = dev(z, dtype)
+    labd = torch.tensor(lab, device="cuda")
+    loss = torch.full((1,), 3.0, device="cuda", dtype=torch.float32)
+    scr = torch.empty(n, device="cuda", dtype=torch.float32)
+    L.call("bm_k_ce_fwd_bwd", dtype, n, V, zd.data_ptr(), labd.data_ptr(), 0.25, loss.data_ptr(), 1.0, 1,
+           scr.data_ptr(), None)
+    torch.cuda.synchronize()
+    zmax = z.max(1, keepdims=True)
+    lse = np.log(np.exp(z - zmax).sum(1, keepdims=True)) + zmax
+    ref = np.mean(lse[:, 0] - z[np.arange(n), lab])
+    p = np.exp(z - lse)
+    p[np.arange(n), lab] -= 1
+    tol = 1e-2 if dtype == BF16 else 1e-5
+    assert abs(host(loss)[0] - (3.0 + ref)) <= 1e-5 * max(1, abs(ref))
+    assert np.abs(host(zd) - 0.25 * p).max() <= tol * 0.25
+
+
+@pytest.mark.parametrize("dtype", [BF16, F32])
+def test_mse(L, dtype):
+    rng = np.random.default_rng(6)
+    n, dt = 173, 16
+    o, t = rnd(rng, n, dt), rnd(rng, n, dt)
+    od, tdv = dev(o, dtype), dev(t, dtype)
+    dout = torch.empty_like(od)
+    loss = torch.full((1,), 1.0, device="cuda", dtype=torch.float32)
+    denom = float(500 * dt)
+    L.call("bm_k_mse_fwd_bwd", dtype, n, dt, od.data_ptr(), tdv.data_ptr(), denom, 0.5, 1.0, loss.data_ptr(),
+           dout.data_ptr(), None)
+    torch.cuda.synchronize()
+    assert abs(host(loss)[0] - (1.0 + np.sum((o - t) ** 2) / denom)) <= 1e-5
+    tol = 1e-2 if dtype == BF16 else 1e-6
+    ref = 2 * (o - t) / denom * 0.5
+    assert np.abs(host(dout) - ref).max() <= tol * np.abs(ref).max()

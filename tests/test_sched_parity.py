@@ -1,0 +1,65 @@
+"""C++ schedule builder (through the C ABI) vs the oracle: byte-identical
+serialization, identical statistics and ring sizes, identical error codes.
+CPU-only (no GPU needed to build schedules)."""
+import pytest
+
+from oracle import schedule as S
+
+L = pytest.importorskip("paper_2605_25451_b200._lib")
+from paper_2605_25451_b200 import schedule as BS  # noqa: E402
+
+GRID = [(P, M, V) for P in (1, 2, 3, 4, 8) for V in (1, 2, 4) for M in (P, 2 * P, 8 * P)]
+GRID += [(4, 64, 2), (8, 64, 1), (8, 64, 2), (4, 16, 1), (4, 32, 2), (2, 4, 1)]
+
+
+def both(P, M, V, **kw):
+    sched = "1f1b" if V == 1 else "interleaved"
+    o = S.build(S.SchedCfg(P, M, V, llm_sched=sched, **kw))
+    c = BS.build(P, M, V, **kw)
+    return o, c
+
+
+@pytest.mark.parametrize("P,M,V", GRID)
+@pytest.mark.parametrize("kw", [{}, {"cost_fwd": 1, "cost_bwd": 1}, {"gen_place": "last_stage"},
+                                {"gen_place": "none", "ring_slack": 0}, {"warmup_units": 3}])
+def test_serialization_identical(P, M, V, kw):
+    try:
+        o = S.build(S.SchedCfg(P, M, V, llm_sched="1f1b" if V == 1 else "interleaved", **kw))
+    except S.ScheduleError as e:
+        with pytest.raises(L.BigMacError) as ce:
+            BS.build(P, M, V, **kw)
+        assert ce.value.code == e.code
+        return
+    c = BS.build(P, M, V, **kw)
+    assert c.serialize() == S.serialize(o)
+    for r in range(P):
+        st, so = c.stats(r), o.stats[r]
+        assert (st.w_star, st.warmup_units, st.peak_enc_units, st.peak_gen_shards, st.peak_llm_inflight,
+                st.n_ops, st.llm_idle_cost_units, st.makespan_cost_units) == \
+            (so.w_star, so.warmup_units, so.peak_enc_units, so.peak_gen_shards, so.peak_llm_inflight,
+             so.n_ops, so.llm_idle_cost_units, so.makespan_cost_units)
+        assert list(st.ring_slots) == [so.ring_slots[p] for p in S.PAYLOADS]
+    for (src, dst, pay), K in o.rings.items():
+        assert c.ring(src, dst, S.PAYLOADS.index(pay))[0] == K
+
+
+@pytest.mark.parametrize("args,code", [((4, 63, 1), 2), ((4, 32, 2, 2), 3)])
+def test_error_codes(args, code):
+    P, M, V = args[:3]
+    kw = {"warmup_units": args[3]} if len(args) > 3 else {}
+    with pytest.raises(L.BigMacError) as e:
+        BS.build(P, M, V, **kw)
+    assert e.value.code == code
+
+
+def test_invalid_v_for_1f1b():
+    with pytest.raises(L.BigMacError) as e:
+        BS.build(2, 4, 2, llm_sched="1f1b")
+    assert e.value.code == 1
+
+
+def test_golden_file():
+    import os
+    path = os.path.join(os.path.dirname(__file__), "golden", "sched_P4_M8_V2.tsv")
+    with open(path) as f:
+        assert BS.build(4, 8, 2).serialize() == f.read()
