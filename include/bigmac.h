@@ -149,7 +149,7 @@ typedef struct {
   int32_t rows, cols; /* [out, in]; norm gains: rows = n, cols = 1          */
   int64_t offset;     /* element offset into the weight and grad buffers    */
   int32_t kind;       /* bm_param_kind                                      */
-  int32_t reserved;
+  int32_t ld;         /* row stride in elements (cols rounded up to 8)      */
 } bm_param_info;
 
 /* Parameters held by `rank` under `sc` (layers of its virtual stages; the
@@ -225,6 +225,13 @@ bm_status bm_ctx_launch_count(const bm_ctx* c, int64_t* n);
 /* Peak bytes of stash memory live during the last step, per module
  * (0 encoder, 1 LLM, 2 generator) -- the schedule's activation footprint. */
 bm_status bm_ctx_stash_peak(const bm_ctx* c, int64_t out[3]);
+/* Measurement support (bench.py roofline): when enabled, every GEMM launch of
+ * subsequent steps is bracketed by CUDA events on the compute stream.
+ * Enabling/disabling resets the totals. */
+bm_status bm_ctx_set_timing(bm_ctx* c, int32_t enable);
+/* Totals since timing was enabled: GEMM launches, algorithmic FLOPs (2MNK),
+ * summed device milliseconds.  Synchronizes on the recorded events. */
+bm_status bm_ctx_gemm_stats(bm_ctx* c, int64_t* n_gemm, double* flops, double* ms);
 void bm_ctx_destroy(bm_ctx* c);
 
 #ifdef __cplusplus

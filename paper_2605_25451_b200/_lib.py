@@ -55,7 +55,7 @@ class ModelCfg(C.Structure):
 
 class ParamInfo(C.Structure):
     _fields_ = [("name", C.c_char * 48), ("rows", C.c_int32), ("cols", C.c_int32), ("offset", C.c_int64),
-                ("kind", C.c_int32), ("reserved", C.c_int32)]
+                ("kind", C.c_int32), ("ld", C.c_int32)]
 
 
 class CtxSizes(C.Structure):
@@ -98,6 +98,8 @@ SIGNATURES = {
     "bm_ctx_loss_ptr": [_P, C.POINTER(_P)],
     "bm_ctx_launch_count": [_P, C.POINTER(_I64)],
     "bm_ctx_stash_peak": [_P, C.POINTER(_I64)],
+    "bm_ctx_set_timing": [_P, _I32],
+    "bm_ctx_gemm_stats": [_P, C.POINTER(_I64), C.POINTER(C.c_double), C.POINTER(C.c_double)],
     "bm_ctx_destroy": [_P],
     # bigmac_kernels.h
     "bm_k_gemm": [_I32, _I32, _I32, _I32, _P, _I64, _I32, _P, _I64, _I32, _P, _I64, _I32, _I32, _P, _I64, _F, _P],

@@ -549,4 +549,12 @@ BM_INST(float)
 
 int64_t rmsnorm_bwd_scratch_floats(int rows, int cols) { return (int64_t)dg_chunks(rows) * cols; }
 
+// step loss L = (1/M) sum_m (CE_m + MSE_m) from loss[0:2M] into loss[2M]
+bm_status loss_finalize(int M, float* loss, cudaStream_t st) {
+  sum_scale_kernel<<<1, 1024, 0, st>>>(2 * M, loss, 1.f / M, 0, loss + 2 * M);
+  count_launch();
+  BM_CUDA_TRY(cudaGetLastError());
+  return BM_OK;
+}
+
 }  // namespace bm

@@ -1,0 +1,1204 @@
+// executor.cu -- BigMac's pipeline executor on one B200 per rank.
+//
+// The rank's op list (bm_build_schedule) is interpreted as an opcode stream
+// (P:351-352): LLM / encoder / generator compute ops enqueue the model's
+// sm_100a kernels on the caller's compute stream; Send ops push the payload
+// into the receiver's peer-mapped receive slot with a copy-engine copy on a
+// per-destination comm stream, then bump the receiver's sequence flag
+// (cuStreamWriteValue32, fenced); Recv ops make the compute stream wait for
+// that flag (cuStreamWaitValue32) -- "waits on receive handles before
+// consuming" without a host round trip.  The op that releases a slot
+// writes a credit back to the sender, which waits for it before reusing the
+// slot (ring sizes from the builder's deadlock check).
+// Runtime buffers are stash slots keyed by (mb, chunk) for the
+// LLM, by unit for the encoder, one for the generator.  DP gradients of the
+// encoder/projector/generator are accumulated locally and summed once at the
+// end of the step with NCCL.
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cstring>
+#include <map>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include <nccl.h>
+
+#include "common.cuh"
+#include "kernels.h"
+#include "sched_internal.h"
+
+namespace bm {
+
+// ------------------------------------------------------------------ driver entry points
+typedef CUresult (*StreamValueFn)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+typedef CUresult (*AddrRangeFn)(CUdeviceptr*, size_t*, CUdeviceptr);
+struct Drv {
+  StreamValueFn wait32 = nullptr, write32 = nullptr;
+  AddrRangeFn addr_range = nullptr;
+};
+static Drv& drv() {
+  static Drv d;
+  static bool init = false;
+  if (!init) {
+    init = true;
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &p, cudaEnableDefault, &q) == cudaSuccess && q == cudaDriverEntryPointSuccess)
+      d.wait32 = (StreamValueFn)p;
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &p, cudaEnableDefault, &q) == cudaSuccess && q == cudaDriverEntryPointSuccess)
+      d.write32 = (StreamValueFn)p;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &p, cudaEnableDefault, &q) == cudaSuccess && q == cudaDriverEntryPointSuccess)
+      d.addr_range = (AddrRangeFn)p;
+  }
+  return d;
+}
+
+// ------------------------------------------------------------------ NCCL (dlopen'ed)
+struct Nccl {
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  bool ok = false;
+};
+static Nccl& nccl() {
+  static Nccl n;
+  static bool init = false;
+  if (!init) {
+    init = true;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (h) {
+      n.GetUniqueId = (decltype(n.GetUniqueId))dlsym(h, "ncclGetUniqueId");
+      n.CommInitRank = (decltype(n.CommInitRank))dlsym(h, "ncclCommInitRank");
+      n.AllReduce = (decltype(n.AllReduce))dlsym(h, "ncclAllReduce");
+      n.GroupStart = (decltype(n.GroupStart))dlsym(h, "ncclGroupStart");
+      n.GroupEnd = (decltype(n.GroupEnd))dlsym(h, "ncclGroupEnd");
+      n.CommDestroy = (decltype(n.CommDestroy))dlsym(h, "ncclCommDestroy");
+      n.GetErrorString = (decltype(n.GetErrorString))dlsym(h, "ncclGetErrorString");
+      n.ok = n.GetUniqueId && n.CommInitRank && n.AllReduce && n.GroupStart && n.GroupEnd && n.CommDestroy;
+    }
+  }
+  return n;
+}
+#define BM_NCCL_TRY(expr)                                                                          \
+  do {                                                                                             \
+    ncclResult_t _r = (expr);                                                                      \
+    if (_r != ncclSuccess) {                                                                       \
+      set_error(std::string(#expr) + ": " + (nccl().GetErrorString ? nccl().GetErrorString(_r) : "nccl error")); \
+      return BM_E_NCCL;                                                                            \
+    }                                                                                              \
+  } while (0)
+
+// ------------------------------------------------------------------ parameter layout
+struct PEntry {
+  std::string name;
+  int rows, cols, ld;
+  int64_t off;
+  int kind;
+};
+
+static int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+static int round8(int x) { return (x + 7) / 8 * 8; }
+
+static bm_status check_model(const bm_model_cfg& mc, const bm_sched_cfg& sc) {
+  BM_CHECK_ARG(mc.S > 0 && mc.d > 0 && mc.f > 0 && mc.L > 0 && mc.vocab > 0, "bad LLM dims");
+  BM_CHECK_ARG(mc.d_in > 0 && mc.d_e > 0 && mc.f_e > 0 && mc.L_e >= 0, "bad encoder dims");
+  BM_CHECK_ARG(mc.d_g > 0 && mc.f_g > 0 && mc.L_g >= 0 && mc.d_t > 0, "bad generator dims");
+  BM_CHECK_ARG(mc.dtype == BM_BF16 || mc.dtype == BM_F32, "dtype must be bf16 or fp32");
+  BM_CHECK_ARG(mc.L % (sc.stages * sc.vchunks) == 0, "L must be a multiple of P*V");
+  BM_CHECK_ARG(mc.d % 8 == 0 && mc.f % 8 == 0 && mc.d_e % 8 == 0 && mc.f_e % 8 == 0 && mc.d_g % 8 == 0 &&
+                   mc.f_g % 8 == 0 && mc.d_t % 8 == 0 && mc.vocab % 8 == 0,
+               "model widths must be multiples of 8");
+  BM_CHECK_ARG(mc.max_n_mod > 0 && mc.max_n_mod <= mc.S && mc.max_n_gen > 0 && mc.max_n_gen <= mc.S,
+               "max_n_mod / max_n_gen must be in [1, S]");
+  return BM_OK;
+}
+
+static std::vector<PEntry> param_layout(const bm_model_cfg& mc, const bm_sched_cfg& sc, int rank, int64_t* total,
+                                        int64_t* dp) {
+  std::vector<PEntry> v;
+  int64_t off = 0;
+  auto add = [&](const std::string& n, int rows, int cols, int kind) {
+    const int ld = cols == 1 ? 1 : round8(cols);
+    v.push_back({n, rows, cols, ld, off, kind});
+    off = align_up(off + (int64_t)rows * ld, 64);
+  };
+  add("enc.patch", mc.d_e, mc.d_in, BM_PARAM_DP);
+  for (int i = 0; i < mc.L_e; ++i) {
+    const std::string p = "enc.blk" + std::to_string(i);
+    add(p + ".norm", mc.d_e, 1, BM_PARAM_DP);
+    add(p + ".fc1", mc.f_e, mc.d_e, BM_PARAM_DP);
+    add(p + ".fc2", mc.d_e, mc.f_e, BM_PARAM_DP);
+  }
+  add("enc.proj1", mc.d, mc.d_e, BM_PARAM_DP);
+  add("enc.proj2", mc.d, mc.d, BM_PARAM_DP);
+  add("gen.in", mc.d_g, mc.d, BM_PARAM_DP);
+  for (int i = 0; i < mc.L_g; ++i) {
+    const std::string p = "gen.blk" + std::to_string(i);
+    add(p + ".norm", mc.d_g, 1, BM_PARAM_DP);
+    add(p + ".fc1", mc.f_g, mc.d_g, BM_PARAM_DP);
+    add(p + ".fc2", mc.d_g, mc.f_g, BM_PARAM_DP);
+  }
+  add("gen.out", mc.d_t, mc.d_g, BM_PARAM_DP);
+  *dp = off;
+  const int P = sc.stages, V = sc.vchunks;
+  const int lps = mc.L / (P * V);
+  if (rank == 0) add("llm.embed", mc.vocab, mc.d, BM_PARAM_LLM);
+  for (int c = 0; c < V; ++c) {
+    const int s = c * P + rank;
+    for (int l = s * lps; l < (s + 1) * lps; ++l) {
+      const std::string p = "llm.layer" + std::to_string(l);
+      add(p + ".norm", mc.d, 1, BM_PARAM_LLM);
+      add(p + ".gate_up", 2 * mc.f, mc.d, BM_PARAM_LLM);
+      add(p + ".down", mc.d, mc.f, BM_PARAM_LLM);
+    }
+  }
+  if (rank == P - 1) {
+    add("llm.final_norm", mc.d, 1, BM_PARAM_LLM);
+    add("llm.head", mc.vocab, mc.d, BM_PARAM_LLM);
+  }
+  *total = off;
+  return v;
+}
+
+// ------------------------------------------------------------------ context
+struct Chan {
+  int src, dst, pay, K, nmsg;
+  int64_t slot_bytes;
+  int64_t data_off;    // in dst's comm buffer
+  int64_t flag_off;    // data flag, in dst's comm buffer
+  int64_t credit_off;  // credit flag, in src's comm buffer
+};
+
+struct LlmSlot {
+  std::vector<char*> x, xn, gu, h;
+  std::vector<float*> rstd;
+  char *gin = nullptr, *Hn = nullptr, *dHn = nullptr;
+  float* rstd_f = nullptr;
+};
+struct MlpSlot {  // encoder (L_e blocks) or generator (L_g blocks)
+  std::vector<char*> E, xn, a, z;
+  std::vector<float*> rstd;
+  char *a1 = nullptr, *p1 = nullptr, *out = nullptr, *dout = nullptr;
+};
+
+}  // namespace bm
+
+using namespace bm;
+
+struct bm_ctx {
+  bm_model_cfg mc;
+  bm_sched_cfg sc;
+  const bm_schedule* s = nullptr;
+  int rank = 0, P = 1, M = 1, V = 1, lps = 1, dtype = 0;
+  size_t es = 2;
+  std::vector<PEntry> params;
+  std::unordered_map<std::string, int> pidx;
+  int64_t total_elems = 0, dp_elems = 0;
+  bool has_enc = false, has_gen = false, gen_last = false;
+  int n_enc_slots = 0, n_llm_slots = 0, gen_rows = 0;
+  // comm layout
+  std::vector<Chan> chans;
+  std::map<std::tuple<int, int, int>, int> chan_idx;
+  std::vector<int64_t> comm_size;  // per rank
+  // op annotations
+  std::vector<std::vector<int>> release_of;  // op index -> recv op indices released after it
+  // work layout
+  int64_t work_bytes = 0;
+  std::vector<LlmSlot> llm;
+  std::vector<MlpSlot> enc;
+  MlpSlot gen;
+  char *dwork[2] = {nullptr, nullptr}, *bout[2] = {nullptr, nullptr}, *dh = nullptr, *dgu = nullptr, *dxn = nullptr;
+  float* part = nullptr;
+  char* embscr = nullptr;
+  char* logits = nullptr;
+  float* ce_scr = nullptr;
+  char *e_dE = nullptr, *e_dp = nullptr, *e_dz = nullptr, *e_da = nullptr, *e_dxn = nullptr;
+  char *g_dG = nullptr, *g_dz = nullptr, *g_da = nullptr, *g_dxn = nullptr, *gout[2] = {nullptr, nullptr};
+  char* emb_local = nullptr;
+  float* loss = nullptr;
+  char *st_patches = nullptr, *st_ids = nullptr, *st_labels = nullptr, *st_targets = nullptr;
+  int ld_patch_stage = 0;
+  // bound buffers
+  char* W = nullptr;
+  float* G = nullptr;
+  char* work = nullptr;
+  char* comm = nullptr;
+  bool bound = false;
+  std::vector<char*> peer;
+  // streams / events
+  std::vector<cudaStream_t> comm_st;
+  std::vector<cudaEvent_t> evpool;
+  size_t evnext = 0;
+  cudaEvent_t bout_ev[2] = {nullptr, nullptr}, gout_ev[2] = {nullptr, nullptr};
+  bool bout_pending[2] = {false, false}, gout_pending[2] = {false, false};
+  int bsel = 0, gsel = 0;
+  ncclComm_t nc = nullptr;
+  int64_t step = 0;
+  int64_t launches = 0;
+  int64_t stash_peak[3] = {0, 0, 0};
+  // per-step state
+  cudaStream_t st = nullptr;
+  std::vector<int> llm_free;
+  std::map<std::pair<int, int>, int> llm_live;
+  std::vector<const char*> mb_patches, mb_targets;
+  const int32_t *ids = nullptr, *labels = nullptr;
+  std::vector<int> n_mod, n_gen;
+  int ld_patch = 0;
+  const void* last_src = nullptr;   // payload source of the last compute op
+  int last_src_ring = -1;           // 0: bout, 1: gout (ring buffers needing a copy-done event)
+  int last_src_idx = 0;
+  std::vector<const char*> genin_src;  // per destination rank (last stage)
+  cudaEvent_t producer_ev = nullptr;
+  // GEMM timing (bench roofline): event pairs around every GEMM, two pools by step parity
+  bool timing = false;
+  std::vector<cudaEvent_t> tev[2];
+  size_t tev_used[2] = {0, 0};
+  double tflop_pending[2] = {0, 0};
+  double gemm_flops = 0, gemm_ms = 0;
+  int64_t gemm_count = 0;
+  int64_t gemm_count_pending[2] = {0, 0};
+  ~bm_ctx();
+};
+
+bm_ctx::~bm_ctx() {
+  for (auto s_ : comm_st)
+    if (s_) cudaStreamDestroy(s_);
+  for (auto e : evpool)
+    if (e) cudaEventDestroy(e);
+  for (int k = 0; k < 2; ++k)
+    for (auto e : tev[k])
+      if (e) cudaEventDestroy(e);
+  for (int i = 0; i < 2; ++i) {
+    if (bout_ev[i]) cudaEventDestroy(bout_ev[i]);
+    if (gout_ev[i]) cudaEventDestroy(gout_ev[i]);
+  }
+  for (size_t r = 0; r < peer.size(); ++r)
+    if (peer[r] && (int)r != rank) cudaIpcCloseMemHandle(peer[r]);
+  if (nc && nccl().ok) nccl().CommDestroy(nc);
+  cudaGetLastError();  // never leave a sticky-looking error for the caller's next API call
+}
+
+namespace bm {
+
+// ------------------------------------------------------------------ layouts
+static int64_t payload_rows_max(const bm_ctx& c, int pay) {
+  switch (pay) {
+    case BM_PAY_ACT:
+    case BM_PAY_GRAD: return c.mc.S;
+    case BM_PAY_EMB:
+    case BM_PAY_EMBGRAD: return c.mc.max_n_mod;
+    default: return c.gen_rows;
+  }
+}
+
+static void comm_layout(bm_ctx& c) {
+  c.comm_size.assign(c.P, 0);
+  std::vector<int64_t> flag_cur(c.P, 0);
+  for (auto& kv : c.s->rings) {
+    Chan ch;
+    ch.src = std::get<0>(kv.first);
+    ch.dst = std::get<1>(kv.first);
+    ch.pay = std::get<2>(kv.first);
+    ch.K = kv.second.first;
+    ch.nmsg = kv.second.second;
+    ch.slot_bytes = align_up(payload_rows_max(c, ch.pay) * c.mc.d * (int64_t)c.es, 256);
+    ch.flag_off = flag_cur[ch.dst];
+    flag_cur[ch.dst] += 64;
+    ch.credit_off = flag_cur[ch.src];
+    flag_cur[ch.src] += 64;
+    c.chan_idx[kv.first] = (int)c.chans.size();
+    c.chans.push_back(ch);
+  }
+  std::vector<int64_t> data_cur(c.P);
+  for (int r = 0; r < c.P; ++r) data_cur[r] = align_up(flag_cur[r], 256);
+  for (auto& ch : c.chans) {
+    ch.data_off = data_cur[ch.dst];
+    data_cur[ch.dst] += ch.K * ch.slot_bytes;
+  }
+  for (int r = 0; r < c.P; ++r) c.comm_size[r] = align_up(std::max<int64_t>(data_cur[r], 256), 256);
+}
+
+struct Bump {
+  char* base;
+  int64_t off = 0;
+  char* take(int64_t bytes) {
+    char* p = base ? base + off : nullptr;
+    off = align_up(off + std::max<int64_t>(bytes, 0), 256);
+    return p;
+  }
+};
+
+static void work_layout(bm_ctx& c, char* base) {
+  Bump b{base};
+  const auto& m = c.mc;
+  const int64_t es = c.es, S = m.S, d = m.d, f = m.f;
+  const bool last_rank = c.rank == c.P - 1;
+  c.llm.assign(c.n_llm_slots, LlmSlot());
+  for (auto& sl : c.llm) {
+    sl.x.resize(c.lps + 1); sl.xn.resize(c.lps); sl.gu.resize(c.lps); sl.h.resize(c.lps); sl.rstd.resize(c.lps);
+    for (int j = 0; j <= c.lps; ++j) sl.x[j] = b.take(S * d * es);
+    for (int j = 0; j < c.lps; ++j) {
+      sl.xn[j] = b.take(S * d * es);
+      sl.rstd[j] = (float*)b.take(S * 4);
+      sl.gu[j] = b.take(S * 2 * f * es);
+      sl.h[j] = b.take(S * f * es);
+    }
+    sl.gin = b.take(S * d * es);
+    if (last_rank) {
+      sl.Hn = b.take(S * d * es);
+      sl.dHn = b.take(S * d * es);
+      sl.rstd_f = (float*)b.take(S * 4);
+    }
+  }
+  auto mlp_slot = [&](MlpSlot& sl, int n, int dm, int fm, int Lb, int dproj, bool proj, int dt) {
+    sl.E.resize(Lb + 1); sl.xn.resize(Lb); sl.a.resize(Lb); sl.z.resize(Lb); sl.rstd.resize(Lb);
+    for (int j = 0; j <= Lb; ++j) sl.E[j] = b.take((int64_t)n * dm * es);
+    for (int j = 0; j < Lb; ++j) {
+      sl.xn[j] = b.take((int64_t)n * dm * es);
+      sl.rstd[j] = (float*)b.take((int64_t)n * 4);
+      sl.a[j] = b.take((int64_t)n * fm * es);
+      sl.z[j] = b.take((int64_t)n * fm * es);
+    }
+    if (proj) {
+      sl.a1 = b.take((int64_t)n * dproj * es);
+      sl.p1 = b.take((int64_t)n * dproj * es);
+      sl.out = b.take((int64_t)n * dproj * es);
+    } else {
+      sl.out = b.take((int64_t)n * dt * es);
+      sl.dout = b.take((int64_t)n * dt * es);
+    }
+  };
+  c.enc.assign(c.n_enc_slots, MlpSlot());
+  for (auto& sl : c.enc) mlp_slot(sl, m.max_n_mod, m.d_e, m.f_e, m.L_e, m.d, true, 0);
+  if (c.has_gen && c.gen_rows > 0) mlp_slot(c.gen, c.gen_rows, m.d_g, m.f_g, m.L_g, 0, false, m.d_t);
+  // LLM scratch
+  for (int i = 0; i < 2; ++i) c.dwork[i] = b.take(S * d * es);
+  for (int i = 0; i < 2; ++i) c.bout[i] = b.take(S * d * es);
+  c.dh = b.take(S * f * es);
+  c.dgu = b.take(S * 2 * f * es);
+  c.dxn = b.take(S * d * es);
+  const int wmax = std::max(std::max(m.d, m.d_e), m.d_g);
+  c.part = (float*)b.take(rmsnorm_bwd_scratch_floats(std::max(S, (int64_t)m.max_n_mod), wmax) * 4);
+  c.embscr = b.take(embed_bwd_scratch_bytes(m.S));
+  if (last_rank) {
+    c.logits = b.take(S * m.vocab * es);
+    c.ce_scr = (float*)b.take(S * 4);
+  }
+  // encoder / generator scratch
+  const int64_t n = m.max_n_mod;
+  c.e_dE = b.take(n * m.d_e * es);
+  c.e_dp = b.take(n * d * es);
+  c.e_dz = b.take(n * m.f_e * es);
+  c.e_da = b.take(n * std::max(m.f_e, m.d) * es);
+  c.e_dxn = b.take(n * m.d_e * es);
+  const int64_t ng = std::max(c.gen_rows, 1);
+  c.g_dG = b.take(ng * m.d_g * es);
+  c.g_dz = b.take(ng * m.f_g * es);
+  c.g_da = b.take(ng * m.f_g * es);
+  c.g_dxn = b.take(ng * m.d_g * es);
+  for (int i = 0; i < 2; ++i) c.gout[i] = b.take(ng * d * es);
+  c.emb_local = b.take(n * d * es);
+  c.loss = (float*)b.take((2 * (int64_t)c.M + 1) * 4);
+  // host-batch staging
+  c.ld_patch_stage = round8(m.d_in);
+  c.st_patches = b.take((int64_t)c.M * m.max_n_mod * c.ld_patch_stage * es);
+  c.st_ids = b.take((int64_t)c.M * S * 4);
+  c.st_labels = b.take((int64_t)c.M * S * 4);
+  c.st_targets = b.take((int64_t)c.M * m.max_n_gen * m.d_t * es);
+  c.work_bytes = b.off;
+}
+
+// ------------------------------------------------------------------ helpers
+static inline char* P_(bm_ctx& c, const char* name) {
+  auto it = c.pidx.find(name);
+  return it == c.pidx.end() ? nullptr : c.W + c.params[it->second].off * c.es;
+}
+static inline float* G_(bm_ctx& c, const char* name) {
+  auto it = c.pidx.find(name);
+  return it == c.pidx.end() ? nullptr : c.G + c.params[it->second].off;
+}
+static inline int LD_(bm_ctx& c, const char* name) { return c.params[c.pidx.at(name)].ld; }
+
+static bm_status timed_gemm(bm_ctx& c, int M, int N, int K, const void* A, int64_t lda, int am, const void* B,
+                            int64_t ldb, int bm_, void* C, int64_t ldc, int cdt, int epi, const void* R, int64_t ldr) {
+  if (!c.timing || M <= 0 || N <= 0 || K <= 0)
+    return gemm(c.dtype, M, N, K, A, lda, am, B, ldb, bm_, C, ldc, cdt, epi, R, ldr, 1.f, c.st);
+  const int pool = (int)(c.step & 1);
+  auto& ev = c.tev[pool];
+  if (c.tev_used[pool] + 2 > ev.size()) {
+    for (int k = 0; k < 256; ++k) {
+      cudaEvent_t e;
+      BM_CUDA_TRY(cudaEventCreate(&e));
+      ev.push_back(e);
+    }
+  }
+  cudaEvent_t e0 = ev[c.tev_used[pool]], e1 = ev[c.tev_used[pool] + 1];
+  c.tev_used[pool] += 2;
+  BM_CUDA_TRY(cudaEventRecord(e0, c.st));
+  BM_TRY(gemm(c.dtype, M, N, K, A, lda, am, B, ldb, bm_, C, ldc, cdt, epi, R, ldr, 1.f, c.st));
+  BM_CUDA_TRY(cudaEventRecord(e1, c.st));
+  c.tflop_pending[pool] += 2.0 * M * N * K;
+  c.gemm_count_pending[pool] += 1;
+  return BM_OK;
+}
+// fold a finished pool's event pairs into the totals (blocks until they completed)
+static bm_status harvest(bm_ctx& c, int pool) {
+  auto& ev = c.tev[pool];
+  if (c.tev_used[pool] == 0) return BM_OK;
+  BM_CUDA_TRY(cudaEventSynchronize(ev[c.tev_used[pool] - 1]));
+  double ms = 0;
+  for (size_t i = 0; i + 1 < c.tev_used[pool]; i += 2) {
+    float t = 0;
+    BM_CUDA_TRY(cudaEventElapsedTime(&t, ev[i], ev[i + 1]));
+    ms += t;
+  }
+  c.gemm_ms += ms;
+  c.gemm_flops += c.tflop_pending[pool];
+  c.gemm_count += c.gemm_count_pending[pool];
+  c.tev_used[pool] = 0;
+  c.tflop_pending[pool] = 0;
+  c.gemm_count_pending[pool] = 0;
+  return BM_OK;
+}
+static bm_status lin_fwd(bm_ctx& c, int n, int in, int out, const void* X, int64_t ldx, const void* Wt, int64_t ldw,
+                         void* Y, int epi = BM_EPI_STORE, const void* R = nullptr) {
+  return timed_gemm(c, n, out, in, X, ldx, 0, Wt, ldw, 0, Y, out, c.dtype, epi, R, out);
+}
+static bm_status lin_dgrad(bm_ctx& c, int n, int in, int out, const void* dY, const void* Wt, int64_t ldw, void* dX,
+                           int64_t lddx, int epi = BM_EPI_STORE, const void* R = nullptr) {
+  return timed_gemm(c, n, in, out, dY, out, 0, Wt, ldw, 1, dX, lddx, c.dtype, epi, R, lddx);
+}
+static bm_status lin_wgrad(bm_ctx& c, int n, int in, int out, const void* dY, const void* X, int64_t ldx, float* dW,
+                           int64_t ldw) {
+  if (n <= 0) return BM_OK;
+  return timed_gemm(c, out, in, n, dY, out, 1, X, ldx, 1, dW, ldw, BM_F32, BM_EPI_ACCUM, nullptr, 0);
+}
+#define TY(c, bfcall, fcall) ((c).dtype == BM_BF16 ? (bfcall) : (fcall))
+static bm_status norm_fwd(bm_ctx& c, int rows, int cols, const void* x, const void* g, void* y, float* rstd) {
+  return TY(c, rmsnorm_fwd<bf16>(rows, cols, (const bf16*)x, (const bf16*)g, (bf16*)y, rstd, c.st),
+            rmsnorm_fwd<float>(rows, cols, (const float*)x, (const float*)g, (float*)y, rstd, c.st));
+}
+static bm_status norm_bwd(bm_ctx& c, int rows, int cols, const void* dy, const void* x, const void* g,
+                          const float* rstd, const void* dres, void* dx, float* dg) {
+  return TY(c, rmsnorm_bwd<bf16>(rows, cols, (const bf16*)dy, (const bf16*)x, (const bf16*)g, rstd, (const bf16*)dres,
+                                 (bf16*)dx, dg, c.part, c.st),
+            rmsnorm_bwd<float>(rows, cols, (const float*)dy, (const float*)x, (const float*)g, rstd, (const float*)dres,
+                               (float*)dx, dg, c.part, c.st));
+}
+static bm_status gelu_f(bm_ctx& c, int64_t n, const void* a, void* z) {
+  return TY(c, gelu_fwd<bf16>(n, (const bf16*)a, (bf16*)z, c.st), gelu_fwd<float>(n, (const float*)a, (float*)z, c.st));
+}
+static bm_status gelu_b(bm_ctx& c, int64_t n, const void* dz, const void* a, void* da) {
+  return TY(c, gelu_bwd<bf16>(n, (const bf16*)dz, (const bf16*)a, (bf16*)da, c.st),
+            gelu_bwd<float>(n, (const float*)dz, (const float*)a, (float*)da, c.st));
+}
+static bm_status add_(bm_ctx& c, int64_t n, const void* a, const void* b, void* o) {
+  return TY(c, add<bf16>(n, (const bf16*)a, (const bf16*)b, (bf16*)o, c.st),
+            add<float>(n, (const float*)a, (const float*)b, (float*)o, c.st));
+}
+static bm_status d2d(bm_ctx& c, void* dst, const void* src, int64_t bytes) {
+  if (bytes > 0) BM_CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, c.st));
+  return BM_OK;
+}
+static cudaEvent_t next_event(bm_ctx& c) {
+  cudaEvent_t e = c.evpool[c.evnext];
+  c.evnext = (c.evnext + 1) % c.evpool.size();
+  return e;
+}
+static void shard_rows(const bm_ctx& c, int m, int r, int* lo, int* hi) {
+  const int n = c.n_gen[m];
+  if (c.gen_last) { *lo = 0; *hi = n; return; }
+  *lo = (int)(((int64_t)r * n) / c.P);
+  *hi = (int)(((int64_t)(r + 1) * n) / c.P);
+}
+
+// ------------------------------------------------------------------ residual MLP blocks (encoder / generator)
+static bm_status mlp_blocks_fwd(bm_ctx& c, MlpSlot& sl, const char* prefix, int Lb, int n, int dm, int fm) {
+  char nm[64];
+  for (int i = 0; i < Lb; ++i) {
+    snprintf(nm, sizeof nm, "%s.blk%d.norm", prefix, i);
+    BM_TRY(norm_fwd(c, n, dm, sl.E[i], P_(c, nm), sl.xn[i], sl.rstd[i]));
+    snprintf(nm, sizeof nm, "%s.blk%d.fc1", prefix, i);
+    BM_TRY(lin_fwd(c, n, dm, fm, sl.xn[i], dm, P_(c, nm), LD_(c, nm), sl.a[i]));
+    BM_TRY(gelu_f(c, (int64_t)n * fm, sl.a[i], sl.z[i]));
+    snprintf(nm, sizeof nm, "%s.blk%d.fc2", prefix, i);
+    BM_TRY(lin_fwd(c, n, fm, dm, sl.z[i], fm, P_(c, nm), LD_(c, nm), sl.E[i + 1], BM_EPI_ADD, sl.E[i]));
+  }
+  return BM_OK;
+}
+// dE (n x dm) in/out, updated in place through the blocks in reverse
+static bm_status mlp_blocks_bwd(bm_ctx& c, MlpSlot& sl, const char* prefix, int Lb, int n, int dm, int fm, char* dE,
+                                char* dz, char* da, char* dxn) {
+  char nm[64];
+  for (int i = Lb - 1; i >= 0; --i) {
+    snprintf(nm, sizeof nm, "%s.blk%d.fc2", prefix, i);
+    BM_TRY(lin_wgrad(c, n, fm, dm, dE, sl.z[i], fm, G_(c, nm), LD_(c, nm)));
+    BM_TRY(lin_dgrad(c, n, fm, dm, dE, P_(c, nm), LD_(c, nm), dz, fm));
+    BM_TRY(gelu_b(c, (int64_t)n * fm, dz, sl.a[i], da));
+    snprintf(nm, sizeof nm, "%s.blk%d.fc1", prefix, i);
+    BM_TRY(lin_wgrad(c, n, dm, fm, da, sl.xn[i], dm, G_(c, nm), LD_(c, nm)));
+    BM_TRY(lin_dgrad(c, n, dm, fm, da, P_(c, nm), LD_(c, nm), dxn, dm));
+    snprintf(nm, sizeof nm, "%s.blk%d.norm", prefix, i);
+    BM_TRY(norm_bwd(c, n, dm, dxn, sl.E[i], P_(c, nm), sl.rstd[i], dE, dE, G_(c, nm)));
+  }
+  return BM_OK;
+}
+
+// ------------------------------------------------------------------ op handlers
+static char* recv_slot(bm_ctx& c, int src, int pay, int seq) {
+  const Chan& ch = c.chans[c.chan_idx.at(std::make_tuple(src, c.rank, pay))];
+  return c.comm + ch.data_off + (int64_t)(seq % ch.K) * ch.slot_bytes;
+}
+
+struct RecvState {  // the Recv ops seen since the last compute op (consumer inputs)
+  std::vector<const bm_op*> ops;
+};
+
+static bm_status op_enc_fwd(bm_ctx& c, const bm_op& o) {
+  const auto& m = c.mc;
+  const int mb = o.mb, n = c.n_mod[mb];
+  MlpSlot& sl = c.enc[o.unit % c.n_enc_slots];
+  BM_TRY(lin_fwd(c, n, m.d_in, m.d_e, c.mb_patches[mb], c.ld_patch, P_(c, "enc.patch"), LD_(c, "enc.patch"), sl.E[0]));
+  BM_TRY(mlp_blocks_fwd(c, sl, "enc", m.L_e, n, m.d_e, m.f_e));
+  BM_TRY(lin_fwd(c, n, m.d_e, m.d, sl.E[m.L_e], m.d_e, P_(c, "enc.proj1"), LD_(c, "enc.proj1"), sl.a1));
+  BM_TRY(gelu_f(c, (int64_t)n * m.d, sl.a1, sl.p1));
+  BM_TRY(lin_fwd(c, n, m.d, m.d, sl.p1, m.d, P_(c, "enc.proj2"), LD_(c, "enc.proj2"), sl.out));
+  c.last_src = sl.out;
+  c.last_src_ring = -1;
+  return BM_OK;
+}
+
+static bm_status op_enc_bwd(bm_ctx& c, const bm_op& o, const RecvState& rs) {
+  const auto& m = c.mc;
+  const int mb = o.mb, n = c.n_mod[mb];
+  MlpSlot& sl = c.enc[o.unit % c.n_enc_slots];
+  const char* dout = c.rank == 0 ? c.emb_local : recv_slot(c, 0, BM_PAY_EMBGRAD, rs.ops.at(0)->seq);
+  BM_TRY(lin_wgrad(c, n, m.d, m.d, dout, sl.p1, m.d, G_(c, "enc.proj2"), LD_(c, "enc.proj2")));
+  BM_TRY(lin_dgrad(c, n, m.d, m.d, dout, P_(c, "enc.proj2"), LD_(c, "enc.proj2"), c.e_dp, m.d));
+  BM_TRY(gelu_b(c, (int64_t)n * m.d, c.e_dp, sl.a1, c.e_da));
+  BM_TRY(lin_wgrad(c, n, m.d_e, m.d, c.e_da, sl.E[m.L_e], m.d_e, G_(c, "enc.proj1"), LD_(c, "enc.proj1")));
+  BM_TRY(lin_dgrad(c, n, m.d_e, m.d, c.e_da, P_(c, "enc.proj1"), LD_(c, "enc.proj1"), c.e_dE, m.d_e));
+  BM_TRY(mlp_blocks_bwd(c, sl, "enc", m.L_e, n, m.d_e, m.f_e, c.e_dE, c.e_dz, c.e_da, c.e_dxn));
+  BM_TRY(lin_wgrad(c, n, m.d_in, m.d_e, c.e_dE, c.mb_patches[mb], c.ld_patch, G_(c, "enc.patch"), LD_(c, "enc.patch")));
+  return BM_OK;
+}
+
+static bm_status op_llm_fwd(bm_ctx& c, const bm_op& o, const RecvState& rs) {
+  const auto& m = c.mc;
+  const int mb = o.mb, ch = o.chunk, s = ch * c.P + c.rank;
+  const int64_t S = m.S, d = m.d, es = c.es;
+  if (c.llm_free.empty()) {
+    set_error("no free LLM stash slot (schedule/peak mismatch)");
+    return BM_E_STATE;
+  }
+  const int slot = c.llm_free.back();
+  c.llm_free.pop_back();
+  c.llm_live[{mb, ch}] = slot;
+  LlmSlot& sl = c.llm[slot];
+  // stage input (P:297 embed_preprocess at the entry stage)
+  if (s == 0) {
+    const int n_mod = c.n_mod[mb];
+    const char* emb = (mb % c.P == 0) ? c.enc[(mb / c.P) % c.n_enc_slots].out
+                                      : recv_slot(c, mb % c.P, BM_PAY_EMB, rs.ops.at(0)->seq);
+    BM_TRY(TY(c, embed_fwd<bf16>(m.S, m.d, n_mod, c.ids + (int64_t)mb * S, (const bf16*)P_(c, "llm.embed"), (const bf16*)emb, (bf16*)sl.x[0], c.st),
+              embed_fwd<float>(m.S, m.d, n_mod, c.ids + (int64_t)mb * S, (const float*)P_(c, "llm.embed"), (const float*)emb, (float*)sl.x[0], c.st)));
+  } else if ((s - 1) % c.P == c.rank) {
+    const int prev = c.llm_live.at({mb, ch - 1});
+    BM_TRY(d2d(c, sl.x[0], c.llm[prev].x[c.lps], S * d * es));
+  } else {
+    BM_TRY(d2d(c, sl.x[0], recv_slot(c, (s - 1) % c.P, BM_PAY_ACT, rs.ops.at(0)->seq), S * d * es));
+  }
+  char nm[64];
+  for (int j = 0; j < c.lps; ++j) {
+    const int l = s * c.lps + j;
+    snprintf(nm, sizeof nm, "llm.layer%d.norm", l);
+    BM_TRY(norm_fwd(c, m.S, m.d, sl.x[j], P_(c, nm), sl.xn[j], sl.rstd[j]));
+    snprintf(nm, sizeof nm, "llm.layer%d.gate_up", l);
+    BM_TRY(lin_fwd(c, m.S, m.d, 2 * m.f, sl.xn[j], m.d, P_(c, nm), LD_(c, nm), sl.gu[j]));
+    BM_TRY(TY(c, swiglu_fwd<bf16>(m.S, m.f, (const bf16*)sl.gu[j], (bf16*)sl.h[j], c.st),
+              swiglu_fwd<float>(m.S, m.f, (const float*)sl.gu[j], (float*)sl.h[j], c.st)));
+    snprintf(nm, sizeof nm, "llm.layer%d.down", l);
+    BM_TRY(lin_fwd(c, m.S, m.f, m.d, sl.h[j], m.f, P_(c, nm), LD_(c, nm), sl.x[j + 1], BM_EPI_ADD, sl.x[j]));
+  }
+  c.last_src = sl.x[c.lps];
+  c.last_src_ring = -1;
+  if (s == c.P * c.V - 1) {
+    // last stage: final norm, LM head + CE (fwd and bwd through the head), generator inputs
+    const int n_mod = c.n_mod[mb], n_text = m.S - n_mod;
+    BM_TRY(norm_fwd(c, m.S, m.d, sl.x[c.lps], P_(c, "llm.final_norm"), sl.Hn, sl.rstd_f));
+    BM_CUDA_TRY(cudaMemsetAsync(sl.dHn, 0, (size_t)n_mod * d * es, c.st));
+    if (n_text > 0) {
+      const char* hn_text = sl.Hn + (int64_t)n_mod * d * es;
+      BM_TRY(lin_fwd(c, n_text, m.d, m.vocab, hn_text, m.d, P_(c, "llm.head"), LD_(c, "llm.head"), c.logits));
+      const float sg = 1.f / ((float)n_text * c.M);
+      BM_TRY(TY(c, ce_fwd_bwd<bf16>(n_text, m.vocab, (bf16*)c.logits, c.labels + (int64_t)mb * S + n_mod, sg, c.loss + mb, 1.f, 0, c.ce_scr, c.st),
+                ce_fwd_bwd<float>(n_text, m.vocab, (float*)c.logits, c.labels + (int64_t)mb * S + n_mod, sg, c.loss + mb, 1.f, 0, c.ce_scr, c.st)));
+      BM_TRY(lin_dgrad(c, n_text, m.d, m.vocab, c.logits, P_(c, "llm.head"), LD_(c, "llm.head"),
+                       sl.dHn + (int64_t)n_mod * d * es, m.d));
+      BM_TRY(lin_wgrad(c, n_text, m.d, m.vocab, c.logits, hn_text, m.d, G_(c, "llm.head"), LD_(c, "llm.head")));
+    }
+    const int n_gen = c.n_gen[mb];
+    c.genin_src.assign(c.P, nullptr);
+    for (int q = 0; q < c.P; ++q) {
+      int lo, hi;
+      shard_rows(c, mb, q, &lo, &hi);
+      c.genin_src[q] = sl.Hn + (int64_t)(m.S - n_gen + lo) * d * es;
+    }
+  }
+  return BM_OK;
+}
+
+static bm_status op_llm_bwd(bm_ctx& c, const bm_op& o, const RecvState& rs) {
+  const auto& m = c.mc;
+  const int mb = o.mb, ch = o.chunk, s = ch * c.P + c.rank;
+  const int64_t S = m.S, d = m.d, es = c.es;
+  const int slot = c.llm_live.at({mb, ch});
+  LlmSlot& sl = c.llm[slot];
+  const char* cur;
+  if (s == c.P * c.V - 1) {
+    // add the generator input-gradient shards into dHn, then final-norm backward
+    const int n_gen = c.n_gen[mb];
+    if (c.has_gen && !c.gen_last) {
+      for (const bm_op* r : rs.ops) {
+        int lo, hi;
+        shard_rows(c, mb, r->peer, &lo, &hi);
+        char* dst = sl.dHn + (int64_t)(m.S - n_gen + lo) * d * es;
+        BM_TRY(add_(c, (int64_t)(hi - lo) * d, dst, recv_slot(c, r->peer, BM_PAY_GENGRAD, r->seq), dst));
+      }
+    }
+    BM_TRY(norm_bwd(c, m.S, m.d, sl.dHn, sl.x[c.lps], P_(c, "llm.final_norm"), sl.rstd_f, nullptr, c.dwork[0],
+                    G_(c, "llm.final_norm")));
+    cur = c.dwork[0];
+  } else if ((s + 1) % c.P == c.rank) {
+    cur = sl.gin;
+  } else {
+    cur = recv_slot(c, (s + 1) % c.P, BM_PAY_GRAD, rs.ops.at(0)->seq);
+  }
+  // output ring buffer (must not be overwritten before its previous send copy finished)
+  const int b = c.bsel;
+  c.bsel ^= 1;
+  if (c.bout_pending[b]) {
+    BM_CUDA_TRY(cudaStreamWaitEvent(c.st, c.bout_ev[b], 0));
+    c.bout_pending[b] = false;
+  }
+  char nm[64];
+  for (int j = c.lps - 1; j >= 0; --j) {
+    const int l = s * c.lps + j;
+    char* out = (j == 0) ? c.bout[b] : (cur == c.dwork[0] ? c.dwork[1] : c.dwork[0]);
+    snprintf(nm, sizeof nm, "llm.layer%d.down", l);
+    BM_TRY(lin_wgrad(c, m.S, m.f, m.d, cur, sl.h[j], m.f, G_(c, nm), LD_(c, nm)));
+    BM_TRY(lin_dgrad(c, m.S, m.f, m.d, cur, P_(c, nm), LD_(c, nm), c.dh, m.f));
+    BM_TRY(TY(c, swiglu_bwd<bf16>(m.S, m.f, (const bf16*)c.dh, (const bf16*)sl.gu[j], (bf16*)c.dgu, c.st),
+              swiglu_bwd<float>(m.S, m.f, (const float*)c.dh, (const float*)sl.gu[j], (float*)c.dgu, c.st)));
+    snprintf(nm, sizeof nm, "llm.layer%d.gate_up", l);
+    BM_TRY(lin_wgrad(c, m.S, m.d, 2 * m.f, c.dgu, sl.xn[j], m.d, G_(c, nm), LD_(c, nm)));
+    BM_TRY(lin_dgrad(c, m.S, m.d, 2 * m.f, c.dgu, P_(c, nm), LD_(c, nm), c.dxn, m.d));
+    snprintf(nm, sizeof nm, "llm.layer%d.norm", l);
+    BM_TRY(norm_bwd(c, m.S, m.d, c.dxn, sl.x[j], P_(c, nm), sl.rstd[j], cur, out, G_(c, nm)));
+    cur = out;
+  }
+  c.last_src = c.bout[b];
+  c.last_src_ring = 0;
+  c.last_src_idx = b;
+  if (s == 0) {
+    const int n_mod = c.n_mod[mb];
+    BM_TRY(TY(c, embed_bwd<bf16>(m.S, m.d, n_mod, c.ids + (int64_t)mb * S, (const bf16*)c.bout[b], G_(c, "llm.embed"), c.embscr, c.st),
+              embed_bwd<float>(m.S, m.d, n_mod, c.ids + (int64_t)mb * S, (const float*)c.bout[b], G_(c, "llm.embed"), c.embscr, c.st)));
+    if (mb % c.P == 0) BM_TRY(d2d(c, c.emb_local, c.bout[b], (int64_t)n_mod * d * es));
+  } else if ((s - 1) % c.P == c.rank) {
+    BM_TRY(d2d(c, c.llm[c.llm_live.at({mb, ch - 1})].gin, c.bout[b], S * d * es));
+  }
+  c.llm_live.erase({mb, ch});
+  c.llm_free.push_back(slot);
+  return BM_OK;
+}
+
+static bm_status op_gen_fwd(bm_ctx& c, const bm_op& o, const RecvState& rs) {
+  const auto& m = c.mc;
+  const int mb = o.mb;
+  int lo, hi;
+  shard_rows(c, mb, c.rank, &lo, &hi);
+  const int n = hi - lo;
+  if (n <= 0) return BM_OK;
+  const char* X = (c.rank == c.P - 1) ? c.genin_src[c.rank] : recv_slot(c, c.P - 1, BM_PAY_GENIN, rs.ops.at(0)->seq);
+  MlpSlot& sl = c.gen;
+  BM_TRY(lin_fwd(c, n, m.d, m.d_g, X, m.d, P_(c, "gen.in"), LD_(c, "gen.in"), sl.E[0]));
+  BM_TRY(mlp_blocks_fwd(c, sl, "gen", m.L_g, n, m.d_g, m.f_g));
+  BM_TRY(lin_fwd(c, n, m.d_g, m.d_t, sl.E[m.L_g], m.d_g, P_(c, "gen.out"), LD_(c, "gen.out"), sl.out));
+  const char* t = c.mb_targets[mb] + (int64_t)lo * m.d_t * c.es;
+  const float denom = (float)c.n_gen[mb] * m.d_t;
+  BM_TRY(TY(c, mse_fwd_bwd<bf16>(n, m.d_t, (const bf16*)sl.out, (const bf16*)t, denom, 1.f / c.M, 1.f, c.loss + c.M + mb, (bf16*)sl.dout, c.st),
+            mse_fwd_bwd<float>(n, m.d_t, (const float*)sl.out, (const float*)t, denom, 1.f / c.M, 1.f, c.loss + c.M + mb, (float*)sl.dout, c.st)));
+  return BM_OK;
+}
+
+static bm_status op_gen_bwd(bm_ctx& c, const bm_op& o, const char* X) {
+  const auto& m = c.mc;
+  const int mb = o.mb;
+  int lo, hi;
+  shard_rows(c, mb, c.rank, &lo, &hi);
+  const int n = hi - lo;
+  MlpSlot& sl = c.gen;
+  const int b = c.gsel;
+  c.gsel ^= 1;
+  c.last_src = c.gout[b];
+  c.last_src_ring = 1;
+  c.last_src_idx = b;
+  if (n <= 0) return BM_OK;
+  if (c.gout_pending[b]) {
+    BM_CUDA_TRY(cudaStreamWaitEvent(c.st, c.gout_ev[b], 0));
+    c.gout_pending[b] = false;
+  }
+  BM_TRY(lin_wgrad(c, n, m.d_g, m.d_t, sl.dout, sl.E[m.L_g], m.d_g, G_(c, "gen.out"), LD_(c, "gen.out")));
+  BM_TRY(lin_dgrad(c, n, m.d_g, m.d_t, sl.dout, P_(c, "gen.out"), LD_(c, "gen.out"), c.g_dG, m.d_g));
+  BM_TRY(mlp_blocks_bwd(c, sl, "gen", m.L_g, n, m.d_g, m.f_g, c.g_dG, c.g_dz, c.g_da, c.g_dxn));
+  BM_TRY(lin_wgrad(c, n, m.d, m.d_g, c.g_dG, X, m.d, G_(c, "gen.in"), LD_(c, "gen.in")));
+  if (c.rank == c.P - 1) {
+    // own shard: add straight into the stashed dHn rows of (mb, V-1)
+    LlmSlot& ls = c.llm[c.llm_live.at({mb, c.V - 1})];
+    char* dst = ls.dHn + (int64_t)(m.S - c.n_gen[mb] + lo) * m.d * c.es;
+    BM_TRY(lin_dgrad(c, n, m.d, m.d_g, c.g_dG, P_(c, "gen.in"), LD_(c, "gen.in"), dst, m.d, BM_EPI_ADD, dst));
+  } else {
+    BM_TRY(lin_dgrad(c, n, m.d, m.d_g, c.g_dG, P_(c, "gen.in"), LD_(c, "gen.in"), c.gout[b], m.d));
+  }
+  return BM_OK;
+}
+
+// ------------------------------------------------------------------ comm ops
+static int64_t payload_bytes(const bm_ctx& c, const bm_op& o, int src_rank_for_shard) {
+  const int64_t row = (int64_t)c.mc.d * c.es;
+  switch (o.payload) {
+    case BM_PAY_ACT:
+    case BM_PAY_GRAD: return c.mc.S * row;
+    case BM_PAY_EMB:
+    case BM_PAY_EMBGRAD: return c.n_mod[o.mb] * row;
+    default: {
+      int lo, hi;
+      shard_rows(c, o.mb, src_rank_for_shard, &lo, &hi);
+      return (int64_t)(hi - lo) * row;
+    }
+  }
+}
+
+static bm_status do_send(bm_ctx& c, const bm_op& o) {
+  const Chan& ch = c.chans[c.chan_idx.at(std::make_tuple(c.rank, o.peer, o.payload))];
+  cudaStream_t cs = c.comm_st[o.peer];
+  if (!c.producer_ev) {
+    c.producer_ev = next_event(c);
+    BM_CUDA_TRY(cudaEventRecord(c.producer_ev, c.st));
+  }
+  BM_CUDA_TRY(cudaStreamWaitEvent(cs, c.producer_ev, 0));
+  const uint32_t base = (uint32_t)(c.step * ch.nmsg);
+  if (o.seq >= ch.K) {
+    CUresult r = drv().wait32((CUstream)cs, (CUdeviceptr)(c.comm + ch.credit_off), base + (uint32_t)(o.seq - ch.K) + 1,
+                              CU_STREAM_WAIT_VALUE_GEQ);
+    if (r != CUDA_SUCCESS) { set_error("cuStreamWaitValue32 (credit) failed " + std::to_string((int)r)); return BM_E_CUDA; }
+  }
+  const char* src;
+  int64_t bytes;
+  if (o.payload == BM_PAY_GENIN) {
+    src = c.genin_src[o.peer];
+    bytes = payload_bytes(c, o, o.peer);
+  } else if (o.payload == BM_PAY_GENGRAD) {
+    src = (const char*)c.last_src;
+    bytes = payload_bytes(c, o, c.rank);
+  } else {
+    src = (const char*)c.last_src;
+    bytes = payload_bytes(c, o, c.rank);
+  }
+  char* dst = c.peer[o.peer] + ch.data_off + (int64_t)(o.seq % ch.K) * ch.slot_bytes;
+  if (bytes > 0) BM_CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, cs));
+  CUresult r = drv().write32((CUstream)cs, (CUdeviceptr)(c.peer[o.peer] + ch.flag_off), base + (uint32_t)o.seq + 1, 0);
+  if (r != CUDA_SUCCESS) { set_error("cuStreamWriteValue32 (data flag) failed " + std::to_string((int)r)); return BM_E_CUDA; }
+  if (c.last_src_ring == 0 && o.payload != BM_PAY_GENIN) {
+    BM_CUDA_TRY(cudaEventRecord(c.bout_ev[c.last_src_idx], cs));
+    c.bout_pending[c.last_src_idx] = true;
+  } else if (c.last_src_ring == 1 && o.payload == BM_PAY_GENGRAD) {
+    BM_CUDA_TRY(cudaEventRecord(c.gout_ev[c.last_src_idx], cs));
+    c.gout_pending[c.last_src_idx] = true;
+  }
+  return BM_OK;
+}
+
+static bm_status do_recv_wait(bm_ctx& c, const bm_op& o) {
+  const Chan& ch = c.chans[c.chan_idx.at(std::make_tuple(o.peer, c.rank, o.payload))];
+  const uint32_t base = (uint32_t)(c.step * ch.nmsg);
+  CUresult r = drv().wait32((CUstream)c.st, (CUdeviceptr)(c.comm + ch.flag_off), base + (uint32_t)o.seq + 1,
+                            CU_STREAM_WAIT_VALUE_GEQ);
+  if (r != CUDA_SUCCESS) { set_error("cuStreamWaitValue32 (data) failed " + std::to_string((int)r)); return BM_E_CUDA; }
+  return BM_OK;
+}
+
+static bm_status do_release(bm_ctx& c, const bm_op& o) {
+  const Chan& ch = c.chans[c.chan_idx.at(std::make_tuple(o.peer, c.rank, o.payload))];
+  const uint32_t base = (uint32_t)(c.step * ch.nmsg);
+  CUresult r = drv().write32((CUstream)c.st, (CUdeviceptr)(c.peer[o.peer] + ch.credit_off), base + (uint32_t)o.seq + 1, 0);
+  if (r != CUDA_SUCCESS) { set_error("cuStreamWriteValue32 (credit) failed " + std::to_string((int)r)); return BM_E_CUDA; }
+  return BM_OK;
+}
+
+}  // namespace bm
+
+// ================================================================ C ABI
+extern "C" {
+
+bm_status bm_param_count(const bm_model_cfg* mc, const bm_sched_cfg* sc, int32_t rank, int32_t* n,
+                         int64_t* total_elems, int64_t* dp_elems) {
+  BM_CHECK_ARG(mc && sc && n && total_elems && dp_elems, "null argument");
+  BM_CHECK_ARG(rank >= 0 && rank < sc->stages, "rank out of range");
+  BM_TRY(check_model(*mc, *sc));
+  auto v = param_layout(*mc, *sc, rank, total_elems, dp_elems);
+  *n = (int32_t)v.size();
+  return BM_OK;
+}
+
+bm_status bm_param_info_get(const bm_model_cfg* mc, const bm_sched_cfg* sc, int32_t rank, int32_t idx,
+                            bm_param_info* out) {
+  BM_CHECK_ARG(mc && sc && out, "null argument");
+  BM_CHECK_ARG(rank >= 0 && rank < sc->stages, "rank out of range");
+  BM_TRY(check_model(*mc, *sc));
+  int64_t t, dp;
+  auto v = param_layout(*mc, *sc, rank, &t, &dp);
+  BM_CHECK_ARG(idx >= 0 && idx < (int)v.size(), "param index out of range");
+  std::memset(out, 0, sizeof(*out));
+  std::strncpy(out->name, v[idx].name.c_str(), sizeof(out->name) - 1);
+  out->rows = v[idx].rows;
+  out->cols = v[idx].cols;
+  out->offset = v[idx].off;
+  out->kind = v[idx].kind;
+  out->ld = v[idx].ld;
+  return BM_OK;
+}
+
+bm_status bm_ctx_create(const bm_model_cfg* mc, const bm_schedule* s, int32_t rank, bm_ctx** out) {
+  BM_CHECK_ARG(mc && s && out, "null argument");
+  BM_CHECK_ARG(rank >= 0 && rank < s->cfg.stages, "rank out of range");
+  BM_TRY(check_model(*mc, s->cfg));
+  auto* c = new bm_ctx();
+  c->mc = *mc;
+  c->sc = s->cfg;
+  c->s = s;
+  c->rank = rank;
+  c->P = s->cfg.stages;
+  c->M = s->cfg.microbatches;
+  c->V = s->cfg.vchunks;
+  c->lps = mc->L / (c->P * c->V);
+  c->dtype = mc->dtype;
+  c->es = mc->dtype == BM_BF16 ? 2 : 4;
+  c->params = param_layout(*mc, s->cfg, rank, &c->total_elems, &c->dp_elems);
+  for (size_t i = 0; i < c->params.size(); ++i) c->pidx[c->params[i].name] = (int)i;
+  c->has_enc = s->cfg.enc_place != BM_ENC_NONE;
+  c->has_gen = s->cfg.gen_place != BM_GEN_NONE;
+  c->gen_last = s->cfg.gen_place == BM_GEN_LAST_STAGE;
+  if (!c->has_enc) {
+    delete c;
+    set_error("the executor requires an encoder placement (embed_preprocess consumes encoder outputs)");
+    return BM_E_INVALID;
+  }
+  const bm_sched_stats& st = s->stats[rank];
+  c->n_llm_slots = std::max(st.peak_llm_inflight, 1);
+  c->n_enc_slots = std::max(st.peak_enc_units, 1);
+  c->gen_rows = c->gen_last ? (rank == c->P - 1 ? mc->max_n_gen : 0) : (mc->max_n_gen + c->P - 1) / c->P;
+  if (!c->has_gen) c->gen_rows = 0;
+  comm_layout(*c);
+  work_layout(*c, nullptr);
+  // release annotations: Recv at i is released after the compute op j (genin: the following GenBwd)
+  const auto& ops = s->ranks[rank];
+  c->release_of.assign(ops.size(), {});
+  for (size_t i = 0; i < ops.size(); ++i) {
+    if (ops[i].kind != BM_OP_RECV) continue;
+    size_t j = i + 1;
+    while (ops[j].kind > BM_OP_GEN_BWD) ++j;
+    if (ops[i].payload == BM_PAY_GENIN)
+      while (ops[j].kind != BM_OP_GEN_BWD) ++j;
+    c->release_of[j].push_back((int)i);
+  }
+  *out = c;
+  return BM_OK;
+}
+
+bm_status bm_ctx_sizes_get(const bm_ctx* c, bm_ctx_sizes* out) {
+  BM_CHECK_ARG(c && out, "null argument");
+  out->weight_bytes = c->total_elems * (int64_t)c->es;
+  out->grad_bytes = c->total_elems * 4;
+  out->work_bytes = c->work_bytes;
+  out->comm_bytes = c->comm_size[c->rank];
+  return BM_OK;
+}
+
+bm_status bm_ctx_bind(bm_ctx* c, const bm_buffers* b) {
+  BM_CHECK_ARG(c && b && b->weights && b->grads && b->work && b->comm, "null buffer");
+  for (const void* p : {b->weights, b->grads, b->work, b->comm})
+    BM_CHECK_ARG((reinterpret_cast<uintptr_t>(p) & 255) == 0, "buffers must be 256-byte aligned");
+  c->W = (char*)b->weights;
+  c->G = (float*)b->grads;
+  c->work = (char*)b->work;
+  c->comm = (char*)b->comm;
+  work_layout(*c, c->work);
+  c->peer.assign(c->P, nullptr);
+  c->peer[c->rank] = c->comm;
+  if (c->comm_st.empty()) {
+    c->comm_st.resize(c->P, nullptr);
+    for (int r = 0; r < c->P; ++r)
+      if (r != c->rank) BM_CUDA_TRY(cudaStreamCreateWithFlags(&c->comm_st[r], cudaStreamNonBlocking));
+    c->evpool.resize(64);
+    for (auto& e : c->evpool) BM_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    for (int i = 0; i < 2; ++i) {
+      BM_CUDA_TRY(cudaEventCreateWithFlags(&c->bout_ev[i], cudaEventDisableTiming));
+      BM_CUDA_TRY(cudaEventCreateWithFlags(&c->gout_ev[i], cudaEventDisableTiming));
+    }
+  }
+  if (!drv().wait32 || !drv().write32) {
+    set_error("cuStreamWaitValue32/cuStreamWriteValue32 unavailable");
+    return BM_E_CUDA;
+  }
+  c->bound = true;
+  return BM_OK;
+}
+
+bm_status bm_ipc_export(const void* dptr, uint8_t handle[64], int64_t* offset) {
+  BM_CHECK_ARG(dptr && handle && offset, "null argument");
+  CUdeviceptr base = 0;
+  size_t sz = 0;
+  if (!drv().addr_range || drv().addr_range(&base, &sz, (CUdeviceptr)dptr) != CUDA_SUCCESS) {
+    set_error("cuMemGetAddressRange failed");
+    return BM_E_CUDA;
+  }
+  cudaIpcMemHandle_t h;
+  BM_CUDA_TRY(cudaIpcGetMemHandle(&h, (void*)base));
+  static_assert(sizeof(h) == 64, "ipc handle size");
+  std::memcpy(handle, &h, 64);
+  *offset = (int64_t)((CUdeviceptr)dptr - base);
+  return BM_OK;
+}
+
+bm_status bm_ctx_open_peer(bm_ctx* c, int32_t peer, const uint8_t handle[64], int64_t offset) {
+  BM_CHECK_ARG(c && handle && c->bound, "bind the context before opening peers");
+  BM_CHECK_ARG(peer >= 0 && peer < c->P && peer != c->rank, "bad peer rank");
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, 64);
+  void* p = nullptr;
+  BM_CUDA_TRY(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+  c->peer[peer] = (char*)p + offset;
+  return BM_OK;
+}
+
+bm_status bm_nccl_unique_id(uint8_t id[128]) {
+  BM_CHECK_ARG(id, "null argument");
+  if (!nccl().ok) {
+    set_error("libnccl.so.2 not loadable");
+    return BM_E_NCCL;
+  }
+  ncclUniqueId u;
+  BM_NCCL_TRY(nccl().GetUniqueId(&u));
+  static_assert(sizeof(u) == 128, "nccl id size");
+  std::memcpy(id, &u, 128);
+  return BM_OK;
+}
+
+bm_status bm_ctx_init_nccl(bm_ctx* c, const uint8_t id[128], int32_t nranks, int32_t rank) {
+  BM_CHECK_ARG(c && id, "null argument");
+  BM_CHECK_ARG(nranks == c->P && rank == c->rank, "NCCL group must be the pipeline group");
+  if (!nccl().ok) {
+    set_error("libnccl.so.2 not loadable");
+    return BM_E_NCCL;
+  }
+  ncclUniqueId u;
+  std::memcpy(&u, id, 128);
+  BM_NCCL_TRY(nccl().CommInitRank(&c->nc, nranks, u, rank));
+  return BM_OK;
+}
+
+bm_status bm_step(bm_ctx* c, const bm_batch* b, void* stream) {
+  BM_CHECK_ARG(c && b, "null argument");
+  if (!c->bound) {
+    set_error("bm_step before bm_ctx_bind");
+    return BM_E_STATE;
+  }
+  BM_CHECK_ARG(b->M == c->M, "batch M does not match the schedule");
+  for (int r = 0; r < c->P; ++r)
+    if (!c->peer[r]) {
+      set_error("peer " + std::to_string(r) + " not opened");
+      return BM_E_STATE;
+    }
+  if (c->P > 1 && !c->nc) {
+    set_error("NCCL not initialised (bm_ctx_init_nccl) for P > 1");
+    return BM_E_STATE;
+  }
+  bm_ctx& x = *c;
+  const auto& m = x.mc;
+  x.st = reinterpret_cast<cudaStream_t>(stream);
+  const int64_t launches0 = launch_count();
+  if (x.timing) BM_TRY(harvest(x, (int)(x.step & 1)));   // pool of step-2, reused now
+  // per-mb views of the batch
+  x.n_mod.assign(b->n_mod, b->n_mod + x.M);
+  x.n_gen.assign(b->n_gen, b->n_gen + x.M);
+  int64_t tot_mod = 0, tot_gen = 0;
+  for (int i = 0; i < x.M; ++i) {
+    BM_CHECK_ARG(x.n_mod[i] >= 0 && x.n_mod[i] <= m.max_n_mod, "n_mod out of range");
+    BM_CHECK_ARG(x.n_gen[i] >= 0 && x.n_gen[i] <= m.max_n_gen, "n_gen out of range");
+    tot_mod += x.n_mod[i];
+    tot_gen += x.n_gen[i];
+  }
+  BM_CHECK_ARG(b->ld_patch >= m.d_in && b->ld_patch % 8 == 0, "ld_patch must be >= d_in and a multiple of 8");
+  const char *patches = (const char*)b->patches, *targets = (const char*)b->targets;
+  x.ids = b->ids;
+  x.labels = b->labels;
+  x.ld_patch = b->ld_patch;
+  if (b->on_host) {
+    // end-to-end path: stage the host batch on the device inside the step
+    BM_CHECK_ARG(tot_mod <= (int64_t)x.M * m.max_n_mod, "patch rows exceed staging");
+    BM_CUDA_TRY(cudaMemcpy2DAsync(x.st_patches, (size_t)x.ld_patch_stage * x.es, patches, (size_t)b->ld_patch * x.es,
+                                  (size_t)m.d_in * x.es, tot_mod, cudaMemcpyHostToDevice, x.st));
+    BM_CUDA_TRY(cudaMemcpyAsync(x.st_ids, b->ids, (size_t)x.M * m.S * 4, cudaMemcpyHostToDevice, x.st));
+    BM_CUDA_TRY(cudaMemcpyAsync(x.st_labels, b->labels, (size_t)x.M * m.S * 4, cudaMemcpyHostToDevice, x.st));
+    BM_CUDA_TRY(cudaMemcpyAsync(x.st_targets, targets, (size_t)tot_gen * m.d_t * x.es, cudaMemcpyHostToDevice, x.st));
+    patches = x.st_patches;
+    targets = x.st_targets;
+    x.ids = (const int32_t*)x.st_ids;
+    x.labels = (const int32_t*)x.st_labels;
+    x.ld_patch = x.ld_patch_stage;
+  }
+  x.mb_patches.resize(x.M);
+  x.mb_targets.resize(x.M);
+  int64_t pm = 0, pg = 0;
+  for (int i = 0; i < x.M; ++i) {
+    x.mb_patches[i] = patches + pm * x.ld_patch * x.es;
+    x.mb_targets[i] = targets + pg * m.d_t * x.es;
+    pm += x.n_mod[i];
+    pg += x.n_gen[i];
+  }
+  // reset step state
+  BM_CUDA_TRY(cudaMemsetAsync(x.G, 0, (size_t)x.total_elems * 4, x.st));
+  BM_CUDA_TRY(cudaMemsetAsync(x.loss, 0, (size_t)(2 * x.M + 1) * 4, x.st));
+  x.llm_free.clear();
+  for (int i = x.n_llm_slots - 1; i >= 0; --i) x.llm_free.push_back(i);
+  x.llm_live.clear();
+  for (int i = 0; i < 2; ++i) { x.bout_pending[i] = false; x.gout_pending[i] = false; }
+  // join: comm streams must see everything before this step (previous step's tail)
+  {
+    cudaEvent_t e = next_event(x);
+    BM_CUDA_TRY(cudaEventRecord(e, x.st));
+    for (int r = 0; r < x.P; ++r)
+      if (r != x.rank) BM_CUDA_TRY(cudaStreamWaitEvent(x.comm_st[r], e, 0));
+  }
+  // ---- the opcode stream
+  const auto& ops = x.s->ranks[x.rank];
+  RecvState rs;
+  const char* gen_x = nullptr;
+  int64_t live_enc = 0, live_llm = 0, live_gen = 0;
+  const int64_t enc_unit_bytes = (int64_t)m.max_n_mod * (m.d_e * (m.L_e + 1) + m.L_e * (m.d_e + 2 * m.f_e) + 3 * m.d) * x.es;
+  const int64_t llm_unit_bytes = (int64_t)m.S * (x.lps * (2 * m.d + 3 * m.f) + m.d) * x.es;
+  const int64_t gen_unit_bytes = (int64_t)x.gen_rows * (m.d_g * (m.L_g + 1) + m.L_g * (m.d_g + 2 * m.f_g) + 2 * m.d_t) * x.es;
+  for (int k = 0; k < 3; ++k) x.stash_peak[k] = 0;
+  for (size_t i = 0; i < ops.size(); ++i) {
+    const bm_op& o = ops[i];
+    switch (o.kind) {
+      case BM_OP_RECV:
+        BM_TRY(do_recv_wait(x, o));
+        rs.ops.push_back(&o);
+        continue;
+      case BM_OP_SEND:
+        BM_TRY(do_send(x, o));
+        continue;
+      default:
+        break;
+    }
+    x.producer_ev = nullptr;
+    switch (o.kind) {
+      case BM_OP_ENC_FWD: BM_TRY(op_enc_fwd(x, o)); live_enc += enc_unit_bytes; break;
+      case BM_OP_ENC_BWD: BM_TRY(op_enc_bwd(x, o, rs)); live_enc -= enc_unit_bytes; break;
+      case BM_OP_LLM_FWD: BM_TRY(op_llm_fwd(x, o, rs)); live_llm += llm_unit_bytes; break;
+      case BM_OP_LLM_BWD: BM_TRY(op_llm_bwd(x, o, rs)); live_llm -= llm_unit_bytes; break;
+      case BM_OP_GEN_FWD:
+        gen_x = (x.rank == x.P - 1) ? nullptr : (rs.ops.empty() ? nullptr : recv_slot(x, x.P - 1, BM_PAY_GENIN, rs.ops[0]->seq));
+        BM_TRY(op_gen_fwd(x, o, rs));
+        live_gen += gen_unit_bytes;
+        break;
+      case BM_OP_GEN_BWD: {
+        const char* X = (x.rank == x.P - 1) ? x.genin_src[x.rank] : gen_x;
+        BM_TRY(op_gen_bwd(x, o, X));
+        live_gen -= gen_unit_bytes;
+        break;
+      }
+      default:
+        set_error("unknown op kind");
+        return BM_E_INVALID;
+    }
+    x.stash_peak[0] = std::max(x.stash_peak[0], live_enc);
+    x.stash_peak[1] = std::max(x.stash_peak[1], live_llm);
+    x.stash_peak[2] = std::max(x.stash_peak[2], live_gen);
+    rs.ops.clear();
+    for (int ri : x.release_of[i]) BM_TRY(do_release(x, ops[ri]));
+  }
+  // join the comm streams back into the compute stream
+  for (int r = 0; r < x.P; ++r) {
+    if (r == x.rank) continue;
+    cudaEvent_t e = next_event(x);
+    BM_CUDA_TRY(cudaEventRecord(e, x.comm_st[r]));
+    BM_CUDA_TRY(cudaStreamWaitEvent(x.st, e, 0));
+  }
+  // finalize: DP gradient sum + loss terms
+  if (x.P > 1) {
+    BM_NCCL_TRY(nccl().GroupStart());
+    BM_NCCL_TRY(nccl().AllReduce(x.G, x.G, (size_t)x.dp_elems, ncclFloat32, ncclSum, x.nc, x.st));
+    BM_NCCL_TRY(nccl().AllReduce(x.loss, x.loss, (size_t)(2 * x.M), ncclFloat32, ncclSum, x.nc, x.st));
+    BM_NCCL_TRY(nccl().GroupEnd());
+  }
+  BM_TRY(loss_finalize(x.M, x.loss, x.st));
+  x.step += 1;
+  x.launches = launch_count() - launches0;
+  return BM_OK;
+}
+
+bm_status bm_ctx_loss_ptr(const bm_ctx* c, const float** dptr) {
+  BM_CHECK_ARG(c && dptr && c->bound, "bound context required");
+  *dptr = c->loss;
+  return BM_OK;
+}
+
+bm_status bm_ctx_launch_count(const bm_ctx* c, int64_t* n) {
+  BM_CHECK_ARG(c && n, "null argument");
+  *n = c->launches;
+  return BM_OK;
+}
+
+bm_status bm_ctx_stash_peak(const bm_ctx* c, int64_t out[3]) {
+  BM_CHECK_ARG(c && out, "null argument");
+  for (int k = 0; k < 3; ++k) out[k] = c->stash_peak[k];
+  return BM_OK;
+}
+
+bm_status bm_ctx_set_timing(bm_ctx* c, int32_t enable) {
+  BM_CHECK_ARG(c, "null argument");
+  if (c->timing && !enable) {
+    BM_TRY(harvest(*c, 0));
+    BM_TRY(harvest(*c, 1));
+  }
+  c->timing = enable != 0;
+  c->gemm_flops = 0;
+  c->gemm_ms = 0;
+  c->gemm_count = 0;
+  return BM_OK;
+}
+
+bm_status bm_ctx_gemm_stats(bm_ctx* c, int64_t* n_gemm, double* flops, double* ms) {
+  BM_CHECK_ARG(c && n_gemm && flops && ms, "null argument");
+  BM_TRY(harvest(*c, 0));
+  BM_TRY(harvest(*c, 1));
+  *n_gemm = c->gemm_count;
+  *flops = c->gemm_flops;
+  *ms = c->gemm_ms;
+  return BM_OK;
+}
+
+void bm_ctx_destroy(bm_ctx* c) { delete c; }
+
+}  // extern "C"

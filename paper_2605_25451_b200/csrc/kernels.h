@@ -40,5 +40,6 @@ bm_status mse_fwd_bwd(int n, int dt, const T* out, const T* t, float denom, floa
                       float* loss_out, T* dout, cudaStream_t st);
 template <typename T> bm_status add(int64_t n, const T* a, const T* b, T* o, cudaStream_t st);
 bm_status cast(int sd, int dd, int64_t n, const void* s, void* d, cudaStream_t st);
+bm_status loss_finalize(int M, float* loss, cudaStream_t st);
 
 }  // namespace bm

@@ -29,12 +29,7 @@ namespace bm {
 void set_error(const std::string& msg);
 }
 
-struct bm_schedule {
-  bm_sched_cfg cfg;
-  std::vector<std::vector<bm_op>> ranks;
-  std::vector<bm_sched_stats> stats;
-  std::map<std::tuple<int, int, int>, std::pair<int, int>> rings;  // (src,dst,payload) -> (K, nmsg)
-};
+#include "sched_internal.h"
 
 namespace bm {
 namespace sched {

@@ -1,0 +1,231 @@
+"""Per-rank runtime: the paper's create_executor / load_schedule / execute
+ over the C ABI.  PyTorch provides device memory, the stream and
+the process group used to exchange IPC handles and the NCCL id; every step of
+the hot path runs in libbigmac.so.  There is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib as L
+from . import schedule as BS
+
+
+def model_cfg(shape, dtype: str, max_n_mod: int | None = None, max_n_gen: int | None = None) -> L.ModelCfg:
+    mc = L.ModelCfg()
+    mc.S, mc.d_in, mc.d_e, mc.f_e, mc.L_e = shape.S, shape.d_in, shape.d_e, shape.f_e, shape.L_e
+    mc.d, mc.f, mc.L, mc.vocab = shape.d, shape.f, shape.L, shape.vocab
+    mc.d_g, mc.f_g, mc.L_g, mc.d_t = shape.d_g, shape.f_g, shape.L_g, shape.d_t
+    mc.dtype = L.BF16 if dtype == "bf16" else L.F32
+    mc.max_n_mod = max_n_mod if max_n_mod is not None else min(shape.n_mod_law[2], shape.S)
+    mc.max_n_gen = max_n_gen if max_n_gen is not None else min(shape.n_gen_law[2], shape.S)
+    return mc
+
+
+def _round8(x):
+    return (x + 7) // 8 * 8
+
+
+@dataclass
+class DeviceBatch:
+    struct: L.Batch
+    keep: list
+    h2d_bytes: int
+
+
+class Runtime:
+    def __init__(self, shape, dtype="bf16", rank=0, world=1, group=None, device=None, sched_kw=None):
+        self.shape = shape
+        self.dtype = dtype
+        self.rank, self.world = rank, world
+        self.P, self.M, self.V = shape.P, shape.M, shape.V
+        if world != self.P:
+            raise ValueError(f"one rank per pipeline stage: world={world} != P={self.P}")
+        self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else device
+        kw = dict(sched_kw or {})
+        self.sched = BS.build(self.P, self.M, self.V, **kw)
+        self.mc = model_cfg(shape, dtype)
+        h = C.c_void_p()
+        L.call("bm_ctx_create", C.byref(self.mc), self.sched.handle, rank, C.byref(h))
+        self.ctx = h.value
+        sz = L.CtxSizes()
+        L.call("bm_ctx_sizes_get", self.ctx, C.byref(sz))
+        self.sizes = sz
+        tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
+        self.tdtype = tdt
+        self.es = 2 if dtype == "bf16" else 4
+
+        def alloc(nbytes, zero=False):
+            n = max(int(nbytes), 256)
+            t = (torch.zeros if zero else torch.empty)(n + 256, dtype=torch.uint8, device=self.device)
+            off = (-t.data_ptr()) % 256
+            return t, t.data_ptr() + off
+
+        self._w, self.w_ptr = alloc(sz.weight_bytes)
+        self._g, self.g_ptr = alloc(sz.grad_bytes)
+        self._work, self.work_ptr = alloc(sz.work_bytes)
+        self._comm, self.comm_ptr = alloc(sz.comm_bytes, zero=True)
+        bufs = L.Buffers(self.w_ptr, self.g_ptr, self.work_ptr, self.comm_ptr)
+        L.call("bm_ctx_bind", self.ctx, C.byref(bufs))
+        # parameter table
+        n, tot, dp = C.c_int32(), C.c_int64(), C.c_int64()
+        L.call("bm_param_count", C.byref(self.mc), C.byref(BS.make_cfg(self.P, self.M, self.V, **kw)), rank,
+               C.byref(n), C.byref(tot), C.byref(dp))
+        self.total_elems, self.dp_elems = tot.value, dp.value
+        self.params = {}
+        scfg = BS.make_cfg(self.P, self.M, self.V, **kw)
+        for i in range(n.value):
+            pi = L.ParamInfo()
+            L.call("bm_param_info_get", C.byref(self.mc), C.byref(scfg), rank, i, C.byref(pi))
+            self.params[pi.name.decode()] = (pi.rows, pi.cols, pi.ld, pi.offset, pi.kind)
+        self.weights_t = self._w[(self.w_ptr - self._w.data_ptr()):][: self.total_elems * self.es].view(tdt)
+        self.grads_t = self._g[(self.g_ptr - self._g.data_ptr()):][: self.total_elems * 4].view(torch.float32)
+        if world > 1:
+            self._connect(group)
+
+    # ------------------------------------------------------------------ peers
+    def _connect(self, group):
+        import torch.distributed as dist
+        hb = (C.c_uint8 * 64)()
+        off = C.c_int64()
+        L.call("bm_ipc_export", self.comm_ptr, hb, C.byref(off))
+        mine = (bytes(hb), off.value)
+        allh = [None] * self.world
+        dist.all_gather_object(allh, mine, group=group)
+        for r, (hbytes, o) in enumerate(allh):
+            if r == self.rank:
+                continue
+            L.call("bm_ctx_open_peer", self.ctx, r, (C.c_uint8 * 64).from_buffer_copy(hbytes), o)
+        nid = (C.c_uint8 * 128)()
+        if self.rank == 0:
+            L.call("bm_nccl_unique_id", nid)
+        obj = [bytes(nid)]
+        dist.broadcast_object_list(obj, src=0, group=group)
+        L.call("bm_ctx_init_nccl", self.ctx, (C.c_uint8 * 128).from_buffer_copy(obj[0]), self.world, self.rank)
+        dist.barrier(group=group)
+
+    # ------------------------------------------------------------------ weights / grads
+    def load_weights(self, weights: dict):
+        """weights: {name: float32 array} (synth.make_weights); only this rank's params are used."""
+        flat = torch.zeros(self.total_elems, dtype=torch.float32)
+        for name, (rows, cols, ld, off, _) in self.params.items():
+            w = np.asarray(weights[name], np.float32).reshape(rows, cols)
+            view = flat[off:off + rows * ld].view(rows, ld)
+            view[:, :cols] = torch.from_numpy(w)
+        self.weights_t.copy_(flat.to(self.device).to(self.tdtype))
+        torch.cuda.synchronize(self.device)
+
+    def names(self):
+        return list(self.params)
+
+    def grad(self, name) -> np.ndarray:
+        rows, cols, ld, off, _ = self.params[name]
+        g = self.grads_t[off:off + rows * ld].view(rows, ld)[:, :cols]
+        out = g.double().cpu().numpy()
+        return out.reshape(rows) if cols == 1 else out
+
+    def grads(self) -> dict:
+        return {n: self.grad(n) for n in self.params}
+
+    # ------------------------------------------------------------------ batch
+    def device_batch(self, batch) -> DeviceBatch:
+        """Pack a synth.Batch on the device (inputs resident in HBM)."""
+        sh = self.shape
+        ldp = _round8(sh.d_in)
+        rows = int(np.sum(batch.n_mod))
+        pat = np.zeros((max(rows, 1), ldp), np.float32)
+        r = 0
+        for p in batch.patches:
+            pat[r:r + p.shape[0], :sh.d_in] = p
+            r += p.shape[0]
+        tgt = np.concatenate([np.asarray(t, np.float32) for t in batch.targets], 0)
+        keep = [torch.from_numpy(pat).to(self.device).to(self.tdtype).contiguous(),
+                torch.from_numpy(np.ascontiguousarray(batch.ids, np.int32)).to(self.device),
+                torch.from_numpy(np.ascontiguousarray(batch.labels, np.int32)).to(self.device),
+                torch.from_numpy(tgt).to(self.device).to(self.tdtype).contiguous()]
+        nm = np.ascontiguousarray(batch.n_mod, np.int32)
+        ng = np.ascontiguousarray(batch.n_gen, np.int32)
+        keep += [nm, ng]
+        b = L.Batch()
+        b.M = len(nm)
+        b.n_mod = nm.ctypes.data
+        b.n_gen = ng.ctypes.data
+        b.patches = keep[0].data_ptr()
+        b.ld_patch = ldp
+        b.ids = keep[1].data_ptr()
+        b.labels = keep[2].data_ptr()
+        b.targets = keep[3].data_ptr()
+        b.on_host = 0
+        return DeviceBatch(b, keep, 0)
+
+    def host_batch(self, batch) -> DeviceBatch:
+        """Pinned host copy of a synth.Batch for the end-to-end path (bm_step copies it in)."""
+        sh = self.shape
+        ldp = _round8(sh.d_in)
+        rows = int(np.sum(batch.n_mod))
+        tdt = self.tdtype
+        pat = torch.zeros((max(rows, 1), ldp), dtype=torch.float32)
+        r = 0
+        for p in batch.patches:
+            pat[r:r + p.shape[0], :sh.d_in] = torch.from_numpy(p)
+            r += p.shape[0]
+        pat = pat.to(tdt).pin_memory()
+        tgt = torch.from_numpy(np.concatenate([np.asarray(t, np.float32) for t in batch.targets], 0)).to(tdt).pin_memory()
+        ids = torch.from_numpy(np.ascontiguousarray(batch.ids, np.int32)).pin_memory()
+        lab = torch.from_numpy(np.ascontiguousarray(batch.labels, np.int32)).pin_memory()
+        nm = np.ascontiguousarray(batch.n_mod, np.int32)
+        ng = np.ascontiguousarray(batch.n_gen, np.int32)
+        b = L.Batch()
+        b.M = len(nm)
+        b.n_mod = nm.ctypes.data
+        b.n_gen = ng.ctypes.data
+        b.patches = pat.data_ptr()
+        b.ld_patch = ldp
+        b.ids = ids.data_ptr()
+        b.labels = lab.data_ptr()
+        b.targets = tgt.data_ptr()
+        b.on_host = 1
+        h2d = rows * sh.d_in * self.es + ids.numel() * 4 + lab.numel() * 4 + tgt.numel() * self.es
+        return DeviceBatch(b, [pat, tgt, ids, lab, nm, ng], h2d)
+
+    # ------------------------------------------------------------------ execute
+    def step(self, db: DeviceBatch, stream=None):
+        s = torch.cuda.current_stream(self.device) if stream is None else stream
+        L.call("bm_step", self.ctx, C.byref(db.struct), C.c_void_p(s.cuda_stream))
+
+    def loss_tensor(self) -> torch.Tensor:
+        p = C.c_void_p()
+        L.call("bm_ctx_loss_ptr", self.ctx, C.byref(p))
+        base = self._work.data_ptr()
+        off = p.value - base
+        return self._work[off:off + (2 * self.M + 1) * 4].view(torch.float32)
+
+    def losses(self):
+        t = self.loss_tensor().double().cpu().numpy()
+        M = self.M
+        return float(t[2 * M]), t[:M].copy(), t[M:2 * M].copy()
+
+    def launch_count(self) -> int:
+        n = C.c_int64()
+        L.call("bm_ctx_launch_count", self.ctx, C.byref(n))
+        return n.value
+
+    def stash_peak(self):
+        a = (C.c_int64 * 3)()
+        L.call("bm_ctx_stash_peak", self.ctx, a)
+        return list(a)
+
+    def close(self):
+        if getattr(self, "ctx", None):
+            L.lib().bm_ctx_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -1,0 +1,69 @@
+"""One rank of a multi-GPU parity run (launched by tests/test_gpu_step.py via torchrun).
+
+usage: mp_step.py CONFIG P M V DTYPE GEN_PLACE
+Every rank runs bm_step on its own GPU; rank 0 gathers all gradients and
+compares them with the fp64 oracle (normwise rel tol 1e-4 fp32 / 2e-2 bf16).
+"""
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+from synth import get_config, make_batch, make_weights  # noqa: E402
+
+
+def main():
+    name, P, M, V, dtype, gen = sys.argv[1], int(sys.argv[2]), int(sys.argv[3]), int(sys.argv[4]), sys.argv[5], sys.argv[6]
+    rank = int(os.environ["RANK"])
+    world = int(os.environ["WORLD_SIZE"])
+    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", rank)))
+    dist.init_process_group("gloo")
+    from paper_2605_25451_b200.runtime import Runtime
+    cfg = get_config(name, P=P, M=M, V=V)
+    W, B = make_weights(cfg), make_batch(cfg)
+    rt = Runtime(cfg, dtype, rank=rank, world=world, sched_kw={"gen_place": gen})
+    rt.load_weights(W)
+    db = rt.device_batch(B)
+    for _ in range(2):
+        rt.step(db)
+    torch.cuda.synchronize()
+    loss, ce, mse = rt.losses()
+    grads = {n: rt.grad(n) for n in rt.names()}
+    kinds = {n: rt.params[n][4] for n in rt.names()}
+    allg = [None] * world
+    dist.gather_object((grads, kinds, loss, ce, mse), allg if rank == 0 else None, dst=0)
+    if rank == 0:
+        from oracle import model as om
+        loss_ref, per_ref, G_ref = om.step_fp64(cfg, W, B)
+        tol = 1e-4 if dtype == "f32" else 2e-2
+        ok = True
+        for r, (g, k, l_, c_, m_) in enumerate(allg):
+            if abs(l_ - loss_ref) > tol * abs(loss_ref):
+                print(f"rank {r} loss {l_} vs {loss_ref}")
+                ok = False
+            for n, v in g.items():
+                ref = G_ref[n]
+                e = np.linalg.norm(v - ref) / max(np.linalg.norm(ref), 1e-30)
+                if e > tol:
+                    print(f"rank {r} grad {n} rel err {e:.3e}")
+                    ok = False
+        seen = set()
+        for g, _, _, _, _ in allg:
+            seen |= set(g)
+        missing = set(G_ref) - seen
+        if missing:
+            print("missing grads", missing)
+            ok = False
+        print("PARITY OK" if ok else "PARITY FAIL", loss, loss_ref)
+    dist.barrier()
+    rt.close()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

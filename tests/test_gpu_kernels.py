@@ -63,7 +63,7 @@ def test_gemm_store_f32(L, M, N, K, a_mn, b_mn, dtype):
     assert err <= tol, (err, tol)
 
 
-@pytest.mark.parametrize("M,N,K", [(300, 200, 100), (257, 513, 130), (1024, 768, 512)])
+@pytest.mark.parametrize("M,N,K", [(300, 200, 104), (257, 513, 136), (1024, 768, 512)])
 @pytest.mark.parametrize("epi", ["bf16_store", "bf16_add", "f32_accum"])
 def test_gemm_epilogues(L, M, N, K, epi):
     rng = np.random.default_rng(1)

@@ -1,0 +1,81 @@
+"""The C-ABI library loads on a CPU-only host and exports every function that
+include/*.h declares (no compute calls).  Also checks the parameter layout
+the library computes against synth.param_specs (host logic only)."""
+import ctypes as C
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_functions():
+    names = []
+    for h in ("bigmac.h", "bigmac_kernels.h"):
+        src = open(os.path.join(ROOT, "include", h)).read()
+        src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+        for m in re.finditer(r"^\s*(?:bm_status|void|int64_t|const char\*)\s+(bm_\w+)\s*\(", src, flags=re.M):
+            names.append(m.group(1))
+    return sorted(set(names))
+
+
+def test_library_exports_every_declared_symbol():
+    from paper_2605_25451_b200 import _lib as L
+    lib = L.lib()
+    names = declared_functions()
+    assert len(names) >= 35
+    missing = [n for n in names if not hasattr(lib, n)]
+    assert not missing, missing
+    assert set(names) == set(L.SIGNATURES), set(names) ^ set(L.SIGNATURES)
+    assert L.MISSING == []
+
+
+def test_library_is_sm100a():
+    import subprocess
+    so = os.path.join(ROOT, "paper_2605_25451_b200", "libbigmac.so")
+    r = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-lelf", so], capture_output=True, text=True)
+    assert "sm_100a" in r.stdout
+    sass = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", so], capture_output=True, text=True).stdout
+    assert "UTCHMMA" in sass          # tcgen05.mma
+    assert "UTMALDG" in sass          # TMA loads
+    assert "LDTM" in sass             # tcgen05.ld (TMEM -> registers)
+
+
+@pytest.mark.parametrize("P,V,rank", [(1, 1, 0), (2, 1, 0), (2, 1, 1), (4, 1, 3), (2, 2, 0), (2, 2, 1), (1, 4, 0)])
+def test_param_layout_matches_model(P, V, rank):
+    from synth import get_config, param_specs
+    from paper_2605_25451_b200 import _lib as L
+    from paper_2605_25451_b200 import schedule as BS
+    from paper_2605_25451_b200.runtime import model_cfg
+    cfg = get_config("C1", P=P, M=2 * P, V=V)
+    mc = model_cfg(cfg, "bf16")
+    sc = BS.make_cfg(P, 2 * P, V)
+    n, tot, dp = C.c_int32(), C.c_int64(), C.c_int64()
+    L.call("bm_param_count", C.byref(mc), C.byref(sc), rank, C.byref(n), C.byref(tot), C.byref(dp))
+    specs = {nm: shp for nm, shp, _ in param_specs(cfg)}
+    got = {}
+    prev_end = 0
+    for i in range(n.value):
+        pi = L.ParamInfo()
+        L.call("bm_param_info_get", C.byref(mc), C.byref(sc), rank, i, C.byref(pi))
+        nm = pi.name.decode()
+        shp = specs[nm]
+        rows, cols = shp[0], (shp[1] if len(shp) > 1 else 1)
+        assert (pi.rows, pi.cols) == (rows, cols)
+        assert pi.offset >= prev_end and pi.offset % 64 == 0 and pi.ld >= cols and pi.ld % (1 if cols == 1 else 8) == 0
+        prev_end = pi.offset + rows * pi.ld
+        got[nm] = pi.kind
+    lps = cfg.L // (P * V)
+    my_layers = {l for c in range(V) for l in range((c * P + rank) * lps, (c * P + rank + 1) * lps)}
+    for nm in specs:
+        if nm.startswith(("enc.", "gen.")):
+            assert got.get(nm) == 0, nm            # DP params on every rank
+        elif nm == "llm.embed":
+            assert (nm in got) == (rank == 0)
+        elif nm in ("llm.final_norm", "llm.head"):
+            assert (nm in got) == (rank == P - 1)
+        else:
+            l = int(nm.split(".")[1][5:])
+            assert (nm in got) == (l in my_layers), nm
+    assert prev_end <= tot.value and dp.value <= tot.value
