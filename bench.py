@@ -1,0 +1,362 @@
+#!/usr/bin/env python
+"""Benchmark of one BigMac nested-pipeline training step on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    (N > 1: python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N ...)
+
+Workload (BASELINE.json configs[1], "C2"): ViT-S-shaped encoder + 1B-shaped
+LLM + small generator, S = 4096, M = 16 microbatches (global batch 16, one
+sample per microbatch), 1F1B LLM schedule with the encoder/generator nested
+in it, P = N pipeline stages (one per GPU), synthetic data with
+log-uniform[256, 1024] modality / generation rows per sample, bf16.
+Global batch is fixed as N grows ("strong" scaling).
+
+Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "MLLM train samples/s + % step roofline at 1/2/4/8 B200; peak HBM vs batch size"
+UNIT = "samples/s"
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return p, "measured"
+    except Exception:
+        return {"bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "hbm_gbs": 6650.0}, "fallback"
+
+
+def step_flops(cfg, n_mod, n_gen):
+    """Algorithmic FLOPs of one step: 2 per MAC forward, 4 per
+    MAC backward (dgrad + wgrad); the patch embedding has no dgrad."""
+    S, d, f, L, V = cfg.S, cfg.d, cfg.f, cfg.L, cfg.vocab
+    tot = 0.0
+    for nm, ng in zip(n_mod, n_gen):
+        llm = 6.0 * S * 3 * d * f * L
+        head = 6.0 * (S - nm) * d * V
+        enc = nm * (4.0 * cfg.d_in * cfg.d_e + 6.0 * (cfg.L_e * 2 * cfg.d_e * cfg.f_e + cfg.d_e * d + d * d))
+        gen = 6.0 * ng * (d * cfg.d_g + cfg.L_g * 2 * cfg.d_g * cfg.f_g + cfg.d_g * cfg.d_t)
+        tot += llm + head + enc + gen
+    return tot
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms (B200_PROFILING.md)."""
+    Q = ("uuid,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, uuid):
+        self.uuid = uuid
+        self.lines = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                          "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            if self.uuid and self.uuid not in parts[0]:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = max(mx, float(parts[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_oracle_sample(cfg, rows=512, repeats=1):
+    """Time the fp64 oracle on a bounded sample: one LLM layer fwd+bwd on `rows`
+    rows of one microbatch at the workload's (d, f).  Returns (sec, flops, cores)."""
+    import numpy as np
+    from oracle import model as om
+    try:
+        from threadpoolctl import threadpool_info
+        cores = max([i.get("num_threads", 1) for i in threadpool_info()] or [1])
+    except Exception:
+        cores = os.cpu_count() or 1
+    rng = np.random.default_rng(0)
+    W = {"llm.layer0.norm": np.ones(cfg.d),
+         "llm.layer0.gate_up": rng.standard_normal((2 * cfg.f, cfg.d)) * 0.02,
+         "llm.layer0.down": rng.standard_normal((cfg.d, cfg.f)) * 0.02}
+    x = rng.standard_normal((rows, cfg.d))
+    dy = rng.standard_normal((rows, cfg.d))
+    t0 = time.perf_counter()
+    for _ in range(repeats):
+        y, caches = om.llm_layers_fwd(W, cfg, [0], x)
+        G = {}
+        om.llm_layers_bwd(W, cfg, [0], caches, dy, G)
+    dt = (time.perf_counter() - t0) / repeats
+    return dt, 18.0 * rows * cfg.d * cfg.f, cores
+
+
+def workload(args, N):
+    from synth import get_config
+    cfg = get_config(args.config, P=N, M=args.microbatches or get_config(args.config).M, V=1)
+    return cfg
+
+
+def config_dict(cfg, N):
+    return {"workload": f"{cfg.name}: ViT-S-shaped encoder (d_e={cfg.d_e}, L_e={cfg.L_e}) + 1B-shaped LLM "
+                        f"(d={cfg.d}, f={cfg.f}, L={cfg.L}, vocab={cfg.vocab}) + generator (d_g={cfg.d_g}, L_g={cfg.L_g}); "
+                        f"nested pipeline P={N} stages, M={cfg.M} microbatches, 1F1B",
+            "global_batch": cfg.M, "seq_len": cfg.S, "parallelism": f"pp{N}",
+            "stages": N, "microbatches": cfg.M, "vchunks": cfg.V,
+            "n_mod_law": list(cfg.n_mod_law), "n_gen_law": list(cfg.n_gen_law),
+            "l2_policy": "working set (weights + activations, GBs) >> 126 MB L2; no flush"}
+
+
+def run_reference(args):
+    """The oracle as it stands, on the host cores (the reference arm for this tier)."""
+    rank = int(os.environ.get("RANK", "0"))
+    N = args.gpus
+    if rank != 0:
+        return
+    from synth import make_batch
+    cfg = workload(args, N)
+    batch = make_batch(cfg)
+    F = step_flops(cfg, batch.n_mod, batch.n_gen)
+    rows = args.ref_rows
+    for _ in range(args.warmup):
+        cpu_oracle_sample(cfg, rows)
+    ts = []
+    for _ in range(args.steps):
+        dt, fl, cores = cpu_oracle_sample(cfg, rows)
+        ts.append((dt, fl))
+    sec = sum(t for t, _ in ts)
+    flops = sum(f for _, f in ts)
+    rate = flops / sec
+    value = rate / (F / cfg.M)
+    sample = (f"per step: oracle (numpy fp64) fwd+bwd of one LLM layer on {rows} rows of a {cfg.name} microbatch "
+              f"(d={cfg.d}, f={cfg.f}); samples/s extrapolated by the step's algorithmic FLOPs per sample")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": N,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * sec / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": config_dict(cfg, N),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--microbatches", type=int, default=0)
+    ap.add_argument("--dtype", default="bf16")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--ref-rows", type=int, default=512)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+
+    import torch
+    import torch.distributed as dist
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    N = world
+    if args.gpus != world:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    group = None
+    if world > 1:
+        dist.init_process_group("cpu:gloo,cuda:nccl", device_id=torch.device("cuda", local))
+        group = dist.new_group(backend="gloo")
+
+    from synth import make_batch
+    from paper_2605_25451_b200.runtime import Runtime
+    cfg = workload(args, N)
+    if args.warmup < 3:
+        raise SystemExit("--warmup must be >= 3")
+    rt = Runtime(cfg, args.dtype, rank=rank, world=world, group=group)
+    rt.init_random_weights(seed=1)
+    batch = make_batch(cfg)
+    db = rt.device_batch(batch)
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if world > 1:
+            dist.barrier(group=group)
+
+    def max_over_ranks(v):
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+        return float(t.item())
+
+    def sum_over_ranks(v):
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+        return float(t.item())
+
+    # ---------------- warmup
+    for _ in range(args.warmup):
+        rt.step(db)
+    torch.cuda.synchronize()
+    torch.cuda.reset_peak_memory_stats()
+
+    # ---------------- timed region (device events, max over ranks)
+    try:
+        uuid = str(torch.cuda.get_device_properties(local).uuid)
+    except Exception:
+        uuid = None
+    clk = ClockSampler(uuid)
+    clk.start()
+    time.sleep(0.3)
+    rt.set_timing(True)
+    barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        rt.step(db)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    clocks = clk.stop()
+    ms = e0.elapsed_time(e1)
+    n_gemm, gemm_flops, gemm_ms = rt.gemm_stats()
+    rt.set_timing(False)
+    launches = rt.launch_count() * args.steps
+    ms_max = max_over_ranks(ms)
+    ms_per_step = ms_max / args.steps
+    samples = cfg.M * args.steps
+    value = samples / (ms_max / 1000.0)
+    loss, _, _ = rt.losses()
+    peak_alloc = max_over_ranks(float(torch.cuda.max_memory_allocated()))
+    stash = rt.stash_peak()
+
+    # ---------------- end-to-end: host inputs copied in, loss read back, every step
+    e2e = None
+    if not args.no_e2e:
+        hb = rt.host_batch(batch)
+        lt = rt.loss_tensor()
+        for _ in range(2):
+            rt.step(hb)
+            float(lt[2 * cfg.M].item())
+        barrier()
+        torch.cuda.synchronize()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        for _ in range(args.steps):
+            rt.step(hb)
+            float(lt[2 * cfg.M].item())   # device -> host read of the step's loss
+        f1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        ems = max_over_ranks(f0.elapsed_time(f1))
+        h2d = sum_over_ranks(hb.h2d_bytes)
+        e2e = {"value": cfg.M * args.steps / (ems / 1000.0), "unit": UNIT,
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(4 * world),
+               "ms_per_step": ems / args.steps}
+
+    launches_all = int(sum_over_ranks(launches))
+    gemm_flops_all = sum_over_ranks(gemm_flops)
+    gemm_ms_all = sum_over_ranks(gemm_ms)
+    n_gemm_all = int(sum_over_ranks(n_gemm))
+
+    if rank != 0:
+        if world > 1:
+            dist.barrier(group=group)
+        rt.close()
+        return
+
+    peaks, peak_src = load_peaks()
+    F = step_flops(cfg, batch.n_mod, batch.n_gen)
+    sustained = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
+    achieved = gemm_flops_all / (gemm_ms_all / 1000.0) / 1e12 if gemm_ms_all > 0 else 0.0
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "gemm_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    roofline = {"bound": "tensor", "kernel": "bm::tc::gemm_kernel (tcgen05.mma kind::f16, TMA, TMEM)",
+                "achieved": achieved, "peak": sustained, "unit": "TFLOP/s", "frac": achieved / sustained,
+                "peak_source": f"{peak_src} bf16_tflops_sustained (GEMMs timed inside a long step)",
+                "traffic": traffic, "launches": n_gemm_all,
+                "gemm_share_of_step": (gemm_ms_all / world) / ms_max if ms_max > 0 else None,
+                "flops_per_launch": gemm_flops_all / max(n_gemm_all, 1),
+                "avg_launch_ms": gemm_ms_all / max(n_gemm_all, 1)}
+    t_roof_ms = F / (N * peaks["bf16_tflops"] * 1e12) * 1e3
+    step_roof = {"flops_per_step": F, "t_roof_ms": t_roof_ms, "frac": t_roof_ms / ms_per_step,
+                 "peak_tflops": peaks["bf16_tflops"], "bubble_bound": (N - 1) / (cfg.M + N - 1)}
+
+    cpu = None
+    if not args.no_cpu and N == 1:
+        dt, fl, cores = cpu_oracle_sample(cfg, rows=2048)
+        rate = fl / dt
+        cpu = {"value": rate / (F / cfg.M), "unit": UNIT, "cores": cores, "kind": "oracle",
+               "sample": f"oracle (numpy fp64) fwd+bwd of one LLM layer on 2048 rows of a {cfg.name} microbatch "
+                         f"({dt:.1f} s); samples/s extrapolated by the step's algorithmic FLOPs per sample"}
+
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": N, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
+            "config": config_dict(cfg, N),
+            "roofline": roofline, "step_roofline": step_roof,
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches_all, "clocks": clocks,
+            "tokens_per_s": cfg.M * cfg.S * args.steps / (ms_max / 1000.0),
+            "peak_hbm_gb_per_gpu": peak_alloc / 1e9, "stash_peak_bytes_rank0": stash,
+            "loss": loss}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier(group=group)
+    rt.close()
+
+
+if __name__ == "__main__":
+    main()

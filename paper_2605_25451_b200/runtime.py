@@ -119,6 +119,35 @@ class Runtime:
         self.weights_t.copy_(flat.to(self.device).to(self.tdtype))
         torch.cuda.synchronize(self.device)
 
+    def init_random_weights(self, seed: int = 1, std: float = 0.02):
+        """Synthetic random init on the device (bench path): N(0, std) for linear
+        weights, residual-branch outputs scaled by 1/sqrt(2 L), RMSNorm gains 1."""
+        sh = self.shape
+        import zlib
+        gen = torch.Generator(device=self.device)
+        depth = {"enc": sh.L_e, "llm": sh.L, "gen": sh.L_g}
+        self.weights_t.zero_()
+        for name, (rows, cols, ld, off, _) in self.params.items():
+            view = self.weights_t[off:off + rows * ld].view(rows, ld)
+            if cols == 1:
+                view.fill_(1.0)
+                continue
+            gen.manual_seed(seed * 1000003 + zlib.crc32(name.encode()))  # DP replicas identical on every rank
+            scale = std
+            if name.endswith((".fc2", ".down")):
+                scale = std / (2.0 * depth[name.split(".")[0]]) ** 0.5
+            w = torch.randn((rows, cols), generator=gen, device=self.device, dtype=torch.float32) * scale
+            view[:, :cols] = w.to(self.tdtype)
+        torch.cuda.synchronize(self.device)
+
+    def set_timing(self, on: bool):
+        L.call("bm_ctx_set_timing", self.ctx, 1 if on else 0)
+
+    def gemm_stats(self):
+        n, fl, ms = C.c_int64(), C.c_double(), C.c_double()
+        L.call("bm_ctx_gemm_stats", self.ctx, C.byref(n), C.byref(fl), C.byref(ms))
+        return n.value, fl.value, ms.value
+
     def names(self):
         return list(self.params)
 
