@@ -22,7 +22,9 @@ extern "C" {
 typedef enum {
   BM_EPI_STORE = 0,   /* C = alpha*acc            (C dtype = c_dtype)           */
   BM_EPI_ACCUM = 1,   /* C += alpha*acc           (C must be fp32; wgrad, β = 1) */
-  BM_EPI_ADD = 2      /* C = alpha*acc + R        (R has c_dtype; residual add)  */
+  BM_EPI_ADD = 2,     /* C = alpha*acc + R        (R has c_dtype; residual add)  */
+  BM_EPI_SWIGLU = 3,  /* internal: gate/up GEMM + SwiGLU (bm_k_gemm_swiglu)      */
+  BM_EPI_DSWIGLU = 4  /* internal: down dgrad + SwiGLU backward (bm_k_gemm_dswiglu) */
 } bm_epilogue;
 
 /* C[m, n] = sum_k A(m, k) * B(n, k), fp32 accumulation.
@@ -40,6 +42,24 @@ bm_status bm_k_gemm(int32_t dtype, int32_t M, int32_t N, int32_t K,
                     const void* B, int64_t ldb, int32_t b_major,
                     void* C, int64_t ldc, int32_t c_dtype, int32_t epilogue,
                     const void* R, int64_t ldr, float alpha, void* stream);
+
+/* LLM gate/up projection with the SwiGLU activation fused into the epilogue
+ * (bf16, tensor cores, CTA pairs):  [g | u] = X W^T with W = [W_gate; W_up]
+ * ([2f, K] row-major, ldw), X [M, K] (ldx);  writes gu [M, 2f] (both halves,
+ * kept for the backward) and h = silu(g) * u [M, f].  f % 128 == 0. */
+bm_status bm_k_gemm_swiglu(int32_t M, int32_t f, int32_t K, const void* X, int64_t ldx,
+                           const void* W, int64_t ldw, void* gu, void* h, void* stream);
+/* LLM down-projection data gradient with the SwiGLU backward fused into the
+ * epilogue:  dh = dY W_down ([M, K] x [K, f], W_down [K, f] row-major, ldw),
+ * then dgu = [dh*u*s*(1 + g(1-s)), dh*g*s] with s = sigmoid(g), g|u from gu
+ * [M, 2f];  writes dgu [M, 2f] (dh is never stored). */
+bm_status bm_k_gemm_dswiglu(int32_t M, int32_t f, int32_t K, const void* dY, int64_t lddy,
+                            const void* W, int64_t ldw, const void* gu, void* dgu, void* stream);
+
+/* Tuning / testing knob for the bf16 GEMM tile scheme: 0 = auto (CTA-pair
+ * cta_group::2 256xBN tiles when M >= 512, N >= 256, K >= 256; 128xBN 1-CTA
+ * tiles otherwise), 1 = always 1-CTA, 2 = always CTA pairs.  Process-wide. */
+bm_status bm_k_gemm_mode(int32_t mode);
 
 /* RMSNorm y = x * rstd * g, rstd = 1/sqrt(mean(x^2) + 1e-5); rstd saved (fp32 [rows]). */
 bm_status bm_k_rmsnorm_fwd(int32_t dtype, int32_t rows, int32_t cols, const void* x,

@@ -103,6 +103,9 @@ SIGNATURES = {
     "bm_ctx_destroy": [_P],
     # bigmac_kernels.h
     "bm_k_gemm": [_I32, _I32, _I32, _I32, _P, _I64, _I32, _P, _I64, _I32, _P, _I64, _I32, _I32, _P, _I64, _F, _P],
+    "bm_k_gemm_mode": [_I32],
+    "bm_k_gemm_swiglu": [_I32, _I32, _I32, _P, _I64, _P, _I64, _P, _P, _P],
+    "bm_k_gemm_dswiglu": [_I32, _I32, _I32, _P, _I64, _P, _I64, _P, _P, _P],
     "bm_k_rmsnorm_fwd": [_I32, _I32, _I32, _P, _P, _P, _P, _P],
     "bm_k_rmsnorm_bwd": [_I32, _I32, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _P],
     "bm_k_rmsnorm_bwd_scratch": [_I32, _I32],

@@ -427,9 +427,10 @@ static inline float* G_(bm_ctx& c, const char* name) {
 static inline int LD_(bm_ctx& c, const char* name) { return c.params[c.pidx.at(name)].ld; }
 
 static bm_status timed_gemm(bm_ctx& c, int M, int N, int K, const void* A, int64_t lda, int am, const void* B,
-                            int64_t ldb, int bm_, void* C, int64_t ldc, int cdt, int epi, const void* R, int64_t ldr) {
+                            int64_t ldb, int bm_, void* C, int64_t ldc, int cdt, int epi, const void* R, int64_t ldr,
+                            int f = 0) {
   if (!c.timing || M <= 0 || N <= 0 || K <= 0)
-    return gemm(c.dtype, M, N, K, A, lda, am, B, ldb, bm_, C, ldc, cdt, epi, R, ldr, 1.f, c.st);
+    return gemm(c.dtype, M, N, K, A, lda, am, B, ldb, bm_, C, ldc, cdt, epi, R, ldr, 1.f, c.st, f);
   const int pool = (int)(c.step & 1);
   auto& ev = c.tev[pool];
   if (c.tev_used[pool] + 2 > ev.size()) {
@@ -442,7 +443,7 @@ static bm_status timed_gemm(bm_ctx& c, int M, int N, int K, const void* A, int64
   cudaEvent_t e0 = ev[c.tev_used[pool]], e1 = ev[c.tev_used[pool] + 1];
   c.tev_used[pool] += 2;
   BM_CUDA_TRY(cudaEventRecord(e0, c.st));
-  BM_TRY(gemm(c.dtype, M, N, K, A, lda, am, B, ldb, bm_, C, ldc, cdt, epi, R, ldr, 1.f, c.st));
+  BM_TRY(gemm(c.dtype, M, N, K, A, lda, am, B, ldb, bm_, C, ldc, cdt, epi, R, ldr, 1.f, c.st, f));
   BM_CUDA_TRY(cudaEventRecord(e1, c.st));
   c.tflop_pending[pool] += 2.0 * M * N * K;
   c.gemm_count_pending[pool] += 1;
@@ -480,6 +481,25 @@ static bm_status lin_wgrad(bm_ctx& c, int n, int in, int out, const void* dY, co
   if (n <= 0) return BM_OK;
   return timed_gemm(c, out, in, n, dY, out, 1, X, ldx, 1, dW, ldw, BM_F32, BM_EPI_ACCUM, nullptr, 0);
 }
+// LLM gate/up GEMM; bf16 fuses SwiGLU into the epilogue (writes gu and h)
+static bm_status lin_gate_up(bm_ctx& c, const void* xn, const void* Wgu, int64_t ldw, void* gu, void* h) {
+  const auto& m = c.mc;
+  if (c.dtype == BM_BF16 && m.f % 128 == 0)
+    return timed_gemm(c, m.S, 2 * m.f, m.d, xn, m.d, 0, Wgu, ldw, 0, gu, 2 * m.f, BM_BF16, BM_EPI_SWIGLU, h, m.f, m.f);
+  BM_TRY(timed_gemm(c, m.S, 2 * m.f, m.d, xn, m.d, 0, Wgu, ldw, 0, gu, 2 * m.f, c.dtype, BM_EPI_STORE, nullptr, 0));
+  return c.dtype == BM_BF16 ? swiglu_fwd<bf16>(m.S, m.f, (const bf16*)gu, (bf16*)h, c.st)
+                            : swiglu_fwd<float>(m.S, m.f, (const float*)gu, (float*)h, c.st);
+}
+// LLM down dgrad; bf16 fuses the SwiGLU backward into the epilogue (writes dgu, never dh)
+static bm_status lin_down_dgrad_swiglu(bm_ctx& c, const void* dy, const void* Wd, int64_t ldw, const void* gu,
+                                       void* dh_scratch, void* dgu) {
+  const auto& m = c.mc;
+  if (c.dtype == BM_BF16)
+    return timed_gemm(c, m.S, m.f, m.d, dy, m.d, 0, Wd, ldw, 1, dgu, 2 * m.f, BM_BF16, BM_EPI_DSWIGLU, gu, 2 * m.f, m.f);
+  BM_TRY(timed_gemm(c, m.S, m.f, m.d, dy, m.d, 0, Wd, ldw, 1, dh_scratch, m.f, c.dtype, BM_EPI_STORE, nullptr, 0));
+  return swiglu_bwd<float>(m.S, m.f, (const float*)dh_scratch, (const float*)gu, (float*)dgu, c.st);
+}
+
 #define TY(c, bfcall, fcall) ((c).dtype == BM_BF16 ? (bfcall) : (fcall))
 static bm_status norm_fwd(bm_ctx& c, int rows, int cols, const void* x, const void* g, void* y, float* rstd) {
   return TY(c, rmsnorm_fwd<bf16>(rows, cols, (const bf16*)x, (const bf16*)g, (bf16*)y, rstd, c.st),
@@ -621,9 +641,7 @@ static bm_status op_llm_fwd(bm_ctx& c, const bm_op& o, const RecvState& rs) {
     snprintf(nm, sizeof nm, "llm.layer%d.norm", l);
     BM_TRY(norm_fwd(c, m.S, m.d, sl.x[j], P_(c, nm), sl.xn[j], sl.rstd[j]));
     snprintf(nm, sizeof nm, "llm.layer%d.gate_up", l);
-    BM_TRY(lin_fwd(c, m.S, m.d, 2 * m.f, sl.xn[j], m.d, P_(c, nm), LD_(c, nm), sl.gu[j]));
-    BM_TRY(TY(c, swiglu_fwd<bf16>(m.S, m.f, (const bf16*)sl.gu[j], (bf16*)sl.h[j], c.st),
-              swiglu_fwd<float>(m.S, m.f, (const float*)sl.gu[j], (float*)sl.h[j], c.st)));
+    BM_TRY(lin_gate_up(c, sl.xn[j], P_(c, nm), LD_(c, nm), sl.gu[j], sl.h[j]));
     snprintf(nm, sizeof nm, "llm.layer%d.down", l);
     BM_TRY(lin_fwd(c, m.S, m.f, m.d, sl.h[j], m.f, P_(c, nm), LD_(c, nm), sl.x[j + 1], BM_EPI_ADD, sl.x[j]));
   }
@@ -694,9 +712,7 @@ static bm_status op_llm_bwd(bm_ctx& c, const bm_op& o, const RecvState& rs) {
     char* out = (j == 0) ? c.bout[b] : (cur == c.dwork[0] ? c.dwork[1] : c.dwork[0]);
     snprintf(nm, sizeof nm, "llm.layer%d.down", l);
     BM_TRY(lin_wgrad(c, m.S, m.f, m.d, cur, sl.h[j], m.f, G_(c, nm), LD_(c, nm)));
-    BM_TRY(lin_dgrad(c, m.S, m.f, m.d, cur, P_(c, nm), LD_(c, nm), c.dh, m.f));
-    BM_TRY(TY(c, swiglu_bwd<bf16>(m.S, m.f, (const bf16*)c.dh, (const bf16*)sl.gu[j], (bf16*)c.dgu, c.st),
-              swiglu_bwd<float>(m.S, m.f, (const float*)c.dh, (const float*)sl.gu[j], (float*)c.dgu, c.st)));
+    BM_TRY(lin_down_dgrad_swiglu(c, cur, P_(c, nm), LD_(c, nm), sl.gu[j], c.dh, c.dgu));
     snprintf(nm, sizeof nm, "llm.layer%d.gate_up", l);
     BM_TRY(lin_wgrad(c, m.S, m.d, 2 * m.f, c.dgu, sl.xn[j], m.d, G_(c, nm), LD_(c, nm)));
     BM_TRY(lin_dgrad(c, m.S, m.d, 2 * m.f, c.dgu, P_(c, nm), LD_(c, nm), c.dxn, m.d));

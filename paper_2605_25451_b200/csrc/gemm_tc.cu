@@ -25,6 +25,7 @@
 #include "common.cuh"
 
 namespace bm {
+int gemm_mode();
 namespace tc {
 
 constexpr int BM = 128;
@@ -49,6 +50,7 @@ struct EpiArgs {
   const void* R;
   int64_t ldr;
   float alpha;
+  int f;           // SwiGLU width (BM_EPI_SWIGLU / BM_EPI_DSWIGLU)
 };
 
 // ---------------------------------------------------------------- PTX helpers
@@ -62,16 +64,28 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+__device__ __forceinline__ bool mbar_try(uint32_t addr, uint32_t parity) {
+  uint32_t ok;
   asm volatile(
       "{\n"
       ".reg .pred p;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      "@!p bra WAIT_%=;\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n"
+      "selp.u32 %0, 1, 0, p;\n"
+      "}\n"
+      : "=r"(ok)
+      : "r"(addr), "r"(parity)
       : "memory");
+  return ok != 0;
+}
+// Wait for the phase with `parity`; a protocol bug traps after ~20 s instead of
+// hanging the GPU.
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  if (mbar_try(a, parity)) return;
+  const long long t0 = clock64();
+  while (!mbar_try(a, parity)) {
+    if (clock64() - t0 > 40000000000LL) __trap();
+  }
 }
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
   asm volatile(
@@ -101,6 +115,50 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
                : "memory");
 }
 
+// ---- CTA-pair (cta_group::2) helpers
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t mapa(uint32_t saddr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+// TMA load whose completion is signalled on the pair leader's mbarrier
+__device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* map, uint32_t leader_bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(leader_bar), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void umma_f16_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                              uint32_t accum) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum));
+}
+// commit: arrive on the barrier at the same offset in both CTAs of the pair
+__device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"((uint16_t)0x3)
+      : "memory");
+}
+
 // UMMA shared-memory descriptor, SWIZZLE_128B, version 1 (sm_100).
 //   K-major : LBO unused (1), SBO = 1024 B (8 rows x 128 B)
 //   MN-major: LBO = byte stride between 64-element MN chunks, SBO = 1024 B
@@ -115,14 +173,14 @@ __device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo_bytes
 }
 
 // Instruction descriptor for kind::f16: bf16 x bf16 -> fp32, M = 128, N = BN.
-__host__ __device__ constexpr uint32_t make_idesc(int N, bool a_mn, bool b_mn) {
+__host__ __device__ constexpr uint32_t make_idesc(int N, bool a_mn, bool b_mn, int M = BM) {
   return (1u << 4)                     // D format fp32
          | (1u << 7)                   // A bf16
          | (1u << 10)                  // B bf16
          | ((a_mn ? 1u : 0u) << 15)    // A major
          | ((b_mn ? 1u : 0u) << 16)    // B major
          | ((uint32_t)(N >> 3) << 17)  // N / 8
-         | ((uint32_t)(BM >> 4) << 24);// M / 16
+         | ((uint32_t)(M >> 4) << 24); // M / 16
 }
 
 __device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int& mb, int& nb) {
@@ -153,11 +211,47 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+__device__ __forceinline__ float sigmoidf_(float x) { return 1.f / (1.f + __expf(-x)); }
+
 __device__ __forceinline__ void epilogue_row(const EpiArgs& a, int row, int col0, const float* v) {
   // one thread writes up to 32 consecutive columns of one row
   const int ncols = min(32, a.N - col0);
   if (ncols <= 0) return;
   const float alpha = a.alpha;
+  if (a.epi == BM_EPI_DSWIGLU) {
+    // v = dh[row, col0..]; gu = R [.., 2f]; write dgu = C [.., 2f]
+    const bf16* gu = reinterpret_cast<const bf16*>(a.R) + (int64_t)row * a.ldr;
+    bf16* dgu = reinterpret_cast<bf16*>(a.C) + (int64_t)row * a.ldc;
+    if (ncols == 32) {
+#pragma unroll
+      for (int j = 0; j < 32; j += 8) {
+        uint4 gv = *reinterpret_cast<const uint4*>(gu + col0 + j);
+        uint4 uv = *reinterpret_cast<const uint4*>(gu + a.f + col0 + j);
+        const bf16* gb = reinterpret_cast<const bf16*>(&gv);
+        const bf16* ub = reinterpret_cast<const bf16*>(&uv);
+        uint4 og, ou;
+        bf16* ogb = reinterpret_cast<bf16*>(&og);
+        bf16* oub = reinterpret_cast<bf16*>(&ou);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const float g = __bfloat162float(gb[q]), u = __bfloat162float(ub[q]), d = alpha * v[j + q];
+          const float sg = sigmoidf_(g);
+          ogb[q] = __float2bfloat16_rn(d * u * sg * (1.f + g * (1.f - sg)));
+          oub[q] = __float2bfloat16_rn(d * g * sg);
+        }
+        *reinterpret_cast<uint4*>(dgu + col0 + j) = og;
+        *reinterpret_cast<uint4*>(dgu + a.f + col0 + j) = ou;
+      }
+    } else {
+      for (int j = 0; j < ncols; ++j) {
+        const float g = __bfloat162float(gu[col0 + j]), u = __bfloat162float(gu[a.f + col0 + j]), d = alpha * v[j];
+        const float sg = sigmoidf_(g);
+        dgu[col0 + j] = __float2bfloat16_rn(d * u * sg * (1.f + g * (1.f - sg)));
+        dgu[a.f + col0 + j] = __float2bfloat16_rn(d * g * sg);
+      }
+    }
+    return;
+  }
   if (a.c_f32) {
     float* c = reinterpret_cast<float*>(a.C) + (int64_t)row * a.ldc + col0;
     const bool vec = (ncols == 32) && ((reinterpret_cast<uintptr_t>(c) & 15) == 0);
@@ -216,6 +310,45 @@ __device__ __forceinline__ void epilogue_row(const EpiArgs& a, int row, int col0
         float w = alpha * v[j] + (r ? __bfloat162float(r[j]) : 0.f);
         c[j] = __float2bfloat16_rn(w);
       }
+    }
+  }
+}
+
+
+// gate/up pair epilogue: g = v_g, u = v_u for features [j0, j0+32) of one row;
+// writes gu[row, j0..] = g, gu[row, f + j0..] = u (C, ld 2f) and h = silu(g) u (R, ld f)
+__device__ __forceinline__ void epilogue_swiglu(const EpiArgs& a, int row, int j0, const float* vg, const float* vu) {
+  const int n = min(32, a.f - j0);
+  if (n <= 0) return;
+  bf16* gu = reinterpret_cast<bf16*>(a.C) + (int64_t)row * a.ldc;
+  bf16* h = reinterpret_cast<bf16*>(const_cast<void*>(a.R)) + (int64_t)row * a.ldr;
+  if (n == 32) {
+#pragma unroll
+    for (int j = 0; j < 32; j += 8) {
+      uint4 og, ou, oh;
+      bf16* ogb = reinterpret_cast<bf16*>(&og);
+      bf16* oub = reinterpret_cast<bf16*>(&ou);
+      bf16* ohb = reinterpret_cast<bf16*>(&oh);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const float g = a.alpha * vg[j + q], u = a.alpha * vu[j + q];
+        const bf16 gb = __float2bfloat16_rn(g), ub = __float2bfloat16_rn(u);
+        ogb[q] = gb;
+        oub[q] = ub;
+        const float gr = __bfloat162float(gb), ur = __bfloat162float(ub);
+        ohb[q] = __float2bfloat16_rn(gr * sigmoidf_(gr) * ur);
+      }
+      *reinterpret_cast<uint4*>(gu + j0 + j) = og;
+      *reinterpret_cast<uint4*>(gu + a.f + j0 + j) = ou;
+      *reinterpret_cast<uint4*>(h + j0 + j) = oh;
+    }
+  } else {
+    for (int j = 0; j < n; ++j) {
+      const bf16 gb = __float2bfloat16_rn(a.alpha * vg[j]), ub = __float2bfloat16_rn(a.alpha * vu[j]);
+      gu[j0 + j] = gb;
+      gu[a.f + j0 + j] = ub;
+      const float gr = __bfloat162float(gb), ur = __bfloat162float(ub);
+      h[j0 + j] = __float2bfloat16_rn(gr * sigmoidf_(gr) * ur);
     }
   }
 }
@@ -359,6 +492,182 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
   }
 }
 
+
+// ============================================================================
+// CTA-pair variant (cta_group::2): a cluster of 2 CTAs computes a 256 x BN
+// tile.  CTA r holds rows [128r, 128r+128) of the A tile and columns
+// [r*BN/2, (r+1)*BN/2) of the B tile in its own shared memory; both CTAs' TMA
+// loads complete on the leader's full barrier; the leader's single thread
+// issues tcgen05.mma.cta_group::2 (M = 256, N = BN) which reads both CTAs'
+// operands and writes rows 0-127 to CTA 0's TMEM and 128-255 to CTA 1's.
+// Commits multicast to both CTAs' barriers; both epilogues report to the
+// leader's tmem_empty barrier.  Per CTA and K-block this moves
+// (128 + BN/2)*64*2 bytes instead of (128 + BN)*64*2.
+// ============================================================================
+template <int BN> struct Cfg2 {
+  static constexpr int A_BYTES = 128 * BK * 2;                 // 16 KB
+  static constexpr int B_BYTES = (BN / 2) * BK * 2;            // 16 KB (BN = 256)
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGES = (BN == 256) ? 6 : 8;
+  static constexpr int TMEM_COLS = 2 * BN;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
+};
+
+template <int BN, bool A_MN, bool B_MN, bool SWIGLU>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
+gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, EpiArgs args) {
+  using C = Cfg2<BN>;
+  constexpr int STAGES = C::STAGES;
+  constexpr int BNH = BN / 2;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smA = smem;
+  uint8_t* smB = smem + STAGES * C::A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * C::STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const uint32_t cta = cluster_rank();
+  const int warp = threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  const int tiles_m = (args.M + 2 * BM - 1) / (2 * BM);
+  const int tiles_n = SWIGLU ? (args.f + BNH - 1) / BNH : (args.N + BN - 1) / BN;
+  const int num_tiles = tiles_m * tiles_n;
+  const int nk = (args.K + BK - 1) / BK;
+  const int pair = blockIdx.x / 2, npairs = gridDim.x / 2;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull[s], 1);
+      mbar_init(&tempty[s], 8);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    tma_prefetch(&tmA);
+    tma_prefetch(&tmB);
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"((uint32_t)C::TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = pair; t < num_tiles; t += npairs) {
+        int mb, nb;
+        tile_coords(t, tiles_m, tiles_n, mb, nb);
+        const int m0 = mb * 2 * BM + (int)cta * BM;
+        // SwiGLU pairing: CTA 0 loads gate rows [nb*BNH, +BNH), CTA 1 the matching up rows
+        const int n0 = SWIGLU ? (nb * BNH + (int)cta * args.f) : (nb * BN + (int)cta * BNH);
+        for (int kb = 0; kb < nk; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          if (cta == 0) mbar_expect_tx(&full[stage], 2 * C::STAGE_BYTES);
+          const uint32_t lbar = mapa(smem_u32(&full[stage]), 0);
+          uint8_t* a_dst = smA + stage * C::A_BYTES;
+          uint8_t* b_dst = smB + stage * C::B_BYTES;
+          const int k0 = kb * BK;
+          if (A_MN) {
+#pragma unroll
+            for (int j = 0; j < BM / 64; ++j) tma_load_2d_pair(a_dst + j * (BK * 128), &tmA, lbar, m0 + 64 * j, k0);
+          } else {
+            tma_load_2d_pair(a_dst, &tmA, lbar, k0, m0);
+          }
+          if (B_MN) {
+#pragma unroll
+            for (int j = 0; j < BNH / 64; ++j) tma_load_2d_pair(b_dst + j * (BK * 128), &tmB, lbar, n0 + 64 * j, k0);
+          } else {
+            tma_load_2d_pair(b_dst, &tmB, lbar, k0, n0);
+          }
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (cta == 0 && lane == 0) {
+      constexpr uint32_t idesc = make_idesc(BN, A_MN, B_MN, 2 * BM);
+      int stage = 0;
+      uint32_t phase = 0;
+      int local = 0;
+      for (int t = pair; t < num_tiles; t += npairs, ++local) {
+        const int acc = local & 1;
+        const uint32_t acc_phase = (local >> 1) & 1;
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t tmem_d = tmem_base + acc * BN;
+        for (int kb = 0; kb < nk; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a_base = smem_u32(smA + stage * C::A_BYTES);
+          const uint32_t b_base = smem_u32(smB + stage * C::B_BYTES);
+#pragma unroll
+          for (int kk = 0; kk < BK / 16; ++kk) {
+            uint64_t ad = A_MN ? make_desc(a_base + kk * 2048, BK * 128, 1024) : make_desc(a_base + kk * 32, 16, 1024);
+            uint64_t bd = B_MN ? make_desc(b_base + kk * 2048, BK * 128, 1024) : make_desc(b_base + kk * 32, 16, 1024);
+            umma_f16_pair(tmem_d, ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
+          }
+          umma_commit_pair(&empty[stage]);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+        umma_commit_pair(&tfull[acc]);
+      }
+    }
+  } else {
+    const int quad = warp & 3;
+    const uint32_t leader_tempty0 = mapa(smem_u32(&tempty[0]), 0);
+    const uint32_t leader_tempty1 = mapa(smem_u32(&tempty[1]), 0);
+    int local = 0;
+    for (int t = pair; t < num_tiles; t += npairs, ++local) {
+      int mb, nb;
+      tile_coords(t, tiles_m, tiles_n, mb, nb);
+      const int acc = local & 1;
+      const uint32_t acc_phase = (local >> 1) & 1;
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const int row = mb * 2 * BM + (int)cta * BM + quad * 32 + lane;
+      const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + acc * BN;
+      if (SWIGLU) {
+#pragma unroll 1
+        for (int c = 0; c < BNH; c += 32) {
+          float vg[32], vu[32];
+          tmem_ld32(taddr + c, vg);
+          tmem_ld32(taddr + BNH + c, vu);
+          if (row < args.M) epilogue_swiglu(args, row, nb * BNH + c, vg, vu);
+        }
+      } else {
+#pragma unroll 1
+        for (int c = 0; c < BN; c += 32) {
+          float v[32];
+          tmem_ld32(taddr + c, v);
+          if (row < args.M) epilogue_row(args, row, nb * BN + c, v);
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(acc ? leader_tempty1 : leader_tempty0);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"((uint32_t)C::TMEM_COLS));
+  }
+}
+
 // ---------------------------------------------------------------- host side
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -459,23 +768,82 @@ static bm_status dispatch_majors(bool a_mn, bool b_mn, const CUtensorMap& ma, co
   return launch<BN, true, false>(ma, mb, ea, st);
 }
 
+
+template <int BN, bool A_MN, bool B_MN, bool SWIGLU = false>
+static bm_status launch2(const CUtensorMap& ma, const CUtensorMap& mb, const EpiArgs& ea, cudaStream_t st) {
+  using C = Cfg2<BN>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    BM_CUDA_TRY(cudaFuncSetAttribute(gemm2_kernel<BN, A_MN, B_MN, SWIGLU>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     C::SMEM));
+    attr_set = true;
+  }
+  const int tiles = ceil_div(ea.M, 2 * BM) * (SWIGLU ? ceil_div(ea.f, BN / 2) : ceil_div(ea.N, BN));
+  const int pairs = num_sms() / 2;
+  const int grid = 2 * (tiles < pairs ? tiles : pairs);
+  gemm2_kernel<BN, A_MN, B_MN, SWIGLU><<<grid, NUM_THREADS, C::SMEM, st>>>(ma, mb, ea);
+  count_launch();
+  BM_CUDA_TRY(cudaGetLastError());
+  return BM_OK;
+}
+
+template <int BN>
+static bm_status dispatch_majors2(bool a_mn, bool b_mn, const CUtensorMap& ma, const CUtensorMap& mb,
+                                  const EpiArgs& ea, cudaStream_t st) {
+  if (!a_mn && !b_mn) return launch2<BN, false, false>(ma, mb, ea, st);
+  if (!a_mn && b_mn) return launch2<BN, false, true>(ma, mb, ea, st);
+  if (a_mn && b_mn) return launch2<BN, true, true>(ma, mb, ea, st);
+  return launch2<BN, true, false>(ma, mb, ea, st);
+}
+
 }  // namespace tc
+
+// 0 = auto (CTA pairs for large contractions), 1 = force 1-CTA, 2 = force CTA pairs
+static int g_gemm_mode = [] {
+  const char* e = getenv("BM_GEMM_MODE");
+  return e ? (e[0] == '1' ? 1 : (e[0] == '2' ? 2 : 0)) : 0;
+}();
+int gemm_mode() { return g_gemm_mode; }
+void set_gemm_mode(int m) { g_gemm_mode = m; }
 
 bm_status gemm_bf16_tc(int M, int N, int K, const void* A, int64_t lda, int a_major, const void* B, int64_t ldb,
                        int b_major, void* Cp, int64_t ldc, int c_dtype, int epi, const void* R, int64_t ldr,
-                       float alpha, cudaStream_t st) {
+                       float alpha, cudaStream_t st, int f) {
   using namespace tc;
   BM_CHECK_ARG(lda % 8 == 0 && ldb % 8 == 0, "lda/ldb must be multiples of 8 (16-byte TMA strides)");
   BM_CHECK_ARG((reinterpret_cast<uintptr_t>(A) & 15) == 0 && (reinterpret_cast<uintptr_t>(B) & 15) == 0,
                "A/B must be 16-byte aligned");
-  const int BN = (N <= 64) ? 64 : (N <= 128 ? 128 : 256);
+  const bool amn = a_major != 0, bmn = b_major != 0;
+  EpiArgs ea{M, N, K, Cp, ldc, c_dtype == BM_F32 ? 1 : 0, epi, R, ldr, alpha, f};
   CUtensorMap ma, mb;
+  if (epi == BM_EPI_SWIGLU) {
+    // gate/up GEMM with fused SwiGLU: always CTA pairs, BN = 256 (128 gate + 128 up features)
+    BM_CHECK_ARG(b_major == 0 && c_dtype == BM_BF16 && N == 2 * f && f % 128 == 0, "SWIGLU epilogue: K-major B, bf16, N = 2f, f % 128 == 0");
+    if (a_major == 0) BM_TRY(make_map(A, K, M, lda, BM, &ma));
+    else BM_TRY(make_map(A, M, K, lda, BK, &ma));
+    BM_TRY(make_map(B, K, N, ldb, 128, &mb));
+    if (a_major == 0) return launch2<256, false, false, true>(ma, mb, ea, st);
+    return launch2<256, true, false, true>(ma, mb, ea, st);
+  }
+  if (epi == BM_EPI_DSWIGLU)
+    BM_CHECK_ARG(c_dtype == BM_BF16 && N == f && ldc >= 2 * f && ldr >= 2 * f, "DSWIGLU epilogue: bf16, N = f, C/R are [M, 2f]");
+  // CTA-pair kernel for the large contractions (the LLM's), 1-CTA otherwise
+  const int mode = gemm_mode();
+  const bool pair = mode == 2 || (mode == 0 && M >= 512 && N >= 256 && K >= 256);
+  if (pair) {
+    const int BN2 = (N >= 256) ? 256 : 128;
+    if (a_major == 0) BM_TRY(make_map(A, K, M, lda, BM, &ma));
+    else BM_TRY(make_map(A, M, K, lda, BK, &ma));
+    if (b_major == 0) BM_TRY(make_map(B, K, N, ldb, BN2 / 2, &mb));
+    else BM_TRY(make_map(B, N, K, ldb, BK, &mb));
+    if (BN2 == 256) return dispatch_majors2<256>(amn, bmn, ma, mb, ea, st);
+    return dispatch_majors2<128>(amn, bmn, ma, mb, ea, st);
+  }
+  const int BN = (N <= 64) ? 64 : (N <= 128 ? 128 : 256);
   if (a_major == 0) BM_TRY(make_map(A, K, M, lda, BM, &ma));
   else BM_TRY(make_map(A, M, K, lda, BK, &ma));
   if (b_major == 0) BM_TRY(make_map(B, K, N, ldb, BN, &mb));
   else BM_TRY(make_map(B, N, K, ldb, BK, &mb));
-  EpiArgs ea{M, N, K, Cp, ldc, c_dtype == BM_F32 ? 1 : 0, epi, R, ldr, alpha};
-  const bool amn = a_major != 0, bmn = b_major != 0;
   if (BN == 64) return dispatch_majors<64>(amn, bmn, ma, mb, ea, st);
   if (BN == 128) return dispatch_majors<128>(amn, bmn, ma, mb, ea, st);
   return dispatch_majors<256>(amn, bmn, ma, mb, ea, st);

@@ -30,8 +30,12 @@ int64_t launch_count() { return g_launches.load(std::memory_order_relaxed); }
 
 bm_status gemm(int dtype, int M, int N, int K, const void* A, int64_t lda, int a_major, const void* B, int64_t ldb,
                int b_major, void* C, int64_t ldc, int c_dtype, int epi, const void* R, int64_t ldr, float alpha,
-               cudaStream_t st) {
+               cudaStream_t st, int f) {
   if (M <= 0 || N <= 0) return BM_OK;
+  if (epi == BM_EPI_SWIGLU || epi == BM_EPI_DSWIGLU) {
+    BM_CHECK_ARG(dtype == BM_BF16 && K > 0, "fused SwiGLU epilogues are bf16 tensor-core only");
+    return gemm_bf16_tc(M, N, K, A, lda, a_major, B, ldb, b_major, C, ldc, c_dtype, epi, R, ldr, alpha, st, f);
+  }
   BM_CHECK_ARG(epi != BM_EPI_ACCUM || c_dtype == BM_F32, "ACCUM epilogue requires an fp32 C");
   if (K <= 0) {
     // empty contraction: C = 0 (STORE) / C = R (ADD) / unchanged (ACCUM)
@@ -65,14 +69,35 @@ using namespace bm;
     return BM_E_INVALID;                                      \
   } while (0)
 
+namespace bm { void set_gemm_mode(int m); }
+
 extern "C" {
 
 const char* bm_last_error(void) { return get_error(); }
 
+bm_status bm_k_gemm_mode(int32_t mode) {
+  BM_CHECK_ARG(mode >= 0 && mode <= 2, "mode must be 0 (auto), 1 (1-CTA) or 2 (CTA pair)");
+  bm::set_gemm_mode(mode);
+  return BM_OK;
+}
+
 bm_status bm_k_gemm(int32_t dtype, int32_t M, int32_t N, int32_t K, const void* A, int64_t lda, int32_t a_major,
                     const void* B, int64_t ldb, int32_t b_major, void* C, int64_t ldc, int32_t c_dtype,
                     int32_t epilogue, const void* R, int64_t ldr, float alpha, void* stream) {
+  BM_CHECK_ARG(epilogue >= BM_EPI_STORE && epilogue <= BM_EPI_ADD, "use bm_k_gemm_swiglu for fused SwiGLU epilogues");
   return gemm(dtype, M, N, K, A, lda, a_major, B, ldb, b_major, C, ldc, c_dtype, epilogue, R, ldr, alpha, ST(stream));
+}
+
+bm_status bm_k_gemm_swiglu(int32_t M, int32_t f, int32_t K, const void* X, int64_t ldx, const void* W, int64_t ldw,
+                           void* gu, void* h, void* stream) {
+  return gemm(BM_BF16, M, 2 * f, K, X, ldx, 0, W, ldw, 0, gu, 2 * (int64_t)f, BM_BF16, BM_EPI_SWIGLU, h, f, 1.f,
+              ST(stream), f);
+}
+
+bm_status bm_k_gemm_dswiglu(int32_t M, int32_t f, int32_t K, const void* dY, int64_t lddy, const void* W, int64_t ldw,
+                            const void* gu, void* dgu, void* stream) {
+  return gemm(BM_BF16, M, f, K, dY, lddy, 0, W, ldw, 1, dgu, 2 * (int64_t)f, BM_BF16, BM_EPI_DSWIGLU, gu,
+              2 * (int64_t)f, 1.f, ST(stream), f);
 }
 
 bm_status bm_k_rmsnorm_fwd(int32_t dtype, int32_t rows, int32_t cols, const void* x, const void* g, void* y,

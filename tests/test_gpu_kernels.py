@@ -42,8 +42,9 @@ GEMM_SHAPES = [(128, 256, 64), (300, 200, 100), (1, 16, 48), (257, 513, 130), (6
 
 @pytest.mark.parametrize("M,N,K", GEMM_SHAPES)
 @pytest.mark.parametrize("a_mn,b_mn", [(0, 0), (0, 1), (1, 1), (1, 0)])
-@pytest.mark.parametrize("dtype", [BF16, F32])
-def test_gemm_store_f32(L, M, N, K, a_mn, b_mn, dtype):
+@pytest.mark.parametrize("dtype,mode", [(BF16, 1), (BF16, 2), (BF16, 0), (F32, 0)])
+def test_gemm_store_f32(L, M, N, K, a_mn, b_mn, dtype, mode):
+    L.call("bm_k_gemm_mode", mode)
     rng = np.random.default_rng(M * 7 + N * 3 + K + 11 * a_mn + 5 * b_mn)
     A = rnd(rng, M, K)
     B = rnd(rng, N, K)
@@ -58,6 +59,7 @@ def test_gemm_store_f32(L, M, N, K, a_mn, b_mn, dtype):
            C.data_ptr(), N, F32, 0, None, 0, 1.0, None)
     torch.cuda.synchronize()
     ref = A @ B.T
+    L.call("bm_k_gemm_mode", 0)
     err = np.abs(host(C) - ref).max()
     tol = 1e-5 * np.sqrt(K) * max(1.0, np.abs(ref).max()) if dtype == BF16 else 2e-6 * np.sqrt(K) * max(1.0, np.abs(ref).max())
     assert err <= tol, (err, tol)
@@ -65,7 +67,9 @@ def test_gemm_store_f32(L, M, N, K, a_mn, b_mn, dtype):
 
 @pytest.mark.parametrize("M,N,K", [(300, 200, 104), (257, 513, 136), (1024, 768, 512)])
 @pytest.mark.parametrize("epi", ["bf16_store", "bf16_add", "f32_accum"])
-def test_gemm_epilogues(L, M, N, K, epi):
+@pytest.mark.parametrize("mode", [1, 2])
+def test_gemm_epilogues(L, M, N, K, epi, mode):
+    L.call("bm_k_gemm_mode", mode)
     rng = np.random.default_rng(1)
     A, B = rnd(rng, M, K), rnd(rng, N, K)
     R = rnd(rng, M, N)
@@ -87,6 +91,7 @@ def test_gemm_epilogues(L, M, N, K, epi):
                None, 0, 0.5, None)
         ref = ref + R
     torch.cuda.synchronize()
+    L.call("bm_k_gemm_mode", 0)
     out = host(C)
     if epi.startswith("bf16"):
         assert np.all(np.abs(out - ref) <= 2.0 ** -8 * np.abs(ref) + 1e-4 * np.sqrt(K))
@@ -221,3 +226,30 @@ def test_mse(L, dtype):
     tol = 1e-2 if dtype == BF16 else 1e-6
     ref = 2 * (o - t) / denom * 0.5
     assert np.abs(host(dout) - ref).max() <= tol * np.abs(ref).max()
+
+
+@pytest.mark.parametrize("M,f,K", [(300, 384, 128), (1000, 1024, 512), (2048, 1024, 256), (1, 128, 64)])
+def test_gemm_fused_swiglu(L, M, f, K):
+    # gate/up GEMM + SwiGLU epilogue, and down dgrad + SwiGLU-backward epilogue
+    rng = np.random.default_rng(9)
+    X = rnd(rng, M, K)
+    Wgu = rnd(rng, 2 * f, K, scale=0.1)
+    Xd, Wd = dev(X, BF16), dev(Wgu, BF16)
+    gu = torch.zeros((M, 2 * f), device="cuda", dtype=torch.bfloat16)
+    h = torch.zeros((M, f), device="cuda", dtype=torch.bfloat16)
+    L.call("bm_k_gemm_swiglu", M, f, K, Xd.data_ptr(), K, Wd.data_ptr(), K, gu.data_ptr(), h.data_ptr(), None)
+    Kd = 256
+    dY = rnd(rng, M, Kd)
+    Wdown = rnd(rng, Kd, f, scale=0.1)
+    dYd, Wdd = dev(dY, BF16), dev(Wdown, BF16)
+    dgu = torch.zeros((M, 2 * f), device="cuda", dtype=torch.bfloat16)
+    L.call("bm_k_gemm_dswiglu", M, f, Kd, dYd.data_ptr(), Kd, Wdd.data_ptr(), f, gu.data_ptr(), dgu.data_ptr(), None)
+    torch.cuda.synchronize()
+    gu_ref = X @ Wgu.T
+    gu_out = host(gu)
+    assert np.all(np.abs(gu_out - gu_ref) <= 2.0 ** -8 * np.abs(gu_ref) + 1e-4 * np.sqrt(K))
+    h_ref = om.swiglu(gu_out, f)     # activation of the stored bf16 g, u
+    assert np.abs(host(h) - h_ref).max() <= 1e-2 * max(1e-3, np.abs(h_ref).max())
+    dh = dY @ Wdown
+    dgu_ref = om.swiglu_bwd(dh, gu_out, f)
+    assert np.abs(host(dgu) - dgu_ref).max() <= 1e-2 * max(1e-3, np.abs(dgu_ref).max())
