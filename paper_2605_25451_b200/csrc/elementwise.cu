@@ -175,36 +175,33 @@ static int dg_chunks(int rows) { return rows < 64 ? (rows > 0 ? rows : 1) : 64; 
 
 // ------------------------------------------------------------------ SwiGLU / GELU
 template <typename T>
-__global__ void swiglu_fwd_kernel(int64_t total, int f, const T* __restrict__ gu, T* __restrict__ h) {
+__global__ void __launch_bounds__(256)
+swiglu_fwd_kernel(int rows, int f, const T* __restrict__ gu, T* __restrict__ h) {
+  // 2-D grid: blockIdx.y = row, x over 16-byte vectors of the row (no division)
   constexpr int N = V16<T>::N;
-  const int64_t nv = total / N;
-  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nv; v += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t e = v * N;
-    const int64_t i = e / f;
-    const int j = (int)(e % f);
-    const T* row = gu + i * 2 * (int64_t)f;
+  const int64_t i = blockIdx.y;
+  const T* row = gu + i * 2 * (int64_t)f;
+  T* out = h + i * (int64_t)f;
+  for (int j = (blockIdx.x * blockDim.x + threadIdx.x) * N; j < f; j += gridDim.x * blockDim.x * N) {
     V16<T> gv = vload(row + j), uv = vload(row + f + j), o;
 #pragma unroll
     for (int q = 0; q < N; ++q) {
       const float gg = gv.get(q);
-      const float s = 1.f / (1.f + __expf(-gg));
-      o.set(q, gg * s * uv.get(q));
+      o.set(q, gg * uv.get(q) / (1.f + __expf(-gg)));
     }
-    vstore(h + e, o);
+    vstore(out + j, o);
   }
 }
 template <typename T>
-__global__ void swiglu_bwd_kernel(int64_t total, int f, const T* __restrict__ dh, const T* __restrict__ gu,
-                                  T* __restrict__ dgu) {
+__global__ void __launch_bounds__(256)
+swiglu_bwd_kernel(int rows, int f, const T* __restrict__ dh, const T* __restrict__ gu, T* __restrict__ dgu) {
   constexpr int N = V16<T>::N;
-  const int64_t nv = total / N;
-  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nv; v += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t e = v * N;
-    const int64_t i = e / f;
-    const int j = (int)(e % f);
-    const T* row = gu + i * 2 * (int64_t)f;
-    T* orow = dgu + i * 2 * (int64_t)f;
-    V16<T> gv = vload(row + j), uv = vload(row + f + j), dv = vload(dh + e), og, ou;
+  const int64_t i = blockIdx.y;
+  const T* row = gu + i * 2 * (int64_t)f;
+  const T* drow = dh + i * (int64_t)f;
+  T* orow = dgu + i * 2 * (int64_t)f;
+  for (int j = (blockIdx.x * blockDim.x + threadIdx.x) * N; j < f; j += gridDim.x * blockDim.x * N) {
+    V16<T> gv = vload(row + j), uv = vload(row + f + j), dv = vload(drow + j), og, ou;
 #pragma unroll
     for (int q = 0; q < N; ++q) {
       const float gg = gv.get(q), uu = uv.get(q), d = dv.get(q);
@@ -397,6 +394,145 @@ __global__ void mse_kernel(int64_t n, const T* __restrict__ out, const T* __rest
   if (threadIdx.x == 0) loss[0] += s * inv_denom * scale_loss;
 }
 
+
+// Fused RMSNorm backward: one pass computes dx (+ dres) for RB rows per block
+// and this block's deterministic partial of dg (per-warp register partials,
+// reduced across the block's warps in a fixed order through shared memory).
+// partial[block][col]; a second tiny kernel sums the blocks in order.
+template <typename T, int CH>
+__global__ void __launch_bounds__(256)
+rmsnorm_bwd_fused_kernel(int rows, int cols, int rows_per_block, const T* __restrict__ dy, const T* __restrict__ x,
+                         const T* __restrict__ g, const float* __restrict__ rstd, const T* dres, T* dx,
+                         float* __restrict__ partial) {
+  constexpr int N = V16<T>::N;
+  extern __shared__ float sdg[];  // [8 warps][cols]
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  float acc[CH][N];
+#pragma unroll
+  for (int k = 0; k < CH; ++k)
+#pragma unroll
+    for (int i = 0; i < N; ++i) acc[k][i] = 0.f;
+  const int r0 = blockIdx.x * rows_per_block;
+  const int r1 = min(rows, r0 + rows_per_block);
+  for (int row = r0 + warp; row < r1; row += 8) {
+    const int64_t off = (int64_t)row * cols;
+    const float r = rstd[row];
+    float dot = 0.f;
+#pragma unroll
+    for (int k = 0; k < CH; ++k) {
+      const int c = (k * 32 + lane) * N;
+      if (c < cols) {
+        V16<T> dv = vload(dy + off + c), xv = vload(x + off + c), gv = vload(g + c);
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+          const float xh = xv.get(i) * r;
+          dot += dv.get(i) * gv.get(i) * xh;
+          acc[k][i] += dv.get(i) * xh;
+        }
+      }
+    }
+    dot = warp_sum(dot) / cols;
+#pragma unroll
+    for (int k = 0; k < CH; ++k) {
+      const int c = (k * 32 + lane) * N;
+      if (c < cols) {
+        V16<T> dv = vload(dy + off + c), xv = vload(x + off + c), gv = vload(g + c), o, rv;
+        if (dres) rv = vload(dres + off + c);
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+          float v = r * (dv.get(i) * gv.get(i) - xv.get(i) * r * dot);
+          if (dres) v += rv.get(i);
+          o.set(i, v);
+        }
+        vstore(dx + off + c, o);
+      }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < CH; ++k) {
+    const int c = (k * 32 + lane) * N;
+    if (c < cols) {
+#pragma unroll
+      for (int i = 0; i < N; ++i) sdg[warp * cols + c + i] = acc[k][i];
+    }
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < cols; c += blockDim.x) {
+    float s = 0.f;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) s += sdg[w * cols + c];
+    partial[(int64_t)blockIdx.x * cols + c] = s;
+  }
+}
+
+// Cross-entropy, vectorized: pass 1 online max/sum over 16-byte vectors, pass 2
+// writes dz = (softmax - onehot) * scale in place.
+template <typename T>
+__global__ void __launch_bounds__(256)
+ce_row_vec_kernel(int V, T* __restrict__ logits, const int32_t* __restrict__ labels, float scale_grad,
+                  float* __restrict__ row_loss) {
+  constexpr int N = V16<T>::N;
+  __shared__ float shm[32], shs[32];
+  const int row = blockIdx.x;
+  T* z = logits + (int64_t)row * V;
+  const int nv = V / N;
+  float m = -FLT_MAX, sum = 0.f;
+  for (int v = threadIdx.x; v < nv; v += blockDim.x) {
+    V16<T> a = vload(z + (int64_t)v * N);
+    float vm = a.get(0);
+#pragma unroll
+    for (int i = 1; i < N; ++i) vm = fmaxf(vm, a.get(i));
+    if (vm > m) { sum *= __expf(m - vm); m = vm; }
+#pragma unroll
+    for (int i = 0; i < N; ++i) sum += __expf(a.get(i) - m);
+  }
+  for (int j = nv * N + threadIdx.x; j < V; j += blockDim.x) {
+    const float a = to_f(z[j]);
+    if (a > m) { sum *= __expf(m - a); m = a; }
+    sum += __expf(a - m);
+  }
+  // combine (m, sum) across the block deterministically
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float m2 = __shfl_xor_sync(0xffffffffu, m, o), s2 = __shfl_xor_sync(0xffffffffu, sum, o);
+    const float mm = fmaxf(m, m2);
+    sum = sum * __expf(m - mm) + s2 * __expf(m2 - mm);
+    m = mm;
+  }
+  const int w = threadIdx.x / 32, l = threadIdx.x % 32;
+  if (l == 0) { shm[w] = m; shs[w] = sum; }
+  __syncthreads();
+  if (w == 0) {
+    const int nw = blockDim.x / 32;
+    m = l < nw ? shm[l] : -FLT_MAX;
+    sum = l < nw ? shs[l] : 0.f;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float m2 = __shfl_xor_sync(0xffffffffu, m, o), s2 = __shfl_xor_sync(0xffffffffu, sum, o);
+      const float mm = fmaxf(m, m2);
+      sum = (sum == 0.f ? 0.f : sum * __expf(m - mm)) + (s2 == 0.f ? 0.f : s2 * __expf(m2 - mm));
+      m = mm;
+    }
+    if (l == 0) { shm[0] = m; shs[0] = sum; }
+  }
+  __syncthreads();
+  const float lse = shm[0] + __logf(shs[0]);
+  const int lab = labels[row];
+  if (threadIdx.x == 0) row_loss[row] = lse - to_f(z[lab]);
+  __syncthreads();
+  for (int v = threadIdx.x; v < nv; v += blockDim.x) {
+    V16<T> a = vload(z + (int64_t)v * N), o;
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      const int j = v * N + i;
+      o.set(i, (__expf(a.get(i) - lse) - (j == lab ? 1.f : 0.f)) * scale_grad);
+    }
+    vstore(z + (int64_t)v * N, o);
+  }
+  for (int j = nv * N + threadIdx.x; j < V; j += blockDim.x)
+    z[j] = from_f<T>((__expf(to_f(z[j]) - lse) - (j == lab ? 1.f : 0.f)) * scale_grad);
+}
+
 // ================================================================== launchers
 static int ew_grid(int64_t work_items) {
   int64_t g = (work_items + 255) / 256;
@@ -414,12 +550,39 @@ bm_status rmsnorm_fwd(int rows, int cols, const T* x, const T* g, T* y, float* r
   BM_CUDA_TRY(cudaGetLastError());
   return BM_OK;
 }
+constexpr int RB_ROWS = 32;  // rows per block of the fused backward
+template <typename T, int CH>
+static bm_status launch_rms_bwd_fused(int rows, int cols, const T* dy, const T* x, const T* g, const float* rstd,
+                                      const T* dres, T* dx, float* dg, float* partial, cudaStream_t st) {
+  const int nb = ceil_div(rows, RB_ROWS);
+  const int smem = 8 * cols * 4;
+  static bool attr = false;
+  if (!attr) {
+    BM_CUDA_TRY(cudaFuncSetAttribute(rmsnorm_bwd_fused_kernel<T, CH>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    attr = true;
+  }
+  rmsnorm_bwd_fused_kernel<T, CH><<<nb, 256, smem, st>>>(rows, cols, RB_ROWS, dy, x, g, rstd, dres, dx, partial);
+  colsum_accum_kernel<<<ceil_div(cols, 256), 256, 0, st>>>(nb, cols, partial, dg);
+  count_launch(2);
+  BM_CUDA_TRY(cudaGetLastError());
+  return BM_OK;
+}
+
 template <typename T>
 bm_status rmsnorm_bwd(int rows, int cols, const T* dy, const T* x, const T* g, const float* rstd, const T* dres,
                       T* dx, float* dg, float* partial, cudaStream_t st) {
   if (rows <= 0) return BM_OK;
-  BM_CHECK_ARG(cols % V16<T>::N == 0, "rmsnorm cols must be a multiple of the vector width");
-  // gain gradient first (dx may alias dy's residual buffer)
+  constexpr int N = V16<T>::N;
+  BM_CHECK_ARG(cols % N == 0, "rmsnorm cols must be a multiple of the vector width");
+  const int ch = ceil_div(cols, 32 * N);  // vector chunks per lane
+  if (ch <= 16 && cols <= 6144) {
+    if (ch <= 1) return launch_rms_bwd_fused<T, 1>(rows, cols, dy, x, g, rstd, dres, dx, dg, partial, st);
+    if (ch <= 2) return launch_rms_bwd_fused<T, 2>(rows, cols, dy, x, g, rstd, dres, dx, dg, partial, st);
+    if (ch <= 4) return launch_rms_bwd_fused<T, 4>(rows, cols, dy, x, g, rstd, dres, dx, dg, partial, st);
+    if (ch <= 8) return launch_rms_bwd_fused<T, 8>(rows, cols, dy, x, g, rstd, dres, dx, dg, partial, st);
+    return launch_rms_bwd_fused<T, 16>(rows, cols, dy, x, g, rstd, dres, dx, dg, partial, st);
+  }
+  // wide rows: separate gain-gradient pass
   const int nch = dg_chunks(rows);
   rmsnorm_dg_partial_kernel<T><<<dim3(ceil_div(cols, 256), nch), 256, 0, st>>>(rows, cols, nch, dy, x, rstd, partial);
   colsum_accum_kernel<<<ceil_div(cols, 256), 256, 0, st>>>(nch, cols, partial, dg);
@@ -433,7 +596,8 @@ bm_status swiglu_fwd(int rows, int f, const T* gu, T* h, cudaStream_t st) {
   const int64_t total = (int64_t)rows * f;
   if (total == 0) return BM_OK;
   BM_CHECK_ARG(f % V16<T>::N == 0, "swiglu f must be a multiple of the vector width");
-  swiglu_fwd_kernel<T><<<ew_grid(total / V16<T>::N), 256, 0, st>>>(total, f, gu, h);
+  const int vx = ceil_div(f / V16<T>::N, 256);
+  swiglu_fwd_kernel<T><<<dim3(vx > 4 ? 4 : vx, rows), 256, 0, st>>>(rows, f, gu, h);
   count_launch();
   BM_CUDA_TRY(cudaGetLastError());
   return BM_OK;
@@ -443,7 +607,8 @@ bm_status swiglu_bwd(int rows, int f, const T* dh, const T* gu, T* dgu, cudaStre
   const int64_t total = (int64_t)rows * f;
   if (total == 0) return BM_OK;
   BM_CHECK_ARG(f % V16<T>::N == 0, "swiglu f must be a multiple of the vector width");
-  swiglu_bwd_kernel<T><<<ew_grid(total / V16<T>::N), 256, 0, st>>>(total, f, dh, gu, dgu);
+  const int vx = ceil_div(f / V16<T>::N, 256);
+  swiglu_bwd_kernel<T><<<dim3(vx > 4 ? 4 : vx, rows), 256, 0, st>>>(rows, f, dh, gu, dgu);
   count_launch();
   BM_CUDA_TRY(cudaGetLastError());
   return BM_OK;
@@ -497,7 +662,10 @@ template <typename T>
 bm_status ce_fwd_bwd(int n, int V, T* logits, const int32_t* labels, float scale_grad, float* loss_out,
                      float scale_loss, int accumulate, float* scratch, cudaStream_t st) {
   if (n <= 0) return BM_OK;
-  ce_row_kernel<T><<<n, 256, 0, st>>>(V, logits, labels, scale_grad, scratch);
+  if (V % V16<T>::N == 0)
+    ce_row_vec_kernel<T><<<n, 256, 0, st>>>(V, logits, labels, scale_grad, scratch);
+  else
+    ce_row_kernel<T><<<n, 256, 0, st>>>(V, logits, labels, scale_grad, scratch);
   sum_scale_kernel<<<1, 1024, 0, st>>>(n, scratch, scale_loss / n, accumulate, loss_out);
   count_launch(2);
   BM_CUDA_TRY(cudaGetLastError());
@@ -547,7 +715,11 @@ bm_status cast(int sd, int dd, int64_t n, const void* s, void* d, cudaStream_t s
 BM_INST(bf16)
 BM_INST(float)
 
-int64_t rmsnorm_bwd_scratch_floats(int rows, int cols) { return (int64_t)dg_chunks(rows) * cols; }
+int64_t rmsnorm_bwd_scratch_floats(int rows, int cols) {
+  const int64_t fused = (int64_t)ceil_div(rows, RB_ROWS) * cols;
+  const int64_t split = (int64_t)dg_chunks(rows) * cols;
+  return fused > split ? fused : split;
+}
 
 // step loss L = (1/M) sum_m (CE_m + MSE_m) from loss[0:2M] into loss[2M]
 bm_status loss_finalize(int M, float* loss, cudaStream_t st) {

@@ -17,6 +17,7 @@
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <array>
 #include <cstring>
 #include <map>
 #include <string>
@@ -256,20 +257,36 @@ struct bm_ctx {
   int last_src_idx = 0;
   std::vector<const char*> genin_src;  // per destination rank (last stage)
   cudaEvent_t producer_ev = nullptr;
+  cudaStream_t producer_st = nullptr;  // stream of the last compute op (sends record their producer event here)
+  // high-priority generator stream (P > 1, DP-sharded generator): gen shards run as
+  // soon as their inputs exist instead of queueing behind the rank's LLM op
+  cudaStream_t gen_st = nullptr;
+  bool use_gen_stream = false;
+  cudaEvent_t hn_ev = nullptr, gen_done_ev = nullptr;
+  bool gen_done_pending = false;
+  std::vector<int> consumer_kind;      // per op index: kind of the first compute op after it
   // GEMM timing (bench roofline): event pairs around every GEMM, two pools by step parity
   bool timing = false;
+  // fused SwiGLU GEMM epilogues (bm_k_gemm_swiglu / _dswiglu); off by default: measured
+  // slower than GEMM + the separate vectorised kernel (profiles/r01/gemm_bench_v4)
+  bool fuse_swiglu = getenv("BM_FUSE_SWIGLU") != nullptr;
   std::vector<cudaEvent_t> tev[2];
   size_t tev_used[2] = {0, 0};
   double tflop_pending[2] = {0, 0};
   double gemm_flops = 0, gemm_ms = 0;
   int64_t gemm_count = 0;
   int64_t gemm_count_pending[2] = {0, 0};
+  std::vector<std::array<int, 4>> tshape[2];              // (M, N, K, epi) per timed launch
+  std::map<std::array<int, 4>, std::pair<int64_t, double>> shape_ms;  // BM_GEMM_LOG=1 breakdown
   ~bm_ctx();
 };
 
 bm_ctx::~bm_ctx() {
   for (auto s_ : comm_st)
     if (s_) cudaStreamDestroy(s_);
+  if (gen_st) cudaStreamDestroy(gen_st);
+  if (hn_ev) cudaEventDestroy(hn_ev);
+  if (gen_done_ev) cudaEventDestroy(gen_done_ev);
   for (auto e : evpool)
     if (e) cudaEventDestroy(e);
   for (int k = 0; k < 2; ++k)
@@ -447,6 +464,7 @@ static bm_status timed_gemm(bm_ctx& c, int M, int N, int K, const void* A, int64
   BM_CUDA_TRY(cudaEventRecord(e1, c.st));
   c.tflop_pending[pool] += 2.0 * M * N * K;
   c.gemm_count_pending[pool] += 1;
+  c.tshape[pool].push_back({M, N, K, epi});
   return BM_OK;
 }
 // fold a finished pool's event pairs into the totals (blocks until they completed)
@@ -459,7 +477,13 @@ static bm_status harvest(bm_ctx& c, int pool) {
     float t = 0;
     BM_CUDA_TRY(cudaEventElapsedTime(&t, ev[i], ev[i + 1]));
     ms += t;
+    if (i / 2 < c.tshape[pool].size()) {
+      auto& e = c.shape_ms[c.tshape[pool][i / 2]];
+      e.first += 1;
+      e.second += t;
+    }
   }
+  c.tshape[pool].clear();
   c.gemm_ms += ms;
   c.gemm_flops += c.tflop_pending[pool];
   c.gemm_count += c.gemm_count_pending[pool];
@@ -484,7 +508,7 @@ static bm_status lin_wgrad(bm_ctx& c, int n, int in, int out, const void* dY, co
 // LLM gate/up GEMM; bf16 fuses SwiGLU into the epilogue (writes gu and h)
 static bm_status lin_gate_up(bm_ctx& c, const void* xn, const void* Wgu, int64_t ldw, void* gu, void* h) {
   const auto& m = c.mc;
-  if (c.dtype == BM_BF16 && m.f % 128 == 0)
+  if (c.fuse_swiglu && c.dtype == BM_BF16 && m.f % 128 == 0)
     return timed_gemm(c, m.S, 2 * m.f, m.d, xn, m.d, 0, Wgu, ldw, 0, gu, 2 * m.f, BM_BF16, BM_EPI_SWIGLU, h, m.f, m.f);
   BM_TRY(timed_gemm(c, m.S, 2 * m.f, m.d, xn, m.d, 0, Wgu, ldw, 0, gu, 2 * m.f, c.dtype, BM_EPI_STORE, nullptr, 0));
   return c.dtype == BM_BF16 ? swiglu_fwd<bf16>(m.S, m.f, (const bf16*)gu, (bf16*)h, c.st)
@@ -494,10 +518,11 @@ static bm_status lin_gate_up(bm_ctx& c, const void* xn, const void* Wgu, int64_t
 static bm_status lin_down_dgrad_swiglu(bm_ctx& c, const void* dy, const void* Wd, int64_t ldw, const void* gu,
                                        void* dh_scratch, void* dgu) {
   const auto& m = c.mc;
-  if (c.dtype == BM_BF16)
+  if (c.fuse_swiglu && c.dtype == BM_BF16)
     return timed_gemm(c, m.S, m.f, m.d, dy, m.d, 0, Wd, ldw, 1, dgu, 2 * m.f, BM_BF16, BM_EPI_DSWIGLU, gu, 2 * m.f, m.f);
   BM_TRY(timed_gemm(c, m.S, m.f, m.d, dy, m.d, 0, Wd, ldw, 1, dh_scratch, m.f, c.dtype, BM_EPI_STORE, nullptr, 0));
-  return swiglu_bwd<float>(m.S, m.f, (const float*)dh_scratch, (const float*)gu, (float*)dgu, c.st);
+  return c.dtype == BM_BF16 ? swiglu_bwd<bf16>(m.S, m.f, (const bf16*)dh_scratch, (const bf16*)gu, (bf16*)dgu, c.st)
+                            : swiglu_bwd<float>(m.S, m.f, (const float*)dh_scratch, (const float*)gu, (float*)dgu, c.st);
 }
 
 #define TY(c, bfcall, fcall) ((c).dtype == BM_BF16 ? (bfcall) : (fcall))
@@ -808,7 +833,7 @@ static bm_status do_send(bm_ctx& c, const bm_op& o) {
   cudaStream_t cs = c.comm_st[o.peer];
   if (!c.producer_ev) {
     c.producer_ev = next_event(c);
-    BM_CUDA_TRY(cudaEventRecord(c.producer_ev, c.st));
+    BM_CUDA_TRY(cudaEventRecord(c.producer_ev, c.producer_st ? c.producer_st : c.st));
   }
   BM_CUDA_TRY(cudaStreamWaitEvent(cs, c.producer_ev, 0));
   const uint32_t base = (uint32_t)(c.step * ch.nmsg);
@@ -843,19 +868,19 @@ static bm_status do_send(bm_ctx& c, const bm_op& o) {
   return BM_OK;
 }
 
-static bm_status do_recv_wait(bm_ctx& c, const bm_op& o) {
+static bm_status do_recv_wait(bm_ctx& c, const bm_op& o, cudaStream_t on) {
   const Chan& ch = c.chans[c.chan_idx.at(std::make_tuple(o.peer, c.rank, o.payload))];
   const uint32_t base = (uint32_t)(c.step * ch.nmsg);
-  CUresult r = drv().wait32((CUstream)c.st, (CUdeviceptr)(c.comm + ch.flag_off), base + (uint32_t)o.seq + 1,
+  CUresult r = drv().wait32((CUstream)on, (CUdeviceptr)(c.comm + ch.flag_off), base + (uint32_t)o.seq + 1,
                             CU_STREAM_WAIT_VALUE_GEQ);
   if (r != CUDA_SUCCESS) { set_error("cuStreamWaitValue32 (data) failed " + std::to_string((int)r)); return BM_E_CUDA; }
   return BM_OK;
 }
 
-static bm_status do_release(bm_ctx& c, const bm_op& o) {
+static bm_status do_release(bm_ctx& c, const bm_op& o, cudaStream_t on) {
   const Chan& ch = c.chans[c.chan_idx.at(std::make_tuple(o.peer, c.rank, o.payload))];
   const uint32_t base = (uint32_t)(c.step * ch.nmsg);
-  CUresult r = drv().write32((CUstream)c.st, (CUdeviceptr)(c.peer[o.peer] + ch.credit_off), base + (uint32_t)o.seq + 1, 0);
+  CUresult r = drv().write32((CUstream)on, (CUdeviceptr)(c.peer[o.peer] + ch.credit_off), base + (uint32_t)o.seq + 1, 0);
   if (r != CUDA_SUCCESS) { set_error("cuStreamWriteValue32 (credit) failed " + std::to_string((int)r)); return BM_E_CUDA; }
   return BM_OK;
 }
@@ -936,6 +961,13 @@ bm_status bm_ctx_create(const bm_model_cfg* mc, const bm_schedule* s, int32_t ra
       while (ops[j].kind != BM_OP_GEN_BWD) ++j;
     c->release_of[j].push_back((int)i);
   }
+  c->consumer_kind.assign(ops.size(), -1);
+  for (size_t i = 0; i < ops.size(); ++i) {
+    size_t j = i;
+    while (j < ops.size() && ops[j].kind > BM_OP_GEN_BWD) ++j;
+    c->consumer_kind[i] = j < ops.size() ? ops[j].kind : -1;
+  }
+  c->use_gen_stream = c->P > 1 && s->cfg.gen_place == BM_GEN_DP_SHARD;
   *out = c;
   return BM_OK;
 }
@@ -969,6 +1001,13 @@ bm_status bm_ctx_bind(bm_ctx* c, const bm_buffers* b) {
     for (int i = 0; i < 2; ++i) {
       BM_CUDA_TRY(cudaEventCreateWithFlags(&c->bout_ev[i], cudaEventDisableTiming));
       BM_CUDA_TRY(cudaEventCreateWithFlags(&c->gout_ev[i], cudaEventDisableTiming));
+    }
+    if (c->use_gen_stream) {
+      int least = 0, greatest = 0;
+      BM_CUDA_TRY(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+      BM_CUDA_TRY(cudaStreamCreateWithPriority(&c->gen_st, cudaStreamNonBlocking, greatest));
+      BM_CUDA_TRY(cudaEventCreateWithFlags(&c->hn_ev, cudaEventDisableTiming));
+      BM_CUDA_TRY(cudaEventCreateWithFlags(&c->gen_done_ev, cudaEventDisableTiming));
     }
   }
   if (!drv().wait32 || !drv().write32) {
@@ -1104,7 +1143,10 @@ bm_status bm_step(bm_ctx* c, const bm_batch* b, void* stream) {
     BM_CUDA_TRY(cudaEventRecord(e, x.st));
     for (int r = 0; r < x.P; ++r)
       if (r != x.rank) BM_CUDA_TRY(cudaStreamWaitEvent(x.comm_st[r], e, 0));
+    if (x.use_gen_stream) BM_CUDA_TRY(cudaStreamWaitEvent(x.gen_st, e, 0));
   }
+  x.gen_done_pending = false;
+  cudaStream_t main_st = x.st;
   // ---- the opcode stream
   const auto& ops = x.s->ranks[x.rank];
   RecvState rs;
@@ -1117,10 +1159,12 @@ bm_status bm_step(bm_ctx* c, const bm_batch* b, void* stream) {
   for (size_t i = 0; i < ops.size(); ++i) {
     const bm_op& o = ops[i];
     switch (o.kind) {
-      case BM_OP_RECV:
-        BM_TRY(do_recv_wait(x, o));
+      case BM_OP_RECV: {
+        const bool on_gen = x.use_gen_stream && x.consumer_kind[i] == BM_OP_GEN_FWD;
+        BM_TRY(do_recv_wait(x, o, on_gen ? x.gen_st : main_st));
         rs.ops.push_back(&o);
         continue;
+      }
       case BM_OP_SEND:
         BM_TRY(do_send(x, o));
         continue;
@@ -1128,10 +1172,25 @@ bm_status bm_step(bm_ctx* c, const bm_batch* b, void* stream) {
         break;
     }
     x.producer_ev = nullptr;
+    const bool gen_op = o.kind == BM_OP_GEN_FWD || o.kind == BM_OP_GEN_BWD;
+    cudaStream_t op_st = (gen_op && x.use_gen_stream) ? x.gen_st : main_st;
+    if (!gen_op && x.gen_done_pending && o.kind == BM_OP_LLM_BWD && o.chunk == x.V - 1 && x.rank == x.P - 1) {
+      // the last stage's backward consumes the generator-input gradients (own shard added in place)
+      BM_CUDA_TRY(cudaStreamWaitEvent(main_st, x.gen_done_ev, 0));
+      x.gen_done_pending = false;
+    }
+    if (gen_op && x.use_gen_stream && o.kind == BM_OP_GEN_FWD && x.rank == x.P - 1)
+      BM_CUDA_TRY(cudaStreamWaitEvent(x.gen_st, x.hn_ev, 0));   // Hn of F(m, V-1)
+    x.st = op_st;
+    x.producer_st = op_st;
     switch (o.kind) {
       case BM_OP_ENC_FWD: BM_TRY(op_enc_fwd(x, o)); live_enc += enc_unit_bytes; break;
       case BM_OP_ENC_BWD: BM_TRY(op_enc_bwd(x, o, rs)); live_enc -= enc_unit_bytes; break;
-      case BM_OP_LLM_FWD: BM_TRY(op_llm_fwd(x, o, rs)); live_llm += llm_unit_bytes; break;
+      case BM_OP_LLM_FWD:
+        BM_TRY(op_llm_fwd(x, o, rs));
+        live_llm += llm_unit_bytes;
+        if (x.use_gen_stream && o.chunk == x.V - 1 && x.rank == x.P - 1) BM_CUDA_TRY(cudaEventRecord(x.hn_ev, main_st));
+        break;
       case BM_OP_LLM_BWD: BM_TRY(op_llm_bwd(x, o, rs)); live_llm -= llm_unit_bytes; break;
       case BM_OP_GEN_FWD:
         gen_x = (x.rank == x.P - 1) ? nullptr : (rs.ops.empty() ? nullptr : recv_slot(x, x.P - 1, BM_PAY_GENIN, rs.ops[0]->seq));
@@ -1142,6 +1201,10 @@ bm_status bm_step(bm_ctx* c, const bm_batch* b, void* stream) {
         const char* X = (x.rank == x.P - 1) ? x.genin_src[x.rank] : gen_x;
         BM_TRY(op_gen_bwd(x, o, X));
         live_gen -= gen_unit_bytes;
+        if (x.use_gen_stream && x.rank == x.P - 1) {
+          BM_CUDA_TRY(cudaEventRecord(x.gen_done_ev, x.gen_st));
+          x.gen_done_pending = true;
+        }
         break;
       }
       default:
@@ -1152,8 +1215,15 @@ bm_status bm_step(bm_ctx* c, const bm_batch* b, void* stream) {
     x.stash_peak[1] = std::max(x.stash_peak[1], live_llm);
     x.stash_peak[2] = std::max(x.stash_peak[2], live_gen);
     rs.ops.clear();
-    for (int ri : x.release_of[i]) BM_TRY(do_release(x, ops[ri]));
+    for (int ri : x.release_of[i]) BM_TRY(do_release(x, ops[ri], op_st));
+    x.st = main_st;
   }
+  if (x.use_gen_stream) {
+    cudaEvent_t e = next_event(x);
+    BM_CUDA_TRY(cudaEventRecord(e, x.gen_st));
+    BM_CUDA_TRY(cudaStreamWaitEvent(main_st, e, 0));
+  }
+  x.producer_st = nullptr;
   // join the comm streams back into the compute stream
   for (int r = 0; r < x.P; ++r) {
     if (r == x.rank) continue;
@@ -1209,6 +1279,15 @@ bm_status bm_ctx_gemm_stats(bm_ctx* c, int64_t* n_gemm, double* flops, double* m
   BM_CHECK_ARG(c && n_gemm && flops && ms, "null argument");
   BM_TRY(harvest(*c, 0));
   BM_TRY(harvest(*c, 1));
+  if (getenv("BM_GEMM_LOG")) {
+    for (auto& kv : c->shape_ms) {
+      const auto& k = kv.first;
+      const double fl = 2.0 * k[0] * k[1] * k[2] * kv.second.first;
+      fprintf(stderr, "GEMM M=%d N=%d K=%d epi=%d n=%lld ms=%.3f tflops=%.1f\n", k[0], k[1], k[2], k[3],
+              (long long)kv.second.first, kv.second.second, fl / (kv.second.second / 1e3) / 1e12);
+    }
+    c->shape_ms.clear();
+  }
   *n_gemm = c->gemm_count;
   *flops = c->gemm_flops;
   *ms = c->gemm_ms;

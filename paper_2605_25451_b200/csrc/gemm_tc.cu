@@ -18,6 +18,7 @@
 // A and B may each be K-major or MN-major; the UMMA smem descriptors and the
 // instruction descriptor's major bits express the transpose, so forward,
 // dgrad and wgrad need no transposed copies.
+#include <cstring>
 #include <unordered_map>
 #include <mutex>
 #include <vector>
@@ -32,13 +33,18 @@ constexpr int BM = 128;
 constexpr int BK = 64;                  // 64 bf16 = 128 B = one swizzle row
 constexpr int NUM_THREADS = 192;
 
+// epilogue staging: per epilogue warp 2 slots of EPI_SLOT bytes (one 32x32
+// output sub-tile per output tensor, 128B/64B-swizzled for the TMA store)
+constexpr int EPI_WARPS = 4;
 template <int BN> struct Cfg {
   static constexpr int A_BYTES = BM * BK * 2;          // 16 KB
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int STAGES = (BN == 256) ? 4 : (BN == 128 ? 6 : 8);
   static constexpr int TMEM_COLS = 2 * BN;             // double-buffered accumulators
-  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int EPI_SLOT = 4096;
+  static constexpr int EPI_BYTES = EPI_WARPS * 2 * EPI_SLOT;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + EPI_BYTES + 1024 /*align*/ + 256 /*barriers*/;
 };
 
 struct EpiArgs {
@@ -51,6 +57,7 @@ struct EpiArgs {
   int64_t ldr;
   float alpha;
   int f;           // SwiGLU width (BM_EPI_SWIGLU / BM_EPI_DSWIGLU)
+  int tma;         // outputs written by TMA stores from swizzled smem staging
 };
 
 // ---------------------------------------------------------------- PTX helpers
@@ -114,6 +121,24 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                : "memory");
 }
+
+// ---- TMA stores (epilogue)
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, uint32_t src, int c0, int c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(src), "r"(c0), "r"(c1)
+               : "memory");
+}
+__device__ __forceinline__ void tma_reduce_add_2d(const CUtensorMap* map, uint32_t src, int c0, int c1) {
+  asm volatile("cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(src), "r"(c0), "r"(c1)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
 // ---- CTA-pair (cta_group::2) helpers
 __device__ __forceinline__ uint32_t cluster_rank() {
@@ -211,7 +236,147 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+
+// ---------------------------------------------------------------- TMA epilogue
+// One epilogue warp owns 32 rows of the tile.  For each 32-column chunk it
+// writes its outputs into a swizzled 32x32 staging sub-tile (64B rows for bf16
+// with SWIZZLE_64B, 128B rows for fp32 with SWIZZLE_128B) and one lane issues
+// the TMA store (or, for fp32 weight gradients, a TMA reduce-add into global).
+// Two staging slots per warp; a slot is reused only after its previous bulk
+// group has been read (cp.async.bulk.wait_group.read 1).
+__device__ __forceinline__ void stage_bf16(uint32_t buf, int lane, const float* w) {
+  const uint32_t row = buf + lane * 64;
+  const int sw = (lane >> 1) & 3;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    uint32_t p[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      __nv_bfloat162 h2 = __floats2bfloat162_rn(w[8 * j + 2 * q], w[8 * j + 2 * q + 1]);
+      p[q] = *reinterpret_cast<uint32_t*>(&h2);
+    }
+    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(row + ((j ^ sw) << 4)), "r"(p[0]), "r"(p[1]),
+                 "r"(p[2]), "r"(p[3])
+                 : "memory");
+  }
+}
+__device__ __forceinline__ void stage_f32(uint32_t buf, int lane, const float* w) {
+  const uint32_t row = buf + lane * 128;
+  const int sw = lane & 7;
+#pragma unroll
+  for (int j = 0; j < 8; ++j)
+    asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(row + ((j ^ sw) << 4)), "f"(w[4 * j]),
+                 "f"(w[4 * j + 1]), "f"(w[4 * j + 2]), "f"(w[4 * j + 3])
+                 : "memory");
+}
 __device__ __forceinline__ float sigmoidf_(float x) { return 1.f / (1.f + __expf(-x)); }
+
+// outputs for one 32-column chunk of a plain / accumulate / residual / dswiglu epilogue
+__device__ __forceinline__ void epi_chunk_tma(const EpiArgs& a, const CUtensorMap* tmC, uint32_t slot, int lane,
+                                              int row0, int col0, const float* v) {
+  const int row = row0 + lane;
+  const bool rv = row < a.M;
+  float w[32];
+  if (a.epi == BM_EPI_DSWIGLU) {
+    // v = dh; g, u from R = gu [.., 2f]; outputs dg -> cols [col0..], du -> cols [f + col0..]
+    float wu[32];
+    const bf16* gu = reinterpret_cast<const bf16*>(a.R) + (int64_t)row * a.ldr;
+    const bool full = rv && col0 + 32 <= a.N;
+#pragma unroll
+    for (int j = 0; j < 32; j += 8) {
+      float g[8], u[8];
+      if (full) {
+        uint4 gv = *reinterpret_cast<const uint4*>(gu + col0 + j);
+        uint4 uv = *reinterpret_cast<const uint4*>(gu + a.f + col0 + j);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          g[q] = __bfloat162float(reinterpret_cast<const bf16*>(&gv)[q]);
+          u[q] = __bfloat162float(reinterpret_cast<const bf16*>(&uv)[q]);
+        }
+      } else {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const bool ok = rv && col0 + j + q < a.N;
+          g[q] = ok ? __bfloat162float(gu[col0 + j + q]) : 0.f;
+          u[q] = ok ? __bfloat162float(gu[a.f + col0 + j + q]) : 0.f;
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const float d = a.alpha * v[j + q], sg = sigmoidf_(g[q]);
+        w[j + q] = d * u[q] * sg * (1.f + g[q] * (1.f - sg));
+        wu[j + q] = d * g[q] * sg;
+      }
+    }
+    stage_bf16(slot, lane, w);
+    stage_bf16(slot + 2048, lane, wu);
+    fence_async_smem();
+    __syncwarp();
+    if (lane == 0) {
+      tma_store_2d(tmC, slot, col0, row0);
+      tma_store_2d(tmC, slot + 2048, a.f + col0, row0);
+      bulk_commit();
+    }
+    return;
+  }
+#pragma unroll
+  for (int j = 0; j < 32; ++j) w[j] = a.alpha * v[j];
+  if (a.epi == BM_EPI_ADD) {
+    if (a.c_f32) {
+      const float* r = reinterpret_cast<const float*>(a.R) + (int64_t)row * a.ldr + col0;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) w[j] += (rv && col0 + j < a.N) ? r[j] : 0.f;
+    } else {
+      const bf16* r = reinterpret_cast<const bf16*>(a.R) + (int64_t)row * a.ldr + col0;
+      if (rv && col0 + 32 <= a.N) {
+#pragma unroll
+        for (int j = 0; j < 32; j += 8) {
+          uint4 q4 = *reinterpret_cast<const uint4*>(r + j);
+#pragma unroll
+          for (int q = 0; q < 8; ++q) w[j + q] += __bfloat162float(reinterpret_cast<const bf16*>(&q4)[q]);
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) w[j] += (rv && col0 + j < a.N) ? __bfloat162float(r[j]) : 0.f;
+      }
+    }
+  }
+  if (a.c_f32) stage_f32(slot, lane, w);
+  else stage_bf16(slot, lane, w);
+  fence_async_smem();
+  __syncwarp();
+  if (lane == 0) {
+    if (a.epi == BM_EPI_ACCUM) tma_reduce_add_2d(tmC, slot, col0, row0);
+    else tma_store_2d(tmC, slot, col0, row0);
+    bulk_commit();
+  }
+}
+
+// gate/up pair chunk with fused SwiGLU: g -> gu[:, j0..], u -> gu[:, f + j0..], h -> h[:, j0..]
+__device__ __forceinline__ void epi_swiglu_tma(const EpiArgs& a, const CUtensorMap* tmGU, const CUtensorMap* tmH,
+                                               uint32_t slot, int lane, int row0, int j0, const float* vg,
+                                               const float* vu) {
+  float g[32], u[32], h[32];
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    const float gr = __bfloat162float(__float2bfloat16_rn(a.alpha * vg[j]));
+    const float ur = __bfloat162float(__float2bfloat16_rn(a.alpha * vu[j]));
+    g[j] = gr;
+    u[j] = ur;
+    h[j] = gr * sigmoidf_(gr) * ur;
+  }
+  stage_bf16(slot, lane, g);
+  stage_bf16(slot + 2048, lane, u);
+  stage_bf16(slot + 4096, lane, h);
+  fence_async_smem();
+  __syncwarp();
+  if (lane == 0) {
+    tma_store_2d(tmGU, slot, j0, row0);
+    tma_store_2d(tmGU, slot + 2048, a.f + j0, row0);
+    tma_store_2d(tmH, slot + 4096, j0, row0);
+    bulk_commit();
+  }
+}
 
 __device__ __forceinline__ void epilogue_row(const EpiArgs& a, int row, int col0, const float* v) {
   // one thread writes up to 32 consecutive columns of one row
@@ -243,11 +408,14 @@ __device__ __forceinline__ void epilogue_row(const EpiArgs& a, int row, int col0
         *reinterpret_cast<uint4*>(dgu + a.f + col0 + j) = ou;
       }
     } else {
-      for (int j = 0; j < ncols; ++j) {
-        const float g = __bfloat162float(gu[col0 + j]), u = __bfloat162float(gu[a.f + col0 + j]), d = alpha * v[j];
-        const float sg = sigmoidf_(g);
-        dgu[col0 + j] = __float2bfloat16_rn(d * u * sg * (1.f + g * (1.f - sg)));
-        dgu[a.f + col0 + j] = __float2bfloat16_rn(d * g * sg);
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        if (j < ncols) {
+          const float g = __bfloat162float(gu[col0 + j]), u = __bfloat162float(gu[a.f + col0 + j]), d = alpha * v[j];
+          const float sg = sigmoidf_(g);
+          dgu[col0 + j] = __float2bfloat16_rn(d * u * sg * (1.f + g * (1.f - sg)));
+          dgu[a.f + col0 + j] = __float2bfloat16_rn(d * g * sg);
+        }
       }
     }
     return;
@@ -264,7 +432,9 @@ __device__ __forceinline__ void epilogue_row(const EpiArgs& a, int row, int col0
           *reinterpret_cast<float4*>(c + j) = o;
         }
       } else {
-        for (int j = 0; j < ncols; ++j) c[j] += alpha * v[j];
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          if (j < ncols) c[j] += alpha * v[j];
       }
     } else {
       const float* r = (a.epi == BM_EPI_ADD) ? reinterpret_cast<const float*>(a.R) + (int64_t)row * a.ldr + col0 : nullptr;
@@ -279,7 +449,9 @@ __device__ __forceinline__ void epilogue_row(const EpiArgs& a, int row, int col0
           *reinterpret_cast<float4*>(c + j) = o;
         }
       } else {
-        for (int j = 0; j < ncols; ++j) c[j] = alpha * v[j] + (r ? r[j] : 0.f);
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          if (j < ncols) c[j] = alpha * v[j] + (r ? r[j] : 0.f);
       }
     }
   } else {
@@ -306,9 +478,12 @@ __device__ __forceinline__ void epilogue_row(const EpiArgs& a, int row, int col0
         *reinterpret_cast<uint4*>(c + j) = ov;
       }
     } else {
-      for (int j = 0; j < ncols; ++j) {
-        float w = alpha * v[j] + (r ? __bfloat162float(r[j]) : 0.f);
-        c[j] = __float2bfloat16_rn(w);
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        if (j < ncols) {
+          float w = alpha * v[j] + (r ? __bfloat162float(r[j]) : 0.f);
+          c[j] = __float2bfloat16_rn(w);
+        }
       }
     }
   }
@@ -343,26 +518,31 @@ __device__ __forceinline__ void epilogue_swiglu(const EpiArgs& a, int row, int j
       *reinterpret_cast<uint4*>(h + j0 + j) = oh;
     }
   } else {
-    for (int j = 0; j < n; ++j) {
-      const bf16 gb = __float2bfloat16_rn(a.alpha * vg[j]), ub = __float2bfloat16_rn(a.alpha * vu[j]);
-      gu[j0 + j] = gb;
-      gu[a.f + j0 + j] = ub;
-      const float gr = __bfloat162float(gb), ur = __bfloat162float(ub);
-      h[j0 + j] = __float2bfloat16_rn(gr * sigmoidf_(gr) * ur);
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      if (j < n) {
+        const bf16 gb = __float2bfloat16_rn(a.alpha * vg[j]), ub = __float2bfloat16_rn(a.alpha * vu[j]);
+        gu[j0 + j] = gb;
+        gu[a.f + j0 + j] = ub;
+        const float gr = __bfloat162float(gb), ur = __bfloat162float(ub);
+        h[j0 + j] = __float2bfloat16_rn(gr * sigmoidf_(gr) * ur);
+      }
     }
   }
 }
 
 template <int BN, bool A_MN, bool B_MN>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
-gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, EpiArgs args) {
+gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+            const __grid_constant__ CUtensorMap tmC, EpiArgs args) {
   using C = Cfg<BN>;
   constexpr int STAGES = C::STAGES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* smA = smem;
   uint8_t* smB = smem + STAGES * C::A_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * C::STAGE_BYTES);
+  uint8_t* smE = smem + STAGES * C::STAGE_BYTES;  // epilogue staging
+  uint64_t* full = reinterpret_cast<uint64_t*>(smE + C::EPI_BYTES);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
@@ -462,6 +642,8 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
   } else {
     // ---------------- epilogue warps 2..5 (TMEM lane quadrant = warp % 4)
     const int quad = warp & 3;
+    const uint32_t ebase = smem_u32(smE) + (uint32_t)((warp - 2) * 2 * C::EPI_SLOT);
+    int eiter = 0;
     int local = 0;
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++local) {
       int mb, nb;
@@ -470,18 +652,32 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
       const uint32_t acc_phase = (local >> 1) & 1;
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      const int row = mb * BM + quad * 32 + lane;
+      const int row0 = mb * BM + quad * 32;
+      const int row = row0 + lane;
       const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + acc * BN;
 #pragma unroll 1
       for (int c = 0; c < BN; c += 32) {
         float v[32];
         tmem_ld32(taddr + c, v);
-        if (row < args.M) epilogue_row(args, row, nb * BN + c, v);
+        if (args.tma) {
+          if (nb * BN + c < args.N) {
+            const uint32_t slot = ebase + (eiter & 1) * C::EPI_SLOT;
+            if (eiter >= 2) {
+              if (lane == 0) bulk_wait_read1();
+              __syncwarp();
+            }
+            epi_chunk_tma(args, &tmC, slot, lane, row0, nb * BN + c, v);
+            ++eiter;
+          }
+        } else if (row < args.M) {
+          epilogue_row(args, row, nb * BN + c, v);
+        }
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);
     }
+    if (lane == 0) bulk_wait_all();
   }
   tc_fence_before();
   __syncthreads();
@@ -504,26 +700,30 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
 // leader's tmem_empty barrier.  Per CTA and K-block this moves
 // (128 + BN/2)*64*2 bytes instead of (128 + BN)*64*2.
 // ============================================================================
-template <int BN> struct Cfg2 {
+template <int BN, bool SWI = false> struct Cfg2 {
   static constexpr int A_BYTES = 128 * BK * 2;                 // 16 KB
   static constexpr int B_BYTES = (BN / 2) * BK * 2;            // 16 KB (BN = 256)
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES = (BN == 256) ? 6 : 8;
+  static constexpr int STAGES = SWI ? 5 : ((BN == 256) ? 6 : 8);
   static constexpr int TMEM_COLS = 2 * BN;
-  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
+  static constexpr int EPI_SLOT = SWI ? 6144 : 4096;
+  static constexpr int EPI_BYTES = EPI_WARPS * 2 * EPI_SLOT;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + EPI_BYTES + 1024 + 256;
 };
 
 template <int BN, bool A_MN, bool B_MN, bool SWIGLU>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
-gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, EpiArgs args) {
-  using C = Cfg2<BN>;
+gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+             const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmC2, EpiArgs args) {
+  using C = Cfg2<BN, SWIGLU>;
   constexpr int STAGES = C::STAGES;
   constexpr int BNH = BN / 2;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* smA = smem;
   uint8_t* smB = smem + STAGES * C::A_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * C::STAGE_BYTES);
+  uint8_t* smE = smem + STAGES * C::STAGE_BYTES;  // epilogue staging
+  uint64_t* full = reinterpret_cast<uint64_t*>(smE + C::EPI_BYTES);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
@@ -625,6 +825,8 @@ gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
     }
   } else {
     const int quad = warp & 3;
+    const uint32_t ebase = smem_u32(smE) + (uint32_t)((warp - 2) * 2 * C::EPI_SLOT);
+    int eiter = 0;
     const uint32_t leader_tempty0 = mapa(smem_u32(&tempty[0]), 0);
     const uint32_t leader_tempty1 = mapa(smem_u32(&tempty[1]), 0);
     int local = 0;
@@ -635,7 +837,8 @@ gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
       const uint32_t acc_phase = (local >> 1) & 1;
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      const int row = mb * 2 * BM + (int)cta * BM + quad * 32 + lane;
+      const int row0 = mb * 2 * BM + (int)cta * BM + quad * 32;
+      const int row = row0 + lane;
       const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + acc * BN;
       if (SWIGLU) {
 #pragma unroll 1
@@ -643,20 +846,45 @@ gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
           float vg[32], vu[32];
           tmem_ld32(taddr + c, vg);
           tmem_ld32(taddr + BNH + c, vu);
-          if (row < args.M) epilogue_swiglu(args, row, nb * BNH + c, vg, vu);
+          if (args.tma) {
+            if (nb * BNH + c < args.f) {
+              const uint32_t slot = ebase + (eiter & 1) * C::EPI_SLOT;
+              if (eiter >= 2) {
+                if (lane == 0) bulk_wait_read1();
+                __syncwarp();
+              }
+              epi_swiglu_tma(args, &tmC, &tmC2, slot, lane, row0, nb * BNH + c, vg, vu);
+              ++eiter;
+            }
+          } else if (row < args.M) {
+            epilogue_swiglu(args, row, nb * BNH + c, vg, vu);
+          }
         }
       } else {
 #pragma unroll 1
         for (int c = 0; c < BN; c += 32) {
           float v[32];
           tmem_ld32(taddr + c, v);
-          if (row < args.M) epilogue_row(args, row, nb * BN + c, v);
+          if (args.tma) {
+            if (nb * BN + c < args.N) {
+              const uint32_t slot = ebase + (eiter & 1) * C::EPI_SLOT;
+              if (eiter >= 2) {
+                if (lane == 0) bulk_wait_read1();
+                __syncwarp();
+              }
+              epi_chunk_tma(args, &tmC, slot, lane, row0, nb * BN + c, v);
+              ++eiter;
+            }
+          } else if (row < args.M) {
+            epilogue_row(args, row, nb * BN + c, v);
+          }
         }
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(acc ? leader_tempty1 : leader_tempty0);
     }
+    if (lane == 0) bulk_wait_all();
   }
   tc_fence_before();
   __syncthreads();
@@ -690,8 +918,10 @@ struct MapKey {
   const void* p;
   uint64_t inner, outer, stride;
   uint32_t box_outer;
+  int kind;  // 0: bf16 operand (64 x box_outer, SW128); 1: bf16 output (32x32, SW64); 2: fp32 output (32x32, SW128)
   bool operator==(const MapKey& o) const {
-    return p == o.p && inner == o.inner && outer == o.outer && stride == o.stride && box_outer == o.box_outer;
+    return p == o.p && inner == o.inner && outer == o.outer && stride == o.stride && box_outer == o.box_outer &&
+           kind == o.kind;
   }
 };
 struct MapKeyHash {
@@ -701,6 +931,7 @@ struct MapKeyHash {
     h = h * 1000003u ^ k.outer;
     h = h * 1000003u ^ k.stride;
     h = h * 1000003u ^ k.box_outer;
+    h = h * 1000003u ^ (size_t)k.kind;
     return h;
   }
 };
@@ -708,10 +939,13 @@ struct MapKeyHash {
 static std::mutex g_map_mu;
 static std::unordered_map<MapKey, CUtensorMap, MapKeyHash> g_maps;
 
-// 2D bf16 tensor [outer][inner] with row stride `ld` elements; box = 64 x box_outer.
-static bm_status make_map(const void* p, uint64_t inner, uint64_t outer, uint64_t ld, uint32_t box_outer,
-                          CUtensorMap* out) {
-  MapKey key{p, inner, outer, ld, box_outer};
+// 2D tensor [outer][inner] with row stride `ld` elements.
+//   kind 0: bf16 operand, box = 64 x box_outer, 128B swizzle (UMMA smem layout)
+//   kind 1: bf16 epilogue output, box = 32 x 32, 64B swizzle (staging layout)
+//   kind 2: fp32 epilogue output, box = 32 x 32, 128B swizzle
+static bm_status make_map_k(const void* p, uint64_t inner, uint64_t outer, uint64_t ld, uint32_t box_outer, int kind,
+                            CUtensorMap* out) {
+  MapKey key{p, inner, outer, ld, box_outer, kind};
   {
     std::lock_guard<std::mutex> g(g_map_mu);
     auto it = g_maps.find(key);
@@ -725,16 +959,18 @@ static bm_status make_map(const void* p, uint64_t inner, uint64_t outer, uint64_
     set_error("cuTensorMapEncodeTiled unavailable");
     return BM_E_CUDA;
   }
+  const uint64_t es = kind == 2 ? 4 : 2;
   cuuint64_t dims[2] = {inner, outer};
-  cuuint64_t strides[1] = {ld * 2};
-  cuuint32_t box[2] = {64, box_outer};
+  cuuint64_t strides[1] = {ld * es};
+  cuuint32_t box[2] = {kind == 0 ? 64u : 32u, kind == 0 ? box_outer : 32u};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = enc(out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(p), dims, strides, box, estr,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  const CUtensorMapDataType dt = kind == 2 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+  const CUtensorMapSwizzle sw = kind == 1 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B;
+  CUresult r = enc(out, dt, 2, const_cast<void*>(p), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     set_error("cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ") inner=" + std::to_string(inner) +
-              " outer=" + std::to_string(outer) + " ld=" + std::to_string(ld));
+              " outer=" + std::to_string(outer) + " ld=" + std::to_string(ld) + " kind=" + std::to_string(kind));
     return BM_E_CUDA;
   }
   std::lock_guard<std::mutex> g(g_map_mu);
@@ -742,9 +978,18 @@ static bm_status make_map(const void* p, uint64_t inner, uint64_t outer, uint64_
   g_maps.emplace(key, *out);
   return BM_OK;
 }
+static bm_status make_map(const void* p, uint64_t inner, uint64_t outer, uint64_t ld, uint32_t box_outer,
+                          CUtensorMap* out) {
+  return make_map_k(p, inner, outer, ld, box_outer, 0, out);
+}
+// output map usable by the TMA epilogue? (16-byte aligned base and row stride)
+static bool tma_out_ok(const void* p, int64_t ld, int es) {
+  return (reinterpret_cast<uintptr_t>(p) & 15) == 0 && (ld * es) % 16 == 0;
+}
 
 template <int BN, bool A_MN, bool B_MN>
-static bm_status launch(const CUtensorMap& ma, const CUtensorMap& mb, const EpiArgs& ea, cudaStream_t st) {
+static bm_status launch(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc, const EpiArgs& ea,
+                        cudaStream_t st) {
   using C = Cfg<BN>;
   static bool attr_set = false;
   if (!attr_set) {
@@ -753,7 +998,7 @@ static bm_status launch(const CUtensorMap& ma, const CUtensorMap& mb, const EpiA
   }
   const int tiles = ceil_div(ea.M, BM) * ceil_div(ea.N, BN);
   const int grid = tiles < num_sms() ? tiles : num_sms();
-  gemm_kernel<BN, A_MN, B_MN><<<grid, NUM_THREADS, C::SMEM, st>>>(ma, mb, ea);
+  gemm_kernel<BN, A_MN, B_MN><<<grid, NUM_THREADS, C::SMEM, st>>>(ma, mb, mc, ea);
   count_launch();
   BM_CUDA_TRY(cudaGetLastError());
   return BM_OK;
@@ -761,17 +1006,18 @@ static bm_status launch(const CUtensorMap& ma, const CUtensorMap& mb, const EpiA
 
 template <int BN>
 static bm_status dispatch_majors(bool a_mn, bool b_mn, const CUtensorMap& ma, const CUtensorMap& mb,
-                                 const EpiArgs& ea, cudaStream_t st) {
-  if (!a_mn && !b_mn) return launch<BN, false, false>(ma, mb, ea, st);
-  if (!a_mn && b_mn) return launch<BN, false, true>(ma, mb, ea, st);
-  if (a_mn && b_mn) return launch<BN, true, true>(ma, mb, ea, st);
-  return launch<BN, true, false>(ma, mb, ea, st);
+                                 const CUtensorMap& mc, const EpiArgs& ea, cudaStream_t st) {
+  if (!a_mn && !b_mn) return launch<BN, false, false>(ma, mb, mc, ea, st);
+  if (!a_mn && b_mn) return launch<BN, false, true>(ma, mb, mc, ea, st);
+  if (a_mn && b_mn) return launch<BN, true, true>(ma, mb, mc, ea, st);
+  return launch<BN, true, false>(ma, mb, mc, ea, st);
 }
 
 
 template <int BN, bool A_MN, bool B_MN, bool SWIGLU = false>
-static bm_status launch2(const CUtensorMap& ma, const CUtensorMap& mb, const EpiArgs& ea, cudaStream_t st) {
-  using C = Cfg2<BN>;
+static bm_status launch2(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc, const CUtensorMap& mc2,
+                         const EpiArgs& ea, cudaStream_t st) {
+  using C = Cfg2<BN, SWIGLU>;
   static bool attr_set = false;
   if (!attr_set) {
     BM_CUDA_TRY(cudaFuncSetAttribute(gemm2_kernel<BN, A_MN, B_MN, SWIGLU>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -781,7 +1027,7 @@ static bm_status launch2(const CUtensorMap& ma, const CUtensorMap& mb, const Epi
   const int tiles = ceil_div(ea.M, 2 * BM) * (SWIGLU ? ceil_div(ea.f, BN / 2) : ceil_div(ea.N, BN));
   const int pairs = num_sms() / 2;
   const int grid = 2 * (tiles < pairs ? tiles : pairs);
-  gemm2_kernel<BN, A_MN, B_MN, SWIGLU><<<grid, NUM_THREADS, C::SMEM, st>>>(ma, mb, ea);
+  gemm2_kernel<BN, A_MN, B_MN, SWIGLU><<<grid, NUM_THREADS, C::SMEM, st>>>(ma, mb, mc, mc2, ea);
   count_launch();
   BM_CUDA_TRY(cudaGetLastError());
   return BM_OK;
@@ -789,11 +1035,11 @@ static bm_status launch2(const CUtensorMap& ma, const CUtensorMap& mb, const Epi
 
 template <int BN>
 static bm_status dispatch_majors2(bool a_mn, bool b_mn, const CUtensorMap& ma, const CUtensorMap& mb,
-                                  const EpiArgs& ea, cudaStream_t st) {
-  if (!a_mn && !b_mn) return launch2<BN, false, false>(ma, mb, ea, st);
-  if (!a_mn && b_mn) return launch2<BN, false, true>(ma, mb, ea, st);
-  if (a_mn && b_mn) return launch2<BN, true, true>(ma, mb, ea, st);
-  return launch2<BN, true, false>(ma, mb, ea, st);
+                                  const CUtensorMap& mc, const EpiArgs& ea, cudaStream_t st) {
+  if (!a_mn && !b_mn) return launch2<BN, false, false>(ma, mb, mc, mc, ea, st);
+  if (!a_mn && b_mn) return launch2<BN, false, true>(ma, mb, mc, mc, ea, st);
+  if (a_mn && b_mn) return launch2<BN, true, true>(ma, mb, mc, mc, ea, st);
+  return launch2<BN, true, false>(ma, mb, mc, mc, ea, st);
 }
 
 }  // namespace tc
@@ -814,39 +1060,61 @@ bm_status gemm_bf16_tc(int M, int N, int K, const void* A, int64_t lda, int a_ma
   BM_CHECK_ARG((reinterpret_cast<uintptr_t>(A) & 15) == 0 && (reinterpret_cast<uintptr_t>(B) & 15) == 0,
                "A/B must be 16-byte aligned");
   const bool amn = a_major != 0, bmn = b_major != 0;
-  EpiArgs ea{M, N, K, Cp, ldc, c_dtype == BM_F32 ? 1 : 0, epi, R, ldr, alpha, f};
-  CUtensorMap ma, mb;
+  EpiArgs ea{M, N, K, Cp, ldc, c_dtype == BM_F32 ? 1 : 0, epi, R, ldr, alpha, f, 0};
+  CUtensorMap ma, mb, mc, mc2;
+  std::memset(&mc, 0, sizeof(mc));
+  std::memset(&mc2, 0, sizeof(mc2));
+  const int ces = c_dtype == BM_F32 ? 4 : 2;
   if (epi == BM_EPI_SWIGLU) {
     // gate/up GEMM with fused SwiGLU: always CTA pairs, BN = 256 (128 gate + 128 up features)
     BM_CHECK_ARG(b_major == 0 && c_dtype == BM_BF16 && N == 2 * f && f % 128 == 0, "SWIGLU epilogue: K-major B, bf16, N = 2f, f % 128 == 0");
     if (a_major == 0) BM_TRY(make_map(A, K, M, lda, BM, &ma));
     else BM_TRY(make_map(A, M, K, lda, BK, &ma));
     BM_TRY(make_map(B, K, N, ldb, 128, &mb));
-    if (a_major == 0) return launch2<256, false, false, true>(ma, mb, ea, st);
-    return launch2<256, true, false, true>(ma, mb, ea, st);
+    if (tma_out_ok(Cp, ldc, 2) && tma_out_ok(R, ldr, 2)) {
+      BM_TRY(make_map_k(Cp, 2 * (uint64_t)f, M, ldc, 32, 1, &mc));
+      BM_TRY(make_map_k(R, (uint64_t)f, M, ldr, 32, 1, &mc2));
+      ea.tma = 1;
+    }
+    if (a_major == 0) return launch2<256, false, false, true>(ma, mb, mc, mc2, ea, st);
+    return launch2<256, true, false, true>(ma, mb, mc, mc2, ea, st);
   }
-  if (epi == BM_EPI_DSWIGLU)
+  if (epi == BM_EPI_DSWIGLU) {
     BM_CHECK_ARG(c_dtype == BM_BF16 && N == f && ldc >= 2 * f && ldr >= 2 * f, "DSWIGLU epilogue: bf16, N = f, C/R are [M, 2f]");
-  // CTA-pair kernel for the large contractions (the LLM's), 1-CTA otherwise
+    if (tma_out_ok(Cp, ldc, 2)) {
+      BM_TRY(make_map_k(Cp, 2 * (uint64_t)f, M, ldc, 32, 1, &mc));
+      ea.tma = 1;
+    }
+  } else if (tma_out_ok(Cp, ldc, ces)) {
+    BM_TRY(make_map_k(Cp, (uint64_t)N, M, ldc, 32, c_dtype == BM_F32 ? 2 : 1, &mc));
+    ea.tma = 1;
+  }
+  // CTA pairs for the large contractions (enough 256-row tiles to fill the
+  // machine), 1-CTA tiles otherwise
   const int mode = gemm_mode();
-  const bool pair = mode == 2 || (mode == 0 && M >= 512 && N >= 256 && K >= 256);
+  const int64_t pair_tiles = (int64_t)ceil_div(M, 2 * BM) * ceil_div(N, 256);
+  const bool pair = mode == 2 || (mode == 0 && M >= 256 && N >= 256 && K >= 256 && pair_tiles >= num_sms() / 2);
   if (pair) {
     const int BN2 = (N >= 256) ? 256 : 128;
     if (a_major == 0) BM_TRY(make_map(A, K, M, lda, BM, &ma));
     else BM_TRY(make_map(A, M, K, lda, BK, &ma));
     if (b_major == 0) BM_TRY(make_map(B, K, N, ldb, BN2 / 2, &mb));
     else BM_TRY(make_map(B, N, K, ldb, BK, &mb));
-    if (BN2 == 256) return dispatch_majors2<256>(amn, bmn, ma, mb, ea, st);
-    return dispatch_majors2<128>(amn, bmn, ma, mb, ea, st);
+    if (BN2 == 256) return dispatch_majors2<256>(amn, bmn, ma, mb, mc, ea, st);
+    return dispatch_majors2<128>(amn, bmn, ma, mb, mc, ea, st);
   }
-  const int BN = (N <= 64) ? 64 : (N <= 128 ? 128 : 256);
+  // 1-CTA tiles: the largest BN that still gives ~a full wave of CTAs (small
+  // encoder / generator contractions have only a few 128-row tiles)
+  int BN = (N <= 64) ? 64 : (N <= 128 ? 128 : 256);
+  const int tm = ceil_div(M, BM);
+  while (BN > 64 && (int64_t)tm * ceil_div(N, BN) < (3 * num_sms()) / 4) BN /= 2;
   if (a_major == 0) BM_TRY(make_map(A, K, M, lda, BM, &ma));
   else BM_TRY(make_map(A, M, K, lda, BK, &ma));
   if (b_major == 0) BM_TRY(make_map(B, K, N, ldb, BN, &mb));
   else BM_TRY(make_map(B, N, K, ldb, BK, &mb));
-  if (BN == 64) return dispatch_majors<64>(amn, bmn, ma, mb, ea, st);
-  if (BN == 128) return dispatch_majors<128>(amn, bmn, ma, mb, ea, st);
-  return dispatch_majors<256>(amn, bmn, ma, mb, ea, st);
+  if (BN == 64) return dispatch_majors<64>(amn, bmn, ma, mb, mc, ea, st);
+  if (BN == 128) return dispatch_majors<128>(amn, bmn, ma, mb, mc, ea, st);
+  return dispatch_majors<256>(amn, bmn, ma, mb, mc, ea, st);
 }
 
 }  // namespace bm

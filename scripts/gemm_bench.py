@@ -77,6 +77,39 @@ def main():
                    cublas_ms=tc, cublas_tflops=fl / tc / 1e9)
         print(json.dumps(row))
         out.append(row)
+    # fused SwiGLU epilogues vs GEMM + separate elementwise kernel (C2 LLM layer)
+    S, d, f = 4096, 2048, 8192
+    X = torch.randn((S, d), device="cuda").to(torch.bfloat16)
+    Wgu = (torch.randn((2 * f, d), device="cuda") * 0.02).to(torch.bfloat16)
+    Wd = (torch.randn((d, f), device="cuda") * 0.02).to(torch.bfloat16)
+    gu = torch.empty((S, 2 * f), device="cuda", dtype=torch.bfloat16)
+    h = torch.empty((S, f), device="cuda", dtype=torch.bfloat16)
+    dY = torch.randn((S, d), device="cuda").to(torch.bfloat16)
+    dh = torch.empty((S, f), device="cuda", dtype=torch.bfloat16)
+    dgu = torch.empty((S, 2 * f), device="cuda", dtype=torch.bfloat16)
+
+    def fused_fwd():
+        L.call("bm_k_gemm_swiglu", S, f, d, X.data_ptr(), d, Wgu.data_ptr(), d, gu.data_ptr(), h.data_ptr(), None)
+
+    def unfused_fwd():
+        L.call("bm_k_gemm", 0, S, 2 * f, d, X.data_ptr(), d, 0, Wgu.data_ptr(), d, 0, gu.data_ptr(), 2 * f, 0, 0, None, 0, 1.0, None)
+        L.call("bm_k_swiglu_fwd", 0, S, f, gu.data_ptr(), h.data_ptr(), None)
+
+    def fused_bwd():
+        L.call("bm_k_gemm_dswiglu", S, f, d, dY.data_ptr(), d, Wd.data_ptr(), f, gu.data_ptr(), dgu.data_ptr(), None)
+
+    def unfused_bwd():
+        L.call("bm_k_gemm", 0, S, f, d, dY.data_ptr(), d, 0, Wd.data_ptr(), f, 1, dh.data_ptr(), f, 0, 0, None, 0, 1.0, None)
+        L.call("bm_k_swiglu_bwd", 0, S, f, dh.data_ptr(), gu.data_ptr(), dgu.data_ptr(), None)
+
+    for name, fn, fl in [("gate_up+swiglu fused", fused_fwd, 2.0 * S * 2 * f * d),
+                         ("gate_up + swiglu kernel", unfused_fwd, 2.0 * S * 2 * f * d),
+                         ("down dgrad+dswiglu fused", fused_bwd, 2.0 * S * f * d),
+                         ("down dgrad + swiglu_bwd kernel", unfused_bwd, 2.0 * S * f * d)]:
+        t = bench(fn, flush=flush)
+        row = dict(name=name, ms=t, tflops=fl / t / 1e9)
+        print(json.dumps(row))
+        out.append(row)
     if "--json" in sys.argv:
         with open(sys.argv[sys.argv.index("--json") + 1], "w") as f:
             json.dump(out, f, indent=1)
