@@ -217,6 +217,7 @@ struct bm_ctx {
   MlpSlot gen;
   char *dwork[2] = {nullptr, nullptr}, *bout[2] = {nullptr, nullptr}, *dh = nullptr, *dgu = nullptr, *dxn = nullptr;
   float* part = nullptr;
+  float* part_gen = nullptr;  // RMSNorm-backward partials of the generator stream (no sharing across streams)
   char* embscr = nullptr;
   char* logits = nullptr;
   float* ce_scr = nullptr;
@@ -403,6 +404,7 @@ static void work_layout(bm_ctx& c, char* base) {
   c.dxn = b.take(S * d * es);
   const int wmax = std::max(std::max(m.d, m.d_e), m.d_g);
   c.part = (float*)b.take(rmsnorm_bwd_scratch_floats(std::max(S, (int64_t)m.max_n_mod), wmax) * 4);
+  c.part_gen = (float*)b.take(rmsnorm_bwd_scratch_floats(std::max(c.gen_rows, 1), m.d_g) * 4);
   c.embscr = b.take(embed_bwd_scratch_bytes(m.S));
   if (last_rank) {
     c.logits = b.take(S * m.vocab * es);
@@ -1183,6 +1185,8 @@ bm_status bm_step(bm_ctx* c, const bm_batch* b, void* stream) {
       BM_CUDA_TRY(cudaStreamWaitEvent(x.gen_st, x.hn_ev, 0));   // Hn of F(m, V-1)
     x.st = op_st;
     x.producer_st = op_st;
+    float* part_main = x.part;
+    if (op_st != main_st) x.part = x.part_gen;
     switch (o.kind) {
       case BM_OP_ENC_FWD: BM_TRY(op_enc_fwd(x, o)); live_enc += enc_unit_bytes; break;
       case BM_OP_ENC_BWD: BM_TRY(op_enc_bwd(x, o, rs)); live_enc -= enc_unit_bytes; break;
@@ -1217,6 +1221,7 @@ bm_status bm_step(bm_ctx* c, const bm_batch* b, void* stream) {
     rs.ops.clear();
     for (int ri : x.release_of[i]) BM_TRY(do_release(x, ops[ri], op_st));
     x.st = main_st;
+    x.part = part_main;
   }
   if (x.use_gen_stream) {
     cudaEvent_t e = next_event(x);
