@@ -218,6 +218,9 @@ struct bm_ctx {
   char *dwork[2] = {nullptr, nullptr}, *bout[2] = {nullptr, nullptr}, *dh = nullptr, *dgu = nullptr, *dxn = nullptr;
   float* part = nullptr;
   float* part_gen = nullptr;  // RMSNorm-backward partials of the generator stream (no sharing across streams)
+  char *ws = nullptr, *ws_gen = nullptr;  // split-K workspaces of the two compute streams
+  int64_t ws_bytes = 0;
+  void* cur_ws = nullptr;
   char* embscr = nullptr;
   char* logits = nullptr;
   float* ce_scr = nullptr;
@@ -405,6 +408,13 @@ static void work_layout(bm_ctx& c, char* base) {
   const int wmax = std::max(std::max(m.d, m.d_e), m.d_g);
   c.part = (float*)b.take(rmsnorm_bwd_scratch_floats(std::max(S, (int64_t)m.max_n_mod), wmax) * 4);
   c.part_gen = (float*)b.take(rmsnorm_bwd_scratch_floats(std::max(c.gen_rows, 1), m.d_g) * 4);
+  {
+    const int64_t rows = ((int64_t)std::max(m.max_n_mod, c.gen_rows) + 127) / 128 * 128;
+    const int64_t cols = std::max<int64_t>({m.d, m.d_e, m.f_e, m.d_g, m.f_g, m.d_in + 8});
+    c.ws_bytes = std::min<int64_t>(64ll << 20, 8 * rows * cols * 4);
+    c.ws = b.take(c.ws_bytes);
+    c.ws_gen = b.take(c.ws_bytes);
+  }
   c.embscr = b.take(embed_bwd_scratch_bytes(m.S));
   if (last_rank) {
     c.logits = b.take(S * m.vocab * es);
@@ -448,8 +458,9 @@ static inline int LD_(bm_ctx& c, const char* name) { return c.params[c.pidx.at(n
 static bm_status timed_gemm(bm_ctx& c, int M, int N, int K, const void* A, int64_t lda, int am, const void* B,
                             int64_t ldb, int bm_, void* C, int64_t ldc, int cdt, int epi, const void* R, int64_t ldr,
                             int f = 0) {
+  void* ws = c.cur_ws;
   if (!c.timing || M <= 0 || N <= 0 || K <= 0)
-    return gemm(c.dtype, M, N, K, A, lda, am, B, ldb, bm_, C, ldc, cdt, epi, R, ldr, 1.f, c.st, f);
+    return gemm(c.dtype, M, N, K, A, lda, am, B, ldb, bm_, C, ldc, cdt, epi, R, ldr, 1.f, c.st, f, ws, c.ws_bytes);
   const int pool = (int)(c.step & 1);
   auto& ev = c.tev[pool];
   if (c.tev_used[pool] + 2 > ev.size()) {
@@ -462,7 +473,7 @@ static bm_status timed_gemm(bm_ctx& c, int M, int N, int K, const void* A, int64
   cudaEvent_t e0 = ev[c.tev_used[pool]], e1 = ev[c.tev_used[pool] + 1];
   c.tev_used[pool] += 2;
   BM_CUDA_TRY(cudaEventRecord(e0, c.st));
-  BM_TRY(gemm(c.dtype, M, N, K, A, lda, am, B, ldb, bm_, C, ldc, cdt, epi, R, ldr, 1.f, c.st, f));
+  BM_TRY(gemm(c.dtype, M, N, K, A, lda, am, B, ldb, bm_, C, ldc, cdt, epi, R, ldr, 1.f, c.st, f, ws, c.ws_bytes));
   BM_CUDA_TRY(cudaEventRecord(e1, c.st));
   c.tflop_pending[pool] += 2.0 * M * N * K;
   c.gemm_count_pending[pool] += 1;
@@ -1187,6 +1198,7 @@ bm_status bm_step(bm_ctx* c, const bm_batch* b, void* stream) {
     x.producer_st = op_st;
     float* part_main = x.part;
     if (op_st != main_st) x.part = x.part_gen;
+    x.cur_ws = (op_st != main_st) ? x.ws_gen : x.ws;
     switch (o.kind) {
       case BM_OP_ENC_FWD: BM_TRY(op_enc_fwd(x, o)); live_enc += enc_unit_bytes; break;
       case BM_OP_ENC_BWD: BM_TRY(op_enc_bwd(x, o, rs)); live_enc -= enc_unit_bytes; break;

@@ -18,6 +18,7 @@
 // A and B may each be K-major or MN-major; the UMMA smem descriptors and the
 // instruction descriptor's major bits express the transpose, so forward,
 // dgrad and wgrad need no transposed copies.
+#include <algorithm>
 #include <cstring>
 #include <unordered_map>
 #include <mutex>
@@ -58,6 +59,9 @@ struct EpiArgs {
   float alpha;
   int f;           // SwiGLU width (BM_EPI_SWIGLU / BM_EPI_DSWIGLU)
   int tma;         // outputs written by TMA stores from swizzled smem staging
+  int splits;      // split-K factor (1-CTA kernel); > 1: fp32 partials to the workspace map
+  int kb_per;      // K blocks per split
+  int mpad;        // workspace rows per split (M rounded up to the tile height)
 };
 
 // ---------------------------------------------------------------- PTX helpers
@@ -552,8 +556,9 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
   const int lane = threadIdx.x % 32;
   const int tiles_m = (args.M + BM - 1) / BM;
   const int tiles_n = (args.N + BN - 1) / BN;
-  const int num_tiles = tiles_m * tiles_n;
-  const int nk = (args.K + BK - 1) / BK;
+  const int base_tiles = tiles_m * tiles_n;
+  const int num_tiles = base_tiles * args.splits;   // (split, tile) work items
+  const int nk_all = (args.K + BK - 1) / BK;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -585,9 +590,11 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
       uint32_t phase = 0;
       for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
         int mb, nb;
-        tile_coords(t, tiles_m, tiles_n, mb, nb);
+        const int sp = t / base_tiles;
+        tile_coords(t - sp * base_tiles, tiles_m, tiles_n, mb, nb);
         const int m0 = mb * BM, n0 = nb * BN;
-        for (int kb = 0; kb < nk; ++kb) {
+        const int kb_lo = sp * args.kb_per, kb_hi = min(nk_all, kb_lo + args.kb_per);
+        for (int kb = kb_lo; kb < kb_hi; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_expect_tx(&full[stage], C::STAGE_BYTES);
           uint8_t* a_dst = smA + stage * C::A_BYTES;
@@ -622,7 +629,9 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t tmem_d = tmem_base + acc * BN;
-        for (int kb = 0; kb < nk; ++kb) {
+        const int sp = t / base_tiles;
+        const int kb_lo = sp * args.kb_per, kb_hi = min(nk_all, kb_lo + args.kb_per);
+        for (int kb = kb_lo; kb < kb_hi; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const uint32_t a_base = smem_u32(smA + stage * C::A_BYTES);
@@ -631,7 +640,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
           for (int kk = 0; kk < BK / 16; ++kk) {
             uint64_t ad = A_MN ? make_desc(a_base + kk * 2048, BK * 128, 1024) : make_desc(a_base + kk * 32, 16, 1024);
             uint64_t bd = B_MN ? make_desc(b_base + kk * 2048, BK * 128, 1024) : make_desc(b_base + kk * 32, 16, 1024);
-            umma_f16(tmem_d, ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
+            umma_f16(tmem_d, ad, bd, idesc, (kb != kb_lo || kk != 0) ? 1u : 0u);
           }
           umma_commit(&empty[stage]);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -645,9 +654,16 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
     const uint32_t ebase = smem_u32(smE) + (uint32_t)((warp - 2) * 2 * C::EPI_SLOT);
     int eiter = 0;
     int local = 0;
+    // split-K partials: raw fp32 tiles stored at rows sp * mpad + row
+    EpiArgs pa = args;
+    pa.epi = BM_EPI_STORE;
+    pa.c_f32 = 1;
+    pa.alpha = 1.f;
+    pa.M = args.splits * args.mpad;
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++local) {
       int mb, nb;
-      tile_coords(t, tiles_m, tiles_n, mb, nb);
+      const int sp = t / base_tiles;
+      tile_coords(t - sp * base_tiles, tiles_m, tiles_n, mb, nb);
       const int acc = local & 1;
       const uint32_t acc_phase = (local >> 1) & 1;
       mbar_wait(&tfull[acc], acc_phase);
@@ -666,7 +682,8 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
               if (lane == 0) bulk_wait_read1();
               __syncwarp();
             }
-            epi_chunk_tma(args, &tmC, slot, lane, row0, nb * BN + c, v);
+            if (args.splits > 1) epi_chunk_tma(pa, &tmC, slot, lane, sp * args.mpad + row0, nb * BN + c, v);
+            else epi_chunk_tma(args, &tmC, slot, lane, row0, nb * BN + c, v);
             ++eiter;
           }
         } else if (row < args.M) {
@@ -896,6 +913,39 @@ gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
   }
 }
 
+
+// Deterministic split-K reduction: out = epilogue(sum_s ws[s]) in split order.
+__global__ void __launch_bounds__(256)
+splitk_reduce_kernel(int M, int N, int splits, int mpad, const float* __restrict__ ws, EpiArgs a) {
+  const int64_t idx = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
+  const int64_t total = (int64_t)M * N;
+  if (idx >= total) return;
+  const int row = (int)(idx / N), col = (int)(idx % N);   // N % 4 == 0
+  float4 acc = *reinterpret_cast<const float4*>(ws + (int64_t)row * N + col);
+  for (int sp = 1; sp < splits; ++sp) {
+    const float4 p = *reinterpret_cast<const float4*>(ws + ((int64_t)sp * mpad + row) * N + col);
+    acc.x += p.x; acc.y += p.y; acc.z += p.z; acc.w += p.w;
+  }
+  float w[4] = {a.alpha * acc.x, a.alpha * acc.y, a.alpha * acc.z, a.alpha * acc.w};
+  if (a.c_f32) {
+    float* c = reinterpret_cast<float*>(a.C) + (int64_t)row * a.ldc + col;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if (a.epi == BM_EPI_ACCUM) c[q] += w[q];
+      else if (a.epi == BM_EPI_ADD) c[q] = w[q] + reinterpret_cast<const float*>(a.R)[(int64_t)row * a.ldr + col + q];
+      else c[q] = w[q];
+    }
+  } else {
+    bf16* c = reinterpret_cast<bf16*>(a.C) + (int64_t)row * a.ldc + col;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      float v = w[q];
+      if (a.epi == BM_EPI_ADD) v += __bfloat162float(reinterpret_cast<const bf16*>(a.R)[(int64_t)row * a.ldr + col + q]);
+      c[q] = __float2bfloat16_rn(v);
+    }
+  }
+}
+
 // ---------------------------------------------------------------- host side
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -996,7 +1046,7 @@ static bm_status launch(const CUtensorMap& ma, const CUtensorMap& mb, const CUte
     BM_CUDA_TRY(cudaFuncSetAttribute(gemm_kernel<BN, A_MN, B_MN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
     attr_set = true;
   }
-  const int tiles = ceil_div(ea.M, BM) * ceil_div(ea.N, BN);
+  const int tiles = ceil_div(ea.M, BM) * ceil_div(ea.N, BN) * ea.splits;
   const int grid = tiles < num_sms() ? tiles : num_sms();
   gemm_kernel<BN, A_MN, B_MN><<<grid, NUM_THREADS, C::SMEM, st>>>(ma, mb, mc, ea);
   count_launch();
@@ -1054,13 +1104,13 @@ void set_gemm_mode(int m) { g_gemm_mode = m; }
 
 bm_status gemm_bf16_tc(int M, int N, int K, const void* A, int64_t lda, int a_major, const void* B, int64_t ldb,
                        int b_major, void* Cp, int64_t ldc, int c_dtype, int epi, const void* R, int64_t ldr,
-                       float alpha, cudaStream_t st, int f) {
+                       float alpha, cudaStream_t st, int f, void* ws, int64_t ws_bytes) {
   using namespace tc;
   BM_CHECK_ARG(lda % 8 == 0 && ldb % 8 == 0, "lda/ldb must be multiples of 8 (16-byte TMA strides)");
   BM_CHECK_ARG((reinterpret_cast<uintptr_t>(A) & 15) == 0 && (reinterpret_cast<uintptr_t>(B) & 15) == 0,
                "A/B must be 16-byte aligned");
   const bool amn = a_major != 0, bmn = b_major != 0;
-  EpiArgs ea{M, N, K, Cp, ldc, c_dtype == BM_F32 ? 1 : 0, epi, R, ldr, alpha, f, 0};
+  EpiArgs ea{M, N, K, Cp, ldc, c_dtype == BM_F32 ? 1 : 0, epi, R, ldr, alpha, f, 0, 1, 1 << 30, 0};
   CUtensorMap ma, mb, mc, mc2;
   std::memset(&mc, 0, sizeof(mc));
   std::memset(&mc2, 0, sizeof(mc2));
@@ -1112,6 +1162,37 @@ bm_status gemm_bf16_tc(int M, int N, int K, const void* A, int64_t lda, int a_ma
   else BM_TRY(make_map(A, M, K, lda, BK, &ma));
   if (b_major == 0) BM_TRY(make_map(B, K, N, ldb, BN, &mb));
   else BM_TRY(make_map(B, N, K, ldb, BK, &mb));
+  // split-K when a full wave of tiles is not available (deterministic: fp32
+  // partial tiles in the caller's workspace, summed in split order)
+  const int tiles = tm * ceil_div(N, BN);
+  const int nk = ceil_div(K, BK);
+  if (ws && tiles < num_sms() / 2 && nk >= 4 && N % 4 == 0 &&
+      (epi == BM_EPI_STORE || epi == BM_EPI_ADD || epi == BM_EPI_ACCUM)) {
+    int splits = std::min(8, std::min(num_sms() / tiles, nk / 2));
+    const int mpad = tm * BM;
+    while (splits > 1 && (int64_t)splits * mpad * N * 4 > ws_bytes) --splits;
+    if (splits > 1) {
+      const int kb_per = ceil_div(nk, splits);
+      splits = ceil_div(nk, kb_per);
+      EpiArgs pe = ea;
+      pe.splits = splits;
+      pe.kb_per = kb_per;
+      pe.mpad = mpad;
+      pe.tma = 1;
+      CUtensorMap mws;
+      BM_TRY(make_map_k(ws, (uint64_t)N, (uint64_t)splits * mpad, N, 32, 2, &mws));
+      bm_status r;
+      if (BN == 64) r = dispatch_majors<64>(amn, bmn, ma, mb, mws, pe, st);
+      else if (BN == 128) r = dispatch_majors<128>(amn, bmn, ma, mb, mws, pe, st);
+      else r = dispatch_majors<256>(amn, bmn, ma, mb, mws, pe, st);
+      BM_TRY(r);
+      const int64_t total = (int64_t)M * N / 4;
+      splitk_reduce_kernel<<<(int)((total + 255) / 256), 256, 0, st>>>(M, N, splits, mpad, (const float*)ws, ea);
+      count_launch();
+      BM_CUDA_TRY(cudaGetLastError());
+      return BM_OK;
+    }
+  }
   if (BN == 64) return dispatch_majors<64>(amn, bmn, ma, mb, mc, ea, st);
   if (BN == 128) return dispatch_majors<128>(amn, bmn, ma, mb, mc, ea, st);
   return dispatch_majors<256>(amn, bmn, ma, mb, mc, ea, st);

@@ -8,14 +8,14 @@ namespace bm {
 
 bm_status gemm_bf16_tc(int M, int N, int K, const void* A, int64_t lda, int a_major, const void* B, int64_t ldb,
                        int b_major, void* C, int64_t ldc, int c_dtype, int epi, const void* R, int64_t ldr,
-                       float alpha, cudaStream_t st, int f = 0);
+                       float alpha, cudaStream_t st, int f = 0, void* ws = nullptr, int64_t ws_bytes = 0);
 bm_status gemm_f32_simt(int M, int N, int K, const float* A, int64_t lda, int a_major, const float* B, int64_t ldb,
                         int b_major, float* C, int64_t ldc, int epi, const float* R, int64_t ldr, float alpha,
                         cudaStream_t st);
 // dtype-dispatching GEMM (bf16 -> tcgen05, fp32 -> exact FFMA)
 bm_status gemm(int dtype, int M, int N, int K, const void* A, int64_t lda, int a_major, const void* B, int64_t ldb,
                int b_major, void* C, int64_t ldc, int c_dtype, int epi, const void* R, int64_t ldr, float alpha,
-               cudaStream_t st, int f = 0);
+               cudaStream_t st, int f = 0, void* ws = nullptr, int64_t ws_bytes = 0);
 
 template <typename T>
 bm_status rmsnorm_fwd(int rows, int cols, const T* x, const T* g, T* y, float* rstd, cudaStream_t st);

@@ -30,7 +30,7 @@ int64_t launch_count() { return g_launches.load(std::memory_order_relaxed); }
 
 bm_status gemm(int dtype, int M, int N, int K, const void* A, int64_t lda, int a_major, const void* B, int64_t ldb,
                int b_major, void* C, int64_t ldc, int c_dtype, int epi, const void* R, int64_t ldr, float alpha,
-               cudaStream_t st, int f) {
+               cudaStream_t st, int f, void* ws, int64_t ws_bytes) {
   if (M <= 0 || N <= 0) return BM_OK;
   if (epi == BM_EPI_SWIGLU || epi == BM_EPI_DSWIGLU) {
     BM_CHECK_ARG(dtype == BM_BF16 && K > 0, "fused SwiGLU epilogues are bf16 tensor-core only");
@@ -49,7 +49,8 @@ bm_status gemm(int dtype, int M, int N, int K, const void* A, int64_t lda, int a
     return BM_OK;
   }
   if (dtype == BM_BF16) {
-    return gemm_bf16_tc(M, N, K, A, lda, a_major, B, ldb, b_major, C, ldc, c_dtype, epi, R, ldr, alpha, st);
+    return gemm_bf16_tc(M, N, K, A, lda, a_major, B, ldb, b_major, C, ldc, c_dtype, epi, R, ldr, alpha, st, f, ws,
+                        ws_bytes);
   }
   BM_CHECK_ARG(c_dtype == BM_F32, "fp32 GEMM writes fp32 C");
   return gemm_f32_simt(M, N, K, (const float*)A, lda, a_major, (const float*)B, ldb, b_major, (float*)C, ldc, epi,
@@ -85,7 +86,14 @@ bm_status bm_k_gemm(int32_t dtype, int32_t M, int32_t N, int32_t K, const void* 
                     const void* B, int64_t ldb, int32_t b_major, void* C, int64_t ldc, int32_t c_dtype,
                     int32_t epilogue, const void* R, int64_t ldr, float alpha, void* stream) {
   BM_CHECK_ARG(epilogue >= BM_EPI_STORE && epilogue <= BM_EPI_ADD, "use bm_k_gemm_swiglu for fused SwiGLU epilogues");
-  return gemm(dtype, M, N, K, A, lda, a_major, B, ldb, b_major, C, ldc, c_dtype, epilogue, R, ldr, alpha, ST(stream));
+  // standalone calls get a library-owned split-K workspace (the executor passes its own, per stream)
+  static void* ws = nullptr;
+  static const int64_t ws_bytes = 64ll << 20;
+  if (!ws && dtype == BM_BF16) {
+    if (cudaMalloc(&ws, ws_bytes) != cudaSuccess) { ws = nullptr; cudaGetLastError(); }
+  }
+  return gemm(dtype, M, N, K, A, lda, a_major, B, ldb, b_major, C, ldc, c_dtype, epilogue, R, ldr, alpha, ST(stream),
+              0, ws, ws ? ws_bytes : 0);
 }
 
 bm_status bm_k_gemm_swiglu(int32_t M, int32_t f, int32_t K, const void* X, int64_t ldx, const void* W, int64_t ldw,

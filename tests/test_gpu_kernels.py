@@ -37,7 +37,9 @@ def rnd(rng, *shape, scale=1.0):
 
 
 GEMM_SHAPES = [(128, 256, 64), (300, 200, 100), (1, 16, 48), (257, 513, 130), (64, 64, 16),
-               (129, 1000, 640), (2048, 2048, 1024), (40, 4096, 16)]
+               (129, 1000, 640), (2048, 2048, 1024), (40, 4096, 16),
+               # encoder/generator-like shapes that take the split-K path
+               (554, 384, 1536), (1536, 384, 560), (704, 1536, 384), (120, 512, 2048)]
 
 
 @pytest.mark.parametrize("M,N,K", GEMM_SHAPES)
@@ -65,7 +67,7 @@ def test_gemm_store_f32(L, M, N, K, a_mn, b_mn, dtype, mode):
     assert err <= tol, (err, tol)
 
 
-@pytest.mark.parametrize("M,N,K", [(300, 200, 104), (257, 513, 136), (1024, 768, 512)])
+@pytest.mark.parametrize("M,N,K", [(300, 200, 104), (257, 513, 136), (1024, 768, 512), (554, 384, 1536)])
 @pytest.mark.parametrize("epi", ["bf16_store", "bf16_add", "f32_accum"])
 @pytest.mark.parametrize("mode", [1, 2])
 def test_gemm_epilogues(L, M, N, K, epi, mode):
