@@ -268,6 +268,7 @@ def main():
     clocks = clk.stop()
     ms = e0.elapsed_time(e1)
     n_gemm, gemm_flops, gemm_ms = rt.gemm_stats()
+    n_msgs, comm_bytes, comm_ms = rt.comm_stats()
     rt.set_timing(False)
     launches = rt.launch_count() * args.steps
     ms_max = max_over_ranks(ms)
@@ -303,6 +304,9 @@ def main():
                "ms_per_step": ems / args.steps}
 
     launches_all = int(sum_over_ranks(launches))
+    comm_bytes_all = sum_over_ranks(comm_bytes)
+    comm_ms_all = sum_over_ranks(comm_ms)
+    n_msgs_all = int(sum_over_ranks(n_msgs))
     gemm_flops_all = sum_over_ranks(gemm_flops)
     gemm_ms_all = sum_over_ranks(gemm_ms)
     n_gemm_all = int(sum_over_ranks(n_gemm))
@@ -349,6 +353,12 @@ def main():
             "config": config_dict(cfg, N),
             "roofline": roofline, "step_roofline": step_roof,
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches_all, "clocks": clocks,
+            "nvlink": ({"bytes_per_step_all_ranks": comm_bytes_all / args.steps,
+                        "messages_per_step": n_msgs_all / args.steps,
+                        "copy_GBps": comm_bytes_all / (comm_ms_all / 1e3) / 1e9 if comm_ms_all > 0 else None,
+                        "avg_link_GBps_over_step": comm_bytes_all / max(world, 1) / (ms_max / 1e3) / 1e9,
+                        "note": "copy-engine peer copies into IPC receive slots; copy_GBps = bytes / summed "
+                                "copy durations on the comm streams"} if world > 1 else None),
             "tokens_per_s": cfg.M * cfg.S * args.steps / (ms_max / 1000.0),
             "peak_hbm_gb_per_gpu": peak_alloc / 1e9, "stash_peak_bytes_rank0": stash,
             "loss": loss}

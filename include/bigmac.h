@@ -232,6 +232,10 @@ bm_status bm_ctx_set_timing(bm_ctx* c, int32_t enable);
 /* Totals since timing was enabled: GEMM launches, algorithmic FLOPs (2MNK),
  * summed device milliseconds.  Synchronizes on the recorded events. */
 bm_status bm_ctx_gemm_stats(bm_ctx* c, int64_t* n_gemm, double* flops, double* ms);
+/* Totals since timing was enabled for the peer copies this rank issued
+ * (stage-boundary, gather/scatter payloads over NVLink): message count,
+ * bytes, summed device milliseconds of the copies on the comm streams. */
+bm_status bm_ctx_comm_stats(bm_ctx* c, int64_t* n_msgs, double* bytes, double* ms);
 void bm_ctx_destroy(bm_ctx* c);
 
 #ifdef __cplusplus

@@ -100,6 +100,7 @@ SIGNATURES = {
     "bm_ctx_stash_peak": [_P, C.POINTER(_I64)],
     "bm_ctx_set_timing": [_P, _I32],
     "bm_ctx_gemm_stats": [_P, C.POINTER(_I64), C.POINTER(C.c_double), C.POINTER(C.c_double)],
+    "bm_ctx_comm_stats": [_P, C.POINTER(_I64), C.POINTER(C.c_double), C.POINTER(C.c_double)],
     "bm_ctx_destroy": [_P],
     # bigmac_kernels.h
     "bm_k_gemm": [_I32, _I32, _I32, _I32, _P, _I64, _I32, _P, _I64, _I32, _P, _I64, _I32, _I32, _P, _I64, _F, _P],

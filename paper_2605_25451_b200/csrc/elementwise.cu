@@ -91,6 +91,7 @@ __device__ __forceinline__ float gelu_grad(float a) {
 template <typename T>
 __global__ void rmsnorm_fwd_kernel(int rows, int cols, const T* __restrict__ x, const T* __restrict__ g,
                                    T* __restrict__ y, float* __restrict__ rstd) {
+  pdl_enter();
   constexpr int N = V16<T>::N;
   const int warps = blockDim.x / 32;
   const int row = blockIdx.x * warps + threadIdx.x / 32;
@@ -118,6 +119,7 @@ __global__ void rmsnorm_fwd_kernel(int rows, int cols, const T* __restrict__ x, 
 template <typename T>
 __global__ void rmsnorm_bwd_kernel(int rows, int cols, const T* __restrict__ dy, const T* __restrict__ x,
                                    const T* __restrict__ g, const float* __restrict__ rstd, const T* dres, T* dx) {
+  pdl_enter();
   constexpr int N = V16<T>::N;
   const int warps = blockDim.x / 32;
   const int row = blockIdx.x * warps + threadIdx.x / 32;
@@ -151,6 +153,7 @@ template <typename T>
 __global__ void rmsnorm_dg_partial_kernel(int rows, int cols, int nchunk, const T* __restrict__ dy,
                                           const T* __restrict__ x, const float* __restrict__ rstd,
                                           float* __restrict__ partial) {
+  pdl_enter();
   const int col = blockIdx.x * blockDim.x + threadIdx.x;
   const int chunk = blockIdx.y;
   if (col >= cols) return;
@@ -163,7 +166,28 @@ __global__ void rmsnorm_dg_partial_kernel(int rows, int cols, int nchunk, const 
   }
   partial[(int64_t)chunk * cols + col] = acc;
 }
+// out[col] += sum_k partial[k][col]; 32 columns per block, 8 row groups per
+// column summed in a fixed order (deterministic)
+__global__ void __launch_bounds__(256)
+colsum2_accum_kernel(int nchunk, int cols, const float* __restrict__ partial, float* __restrict__ out) {
+  pdl_enter();
+  __shared__ float sh[8][33];
+  const int c = blockIdx.x * 32 + (threadIdx.x & 31);
+  const int g = threadIdx.x >> 5;
+  float acc = 0.f;
+  if (c < cols)
+    for (int k = g; k < nchunk; k += 8) acc += partial[(int64_t)k * cols + c];
+  sh[g][threadIdx.x & 31] = acc;
+  __syncthreads();
+  if (g == 0 && c < cols) {
+    float s = 0.f;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) s += sh[q][threadIdx.x];
+    out[c] += s;
+  }
+}
 __global__ void colsum_accum_kernel(int nchunk, int cols, const float* __restrict__ partial, float* __restrict__ out) {
+  pdl_enter();
   const int col = blockIdx.x * blockDim.x + threadIdx.x;
   if (col >= cols) return;
   float acc = 0.f;
@@ -177,6 +201,7 @@ static int dg_chunks(int rows) { return rows < 64 ? (rows > 0 ? rows : 1) : 64; 
 template <typename T>
 __global__ void __launch_bounds__(256)
 swiglu_fwd_kernel(int rows, int f, const T* __restrict__ gu, T* __restrict__ h) {
+  pdl_enter();
   // 2-D grid: blockIdx.y = row, x over 16-byte vectors of the row (no division)
   constexpr int N = V16<T>::N;
   const int64_t i = blockIdx.y;
@@ -195,6 +220,7 @@ swiglu_fwd_kernel(int rows, int f, const T* __restrict__ gu, T* __restrict__ h) 
 template <typename T>
 __global__ void __launch_bounds__(256)
 swiglu_bwd_kernel(int rows, int f, const T* __restrict__ dh, const T* __restrict__ gu, T* __restrict__ dgu) {
+  pdl_enter();
   constexpr int N = V16<T>::N;
   const int64_t i = blockIdx.y;
   const T* row = gu + i * 2 * (int64_t)f;
@@ -215,6 +241,7 @@ swiglu_bwd_kernel(int rows, int f, const T* __restrict__ dh, const T* __restrict
 }
 template <typename T>
 __global__ void gelu_fwd_kernel(int64_t n, const T* __restrict__ a, T* __restrict__ z) {
+  pdl_enter();
   constexpr int N = V16<T>::N;
   const int64_t nv = n / N;
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nv; v += (int64_t)gridDim.x * blockDim.x) {
@@ -228,6 +255,7 @@ __global__ void gelu_fwd_kernel(int64_t n, const T* __restrict__ a, T* __restric
 }
 template <typename T>
 __global__ void gelu_bwd_kernel(int64_t n, const T* __restrict__ dz, const T* __restrict__ a, T* __restrict__ da) {
+  pdl_enter();
   constexpr int N = V16<T>::N;
   const int64_t nv = n / N;
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nv; v += (int64_t)gridDim.x * blockDim.x) {
@@ -241,11 +269,13 @@ __global__ void gelu_bwd_kernel(int64_t n, const T* __restrict__ dz, const T* __
 }
 template <typename T>
 __global__ void add_kernel(int64_t n, const T* __restrict__ a, const T* __restrict__ b, T* __restrict__ o) {
+  pdl_enter();
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
     o[e] = from_f<T>(to_f(a[e]) + to_f(b[e]));
 }
 template <typename S, typename D>
 __global__ void cast_kernel(int64_t n, const S* __restrict__ a, D* __restrict__ o) {
+  pdl_enter();
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
     o[e] = from_f<D>(to_f(a[e]));
 }
@@ -254,6 +284,7 @@ __global__ void cast_kernel(int64_t n, const S* __restrict__ a, D* __restrict__ 
 template <typename T>
 __global__ void embed_fwd_kernel(int S, int d, int n_mod, const int32_t* __restrict__ ids, const T* __restrict__ table,
                                  const T* __restrict__ emb, T* __restrict__ X) {
+  pdl_enter();
   constexpr int N = V16<T>::N;
   const int warps = blockDim.x / 32;
   const int row = blockIdx.x * warps + threadIdx.x / 32;
@@ -268,6 +299,7 @@ __global__ void embed_fwd_kernel(int S, int d, int n_mod, const int32_t* __restr
 // emit positions in sorted order and segment starts.
 // scratch layout (int32): [0] nseg | order[S] | seg_start[S+1]
 __global__ void embed_sort_kernel(int S, int n_mod, const int32_t* __restrict__ ids, int32_t* __restrict__ scratch) {
+  pdl_enter();
   extern __shared__ unsigned long long keys[];
   __shared__ int wsum[32];
   const int cnt = S - n_mod;
@@ -333,6 +365,7 @@ __global__ void embed_sort_kernel(int S, int n_mod, const int32_t* __restrict__ 
 template <typename T>
 __global__ void embed_segsum_kernel(int S, int d, const int32_t* __restrict__ ids, const T* __restrict__ dX,
                                     const int32_t* __restrict__ scratch, float* __restrict__ dT) {
+  pdl_enter();
   const int nseg = scratch[0];
   const int32_t* order = scratch + 1;
   const int32_t* seg = scratch + 1 + S;
@@ -354,6 +387,7 @@ __global__ void embed_segsum_kernel(int S, int d, const int32_t* __restrict__ id
 template <typename T>
 __global__ void ce_row_kernel(int V, T* __restrict__ logits, const int32_t* __restrict__ labels, float scale_grad,
                               float* __restrict__ row_loss) {
+  pdl_enter();
   __shared__ float sh[32];
   const int row = blockIdx.x;
   T* z = logits + (int64_t)row * V;
@@ -374,6 +408,7 @@ __global__ void ce_row_kernel(int V, T* __restrict__ logits, const int32_t* __re
   }
 }
 __global__ void sum_scale_kernel(int n, const float* __restrict__ v, float scale, int accumulate, float* out) {
+  pdl_enter();
   __shared__ float sh[32];
   float s = 0.f;
   for (int i = threadIdx.x; i < n; i += blockDim.x) s += v[i];
@@ -383,6 +418,7 @@ __global__ void sum_scale_kernel(int n, const float* __restrict__ v, float scale
 template <typename T>
 __global__ void mse_kernel(int64_t n, const T* __restrict__ out, const T* __restrict__ t, float inv_denom,
                            float scale_grad, float scale_loss, float* loss, T* __restrict__ dout) {
+  pdl_enter();
   __shared__ float sh[32];
   float s = 0.f;
   for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
@@ -404,6 +440,7 @@ __global__ void __launch_bounds__(256)
 rmsnorm_bwd_fused_kernel(int rows, int cols, int rows_per_block, const T* __restrict__ dy, const T* __restrict__ x,
                          const T* __restrict__ g, const float* __restrict__ rstd, const T* dres, T* dx,
                          float* __restrict__ partial) {
+  pdl_enter();
   constexpr int N = V16<T>::N;
   extern __shared__ float sdg[];  // [8 warps][cols]
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -471,6 +508,7 @@ template <typename T>
 __global__ void __launch_bounds__(256)
 ce_row_vec_kernel(int V, T* __restrict__ logits, const int32_t* __restrict__ labels, float scale_grad,
                   float* __restrict__ row_loss) {
+  pdl_enter();
   constexpr int N = V16<T>::N;
   __shared__ float shm[32], shs[32];
   const int row = blockIdx.x;
@@ -545,24 +583,30 @@ template <typename T>
 bm_status rmsnorm_fwd(int rows, int cols, const T* x, const T* g, T* y, float* rstd, cudaStream_t st) {
   if (rows <= 0) return BM_OK;
   BM_CHECK_ARG(cols % V16<T>::N == 0, "rmsnorm cols must be a multiple of the vector width");
-  rmsnorm_fwd_kernel<T><<<ceil_div(rows, 8), 256, 0, st>>>(rows, cols, x, g, y, rstd);
+  BM_CUDA_TRY(launch_k(rmsnorm_fwd_kernel<T>, dim3(ceil_div(rows, 8)), dim3(256), 0, st, rows, cols, x, g, y, rstd));
   count_launch();
   BM_CUDA_TRY(cudaGetLastError());
   return BM_OK;
 }
-constexpr int RB_ROWS = 32;  // rows per block of the fused backward
+// rows per block of the fused backward: ~2 waves of blocks over the 148 SMs
+static int rb_rows(int rows) {
+  int rb = ceil_div(rows, 2 * num_sms());
+  rb = (rb + 7) / 8 * 8;
+  return rb < 8 ? 8 : rb;
+}
 template <typename T, int CH>
 static bm_status launch_rms_bwd_fused(int rows, int cols, const T* dy, const T* x, const T* g, const float* rstd,
                                       const T* dres, T* dx, float* dg, float* partial, cudaStream_t st) {
-  const int nb = ceil_div(rows, RB_ROWS);
+  const int rb = rb_rows(rows);
+  const int nb = ceil_div(rows, rb);
   const int smem = 8 * cols * 4;
   static bool attr = false;
   if (!attr) {
     BM_CUDA_TRY(cudaFuncSetAttribute(rmsnorm_bwd_fused_kernel<T, CH>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     attr = true;
   }
-  rmsnorm_bwd_fused_kernel<T, CH><<<nb, 256, smem, st>>>(rows, cols, RB_ROWS, dy, x, g, rstd, dres, dx, partial);
-  colsum_accum_kernel<<<ceil_div(cols, 256), 256, 0, st>>>(nb, cols, partial, dg);
+  BM_CUDA_TRY(launch_k(rmsnorm_bwd_fused_kernel<T, CH>, dim3(nb), dim3(256), smem, st, rows, cols, rb, dy, x, g, rstd, dres, dx, partial));
+  BM_CUDA_TRY(launch_k(colsum2_accum_kernel, dim3(ceil_div(cols, 32)), dim3(256), 0, st, nb, cols, partial, dg));
   count_launch(2);
   BM_CUDA_TRY(cudaGetLastError());
   return BM_OK;
@@ -584,9 +628,9 @@ bm_status rmsnorm_bwd(int rows, int cols, const T* dy, const T* x, const T* g, c
   }
   // wide rows: separate gain-gradient pass
   const int nch = dg_chunks(rows);
-  rmsnorm_dg_partial_kernel<T><<<dim3(ceil_div(cols, 256), nch), 256, 0, st>>>(rows, cols, nch, dy, x, rstd, partial);
-  colsum_accum_kernel<<<ceil_div(cols, 256), 256, 0, st>>>(nch, cols, partial, dg);
-  rmsnorm_bwd_kernel<T><<<ceil_div(rows, 8), 256, 0, st>>>(rows, cols, dy, x, g, rstd, dres, dx);
+  BM_CUDA_TRY(launch_k(rmsnorm_dg_partial_kernel<T>, dim3(dim3(ceil_div(cols, 256), nch)), dim3(256), 0, st, rows, cols, nch, dy, x, rstd, partial));
+  BM_CUDA_TRY(launch_k(colsum_accum_kernel, dim3(ceil_div(cols, 256)), dim3(256), 0, st, nch, cols, partial, dg));
+  BM_CUDA_TRY(launch_k(rmsnorm_bwd_kernel<T>, dim3(ceil_div(rows, 8)), dim3(256), 0, st, rows, cols, dy, x, g, rstd, dres, dx));
   count_launch(3);
   BM_CUDA_TRY(cudaGetLastError());
   return BM_OK;
@@ -597,7 +641,7 @@ bm_status swiglu_fwd(int rows, int f, const T* gu, T* h, cudaStream_t st) {
   if (total == 0) return BM_OK;
   BM_CHECK_ARG(f % V16<T>::N == 0, "swiglu f must be a multiple of the vector width");
   const int vx = ceil_div(f / V16<T>::N, 256);
-  swiglu_fwd_kernel<T><<<dim3(vx > 4 ? 4 : vx, rows), 256, 0, st>>>(rows, f, gu, h);
+  BM_CUDA_TRY(launch_k(swiglu_fwd_kernel<T>, dim3(dim3(vx > 4 ? 4 : vx, rows)), dim3(256), 0, st, rows, f, gu, h));
   count_launch();
   BM_CUDA_TRY(cudaGetLastError());
   return BM_OK;
@@ -608,7 +652,7 @@ bm_status swiglu_bwd(int rows, int f, const T* dh, const T* gu, T* dgu, cudaStre
   if (total == 0) return BM_OK;
   BM_CHECK_ARG(f % V16<T>::N == 0, "swiglu f must be a multiple of the vector width");
   const int vx = ceil_div(f / V16<T>::N, 256);
-  swiglu_bwd_kernel<T><<<dim3(vx > 4 ? 4 : vx, rows), 256, 0, st>>>(rows, f, dh, gu, dgu);
+  BM_CUDA_TRY(launch_k(swiglu_bwd_kernel<T>, dim3(dim3(vx > 4 ? 4 : vx, rows)), dim3(256), 0, st, rows, f, dh, gu, dgu));
   count_launch();
   BM_CUDA_TRY(cudaGetLastError());
   return BM_OK;
@@ -616,7 +660,7 @@ bm_status swiglu_bwd(int rows, int f, const T* dh, const T* gu, T* dgu, cudaStre
 template <typename T>
 bm_status gelu_fwd(int64_t n, const T* a, T* z, cudaStream_t st) {
   if (n == 0) return BM_OK;
-  gelu_fwd_kernel<T><<<ew_grid(n / V16<T>::N + 1), 256, 0, st>>>(n, a, z);
+  BM_CUDA_TRY(launch_k(gelu_fwd_kernel<T>, dim3(ew_grid(n / V16<T>::N + 1)), dim3(256), 0, st, n, a, z));
   count_launch();
   BM_CUDA_TRY(cudaGetLastError());
   return BM_OK;
@@ -624,7 +668,7 @@ bm_status gelu_fwd(int64_t n, const T* a, T* z, cudaStream_t st) {
 template <typename T>
 bm_status gelu_bwd(int64_t n, const T* dz, const T* a, T* da, cudaStream_t st) {
   if (n == 0) return BM_OK;
-  gelu_bwd_kernel<T><<<ew_grid(n / V16<T>::N + 1), 256, 0, st>>>(n, dz, a, da);
+  BM_CUDA_TRY(launch_k(gelu_bwd_kernel<T>, dim3(ew_grid(n / V16<T>::N + 1)), dim3(256), 0, st, n, dz, a, da));
   count_launch();
   BM_CUDA_TRY(cudaGetLastError());
   return BM_OK;
@@ -632,7 +676,7 @@ bm_status gelu_bwd(int64_t n, const T* dz, const T* a, T* da, cudaStream_t st) {
 template <typename T>
 bm_status embed_fwd(int S, int d, int n_mod, const int32_t* ids, const T* table, const T* emb, T* X, cudaStream_t st) {
   BM_CHECK_ARG(d % V16<T>::N == 0, "embed width must be a multiple of the vector width");
-  embed_fwd_kernel<T><<<ceil_div(S, 8), 256, 0, st>>>(S, d, n_mod, ids, table, emb, X);
+  BM_CUDA_TRY(launch_k(embed_fwd_kernel<T>, dim3(ceil_div(S, 8)), dim3(256), 0, st, S, d, n_mod, ids, table, emb, X));
   count_launch();
   BM_CUDA_TRY(cudaGetLastError());
   return BM_OK;
@@ -652,8 +696,8 @@ bm_status embed_bwd(int S, int d, int n_mod, const int32_t* ids, const T* dX, fl
     BM_CUDA_TRY(cudaFuncSetAttribute(embed_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 16384 * 8));
     attr = true;
   }
-  embed_sort_kernel<<<1, 1024, smem, st>>>(S, n_mod, ids, reinterpret_cast<int32_t*>(scratch));
-  embed_segsum_kernel<T><<<ceil_div(cnt, 8), 256, 0, st>>>(S, d, ids, dX, reinterpret_cast<int32_t*>(scratch), dT);
+  BM_CUDA_TRY(launch_k(embed_sort_kernel, dim3(1), dim3(1024), smem, st, S, n_mod, ids, reinterpret_cast<int32_t*>(scratch)));
+  BM_CUDA_TRY(launch_k(embed_segsum_kernel<T>, dim3(ceil_div(cnt, 8)), dim3(256), 0, st, S, d, ids, dX, reinterpret_cast<int32_t*>(scratch), dT));
   count_launch(2);
   BM_CUDA_TRY(cudaGetLastError());
   return BM_OK;
@@ -663,10 +707,10 @@ bm_status ce_fwd_bwd(int n, int V, T* logits, const int32_t* labels, float scale
                      float scale_loss, int accumulate, float* scratch, cudaStream_t st) {
   if (n <= 0) return BM_OK;
   if (V % V16<T>::N == 0)
-    ce_row_vec_kernel<T><<<n, 256, 0, st>>>(V, logits, labels, scale_grad, scratch);
+    BM_CUDA_TRY(launch_k(ce_row_vec_kernel<T>, dim3(n), dim3(256), 0, st, V, logits, labels, scale_grad, scratch));
   else
-    ce_row_kernel<T><<<n, 256, 0, st>>>(V, logits, labels, scale_grad, scratch);
-  sum_scale_kernel<<<1, 1024, 0, st>>>(n, scratch, scale_loss / n, accumulate, loss_out);
+    BM_CUDA_TRY(launch_k(ce_row_kernel<T>, dim3(n), dim3(256), 0, st, V, logits, labels, scale_grad, scratch));
+  BM_CUDA_TRY(launch_k(sum_scale_kernel, dim3(1), dim3(1024), 0, st, n, scratch, scale_loss / n, accumulate, loss_out));
   count_launch(2);
   BM_CUDA_TRY(cudaGetLastError());
   return BM_OK;
@@ -675,7 +719,7 @@ template <typename T>
 bm_status mse_fwd_bwd(int n, int dt, const T* out, const T* t, float denom, float scale_grad, float scale_loss,
                       float* loss_out, T* dout, cudaStream_t st) {
   if (n <= 0) return BM_OK;
-  mse_kernel<T><<<1, 1024, 0, st>>>((int64_t)n * dt, out, t, 1.f / denom, scale_grad, scale_loss, loss_out, dout);
+  BM_CUDA_TRY(launch_k(mse_kernel<T>, dim3(1), dim3(1024), 0, st, (int64_t)n * dt, out, t, 1.f / denom, scale_grad, scale_loss, loss_out, dout));
   count_launch();
   BM_CUDA_TRY(cudaGetLastError());
   return BM_OK;
@@ -683,17 +727,17 @@ bm_status mse_fwd_bwd(int n, int dt, const T* out, const T* t, float denom, floa
 template <typename T>
 bm_status add(int64_t n, const T* a, const T* b, T* o, cudaStream_t st) {
   if (n == 0) return BM_OK;
-  add_kernel<T><<<ew_grid(n), 256, 0, st>>>(n, a, b, o);
+  BM_CUDA_TRY(launch_k(add_kernel<T>, dim3(ew_grid(n)), dim3(256), 0, st, n, a, b, o));
   count_launch();
   BM_CUDA_TRY(cudaGetLastError());
   return BM_OK;
 }
 bm_status cast(int sd, int dd, int64_t n, const void* s, void* d, cudaStream_t st) {
   if (n == 0) return BM_OK;
-  if (sd == BM_F32 && dd == BM_BF16) cast_kernel<float, bf16><<<ew_grid(n), 256, 0, st>>>(n, (const float*)s, (bf16*)d);
-  else if (sd == BM_BF16 && dd == BM_F32) cast_kernel<bf16, float><<<ew_grid(n), 256, 0, st>>>(n, (const bf16*)s, (float*)d);
-  else if (sd == BM_F32 && dd == BM_F32) cast_kernel<float, float><<<ew_grid(n), 256, 0, st>>>(n, (const float*)s, (float*)d);
-  else cast_kernel<bf16, bf16><<<ew_grid(n), 256, 0, st>>>(n, (const bf16*)s, (bf16*)d);
+  if (sd == BM_F32 && dd == BM_BF16) BM_CUDA_TRY(launch_k(cast_kernel<float, bf16>, dim3(ew_grid(n)), dim3(256), 0, st, n, (const float*)s, (bf16*)d));
+  else if (sd == BM_BF16 && dd == BM_F32) BM_CUDA_TRY(launch_k(cast_kernel<bf16, float>, dim3(ew_grid(n)), dim3(256), 0, st, n, (const bf16*)s, (float*)d));
+  else if (sd == BM_F32 && dd == BM_F32) BM_CUDA_TRY(launch_k(cast_kernel<float, float>, dim3(ew_grid(n)), dim3(256), 0, st, n, (const float*)s, (float*)d));
+  else BM_CUDA_TRY(launch_k(cast_kernel<bf16, bf16>, dim3(ew_grid(n)), dim3(256), 0, st, n, (const bf16*)s, (bf16*)d));
   count_launch();
   BM_CUDA_TRY(cudaGetLastError());
   return BM_OK;
@@ -716,14 +760,14 @@ BM_INST(bf16)
 BM_INST(float)
 
 int64_t rmsnorm_bwd_scratch_floats(int rows, int cols) {
-  const int64_t fused = (int64_t)ceil_div(rows, RB_ROWS) * cols;
+  const int64_t fused = (int64_t)ceil_div(rows, 8) * cols;
   const int64_t split = (int64_t)dg_chunks(rows) * cols;
   return fused > split ? fused : split;
 }
 
 // step loss L = (1/M) sum_m (CE_m + MSE_m) from loss[0:2M] into loss[2M]
 bm_status loss_finalize(int M, float* loss, cudaStream_t st) {
-  sum_scale_kernel<<<1, 1024, 0, st>>>(2 * M, loss, 1.f / M, 0, loss + 2 * M);
+  BM_CUDA_TRY(launch_k(sum_scale_kernel, dim3(1), dim3(1024), 0, st, 2 * M, loss, 1.f / M, 0, loss + 2 * M));
   count_launch();
   BM_CUDA_TRY(cudaGetLastError());
   return BM_OK;

@@ -281,6 +281,11 @@ struct bm_ctx {
   int64_t gemm_count = 0;
   int64_t gemm_count_pending[2] = {0, 0};
   std::vector<std::array<int, 4>> tshape[2];              // (M, N, K, epi) per timed launch
+  // peer-copy timing (NVLink): event pairs on the comm streams, bytes per copy
+  std::vector<cudaEvent_t> cev[2];
+  std::vector<int64_t> cbytes[2];
+  double comm_ms = 0, comm_bytes = 0;
+  int64_t comm_msgs = 0;
   std::map<std::array<int, 4>, std::pair<int64_t, double>> shape_ms;  // BM_GEMM_LOG=1 breakdown
   ~bm_ctx();
 };
@@ -293,9 +298,12 @@ bm_ctx::~bm_ctx() {
   if (gen_done_ev) cudaEventDestroy(gen_done_ev);
   for (auto e : evpool)
     if (e) cudaEventDestroy(e);
-  for (int k = 0; k < 2; ++k)
+  for (int k = 0; k < 2; ++k) {
     for (auto e : tev[k])
       if (e) cudaEventDestroy(e);
+    for (auto e : cev[k])
+      if (e) cudaEventDestroy(e);
+  }
   for (int i = 0; i < 2; ++i) {
     if (bout_ev[i]) cudaEventDestroy(bout_ev[i]);
     if (gout_ev[i]) cudaEventDestroy(gout_ev[i]);
@@ -481,7 +489,23 @@ static bm_status timed_gemm(bm_ctx& c, int M, int N, int K, const void* A, int64
   return BM_OK;
 }
 // fold a finished pool's event pairs into the totals (blocks until they completed)
+static bm_status harvest_comm(bm_ctx& c, int pool) {
+  auto& ev = c.cev[pool];
+  const size_t n = c.cbytes[pool].size();
+  if (n == 0) return BM_OK;
+  for (size_t i = 0; i < n; ++i) {
+    BM_CUDA_TRY(cudaEventSynchronize(ev[2 * i + 1]));
+    float t = 0;
+    BM_CUDA_TRY(cudaEventElapsedTime(&t, ev[2 * i], ev[2 * i + 1]));
+    c.comm_ms += t;
+    c.comm_bytes += (double)c.cbytes[pool][i];
+  }
+  c.comm_msgs += (int64_t)n;
+  c.cbytes[pool].clear();
+  return BM_OK;
+}
 static bm_status harvest(bm_ctx& c, int pool) {
+  BM_TRY(harvest_comm(c, pool));
   auto& ev = c.tev[pool];
   if (c.tev_used[pool] == 0) return BM_OK;
   BM_CUDA_TRY(cudaEventSynchronize(ev[c.tev_used[pool] - 1]));
@@ -868,7 +892,22 @@ static bm_status do_send(bm_ctx& c, const bm_op& o) {
     bytes = payload_bytes(c, o, c.rank);
   }
   char* dst = c.peer[o.peer] + ch.data_off + (int64_t)(o.seq % ch.K) * ch.slot_bytes;
-  if (bytes > 0) BM_CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, cs));
+  if (c.timing && bytes > 0) {
+    const int pool = (int)(c.step & 1);
+    auto& ev = c.cev[pool];
+    const size_t k = c.cbytes[pool].size();
+    while (ev.size() < 2 * (k + 1)) {
+      cudaEvent_t e;
+      BM_CUDA_TRY(cudaEventCreate(&e));
+      ev.push_back(e);
+    }
+    BM_CUDA_TRY(cudaEventRecord(ev[2 * k], cs));
+    BM_CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, cs));
+    BM_CUDA_TRY(cudaEventRecord(ev[2 * k + 1], cs));
+    c.cbytes[pool].push_back(bytes);
+  } else if (bytes > 0) {
+    BM_CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, cs));
+  }
   CUresult r = drv().write32((CUstream)cs, (CUdeviceptr)(c.peer[o.peer] + ch.flag_off), base + (uint32_t)o.seq + 1, 0);
   if (r != CUDA_SUCCESS) { set_error("cuStreamWriteValue32 (data flag) failed " + std::to_string((int)r)); return BM_E_CUDA; }
   if (c.last_src_ring == 0 && o.payload != BM_PAY_GENIN) {
@@ -1289,6 +1328,19 @@ bm_status bm_ctx_set_timing(bm_ctx* c, int32_t enable) {
   c->gemm_flops = 0;
   c->gemm_ms = 0;
   c->gemm_count = 0;
+  c->comm_ms = 0;
+  c->comm_bytes = 0;
+  c->comm_msgs = 0;
+  return BM_OK;
+}
+
+bm_status bm_ctx_comm_stats(bm_ctx* c, int64_t* n_msgs, double* bytes, double* ms) {
+  BM_CHECK_ARG(c && n_msgs && bytes && ms, "null argument");
+  BM_TRY(harvest(*c, 0));
+  BM_TRY(harvest(*c, 1));
+  *n_msgs = c->comm_msgs;
+  *bytes = c->comm_bytes;
+  *ms = c->comm_ms;
   return BM_OK;
 }
 

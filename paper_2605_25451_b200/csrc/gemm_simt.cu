@@ -16,6 +16,7 @@ gemm_f32_kernel(int M, int N, int K, const float* __restrict__ A, int64_t lda, i
                 int epi, const float* __restrict__ R, int64_t ldr, float alpha) {
   __shared__ float As[TK][TM + 4];
   __shared__ float Bs[TK][TN + 4];
+  pdl_enter();
   const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
   const int m0 = blockIdx.y * TM, n0 = blockIdx.x * TN;
   float acc[4][4];
@@ -77,7 +78,8 @@ bm_status gemm_f32_simt(int M, int N, int K, const float* A, int64_t lda, int a_
                         int b_major, float* C, int64_t ldc, int epi, const float* R, int64_t ldr, float alpha,
                         cudaStream_t st) {
   dim3 grid(ceil_div(N, TN), ceil_div(M, TM));
-  gemm_f32_kernel<<<grid, 256, 0, st>>>(M, N, K, A, lda, a_major, B, ldb, b_major, C, ldc, epi, R, ldr, alpha);
+  BM_CUDA_TRY(launch_k(gemm_f32_kernel, grid, dim3(256), 0, st, M, N, K, A, lda, a_major, B, ldb, b_major, C, ldc, epi, R,
+                       ldr, alpha));
   count_launch();
   BM_CUDA_TRY(cudaGetLastError());
   return BM_OK;

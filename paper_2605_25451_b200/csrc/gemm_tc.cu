@@ -582,6 +582,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_enter();   // everything above is data independent (PDL overlap with the previous kernel)
 
   if (warp == 0) {
     if (lane == 0) {
@@ -777,6 +778,7 @@ gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_enter();
 
   if (warp == 0) {
     if (lane == 0) {
@@ -917,6 +919,7 @@ gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
 // Deterministic split-K reduction: out = epilogue(sum_s ws[s]) in split order.
 __global__ void __launch_bounds__(256)
 splitk_reduce_kernel(int M, int N, int splits, int mpad, const float* __restrict__ ws, EpiArgs a) {
+  pdl_enter();
   const int64_t idx = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
   const int64_t total = (int64_t)M * N;
   if (idx >= total) return;
@@ -1048,7 +1051,7 @@ static bm_status launch(const CUtensorMap& ma, const CUtensorMap& mb, const CUte
   }
   const int tiles = ceil_div(ea.M, BM) * ceil_div(ea.N, BN) * ea.splits;
   const int grid = tiles < num_sms() ? tiles : num_sms();
-  gemm_kernel<BN, A_MN, B_MN><<<grid, NUM_THREADS, C::SMEM, st>>>(ma, mb, mc, ea);
+  BM_CUDA_TRY(launch_k(gemm_kernel<BN, A_MN, B_MN>, dim3(grid), dim3(NUM_THREADS), C::SMEM, st, ma, mb, mc, ea));
   count_launch();
   BM_CUDA_TRY(cudaGetLastError());
   return BM_OK;
@@ -1077,7 +1080,8 @@ static bm_status launch2(const CUtensorMap& ma, const CUtensorMap& mb, const CUt
   const int tiles = ceil_div(ea.M, 2 * BM) * (SWIGLU ? ceil_div(ea.f, BN / 2) : ceil_div(ea.N, BN));
   const int pairs = num_sms() / 2;
   const int grid = 2 * (tiles < pairs ? tiles : pairs);
-  gemm2_kernel<BN, A_MN, B_MN, SWIGLU><<<grid, NUM_THREADS, C::SMEM, st>>>(ma, mb, mc, mc2, ea);
+  BM_CUDA_TRY(launch_k(gemm2_kernel<BN, A_MN, B_MN, SWIGLU>, dim3(grid), dim3(NUM_THREADS), C::SMEM, st, ma, mb, mc,
+                       mc2, ea));
   count_launch();
   BM_CUDA_TRY(cudaGetLastError());
   return BM_OK;
@@ -1187,7 +1191,8 @@ bm_status gemm_bf16_tc(int M, int N, int K, const void* A, int64_t lda, int a_ma
       else r = dispatch_majors<256>(amn, bmn, ma, mb, mws, pe, st);
       BM_TRY(r);
       const int64_t total = (int64_t)M * N / 4;
-      splitk_reduce_kernel<<<(int)((total + 255) / 256), 256, 0, st>>>(M, N, splits, mpad, (const float*)ws, ea);
+      BM_CUDA_TRY(launch_k(splitk_reduce_kernel, dim3((int)((total + 255) / 256)), dim3(256), 0, st, M, N, splits, mpad,
+                           (const float*)ws, ea));
       count_launch();
       BM_CUDA_TRY(cudaGetLastError());
       return BM_OK;

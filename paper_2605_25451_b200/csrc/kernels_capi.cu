@@ -24,6 +24,14 @@ int num_sms() {
   return n;
 }
 
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("BM_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 static std::atomic<int64_t> g_launches{0};
 void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 int64_t launch_count() { return g_launches.load(std::memory_order_relaxed); }

@@ -148,6 +148,11 @@ class Runtime:
         L.call("bm_ctx_gemm_stats", self.ctx, C.byref(n), C.byref(fl), C.byref(ms))
         return n.value, fl.value, ms.value
 
+    def comm_stats(self):
+        n, b, ms = C.c_int64(), C.c_double(), C.c_double()
+        L.call("bm_ctx_comm_stats", self.ctx, C.byref(n), C.byref(b), C.byref(ms))
+        return n.value, b.value, ms.value
+
     def names(self):
         return list(self.params)
 

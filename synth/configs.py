@@ -59,6 +59,16 @@ _C1 = ModelShape(
     n_mod_law=("uniform", 16, 64), n_gen_law=("uniform", 16, 64),
 )
 
+# parity-medium: C1's structure at sizes that span several GEMM tiles in every
+# dimension with ragged tails (row counts not multiples of 128), oracle in seconds
+_C1M = ModelShape(
+    name="C1M", P=2, M=4, V=1, S=384,
+    d_in=200, d_e=128, f_e=384, L_e=2,
+    d=256, f=640, L=4, vocab=1000,
+    d_g=128, f_g=256, L_g=2, d_t=16,
+    n_mod_law=("uniform", 60, 200), n_gen_law=("uniform", 60, 200),
+)
+
 # ViT-S-shaped encoder + 1B-shaped LLM + small generator (‡ frozen)
 _C2 = ModelShape(
     name="C2", P=4, M=16, V=1, S=4096,
@@ -81,7 +91,7 @@ _C4 = ModelShape(
 
 _C5 = _C4.replace(name="C5")   # global-batch sweep M in {8,...,256} at P=8
 
-CONFIGS = {c.name: c for c in (_C1, _C2, _C3, _C4, _C5)}
+CONFIGS = {c.name: c for c in (_C1, _C1M, _C2, _C3, _C4, _C5)}
 
 
 def get_config(name: str, **overrides) -> ModelShape:

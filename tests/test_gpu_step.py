@@ -73,6 +73,26 @@ def test_step_single_gpu(oracle_cache, dtype, M, V):
     rt.close()
 
 
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("M,V", [(4, 1), (4, 2)])
+def test_step_single_gpu_medium(oracle_cache, dtype, M, V):
+    # C1M: several tiles per GEMM dimension, ragged row counts (60..200 modality rows)
+    from paper_2605_25451_b200.runtime import Runtime
+    cfg = get_config("C1M", P=1, M=M, V=V)
+    W, B, (loss_ref, per_ref, G_ref) = reference(oracle_cache, cfg)
+    rt = Runtime(cfg, dtype)
+    rt.load_weights(W)
+    rt.step(rt.device_batch(B))
+    torch.cuda.synchronize()
+    loss, ce, mse = rt.losses()
+    tol = TOL[dtype]
+    assert abs(loss - loss_ref) <= tol * abs(loss_ref)
+    bad = {n: rel(rt.grad(n), G_ref[n]) for n in rt.names()}
+    bad = {k: v for k, v in bad.items() if v > tol}
+    assert not bad, bad
+    rt.close()
+
+
 def _torchrun(nproc, *args, timeout=600):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
            "--master-addr", "127.0.0.1", "--master-port", str(29500 + nproc), os.path.join(ROOT, "tests", "mp_step.py"),
@@ -88,6 +108,14 @@ def test_step_two_gpus(P, M, V, dtype, gen):
     if torch.cuda.device_count() < P:
         pytest.skip(f"needs {P} GPUs")
     out = _torchrun(P, "C1", P, M, V, dtype, gen)
+    assert "PARITY OK" in out, out
+
+
+@pytest.mark.parametrize("cfg_name,P,M,V,dtype", [("C1M", 2, 4, 1, "bf16"), ("C1M", 2, 4, 2, "f32")])
+def test_step_two_gpus_medium(cfg_name, P, M, V, dtype):
+    if torch.cuda.device_count() < P:
+        pytest.skip(f"needs {P} GPUs")
+    out = _torchrun(P, cfg_name, P, M, V, dtype, "dp_shard")
     assert "PARITY OK" in out, out
 
 
