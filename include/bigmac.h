@@ -48,7 +48,12 @@ typedef enum {
 } bm_status;
 
 typedef enum { BM_LLM_1F1B = 0, BM_LLM_INTERLEAVED = 1 } bm_llm_sched;          /* P:14, P:133, P:200 */
-typedef enum { BM_ENC_NONE = 0, BM_ENC_DP_UNIT = 1 } bm_enc_place;              /* P:193-195 */
+/* BM_ENC_DP_UNIT: BigMac (units of P microbatches, one per rank).
+ * BM_ENC_ENTRY_STAGE: memory-efficient baseline (Fig. 3): the
+ * encoder runs as the entry stage's first layers -- EncFwd(m) right before
+ * F(m, 0) and EncBwd(m) right after B(m, 0) on rank 0.  (The compute-efficient
+ * baseline of P:129-138 is BM_ENC_DP_UNIT with warmup_units = M / P.) */
+typedef enum { BM_ENC_NONE = 0, BM_ENC_DP_UNIT = 1, BM_ENC_ENTRY_STAGE = 2 } bm_enc_place;
 typedef enum { BM_GEN_NONE = 0, BM_GEN_DP_SHARD = 1, BM_GEN_LAST_STAGE = 2 } bm_gen_place; /* P:211, P:344 */
 
 typedef enum {

@@ -92,7 +92,8 @@ def run(sched, cfg, weights, batch):
                 n_mod = int(batch.n_mod[m])
                 if sc.enc_place == "none":
                     raise InterpError("encoder placement 'none' unsupported by the interpreter")
-                emb = local[r][("emb", m)] if m % P == 0 else take(r, "emb", m)[0]
+                own = m % P == 0 or sc.enc_place == "entry_stage"
+                emb = local[r][("emb", m)] if own else take(r, "emb", m)[0]
                 x = om.embed_fwd(W, batch.ids[m], emb, n_mod)
             elif (s - 1) % P == r:
                 x = local[r].pop(("act", m, s - 1))
@@ -147,7 +148,7 @@ def run(sched, cfg, weights, batch):
             out = {}
             if s == 0:
                 dE = om.embed_bwd(cfg, dx, batch.ids[m], int(batch.n_mod[m]), G[r])
-                if m % P == 0:
+                if m % P == 0 or sc.enc_place == "entry_stage":
                     local[r][("embgrad", m)] = dE
                 out["embgrad"] = dE
             else:

@@ -50,7 +50,7 @@ class SchedCfg:
     vchunks: int = 1            # V  (vpp size)
     warmup_units: int = 0       # W; 0 => W*
     llm_sched: str = "1f1b"     # "1f1b" | "interleaved"
-    enc_place: str = "dp_unit"  # "none" | "dp_unit"
+    enc_place: str = "dp_unit"  # "none" | "dp_unit" | "entry_stage"
     gen_place: str = "dp_shard" # "none" | "dp_shard" | "last_stage"
     cost_fwd: int = 1           # cut-timeline cost ratio, default 1:2
     cost_bwd: int = 2
@@ -95,7 +95,7 @@ def validate(cfg: SchedCfg) -> None:
         raise ScheduleError(E_INVALID, "interleaved 1F1B requires V >= 2")
     if cfg.llm_sched not in ("1f1b", "interleaved"):
         raise ScheduleError(E_INVALID, "unknown llm_sched")
-    if cfg.enc_place not in ("none", "dp_unit"):
+    if cfg.enc_place not in ("none", "dp_unit", "entry_stage"):
         raise ScheduleError(E_INVALID, "unknown enc_place")
     if cfg.gen_place not in ("none", "dp_shard", "last_stage"):
         raise ScheduleError(E_INVALID, "unknown gen_place")
@@ -196,8 +196,9 @@ def nest(cfg: SchedCfg, base, times):
     """Compute-op lists per rank (O-S steps 4-5)."""
     P, M, V = cfg.stages, cfg.microbatches, cfg.vchunks
     n_u = M // P
-    W = cfg.warmup_units if cfg.warmup_units > 0 else w_star(base[0], P)
-    enc = cfg.enc_place != "none"
+    entry = cfg.enc_place == "entry_stage"
+    W = 0 if entry else (cfg.warmup_units if cfg.warmup_units > 0 else w_star(base[0], P))
+    enc = cfg.enc_place == "dp_unit"
     gen = cfg.gen_place
 
     events = []
@@ -228,7 +229,13 @@ def nest(cfg: SchedCfg, base, times):
             if enc and k == "F" and r == 0 and c == 0 and m // P >= nxt:
                 raise ScheduleError(
                     E_WARMUP, f"W={W} too small: F({m},0)@0 precedes EncFwd({m // P})")
+            # memory-efficient baseline (Fig. 3): the encoder is the entry
+            # stage's first layers -- EncFwd(m) right before F(m,0), EncBwd(m) right after B(m,0)
+            if entry and k == "F" and r == 0 and c == 0:
+                lists[r].append(Op(ENC_FWD, mb=m, unit=m))
             lists[r].append(Op(LLM_FWD if k == "F" else LLM_BWD, mb=m, chunk=c))
+            if entry and k == "B" and r == 0 and c == 0:
+                lists[r].append(Op(ENC_BWD, mb=m, unit=m))
         elif cls == 0:
             m = ev[1]
             targets = range(P) if gen == "dp_shard" else [P - 1]
@@ -256,7 +263,7 @@ def _recvs_before(cfg: SchedCfg, r: int, op: Op):
         s = vstage(P, r, op.chunk)
         if s > 0 and (s - 1) % P != r:
             out.append(Op(RECV, mb=op.mb, chunk=op.chunk, peer=(s - 1) % P, payload="act"))
-        if s == 0 and cfg.enc_place != "none" and op.mb % P != 0:
+        if s == 0 and cfg.enc_place == "dp_unit" and op.mb % P != 0:
             out.append(Op(RECV, mb=op.mb, unit=op.mb // P, peer=op.mb % P, payload="emb"))
     elif op.kind == LLM_BWD:
         s = vstage(P, r, op.chunk)
@@ -266,7 +273,7 @@ def _recvs_before(cfg: SchedCfg, r: int, op: Op):
             for q in range(P):
                 if q != r:
                     out.append(Op(RECV, mb=op.mb, peer=q, payload="gengrad"))
-    elif op.kind == ENC_BWD and r != 0:
+    elif op.kind == ENC_BWD and r != 0 and cfg.enc_place == "dp_unit":
         out.append(Op(RECV, mb=op.mb, unit=op.unit, peer=0, payload="embgrad"))
     elif op.kind == GEN_FWD and cfg.gen_place == "dp_shard" and r != P - 1:
         out.append(Op(RECV, mb=op.mb, peer=P - 1, payload="genin"))
@@ -288,9 +295,9 @@ def _sends_after(cfg: SchedCfg, r: int, op: Op):
         s = vstage(P, r, op.chunk)
         if s > 0 and (s - 1) % P != r:
             out.append(Op(SEND, mb=op.mb, chunk=op.chunk, peer=(s - 1) % P, payload="grad"))
-        if s == 0 and cfg.enc_place != "none" and op.mb % P != 0:
+        if s == 0 and cfg.enc_place == "dp_unit" and op.mb % P != 0:
             out.append(Op(SEND, mb=op.mb, unit=op.mb // P, peer=op.mb % P, payload="embgrad"))
-    elif op.kind == ENC_FWD and r != 0:
+    elif op.kind == ENC_FWD and r != 0 and cfg.enc_place == "dp_unit":
         out.append(Op(SEND, mb=op.mb, unit=op.unit, peer=0, payload="emb"))
     elif op.kind == GEN_BWD and cfg.gen_place == "dp_shard" and r != P - 1:
         out.append(Op(SEND, mb=op.mb, peer=P - 1, payload="gengrad"))
@@ -476,8 +483,10 @@ def compute_deps(cfg: SchedCfg, r: int, op: Op):
         s = vstage(P, r, op.chunk)
         if s > 0:
             deps.append(((s - 1) % P, LLM_FWD, op.mb, (s - 1) // P))
-        elif cfg.enc_place != "none":
+        elif cfg.enc_place == "dp_unit":
             deps.append((op.mb % P, ENC_FWD, op.mb, -1))
+        elif cfg.enc_place == "entry_stage":
+            deps.append((0, ENC_FWD, op.mb, -1))
     elif op.kind == LLM_BWD:
         s = vstage(P, r, op.chunk)
         deps.append((r, LLM_FWD, op.mb, op.chunk))
@@ -615,7 +624,7 @@ def build(cfg: SchedCfg) -> Schedule:
     final = assign_slots(with_comm, rings)
 
     makespan = max(en for (_, en) in times.values())
-    ws = w_star(base[0], P) if cfg.enc_place != "none" else 0
+    ws = w_star(base[0], P) if cfg.enc_place == "dp_unit" else 0
     stats = []
     for r in range(P):
         busy = sum(en - st for (rr, *_), (st, en) in times.items() if rr == r)
@@ -631,7 +640,7 @@ def build(cfg: SchedCfg) -> Schedule:
             elif o.kind == LLM_BWD:
                 cur -= 1
         stats.append(Stats(
-            w_star=ws, warmup_units=W if cfg.enc_place != "none" else 0,
+            w_star=ws, warmup_units=W if cfg.enc_place == "dp_unit" else 0,
             peak_enc_units=peak_window(lists[r], ENC_FWD, ENC_BWD),
             peak_gen_shards=peak_window(lists[r], GEN_FWD, GEN_BWD),
             peak_llm_inflight=inflight,

@@ -19,7 +19,7 @@ EPI_STORE, EPI_ACCUM, EPI_ADD = 0, 1, 2
 OP_KINDS = ["EncFwd", "EncBwd", "LlmFwd", "LlmBwd", "GenFwd", "GenBwd", "Send", "Recv"]
 PAYLOADS = ["act", "grad", "emb", "embgrad", "genin", "gengrad"]
 LLM_SCHED = {"1f1b": 0, "interleaved": 1}
-ENC_PLACE = {"none": 0, "dp_unit": 1}
+ENC_PLACE = {"none": 0, "dp_unit": 1, "entry_stage": 2}
 GEN_PLACE = {"none": 0, "dp_shard": 1, "last_stage": 2}
 
 

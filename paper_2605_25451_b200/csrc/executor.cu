@@ -203,6 +203,7 @@ struct bm_ctx {
   std::unordered_map<std::string, int> pidx;
   int64_t total_elems = 0, dp_elems = 0;
   bool has_enc = false, has_gen = false, gen_last = false;
+  bool enc_entry = false;  // memory-efficient baseline: encoder as the entry stage's first layers
   int n_enc_slots = 0, n_llm_slots = 0, gen_rows = 0;
   // comm layout
   std::vector<Chan> chans;
@@ -687,8 +688,9 @@ static bm_status op_llm_fwd(bm_ctx& c, const bm_op& o, const RecvState& rs) {
   // stage input (P:297 embed_preprocess at the entry stage)
   if (s == 0) {
     const int n_mod = c.n_mod[mb];
-    const char* emb = (mb % c.P == 0) ? c.enc[(mb / c.P) % c.n_enc_slots].out
-                                      : recv_slot(c, mb % c.P, BM_PAY_EMB, rs.ops.at(0)->seq);
+    const char* emb = c.enc_entry      ? c.enc[mb % c.n_enc_slots].out
+                      : (mb % c.P == 0) ? c.enc[(mb / c.P) % c.n_enc_slots].out
+                                        : recv_slot(c, mb % c.P, BM_PAY_EMB, rs.ops.at(0)->seq);
     BM_TRY(TY(c, embed_fwd<bf16>(m.S, m.d, n_mod, c.ids + (int64_t)mb * S, (const bf16*)P_(c, "llm.embed"), (const bf16*)emb, (bf16*)sl.x[0], c.st),
               embed_fwd<float>(m.S, m.d, n_mod, c.ids + (int64_t)mb * S, (const float*)P_(c, "llm.embed"), (const float*)emb, (float*)sl.x[0], c.st)));
   } else if ((s - 1) % c.P == c.rank) {
@@ -789,7 +791,7 @@ static bm_status op_llm_bwd(bm_ctx& c, const bm_op& o, const RecvState& rs) {
     const int n_mod = c.n_mod[mb];
     BM_TRY(TY(c, embed_bwd<bf16>(m.S, m.d, n_mod, c.ids + (int64_t)mb * S, (const bf16*)c.bout[b], G_(c, "llm.embed"), c.embscr, c.st),
               embed_bwd<float>(m.S, m.d, n_mod, c.ids + (int64_t)mb * S, (const float*)c.bout[b], G_(c, "llm.embed"), c.embscr, c.st)));
-    if (mb % c.P == 0) BM_TRY(d2d(c, c.emb_local, c.bout[b], (int64_t)n_mod * d * es));
+    if (c.enc_entry || mb % c.P == 0) BM_TRY(d2d(c, c.emb_local, c.bout[b], (int64_t)n_mod * d * es));
   } else if ((s - 1) % c.P == c.rank) {
     BM_TRY(d2d(c, c.llm[c.llm_live.at({mb, ch - 1})].gin, c.bout[b], S * d * es));
   }
@@ -990,6 +992,7 @@ bm_status bm_ctx_create(const bm_model_cfg* mc, const bm_schedule* s, int32_t ra
   c->has_enc = s->cfg.enc_place != BM_ENC_NONE;
   c->has_gen = s->cfg.gen_place != BM_GEN_NONE;
   c->gen_last = s->cfg.gen_place == BM_GEN_LAST_STAGE;
+  c->enc_entry = s->cfg.enc_place == BM_ENC_ENTRY_STAGE;
   if (!c->has_enc) {
     delete c;
     set_error("the executor requires an encoder placement (embed_preprocess consumes encoder outputs)");

@@ -59,7 +59,8 @@ static void validate(const bm_sched_cfg& c) {
   if (c.llm_sched == BM_LLM_1F1B && V != 1) throw Fail{BM_E_INVALID, "1F1B requires V == 1"};
   if (c.llm_sched == BM_LLM_INTERLEAVED && V < 2) throw Fail{BM_E_INVALID, "interleaved 1F1B requires V >= 2"};
   if (c.llm_sched != BM_LLM_1F1B && c.llm_sched != BM_LLM_INTERLEAVED) throw Fail{BM_E_INVALID, "unknown llm_sched"};
-  if (c.enc_place != BM_ENC_NONE && c.enc_place != BM_ENC_DP_UNIT) throw Fail{BM_E_INVALID, "unknown enc_place"};
+  if (c.enc_place != BM_ENC_NONE && c.enc_place != BM_ENC_DP_UNIT && c.enc_place != BM_ENC_ENTRY_STAGE)
+    throw Fail{BM_E_INVALID, "unknown enc_place"};
   if (c.gen_place != BM_GEN_NONE && c.gen_place != BM_GEN_DP_SHARD && c.gen_place != BM_GEN_LAST_STAGE)
     throw Fail{BM_E_INVALID, "unknown gen_place"};
   for (int i = 0; i < 6; ++i)
@@ -159,9 +160,10 @@ static std::vector<std::vector<bm_op>> nest(const bm_sched_cfg& c, const std::ve
                                             const Times& T, int& W_out) {
   const int P = c.stages, M = c.microbatches, V = c.vchunks;
   const int n_u = M / P;
-  const int W = c.warmup_units > 0 ? c.warmup_units : w_star(base[0], P, M);
+  const bool entry = c.enc_place == BM_ENC_ENTRY_STAGE;
+  const int W = entry ? 0 : (c.warmup_units > 0 ? c.warmup_units : w_star(base[0], P, M));
   W_out = W;
-  const bool enc = c.enc_place != BM_ENC_NONE;
+  const bool enc = c.enc_place == BM_ENC_DP_UNIT;
   struct Ev {
     int64_t t;
     int cls, tb;
@@ -195,7 +197,10 @@ static std::vector<std::vector<bm_op>> nest(const bm_sched_cfg& c, const std::ve
       if (enc && !o.bwd && e.r == 0 && o.chunk == 0 && o.mb / P >= nxt)
         throw Fail{BM_E_WARMUP, "W=" + std::to_string(W) + " too small: F(" + std::to_string(o.mb) +
                                     ",0)@0 precedes EncFwd(" + std::to_string(o.mb / P) + ")"};
+      // memory-efficient baseline: the encoder is the entry stage's first layers
+      if (entry && !o.bwd && e.r == 0 && o.chunk == 0) lists[0].push_back(mk(BM_OP_ENC_FWD, o.mb, -1, o.mb));
       lists[e.r].push_back(mk(o.bwd ? BM_OP_LLM_BWD : BM_OP_LLM_FWD, o.mb, o.chunk));
+      if (entry && o.bwd && e.r == 0 && o.chunk == 0) lists[0].push_back(mk(BM_OP_ENC_BWD, o.mb, -1, o.mb));
     } else if (e.cls == 0) {
       const int m = e.idx;
       if (c.gen_place == BM_GEN_DP_SHARD) {
@@ -227,7 +232,7 @@ static void recvs_before(const bm_sched_cfg& c, int r, const bm_op& o, std::vect
   if (o.kind == BM_OP_LLM_FWD) {
     const int s = o.chunk * P + r;
     if (s > 0 && (s - 1) % P != r) out.push_back(mk(BM_OP_RECV, o.mb, o.chunk, -1, (s - 1) % P, BM_PAY_ACT));
-    if (s == 0 && c.enc_place != BM_ENC_NONE && o.mb % P != 0)
+    if (s == 0 && c.enc_place == BM_ENC_DP_UNIT && o.mb % P != 0)
       out.push_back(mk(BM_OP_RECV, o.mb, -1, o.mb / P, o.mb % P, BM_PAY_EMB));
   } else if (o.kind == BM_OP_LLM_BWD) {
     const int s = o.chunk * P + r;
@@ -235,7 +240,7 @@ static void recvs_before(const bm_sched_cfg& c, int r, const bm_op& o, std::vect
     if (s == P * V - 1 && c.gen_place == BM_GEN_DP_SHARD)
       for (int q = 0; q < P; ++q)
         if (q != r) out.push_back(mk(BM_OP_RECV, o.mb, -1, -1, q, BM_PAY_GENGRAD));
-  } else if (o.kind == BM_OP_ENC_BWD && r != 0) {
+  } else if (o.kind == BM_OP_ENC_BWD && r != 0 && c.enc_place == BM_ENC_DP_UNIT) {
     out.push_back(mk(BM_OP_RECV, o.mb, -1, o.unit, 0, BM_PAY_EMBGRAD));
   } else if (o.kind == BM_OP_GEN_FWD && c.gen_place == BM_GEN_DP_SHARD && r != P - 1) {
     out.push_back(mk(BM_OP_RECV, o.mb, -1, -1, P - 1, BM_PAY_GENIN));
@@ -253,9 +258,9 @@ static void sends_after(const bm_sched_cfg& c, int r, const bm_op& o, std::vecto
   } else if (o.kind == BM_OP_LLM_BWD) {
     const int s = o.chunk * P + r;
     if (s > 0 && (s - 1) % P != r) out.push_back(mk(BM_OP_SEND, o.mb, o.chunk, -1, (s - 1) % P, BM_PAY_GRAD));
-    if (s == 0 && c.enc_place != BM_ENC_NONE && o.mb % P != 0)
+    if (s == 0 && c.enc_place == BM_ENC_DP_UNIT && o.mb % P != 0)
       out.push_back(mk(BM_OP_SEND, o.mb, -1, o.mb / P, o.mb % P, BM_PAY_EMBGRAD));
-  } else if (o.kind == BM_OP_ENC_FWD && r != 0) {
+  } else if (o.kind == BM_OP_ENC_FWD && r != 0 && c.enc_place == BM_ENC_DP_UNIT) {
     out.push_back(mk(BM_OP_SEND, o.mb, -1, o.unit, 0, BM_PAY_EMB));
   } else if (o.kind == BM_OP_GEN_BWD && c.gen_place == BM_GEN_DP_SHARD && r != P - 1) {
     out.push_back(mk(BM_OP_SEND, o.mb, -1, -1, P - 1, BM_PAY_GENGRAD));
@@ -365,7 +370,8 @@ static void verify_deps(const bm_sched_cfg& c, const std::vector<std::vector<bm_
       if (o.kind == BM_OP_LLM_FWD) {
         const int s = o.chunk * P + r;
         if (s > 0) dep((s - 1) % P, BM_OP_LLM_FWD, o.mb, (s - 1) / P, me);
-        else if (c.enc_place != BM_ENC_NONE) dep(o.mb % P, BM_OP_ENC_FWD, o.mb, -1, me);
+        else if (c.enc_place == BM_ENC_DP_UNIT) dep(o.mb % P, BM_OP_ENC_FWD, o.mb, -1, me);
+        else if (c.enc_place == BM_ENC_ENTRY_STAGE) dep(0, BM_OP_ENC_FWD, o.mb, -1, me);
       } else if (o.kind == BM_OP_LLM_BWD) {
         const int s = o.chunk * P + r;
         dep(r, BM_OP_LLM_FWD, o.mb, o.chunk, me);
@@ -464,7 +470,7 @@ static bm_schedule* build(const bm_sched_cfg& c) {
   for (auto& kv : scnt) s->rings[kv.first] = {K[kv.first], kv.second};
   int64_t makespan = 0;
   for (auto e : T.en) makespan = std::max(makespan, e);
-  const bool enc = c.enc_place != BM_ENC_NONE;
+  const bool enc = c.enc_place == BM_ENC_DP_UNIT;
   const int ws = enc ? w_star(base[0], P, M) : 0;
   for (int r = 0; r < P; ++r) {
     bm_sched_stats st;

@@ -26,7 +26,15 @@ def main():
     from paper_2605_25451_b200.runtime import Runtime
     cfg = get_config(name, P=P, M=M, V=V)
     W, B = make_weights(cfg), make_batch(cfg)
-    rt = Runtime(cfg, dtype, rank=rank, world=world, sched_kw={"gen_place": gen})
+    # strategy spec: "<gen_place>", "entry_stage+<gen_place>" (memory-efficient baseline),
+    # "ce" (compute-efficient baseline: all encoder forwards first, W = M / P)
+    if gen == "ce":
+        kw = {"warmup_units": M // P}
+    elif gen.startswith("entry_stage+"):
+        kw = {"enc_place": "entry_stage", "gen_place": gen.split("+")[1]}
+    else:
+        kw = {"gen_place": gen}
+    rt = Runtime(cfg, dtype, rank=rank, world=world, sched_kw=kw)
     rt.load_weights(W)
     db = rt.device_batch(B)
     for _ in range(2):

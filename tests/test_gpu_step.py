@@ -73,6 +73,22 @@ def test_step_single_gpu(oracle_cache, dtype, M, V):
     rt.close()
 
 
+@pytest.mark.parametrize("kw", [{"enc_place": "entry_stage", "gen_place": "last_stage"}, {"warmup_units": 4}])
+def test_step_single_gpu_baselines(oracle_cache, kw):
+    from paper_2605_25451_b200.runtime import Runtime
+    cfg = get_config("C1", P=1, M=4, V=1)
+    W, B, (loss_ref, per_ref, G_ref) = reference(oracle_cache, cfg)
+    rt = Runtime(cfg, "f32", sched_kw=kw)
+    rt.load_weights(W)
+    rt.step(rt.device_batch(B))
+    torch.cuda.synchronize()
+    loss, _, _ = rt.losses()
+    assert abs(loss - loss_ref) <= 1e-4 * abs(loss_ref)
+    bad = {n: rel(rt.grad(n), G_ref[n]) for n in rt.names()}
+    assert not {k: v for k, v in bad.items() if v > 1e-4}
+    rt.close()
+
+
 @pytest.mark.parametrize("dtype", ["f32", "bf16"])
 @pytest.mark.parametrize("M,V", [(4, 1), (4, 2)])
 def test_step_single_gpu_medium(oracle_cache, dtype, M, V):
@@ -103,7 +119,9 @@ def _torchrun(nproc, *args, timeout=600):
 
 
 @pytest.mark.parametrize("P,M,V,dtype,gen", [(2, 4, 1, "f32", "dp_shard"), (2, 4, 1, "bf16", "dp_shard"),
-                                           (2, 8, 2, "f32", "dp_shard"), (2, 4, 1, "f32", "last_stage")])
+                                           (2, 8, 2, "f32", "dp_shard"), (2, 4, 1, "f32", "last_stage"),
+                                           (2, 4, 1, "f32", "entry_stage+last_stage"),
+                                           (2, 4, 1, "bf16", "ce")])
 def test_step_two_gpus(P, M, V, dtype, gen):
     if torch.cuda.device_count() < P:
         pytest.skip(f"needs {P} GPUs")

@@ -162,3 +162,19 @@ def test_interpreter_matches_sequential(P, M, V, gen):
         assert np.linalg.norm(G2[k] - G[k]) <= 1e-12 * max(np.linalg.norm(G[k]), 1e-30), k
     # per-microbatch CE identical bitwise (forward is order independent)
     assert [a for a, _ in per] == [a for a, _ in per2]
+
+
+@pytest.mark.parametrize("P,M,V,enc,gen,W", [(2, 4, 1, "entry_stage", "last_stage", 0), (2, 4, 1, "entry_stage", "dp_shard", 0),
+                                             (4, 8, 1, "dp_unit", "dp_shard", 2), (2, 8, 2, "entry_stage", "last_stage", 0)])
+def test_interpreter_baseline_strategies(P, M, V, enc, gen, W):
+    # the baselines (memory-efficient entry-stage encoder, compute-efficient W = M/P)
+    # reach the same gradients as the sequential definition
+    cfg = get_config("C1", P=P, M=M, V=V)
+    Wt, B = make_weights(cfg), make_batch(cfg)
+    loss, per, G = om.step_fp64(cfg, Wt, B)
+    sched = S.build(S.SchedCfg(P, M, V, llm_sched=cfg.llm_sched, enc_place=enc, gen_place=gen,
+                               warmup_units=W if W else 0))
+    loss2, per2, G2, _ = interp.run(sched, cfg, Wt, B)
+    assert abs(loss2 - loss) <= 1e-12 * abs(loss)
+    for k in G:
+        assert np.linalg.norm(G2[k] - G[k]) <= 1e-12 * max(np.linalg.norm(G[k]), 1e-30), k

@@ -284,3 +284,54 @@ def test_serialization_golden():
     path = os.path.join(os.path.dirname(__file__), "golden", "sched_P2_M4_V1.tsv")
     with open(path) as f:
         assert S.serialize(S.build(cfg_of(2, 4, 1))) == f.read()
+
+
+# --------------------------------------------------------------------------- f1 baselines
+def test_memory_efficient_baseline_structure():
+    # S:204 / P:150-151 (Fig. 3): EncFwd(mb) immediately precedes the entry-stage F(mb, 0);
+    # S:205 / P:164: peak live encoder microbatches on rank 0 <= P; S:206 strict chain at P=1
+    s = S.build(cfg_of(4, 8, 1, enc_place="entry_stage", gen_place="last_stage"))
+    ops0 = [o for o in s.ranks[0] if o.kind in S.COMPUTE_KINDS]
+    for i, o in enumerate(ops0):
+        if o.kind == "LlmFwd":
+            assert ops0[i - 1].kind == "EncFwd" and ops0[i - 1].mb == o.mb
+        if o.kind == "LlmBwd":
+            assert ops0[i + 1].kind == "EncBwd" and ops0[i + 1].mb == o.mb
+    assert s.stats[0].peak_enc_units == 4 and all(st.peak_enc_units == 0 for st in s.stats[1:])
+    assert all(o.kind not in ("EncFwd", "EncBwd") for r in range(1, 4) for o in s.ranks[r])
+    assert not any(o.payload in ("emb", "embgrad") for ops in s.ranks for o in ops)
+    t = S.build(cfg_of(1, 2, 1, enc_place="entry_stage", gen_place="last_stage"))
+    assert [o.kind for o in t.ranks[0]] == ["EncFwd", "LlmFwd", "GenFwd", "GenBwd", "LlmBwd", "EncBwd",
+                                            "EncFwd", "LlmFwd", "GenFwd", "GenBwd", "LlmBwd", "EncBwd"]
+
+
+@pytest.mark.parametrize("P,M", [(4, 16), (4, 64), (2, 8)])
+def test_compute_efficient_baseline_memory(P, M):
+    # S:195-196 / P:132: all encoder forwards first -> (M/P) live units per rank,
+    # i.e. memory that grows with M, while BigMac's window stays at W*
+    ce = S.build(cfg_of(P, M, 1, warmup_units=M // P))
+    ops0 = ce.ranks[0]
+    first_llm = next(i for i, o in enumerate(ops0) if o.kind == "LlmFwd")
+    assert sum(1 for o in ops0[:first_llm] if o.kind == "EncFwd") == M // P
+    assert all(st.peak_enc_units == M // P for st in ce.stats)
+    bm = S.build(cfg_of(P, M, 1))
+    assert all(st.peak_enc_units == bm.stats[0].w_star for st in bm.stats)
+
+
+def test_bigmac_vs_baselines_des():
+    # P:229 / S:305: BigMac matches the compute-efficient time; S:315 / S:552: with
+    # heterogeneous encoder costs the memory-efficient pipeline is strictly slower
+    P, M = 4, 16
+    enc_cost = [1 if m % 2 else 3 for m in range(M)]
+
+    def cost(r, op):
+        if op.kind in ("EncFwd", "EncBwd"):
+            return enc_cost[op.mb] * (1 if op.kind == "EncFwd" else 2)
+        return {"LlmFwd": 2, "LlmBwd": 4, "GenFwd": 0, "GenBwd": 0}[op.kind]
+    bigmac = simulate(S.build(cfg_of(P, M, 1, gen_place="none")).ranks, cost)[0]
+    ce = simulate(S.build(cfg_of(P, M, 1, gen_place="none", warmup_units=M // P)).ranks, cost)[0]
+    me = simulate(S.build(cfg_of(P, M, 1, enc_place="entry_stage", gen_place="none")).ranks, cost)[0]
+    assert me > bigmac
+    # per-rank encoder work differs across ranks (data heterogeneity), so both DP designs
+    # pay the slowest rank's encoder time per unit; BigMac never exceeds compute-efficient
+    assert bigmac <= ce
