@@ -146,7 +146,8 @@ def config_dict(cfg, N):
             "global_batch": cfg.M, "seq_len": cfg.S, "parallelism": f"pp{N}",
             "stages": N, "microbatches": cfg.M, "vchunks": cfg.V,
             "n_mod_law": list(cfg.n_mod_law), "n_gen_law": list(cfg.n_gen_law),
-            "l2_policy": "working set (weights + activations, GBs) >> 126 MB L2; no flush"}
+            "l2_policy": "working set (weights + activations, GBs) >> 126 MB L2; no flush",
+            "strategy": getattr(cfg, "_strategy", "bigmac")}
 
 
 def run_reference(args):
@@ -193,6 +194,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--ref-rows", type=int, default=512)
+    ap.add_argument("--strategy", default="bigmac", choices=["bigmac", "compute_efficient", "memory_efficient"],
+                    help="bigmac (default); the paper's baselines on the same executor (P:129-156)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
@@ -217,7 +220,9 @@ def main():
     cfg = workload(args, N)
     if args.warmup < 3:
         raise SystemExit("--warmup must be >= 3")
-    rt = Runtime(cfg, args.dtype, rank=rank, world=world, group=group)
+    sched_kw = {"bigmac": {}, "compute_efficient": {"warmup_units": cfg.M // N},
+                "memory_efficient": {"enc_place": "entry_stage", "gen_place": "last_stage"}}[args.strategy]
+    rt = Runtime(cfg, args.dtype, rank=rank, world=world, group=group, sched_kw=sched_kw)
     rt.init_random_weights(seed=1)
     batch = make_batch(cfg)
     db = rt.device_batch(batch)
@@ -348,6 +353,7 @@ def main():
                          f"({dt:.1f} s); samples/s extrapolated by the step's algorithmic FLOPs per sample"}
 
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": N, "steps": args.steps,
+            "strategy": args.strategy,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
             "config": config_dict(cfg, N),
