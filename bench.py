@@ -19,6 +19,10 @@ import argparse
 import json
 import math
 import os
+
+# one hardware work queue per stream (compute, P-1 comm, generator, NCCL): a comm
+# stream parked on a credit wait must not block unrelated streams sharing its queue
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 import statistics
 import subprocess
 import sys

@@ -241,6 +241,11 @@ bm_status bm_ctx_gemm_stats(bm_ctx* c, int64_t* n_gemm, double* flops, double* m
  * (stage-boundary, gather/scatter payloads over NVLink): message count,
  * bytes, summed device milliseconds of the copies on the comm streams. */
 bm_status bm_ctx_comm_stats(bm_ctx* c, int64_t* n_msgs, double* bytes, double* ms);
+/* Diagnostics: text dump of this rank's receive/credit flags and (with
+ * BM_DEBUG_PROGRESS=1 at bm_ctx_create time) the index of the last op each of its
+ * streams finished.  Reads device memory on a private non-blocking stream, so
+ * it works while the step's streams are blocked. */
+bm_status bm_ctx_debug_dump(bm_ctx* c, char* buf, size_t cap);
 void bm_ctx_destroy(bm_ctx* c);
 
 #ifdef __cplusplus

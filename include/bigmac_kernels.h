@@ -105,6 +105,19 @@ bm_status bm_k_mse_fwd_bwd(int32_t dtype, int32_t n, int32_t dt, const void* out
 /* Elementwise helpers used by the executor. */
 bm_status bm_k_add(int32_t dtype, int64_t n, const void* a, const void* b, void* out, void* stream);
 bm_status bm_k_cast(int32_t src_dtype, int32_t dst_dtype, int64_t n, const void* src, void* dst, void* stream);
+/* Byte copy / zero fill on SMs (16-byte vectors when dst, src and bytes are 16-byte
+ * aligned).  dst may be a peer GPU's IPC-mapped buffer (NVLink stores).  The
+ * executor moves every byte inside a step with these kernels, never with a
+ * copy-engine memcpy.  max_ctas <= 0: the elementwise grid (8 CTAs per SM). */
+bm_status bm_k_copy(void* dst, const void* src, int64_t bytes, int32_t max_ctas, void* stream);
+bm_status bm_k_zero(void* dst, int64_t bytes, void* stream);
+
+/* Load every kernel of the library onto the current device now (synchronous,
+ * idempotent).  Under CUDA lazy module loading a kernel is otherwise loaded at its
+ * first launch, and that load blocks while any stream of the context is parked on
+ * a cross-GPU flag wait -- a device-wide stall of the pipelined step (measured:
+ * compute-efficient schedule, P = 4).  bm_ctx_create calls it. */
+bm_status bm_k_preload(void);
 
 #ifdef __cplusplus
 }

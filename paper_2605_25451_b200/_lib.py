@@ -101,6 +101,7 @@ SIGNATURES = {
     "bm_ctx_set_timing": [_P, _I32],
     "bm_ctx_gemm_stats": [_P, C.POINTER(_I64), C.POINTER(C.c_double), C.POINTER(C.c_double)],
     "bm_ctx_comm_stats": [_P, C.POINTER(_I64), C.POINTER(C.c_double), C.POINTER(C.c_double)],
+    "bm_ctx_debug_dump": [_P, C.c_char_p, _SZ],
     "bm_ctx_destroy": [_P],
     # bigmac_kernels.h
     "bm_k_gemm": [_I32, _I32, _I32, _I32, _P, _I64, _I32, _P, _I64, _I32, _P, _I64, _I32, _I32, _P, _I64, _F, _P],
@@ -121,6 +122,9 @@ SIGNATURES = {
     "bm_k_mse_fwd_bwd": [_I32, _I32, _I32, _P, _P, _F, _F, _F, _P, _P, _P],
     "bm_k_add": [_I32, _I64, _P, _P, _P, _P],
     "bm_k_cast": [_I32, _I32, _I64, _P, _P, _P],
+    "bm_k_copy": [_P, _P, _I64, _I32, _P],
+    "bm_k_zero": [_P, _I64, _P],
+    "bm_k_preload": [],
 }
 RESTYPE = {"bm_last_error": C.c_char_p, "bm_schedule_free": None, "bm_ctx_destroy": None,
            "bm_k_rmsnorm_bwd_scratch": C.c_int64, "bm_k_embed_bwd_scratch": C.c_int64}

@@ -82,6 +82,9 @@ __device__ __forceinline__ void pdl_enter() {
   pdl_trigger();
 }
 
+// debug hook (BM_DEBUG_PROGRESS): called after every library kernel launch
+extern void (*g_launch_hook)(cudaStream_t, const void*);
+
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
                             Args&&... args) {
@@ -95,7 +98,9 @@ inline cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl_enabled() ? 1 : 0;
-  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+  if (g_launch_hook) g_launch_hook(st, (const void*)kern);
+  return e;
 }
 
 // launch census (kernels launched through the library)

@@ -5,8 +5,10 @@
 // reductions in fp32 with fixed (deterministic) shuffle/shared-memory trees,
 // and accumulate weight-like gradients (RMSNorm gains, text table) through
 // deterministic two-pass reductions so reruns are bitwise identical.
+#include <algorithm>
 #include <cfloat>
 
+#include <vector>
 #include "common.cuh"
 
 namespace bm {
@@ -278,6 +280,63 @@ __global__ void cast_kernel(int64_t n, const S* __restrict__ a, D* __restrict__ 
   pdl_enter();
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
     o[e] = from_f<D>(to_f(a[e]));
+}
+
+// ------------------------------------------------------------------ copies / fills on SMs
+// Every byte move inside the step runs as a kernel on the issuing stream's own
+// compute channel: a copy-engine copy can queue in a copy channel behind another
+// stream's copy that is parked on a peer credit wait ("copy
+// channels"), turning an acyclic schedule into a device deadlock.  dst may be a
+// peer GPU's IPC-mapped buffer (NVLink stores).
+__global__ void copy16_kernel(int64_t n16, const uint4* __restrict__ src, uint4* __restrict__ dst) {
+  pdl_enter();
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  for (; e + 3 * stride < n16; e += 4 * stride) {
+    const uint4 a = __ldg(src + e), b = __ldg(src + e + stride), c = __ldg(src + e + 2 * stride),
+                d = __ldg(src + e + 3 * stride);
+    dst[e] = a;
+    dst[e + stride] = b;
+    dst[e + 2 * stride] = c;
+    dst[e + 3 * stride] = d;
+  }
+  for (; e < n16; e += stride) dst[e] = __ldg(src + e);
+}
+__global__ void copy1_kernel(int64_t n, const uint8_t* __restrict__ src, uint8_t* __restrict__ dst) {
+  pdl_enter();
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
+    dst[e] = src[e];
+}
+__global__ void zero16_kernel(int64_t n16, uint4* __restrict__ dst) {
+  pdl_enter();
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n16; e += (int64_t)gridDim.x * blockDim.x)
+    dst[e] = make_uint4(0, 0, 0, 0);
+}
+__global__ void zero1_kernel(int64_t n, uint8_t* __restrict__ dst) {
+  pdl_enter();
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) dst[e] = 0;
+}
+
+// ------------------------------------------------------------------ flag wait on an SM
+// One thread polls a 32-bit flag (written by a peer GPU over NVLink or by another
+// stream) until it reaches v (unsigned, >=).  Used instead of a stream wait-value
+// operation when BM_WAIT=spin.  Traps after 60 s so a lost message becomes an error.
+__global__ void spin_wait_kernel(const uint32_t* flag, uint32_t v) {
+  if (threadIdx.x != 0) return;
+  uint64_t t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (;;) {
+    uint32_t x;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(x) : "l"(flag) : "memory");
+    if ((int32_t)(x - v) >= 0) break;
+    __nanosleep(200);
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 > 60ull * 1000000000ull) {
+      printf("bigmac: spin wait timeout flag=%p have=%u want=%u\n", flag, x, v);
+      __trap();
+    }
+  }
 }
 
 // ------------------------------------------------------------------ embed_preprocess
@@ -732,6 +791,35 @@ bm_status add(int64_t n, const T* a, const T* b, T* o, cudaStream_t st) {
   BM_CUDA_TRY(cudaGetLastError());
   return BM_OK;
 }
+bm_status copy_bytes(void* dst, const void* src, int64_t bytes, int max_ctas, cudaStream_t st) {
+  if (bytes <= 0) return BM_OK;
+  const bool v = ((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src) | (uintptr_t)bytes) & 15) == 0;
+  const int64_t items = v ? bytes / 16 : bytes;
+  int grid = ew_grid(v ? items / 4 + 1 : items);
+  if (max_ctas > 0) grid = std::min(grid, max_ctas);
+  if (v) BM_CUDA_TRY(launch_k(copy16_kernel, dim3(grid), dim3(256), 0, st, items, (const uint4*)src, (uint4*)dst));
+  else BM_CUDA_TRY(launch_k(copy1_kernel, dim3(grid), dim3(256), 0, st, items, (const uint8_t*)src, (uint8_t*)dst));
+  count_launch();
+  BM_CUDA_TRY(cudaGetLastError());
+  return BM_OK;
+}
+bm_status spin_wait(const uint32_t* flag, uint32_t v, cudaStream_t st) {
+  spin_wait_kernel<<<1, 32, 0, st>>>(flag, v);
+  if (g_launch_hook) g_launch_hook(st, (const void*)spin_wait_kernel);
+  count_launch();
+  BM_CUDA_TRY(cudaGetLastError());
+  return BM_OK;
+}
+bm_status zero_bytes(void* dst, int64_t bytes, cudaStream_t st) {
+  if (bytes <= 0) return BM_OK;
+  const bool v = ((reinterpret_cast<uintptr_t>(dst) | (uintptr_t)bytes) & 15) == 0;
+  const int64_t items = v ? bytes / 16 : bytes;
+  if (v) BM_CUDA_TRY(launch_k(zero16_kernel, dim3(ew_grid(items)), dim3(256), 0, st, items, (uint4*)dst));
+  else BM_CUDA_TRY(launch_k(zero1_kernel, dim3(ew_grid(items)), dim3(256), 0, st, items, (uint8_t*)dst));
+  count_launch();
+  BM_CUDA_TRY(cudaGetLastError());
+  return BM_OK;
+}
 bm_status cast(int sd, int dd, int64_t n, const void* s, void* d, cudaStream_t st) {
   if (n == 0) return BM_OK;
   if (sd == BM_F32 && dd == BM_BF16) BM_CUDA_TRY(launch_k(cast_kernel<float, bf16>, dim3(ew_grid(n)), dim3(256), 0, st, n, (const float*)s, (bf16*)d));
@@ -771,6 +859,30 @@ bm_status loss_finalize(int M, float* loss, cudaStream_t st) {
   count_launch();
   BM_CUDA_TRY(cudaGetLastError());
   return BM_OK;
+}
+
+// every kernel of this file (bm::preload_kernels)
+template <typename T>
+static void preload_t(std::vector<const void*>& v) {
+  for (const void* f : {(const void*)rmsnorm_fwd_kernel<T>, (const void*)rmsnorm_bwd_kernel<T>,
+                        (const void*)rmsnorm_dg_partial_kernel<T>, (const void*)rmsnorm_bwd_fused_kernel<T, 1>,
+                        (const void*)rmsnorm_bwd_fused_kernel<T, 2>, (const void*)rmsnorm_bwd_fused_kernel<T, 4>,
+                        (const void*)rmsnorm_bwd_fused_kernel<T, 8>, (const void*)rmsnorm_bwd_fused_kernel<T, 16>,
+                        (const void*)swiglu_fwd_kernel<T>, (const void*)swiglu_bwd_kernel<T>,
+                        (const void*)gelu_fwd_kernel<T>, (const void*)gelu_bwd_kernel<T>, (const void*)add_kernel<T>,
+                        (const void*)embed_fwd_kernel<T>, (const void*)embed_segsum_kernel<T>,
+                        (const void*)ce_row_kernel<T>, (const void*)ce_row_vec_kernel<T>, (const void*)mse_kernel<T>})
+    v.push_back(f);
+}
+void preload_elementwise(std::vector<const void*>& v) {
+  preload_t<bf16>(v);
+  preload_t<float>(v);
+  for (const void* f : {(const void*)cast_kernel<float, bf16>, (const void*)cast_kernel<bf16, float>,
+                        (const void*)cast_kernel<float, float>, (const void*)cast_kernel<bf16, bf16>,
+                        (const void*)colsum_accum_kernel, (const void*)colsum2_accum_kernel, (const void*)copy16_kernel,
+                        (const void*)copy1_kernel, (const void*)zero16_kernel, (const void*)zero1_kernel,
+                        (const void*)spin_wait_kernel, (const void*)embed_sort_kernel, (const void*)sum_scale_kernel})
+    v.push_back(f);
 }
 
 }  // namespace bm

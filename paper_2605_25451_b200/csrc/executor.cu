@@ -18,6 +18,7 @@
 
 #include <algorithm>
 #include <array>
+#include <cstdio>
 #include <cstring>
 #include <map>
 #include <string>
@@ -222,6 +223,11 @@ struct bm_ctx {
   char *ws = nullptr, *ws_gen = nullptr;  // split-K workspaces of the two compute streams
   int64_t ws_bytes = 0;
   void* cur_ws = nullptr;
+  // BM_DEBUG_PROGRESS=1: each stream writes the index of the last op it finished
+  // into a progress word (main, gen, one per comm peer), readable by bm_ctx_debug_dump
+  bool debug_progress = getenv("BM_DEBUG_PROGRESS") != nullptr;
+  uint32_t* progress = nullptr;  // [2 + P] words
+  volatile uint32_t* progress_h = nullptr;  // debug: host-mapped copy (read without CUDA calls)
   char* embscr = nullptr;
   char* logits = nullptr;
   float* ce_scr = nullptr;
@@ -251,6 +257,7 @@ struct bm_ctx {
   int64_t stash_peak[3] = {0, 0, 0};
   // per-step state
   cudaStream_t st = nullptr;
+  cudaStream_t st_main = nullptr;   // the caller's stream during bm_step (debug hook)
   std::vector<int> llm_free;
   std::map<std::pair<int, int>, int> llm_live;
   std::vector<const char*> mb_patches, mb_targets;
@@ -275,6 +282,9 @@ struct bm_ctx {
   // fused SwiGLU GEMM epilogues (bm_k_gemm_swiglu / _dswiglu); off by default: measured
   // slower than GEMM + the separate vectorised kernel (profiles/r01/gemm_bench_v4)
   bool fuse_swiglu = getenv("BM_FUSE_SWIGLU") != nullptr;
+  bool peer_copy_ce = getenv("BM_PEER_COPY") && std::string(getenv("BM_PEER_COPY")) == "ce";
+  int peer_copy_ctas = getenv("BM_PEER_COPY_CTAS") ? std::atoi(getenv("BM_PEER_COPY_CTAS")) : 32;
+  bool spin_wait = getenv("BM_WAIT") && std::string(getenv("BM_WAIT")) == "spin";
   std::vector<cudaEvent_t> tev[2];
   size_t tev_used[2] = {0, 0};
   double tflop_pending[2] = {0, 0};
@@ -290,6 +300,8 @@ struct bm_ctx {
   std::map<std::array<int, 4>, std::pair<int64_t, double>> shape_ms;  // BM_GEMM_LOG=1 breakdown
   ~bm_ctx();
 };
+
+static bm_ctx* g_dbg_ctx = nullptr;   // BM_DEBUG_PROGRESS launch hook target
 
 bm_ctx::~bm_ctx() {
   for (auto s_ : comm_st)
@@ -312,6 +324,11 @@ bm_ctx::~bm_ctx() {
   for (size_t r = 0; r < peer.size(); ++r)
     if (peer[r] && (int)r != rank) cudaIpcCloseMemHandle(peer[r]);
   if (nc && nccl().ok) nccl().CommDestroy(nc);
+  if (progress_h) cudaFreeHost((void*)progress_h);
+  if (g_dbg_ctx == this) {
+    g_dbg_ctx = nullptr;
+    g_launch_hook = nullptr;
+  }
   cudaGetLastError();  // never leave a sticky-looking error for the caller's next API call
 }
 
@@ -444,6 +461,7 @@ static void work_layout(bm_ctx& c, char* base) {
   for (int i = 0; i < 2; ++i) c.gout[i] = b.take(ng * d * es);
   c.emb_local = b.take(n * d * es);
   c.loss = (float*)b.take((2 * (int64_t)c.M + 1) * 4);
+  c.progress = (uint32_t*)b.take((2 + c.P) * 64);
   // host-batch staging
   c.ld_patch_stage = round8(m.d_in);
   c.st_patches = b.take((int64_t)c.M * m.max_n_mod * c.ld_patch_stage * es);
@@ -587,9 +605,29 @@ static bm_status add_(bm_ctx& c, int64_t n, const void* a, const void* b, void* 
             add<float>(n, (const float*)a, (const float*)b, (float*)o, c.st));
 }
 static bm_status d2d(bm_ctx& c, void* dst, const void* src, int64_t bytes) {
-  if (bytes > 0) BM_CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, c.st));
-  return BM_OK;
+  return copy_bytes(dst, src, bytes, 0, c.st);
 }
+// BM_DEBUG_PROGRESS: after every kernel launch, the issuing stream writes the global
+// launch number into word 1 of its progress block; the host logs (number, stream,
+// kernel name), so a dump names the last kernel each stream finished.
+static uint32_t g_dbg_launch = 0;
+static void dbg_launch_hook(cudaStream_t st, const void* kern) {
+  bm_ctx* c = g_dbg_ctx;
+  if (!c || !c->progress) return;
+  int slot = -1;
+  if (st == c->st_main) slot = 0;
+  else if (st == c->gen_st) slot = 1;
+  else
+    for (int q = 0; q < c->P; ++q)
+      if (q != c->rank && st == c->comm_st[q]) slot = 2 + q;
+  if (slot < 0) return;
+  ++g_dbg_launch;
+  const char* name = nullptr;
+  if (cudaFuncGetName(&name, kern) != cudaSuccess) { name = "?"; cudaGetLastError(); }
+  std::fprintf(stderr, "[bm r%d] launch %u stream %d %s\n", c->rank, g_dbg_launch, slot, name ? name : "?");
+  drv().write32((CUstream)st, (CUdeviceptr)(c->progress + 16 * slot + 1), g_dbg_launch, 0);
+}
+
 static cudaEvent_t next_event(bm_ctx& c) {
   cudaEvent_t e = c.evpool[c.evnext];
   c.evnext = (c.evnext + 1) % c.evpool.size();
@@ -715,7 +753,7 @@ static bm_status op_llm_fwd(bm_ctx& c, const bm_op& o, const RecvState& rs) {
     // last stage: final norm, LM head + CE (fwd and bwd through the head), generator inputs
     const int n_mod = c.n_mod[mb], n_text = m.S - n_mod;
     BM_TRY(norm_fwd(c, m.S, m.d, sl.x[c.lps], P_(c, "llm.final_norm"), sl.Hn, sl.rstd_f));
-    BM_CUDA_TRY(cudaMemsetAsync(sl.dHn, 0, (size_t)n_mod * d * es, c.st));
+    BM_TRY(zero_bytes(sl.dHn, (int64_t)n_mod * d * es, c.st));
     if (n_text > 0) {
       const char* hn_text = sl.Hn + (int64_t)n_mod * d * es;
       BM_TRY(lin_fwd(c, n_text, m.d, m.vocab, hn_text, m.d, P_(c, "llm.head"), LD_(c, "llm.head"), c.logits));
@@ -867,6 +905,31 @@ static int64_t payload_bytes(const bm_ctx& c, const bm_op& o, int src_rank_for_s
   }
 }
 
+// NVLink write of one message into the peer's receive slot.  Default: an SM copy
+// kernel on the comm stream's own compute channel.  A copy-engine copy would sit in
+// a copy channel shared with other streams; when this stream is parked on a credit
+// wait, those streams' copies queue behind it and the acyclic schedule deadlocks
+// (measured: compute-efficient strategy, P = 4).  BM_PEER_COPY=ce restores the
+// copy engine for experiments.
+static bm_status peer_copy(bm_ctx& c, char* dst, const char* src, int64_t bytes, cudaStream_t cs) {
+  if (c.peer_copy_ce) {
+    BM_CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, cs));
+    return BM_OK;
+  }
+  return copy_bytes(dst, src, bytes, c.peer_copy_ctas, cs);
+}
+
+// stream-ordered wait until a local flag (written by a peer) reaches v
+static bm_status wait_flag(bm_ctx& c, cudaStream_t on, char* flag, uint32_t v, const char* what) {
+  if (c.spin_wait) return spin_wait((const uint32_t*)flag, v, on);
+  CUresult r = drv().wait32((CUstream)on, (CUdeviceptr)flag, v, CU_STREAM_WAIT_VALUE_GEQ);
+  if (r != CUDA_SUCCESS) {
+    set_error(std::string("cuStreamWaitValue32 (") + what + ") failed " + std::to_string((int)r));
+    return BM_E_CUDA;
+  }
+  return BM_OK;
+}
+
 static bm_status do_send(bm_ctx& c, const bm_op& o) {
   const Chan& ch = c.chans[c.chan_idx.at(std::make_tuple(c.rank, o.peer, o.payload))];
   cudaStream_t cs = c.comm_st[o.peer];
@@ -877,9 +940,7 @@ static bm_status do_send(bm_ctx& c, const bm_op& o) {
   BM_CUDA_TRY(cudaStreamWaitEvent(cs, c.producer_ev, 0));
   const uint32_t base = (uint32_t)(c.step * ch.nmsg);
   if (o.seq >= ch.K) {
-    CUresult r = drv().wait32((CUstream)cs, (CUdeviceptr)(c.comm + ch.credit_off), base + (uint32_t)(o.seq - ch.K) + 1,
-                              CU_STREAM_WAIT_VALUE_GEQ);
-    if (r != CUDA_SUCCESS) { set_error("cuStreamWaitValue32 (credit) failed " + std::to_string((int)r)); return BM_E_CUDA; }
+    BM_TRY(wait_flag(c, cs, c.comm + ch.credit_off, base + (uint32_t)(o.seq - ch.K) + 1, "credit"));
   }
   const char* src;
   int64_t bytes;
@@ -904,11 +965,11 @@ static bm_status do_send(bm_ctx& c, const bm_op& o) {
       ev.push_back(e);
     }
     BM_CUDA_TRY(cudaEventRecord(ev[2 * k], cs));
-    BM_CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, cs));
+    BM_TRY(peer_copy(c, dst, src, bytes, cs));
     BM_CUDA_TRY(cudaEventRecord(ev[2 * k + 1], cs));
     c.cbytes[pool].push_back(bytes);
   } else if (bytes > 0) {
-    BM_CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, cs));
+    BM_TRY(peer_copy(c, dst, src, bytes, cs));
   }
   CUresult r = drv().write32((CUstream)cs, (CUdeviceptr)(c.peer[o.peer] + ch.flag_off), base + (uint32_t)o.seq + 1, 0);
   if (r != CUDA_SUCCESS) { set_error("cuStreamWriteValue32 (data flag) failed " + std::to_string((int)r)); return BM_E_CUDA; }
@@ -925,10 +986,7 @@ static bm_status do_send(bm_ctx& c, const bm_op& o) {
 static bm_status do_recv_wait(bm_ctx& c, const bm_op& o, cudaStream_t on) {
   const Chan& ch = c.chans[c.chan_idx.at(std::make_tuple(o.peer, c.rank, o.payload))];
   const uint32_t base = (uint32_t)(c.step * ch.nmsg);
-  CUresult r = drv().wait32((CUstream)on, (CUdeviceptr)(c.comm + ch.flag_off), base + (uint32_t)o.seq + 1,
-                            CU_STREAM_WAIT_VALUE_GEQ);
-  if (r != CUDA_SUCCESS) { set_error("cuStreamWaitValue32 (data) failed " + std::to_string((int)r)); return BM_E_CUDA; }
-  return BM_OK;
+  return wait_flag(c, on, c.comm + ch.flag_off, base + (uint32_t)o.seq + 1, "data");
 }
 
 static bm_status do_release(bm_ctx& c, const bm_op& o, cudaStream_t on) {
@@ -1022,7 +1080,8 @@ bm_status bm_ctx_create(const bm_model_cfg* mc, const bm_schedule* s, int32_t ra
     while (j < ops.size() && ops[j].kind > BM_OP_GEN_BWD) ++j;
     c->consumer_kind[i] = j < ops.size() ? ops[j].kind : -1;
   }
-  c->use_gen_stream = c->P > 1 && s->cfg.gen_place == BM_GEN_DP_SHARD;
+  c->use_gen_stream = c->P > 1 && s->cfg.gen_place == BM_GEN_DP_SHARD &&
+                      !(getenv("BM_GEN_STREAM") && getenv("BM_GEN_STREAM")[0] == '0');
   *out = c;
   return BM_OK;
 }
@@ -1040,11 +1099,26 @@ bm_status bm_ctx_bind(bm_ctx* c, const bm_buffers* b) {
   BM_CHECK_ARG(c && b && b->weights && b->grads && b->work && b->comm, "null buffer");
   for (const void* p : {b->weights, b->grads, b->work, b->comm})
     BM_CHECK_ARG((reinterpret_cast<uintptr_t>(p) & 255) == 0, "buffers must be 256-byte aligned");
+  // every kernel loaded before the first step (lazy loading stalls behind flag waits)
+  BM_TRY(preload_kernels());
   c->W = (char*)b->weights;
   c->G = (float*)b->grads;
   c->work = (char*)b->work;
   c->comm = (char*)b->comm;
   work_layout(*c, c->work);
+  if (c->debug_progress) {
+    // progress words in mapped pinned memory: a dump must not need a CUDA call, which a
+    // device-synchronising call blocked inside the step would hold up
+    if (!c->progress_h) {
+      void* h = nullptr;
+      BM_CUDA_TRY(cudaHostAlloc(&h, (size_t)(2 + c->P) * 64, cudaHostAllocMapped));
+      std::memset(h, 0, (size_t)(2 + c->P) * 64);
+      c->progress_h = (volatile uint32_t*)h;
+    }
+    void* d = nullptr;
+    BM_CUDA_TRY(cudaHostGetDevicePointer(&d, (void*)c->progress_h, 0));
+    c->progress = (uint32_t*)d;
+  }
   c->peer.assign(c->P, nullptr);
   c->peer[c->rank] = c->comm;
   if (c->comm_st.empty()) {
@@ -1186,8 +1260,8 @@ bm_status bm_step(bm_ctx* c, const bm_batch* b, void* stream) {
     pg += x.n_gen[i];
   }
   // reset step state
-  BM_CUDA_TRY(cudaMemsetAsync(x.G, 0, (size_t)x.total_elems * 4, x.st));
-  BM_CUDA_TRY(cudaMemsetAsync(x.loss, 0, (size_t)(2 * x.M + 1) * 4, x.st));
+  BM_TRY(zero_bytes(x.G, x.total_elems * 4, x.st));
+  BM_TRY(zero_bytes(x.loss, (2 * (int64_t)x.M + 1) * 4, x.st));
   x.llm_free.clear();
   for (int i = x.n_llm_slots - 1; i >= 0; --i) x.llm_free.push_back(i);
   x.llm_live.clear();
@@ -1202,6 +1276,11 @@ bm_status bm_step(bm_ctx* c, const bm_batch* b, void* stream) {
   }
   x.gen_done_pending = false;
   cudaStream_t main_st = x.st;
+  x.st_main = main_st;
+  if (x.debug_progress) {
+    g_dbg_ctx = c;
+    g_launch_hook = dbg_launch_hook;
+  }
   // ---- the opcode stream
   const auto& ops = x.s->ranks[x.rank];
   RecvState rs;
@@ -1213,15 +1292,25 @@ bm_status bm_step(bm_ctx* c, const bm_batch* b, void* stream) {
   for (int k = 0; k < 3; ++k) x.stash_peak[k] = 0;
   for (size_t i = 0; i < ops.size(); ++i) {
     const bm_op& o = ops[i];
+    if (x.debug_progress) {
+      std::fprintf(stderr, "[bm r%d s%lld] enqueue op %zu kind %d mb %d chunk %d peer %d pay %d seq %d\n", x.rank,
+                   (long long)x.step, i, (int)o.kind, (int)o.mb, (int)o.chunk, (int)o.peer, (int)o.payload, (int)o.seq);
+      std::fflush(stderr);
+    }
     switch (o.kind) {
       case BM_OP_RECV: {
         const bool on_gen = x.use_gen_stream && x.consumer_kind[i] == BM_OP_GEN_FWD;
         BM_TRY(do_recv_wait(x, o, on_gen ? x.gen_st : main_st));
+        if (x.debug_progress)
+          drv().write32((CUstream)(on_gen ? x.gen_st : main_st), (CUdeviceptr)(x.progress + 16 * (on_gen ? 1 : 0)),
+                        (uint32_t)i + 1, 0);
         rs.ops.push_back(&o);
         continue;
       }
       case BM_OP_SEND:
         BM_TRY(do_send(x, o));
+        if (x.debug_progress)
+          drv().write32((CUstream)x.comm_st[o.peer], (CUdeviceptr)(x.progress + 16 * (2 + o.peer)), (uint32_t)i + 1, 0);
         continue;
       default:
         break;
@@ -1274,6 +1363,8 @@ bm_status bm_step(bm_ctx* c, const bm_batch* b, void* stream) {
     x.stash_peak[2] = std::max(x.stash_peak[2], live_gen);
     rs.ops.clear();
     for (int ri : x.release_of[i]) BM_TRY(do_release(x, ops[ri], op_st));
+    if (x.debug_progress)
+      drv().write32((CUstream)op_st, (CUdeviceptr)(x.progress + 16 * (op_st == main_st ? 0 : 1)), (uint32_t)i + 1, 0);
     x.st = main_st;
     x.part = part_main;
   }
@@ -1291,7 +1382,8 @@ bm_status bm_step(bm_ctx* c, const bm_batch* b, void* stream) {
     BM_CUDA_TRY(cudaStreamWaitEvent(x.st, e, 0));
   }
   // finalize: DP gradient sum + loss terms
-  if (x.P > 1) {
+  static const bool no_allreduce = getenv("BM_DEBUG_NO_ALLREDUCE") != nullptr;   // hang triage only
+  if (x.P > 1 && !no_allreduce) {
     BM_NCCL_TRY(nccl().GroupStart());
     BM_NCCL_TRY(nccl().AllReduce(x.G, x.G, (size_t)x.dp_elems, ncclFloat32, ncclSum, x.nc, x.st));
     BM_NCCL_TRY(nccl().AllReduce(x.loss, x.loss, (size_t)(2 * x.M), ncclFloat32, ncclSum, x.nc, x.st));
@@ -1334,6 +1426,58 @@ bm_status bm_ctx_set_timing(bm_ctx* c, int32_t enable) {
   c->comm_ms = 0;
   c->comm_bytes = 0;
   c->comm_msgs = 0;
+  return BM_OK;
+}
+
+bm_status bm_ctx_debug_dump(bm_ctx* c, char* buf, size_t cap) {
+  BM_CHECK_ARG(c && buf && cap > 0 && c->bound, "bound context and buffer required");
+  if (c->progress_h) {
+    // host-mapped progress only: safe while the owning thread is blocked in the driver
+    std::string out = "rank " + std::to_string(c->rank) + " step " + std::to_string(c->step) + " ops " +
+                      std::to_string(c->s->ranks[c->rank].size()) + " progress main=" +
+                      std::to_string(c->progress_h[0]) + " gen=" + std::to_string(c->progress_h[16]);
+    for (int q = 0; q < c->P; ++q) out += " comm" + std::to_string(q) + "=" + std::to_string(c->progress_h[16 * (2 + q)]);
+    out += "\n  last launch done: main=" + std::to_string(c->progress_h[1]) + " gen=" + std::to_string(c->progress_h[17]);
+    for (int q = 0; q < c->P; ++q) out += " comm" + std::to_string(q) + "=" + std::to_string(c->progress_h[16 * (2 + q) + 1]);
+    out += "\n";
+    if (getenv("BM_DEBUG_DUMP_FLAGS") == nullptr) {
+      std::strncpy(buf, out.c_str(), cap - 1);
+      buf[cap - 1] = 0;
+      return BM_OK;
+    }
+    std::strncpy(buf, out.c_str(), cap - 1);
+    buf[cap - 1] = 0;
+    const size_t used = std::strlen(buf);
+    buf += used;
+    cap -= used;
+  }
+  cudaStream_t s;
+  BM_CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  int64_t fl = 0;
+  for (auto& ch : c->chans) fl = std::max(fl, std::max(ch.flag_off, ch.credit_off) + 64);
+  std::vector<uint32_t> flags((size_t)fl / 4 + 1, 0), prog((size_t)(2 + c->P) * 16, 0);
+  if (fl > 0) BM_CUDA_TRY(cudaMemcpyAsync(flags.data(), c->comm, fl, cudaMemcpyDeviceToHost, s));
+  BM_CUDA_TRY(cudaMemcpyAsync(prog.data(), c->progress, prog.size() * 4, cudaMemcpyDeviceToHost, s));
+  BM_CUDA_TRY(cudaStreamSynchronize(s));
+  cudaStreamDestroy(s);
+  std::string out = "rank " + std::to_string(c->rank) + " step " + std::to_string(c->step) + " ops " +
+                    std::to_string(c->s->ranks[c->rank].size()) + " progress main=" + std::to_string(prog[0]) +
+                    " gen=" + std::to_string(prog[16]);
+  for (int q = 0; q < c->P; ++q) out += " comm" + std::to_string(q) + "=" + std::to_string(prog[16 * (2 + q)]);
+  out += "\n";
+  static const char* PN[] = {"act", "grad", "emb", "embgrad", "genin", "gengrad"};
+  for (auto& ch : c->chans) {
+    if (ch.dst == c->rank)
+      out += "  recv " + std::to_string(ch.src) + "->" + std::to_string(ch.dst) + " " + PN[ch.pay] +
+             " data_flag=" + std::to_string(flags[ch.flag_off / 4]) + " nmsg=" + std::to_string(ch.nmsg) +
+             " K=" + std::to_string(ch.K) + "\n";
+    if (ch.src == c->rank)
+      out += "  send " + std::to_string(ch.src) + "->" + std::to_string(ch.dst) + " " + PN[ch.pay] +
+             " credit=" + std::to_string(flags[ch.credit_off / 4]) + " nmsg=" + std::to_string(ch.nmsg) +
+             " K=" + std::to_string(ch.K) + "\n";
+  }
+  std::strncpy(buf, out.c_str(), cap - 1);
+  buf[cap - 1] = 0;
   return BM_OK;
 }
 

@@ -3,6 +3,7 @@
 // The 1e-4 fp32 tolerance (BASELINE.json north_star) rules out TF32 tensor
 // cores (rel. err ~1e-3); C1-sized parity runs use this 64x64-tile FFMA
 // kernel with the same operand conventions and epilogues as gemm_tc.cu.
+#include <vector>
 #include "common.cuh"
 
 namespace bm {
@@ -84,5 +85,7 @@ bm_status gemm_f32_simt(int M, int N, int K, const float* A, int64_t lda, int a_
   BM_CUDA_TRY(cudaGetLastError());
   return BM_OK;
 }
+
+void preload_simt(std::vector<const void*>& v) { v.push_back((const void*)gemm_f32_kernel); }
 
 }  // namespace bm

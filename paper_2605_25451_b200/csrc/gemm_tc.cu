@@ -141,6 +141,7 @@ __device__ __forceinline__ void tma_reduce_add_2d(const CUtensorMap* map, uint32
 }
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
@@ -273,7 +274,12 @@ __device__ __forceinline__ void stage_f32(uint32_t buf, int lane, const float* w
                  "f"(w[4 * j + 1]), "f"(w[4 * j + 2]), "f"(w[4 * j + 3])
                  : "memory");
 }
-__device__ __forceinline__ float sigmoidf_(float x) { return 1.f / (1.f + __expf(-x)); }
+// sigmoid(x) = 0.5 + 0.5 tanh(x / 2): one MUFU.TANH instead of ex2 + reciprocal
+__device__ __forceinline__ float sigmoidf_(float x) {
+  float t;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(0.5f * x));
+  return fmaf(0.5f, t, 0.5f);
+}
 
 // outputs for one 32-column chunk of a plain / accumulate / residual / dswiglu epilogue
 __device__ __forceinline__ void epi_chunk_tma(const EpiArgs& a, const CUtensorMap* tmC, uint32_t slot, int lane,
@@ -718,19 +724,21 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
 // leader's tmem_empty barrier.  Per CTA and K-block this moves
 // (128 + BN/2)*64*2 bytes instead of (128 + BN)*64*2.
 // ============================================================================
+constexpr int EPI_WARPS2 = 8;   // CTA-pair kernel: two epilogue warps per TMEM lane quadrant
+constexpr int NUM_THREADS2 = 64 + 32 * EPI_WARPS2;
 template <int BN, bool SWI = false> struct Cfg2 {
   static constexpr int A_BYTES = 128 * BK * 2;                 // 16 KB
   static constexpr int B_BYTES = (BN / 2) * BK * 2;            // 16 KB (BN = 256)
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int STAGES = SWI ? 5 : ((BN == 256) ? 6 : 8);
   static constexpr int TMEM_COLS = 2 * BN;
-  static constexpr int EPI_SLOT = SWI ? 6144 : 4096;
-  static constexpr int EPI_BYTES = EPI_WARPS * 2 * EPI_SLOT;
+  static constexpr int EPI_SLOT = SWI ? 6144 : 4096;           // one staging slot per epilogue warp
+  static constexpr int EPI_BYTES = EPI_WARPS2 * EPI_SLOT;
   static constexpr int SMEM = STAGES * STAGE_BYTES + EPI_BYTES + 1024 + 256;
 };
 
 template <int BN, bool A_MN, bool B_MN, bool SWIGLU>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS2, 1)
 gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
              const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmC2, EpiArgs args) {
   using C = Cfg2<BN, SWIGLU>;
@@ -763,7 +771,7 @@ gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull[s], 1);
-      mbar_init(&tempty[s], 8);
+      mbar_init(&tempty[s], 2 * EPI_WARPS2);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     tma_prefetch(&tmA);
@@ -843,8 +851,10 @@ gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
       }
     }
   } else {
+    // epilogue warps 2..9: TMEM lane quadrant = warp % 4, column half = (warp - 2) / 4
     const int quad = warp & 3;
-    const uint32_t ebase = smem_u32(smE) + (uint32_t)((warp - 2) * 2 * C::EPI_SLOT);
+    const int half = (warp - 2) / 4;
+    const uint32_t slot = smem_u32(smE) + (uint32_t)((warp - 2) * C::EPI_SLOT);
     int eiter = 0;
     const uint32_t leader_tempty0 = mapa(smem_u32(&tempty[0]), 0);
     const uint32_t leader_tempty1 = mapa(smem_u32(&tempty[1]), 0);
@@ -860,16 +870,16 @@ gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
       const int row = row0 + lane;
       const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + acc * BN;
       if (SWIGLU) {
+        constexpr int W = BNH / 2;   // features per warp
 #pragma unroll 1
-        for (int c = 0; c < BNH; c += 32) {
+        for (int c = half * W; c < (half + 1) * W; c += 32) {
           float vg[32], vu[32];
           tmem_ld32(taddr + c, vg);
           tmem_ld32(taddr + BNH + c, vu);
           if (args.tma) {
             if (nb * BNH + c < args.f) {
-              const uint32_t slot = ebase + (eiter & 1) * C::EPI_SLOT;
-              if (eiter >= 2) {
-                if (lane == 0) bulk_wait_read1();
+              if (eiter >= 1) {
+                if (lane == 0) bulk_wait_read0();
                 __syncwarp();
               }
               epi_swiglu_tma(args, &tmC, &tmC2, slot, lane, row0, nb * BNH + c, vg, vu);
@@ -880,15 +890,15 @@ gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
           }
         }
       } else {
+        constexpr int W = BN / 2;    // columns per warp
 #pragma unroll 1
-        for (int c = 0; c < BN; c += 32) {
+        for (int c = half * W; c < (half + 1) * W; c += 32) {
           float v[32];
           tmem_ld32(taddr + c, v);
           if (args.tma) {
             if (nb * BN + c < args.N) {
-              const uint32_t slot = ebase + (eiter & 1) * C::EPI_SLOT;
-              if (eiter >= 2) {
-                if (lane == 0) bulk_wait_read1();
+              if (eiter >= 1) {
+                if (lane == 0) bulk_wait_read0();
                 __syncwarp();
               }
               epi_chunk_tma(args, &tmC, slot, lane, row0, nb * BN + c, v);
@@ -1080,7 +1090,7 @@ static bm_status launch2(const CUtensorMap& ma, const CUtensorMap& mb, const CUt
   const int tiles = ceil_div(ea.M, 2 * BM) * (SWIGLU ? ceil_div(ea.f, BN / 2) : ceil_div(ea.N, BN));
   const int pairs = num_sms() / 2;
   const int grid = 2 * (tiles < pairs ? tiles : pairs);
-  BM_CUDA_TRY(launch_k(gemm2_kernel<BN, A_MN, B_MN, SWIGLU>, dim3(grid), dim3(NUM_THREADS), C::SMEM, st, ma, mb, mc,
+  BM_CUDA_TRY(launch_k(gemm2_kernel<BN, A_MN, B_MN, SWIGLU>, dim3(grid), dim3(NUM_THREADS2), C::SMEM, st, ma, mb, mc,
                        mc2, ea));
   count_launch();
   BM_CUDA_TRY(cudaGetLastError());
@@ -1201,6 +1211,32 @@ bm_status gemm_bf16_tc(int M, int N, int K, const void* A, int64_t lda, int a_ma
   if (BN == 64) return dispatch_majors<64>(amn, bmn, ma, mb, mc, ea, st);
   if (BN == 128) return dispatch_majors<128>(amn, bmn, ma, mb, mc, ea, st);
   return dispatch_majors<256>(amn, bmn, ma, mb, mc, ea, st);
+}
+
+// every tcgen05 GEMM instantiation the dispatcher can launch (bm::preload_kernels)
+template <int BN>
+static void preload_bn(std::vector<const void*>& v) {
+  using namespace tc;
+  for (const void* f : {(const void*)gemm_kernel<BN, false, false>, (const void*)gemm_kernel<BN, false, true>,
+                        (const void*)gemm_kernel<BN, true, true>, (const void*)gemm_kernel<BN, true, false>})
+    v.push_back(f);
+}
+template <int BN>
+static void preload_bn2(std::vector<const void*>& v) {
+  using namespace tc;
+  for (const void* f : {(const void*)gemm2_kernel<BN, false, false, false>, (const void*)gemm2_kernel<BN, false, true, false>,
+                        (const void*)gemm2_kernel<BN, true, true, false>, (const void*)gemm2_kernel<BN, true, false, false>})
+    v.push_back(f);
+}
+void preload_tc(std::vector<const void*>& v) {
+  preload_bn<64>(v);
+  preload_bn<128>(v);
+  preload_bn<256>(v);
+  preload_bn2<128>(v);
+  preload_bn2<256>(v);
+  v.push_back((const void*)tc::gemm2_kernel<256, false, false, true>);
+  v.push_back((const void*)tc::gemm2_kernel<256, true, false, true>);
+  v.push_back((const void*)tc::splitk_reduce_kernel);
 }
 
 }  // namespace bm

@@ -40,6 +40,13 @@ bm_status mse_fwd_bwd(int n, int dt, const T* out, const T* t, float denom, floa
                       float* loss_out, T* dout, cudaStream_t st);
 template <typename T> bm_status add(int64_t n, const T* a, const T* b, T* o, cudaStream_t st);
 bm_status cast(int sd, int dd, int64_t n, const void* s, void* d, cudaStream_t st);
+// load every library kernel onto the current device (defeats lazy loading; see kernels_capi.cu)
+bm_status preload_kernels();
+// SM copy / zero fill (16-byte vectors when aligned); max_ctas <= 0: full elementwise grid
+bm_status copy_bytes(void* dst, const void* src, int64_t bytes, int max_ctas, cudaStream_t st);
+bm_status zero_bytes(void* dst, int64_t bytes, cudaStream_t st);
+// one-thread kernel polling *flag until (int32)(*flag - v) >= 0 (BM_WAIT=spin)
+bm_status spin_wait(const uint32_t* flag, uint32_t v, cudaStream_t st);
 bm_status loss_finalize(int M, float* loss, cudaStream_t st);
 
 }  // namespace bm

@@ -3,6 +3,7 @@
 #include <atomic>
 #include <mutex>
 
+#include <vector>
 #include "common.cuh"
 #include "kernels.h"
 
@@ -33,6 +34,7 @@ bool pdl_enabled() {
 }
 
 static std::atomic<int64_t> g_launches{0};
+void (*g_launch_hook)(cudaStream_t, const void*) = nullptr;
 void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 int64_t launch_count() { return g_launches.load(std::memory_order_relaxed); }
 
@@ -65,6 +67,25 @@ bm_status gemm(int dtype, int M, int N, int K, const void* A, int64_t lda, int a
                        (const float*)R, ldr, alpha, st);
 }
 
+void preload_elementwise(std::vector<const void*>& v);
+void preload_simt(std::vector<const void*>& v);
+void preload_tc(std::vector<const void*>& v);
+// Load every kernel of the library onto the current device now.  Under CUDA lazy
+// module loading (the default) a kernel is loaded at its first launch, and that
+// load blocks while another stream of the context is parked on a cross-GPU flag
+// wait: measured as a device-wide stall of the compute-efficient schedule at
+// P = 4 (the first SwiGLU launch behind a send waiting for a credit).
+bm_status preload_kernels() {
+  std::vector<const void*> v;
+  preload_elementwise(v);
+  preload_simt(v);
+  preload_tc(v);
+  for (const void* f : v) {
+    cudaFuncAttributes a;
+    BM_CUDA_TRY(cudaFuncGetAttributes(&a, f));
+  }
+  return BM_OK;
+}
 }  // namespace bm
 
 using namespace bm;
@@ -183,5 +204,15 @@ bm_status bm_k_add(int32_t dtype, int64_t n, const void* a, const void* b, void*
 bm_status bm_k_cast(int32_t src_dtype, int32_t dst_dtype, int64_t n, const void* src, void* dst, void* stream) {
   return cast(src_dtype, dst_dtype, n, src, dst, ST(stream));
 }
+
+bm_status bm_k_copy(void* dst, const void* src, int64_t bytes, int32_t max_ctas, void* stream) {
+  BM_CHECK_ARG(bytes >= 0 && (bytes == 0 || (dst && src)), "invalid copy");
+  return copy_bytes(dst, src, bytes, max_ctas, ST(stream));
+}
+bm_status bm_k_zero(void* dst, int64_t bytes, void* stream) {
+  BM_CHECK_ARG(bytes >= 0 && (bytes == 0 || dst), "invalid fill");
+  return zero_bytes(dst, bytes, ST(stream));
+}
+bm_status bm_k_preload(void) { return preload_kernels(); }
 
 }  // extern "C"

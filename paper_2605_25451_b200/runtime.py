@@ -6,10 +6,17 @@ the hot path runs in libbigmac.so.  There is no CPU fallback.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass
 
-import numpy as np
-import torch
+# Each rank runs a compute stream, P-1 comm streams, a generator stream and NCCL's;
+# with fewer hardware work queues than streams, a comm stream parked on a credit
+# wait (cuStreamWaitValue32) would serialize unrelated streams behind it.  Must be
+# set before the CUDA context exists (importing this module before torch.cuda use).
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
 
 from . import _lib as L
 from . import schedule as BS
@@ -46,6 +53,7 @@ class Runtime:
         if world != self.P:
             raise ValueError(f"one rank per pipeline stage: world={world} != P={self.P}")
         self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else device
+        self._stream = None   # own compute stream (created on first step)
         kw = dict(sched_kw or {})
         self.sched = BS.build(self.P, self.M, self.V, **kw)
         self.mc = model_cfg(shape, dtype)
@@ -153,6 +161,11 @@ class Runtime:
         L.call("bm_ctx_comm_stats", self.ctx, C.byref(n), C.byref(b), C.byref(ms))
         return n.value, b.value, ms.value
 
+    def debug_dump(self) -> str:
+        buf = C.create_string_buffer(1 << 16)
+        L.call("bm_ctx_debug_dump", self.ctx, buf, len(buf))
+        return buf.value.decode()
+
     def names(self):
         return list(self.params)
 
@@ -228,8 +241,22 @@ class Runtime:
 
     # ------------------------------------------------------------------ execute
     def step(self, db: DeviceBatch, stream=None):
-        s = torch.cuda.current_stream(self.device) if stream is None else stream
-        L.call("bm_step", self.ctx, C.byref(db.struct), C.c_void_p(s.cuda_stream))
+        """One training step on `stream` (default: the runtime's own non-blocking
+        compute stream, ordered after and before the caller's current stream).
+        The legacy default stream is never used as the compute stream: it takes part
+        in implicit cross-stream synchronisation."""
+        if stream is not None:
+            L.call("bm_step", self.ctx, C.byref(db.struct), C.c_void_p(stream.cuda_stream))
+            return
+        cur = torch.cuda.current_stream(self.device)
+        if os.environ.get("BM_CALLER_STREAM") == "1":   # triage: run on the caller's stream
+            L.call("bm_step", self.ctx, C.byref(db.struct), C.c_void_p(cur.cuda_stream))
+            return
+        if self._stream is None:
+            self._stream = torch.cuda.Stream(self.device)
+        self._stream.wait_stream(cur)
+        L.call("bm_step", self.ctx, C.byref(db.struct), C.c_void_p(self._stream.cuda_stream))
+        cur.wait_stream(self._stream)
 
     def loss_tensor(self) -> torch.Tensor:
         p = C.c_void_p()

@@ -10,6 +10,10 @@ Prints one JSON line per M on rank 0.
 import argparse
 import json
 import os
+
+# one hardware work queue per stream (compute, P-1 comm, generator, NCCL): a comm
+# stream parked on a credit wait must not block unrelated streams sharing its queue
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 import sys
 
 import torch

@@ -1,6 +1,7 @@
 """Diagnose the step: device time with/without GEMM event timing, host enqueue
 time per step, and the GEMM share, on one GPU (C2, P=1 by default)."""
 import json, os, sys, time
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from synth import get_config, make_batch

@@ -5,6 +5,10 @@ Every rank runs bm_step on its own GPU; rank 0 gathers all gradients and
 compares them with the fp64 oracle (normwise rel tol 1e-4 fp32 / 2e-2 bf16).
 """
 import os
+
+# one hardware work queue per stream (compute, P-1 comm, generator, NCCL): a comm
+# stream parked on a credit wait must not block unrelated streams sharing its queue
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 import sys
 
 import numpy as np

@@ -137,9 +137,13 @@ def test_step_two_gpus_medium(cfg_name, P, M, V, dtype):
     assert "PARITY OK" in out, out
 
 
-@pytest.mark.parametrize("P,M,V,dtype", [(4, 8, 1, "f32"), (4, 8, 1, "bf16")])
-def test_step_four_gpus(P, M, V, dtype):
+@pytest.mark.parametrize("P,M,V,dtype,gen", [(4, 8, 1, "f32", "dp_shard"), (4, 8, 1, "bf16", "dp_shard"),
+                                           (4, 16, 1, "bf16", "dp_shard"), (4, 16, 1, "bf16", "ce"),
+                                           (4, 16, 1, "f32", "entry_stage+last_stage"), (4, 16, 2, "bf16", "ce")])
+def test_step_four_gpus(P, M, V, dtype, gen):
+    # "ce" (W = M / P) once deadlocked: a copy-engine send parked on a credit wait
+    # blocked another stream's copy in a shared copy channel
     if torch.cuda.device_count() < P:
         pytest.skip(f"needs {P} GPUs")
-    out = _torchrun(P, "C1", P, M, V, dtype, "dp_shard")
+    out = _torchrun(P, "C1", P, M, V, dtype, gen, timeout=240)
     assert "PARITY OK" in out, out
