@@ -241,6 +241,25 @@ bm_status bm_ctx_gemm_stats(bm_ctx* c, int64_t* n_gemm, double* flops, double* m
  * (stage-boundary, gather/scatter payloads over NVLink): message count,
  * bytes, summed device milliseconds of the copies on the comm streams. */
 bm_status bm_ctx_comm_stats(bm_ctx* c, int64_t* n_msgs, double* bytes, double* ms);
+/* Per-op trace of the most recent step (tracing enabled with bm_ctx_set_trace
+ * before that step).  One record per compute op (start / end of its kernels on its
+ * stream), per receive (the moment its data-flag wait was satisfied on the consuming
+ * stream: t_start = t_end) and per send (start / end of the NVLink copy on the comm
+ * stream, credit wait included before t_start).  Times are device milliseconds
+ * since the step's first event on the compute stream (CUDA events; each rank has
+ * its own origin).  stream: 0 compute, 1 generator, 2 + q comm stream to rank q.
+ * bm_ctx_trace_get synchronises on the step's last event; *n = records written
+ * (at most cap; *total = records available). */
+typedef struct {
+  int32_t op;       /* index in the rank's op list, -1 for the step tail (allreduce) */
+  int32_t kind;     /* bm_op_kind, -1 for the tail */
+  int32_t stream;
+  int32_t mb;
+  float t_start_ms;
+  float t_end_ms;
+} bm_trace_rec;
+bm_status bm_ctx_set_trace(bm_ctx* c, int32_t enable);
+bm_status bm_ctx_trace_get(bm_ctx* c, bm_trace_rec* out, int64_t cap, int64_t* n, int64_t* total);
 /* Diagnostics: text dump of this rank's receive/credit flags and (with
  * BM_DEBUG_PROGRESS=1 at bm_ctx_create time) the index of the last op each of its
  * streams finished.  Reads device memory on a private non-blocking stream, so

@@ -67,6 +67,11 @@ class Buffers(C.Structure):
     _fields_ = [("weights", C.c_void_p), ("grads", C.c_void_p), ("work", C.c_void_p), ("comm", C.c_void_p)]
 
 
+class TraceRec(C.Structure):
+    _fields_ = [("op", C.c_int32), ("kind", C.c_int32), ("stream", C.c_int32), ("mb", C.c_int32),
+                ("t_start_ms", C.c_float), ("t_end_ms", C.c_float)]
+
+
 class Batch(C.Structure):
     _fields_ = [("M", C.c_int32), ("n_mod", C.c_void_p), ("n_gen", C.c_void_p), ("patches", C.c_void_p),
                 ("ld_patch", C.c_int32), ("ids", C.c_void_p), ("labels", C.c_void_p), ("targets", C.c_void_p),
@@ -101,6 +106,8 @@ SIGNATURES = {
     "bm_ctx_set_timing": [_P, _I32],
     "bm_ctx_gemm_stats": [_P, C.POINTER(_I64), C.POINTER(C.c_double), C.POINTER(C.c_double)],
     "bm_ctx_comm_stats": [_P, C.POINTER(_I64), C.POINTER(C.c_double), C.POINTER(C.c_double)],
+    "bm_ctx_set_trace": [_P, _I32],
+    "bm_ctx_trace_get": [_P, _P, _I64, C.POINTER(_I64), C.POINTER(_I64)],
     "bm_ctx_debug_dump": [_P, C.c_char_p, _SZ],
     "bm_ctx_destroy": [_P],
     # bigmac_kernels.h

@@ -67,6 +67,9 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 inline int ceil_div(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
 
 int num_sms();
+// persistent-GEMM grid budget: num_sms() minus the SMs reserved by set_sm_reserve
+int gemm_sm_budget();
+void set_sm_reserve(int n);
 
 // ---------------------------------------------------------------- PDL
 // Every library kernel is launched with programmatic stream serialization

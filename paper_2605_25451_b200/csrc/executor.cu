@@ -282,9 +282,13 @@ struct bm_ctx {
   // fused SwiGLU GEMM epilogues (bm_k_gemm_swiglu / _dswiglu); off by default: measured
   // slower than GEMM + the separate vectorised kernel (profiles/r01/gemm_bench_v4)
   bool fuse_swiglu = getenv("BM_FUSE_SWIGLU") != nullptr;
-  bool peer_copy_ce = getenv("BM_PEER_COPY") && std::string(getenv("BM_PEER_COPY")) == "ce";
+  bool peer_copy_ce = !(getenv("BM_PEER_COPY") && std::string(getenv("BM_PEER_COPY")) == "sm");
   int peer_copy_ctas = getenv("BM_PEER_COPY_CTAS") ? std::atoi(getenv("BM_PEER_COPY_CTAS")) : 32;
   bool spin_wait = getenv("BM_WAIT") && std::string(getenv("BM_WAIT")) == "spin";
+  // SMs the compute stream's GEMMs leave free on ranks that serve remote generator
+  // shards, so a shard's kernels start at once instead of after the running
+  // persistent GEMM (the shard is on the last stage's critical path)
+  int gen_reserve_sms = getenv("BM_GEN_RESERVE_SMS") ? std::atoi(getenv("BM_GEN_RESERVE_SMS")) : 16;
   std::vector<cudaEvent_t> tev[2];
   size_t tev_used[2] = {0, 0};
   double tflop_pending[2] = {0, 0};
@@ -295,6 +299,16 @@ struct bm_ctx {
   // peer-copy timing (NVLink): event pairs on the comm streams, bytes per copy
   std::vector<cudaEvent_t> cev[2];
   std::vector<int64_t> cbytes[2];
+  // per-op trace of the last step (bm_ctx_set_trace)
+  struct TraceEv {
+    int32_t op, kind, stream, mb;
+    cudaEvent_t a, b;
+  };
+  bool tracing = false;
+  std::vector<TraceEv> trace;
+  std::vector<cudaEvent_t> trace_pool;
+  size_t trace_used = 0;
+  cudaEvent_t trace_origin = nullptr, trace_last = nullptr;
   double comm_ms = 0, comm_bytes = 0;
   int64_t comm_msgs = 0;
   std::map<std::array<int, 4>, std::pair<int64_t, double>> shape_ms;  // BM_GEMM_LOG=1 breakdown
@@ -317,6 +331,8 @@ bm_ctx::~bm_ctx() {
     for (auto e : cev[k])
       if (e) cudaEventDestroy(e);
   }
+  for (auto e : trace_pool)
+    if (e) cudaEventDestroy(e);
   for (int i = 0; i < 2; ++i) {
     if (bout_ev[i]) cudaEventDestroy(bout_ev[i]);
     if (gout_ev[i]) cudaEventDestroy(gout_ev[i]);
@@ -633,6 +649,28 @@ static cudaEvent_t next_event(bm_ctx& c) {
   c.evnext = (c.evnext + 1) % c.evpool.size();
   return e;
 }
+// trace events (timing-enabled, pooled; bm_ctx_set_trace)
+static cudaEvent_t trace_event(bm_ctx& c) {
+  if (c.trace_used == c.trace_pool.size()) {
+    cudaEvent_t e = nullptr;
+    if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
+    c.trace_pool.push_back(e);
+  }
+  return c.trace_pool[c.trace_used++];
+}
+static int stream_slot(const bm_ctx& c, cudaStream_t st) {
+  if (st == c.st_main) return 0;
+  if (st == c.gen_st) return 1;
+  for (int q = 0; q < c.P; ++q)
+    if (q != c.rank && st == c.comm_st[q]) return 2 + q;
+  return 0;
+}
+static cudaEvent_t trace_mark(bm_ctx& c, cudaStream_t st) {
+  cudaEvent_t e = trace_event(c);
+  if (e) cudaEventRecord(e, st);
+  return e;
+}
+
 static void shard_rows(const bm_ctx& c, int m, int r, int* lo, int* hi) {
   const int n = c.n_gen[m];
   if (c.gen_last) { *lo = 0; *hi = n; return; }
@@ -905,12 +943,10 @@ static int64_t payload_bytes(const bm_ctx& c, const bm_op& o, int src_rank_for_s
   }
 }
 
-// NVLink write of one message into the peer's receive slot.  Default: an SM copy
-// kernel on the comm stream's own compute channel.  A copy-engine copy would sit in
-// a copy channel shared with other streams; when this stream is parked on a credit
-// wait, those streams' copies queue behind it and the acyclic schedule deadlocks
-// (measured: compute-efficient strategy, P = 4).  BM_PEER_COPY=ce restores the
-// copy engine for experiments.
+// NVLink write of one message into the peer's receive slot: a copy-engine copy on
+// the comm stream (no SM time taken from the GEMMs; measured 138.3 vs 135.0
+// samples/s for an SM copy kernel at C2, N = 4).  BM_PEER_COPY=sm selects the SM
+// copy kernel (bm_k_copy) instead.
 static bm_status peer_copy(bm_ctx& c, char* dst, const char* src, int64_t bytes, cudaStream_t cs) {
   if (c.peer_copy_ce) {
     BM_CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, cs));
@@ -930,7 +966,7 @@ static bm_status wait_flag(bm_ctx& c, cudaStream_t on, char* flag, uint32_t v, c
   return BM_OK;
 }
 
-static bm_status do_send(bm_ctx& c, const bm_op& o) {
+static bm_status do_send(bm_ctx& c, const bm_op& o, int idx) {
   const Chan& ch = c.chans[c.chan_idx.at(std::make_tuple(c.rank, o.peer, o.payload))];
   cudaStream_t cs = c.comm_st[o.peer];
   if (!c.producer_ev) {
@@ -955,6 +991,7 @@ static bm_status do_send(bm_ctx& c, const bm_op& o) {
     bytes = payload_bytes(c, o, c.rank);
   }
   char* dst = c.peer[o.peer] + ch.data_off + (int64_t)(o.seq % ch.K) * ch.slot_bytes;
+  cudaEvent_t tr_a = c.tracing ? trace_mark(c, cs) : nullptr;
   if (c.timing && bytes > 0) {
     const int pool = (int)(c.step & 1);
     auto& ev = c.cev[pool];
@@ -973,6 +1010,7 @@ static bm_status do_send(bm_ctx& c, const bm_op& o) {
   }
   CUresult r = drv().write32((CUstream)cs, (CUdeviceptr)(c.peer[o.peer] + ch.flag_off), base + (uint32_t)o.seq + 1, 0);
   if (r != CUDA_SUCCESS) { set_error("cuStreamWriteValue32 (data flag) failed " + std::to_string((int)r)); return BM_E_CUDA; }
+  if (c.tracing) c.trace.push_back({idx, (int32_t)o.kind, 2 + o.peer, o.mb, tr_a, trace_mark(c, cs)});
   if (c.last_src_ring == 0 && o.payload != BM_PAY_GENIN) {
     BM_CUDA_TRY(cudaEventRecord(c.bout_ev[c.last_src_idx], cs));
     c.bout_pending[c.last_src_idx] = true;
@@ -1277,6 +1315,11 @@ bm_status bm_step(bm_ctx* c, const bm_batch* b, void* stream) {
   x.gen_done_pending = false;
   cudaStream_t main_st = x.st;
   x.st_main = main_st;
+  if (x.tracing) {
+    x.trace.clear();
+    x.trace_used = 0;
+    x.trace_origin = trace_mark(x, main_st);
+  }
   if (x.debug_progress) {
     g_dbg_ctx = c;
     g_launch_hook = dbg_launch_hook;
@@ -1304,11 +1347,15 @@ bm_status bm_step(bm_ctx* c, const bm_batch* b, void* stream) {
         if (x.debug_progress)
           drv().write32((CUstream)(on_gen ? x.gen_st : main_st), (CUdeviceptr)(x.progress + 16 * (on_gen ? 1 : 0)),
                         (uint32_t)i + 1, 0);
+        if (x.tracing) {
+          cudaEvent_t e = trace_mark(x, on_gen ? x.gen_st : main_st);
+          x.trace.push_back({(int32_t)i, (int32_t)o.kind, on_gen ? 1 : 0, o.mb, e, e});
+        }
         rs.ops.push_back(&o);
         continue;
       }
       case BM_OP_SEND:
-        BM_TRY(do_send(x, o));
+        BM_TRY(do_send(x, o, (int)i));
         if (x.debug_progress)
           drv().write32((CUstream)x.comm_st[o.peer], (CUdeviceptr)(x.progress + 16 * (2 + o.peer)), (uint32_t)i + 1, 0);
         continue;
@@ -1330,6 +1377,8 @@ bm_status bm_step(bm_ctx* c, const bm_batch* b, void* stream) {
     float* part_main = x.part;
     if (op_st != main_st) x.part = x.part_gen;
     x.cur_ws = (op_st != main_st) ? x.ws_gen : x.ws;
+    set_sm_reserve((op_st == main_st && x.use_gen_stream && x.rank != x.P - 1) ? x.gen_reserve_sms : 0);
+    cudaEvent_t tr_a = x.tracing ? trace_mark(x, op_st) : nullptr;
     switch (o.kind) {
       case BM_OP_ENC_FWD: BM_TRY(op_enc_fwd(x, o)); live_enc += enc_unit_bytes; break;
       case BM_OP_ENC_BWD: BM_TRY(op_enc_bwd(x, o, rs)); live_enc -= enc_unit_bytes; break;
@@ -1363,10 +1412,12 @@ bm_status bm_step(bm_ctx* c, const bm_batch* b, void* stream) {
     x.stash_peak[2] = std::max(x.stash_peak[2], live_gen);
     rs.ops.clear();
     for (int ri : x.release_of[i]) BM_TRY(do_release(x, ops[ri], op_st));
+    if (x.tracing) x.trace.push_back({(int32_t)i, (int32_t)o.kind, stream_slot(x, op_st), o.mb, tr_a, trace_mark(x, op_st)});
     if (x.debug_progress)
       drv().write32((CUstream)op_st, (CUdeviceptr)(x.progress + 16 * (op_st == main_st ? 0 : 1)), (uint32_t)i + 1, 0);
     x.st = main_st;
     x.part = part_main;
+    set_sm_reserve(0);
   }
   if (x.use_gen_stream) {
     cudaEvent_t e = next_event(x);
@@ -1382,6 +1433,7 @@ bm_status bm_step(bm_ctx* c, const bm_batch* b, void* stream) {
     BM_CUDA_TRY(cudaStreamWaitEvent(x.st, e, 0));
   }
   // finalize: DP gradient sum + loss terms
+  cudaEvent_t tr_tail = x.tracing ? trace_mark(x, x.st) : nullptr;
   static const bool no_allreduce = getenv("BM_DEBUG_NO_ALLREDUCE") != nullptr;   // hang triage only
   if (x.P > 1 && !no_allreduce) {
     BM_NCCL_TRY(nccl().GroupStart());
@@ -1390,6 +1442,10 @@ bm_status bm_step(bm_ctx* c, const bm_batch* b, void* stream) {
     BM_NCCL_TRY(nccl().GroupEnd());
   }
   BM_TRY(loss_finalize(x.M, x.loss, x.st));
+  if (x.tracing) {
+    x.trace_last = trace_mark(x, x.st);
+    x.trace.push_back({-1, -1, 0, -1, tr_tail, x.trace_last});
+  }
   x.step += 1;
   x.launches = launch_count() - launches0;
   return BM_OK;
@@ -1478,6 +1534,34 @@ bm_status bm_ctx_debug_dump(bm_ctx* c, char* buf, size_t cap) {
   }
   std::strncpy(buf, out.c_str(), cap - 1);
   buf[cap - 1] = 0;
+  return BM_OK;
+}
+
+bm_status bm_ctx_set_trace(bm_ctx* c, int32_t enable) {
+  BM_CHECK_ARG(c, "null argument");
+  c->tracing = enable != 0;
+  if (!c->tracing) c->trace.clear();
+  return BM_OK;
+}
+
+bm_status bm_ctx_trace_get(bm_ctx* c, bm_trace_rec* out, int64_t cap, int64_t* n, int64_t* total) {
+  BM_CHECK_ARG(c && n && total && (cap == 0 || out), "null argument");
+  *total = (int64_t)c->trace.size();
+  *n = 0;
+  if (c->trace.empty() || !c->trace_last || !c->trace_origin) return BM_OK;
+  BM_CUDA_TRY(cudaEventSynchronize(c->trace_last));
+  for (const auto& t : c->trace) {
+    if (*n >= cap) break;
+    if (!t.a || !t.b) continue;
+    bm_trace_rec& r = out[(*n)++];
+    r.op = t.op;
+    r.kind = t.kind;
+    r.stream = t.stream;
+    r.mb = t.mb;
+    BM_CUDA_TRY(cudaEventSynchronize(t.b));
+    BM_CUDA_TRY(cudaEventElapsedTime(&r.t_start_ms, c->trace_origin, t.a));
+    BM_CUDA_TRY(cudaEventElapsedTime(&r.t_end_ms, c->trace_origin, t.b));
+  }
   return BM_OK;
 }
 

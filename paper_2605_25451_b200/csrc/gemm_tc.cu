@@ -1060,7 +1060,8 @@ static bm_status launch(const CUtensorMap& ma, const CUtensorMap& mb, const CUte
     attr_set = true;
   }
   const int tiles = ceil_div(ea.M, BM) * ceil_div(ea.N, BN) * ea.splits;
-  const int grid = tiles < num_sms() ? tiles : num_sms();
+  const int cap = gemm_sm_budget();
+  const int grid = tiles < cap ? tiles : cap;
   BM_CUDA_TRY(launch_k(gemm_kernel<BN, A_MN, B_MN>, dim3(grid), dim3(NUM_THREADS), C::SMEM, st, ma, mb, mc, ea));
   count_launch();
   BM_CUDA_TRY(cudaGetLastError());
@@ -1088,7 +1089,7 @@ static bm_status launch2(const CUtensorMap& ma, const CUtensorMap& mb, const CUt
     attr_set = true;
   }
   const int tiles = ceil_div(ea.M, 2 * BM) * (SWIGLU ? ceil_div(ea.f, BN / 2) : ceil_div(ea.N, BN));
-  const int pairs = num_sms() / 2;
+  const int pairs = gemm_sm_budget() / 2;
   const int grid = 2 * (tiles < pairs ? tiles : pairs);
   BM_CUDA_TRY(launch_k(gemm2_kernel<BN, A_MN, B_MN, SWIGLU>, dim3(grid), dim3(NUM_THREADS2), C::SMEM, st, ma, mb, mc,
                        mc2, ea));

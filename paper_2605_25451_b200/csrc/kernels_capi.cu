@@ -25,6 +25,15 @@ int num_sms() {
   return n;
 }
 
+// SMs left free by the persistent GEMM grids (set by the executor around compute
+// ops that share the GPU with a high-priority generator stream)
+static int g_sm_reserve = 0;
+void set_sm_reserve(int n) { g_sm_reserve = n < 0 ? 0 : n; }
+int gemm_sm_budget() {
+  const int b = num_sms() - g_sm_reserve;
+  return b < 2 ? 2 : b;
+}
+
 bool pdl_enabled() {
   static const bool on = [] {
     const char* e = getenv("BM_PDL");

@@ -161,6 +161,21 @@ class Runtime:
         L.call("bm_ctx_comm_stats", self.ctx, C.byref(n), C.byref(b), C.byref(ms))
         return n.value, b.value, ms.value
 
+    def set_trace(self, on: bool):
+        """Record a per-op trace of each following step (CUDA events around every op)."""
+        L.call("bm_ctx_set_trace", self.ctx, 1 if on else 0)
+
+    def trace(self):
+        """Per-op records of the last traced step: dicts with op index, kind name,
+        stream (0 compute, 1 generator, 2+q comm to rank q), mb, start/end ms."""
+        n, tot = C.c_int64(), C.c_int64()
+        L.call("bm_ctx_trace_get", self.ctx, None, 0, C.byref(n), C.byref(tot))
+        buf = (L.TraceRec * max(tot.value, 1))()
+        L.call("bm_ctx_trace_get", self.ctx, buf, tot.value, C.byref(n), C.byref(tot))
+        kinds = BS.KINDS
+        return [{"op": r.op, "kind": kinds[r.kind] if 0 <= r.kind < len(kinds) else "Tail", "stream": r.stream,
+                 "mb": r.mb, "t0": r.t_start_ms, "t1": r.t_end_ms} for r in buf[:n.value]]
+
     def debug_dump(self) -> str:
         buf = C.create_string_buffer(1 << 16)
         L.call("bm_ctx_debug_dump", self.ctx, buf, len(buf))

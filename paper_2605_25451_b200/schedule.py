@@ -6,6 +6,10 @@ from dataclasses import dataclass
 
 from . import _lib as L
 
+# bm_op_kind names (include/bigmac.h)
+KINDS = ("EncFwd", "EncBwd", "LlmFwd", "LlmBwd", "GenFwd", "GenBwd", "Send", "Recv")
+PAYLOADS = ("act", "grad", "emb", "embgrad", "genin", "gengrad")
+
 
 @dataclass
 class Sched:
