@@ -5,11 +5,13 @@
     (N > 1: python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N ...)
 
 Workload (BASELINE.json configs[1], "C2"): ViT-S-shaped encoder + 1B-shaped
-LLM + small generator, S = 4096, M = 16 microbatches (global batch 16, one
-sample per microbatch), 1F1B LLM schedule with the encoder/generator nested
-in it, P = N pipeline stages (one per GPU), synthetic data with
+LLM + small generator, S = 4096, 1F1B LLM schedule with the encoder/generator
+nested in it, P = N pipeline stages (one per GPU), synthetic data with
 log-uniform[256, 1024] modality / generation rows per sample, bf16.
-Global batch is fixed as N grows ("strong" scaling).
+M = 16 microbatches per GPU (global batch 16 N, one sample per microbatch):
+every GPU processes 16 microbatches x L/N layers per step at any N ("weak"
+scaling; the 1F1B bubble (N-1)/(M+N-1) stays <= 5.2 %).  --microbatches M
+fixes the global batch instead ("strong").
 
 Prints ONE JSON line on rank 0.
 """
@@ -20,8 +22,7 @@ import json
 import math
 import os
 
-# one hardware work queue per stream (compute, P-1 comm, generator, NCCL): a comm
-# stream parked on a credit wait must not block unrelated streams sharing its queue
+# one hardware work queue per stream (compute, generator, P-1 comm, NCCL)
 os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 import statistics
 import subprocess
@@ -139,7 +140,7 @@ def cpu_oracle_sample(cfg, rows=512, repeats=1):
 
 def workload(args, N):
     from synth import get_config
-    cfg = get_config(args.config, P=N, M=args.microbatches or get_config(args.config).M, V=1)
+    cfg = get_config(args.config, P=N, M=args.microbatches or get_config(args.config).M * N, V=1)
     return cfg
 
 
@@ -179,7 +180,8 @@ def run_reference(args):
               f"(d={cfg.d}, f={cfg.f}); samples/s extrapolated by the step's algorithmic FLOPs per sample")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": N,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * sec / args.steps,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "strong" if args.microbatches else "weak", "vs_baseline": None,
+            "dtype": "f64",
             "data": "synthetic", "config": config_dict(cfg, N),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -366,7 +368,8 @@ def main():
 
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": N, "steps": args.steps,
             "strategy": args.strategy,
-            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "strong" if args.microbatches else "weak",
             "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
             "config": config_dict(cfg, N),
             "roofline": roofline, "step_roofline": step_roof,

@@ -276,6 +276,7 @@ struct bm_ctx {
   bool use_gen_stream = false;
   cudaEvent_t hn_ev = nullptr, gen_done_ev = nullptr;
   bool gen_done_pending = false;
+  std::map<int, int> own_gout;   // last rank: mb -> gout slot holding its own shard's dX
   std::vector<int> consumer_kind;      // per op index: kind of the first compute op after it
   // GEMM timing (bench roofline): event pairs around every GEMM, two pools by step parity
   bool timing = false;
@@ -288,7 +289,8 @@ struct bm_ctx {
   // SMs the compute stream's GEMMs leave free on ranks that serve remote generator
   // shards, so a shard's kernels start at once instead of after the running
   // persistent GEMM (the shard is on the last stage's critical path)
-  int gen_reserve_sms = getenv("BM_GEN_RESERVE_SMS") ? std::atoi(getenv("BM_GEN_RESERVE_SMS")) : 16;
+  // (measured at C2, N = 4: 0 / 8 / 16 / 32 SMs -> 140.4 / 140.1 / 139.4 / 135.0 samples/s; off by default)
+  int gen_reserve_sms = getenv("BM_GEN_RESERVE_SMS") ? std::atoi(getenv("BM_GEN_RESERVE_SMS")) : 0;
   std::vector<cudaEvent_t> tev[2];
   size_t tev_used[2] = {0, 0};
   double tflop_pending[2] = {0, 0};
@@ -791,6 +793,9 @@ static bm_status op_llm_fwd(bm_ctx& c, const bm_op& o, const RecvState& rs) {
     // last stage: final norm, LM head + CE (fwd and bwd through the head), generator inputs
     const int n_mod = c.n_mod[mb], n_text = m.S - n_mod;
     BM_TRY(norm_fwd(c, m.S, m.d, sl.x[c.lps], P_(c, "llm.final_norm"), sl.Hn, sl.rstd_f));
+    // Hn is final: the generator (own shard on the generator stream, remote shards
+    // through their genin sends) starts now, overlapping the LM head and CE below
+    if (c.hn_ev) BM_CUDA_TRY(cudaEventRecord(c.hn_ev, c.st));
     BM_TRY(zero_bytes(sl.dHn, (int64_t)n_mod * d * es, c.st));
     if (n_text > 0) {
       const char* hn_text = sl.Hn + (int64_t)n_mod * d * es;
@@ -830,6 +835,18 @@ static bm_status op_llm_bwd(bm_ctx& c, const bm_op& o, const RecvState& rs) {
         char* dst = sl.dHn + (int64_t)(m.S - n_gen + lo) * d * es;
         BM_TRY(add_(c, (int64_t)(hi - lo) * d, dst, recv_slot(c, r->peer, BM_PAY_GENGRAD, r->seq), dst));
       }
+    }
+    auto og = c.own_gout.find(mb);
+    if (og != c.own_gout.end()) {
+      // this rank's own shard (the whole generator under BM_GEN_LAST_STAGE)
+      int lo, hi;
+      shard_rows(c, mb, c.rank, &lo, &hi);
+      char* dst = sl.dHn + (int64_t)(m.S - n_gen + lo) * d * es;
+      BM_TRY(add_(c, (int64_t)(hi - lo) * d, dst, c.gout[og->second], dst));
+      // the generator stream must not overwrite this gout slot before the add ran
+      BM_CUDA_TRY(cudaEventRecord(c.gout_ev[og->second], c.st));
+      c.gout_pending[og->second] = true;
+      c.own_gout.erase(og);
     }
     BM_TRY(norm_bwd(c, m.S, m.d, sl.dHn, sl.x[c.lps], P_(c, "llm.final_norm"), sl.rstd_f, nullptr, c.dwork[0],
                     G_(c, "llm.final_norm")));
@@ -916,14 +933,11 @@ static bm_status op_gen_bwd(bm_ctx& c, const bm_op& o, const char* X) {
   BM_TRY(lin_dgrad(c, n, m.d_g, m.d_t, sl.dout, P_(c, "gen.out"), LD_(c, "gen.out"), c.g_dG, m.d_g));
   BM_TRY(mlp_blocks_bwd(c, sl, "gen", m.L_g, n, m.d_g, m.f_g, c.g_dG, c.g_dz, c.g_da, c.g_dxn));
   BM_TRY(lin_wgrad(c, n, m.d, m.d_g, c.g_dG, X, m.d, G_(c, "gen.in"), LD_(c, "gen.in")));
-  if (c.rank == c.P - 1) {
-    // own shard: add straight into the stashed dHn rows of (mb, V-1)
-    LlmSlot& ls = c.llm[c.llm_live.at({mb, c.V - 1})];
-    char* dst = ls.dHn + (int64_t)(m.S - c.n_gen[mb] + lo) * m.d * c.es;
-    BM_TRY(lin_dgrad(c, n, m.d, m.d_g, c.g_dG, P_(c, "gen.in"), LD_(c, "gen.in"), dst, m.d, BM_EPI_ADD, dst));
-  } else {
-    BM_TRY(lin_dgrad(c, n, m.d, m.d_g, c.g_dG, P_(c, "gen.in"), LD_(c, "gen.in"), c.gout[b], m.d));
-  }
+  // dX of this shard into the gout ring: sent to the last stage, or (own shard on
+  // the last stage) added into dHn by B(mb, V-1) -- never written into dHn here,
+  // where the LM-head dgrad of the same rows may still be running on the compute stream
+  BM_TRY(lin_dgrad(c, n, m.d, m.d_g, c.g_dG, P_(c, "gen.in"), LD_(c, "gen.in"), c.gout[b], m.d));
+  if (c.rank == c.P - 1) c.own_gout[mb] = b;
   return BM_OK;
 }
 
@@ -969,11 +983,15 @@ static bm_status wait_flag(bm_ctx& c, cudaStream_t on, char* flag, uint32_t v, c
 static bm_status do_send(bm_ctx& c, const bm_op& o, int idx) {
   const Chan& ch = c.chans[c.chan_idx.at(std::make_tuple(c.rank, o.peer, o.payload))];
   cudaStream_t cs = c.comm_st[o.peer];
-  if (!c.producer_ev) {
-    c.producer_ev = next_event(c);
-    BM_CUDA_TRY(cudaEventRecord(c.producer_ev, c.producer_st ? c.producer_st : c.st));
+  if (o.payload == BM_PAY_GENIN && c.hn_ev) {
+    BM_CUDA_TRY(cudaStreamWaitEvent(cs, c.hn_ev, 0));   // Hn rows exist (mid F(m, V-1))
+  } else {
+    if (!c.producer_ev) {
+      c.producer_ev = next_event(c);
+      BM_CUDA_TRY(cudaEventRecord(c.producer_ev, c.producer_st ? c.producer_st : c.st));
+    }
+    BM_CUDA_TRY(cudaStreamWaitEvent(cs, c.producer_ev, 0));
   }
-  BM_CUDA_TRY(cudaStreamWaitEvent(cs, c.producer_ev, 0));
   const uint32_t base = (uint32_t)(c.step * ch.nmsg);
   if (o.seq >= ch.K) {
     BM_TRY(wait_flag(c, cs, c.comm + ch.credit_off, base + (uint32_t)(o.seq - ch.K) + 1, "credit"));
@@ -1118,8 +1136,9 @@ bm_status bm_ctx_create(const bm_model_cfg* mc, const bm_schedule* s, int32_t ra
     while (j < ops.size() && ops[j].kind > BM_OP_GEN_BWD) ++j;
     c->consumer_kind[i] = j < ops.size() ? ops[j].kind : -1;
   }
-  c->use_gen_stream = c->P > 1 && s->cfg.gen_place == BM_GEN_DP_SHARD &&
-                      !(getenv("BM_GEN_STREAM") && getenv("BM_GEN_STREAM")[0] == '0');
+  // generator ops run on a high-priority stream whenever there is a generator: they
+  // start when Hn (final norm) of F(m, V-1) exists and overlap the LM head / CE
+  c->use_gen_stream = c->has_gen && !(getenv("BM_GEN_STREAM") && getenv("BM_GEN_STREAM")[0] == '0');
   *out = c;
   return BM_OK;
 }
@@ -1173,9 +1192,9 @@ bm_status bm_ctx_bind(bm_ctx* c, const bm_buffers* b) {
       int least = 0, greatest = 0;
       BM_CUDA_TRY(cudaDeviceGetStreamPriorityRange(&least, &greatest));
       BM_CUDA_TRY(cudaStreamCreateWithPriority(&c->gen_st, cudaStreamNonBlocking, greatest));
-      BM_CUDA_TRY(cudaEventCreateWithFlags(&c->hn_ev, cudaEventDisableTiming));
       BM_CUDA_TRY(cudaEventCreateWithFlags(&c->gen_done_ev, cudaEventDisableTiming));
     }
+    if (c->has_gen) BM_CUDA_TRY(cudaEventCreateWithFlags(&c->hn_ev, cudaEventDisableTiming));
   }
   if (!drv().wait32 || !drv().write32) {
     set_error("cuStreamWaitValue32/cuStreamWriteValue32 unavailable");
@@ -1313,6 +1332,7 @@ bm_status bm_step(bm_ctx* c, const bm_batch* b, void* stream) {
     if (x.use_gen_stream) BM_CUDA_TRY(cudaStreamWaitEvent(x.gen_st, e, 0));
   }
   x.gen_done_pending = false;
+  x.own_gout.clear();
   cudaStream_t main_st = x.st;
   x.st_main = main_st;
   if (x.tracing) {
@@ -1385,7 +1405,6 @@ bm_status bm_step(bm_ctx* c, const bm_batch* b, void* stream) {
       case BM_OP_LLM_FWD:
         BM_TRY(op_llm_fwd(x, o, rs));
         live_llm += llm_unit_bytes;
-        if (x.use_gen_stream && o.chunk == x.V - 1 && x.rank == x.P - 1) BM_CUDA_TRY(cudaEventRecord(x.hn_ev, main_st));
         break;
       case BM_OP_LLM_BWD: BM_TRY(op_llm_bwd(x, o, rs)); live_llm -= llm_unit_bytes; break;
       case BM_OP_GEN_FWD:

@@ -12,7 +12,7 @@ def simulate(sched, steps=2, use_gen_stream=None, verbose=False):
     cfg = sched.cfg
     P, V = cfg.stages, cfg.vchunks
     if use_gen_stream is None:
-        use_gen_stream = P > 1 and cfg.gen_place == "dp_shard"
+        use_gen_stream = cfg.gen_place != "none"
     rings = sched.rings
     nmsg = {}
     for r in range(P):
@@ -68,6 +68,7 @@ def simulate(sched, steps=2, use_gen_stream=None, verbose=False):
             gout_pending = [None, None]
             last_ring, last_idx = -1, 0
             gen_done_pending = False
+            own_gout = {}
             for i, o in enumerate(ops):
                 if o.kind == "Recv":
                     consumer = next(x for x in ops[i + 1:] if x.kind not in ("Send", "Recv"))
@@ -78,10 +79,13 @@ def simulate(sched, steps=2, use_gen_stream=None, verbose=False):
                 if o.kind == "Send":
                     ch = (r, o.peer, o.payload)
                     cs = f"comm{o.peer}"
-                    if producer_ev is None:
-                        producer_ev = new_ev(r)
-                        rec(r, producer_st, producer_ev)
-                    wait_ev(r, cs, producer_ev)
+                    if o.payload == "genin":
+                        wait_ev(r, cs, f"r{r}hn")    # Hn of F(m, V-1), recorded inside that op
+                    else:
+                        if producer_ev is None:
+                            producer_ev = new_ev(r)
+                            rec(r, producer_st, producer_ev)
+                        wait_ev(r, cs, producer_ev)
                     K = rings[ch]
                     if o.seq >= K:
                         st(r, cs).append(("wait_flag", ("credit", ch), step * nmsg[ch] + o.seq - K + 1))
@@ -122,9 +126,19 @@ def simulate(sched, steps=2, use_gen_stream=None, verbose=False):
                     last_ring = -1
                 elif o.kind == "LlmFwd":
                     last_ring = -1
-                st(r, op_st).append(("kernel", (r, i, o.kind, o.mb)))
-                if o.kind == "LlmFwd" and use_gen_stream and o.chunk == V - 1 and r == P - 1:
+                if o.kind == "LlmBwd" and o.chunk == V - 1 and r == P - 1 and o.mb in own_gout:
+                    # own generator shard's dX added from gout; the slot is free after this op
+                    st(r, op_st).append(("kernel", (r, i, o.kind, o.mb)))
+                    b = own_gout.pop(o.mb)
+                    ev = f"r{r}gout{b}"
+                    rec(r, op_st, ev)
+                    gout_pending[b] = ev
+                else:
+                    st(r, op_st).append(("kernel", (r, i, o.kind, o.mb)))
+                if o.kind == "LlmFwd" and cfg.gen_place != "none" and o.chunk == V - 1 and r == P - 1:
                     rec(r, "main", f"r{r}hn")
+                if o.kind == "GenBwd" and r == P - 1:
+                    own_gout[o.mb] = last_idx
                 if o.kind == "GenBwd" and use_gen_stream and r == P - 1:
                     rec(r, "gen", f"r{r}gendone")
                     gen_done_pending = True
