@@ -155,6 +155,12 @@ def config_dict(cfg, N):
             "strategy": getattr(cfg, "_strategy", "bigmac")}
 
 
+def head_place_name(args, N):
+    if args.head != "auto":
+        return args.head
+    return "last_stage"
+
+
 def run_reference(args):
     """The oracle as it stands, on the host cores (the reference arm for this tier)."""
     rank = int(os.environ.get("RANK", "0"))
@@ -200,6 +206,9 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--ref-rows", type=int, default=512)
+    ap.add_argument("--head", default="auto", choices=["auto", "last_stage", "dp_shard"],
+                    help="LM head + CE placement (bigmac.h bm_head_place): auto = last_stage (the paper's "
+                         "Megatron placement), dp_shard = DP-sharded with the generator")
     ap.add_argument("--strategy", default="bigmac", choices=["bigmac", "compute_efficient", "memory_efficient"],
                     help="bigmac (default); the paper's baselines on the same executor (P:129-156)")
     args = ap.parse_args()
@@ -228,7 +237,7 @@ def main():
         raise SystemExit("--warmup must be >= 3")
     sched_kw = {"bigmac": {}, "compute_efficient": {"warmup_units": cfg.M // N},
                 "memory_efficient": {"enc_place": "entry_stage", "gen_place": "last_stage"}}[args.strategy]
-    rt = Runtime(cfg, args.dtype, rank=rank, world=world, group=group, sched_kw=sched_kw)
+    rt = Runtime(cfg, args.dtype, rank=rank, world=world, group=group, sched_kw=sched_kw, head_place=args.head)
     rt.init_random_weights(seed=1)
     batch = make_batch(cfg)
     db = rt.device_batch(batch)
@@ -371,7 +380,7 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "strong" if args.microbatches else "weak",
             "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
-            "config": config_dict(cfg, N),
+            "config": dict(config_dict(cfg, N), strategy=args.strategy, head_place=head_place_name(args, N)),
             "roofline": roofline, "step_roofline": step_roof,
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches_all, "clocks": clocks,
             "nvlink": ({"bytes_per_step_all_ranks": comm_bytes_all / n_inst,

@@ -142,8 +142,26 @@ typedef struct {
   int32_t d_g, f_g, L_g, d_t;     /* generator                                */
   int32_t dtype;                  /* bm_dtype of weights/activations           */
   int32_t max_n_mod, max_n_gen;   /* upper bounds on per-sample row counts     */
-  int32_t reserved[8];
+  int32_t head_place;             /* bm_head_place                             */
+  int32_t reserved[7];            /* must be zero                              */
 } bm_model_cfg;
+
+/* Where the final-norm output's LM head + cross-entropy (fwd and bwd) run.
+ * BM_HEAD_LAST_STAGE: in F(m, V-1) on rank P-1, as in the paper's Megatron
+ *   setting.
+ * BM_HEAD_DP_SHARD: the head is token-wise like the generator, so it rides on
+ *   the DP-sharded generator ops (reading R14): rank r's GenFwd(m)
+ *   computes the logits, CE and dHn of text rows
+ *   [n_mod + floor(r n_text / P), n_mod + floor((r+1) n_text / P)),
+ *   n_text = S - n_mod, with the full-microbatch CE denominator; the genin
+ *   message carries [head rows | generator rows] of Hn, the gengrad message
+ *   [dHn head rows | generator dX rows].  llm.head becomes a DP parameter
+ *   (every rank, summed by the step-end allreduce).  Requires
+ *   gen_place == BM_GEN_DP_SHARD.  Schedules (op lists) are unchanged.
+ * BM_HEAD_AUTO: BM_HEAD_LAST_STAGE (measured faster at C2, N = 2: a remote
+ *   head shard competes with that rank's running LLM op, and the last stage
+ *   waits for it -- profiles/r01/traces/trace_n2_m32_*.summary.json). */
+typedef enum { BM_HEAD_AUTO = 0, BM_HEAD_LAST_STAGE = 1, BM_HEAD_DP_SHARD = 2 } bm_head_place;
 
 /* Parameter kinds: DP parameters (encoder, projector, generator) are summed
  * over ranks at step end; LLM parameters belong to one stage. */
@@ -158,7 +176,8 @@ typedef struct {
 } bm_param_info;
 
 /* Parameters held by `rank` under `sc` (layers of its virtual stages; the
- * text table on rank 0, final norm + head on rank P-1; DP params everywhere).
+ * text table on rank 0, final norm + head on rank P-1; DP params everywhere;
+ * under BM_HEAD_DP_SHARD llm.head is a DP parameter).
  * DP parameters occupy the prefix [0, *dp_elems) of the buffers. */
 bm_status bm_param_count(const bm_model_cfg* mc, const bm_sched_cfg* sc, int32_t rank,
                          int32_t* n, int64_t* total_elems, int64_t* dp_elems);

@@ -21,6 +21,7 @@ PAYLOADS = ["act", "grad", "emb", "embgrad", "genin", "gengrad"]
 LLM_SCHED = {"1f1b": 0, "interleaved": 1}
 ENC_PLACE = {"none": 0, "dp_unit": 1, "entry_stage": 2}
 GEN_PLACE = {"none": 0, "dp_shard": 1, "last_stage": 2}
+HEAD_PLACE = {"auto": 0, "last_stage": 1, "dp_shard": 2}
 
 
 class BigMacError(RuntimeError):
@@ -49,8 +50,9 @@ class SchedStats(C.Structure):
 
 class ModelCfg(C.Structure):
     _fields_ = [(n, C.c_int32) for n in ("S", "d_in", "d_e", "f_e", "L_e", "d", "f", "L", "vocab",
-                                         "d_g", "f_g", "L_g", "d_t", "dtype", "max_n_mod", "max_n_gen")] + \
-               [("reserved", C.c_int32 * 8)]
+                                         "d_g", "f_g", "L_g", "d_t", "dtype", "max_n_mod", "max_n_gen",
+                                         "head_place")] + \
+               [("reserved", C.c_int32 * 7)]
 
 
 class ParamInfo(C.Structure):

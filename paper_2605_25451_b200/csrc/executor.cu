@@ -119,7 +119,16 @@ static bm_status check_model(const bm_model_cfg& mc, const bm_sched_cfg& sc) {
                "model widths must be multiples of 8");
   BM_CHECK_ARG(mc.max_n_mod > 0 && mc.max_n_mod <= mc.S && mc.max_n_gen > 0 && mc.max_n_gen <= mc.S,
                "max_n_mod / max_n_gen must be in [1, S]");
+  BM_CHECK_ARG(mc.head_place >= BM_HEAD_AUTO && mc.head_place <= BM_HEAD_DP_SHARD, "bad head_place");
+  BM_CHECK_ARG(mc.head_place != BM_HEAD_DP_SHARD || sc.gen_place == BM_GEN_DP_SHARD,
+               "BM_HEAD_DP_SHARD rides on the DP-sharded generator ops (gen_place = BM_GEN_DP_SHARD)");
   return BM_OK;
+}
+
+// LM head + CE DP-sharded over the ranks with the generator (bigmac.h bm_head_place)
+static bool head_dp(const bm_model_cfg& mc, const bm_sched_cfg& sc) {
+  if (sc.gen_place != BM_GEN_DP_SHARD) return false;
+  return mc.head_place == BM_HEAD_DP_SHARD;   // BM_HEAD_AUTO = last stage (bigmac.h)
 }
 
 static std::vector<PEntry> param_layout(const bm_model_cfg& mc, const bm_sched_cfg& sc, int rank, int64_t* total,
@@ -148,6 +157,8 @@ static std::vector<PEntry> param_layout(const bm_model_cfg& mc, const bm_sched_c
     add(p + ".fc2", mc.d_g, mc.f_g, BM_PARAM_DP);
   }
   add("gen.out", mc.d_t, mc.d_g, BM_PARAM_DP);
+  const bool hdp = head_dp(mc, sc);
+  if (hdp) add("llm.head", mc.vocab, mc.d, BM_PARAM_DP);
   *dp = off;
   const int P = sc.stages, V = sc.vchunks;
   const int lps = mc.L / (P * V);
@@ -163,7 +174,7 @@ static std::vector<PEntry> param_layout(const bm_model_cfg& mc, const bm_sched_c
   }
   if (rank == P - 1) {
     add("llm.final_norm", mc.d, 1, BM_PARAM_LLM);
-    add("llm.head", mc.vocab, mc.d, BM_PARAM_LLM);
+    if (!hdp) add("llm.head", mc.vocab, mc.d, BM_PARAM_LLM);
   }
   *total = off;
   return v;
@@ -205,7 +216,9 @@ struct bm_ctx {
   int64_t total_elems = 0, dp_elems = 0;
   bool has_enc = false, has_gen = false, gen_last = false;
   bool enc_entry = false;  // memory-efficient baseline: encoder as the entry stage's first layers
+  bool head_dp = false;    // LM head + CE DP-sharded with the generator (bm_head_place)
   int n_enc_slots = 0, n_llm_slots = 0, gen_rows = 0;
+  int head_rows = 0;       // max text rows of one head shard (head_dp)
   // comm layout
   std::vector<Chan> chans;
   std::map<std::tuple<int, int, int>, int> chan_idx;
@@ -267,7 +280,9 @@ struct bm_ctx {
   const void* last_src = nullptr;   // payload source of the last compute op
   int last_src_ring = -1;           // 0: bout, 1: gout (ring buffers needing a copy-done event)
   int last_src_idx = 0;
-  std::vector<const char*> genin_src;  // per destination rank (last stage)
+  std::vector<const char*> genin_src;  // per destination rank (last stage): generator rows of Hn
+  std::vector<const char*> headin_src; // per destination rank (last stage, head_dp): head rows of Hn
+  int gen_b = 0;                       // gout slot of the current generator microbatch
   cudaEvent_t producer_ev = nullptr;
   cudaStream_t producer_st = nullptr;  // stream of the last compute op (sends record their producer event here)
   // high-priority generator stream (P > 1, DP-sharded generator): gen shards run as
@@ -359,7 +374,7 @@ static int64_t payload_rows_max(const bm_ctx& c, int pay) {
     case BM_PAY_GRAD: return c.mc.S;
     case BM_PAY_EMB:
     case BM_PAY_EMBGRAD: return c.mc.max_n_mod;
-    default: return c.gen_rows;
+    default: return c.gen_rows + c.head_rows;   // genin / gengrad: [head rows | generator rows]
   }
 }
 
@@ -460,7 +475,10 @@ static void work_layout(bm_ctx& c, char* base) {
     c.ws_gen = b.take(c.ws_bytes);
   }
   c.embscr = b.take(embed_bwd_scratch_bytes(m.S));
-  if (last_rank) {
+  if (c.head_dp) {
+    c.logits = b.take((int64_t)c.head_rows * m.vocab * es);
+    c.ce_scr = (float*)b.take(S * 4);
+  } else if (last_rank) {
     c.logits = b.take(S * m.vocab * es);
     c.ce_scr = (float*)b.take(S * 4);
   }
@@ -476,7 +494,7 @@ static void work_layout(bm_ctx& c, char* base) {
   c.g_dz = b.take(ng * m.f_g * es);
   c.g_da = b.take(ng * m.f_g * es);
   c.g_dxn = b.take(ng * m.d_g * es);
-  for (int i = 0; i < 2; ++i) c.gout[i] = b.take(ng * d * es);
+  for (int i = 0; i < 2; ++i) c.gout[i] = b.take((ng + c.head_rows) * d * es);
   c.emb_local = b.take(n * d * es);
   c.loss = (float*)b.take((2 * (int64_t)c.M + 1) * 4);
   c.progress = (uint32_t*)b.take((2 + c.P) * 64);
@@ -680,6 +698,14 @@ static void shard_rows(const bm_ctx& c, int m, int r, int* lo, int* hi) {
   *hi = (int)(((int64_t)(r + 1) * n) / c.P);
 }
 
+// head shard r of microbatch m (head_dp): absolute rows of the text range [n_mod, S)
+static void head_rows_of(const bm_ctx& c, int m, int r, int* lo, int* hi) {
+  if (!c.head_dp) { *lo = *hi = 0; return; }
+  const int n_mod = c.n_mod[m], n_text = c.mc.S - n_mod;
+  *lo = n_mod + (int)(((int64_t)r * n_text) / c.P);
+  *hi = n_mod + (int)(((int64_t)(r + 1) * n_text) / c.P);
+}
+
 // ------------------------------------------------------------------ residual MLP blocks (encoder / generator)
 static bm_status mlp_blocks_fwd(bm_ctx& c, MlpSlot& sl, const char* prefix, int Lb, int n, int dm, int fm) {
   char nm[64];
@@ -797,7 +823,7 @@ static bm_status op_llm_fwd(bm_ctx& c, const bm_op& o, const RecvState& rs) {
     // through their genin sends) starts now, overlapping the LM head and CE below
     if (c.hn_ev) BM_CUDA_TRY(cudaEventRecord(c.hn_ev, c.st));
     BM_TRY(zero_bytes(sl.dHn, (int64_t)n_mod * d * es, c.st));
-    if (n_text > 0) {
+    if (n_text > 0 && !c.head_dp) {
       const char* hn_text = sl.Hn + (int64_t)n_mod * d * es;
       BM_TRY(lin_fwd(c, n_text, m.d, m.vocab, hn_text, m.d, P_(c, "llm.head"), LD_(c, "llm.head"), c.logits));
       const float sg = 1.f / ((float)n_text * c.M);
@@ -809,10 +835,13 @@ static bm_status op_llm_fwd(bm_ctx& c, const bm_op& o, const RecvState& rs) {
     }
     const int n_gen = c.n_gen[mb];
     c.genin_src.assign(c.P, nullptr);
+    c.headin_src.assign(c.P, nullptr);
     for (int q = 0; q < c.P; ++q) {
       int lo, hi;
       shard_rows(c, mb, q, &lo, &hi);
       c.genin_src[q] = sl.Hn + (int64_t)(m.S - n_gen + lo) * d * es;
+      head_rows_of(c, mb, q, &lo, &hi);
+      c.headin_src[q] = sl.Hn + (int64_t)lo * d * es;
     }
   }
   return BM_OK;
@@ -828,21 +857,37 @@ static bm_status op_llm_bwd(bm_ctx& c, const bm_op& o, const RecvState& rs) {
   if (s == c.P * c.V - 1) {
     // add the generator input-gradient shards into dHn, then final-norm backward
     const int n_gen = c.n_gen[mb];
-    if (c.has_gen && !c.gen_last) {
+    auto og = c.own_gout.find(mb);
+    if (c.head_dp) {
+      // head shards' dHn (text rows, disjoint across shards) first, then the generator adds
       for (const bm_op* r : rs.ops) {
         int lo, hi;
-        shard_rows(c, mb, r->peer, &lo, &hi);
-        char* dst = sl.dHn + (int64_t)(m.S - n_gen + lo) * d * es;
-        BM_TRY(add_(c, (int64_t)(hi - lo) * d, dst, recv_slot(c, r->peer, BM_PAY_GENGRAD, r->seq), dst));
+        head_rows_of(c, mb, r->peer, &lo, &hi);
+        BM_TRY(d2d(c, sl.dHn + (int64_t)lo * d * es, recv_slot(c, r->peer, BM_PAY_GENGRAD, r->seq), (int64_t)(hi - lo) * d * es));
+      }
+      if (og != c.own_gout.end()) {
+        int lo, hi;
+        head_rows_of(c, mb, c.rank, &lo, &hi);
+        BM_TRY(d2d(c, sl.dHn + (int64_t)lo * d * es, c.gout[og->second], (int64_t)(hi - lo) * d * es));
       }
     }
-    auto og = c.own_gout.find(mb);
+    if (c.has_gen && !c.gen_last) {
+      for (const bm_op* r : rs.ops) {
+        int lo, hi, hlo, hhi;
+        shard_rows(c, mb, r->peer, &lo, &hi);
+        head_rows_of(c, mb, r->peer, &hlo, &hhi);
+        char* dst = sl.dHn + (int64_t)(m.S - n_gen + lo) * d * es;
+        const char* src = recv_slot(c, r->peer, BM_PAY_GENGRAD, r->seq) + (int64_t)(hhi - hlo) * d * es;
+        BM_TRY(add_(c, (int64_t)(hi - lo) * d, dst, src, dst));
+      }
+    }
     if (og != c.own_gout.end()) {
       // this rank's own shard (the whole generator under BM_GEN_LAST_STAGE)
-      int lo, hi;
+      int lo, hi, hlo, hhi;
       shard_rows(c, mb, c.rank, &lo, &hi);
+      head_rows_of(c, mb, c.rank, &hlo, &hhi);
       char* dst = sl.dHn + (int64_t)(m.S - n_gen + lo) * d * es;
-      BM_TRY(add_(c, (int64_t)(hi - lo) * d, dst, c.gout[og->second], dst));
+      BM_TRY(add_(c, (int64_t)(hi - lo) * d, dst, c.gout[og->second] + (int64_t)(hhi - hlo) * d * es, dst));
       // the generator stream must not overwrite this gout slot before the add ran
       BM_CUDA_TRY(cudaEventRecord(c.gout_ev[og->second], c.st));
       c.gout_pending[og->second] = true;
@@ -896,11 +941,39 @@ static bm_status op_llm_bwd(bm_ctx& c, const bm_op& o, const RecvState& rs) {
 static bm_status op_gen_fwd(bm_ctx& c, const bm_op& o, const RecvState& rs) {
   const auto& m = c.mc;
   const int mb = o.mb;
+  const int64_t row = (int64_t)m.d * c.es;
+  // this microbatch's gout slot ([dHn head rows | generator dX rows]); it must not be
+  // overwritten before its previous send copy / own-shard add finished
+  const int b = c.gsel;
+  c.gsel ^= 1;
+  c.gen_b = b;
+  if (c.gout_pending[b]) {
+    BM_CUDA_TRY(cudaStreamWaitEvent(c.st, c.gout_ev[b], 0));
+    c.gout_pending[b] = false;
+  }
+  const bool own = c.rank == c.P - 1;
+  const char* slot = own ? nullptr : recv_slot(c, c.P - 1, BM_PAY_GENIN, rs.ops.at(0)->seq);
+  int hlo, hhi;
+  head_rows_of(c, mb, c.rank, &hlo, &hhi);
+  const int nh = hhi - hlo;
+  if (nh > 0) {
+    // LM head shard (head_dp): logits, CE fwd+bwd with the full-microbatch denominator
+    // (R8), dHn rows into gout, head weight gradient (DP parameter)
+    const char* Xh = own ? c.headin_src[c.rank] : slot;
+    const int n_text = m.S - c.n_mod[mb];
+    BM_TRY(lin_fwd(c, nh, m.d, m.vocab, Xh, m.d, P_(c, "llm.head"), LD_(c, "llm.head"), c.logits));
+    const float sg = 1.f / ((float)n_text * c.M);
+    const float sl_ = (float)nh / (float)n_text;
+    BM_TRY(TY(c, ce_fwd_bwd<bf16>(nh, m.vocab, (bf16*)c.logits, c.labels + (int64_t)mb * m.S + hlo, sg, c.loss + mb, sl_, 1, c.ce_scr, c.st),
+              ce_fwd_bwd<float>(nh, m.vocab, (float*)c.logits, c.labels + (int64_t)mb * m.S + hlo, sg, c.loss + mb, sl_, 1, c.ce_scr, c.st)));
+    BM_TRY(lin_dgrad(c, nh, m.d, m.vocab, c.logits, P_(c, "llm.head"), LD_(c, "llm.head"), c.gout[b], m.d));
+    BM_TRY(lin_wgrad(c, nh, m.d, m.vocab, c.logits, Xh, m.d, G_(c, "llm.head"), LD_(c, "llm.head")));
+  }
   int lo, hi;
   shard_rows(c, mb, c.rank, &lo, &hi);
   const int n = hi - lo;
   if (n <= 0) return BM_OK;
-  const char* X = (c.rank == c.P - 1) ? c.genin_src[c.rank] : recv_slot(c, c.P - 1, BM_PAY_GENIN, rs.ops.at(0)->seq);
+  const char* X = own ? c.genin_src[c.rank] : slot + (int64_t)nh * row;
   MlpSlot& sl = c.gen;
   BM_TRY(lin_fwd(c, n, m.d, m.d_g, X, m.d, P_(c, "gen.in"), LD_(c, "gen.in"), sl.E[0]));
   BM_TRY(mlp_blocks_fwd(c, sl, "gen", m.L_g, n, m.d_g, m.f_g));
@@ -915,20 +988,17 @@ static bm_status op_gen_fwd(bm_ctx& c, const bm_op& o, const RecvState& rs) {
 static bm_status op_gen_bwd(bm_ctx& c, const bm_op& o, const char* X) {
   const auto& m = c.mc;
   const int mb = o.mb;
-  int lo, hi;
+  int lo, hi, hlo, hhi;
   shard_rows(c, mb, c.rank, &lo, &hi);
+  head_rows_of(c, mb, c.rank, &hlo, &hhi);
   const int n = hi - lo;
   MlpSlot& sl = c.gen;
-  const int b = c.gsel;
-  c.gsel ^= 1;
+  const int b = c.gen_b;   // chosen (and waited for) by GenFwd
   c.last_src = c.gout[b];
   c.last_src_ring = 1;
   c.last_src_idx = b;
+  if (c.rank == c.P - 1) c.own_gout[mb] = b;
   if (n <= 0) return BM_OK;
-  if (c.gout_pending[b]) {
-    BM_CUDA_TRY(cudaStreamWaitEvent(c.st, c.gout_ev[b], 0));
-    c.gout_pending[b] = false;
-  }
   BM_TRY(lin_wgrad(c, n, m.d_g, m.d_t, sl.dout, sl.E[m.L_g], m.d_g, G_(c, "gen.out"), LD_(c, "gen.out")));
   BM_TRY(lin_dgrad(c, n, m.d_g, m.d_t, sl.dout, P_(c, "gen.out"), LD_(c, "gen.out"), c.g_dG, m.d_g));
   BM_TRY(mlp_blocks_bwd(c, sl, "gen", m.L_g, n, m.d_g, m.f_g, c.g_dG, c.g_dz, c.g_da, c.g_dxn));
@@ -936,8 +1006,8 @@ static bm_status op_gen_bwd(bm_ctx& c, const bm_op& o, const char* X) {
   // dX of this shard into the gout ring: sent to the last stage, or (own shard on
   // the last stage) added into dHn by B(mb, V-1) -- never written into dHn here,
   // where the LM-head dgrad of the same rows may still be running on the compute stream
-  BM_TRY(lin_dgrad(c, n, m.d, m.d_g, c.g_dG, P_(c, "gen.in"), LD_(c, "gen.in"), c.gout[b], m.d));
-  if (c.rank == c.P - 1) c.own_gout[mb] = b;
+  BM_TRY(lin_dgrad(c, n, m.d, m.d_g, c.g_dG, P_(c, "gen.in"), LD_(c, "gen.in"),
+                   c.gout[b] + (int64_t)(hhi - hlo) * m.d * c.es, m.d));
   return BM_OK;
 }
 
@@ -949,10 +1019,11 @@ static int64_t payload_bytes(const bm_ctx& c, const bm_op& o, int src_rank_for_s
     case BM_PAY_GRAD: return c.mc.S * row;
     case BM_PAY_EMB:
     case BM_PAY_EMBGRAD: return c.n_mod[o.mb] * row;
-    default: {
-      int lo, hi;
+    default: {   // genin / gengrad: [head rows | generator rows] of the shard's rank
+      int lo, hi, hlo, hhi;
       shard_rows(c, o.mb, src_rank_for_shard, &lo, &hi);
-      return (int64_t)(hi - lo) * row;
+      head_rows_of(c, o.mb, src_rank_for_shard, &hlo, &hhi);
+      return (int64_t)(hi - lo + hhi - hlo) * row;
     }
   }
 }
@@ -996,19 +1067,28 @@ static bm_status do_send(bm_ctx& c, const bm_op& o, int idx) {
   if (o.seq >= ch.K) {
     BM_TRY(wait_flag(c, cs, c.comm + ch.credit_off, base + (uint32_t)(o.seq - ch.K) + 1, "credit"));
   }
-  const char* src;
-  int64_t bytes;
+  // the message as (source, bytes) segments packed back to back into the slot:
+  // genin = [head rows of Hn (head_dp) | generator rows of Hn]; others one segment
+  const char* seg_src[2] = {nullptr, nullptr};
+  int64_t seg_bytes[2] = {0, 0};
   if (o.payload == BM_PAY_GENIN) {
-    src = c.genin_src[o.peer];
-    bytes = payload_bytes(c, o, o.peer);
-  } else if (o.payload == BM_PAY_GENGRAD) {
-    src = (const char*)c.last_src;
-    bytes = payload_bytes(c, o, c.rank);
+    int hlo, hhi;
+    head_rows_of(c, o.mb, o.peer, &hlo, &hhi);
+    seg_src[0] = c.headin_src.empty() ? nullptr : c.headin_src[o.peer];
+    seg_bytes[0] = (int64_t)(hhi - hlo) * c.mc.d * c.es;
+    seg_src[1] = c.genin_src[o.peer];
+    seg_bytes[1] = payload_bytes(c, o, o.peer) - seg_bytes[0];
   } else {
-    src = (const char*)c.last_src;
-    bytes = payload_bytes(c, o, c.rank);
+    seg_src[0] = (const char*)c.last_src;
+    seg_bytes[0] = payload_bytes(c, o, c.rank);
   }
+  const int64_t bytes = seg_bytes[0] + seg_bytes[1];
   char* dst = c.peer[o.peer] + ch.data_off + (int64_t)(o.seq % ch.K) * ch.slot_bytes;
+  auto copy_msg = [&]() -> bm_status {
+    if (seg_bytes[0] > 0) BM_TRY(peer_copy(c, dst, seg_src[0], seg_bytes[0], cs));
+    if (seg_bytes[1] > 0) BM_TRY(peer_copy(c, dst + seg_bytes[0], seg_src[1], seg_bytes[1], cs));
+    return BM_OK;
+  };
   cudaEvent_t tr_a = c.tracing ? trace_mark(c, cs) : nullptr;
   if (c.timing && bytes > 0) {
     const int pool = (int)(c.step & 1);
@@ -1020,11 +1100,11 @@ static bm_status do_send(bm_ctx& c, const bm_op& o, int idx) {
       ev.push_back(e);
     }
     BM_CUDA_TRY(cudaEventRecord(ev[2 * k], cs));
-    BM_TRY(peer_copy(c, dst, src, bytes, cs));
+    BM_TRY(copy_msg());
     BM_CUDA_TRY(cudaEventRecord(ev[2 * k + 1], cs));
     c.cbytes[pool].push_back(bytes);
   } else if (bytes > 0) {
-    BM_TRY(peer_copy(c, dst, src, bytes, cs));
+    BM_TRY(copy_msg());
   }
   CUresult r = drv().write32((CUstream)cs, (CUdeviceptr)(c.peer[o.peer] + ch.flag_off), base + (uint32_t)o.seq + 1, 0);
   if (r != CUDA_SUCCESS) { set_error("cuStreamWriteValue32 (data flag) failed " + std::to_string((int)r)); return BM_E_CUDA; }
@@ -1117,6 +1197,8 @@ bm_status bm_ctx_create(const bm_model_cfg* mc, const bm_schedule* s, int32_t ra
   c->n_enc_slots = std::max(st.peak_enc_units, 1);
   c->gen_rows = c->gen_last ? (rank == c->P - 1 ? mc->max_n_gen : 0) : (mc->max_n_gen + c->P - 1) / c->P;
   if (!c->has_gen) c->gen_rows = 0;
+  c->head_dp = head_dp(*mc, s->cfg);
+  c->head_rows = c->head_dp ? (mc->S + c->P - 1) / c->P : 0;
   comm_layout(*c);
   work_layout(*c, nullptr);
   // release annotations: Recv at i is released after the compute op j (genin: the following GenBwd)
@@ -1408,7 +1490,12 @@ bm_status bm_step(bm_ctx* c, const bm_batch* b, void* stream) {
         break;
       case BM_OP_LLM_BWD: BM_TRY(op_llm_bwd(x, o, rs)); live_llm -= llm_unit_bytes; break;
       case BM_OP_GEN_FWD:
-        gen_x = (x.rank == x.P - 1) ? nullptr : (rs.ops.empty() ? nullptr : recv_slot(x, x.P - 1, BM_PAY_GENIN, rs.ops[0]->seq));
+        gen_x = nullptr;
+        if (x.rank != x.P - 1 && !rs.ops.empty()) {
+          int hlo, hhi;   // the generator rows follow the head rows in the genin slot
+          head_rows_of(x, o.mb, x.rank, &hlo, &hhi);
+          gen_x = recv_slot(x, x.P - 1, BM_PAY_GENIN, rs.ops[0]->seq) + (int64_t)(hhi - hlo) * m.d * x.es;
+        }
         BM_TRY(op_gen_fwd(x, o, rs));
         live_gen += gen_unit_bytes;
         break;

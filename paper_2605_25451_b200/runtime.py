@@ -22,7 +22,8 @@ from . import _lib as L
 from . import schedule as BS
 
 
-def model_cfg(shape, dtype: str, max_n_mod: int | None = None, max_n_gen: int | None = None) -> L.ModelCfg:
+def model_cfg(shape, dtype: str, max_n_mod: int | None = None, max_n_gen: int | None = None,
+              head_place: str = "auto") -> L.ModelCfg:
     mc = L.ModelCfg()
     mc.S, mc.d_in, mc.d_e, mc.f_e, mc.L_e = shape.S, shape.d_in, shape.d_e, shape.f_e, shape.L_e
     mc.d, mc.f, mc.L, mc.vocab = shape.d, shape.f, shape.L, shape.vocab
@@ -30,6 +31,7 @@ def model_cfg(shape, dtype: str, max_n_mod: int | None = None, max_n_gen: int | 
     mc.dtype = L.BF16 if dtype == "bf16" else L.F32
     mc.max_n_mod = max_n_mod if max_n_mod is not None else min(shape.n_mod_law[2], shape.S)
     mc.max_n_gen = max_n_gen if max_n_gen is not None else min(shape.n_gen_law[2], shape.S)
+    mc.head_place = L.HEAD_PLACE[head_place]
     return mc
 
 
@@ -45,7 +47,8 @@ class DeviceBatch:
 
 
 class Runtime:
-    def __init__(self, shape, dtype="bf16", rank=0, world=1, group=None, device=None, sched_kw=None):
+    def __init__(self, shape, dtype="bf16", rank=0, world=1, group=None, device=None, sched_kw=None,
+                 head_place="auto"):
         self.shape = shape
         self.dtype = dtype
         self.rank, self.world = rank, world
@@ -56,7 +59,7 @@ class Runtime:
         self._stream = None   # own compute stream (created on first step)
         kw = dict(sched_kw or {})
         self.sched = BS.build(self.P, self.M, self.V, **kw)
-        self.mc = model_cfg(shape, dtype)
+        self.mc = model_cfg(shape, dtype, head_place=head_place)
         h = C.c_void_p()
         L.call("bm_ctx_create", C.byref(self.mc), self.sched.handle, rank, C.byref(h))
         self.ctx = h.value

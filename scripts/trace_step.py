@@ -29,6 +29,7 @@ def main():
     ap.add_argument("--V", type=int, default=1)
     ap.add_argument("--strategy", default="bigmac")
     ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--head", default="auto", choices=["auto", "last_stage", "dp_shard"])
     ap.add_argument("--out", default="gpurun_out/trace.json")
     a = ap.parse_args()
     rank, world = int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
@@ -42,7 +43,7 @@ def main():
     cfg = get_config(a.config, P=world, M=a.M, V=a.V)
     kw = {"bigmac": {}, "compute_efficient": {"warmup_units": cfg.M // world},
           "memory_efficient": {"enc_place": "entry_stage", "gen_place": "last_stage"}}[a.strategy]
-    rt = Runtime(cfg, "bf16", rank=rank, world=world, group=group, sched_kw=kw)
+    rt = Runtime(cfg, "bf16", rank=rank, world=world, group=group, sched_kw=kw, head_place=a.head)
     rt.init_random_weights(1)
     db = rt.device_batch(make_batch(cfg))
     for _ in range(a.warmup):
@@ -91,15 +92,22 @@ def main():
                     gaps.append((x["t0"] - prev, x["kind"], x["mb"], x["op"]))
                 prev = max(prev, x["t1"])
             gaps.sort(reverse=True)
-            per_kind = {}
+            per_kind, n_kind = {}, {}
             for x in comp:
                 per_kind[x["kind"]] = per_kind.get(x["kind"], 0.0) + x["t1"] - x["t0"]
+                n_kind[x["kind"]] = n_kind.get(x["kind"], 0) + 1
+            idle_by_next = {}
+            for g in gaps:
+                idle_by_next[g[1]] = idle_by_next.get(g[1], 0.0) + g[0]
             summ.append({"rank": r, "step_ms": end, "busy_ms": busy,
                          "compute_idle_ms": sum(g[0] for g in gaps),
                          "op_ms_by_kind": per_kind,
+                         "op_mean_ms": {k: per_kind[k] / n_kind[k] for k in per_kind},
+                         "compute_idle_ms_by_next_op": idle_by_next,
                          "top_idle_gaps_before": [{"ms": round(g[0], 3), "op": g[1], "mb": g[2], "idx": g[3]}
                                                   for g in gaps[:8]]})
-        print(json.dumps({"config": a.config, "P": world, "M": a.M, "strategy": a.strategy, "ranks": summ}))
+        print(json.dumps({"config": a.config, "P": world, "M": a.M, "strategy": a.strategy, "head": a.head,
+                          "ranks": summ}))
     if world > 1:
         dist.barrier(group=group)
     rt.close()

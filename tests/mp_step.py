@@ -1,6 +1,6 @@
 """One rank of a multi-GPU parity run (launched by tests/test_gpu_step.py via torchrun).
 
-usage: mp_step.py CONFIG P M V DTYPE GEN_PLACE
+usage: mp_step.py CONFIG P M V DTYPE GEN_PLACE[+head_dp]
 Every rank runs bm_step on its own GPU; rank 0 gathers all gradients and
 compares them with the fp64 oracle (normwise rel tol 1e-4 fp32 / 2e-2 bf16).
 """
@@ -31,14 +31,18 @@ def main():
     cfg = get_config(name, P=P, M=M, V=V)
     W, B = make_weights(cfg), make_batch(cfg)
     # strategy spec: "<gen_place>", "entry_stage+<gen_place>" (memory-efficient baseline),
-    # "ce" (compute-efficient baseline: all encoder forwards first, W = M / P)
+    # "ce" (compute-efficient baseline: all encoder forwards first, W = M / P);
+    # "<gen_place>+head_dp": the LM head + CE DP-sharded with the generator (BM_HEAD_DP_SHARD)
+    head = "auto"
+    if gen.endswith("+head_dp"):
+        gen, head = gen[: -len("+head_dp")], "dp_shard"
     if gen == "ce":
         kw = {"warmup_units": M // P}
     elif gen.startswith("entry_stage+"):
         kw = {"enc_place": "entry_stage", "gen_place": gen.split("+")[1]}
     else:
         kw = {"gen_place": gen}
-    rt = Runtime(cfg, dtype, rank=rank, world=world, sched_kw=kw)
+    rt = Runtime(cfg, dtype, rank=rank, world=world, sched_kw=kw, head_place=head)
     rt.load_weights(W)
     db = rt.device_batch(B)
     for _ in range(2):

@@ -89,6 +89,32 @@ def test_step_single_gpu_baselines(oracle_cache, kw):
     rt.close()
 
 
+@pytest.mark.parametrize("cfg_name,dtype", [("C1", "f32"), ("C1", "bf16"), ("C1M", "f32"), ("C1M", "bf16")])
+def test_step_single_gpu_head_dp_shard(oracle_cache, cfg_name, dtype):
+    """BM_HEAD_DP_SHARD at P = 1: the LM head + CE run inside GenFwd on the
+    generator stream (the single shard is the whole text range); same results."""
+    from paper_2605_25451_b200.runtime import Runtime
+    cfg = get_config(cfg_name, P=1, M=4, V=1)
+    W, B, (loss_ref, per_ref, G_ref) = reference(oracle_cache, cfg)
+    rt = Runtime(cfg, dtype, head_place="dp_shard")
+    assert rt.params["llm.head"][4] == 0          # DP parameter
+    rt.load_weights(W)
+    db = rt.device_batch(B)
+    rt.step(db)
+    torch.cuda.synchronize()
+    loss, ce, mse = rt.losses()
+    tol = TOL[dtype]
+    assert abs(loss - loss_ref) <= tol * abs(loss_ref)
+    assert rel(ce, np.array([a for a, _ in per_ref])) <= tol
+    bad = {n: rel(rt.grad(n), G_ref[n]) for n in rt.names()}
+    assert not {k: v for k, v in bad.items() if v > tol}, bad
+    g1 = rt.grads_t.clone()
+    rt.step(db)
+    torch.cuda.synchronize()
+    assert torch.equal(g1, rt.grads_t)
+    rt.close()
+
+
 def test_trace_records_every_op():
     """bm_ctx_trace_get: one record per compute op / receive (+ the tail), in the
     rank's op order on each stream, with non-decreasing times; tracing does not
@@ -150,6 +176,7 @@ def _torchrun(nproc, *args, timeout=600):
 
 @pytest.mark.parametrize("P,M,V,dtype,gen", [(2, 4, 1, "f32", "dp_shard"), (2, 4, 1, "bf16", "dp_shard"),
                                            (2, 8, 2, "f32", "dp_shard"), (2, 4, 1, "f32", "last_stage"),
+                                           (2, 4, 1, "f32", "dp_shard+head_dp"), (2, 8, 2, "bf16", "dp_shard+head_dp"),
                                            (2, 4, 1, "f32", "entry_stage+last_stage"),
                                            (2, 4, 1, "bf16", "ce")])
 def test_step_two_gpus(P, M, V, dtype, gen):
@@ -169,7 +196,8 @@ def test_step_two_gpus_medium(cfg_name, P, M, V, dtype):
 
 @pytest.mark.parametrize("P,M,V,dtype,gen", [(4, 8, 1, "f32", "dp_shard"), (4, 8, 1, "bf16", "dp_shard"),
                                            (4, 16, 1, "bf16", "dp_shard"), (4, 16, 1, "bf16", "ce"),
-                                           (4, 16, 1, "f32", "entry_stage+last_stage"), (4, 16, 1, "f32", "ce")])
+                                           (4, 16, 1, "f32", "entry_stage+last_stage"), (4, 16, 1, "f32", "ce"),
+                                           (4, 8, 1, "bf16", "dp_shard+head_dp")])
 def test_step_four_gpus(P, M, V, dtype, gen):
     # "ce" (W = M / P) once deadlocked: a copy-engine send parked on a credit wait
     # blocked another stream's copy in a shared copy channel

@@ -42,15 +42,17 @@ def test_library_is_sm100a():
     assert "LDTM" in sass             # tcgen05.ld (TMEM -> registers)
 
 
+@pytest.mark.parametrize("head", ["auto", "last_stage", "dp_shard"])
 @pytest.mark.parametrize("P,V,rank", [(1, 1, 0), (2, 1, 0), (2, 1, 1), (4, 1, 3), (2, 2, 0), (2, 2, 1), (1, 4, 0)])
-def test_param_layout_matches_model(P, V, rank):
+def test_param_layout_matches_model(P, V, rank, head):
     from synth import get_config, param_specs
     from paper_2605_25451_b200 import _lib as L
     from paper_2605_25451_b200 import schedule as BS
     from paper_2605_25451_b200.runtime import model_cfg
     cfg = get_config("C1", P=P, M=2 * P, V=V)
-    mc = model_cfg(cfg, "bf16")
+    mc = model_cfg(cfg, "bf16", head_place=head)
     sc = BS.make_cfg(P, 2 * P, V)
+    head_dp = head == "dp_shard"   # bigmac.h bm_head_place (auto = last stage)
     n, tot, dp = C.c_int32(), C.c_int64(), C.c_int64()
     L.call("bm_param_count", C.byref(mc), C.byref(sc), rank, C.byref(n), C.byref(tot), C.byref(dp))
     specs = {nm: shp for nm, shp, _ in param_specs(cfg)}
@@ -73,6 +75,8 @@ def test_param_layout_matches_model(P, V, rank):
             assert got.get(nm) == 0, nm            # DP params on every rank
         elif nm == "llm.embed":
             assert (nm in got) == (rank == 0)
+        elif nm == "llm.head" and head_dp:
+            assert got.get(nm) == 0, nm            # DP-sharded head: a DP param on every rank
         elif nm in ("llm.final_norm", "llm.head"):
             assert (nm in got) == (rank == P - 1)
         else:
