@@ -8,10 +8,13 @@ Workload (BASELINE.json configs[1], "C2"): ViT-S-shaped encoder + 1B-shaped
 LLM + small generator, S = 4096, 1F1B LLM schedule with the encoder/generator
 nested in it, P = N pipeline stages (one per GPU), synthetic data with
 log-uniform[256, 1024] modality / generation rows per sample, bf16.
-M = 16 microbatches per GPU (global batch 16 N, one sample per microbatch):
-every GPU processes 16 microbatches x L/N layers per step at any N ("weak"
-scaling; the 1F1B bubble (N-1)/(M+N-1) stays <= 5.2 %).  --microbatches M
-fixes the global batch instead ("strong").
+P = min(N, 4) pipeline stages and D = N / P pipeline replicas (SURVEY §8(d)
+GPU ladder: "at G = 8, P = 4 x DP = 2"; replicas all-reduce their LLM stage
+gradients, every process the DP modules').  16 microbatches per GPU: each
+replica runs M = 16 P, global batch 16 N (one sample per microbatch), so every
+GPU processes 16 microbatches x L/P layers per step at any N ("weak" scaling;
+the 1F1B bubble (P-1)/(M+P-1) stays <= 4.5 %).  --stages P overrides P;
+--microbatches M fixes the per-replica M instead ("strong").
 
 Prints ONE JSON line on rank 0.
 """
@@ -138,18 +141,57 @@ def cpu_oracle_sample(cfg, rows=512, repeats=1):
     return dt, 18.0 * rows * cfg.d * cfg.f, cores
 
 
+def stages_of(args, N):
+    P = args.stages or min(N, 4)
+    if N % P:
+        raise SystemExit(f"--gpus {N} is not a multiple of --stages {P}")
+    return P
+
+
 def workload(args, N):
+    """(per-replica config, P, D)."""
     from synth import get_config
-    cfg = get_config(args.config, P=N, M=args.microbatches or get_config(args.config).M * N, V=1)
-    return cfg
+    P = stages_of(args, N)
+    cfg = get_config(args.config, P=P, M=args.microbatches or get_config(args.config).M * P, V=1)
+    return cfg, P, N // P
 
 
-def config_dict(cfg, N):
+# LM head + CE of one microbatch on the last stage, in LLM-layer (fwd+bwd) equivalents,
+# measured at C2 (profiles/r01/traces/trace_n2_m32_last_stage.summary.json: the last
+# stage's F(m) takes 4.27 ms vs 2.55 ms elsewhere for 8 layers whose F+B is 8.2 ms)
+HEAD_LAYERS = 1.7
+
+
+def last_stage_layers(args, cfg, P):
+    """Uneven LLM partition (bigmac.h last_stage_layers): the n minimising the
+    slowest stage max(ceil((L - n) / (P V - 1)), n + HEAD_LAYERS); ties -> larger n."""
+    if args.last_stage_layers >= 0:
+        return args.last_stage_layers
+    PV = P * cfg.V
+    if PV == 1:
+        return 0
+    best = None
+    for n in range(1, cfg.L - (PV - 1) + 1):
+        cost = max(-(-(cfg.L - n) // (PV - 1)), n + HEAD_LAYERS)
+        if best is None or cost <= best[0]:
+            best = (cost, n)
+    uniform = cfg.L // PV + HEAD_LAYERS if cfg.L % PV == 0 else float("inf")
+    return 0 if uniform <= best[0] else best[1]
+
+
+def global_batch(cfg, D):
+    """One global batch of M D microbatches; replica k runs [kM, (k+1)M)."""
+    from synth import make_batch
+    return make_batch(cfg, M=cfg.M * D)
+
+
+def config_dict(cfg, P, D):
+    rep_txt = f" x {D} pipeline replicas" if D > 1 else ""
     return {"workload": f"{cfg.name}: ViT-S-shaped encoder (d_e={cfg.d_e}, L_e={cfg.L_e}) + 1B-shaped LLM "
                         f"(d={cfg.d}, f={cfg.f}, L={cfg.L}, vocab={cfg.vocab}) + generator (d_g={cfg.d_g}, L_g={cfg.L_g}); "
-                        f"nested pipeline P={N} stages, M={cfg.M} microbatches, 1F1B",
-            "global_batch": cfg.M, "seq_len": cfg.S, "parallelism": f"pp{N}",
-            "stages": N, "microbatches": cfg.M, "vchunks": cfg.V,
+                        f"nested pipeline P={P} stages{rep_txt}, M={cfg.M} microbatches per replica, 1F1B",
+            "global_batch": cfg.M * D, "seq_len": cfg.S, "parallelism": f"pp{P}" + (f"xdp{D}" if D > 1 else ""),
+            "stages": P, "replicas": D, "microbatches": cfg.M, "vchunks": cfg.V,
             "n_mod_law": list(cfg.n_mod_law), "n_gen_law": list(cfg.n_gen_law),
             "l2_policy": "working set (weights + activations, GBs) >> 126 MB L2; no flush",
             "strategy": getattr(cfg, "_strategy", "bigmac")}
@@ -167,9 +209,8 @@ def run_reference(args):
     N = args.gpus
     if rank != 0:
         return
-    from synth import make_batch
-    cfg = workload(args, N)
-    batch = make_batch(cfg)
+    cfg, P, D = workload(args, N)
+    batch = global_batch(cfg, D)
     F = step_flops(cfg, batch.n_mod, batch.n_gen)
     rows = args.ref_rows
     for _ in range(args.warmup):
@@ -181,14 +222,14 @@ def run_reference(args):
     sec = sum(t for t, _ in ts)
     flops = sum(f for _, f in ts)
     rate = flops / sec
-    value = rate / (F / cfg.M)
+    value = rate / (F / (cfg.M * D))
     sample = (f"per step: oracle (numpy fp64) fwd+bwd of one LLM layer on {rows} rows of a {cfg.name} microbatch "
               f"(d={cfg.d}, f={cfg.f}); samples/s extrapolated by the step's algorithmic FLOPs per sample")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": N,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * sec / args.steps,
             "higher_is_better": True, "scaling": "strong" if args.microbatches else "weak", "vs_baseline": None,
             "dtype": "f64",
-            "data": "synthetic", "config": config_dict(cfg, N),
+            "data": "synthetic", "config": config_dict(cfg, P, D),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -201,7 +242,10 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C2")
-    ap.add_argument("--microbatches", type=int, default=0)
+    ap.add_argument("--microbatches", type=int, default=0, help="per-replica M (default 16 P)")
+    ap.add_argument("--last-stage-layers", type=int, default=-1,
+                    help="LLM layers of the last stage (bigmac.h); -1 = balance the LM head (HEAD_LAYERS), 0 = uniform")
+    ap.add_argument("--stages", type=int, default=0, help="pipeline stages P (default min(N, 4)); D = N / P replicas")
     ap.add_argument("--dtype", default="bf16")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -230,16 +274,20 @@ def main():
         dist.init_process_group("cpu:gloo,cuda:nccl", device_id=torch.device("cuda", local))
         group = dist.new_group(backend="gloo")
 
-    from synth import make_batch
+    from synth import slice_batch
     from paper_2605_25451_b200.runtime import Runtime
-    cfg = workload(args, N)
+    cfg, P, D = workload(args, N)
     if args.warmup < 3:
         raise SystemExit("--warmup must be >= 3")
-    sched_kw = {"bigmac": {}, "compute_efficient": {"warmup_units": cfg.M // N},
+    sched_kw = {"bigmac": {}, "compute_efficient": {"warmup_units": cfg.M // P},
                 "memory_efficient": {"enc_place": "entry_stage", "gen_place": "last_stage"}}[args.strategy]
-    rt = Runtime(cfg, args.dtype, rank=rank, world=world, group=group, sched_kw=sched_kw, head_place=args.head)
+    n_last = last_stage_layers(args, cfg, P)
+    rt = Runtime(cfg, args.dtype, rank=rank, world=world, group=group, sched_kw=sched_kw, head_place=args.head,
+                 last_stage_layers=n_last)
     rt.init_random_weights(seed=1)
-    batch = make_batch(cfg)
+    gbatch = global_batch(cfg, D)
+    replica = rank // P
+    batch = slice_batch(gbatch, replica * cfg.M, (replica + 1) * cfg.M)
     db = rt.device_batch(batch)
     stream = torch.cuda.current_stream()
 
@@ -300,7 +348,7 @@ def main():
     barrier()
     ms_max = max_over_ranks(ms)
     ms_per_step = ms_max / args.steps
-    samples = cfg.M * args.steps
+    samples = cfg.M * D * args.steps
     value = samples / (ms_max / 1000.0)
     loss, _, _ = rt.losses()
     peak_alloc = max_over_ranks(float(torch.cuda.max_memory_allocated()))
@@ -326,7 +374,7 @@ def main():
         barrier()
         ems = max_over_ranks(f0.elapsed_time(f1))
         h2d = sum_over_ranks(hb.h2d_bytes)
-        e2e = {"value": cfg.M * args.steps / (ems / 1000.0), "unit": UNIT,
+        e2e = {"value": cfg.M * D * args.steps / (ems / 1000.0), "unit": UNIT,
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(4 * world),
                "ms_per_step": ems / args.steps}
 
@@ -345,7 +393,7 @@ def main():
         return
 
     peaks, peak_src = load_peaks()
-    F = step_flops(cfg, batch.n_mod, batch.n_gen)
+    F = step_flops(cfg, gbatch.n_mod, gbatch.n_gen)
     sustained = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
     achieved = gemm_flops_all / (gemm_ms_all / 1000.0) / 1e12 if gemm_ms_all > 0 else 0.0
     traffic = None
@@ -365,13 +413,13 @@ def main():
                 "avg_launch_ms": gemm_ms_all / max(n_gemm_all, 1)}
     t_roof_ms = F / (N * peaks["bf16_tflops"] * 1e12) * 1e3
     step_roof = {"flops_per_step": F, "t_roof_ms": t_roof_ms, "frac": t_roof_ms / ms_per_step,
-                 "peak_tflops": peaks["bf16_tflops"], "bubble_bound": (N - 1) / (cfg.M + N - 1)}
+                 "peak_tflops": peaks["bf16_tflops"], "bubble_bound": (P - 1) / (cfg.M + P - 1)}
 
     cpu = None
     if not args.no_cpu and N == 1:
         dt, fl, cores = cpu_oracle_sample(cfg, rows=2048)
         rate = fl / dt
-        cpu = {"value": rate / (F / cfg.M), "unit": UNIT, "cores": cores, "kind": "oracle",
+        cpu = {"value": rate / (F / (cfg.M * D)), "unit": UNIT, "cores": cores, "kind": "oracle",
                "sample": f"oracle (numpy fp64) fwd+bwd of one LLM layer on 2048 rows of a {cfg.name} microbatch "
                          f"({dt:.1f} s); samples/s extrapolated by the step's algorithmic FLOPs per sample"}
 
@@ -380,7 +428,8 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "strong" if args.microbatches else "weak",
             "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
-            "config": dict(config_dict(cfg, N), strategy=args.strategy, head_place=head_place_name(args, N)),
+            "config": dict(config_dict(cfg, P, D), strategy=args.strategy, head_place=head_place_name(args, N),
+                           last_stage_layers=n_last),
             "roofline": roofline, "step_roofline": step_roof,
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches_all, "clocks": clocks,
             "nvlink": ({"bytes_per_step_all_ranks": comm_bytes_all / n_inst,
@@ -389,7 +438,7 @@ def main():
                         "avg_link_GBps_over_step": comm_bytes_all / n_inst / max(world, 1) / (ms_per_step / 1e3) / 1e9,
                         "note": "copy-engine copies into peer IPC receive slots over NVLink; copy_GBps = bytes / "
                                 "summed copy durations on the comm streams"} if world > 1 else None),
-            "tokens_per_s": cfg.M * cfg.S * args.steps / (ms_max / 1000.0),
+            "tokens_per_s": cfg.M * D * cfg.S * args.steps / (ms_max / 1000.0),
             "peak_hbm_gb_per_gpu": peak_alloc / 1e9, "stash_peak_bytes_rank0": stash,
             "loss": loss}
     print(json.dumps(line), flush=True)

@@ -143,8 +143,18 @@ typedef struct {
   int32_t dtype;                  /* bm_dtype of weights/activations           */
   int32_t max_n_mod, max_n_gen;   /* upper bounds on per-sample row counts     */
   int32_t head_place;             /* bm_head_place                             */
-  int32_t reserved[7];            /* must be zero                              */
+  int32_t last_stage_layers;      /* LLM layers of the last virtual stage; 0 = uniform (below) */
+  int32_t reserved[6];            /* must be zero                              */
 } bm_model_cfg;
+
+/* LLM layer partition over the P V virtual stages (s = chunk P + rank), in
+ * layer order.  last_stage_layers = 0: L / (P V) layers each (L % (P V) == 0
+ * required).  last_stage_layers = n > 0: virtual stage P V - 1 (which also
+ * runs the LM head + CE under BM_HEAD_LAST_STAGE) gets n layers; the other
+ * P V - 1 stages split the remaining L - n as evenly as possible, the first
+ * (L - n) mod (P V - 1) stages one layer more.  Requires 1 <= n and
+ * L - n >= P V - 1 (every stage holds a layer).  Uneven splits balance the
+ * head's cost; op lists do not depend on the partition. */
 
 /* Where the final-norm output's LM head + cross-entropy (fwd and bwd) run.
  * BM_HEAD_LAST_STAGE: in F(m, V-1) on rank P-1, as in the paper's Megatron
@@ -218,6 +228,23 @@ bm_status bm_ctx_open_peer(bm_ctx* c, int32_t peer, const uint8_t handle[64], in
  * the id, the caller broadcasts it. */
 bm_status bm_nccl_unique_id(uint8_t id[128]);
 bm_status bm_ctx_init_nccl(bm_ctx* c, const uint8_t id[128], int32_t nranks, int32_t rank);
+
+/* Pipeline replicas ("if G > P, pipeline replicas are added,
+ * with an allreduce of LLM stage grads across replicas of the same stage").
+ * G = P * D processes; this context is stage `rank` (bm_ctx_create) of
+ * replica `replica` in [0, D), and runs its own M microbatches (global batch
+ * M * D).  id_world: one NCCL id shared by all P * D processes (communicator
+ * rank replica * P + stage) for the DP parameters (encoder, projector,
+ * generator); id_stage: one id shared by the D processes of this stage
+ * (communicator rank = replica) for this stage's LLM parameters.  Call after
+ * bm_ctx_init_nccl (the replica's own pipeline group, which still sums the
+ * loss terms; P = 1 needs no pipeline group).  From then on gradients are the
+ * mean over the global batch (per-sample scale 1 / (M D)) and the step loss
+ * (bm_ctx_loss_ptr element 2M) is the global-batch loss; the per-microbatch
+ * terms stay the replica's own.  D = 1 is the plain single-pipeline case.
+ * Errors: BM_E_INVALID (D < 1, replica out of range), BM_E_NCCL. */
+bm_status bm_ctx_init_replicas(bm_ctx* c, int32_t D, int32_t replica, const uint8_t id_world[128],
+                               const uint8_t id_stage[128]);
 
 /* One step's inputs.  If on_host != 0 the array pointers are host pointers
  * and bm_step copies them to the device inside the step (end-to-end path).

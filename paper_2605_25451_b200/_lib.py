@@ -51,8 +51,8 @@ class SchedStats(C.Structure):
 class ModelCfg(C.Structure):
     _fields_ = [(n, C.c_int32) for n in ("S", "d_in", "d_e", "f_e", "L_e", "d", "f", "L", "vocab",
                                          "d_g", "f_g", "L_g", "d_t", "dtype", "max_n_mod", "max_n_gen",
-                                         "head_place")] + \
-               [("reserved", C.c_int32 * 7)]
+                                         "head_place", "last_stage_layers")] + \
+               [("reserved", C.c_int32 * 6)]
 
 
 class ParamInfo(C.Structure):
@@ -101,6 +101,7 @@ SIGNATURES = {
     "bm_ctx_open_peer": [_P, _I32, C.POINTER(C.c_uint8), _I64],
     "bm_nccl_unique_id": [C.POINTER(C.c_uint8)],
     "bm_ctx_init_nccl": [_P, C.POINTER(C.c_uint8), _I32, _I32],
+    "bm_ctx_init_replicas": [_P, _I32, _I32, C.POINTER(C.c_uint8), C.POINTER(C.c_uint8)],
     "bm_step": [_P, C.POINTER(Batch), _P],
     "bm_ctx_loss_ptr": [_P, C.POINTER(_P)],
     "bm_ctx_launch_count": [_P, C.POINTER(_I64)],

@@ -854,8 +854,8 @@ int64_t rmsnorm_bwd_scratch_floats(int rows, int cols) {
 }
 
 // step loss L = (1/M) sum_m (CE_m + MSE_m) from loss[0:2M] into loss[2M]
-bm_status loss_finalize(int M, float* loss, cudaStream_t st) {
-  BM_CUDA_TRY(launch_k(sum_scale_kernel, dim3(1), dim3(1024), 0, st, 2 * M, loss, 1.f / M, 0, loss + 2 * M));
+bm_status loss_finalize(int M, float* loss, float scale, cudaStream_t st) {
+  BM_CUDA_TRY(launch_k(sum_scale_kernel, dim3(1), dim3(1024), 0, st, 2 * M, loss, scale, 0, loss + 2 * M));
   count_launch();
   BM_CUDA_TRY(cudaGetLastError());
   return BM_OK;

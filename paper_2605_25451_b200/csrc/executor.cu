@@ -113,7 +113,11 @@ static bm_status check_model(const bm_model_cfg& mc, const bm_sched_cfg& sc) {
   BM_CHECK_ARG(mc.d_in > 0 && mc.d_e > 0 && mc.f_e > 0 && mc.L_e >= 0, "bad encoder dims");
   BM_CHECK_ARG(mc.d_g > 0 && mc.f_g > 0 && mc.L_g >= 0 && mc.d_t > 0, "bad generator dims");
   BM_CHECK_ARG(mc.dtype == BM_BF16 || mc.dtype == BM_F32, "dtype must be bf16 or fp32");
-  BM_CHECK_ARG(mc.L % (sc.stages * sc.vchunks) == 0, "L must be a multiple of P*V");
+  if (mc.last_stage_layers == 0)
+    BM_CHECK_ARG(mc.L % (sc.stages * sc.vchunks) == 0, "L must be a multiple of P*V (or set last_stage_layers)");
+  else
+    BM_CHECK_ARG(mc.last_stage_layers >= 1 && mc.L - mc.last_stage_layers >= sc.stages * sc.vchunks - 1,
+                 "last_stage_layers must leave at least one layer per virtual stage");
   BM_CHECK_ARG(mc.d % 8 == 0 && mc.f % 8 == 0 && mc.d_e % 8 == 0 && mc.f_e % 8 == 0 && mc.d_g % 8 == 0 &&
                    mc.f_g % 8 == 0 && mc.d_t % 8 == 0 && mc.vocab % 8 == 0,
                "model widths must be multiples of 8");
@@ -123,6 +127,33 @@ static bm_status check_model(const bm_model_cfg& mc, const bm_sched_cfg& sc) {
   BM_CHECK_ARG(mc.head_place != BM_HEAD_DP_SHARD || sc.gen_place == BM_GEN_DP_SHARD,
                "BM_HEAD_DP_SHARD rides on the DP-sharded generator ops (gen_place = BM_GEN_DP_SHARD)");
   return BM_OK;
+}
+
+// LLM layers [*l0, *l0 + *n) of virtual stage s (bigmac.h, last_stage_layers)
+static void stage_layers(const bm_model_cfg& mc, int PV, int s, int* l0, int* n) {
+  if (mc.last_stage_layers == 0 || PV == 1) {
+    *n = mc.L / PV;
+    *l0 = s * *n;
+    return;
+  }
+  if (s == PV - 1) {
+    *n = mc.last_stage_layers;
+    *l0 = mc.L - *n;
+    return;
+  }
+  const int rest = mc.L - mc.last_stage_layers, q = rest / (PV - 1), r = rest % (PV - 1);
+  *n = q + (s < r ? 1 : 0);
+  *l0 = s * q + std::min(s, r);
+}
+// most layers of one virtual stage held by `rank` (stash slot depth)
+static int max_stage_layers(const bm_model_cfg& mc, int P, int V, int rank) {
+  int mx = 0;
+  for (int c = 0; c < V; ++c) {
+    int l0, n;
+    stage_layers(mc, P * V, c * P + rank, &l0, &n);
+    mx = std::max(mx, n);
+  }
+  return mx;
 }
 
 // LM head + CE DP-sharded over the ranks with the generator (bigmac.h bm_head_place)
@@ -161,11 +192,11 @@ static std::vector<PEntry> param_layout(const bm_model_cfg& mc, const bm_sched_c
   if (hdp) add("llm.head", mc.vocab, mc.d, BM_PARAM_DP);
   *dp = off;
   const int P = sc.stages, V = sc.vchunks;
-  const int lps = mc.L / (P * V);
   if (rank == 0) add("llm.embed", mc.vocab, mc.d, BM_PARAM_LLM);
   for (int c = 0; c < V; ++c) {
-    const int s = c * P + rank;
-    for (int l = s * lps; l < (s + 1) * lps; ++l) {
+    int l0, nl;
+    stage_layers(mc, P * V, c * P + rank, &l0, &nl);
+    for (int l = l0; l < l0 + nl; ++l) {
       const std::string p = "llm.layer" + std::to_string(l);
       add(p + ".norm", mc.d, 1, BM_PARAM_LLM);
       add(p + ".gate_up", 2 * mc.f, mc.d, BM_PARAM_LLM);
@@ -194,6 +225,7 @@ struct LlmSlot {
   std::vector<float*> rstd;
   char *gin = nullptr, *Hn = nullptr, *dHn = nullptr;
   float* rstd_f = nullptr;
+  int nl = 0;   // layers of the virtual stage the slot currently stashes
 };
 struct MlpSlot {  // encoder (L_e blocks) or generator (L_g blocks)
   std::vector<char*> E, xn, a, z;
@@ -265,6 +297,11 @@ struct bm_ctx {
   bool bout_pending[2] = {false, false}, gout_pending[2] = {false, false};
   int bsel = 0, gsel = 0;
   ncclComm_t nc = nullptr;
+  // pipeline replicas (bm_ctx_init_replicas): D pipelines, this one is `replica`
+  int D = 1, replica = 0;
+  ncclComm_t nc_world = nullptr;   // all P * D processes: DP parameters
+  ncclComm_t nc_stage = nullptr;   // the D processes of this stage: its LLM parameters
+  float gscale = 1.f;              // per-sample gradient scale 1 / (M D)
   int64_t step = 0;
   int64_t launches = 0;
   int64_t stash_peak[3] = {0, 0, 0};
@@ -357,6 +394,8 @@ bm_ctx::~bm_ctx() {
   for (size_t r = 0; r < peer.size(); ++r)
     if (peer[r] && (int)r != rank) cudaIpcCloseMemHandle(peer[r]);
   if (nc && nccl().ok) nccl().CommDestroy(nc);
+  if (nc_world && nccl().ok) nccl().CommDestroy(nc_world);
+  if (nc_stage && nccl().ok) nccl().CommDestroy(nc_stage);
   if (progress_h) cudaFreeHost((void*)progress_h);
   if (g_dbg_ctx == this) {
     g_dbg_ctx = nullptr;
@@ -799,13 +838,16 @@ static bm_status op_llm_fwd(bm_ctx& c, const bm_op& o, const RecvState& rs) {
               embed_fwd<float>(m.S, m.d, n_mod, c.ids + (int64_t)mb * S, (const float*)P_(c, "llm.embed"), (const float*)emb, (float*)sl.x[0], c.st)));
   } else if ((s - 1) % c.P == c.rank) {
     const int prev = c.llm_live.at({mb, ch - 1});
-    BM_TRY(d2d(c, sl.x[0], c.llm[prev].x[c.lps], S * d * es));
+    BM_TRY(d2d(c, sl.x[0], c.llm[prev].x[c.llm[prev].nl], S * d * es));
   } else {
     BM_TRY(d2d(c, sl.x[0], recv_slot(c, (s - 1) % c.P, BM_PAY_ACT, rs.ops.at(0)->seq), S * d * es));
   }
+  int l0, nl;
+  stage_layers(m, c.P * c.V, s, &l0, &nl);
+  sl.nl = nl;
   char nm[64];
-  for (int j = 0; j < c.lps; ++j) {
-    const int l = s * c.lps + j;
+  for (int j = 0; j < nl; ++j) {
+    const int l = l0 + j;
     snprintf(nm, sizeof nm, "llm.layer%d.norm", l);
     BM_TRY(norm_fwd(c, m.S, m.d, sl.x[j], P_(c, nm), sl.xn[j], sl.rstd[j]));
     snprintf(nm, sizeof nm, "llm.layer%d.gate_up", l);
@@ -813,12 +855,12 @@ static bm_status op_llm_fwd(bm_ctx& c, const bm_op& o, const RecvState& rs) {
     snprintf(nm, sizeof nm, "llm.layer%d.down", l);
     BM_TRY(lin_fwd(c, m.S, m.f, m.d, sl.h[j], m.f, P_(c, nm), LD_(c, nm), sl.x[j + 1], BM_EPI_ADD, sl.x[j]));
   }
-  c.last_src = sl.x[c.lps];
+  c.last_src = sl.x[nl];
   c.last_src_ring = -1;
   if (s == c.P * c.V - 1) {
     // last stage: final norm, LM head + CE (fwd and bwd through the head), generator inputs
     const int n_mod = c.n_mod[mb], n_text = m.S - n_mod;
-    BM_TRY(norm_fwd(c, m.S, m.d, sl.x[c.lps], P_(c, "llm.final_norm"), sl.Hn, sl.rstd_f));
+    BM_TRY(norm_fwd(c, m.S, m.d, sl.x[nl], P_(c, "llm.final_norm"), sl.Hn, sl.rstd_f));
     // Hn is final: the generator (own shard on the generator stream, remote shards
     // through their genin sends) starts now, overlapping the LM head and CE below
     if (c.hn_ev) BM_CUDA_TRY(cudaEventRecord(c.hn_ev, c.st));
@@ -826,7 +868,7 @@ static bm_status op_llm_fwd(bm_ctx& c, const bm_op& o, const RecvState& rs) {
     if (n_text > 0 && !c.head_dp) {
       const char* hn_text = sl.Hn + (int64_t)n_mod * d * es;
       BM_TRY(lin_fwd(c, n_text, m.d, m.vocab, hn_text, m.d, P_(c, "llm.head"), LD_(c, "llm.head"), c.logits));
-      const float sg = 1.f / ((float)n_text * c.M);
+      const float sg = c.gscale / (float)n_text;
       BM_TRY(TY(c, ce_fwd_bwd<bf16>(n_text, m.vocab, (bf16*)c.logits, c.labels + (int64_t)mb * S + n_mod, sg, c.loss + mb, 1.f, 0, c.ce_scr, c.st),
                 ce_fwd_bwd<float>(n_text, m.vocab, (float*)c.logits, c.labels + (int64_t)mb * S + n_mod, sg, c.loss + mb, 1.f, 0, c.ce_scr, c.st)));
       BM_TRY(lin_dgrad(c, n_text, m.d, m.vocab, c.logits, P_(c, "llm.head"), LD_(c, "llm.head"),
@@ -893,7 +935,7 @@ static bm_status op_llm_bwd(bm_ctx& c, const bm_op& o, const RecvState& rs) {
       c.gout_pending[og->second] = true;
       c.own_gout.erase(og);
     }
-    BM_TRY(norm_bwd(c, m.S, m.d, sl.dHn, sl.x[c.lps], P_(c, "llm.final_norm"), sl.rstd_f, nullptr, c.dwork[0],
+    BM_TRY(norm_bwd(c, m.S, m.d, sl.dHn, sl.x[sl.nl], P_(c, "llm.final_norm"), sl.rstd_f, nullptr, c.dwork[0],
                     G_(c, "llm.final_norm")));
     cur = c.dwork[0];
   } else if ((s + 1) % c.P == c.rank) {
@@ -909,8 +951,10 @@ static bm_status op_llm_bwd(bm_ctx& c, const bm_op& o, const RecvState& rs) {
     c.bout_pending[b] = false;
   }
   char nm[64];
-  for (int j = c.lps - 1; j >= 0; --j) {
-    const int l = s * c.lps + j;
+  int l0, nl;
+  stage_layers(m, c.P * c.V, s, &l0, &nl);
+  for (int j = nl - 1; j >= 0; --j) {
+    const int l = l0 + j;
     char* out = (j == 0) ? c.bout[b] : (cur == c.dwork[0] ? c.dwork[1] : c.dwork[0]);
     snprintf(nm, sizeof nm, "llm.layer%d.down", l);
     BM_TRY(lin_wgrad(c, m.S, m.f, m.d, cur, sl.h[j], m.f, G_(c, nm), LD_(c, nm)));
@@ -962,7 +1006,7 @@ static bm_status op_gen_fwd(bm_ctx& c, const bm_op& o, const RecvState& rs) {
     const char* Xh = own ? c.headin_src[c.rank] : slot;
     const int n_text = m.S - c.n_mod[mb];
     BM_TRY(lin_fwd(c, nh, m.d, m.vocab, Xh, m.d, P_(c, "llm.head"), LD_(c, "llm.head"), c.logits));
-    const float sg = 1.f / ((float)n_text * c.M);
+    const float sg = c.gscale / (float)n_text;
     const float sl_ = (float)nh / (float)n_text;
     BM_TRY(TY(c, ce_fwd_bwd<bf16>(nh, m.vocab, (bf16*)c.logits, c.labels + (int64_t)mb * m.S + hlo, sg, c.loss + mb, sl_, 1, c.ce_scr, c.st),
               ce_fwd_bwd<float>(nh, m.vocab, (float*)c.logits, c.labels + (int64_t)mb * m.S + hlo, sg, c.loss + mb, sl_, 1, c.ce_scr, c.st)));
@@ -980,8 +1024,8 @@ static bm_status op_gen_fwd(bm_ctx& c, const bm_op& o, const RecvState& rs) {
   BM_TRY(lin_fwd(c, n, m.d_g, m.d_t, sl.E[m.L_g], m.d_g, P_(c, "gen.out"), LD_(c, "gen.out"), sl.out));
   const char* t = c.mb_targets[mb] + (int64_t)lo * m.d_t * c.es;
   const float denom = (float)c.n_gen[mb] * m.d_t;
-  BM_TRY(TY(c, mse_fwd_bwd<bf16>(n, m.d_t, (const bf16*)sl.out, (const bf16*)t, denom, 1.f / c.M, 1.f, c.loss + c.M + mb, (bf16*)sl.dout, c.st),
-            mse_fwd_bwd<float>(n, m.d_t, (const float*)sl.out, (const float*)t, denom, 1.f / c.M, 1.f, c.loss + c.M + mb, (float*)sl.dout, c.st)));
+  BM_TRY(TY(c, mse_fwd_bwd<bf16>(n, m.d_t, (const bf16*)sl.out, (const bf16*)t, denom, c.gscale, 1.f, c.loss + c.M + mb, (bf16*)sl.dout, c.st),
+            mse_fwd_bwd<float>(n, m.d_t, (const float*)sl.out, (const float*)t, denom, c.gscale, 1.f, c.loss + c.M + mb, (float*)sl.dout, c.st)));
   return BM_OK;
 }
 
@@ -1177,8 +1221,9 @@ bm_status bm_ctx_create(const bm_model_cfg* mc, const bm_schedule* s, int32_t ra
   c->rank = rank;
   c->P = s->cfg.stages;
   c->M = s->cfg.microbatches;
+  c->gscale = 1.f / (float)c->M;
   c->V = s->cfg.vchunks;
-  c->lps = mc->L / (c->P * c->V);
+  c->lps = max_stage_layers(*mc, c->P, c->V, rank);
   c->dtype = mc->dtype;
   c->es = mc->dtype == BM_BF16 ? 2 : 4;
   c->params = param_layout(*mc, s->cfg, rank, &c->total_elems, &c->dp_elems);
@@ -1339,6 +1384,27 @@ bm_status bm_ctx_init_nccl(bm_ctx* c, const uint8_t id[128], int32_t nranks, int
   return BM_OK;
 }
 
+bm_status bm_ctx_init_replicas(bm_ctx* c, int32_t D, int32_t replica, const uint8_t id_world[128],
+                               const uint8_t id_stage[128]) {
+  BM_CHECK_ARG(c && id_world && id_stage, "null argument");
+  BM_CHECK_ARG(D >= 1 && replica >= 0 && replica < D, "replica out of range");
+  BM_CHECK_ARG(!c->nc_world && !c->nc_stage, "replicas already initialised");
+  if (!nccl().ok) {
+    set_error("libnccl.so.2 not loadable");
+    return BM_E_NCCL;
+  }
+  c->D = D;
+  c->replica = replica;
+  c->gscale = 1.f / ((float)c->M * (float)D);
+  if (D == 1) return BM_OK;
+  ncclUniqueId u;
+  std::memcpy(&u, id_world, 128);
+  BM_NCCL_TRY(nccl().CommInitRank(&c->nc_world, c->P * D, u, replica * c->P + c->rank));
+  std::memcpy(&u, id_stage, 128);
+  BM_NCCL_TRY(nccl().CommInitRank(&c->nc_stage, D, u, replica));
+  return BM_OK;
+}
+
 bm_status bm_step(bm_ctx* c, const bm_batch* b, void* stream) {
   BM_CHECK_ARG(c && b, "null argument");
   if (!c->bound) {
@@ -1353,6 +1419,10 @@ bm_status bm_step(bm_ctx* c, const bm_batch* b, void* stream) {
     }
   if (c->P > 1 && !c->nc) {
     set_error("NCCL not initialised (bm_ctx_init_nccl) for P > 1");
+    return BM_E_STATE;
+  }
+  if (c->D > 1 && (!c->nc_world || !c->nc_stage)) {
+    set_error("replica communicators not initialised (bm_ctx_init_replicas)");
     return BM_E_STATE;
   }
   bm_ctx& x = *c;
@@ -1541,13 +1611,22 @@ bm_status bm_step(bm_ctx* c, const bm_batch* b, void* stream) {
   // finalize: DP gradient sum + loss terms
   cudaEvent_t tr_tail = x.tracing ? trace_mark(x, x.st) : nullptr;
   static const bool no_allreduce = getenv("BM_DEBUG_NO_ALLREDUCE") != nullptr;   // hang triage only
-  if (x.P > 1 && !no_allreduce) {
+  if (!no_allreduce && (x.P > 1 || x.D > 1)) {
+    // DP parameters over every process (the replica's pipeline group when D = 1),
+    // this stage's LLM parameters over its D replicas, loss terms over the pipeline
     BM_NCCL_TRY(nccl().GroupStart());
-    BM_NCCL_TRY(nccl().AllReduce(x.G, x.G, (size_t)x.dp_elems, ncclFloat32, ncclSum, x.nc, x.st));
-    BM_NCCL_TRY(nccl().AllReduce(x.loss, x.loss, (size_t)(2 * x.M), ncclFloat32, ncclSum, x.nc, x.st));
+    ncclComm_t dp_comm = x.D > 1 ? x.nc_world : x.nc;
+    BM_NCCL_TRY(nccl().AllReduce(x.G, x.G, (size_t)x.dp_elems, ncclFloat32, ncclSum, dp_comm, x.st));
+    if (x.D > 1 && x.total_elems > x.dp_elems)
+      BM_NCCL_TRY(nccl().AllReduce(x.G + x.dp_elems, x.G + x.dp_elems, (size_t)(x.total_elems - x.dp_elems), ncclFloat32,
+                                   ncclSum, x.nc_stage, x.st));
+    if (x.P > 1) BM_NCCL_TRY(nccl().AllReduce(x.loss, x.loss, (size_t)(2 * x.M), ncclFloat32, ncclSum, x.nc, x.st));
     BM_NCCL_TRY(nccl().GroupEnd());
   }
-  BM_TRY(loss_finalize(x.M, x.loss, x.st));
+  // L = (1/M) sum of the replica's terms; with replicas, the mean of the D replica losses
+  BM_TRY(loss_finalize(x.M, x.loss, 1.f / ((float)x.M * (float)x.D), x.st));
+  if (x.D > 1 && !no_allreduce)
+    BM_NCCL_TRY(nccl().AllReduce(x.loss + 2 * x.M, x.loss + 2 * x.M, 1, ncclFloat32, ncclSum, x.nc_stage, x.st));
   if (x.tracing) {
     x.trace_last = trace_mark(x, x.st);
     x.trace.push_back({-1, -1, 0, -1, tr_tail, x.trace_last});

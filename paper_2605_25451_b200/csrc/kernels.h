@@ -47,6 +47,7 @@ bm_status copy_bytes(void* dst, const void* src, int64_t bytes, int max_ctas, cu
 bm_status zero_bytes(void* dst, int64_t bytes, cudaStream_t st);
 // one-thread kernel polling *flag until (int32)(*flag - v) >= 0 (BM_WAIT=spin)
 bm_status spin_wait(const uint32_t* flag, uint32_t v, cudaStream_t st);
-bm_status loss_finalize(int M, float* loss, cudaStream_t st);
+// loss[2M] = scale * sum(loss[0 .. 2M))
+bm_status loss_finalize(int M, float* loss, float scale, cudaStream_t st);
 
 }  // namespace bm

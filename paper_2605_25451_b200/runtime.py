@@ -23,7 +23,7 @@ from . import schedule as BS
 
 
 def model_cfg(shape, dtype: str, max_n_mod: int | None = None, max_n_gen: int | None = None,
-              head_place: str = "auto") -> L.ModelCfg:
+              head_place: str = "auto", last_stage_layers: int = 0) -> L.ModelCfg:
     mc = L.ModelCfg()
     mc.S, mc.d_in, mc.d_e, mc.f_e, mc.L_e = shape.S, shape.d_in, shape.d_e, shape.f_e, shape.L_e
     mc.d, mc.f, mc.L, mc.vocab = shape.d, shape.f, shape.L, shape.vocab
@@ -32,7 +32,30 @@ def model_cfg(shape, dtype: str, max_n_mod: int | None = None, max_n_gen: int | 
     mc.max_n_mod = max_n_mod if max_n_mod is not None else min(shape.n_mod_law[2], shape.S)
     mc.max_n_gen = max_n_gen if max_n_gen is not None else min(shape.n_gen_law[2], shape.S)
     mc.head_place = L.HEAD_PLACE[head_place]
+    mc.last_stage_layers = last_stage_layers
     return mc
+
+
+def exchange(group, P: int, D: int, global_rank: int, payload, new_id):
+    """Host side of the process-group plumbing for D pipeline replicas of P stages
+    (process rank = replica * P + stage).  One all_gather; returns
+    (payloads of the P stages of this process's replica, in stage order,
+     {"pipe": id of this replica's pipeline group (P > 1),
+      "world": id of the all-process group (D > 1),
+      "stage": id of this stage's replica group (D > 1)}).
+    Ids are made by one member of each group (new_id() -> bytes): the pipeline's
+    stage 0, process 0, and replica 0's process of the stage."""
+    import torch.distributed as dist
+    replica, stage = divmod(global_rank, P)
+    mine = {"pipe": new_id() if (stage == 0 and P > 1) else None,
+            "world": new_id() if (global_rank == 0 and D > 1) else None,
+            "stage": new_id() if (replica == 0 and D > 1) else None}
+    allp = [None] * (P * D)
+    dist.all_gather_object(allp, (payload, mine), group=group)
+    base = replica * P
+    peers = [allp[base + q][0] for q in range(P)]
+    ids = {"pipe": allp[base][1]["pipe"], "world": allp[0][1]["world"], "stage": allp[stage][1]["stage"]}
+    return peers, ids
 
 
 def _round8(x):
@@ -48,18 +71,23 @@ class DeviceBatch:
 
 class Runtime:
     def __init__(self, shape, dtype="bf16", rank=0, world=1, group=None, device=None, sched_kw=None,
-                 head_place="auto"):
+                 head_place="auto", last_stage_layers=0):
         self.shape = shape
         self.dtype = dtype
-        self.rank, self.world = rank, world
+        self.world = world
         self.P, self.M, self.V = shape.P, shape.M, shape.V
-        if world != self.P:
-            raise ValueError(f"one rank per pipeline stage: world={world} != P={self.P}")
+        if world % self.P:
+            raise ValueError(f"world={world} is not a multiple of P={self.P} (D pipeline replicas of P stages)")
+        # D pipeline replicas of P stages; process rank = replica * P + stage
+        self.D = world // self.P
+        self.global_rank = rank
+        self.replica, self.rank = divmod(rank, self.P)
+        rank = self.rank
         self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else device
         self._stream = None   # own compute stream (created on first step)
         kw = dict(sched_kw or {})
         self.sched = BS.build(self.P, self.M, self.V, **kw)
-        self.mc = model_cfg(shape, dtype, head_place=head_place)
+        self.mc = model_cfg(shape, dtype, head_place=head_place, last_stage_layers=last_stage_layers)
         h = C.c_void_p()
         L.call("bm_ctx_create", C.byref(self.mc), self.sched.handle, rank, C.byref(h))
         self.ctx = h.value
@@ -100,23 +128,27 @@ class Runtime:
 
     # ------------------------------------------------------------------ peers
     def _connect(self, group):
+        """Peer memory inside this replica's pipeline (CUDA IPC), the pipeline's NCCL
+        group, and with D > 1 the all-process and per-stage NCCL groups."""
         import torch.distributed as dist
+        P, D = self.P, self.D
         hb = (C.c_uint8 * 64)()
         off = C.c_int64()
         L.call("bm_ipc_export", self.comm_ptr, hb, C.byref(off))
-        mine = (bytes(hb), off.value)
-        allh = [None] * self.world
-        dist.all_gather_object(allh, mine, group=group)
-        for r, (hbytes, o) in enumerate(allh):
-            if r == self.rank:
-                continue
-            L.call("bm_ctx_open_peer", self.ctx, r, (C.c_uint8 * 64).from_buffer_copy(hbytes), o)
-        nid = (C.c_uint8 * 128)()
-        if self.rank == 0:
+
+        def new_id():
+            nid = (C.c_uint8 * 128)()
             L.call("bm_nccl_unique_id", nid)
-        obj = [bytes(nid)]
-        dist.broadcast_object_list(obj, src=0, group=group)
-        L.call("bm_ctx_init_nccl", self.ctx, (C.c_uint8 * 128).from_buffer_copy(obj[0]), self.world, self.rank)
+            return bytes(nid)
+        peers, ids = exchange(group, P, D, self.global_rank, (bytes(hb), off.value), new_id)
+        for q, (hbytes, o) in enumerate(peers):
+            if q != self.rank:
+                L.call("bm_ctx_open_peer", self.ctx, q, (C.c_uint8 * 64).from_buffer_copy(hbytes), o)
+        as_c = lambda b: (C.c_uint8 * 128).from_buffer_copy(b)  # noqa: E731
+        if P > 1:
+            L.call("bm_ctx_init_nccl", self.ctx, as_c(ids["pipe"]), P, self.rank)
+        if D > 1:
+            L.call("bm_ctx_init_replicas", self.ctx, D, self.replica, as_c(ids["world"]), as_c(ids["stage"]))
         dist.barrier(group=group)
 
     # ------------------------------------------------------------------ weights / grads

@@ -30,6 +30,7 @@ def main():
     ap.add_argument("--strategy", default="bigmac")
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--head", default="auto", choices=["auto", "last_stage", "dp_shard"])
+    ap.add_argument("--last-stage-layers", type=int, default=0)
     ap.add_argument("--out", default="gpurun_out/trace.json")
     a = ap.parse_args()
     rank, world = int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
@@ -43,7 +44,8 @@ def main():
     cfg = get_config(a.config, P=world, M=a.M, V=a.V)
     kw = {"bigmac": {}, "compute_efficient": {"warmup_units": cfg.M // world},
           "memory_efficient": {"enc_place": "entry_stage", "gen_place": "last_stage"}}[a.strategy]
-    rt = Runtime(cfg, "bf16", rank=rank, world=world, group=group, sched_kw=kw, head_place=a.head)
+    rt = Runtime(cfg, "bf16", rank=rank, world=world, group=group, sched_kw=kw, head_place=a.head,
+                 last_stage_layers=a.last_stage_layers)
     rt.init_random_weights(1)
     db = rt.device_batch(make_batch(cfg))
     for _ in range(a.warmup):

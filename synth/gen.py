@@ -131,3 +131,9 @@ def make_batch(cfg: ModelShape, seed: int | None = None, M: int | None = None) -
         labels[m] = rng.integers(0, cfg.vocab, size=cfg.S)
         targets.append(bf16_round(rng.standard_normal((int(n_gen[m]), cfg.d_t), dtype=np.float32)))
     return Batch(n_mod=n_mod, n_gen=n_gen, patches=patches, ids=ids, labels=labels, targets=targets)
+
+
+def slice_batch(b: Batch, lo: int, hi: int) -> Batch:
+    """Microbatches [lo, hi) of a batch (one pipeline replica's share of a global batch)."""
+    return Batch(n_mod=b.n_mod[lo:hi].copy(), n_gen=b.n_gen[lo:hi].copy(), patches=list(b.patches[lo:hi]),
+                 ids=b.ids[lo:hi].copy(), labels=b.labels[lo:hi].copy(), targets=list(b.targets[lo:hi]))

@@ -115,6 +115,24 @@ def test_step_single_gpu_head_dp_shard(oracle_cache, cfg_name, dtype):
     rt.close()
 
 
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_step_single_gpu_uneven_partition(oracle_cache, dtype):
+    """last_stage_layers = 1 at P = 1, V = 2: virtual stages hold layers (3, 1)."""
+    from paper_2605_25451_b200.runtime import Runtime
+    cfg = get_config("C1", P=1, M=4, V=2)
+    W, B, (loss_ref, per_ref, G_ref) = reference(oracle_cache, cfg)
+    rt = Runtime(cfg, dtype, last_stage_layers=1)
+    rt.load_weights(W)
+    rt.step(rt.device_batch(B))
+    torch.cuda.synchronize()
+    loss, _, _ = rt.losses()
+    tol = TOL[dtype]
+    assert abs(loss - loss_ref) <= tol * abs(loss_ref)
+    bad = {n: rel(rt.grad(n), G_ref[n]) for n in rt.names()}
+    assert not {k: v for k, v in bad.items() if v > tol}, bad
+    rt.close()
+
+
 def test_trace_records_every_op():
     """bm_ctx_trace_get: one record per compute op / receive (+ the tail), in the
     rank's op order on each stream, with non-decreasing times; tracing does not
@@ -177,6 +195,7 @@ def _torchrun(nproc, *args, timeout=600):
 @pytest.mark.parametrize("P,M,V,dtype,gen", [(2, 4, 1, "f32", "dp_shard"), (2, 4, 1, "bf16", "dp_shard"),
                                            (2, 8, 2, "f32", "dp_shard"), (2, 4, 1, "f32", "last_stage"),
                                            (2, 4, 1, "f32", "dp_shard+head_dp"), (2, 8, 2, "bf16", "dp_shard+head_dp"),
+                                           (2, 4, 1, "f32", "dp_shard+last1"), (2, 4, 1, "bf16", "dp_shard+last3"),
                                            (2, 4, 1, "f32", "entry_stage+last_stage"),
                                            (2, 4, 1, "bf16", "ce")])
 def test_step_two_gpus(P, M, V, dtype, gen):
@@ -204,4 +223,21 @@ def test_step_four_gpus(P, M, V, dtype, gen):
     if torch.cuda.device_count() < P:
         pytest.skip(f"needs {P} GPUs")
     out = _torchrun(P, "C1", P, M, V, dtype, gen, timeout=240)
+    assert "PARITY OK" in out, out
+
+
+@pytest.mark.parametrize("P,D,M,V,dtype", [(1, 2, 4, 1, "f32"), (1, 2, 4, 1, "bf16")])
+def test_step_replicas_two_gpus(P, D, M, V, dtype):
+    # D pipeline replicas: DP params over all processes, LLM params per stage
+    if torch.cuda.device_count() < P * D:
+        pytest.skip(f"needs {P * D} GPUs")
+    out = _torchrun(P * D, "C1", P, M, V, dtype, "dp_shard", D)
+    assert "PARITY OK" in out, out
+
+
+@pytest.mark.parametrize("P,D,M,V,dtype", [(2, 2, 4, 1, "f32"), (2, 2, 4, 1, "bf16"), (2, 2, 8, 2, "f32")])
+def test_step_replicas_four_gpus(P, D, M, V, dtype):
+    if torch.cuda.device_count() < P * D:
+        pytest.skip(f"needs {P * D} GPUs")
+    out = _torchrun(P * D, "C1", P, M, V, dtype, "dp_shard", D, timeout=300)
     assert "PARITY OK" in out, out

@@ -42,15 +42,30 @@ def test_library_is_sm100a():
     assert "LDTM" in sass             # tcgen05.ld (TMEM -> registers)
 
 
-@pytest.mark.parametrize("head", ["auto", "last_stage", "dp_shard"])
+def expected_layers(L, P, V, last, s):
+    """bigmac.h "LLM layer partition": layers of virtual stage s."""
+    PV = P * V
+    if last == 0 or PV == 1:
+        n = L // PV
+        return list(range(s * n, (s + 1) * n))
+    if s == PV - 1:
+        return list(range(L - last, L))
+    counts = [(L - last) // (PV - 1) + (1 if i < (L - last) % (PV - 1) else 0) for i in range(PV - 1)]
+    start = sum(counts[:s])
+    return list(range(start, start + counts[s]))
+
+
+@pytest.mark.parametrize("head,last", [("auto", 0), ("last_stage", 0), ("dp_shard", 0), ("auto", 1), ("auto", 2)])
 @pytest.mark.parametrize("P,V,rank", [(1, 1, 0), (2, 1, 0), (2, 1, 1), (4, 1, 3), (2, 2, 0), (2, 2, 1), (1, 4, 0)])
-def test_param_layout_matches_model(P, V, rank, head):
+def test_param_layout_matches_model(P, V, rank, head, last):
     from synth import get_config, param_specs
     from paper_2605_25451_b200 import _lib as L
     from paper_2605_25451_b200 import schedule as BS
     from paper_2605_25451_b200.runtime import model_cfg
     cfg = get_config("C1", P=P, M=2 * P, V=V)
-    mc = model_cfg(cfg, "bf16", head_place=head)
+    if last and cfg.L - last < P * V - 1:
+        pytest.skip("partition needs a layer per virtual stage")
+    mc = model_cfg(cfg, "bf16", head_place=head, last_stage_layers=last)
     sc = BS.make_cfg(P, 2 * P, V)
     head_dp = head == "dp_shard"   # bigmac.h bm_head_place (auto = last stage)
     n, tot, dp = C.c_int32(), C.c_int64(), C.c_int64()
@@ -68,8 +83,7 @@ def test_param_layout_matches_model(P, V, rank, head):
         assert pi.offset >= prev_end and pi.offset % 64 == 0 and pi.ld >= cols and pi.ld % (1 if cols == 1 else 8) == 0
         prev_end = pi.offset + rows * pi.ld
         got[nm] = pi.kind
-    lps = cfg.L // (P * V)
-    my_layers = {l for c in range(V) for l in range((c * P + rank) * lps, (c * P + rank + 1) * lps)}
+    my_layers = {l for c in range(V) for l in expected_layers(cfg.L, P, V, last, c * P + rank)}
     for nm in specs:
         if nm.startswith(("enc.", "gen.")):
             assert got.get(nm) == 0, nm            # DP params on every rank
@@ -83,3 +97,28 @@ def test_param_layout_matches_model(P, V, rank, head):
             l = int(nm.split(".")[1][5:])
             assert (nm in got) == (l in my_layers), nm
     assert prev_end <= tot.value and dp.value <= tot.value
+
+
+def test_layer_partition_examples_and_errors():
+    # (5, 4, 4, 3) at L = 16, P = 4 and (3, 2, 2, 2, 2, 2, 2, 1) at P = 8
+    assert [len(expected_layers(16, 4, 1, 3, s)) for s in range(4)] == [5, 4, 4, 3]
+    assert [len(expected_layers(16, 8, 1, 1, s)) for s in range(8)] == [3, 2, 2, 2, 2, 2, 2, 1]
+    from synth import get_config
+    from paper_2605_25451_b200 import _lib as L
+    from paper_2605_25451_b200 import schedule as BS
+    from paper_2605_25451_b200.runtime import model_cfg
+    cfg = get_config("C1", P=2, M=4, V=1)
+    n, tot, dp = C.c_int32(), C.c_int64(), C.c_int64()
+    for bad in (cfg.L, -1):
+        mc = model_cfg(cfg, "bf16", last_stage_layers=bad)
+        with pytest.raises(L.BigMacError):
+            L.call("bm_param_count", C.byref(mc), C.byref(BS.make_cfg(2, 4, 1)), 0, C.byref(n), C.byref(tot), C.byref(dp))
+    mc = model_cfg(cfg.replace(L=5), "bf16")       # L % (P V) != 0 needs an explicit partition
+    with pytest.raises(L.BigMacError):
+        L.call("bm_param_count", C.byref(mc), C.byref(BS.make_cfg(2, 4, 1)), 0, C.byref(n), C.byref(tot), C.byref(dp))
+    mc = model_cfg(cfg.replace(L=5), "bf16", last_stage_layers=2)
+    L.call("bm_param_count", C.byref(mc), C.byref(BS.make_cfg(2, 4, 1)), 0, C.byref(n), C.byref(tot), C.byref(dp))
+    mc = model_cfg(cfg, "bf16", head_place="dp_shard")
+    with pytest.raises(L.BigMacError):       # the DP-sharded head rides on DP-sharded generator ops
+        L.call("bm_param_count", C.byref(mc), C.byref(BS.make_cfg(2, 4, 1, gen_place="last_stage")), 0,
+               C.byref(n), C.byref(tot), C.byref(dp))

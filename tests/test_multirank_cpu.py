@@ -71,3 +71,53 @@ def test_multirank_host_logic(world):
     for p in procs:
         p.join(timeout=60)
     assert all(ok for _, ok, _ in res), res
+
+
+def _replica_worker(rank, world, P, port, q):
+    try:
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        from paper_2605_25451_b200.runtime import exchange
+        cnt = [0]
+
+        def new_id():
+            cnt[0] += 1
+            return f"id-{rank}-{cnt[0]}".encode()
+        peers, ids = exchange(None, P, world // P, rank, f"ipc-{rank}", new_id)
+        got = [None] * world
+        dist.all_gather_object(got, (peers, ids))
+        dist.barrier()
+        dist.destroy_process_group()
+        q.put((rank, got, ""))
+    except Exception as e:  # pragma: no cover
+        q.put((rank, None, repr(e)))
+
+
+@pytest.mark.parametrize("world,P", [(4, 2), (2, 1), (4, 4), (8, 4)])
+def test_replica_exchange_groups(world, P):
+    """D = world / P pipeline replicas: IPC peers are the process's own replica
+    (stage order), every process of a replica shares one pipeline id, every
+    process the world id, and the D processes of a stage one stage id -- each id
+    distinct per group."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_replica_worker, args=(r, world, P, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+    assert all(g is not None for _, g, _ in res), res
+    got = res[0][1]
+    D = world // P
+    for r, (peers, ids) in enumerate(got):
+        rep, st = divmod(r, P)
+        assert peers == [f"ipc-{rep * P + s}" for s in range(P)]
+        assert ids["pipe"] == (got[rep * P][1]["pipe"] if P > 1 else None)
+        assert ids["world"] == (b"id-0-" + (b"2" if P > 1 else b"1") if D > 1 else None)
+        assert ids["stage"] == (got[st][1]["stage"] if D > 1 else None)
+    if P > 1:
+        assert len({got[k * P][1]["pipe"] for k in range(D)}) == D
+    if D > 1:
+        assert len({got[s][1]["stage"] for s in range(P)}) == P
