@@ -152,7 +152,8 @@ def workload(args, N):
     """(per-replica config, P, D)."""
     from synth import get_config
     P = stages_of(args, N)
-    cfg = get_config(args.config, P=P, M=args.microbatches or get_config(args.config).M * P, V=1)
+    base = get_config(args.config)
+    cfg = get_config(args.config, P=P, M=args.microbatches or base.M * P, V=base.V)
     return cfg, P, N // P
 
 
@@ -160,6 +161,21 @@ def workload(args, N):
 # measured at C2 (profiles/r01/traces/trace_n2_m32_last_stage.summary.json: the last
 # stage's F(m) takes 4.27 ms vs 2.55 ms elsewhere for 8 layers whose F+B is 8.2 ms)
 HEAD_LAYERS = 1.7
+
+
+# explicit partitions measured best at C2 (L = 16): stage 0 also runs the text
+# embedding and is slowed by the generator shards it serves, so the extra layer
+# goes to a middle stage (profiles/r01/traces/trace_n4_m64_bigmac.summary.json)
+DEFAULT_SPLIT = {("C2", 4): [4, 4, 5, 3]}
+
+
+def stage_split(args, cfg, P):
+    """Explicit stage_layers (bigmac.h) or None."""
+    if args.stage_layers:
+        return [int(x) for x in args.stage_layers.split(",")]
+    if args.last_stage_layers >= 0:
+        return None
+    return DEFAULT_SPLIT.get((cfg.name, P * cfg.V))
 
 
 def last_stage_layers(args, cfg, P):
@@ -185,11 +201,17 @@ def global_batch(cfg, D):
     return make_batch(cfg, M=cfg.M * D)
 
 
+SHAPES = {"C2": ("ViT-S", "1B", "small"), "C3": ("ViT-S", "1B", "small"), "C4": ("ViT-L", "7B", "diffusion-head")}
+
+
 def config_dict(cfg, P, D):
     rep_txt = f" x {D} pipeline replicas" if D > 1 else ""
-    return {"workload": f"{cfg.name}: ViT-S-shaped encoder (d_e={cfg.d_e}, L_e={cfg.L_e}) + 1B-shaped LLM "
-                        f"(d={cfg.d}, f={cfg.f}, L={cfg.L}, vocab={cfg.vocab}) + generator (d_g={cfg.d_g}, L_g={cfg.L_g}); "
-                        f"nested pipeline P={P} stages{rep_txt}, M={cfg.M} microbatches per replica, 1F1B",
+    enc, llm, gen = SHAPES.get(cfg.name, ("synthetic", "synthetic", "synthetic"))
+    sched = "1F1B" if cfg.V == 1 else f"interleaved 1F1B ({cfg.V} chunks/stage)"
+    return {"workload": f"{cfg.name}: {enc}-shaped encoder (d_e={cfg.d_e}, L_e={cfg.L_e}) + {llm}-shaped LLM "
+                        f"(d={cfg.d}, f={cfg.f}, L={cfg.L}, vocab={cfg.vocab}) + {gen}-shaped generator (d_g={cfg.d_g}, "
+                        f"L_g={cfg.L_g}); nested pipeline P={P} stages{rep_txt}, M={cfg.M} microbatches per replica, "
+                        f"{sched}",
             "global_batch": cfg.M * D, "seq_len": cfg.S, "parallelism": f"pp{P}" + (f"xdp{D}" if D > 1 else ""),
             "stages": P, "replicas": D, "microbatches": cfg.M, "vchunks": cfg.V,
             "n_mod_law": list(cfg.n_mod_law), "n_gen_law": list(cfg.n_gen_law),
@@ -245,6 +267,7 @@ def main():
     ap.add_argument("--microbatches", type=int, default=0, help="per-replica M (default 16 P)")
     ap.add_argument("--last-stage-layers", type=int, default=-1,
                     help="LLM layers of the last stage (bigmac.h); -1 = balance the LM head (HEAD_LAYERS), 0 = uniform")
+    ap.add_argument("--stage-layers", default="", help="explicit LLM layers per stage, e.g. 4,5,4,3 (bigmac.h)")
     ap.add_argument("--stages", type=int, default=0, help="pipeline stages P (default min(N, 4)); D = N / P replicas")
     ap.add_argument("--dtype", default="bf16")
     ap.add_argument("--no-e2e", action="store_true")
@@ -281,9 +304,10 @@ def main():
         raise SystemExit("--warmup must be >= 3")
     sched_kw = {"bigmac": {}, "compute_efficient": {"warmup_units": cfg.M // P},
                 "memory_efficient": {"enc_place": "entry_stage", "gen_place": "last_stage"}}[args.strategy]
-    n_last = last_stage_layers(args, cfg, P)
+    split = stage_split(args, cfg, P)
+    n_last = 0 if split else last_stage_layers(args, cfg, P)
     rt = Runtime(cfg, args.dtype, rank=rank, world=world, group=group, sched_kw=sched_kw, head_place=args.head,
-                 last_stage_layers=n_last)
+                 last_stage_layers=n_last, stage_layers=split)
     rt.init_random_weights(seed=1)
     gbatch = global_batch(cfg, D)
     replica = rank // P
@@ -413,7 +437,7 @@ def main():
                 "avg_launch_ms": gemm_ms_all / max(n_gemm_all, 1)}
     t_roof_ms = F / (N * peaks["bf16_tflops"] * 1e12) * 1e3
     step_roof = {"flops_per_step": F, "t_roof_ms": t_roof_ms, "frac": t_roof_ms / ms_per_step,
-                 "peak_tflops": peaks["bf16_tflops"], "bubble_bound": (P - 1) / (cfg.M + P - 1)}
+                 "peak_tflops": peaks["bf16_tflops"], "bubble_bound": (P - 1) / (cfg.M * cfg.V + P - 1)}
 
     cpu = None
     if not args.no_cpu and N == 1:
@@ -429,7 +453,7 @@ def main():
             "scaling": "strong" if args.microbatches else "weak",
             "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
             "config": dict(config_dict(cfg, P, D), strategy=args.strategy, head_place=head_place_name(args, N),
-                           last_stage_layers=n_last),
+                           last_stage_layers=n_last, stage_layers=split),
             "roofline": roofline, "step_roofline": step_roof,
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches_all, "clocks": clocks,
             "nvlink": ({"bytes_per_step_all_ranks": comm_bytes_all / n_inst,

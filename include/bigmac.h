@@ -134,6 +134,7 @@ const char* bm_last_error(void);
 /* LLM (pipeline stages), generator (DP row shards).                        */
 /* ------------------------------------------------------------------------ */
 typedef enum { BM_BF16 = 0, BM_F32 = 1 } bm_dtype;
+#define BM_MAX_VSTAGES 32   /* P * V bound of an explicit layer partition */
 
 typedef struct {
   int32_t S;                      /* LLM sequence length                      */
@@ -145,11 +146,14 @@ typedef struct {
   int32_t head_place;             /* bm_head_place                             */
   int32_t last_stage_layers;      /* LLM layers of the last virtual stage; 0 = uniform (below) */
   int32_t reserved[6];            /* must be zero                              */
+  int32_t stage_layers[BM_MAX_VSTAGES]; /* explicit partition (below); all 0 = unset */
 } bm_model_cfg;
 
 /* LLM layer partition over the P V virtual stages (s = chunk P + rank), in
- * layer order.  last_stage_layers = 0: L / (P V) layers each (L % (P V) == 0
- * required).  last_stage_layers = n > 0: virtual stage P V - 1 (which also
+ * layer order.  stage_layers[0] != 0: virtual stage s holds stage_layers[s]
+ * layers (P V <= BM_MAX_VSTAGES, every entry >= 1, sum = L; last_stage_layers
+ * ignored).  Otherwise, last_stage_layers = 0: L / (P V) layers each
+ * (L % (P V) == 0 required).  last_stage_layers = n > 0: virtual stage P V - 1 (which also
  * runs the LM head + CE under BM_HEAD_LAST_STAGE) gets n layers; the other
  * P V - 1 stages split the remaining L - n as evenly as possible, the first
  * (L - n) mod (P V - 1) stages one layer more.  Requires 1 <= n and

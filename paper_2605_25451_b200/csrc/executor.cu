@@ -113,7 +113,17 @@ static bm_status check_model(const bm_model_cfg& mc, const bm_sched_cfg& sc) {
   BM_CHECK_ARG(mc.d_in > 0 && mc.d_e > 0 && mc.f_e > 0 && mc.L_e >= 0, "bad encoder dims");
   BM_CHECK_ARG(mc.d_g > 0 && mc.f_g > 0 && mc.L_g >= 0 && mc.d_t > 0, "bad generator dims");
   BM_CHECK_ARG(mc.dtype == BM_BF16 || mc.dtype == BM_F32, "dtype must be bf16 or fp32");
-  if (mc.last_stage_layers == 0)
+  const int PV = sc.stages * sc.vchunks;
+  if (mc.stage_layers[0] != 0) {
+    BM_CHECK_ARG(PV <= BM_MAX_VSTAGES, "explicit stage_layers needs P*V <= BM_MAX_VSTAGES");
+    int sum = 0;
+    for (int s = 0; s < PV; ++s) {
+      BM_CHECK_ARG(mc.stage_layers[s] >= 1, "stage_layers: every virtual stage needs >= 1 layer");
+      sum += mc.stage_layers[s];
+    }
+    for (int s = PV; s < BM_MAX_VSTAGES; ++s) BM_CHECK_ARG(mc.stage_layers[s] == 0, "stage_layers beyond P*V must be 0");
+    BM_CHECK_ARG(sum == mc.L, "stage_layers must sum to L");
+  } else if (mc.last_stage_layers == 0)
     BM_CHECK_ARG(mc.L % (sc.stages * sc.vchunks) == 0, "L must be a multiple of P*V (or set last_stage_layers)");
   else
     BM_CHECK_ARG(mc.last_stage_layers >= 1 && mc.L - mc.last_stage_layers >= sc.stages * sc.vchunks - 1,
@@ -131,6 +141,12 @@ static bm_status check_model(const bm_model_cfg& mc, const bm_sched_cfg& sc) {
 
 // LLM layers [*l0, *l0 + *n) of virtual stage s (bigmac.h, last_stage_layers)
 static void stage_layers(const bm_model_cfg& mc, int PV, int s, int* l0, int* n) {
+  if (mc.stage_layers[0] != 0) {
+    *l0 = 0;
+    for (int i = 0; i < s; ++i) *l0 += mc.stage_layers[i];
+    *n = mc.stage_layers[s];
+    return;
+  }
   if (mc.last_stage_layers == 0 || PV == 1) {
     *n = mc.L / PV;
     *l0 = s * *n;

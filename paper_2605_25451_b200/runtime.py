@@ -23,7 +23,7 @@ from . import schedule as BS
 
 
 def model_cfg(shape, dtype: str, max_n_mod: int | None = None, max_n_gen: int | None = None,
-              head_place: str = "auto", last_stage_layers: int = 0) -> L.ModelCfg:
+              head_place: str = "auto", last_stage_layers: int = 0, stage_layers=None) -> L.ModelCfg:
     mc = L.ModelCfg()
     mc.S, mc.d_in, mc.d_e, mc.f_e, mc.L_e = shape.S, shape.d_in, shape.d_e, shape.f_e, shape.L_e
     mc.d, mc.f, mc.L, mc.vocab = shape.d, shape.f, shape.L, shape.vocab
@@ -33,6 +33,8 @@ def model_cfg(shape, dtype: str, max_n_mod: int | None = None, max_n_gen: int | 
     mc.max_n_gen = max_n_gen if max_n_gen is not None else min(shape.n_gen_law[2], shape.S)
     mc.head_place = L.HEAD_PLACE[head_place]
     mc.last_stage_layers = last_stage_layers
+    for i, n in enumerate(stage_layers or ()):
+        mc.stage_layers[i] = n
     return mc
 
 
@@ -71,7 +73,7 @@ class DeviceBatch:
 
 class Runtime:
     def __init__(self, shape, dtype="bf16", rank=0, world=1, group=None, device=None, sched_kw=None,
-                 head_place="auto", last_stage_layers=0):
+                 head_place="auto", last_stage_layers=0, stage_layers=None):
         self.shape = shape
         self.dtype = dtype
         self.world = world
@@ -87,7 +89,8 @@ class Runtime:
         self._stream = None   # own compute stream (created on first step)
         kw = dict(sched_kw or {})
         self.sched = BS.build(self.P, self.M, self.V, **kw)
-        self.mc = model_cfg(shape, dtype, head_place=head_place, last_stage_layers=last_stage_layers)
+        self.mc = model_cfg(shape, dtype, head_place=head_place, last_stage_layers=last_stage_layers,
+                            stage_layers=stage_layers)
         h = C.c_void_p()
         L.call("bm_ctx_create", C.byref(self.mc), self.sched.handle, rank, C.byref(h))
         self.ctx = h.value

@@ -42,8 +42,13 @@ def main():
     # "ce" (compute-efficient baseline: all encoder forwards first, W = M / P);
     # "<gen_place>+head_dp": the LM head + CE DP-sharded with the generator (BM_HEAD_DP_SHARD)
     # "...+last<n>": last_stage_layers = n (uneven LLM layer partition, bigmac.h)
-    head, last = "auto", 0
+    # "...+split<a>-<b>-...": explicit stage_layers
+    head, last, split = "auto", 0, None
     toks = gen.split("+")
+    for t in toks:
+        if t.startswith("split"):
+            split = [int(x) for x in t[5:].split("-")]
+    toks = [t for t in toks if not t.startswith("split")]
     if "head_dp" in toks:
         head = "dp_shard"
     for t in toks:
@@ -56,7 +61,8 @@ def main():
         kw = {"enc_place": "entry_stage", "gen_place": gen.split("+")[1]}
     else:
         kw = {"gen_place": gen}
-    rt = Runtime(cfg, dtype, rank=rank, world=world, sched_kw=kw, head_place=head, last_stage_layers=last)
+    rt = Runtime(cfg, dtype, rank=rank, world=world, sched_kw=kw, head_place=head, last_stage_layers=last,
+                 stage_layers=split)
     rt.load_weights(W)
     db = rt.device_batch(B)
     for _ in range(2):

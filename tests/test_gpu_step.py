@@ -195,7 +195,7 @@ def _torchrun(nproc, *args, timeout=600):
 @pytest.mark.parametrize("P,M,V,dtype,gen", [(2, 4, 1, "f32", "dp_shard"), (2, 4, 1, "bf16", "dp_shard"),
                                            (2, 8, 2, "f32", "dp_shard"), (2, 4, 1, "f32", "last_stage"),
                                            (2, 4, 1, "f32", "dp_shard+head_dp"), (2, 8, 2, "bf16", "dp_shard+head_dp"),
-                                           (2, 4, 1, "f32", "dp_shard+last1"), (2, 4, 1, "bf16", "dp_shard+last3"),
+                                           (2, 4, 1, "f32", "dp_shard+last1"), (2, 4, 1, "bf16", "dp_shard+last3"), (2, 4, 1, "f32", "dp_shard+split1-3"),
                                            (2, 4, 1, "f32", "entry_stage+last_stage"),
                                            (2, 4, 1, "bf16", "ce")])
 def test_step_two_gpus(P, M, V, dtype, gen):

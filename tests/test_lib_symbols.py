@@ -42,9 +42,12 @@ def test_library_is_sm100a():
     assert "LDTM" in sass             # tcgen05.ld (TMEM -> registers)
 
 
-def expected_layers(L, P, V, last, s):
+def expected_layers(L, P, V, last, s, explicit=None):
     """bigmac.h "LLM layer partition": layers of virtual stage s."""
     PV = P * V
+    if explicit:
+        start = sum(explicit[:s])
+        return list(range(start, start + explicit[s]))
     if last == 0 or PV == 1:
         n = L // PV
         return list(range(s * n, (s + 1) * n))
@@ -65,7 +68,10 @@ def test_param_layout_matches_model(P, V, rank, head, last):
     cfg = get_config("C1", P=P, M=2 * P, V=V)
     if last and cfg.L - last < P * V - 1:
         pytest.skip("partition needs a layer per virtual stage")
-    mc = model_cfg(cfg, "bf16", head_place=head, last_stage_layers=last)
+    explicit = None
+    if last == 2 and P * V == 2:     # also an explicit partition (stage_layers)
+        explicit = [1, 3]
+    mc = model_cfg(cfg, "bf16", head_place=head, last_stage_layers=last, stage_layers=explicit)
     sc = BS.make_cfg(P, 2 * P, V)
     head_dp = head == "dp_shard"   # bigmac.h bm_head_place (auto = last stage)
     n, tot, dp = C.c_int32(), C.c_int64(), C.c_int64()
@@ -83,7 +89,7 @@ def test_param_layout_matches_model(P, V, rank, head, last):
         assert pi.offset >= prev_end and pi.offset % 64 == 0 and pi.ld >= cols and pi.ld % (1 if cols == 1 else 8) == 0
         prev_end = pi.offset + rows * pi.ld
         got[nm] = pi.kind
-    my_layers = {l for c in range(V) for l in expected_layers(cfg.L, P, V, last, c * P + rank)}
+    my_layers = {l for c in range(V) for l in expected_layers(cfg.L, P, V, last, c * P + rank, explicit)}
     for nm in specs:
         if nm.startswith(("enc.", "gen.")):
             assert got.get(nm) == 0, nm            # DP params on every rank
@@ -118,6 +124,10 @@ def test_layer_partition_examples_and_errors():
         L.call("bm_param_count", C.byref(mc), C.byref(BS.make_cfg(2, 4, 1)), 0, C.byref(n), C.byref(tot), C.byref(dp))
     mc = model_cfg(cfg.replace(L=5), "bf16", last_stage_layers=2)
     L.call("bm_param_count", C.byref(mc), C.byref(BS.make_cfg(2, 4, 1)), 0, C.byref(n), C.byref(tot), C.byref(dp))
+    for bad in ([1, 2], [4, 0], [2, 2, 1]):      # sum != L, empty stage, beyond P*V ([0, ...] = unset)
+        mc = model_cfg(cfg, "bf16", stage_layers=bad)
+        with pytest.raises(L.BigMacError):
+            L.call("bm_param_count", C.byref(mc), C.byref(BS.make_cfg(2, 4, 1)), 0, C.byref(n), C.byref(tot), C.byref(dp))
     mc = model_cfg(cfg, "bf16", head_place="dp_shard")
     with pytest.raises(L.BigMacError):       # the DP-sharded head rides on DP-sharded generator ops
         L.call("bm_param_count", C.byref(mc), C.byref(BS.make_cfg(2, 4, 1, gen_place="last_stage")), 0,
