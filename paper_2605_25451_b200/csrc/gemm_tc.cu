@@ -21,6 +21,7 @@
 #include <algorithm>
 #include <cstring>
 #include <unordered_map>
+#include <unordered_set>
 #include <mutex>
 #include <vector>
 
@@ -62,6 +63,12 @@ struct EpiArgs {
   int splits;      // split-K factor (1-CTA kernel); > 1: fp32 partials to the workspace map
   int kb_per;      // K blocks per split
   int mpad;        // workspace rows per split (M rounded up to the tile height)
+  // stream-K (CTA-pair kernel, sk != 0): pair p runs the k-iterations
+  // [p T / npairs, (p+1) T / npairs) of the T = tiles * nk (tile, k-block) sequence
+  int sk;
+  float* sk_ws;          // fp32 tail partials: [npairs][2 CTAs][128 rows][BN]
+  uint32_t* sk_flags;    // [npairs][2 CTAs][8 epilogue warps], = sk_epoch when a partial is ready
+  uint32_t sk_epoch;     // unique per launch on this flag set
 };
 
 // ---------------------------------------------------------------- PTX helpers
@@ -223,6 +230,46 @@ __device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int
   int r = t % per_group;
   mb = first_m + r % gm;
   nb = r / gm;
+}
+
+// The (tile, k-block range) segments of one CTA pair: round-robin whole tiles,
+// or (stream-K) the pair's contiguous share of the tile-major k-iteration
+// sequence.  With tiles >= pairs a share spans >= nk iterations, so a tile is
+// cut at most once: its head [0, kb1) ends the share of pair p and its tail
+// [kb1, nk) starts the share of pair p + 1.
+struct SegIter {
+  int sk, nk, num_tiles, step, t;
+  int64_t g, g1;
+  __device__ SegIter(const EpiArgs& a, int pair, int npairs, int tiles, int nk_)
+      : sk(a.sk), nk(nk_), num_tiles(tiles), step(npairs), t(pair) {
+    const int64_t tot = (int64_t)tiles * nk_;
+    g = tot * pair / npairs;
+    g1 = tot * (pair + 1) / npairs;
+  }
+  __device__ bool next(int& tile, int& kb0, int& kb1) {
+    if (!sk) {
+      if (t >= num_tiles) return false;
+      tile = t;
+      kb0 = 0;
+      kb1 = nk;
+      t += step;
+      return true;
+    }
+    if (g >= g1) return false;
+    tile = (int)(g / nk);
+    kb0 = (int)(g % nk);
+    kb1 = (int)min((int64_t)nk, (int64_t)kb0 + (g1 - g));
+    g += kb1 - kb0;
+    return true;
+  }
+};
+__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u32(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
@@ -792,13 +839,15 @@ gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = pair; t < num_tiles; t += npairs) {
+      SegIter it(args, pair, npairs, num_tiles, nk);
+      int t, kb0, kb1;
+      while (it.next(t, kb0, kb1)) {
         int mb, nb;
         tile_coords(t, tiles_m, tiles_n, mb, nb);
         const int m0 = mb * 2 * BM + (int)cta * BM;
         // SwiGLU pairing: CTA 0 loads gate rows [nb*BNH, +BNH), CTA 1 the matching up rows
         const int n0 = SWIGLU ? (nb * BNH + (int)cta * args.f) : (nb * BN + (int)cta * BNH);
-        for (int kb = 0; kb < nk; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           if (cta == 0) mbar_expect_tx(&full[stage], 2 * C::STAGE_BYTES);
           const uint32_t lbar = mapa(smem_u32(&full[stage]), 0);
@@ -827,13 +876,15 @@ gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
       int stage = 0;
       uint32_t phase = 0;
       int local = 0;
-      for (int t = pair; t < num_tiles; t += npairs, ++local) {
+      SegIter it(args, pair, npairs, num_tiles, nk);
+      int t, kb0, kb1;
+      for (; it.next(t, kb0, kb1); ++local) {
         const int acc = local & 1;
         const uint32_t acc_phase = (local >> 1) & 1;
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t tmem_d = tmem_base + acc * BN;
-        for (int kb = 0; kb < nk; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const uint32_t a_base = smem_u32(smA + stage * C::A_BYTES);
@@ -842,7 +893,7 @@ gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
           for (int kk = 0; kk < BK / 16; ++kk) {
             uint64_t ad = A_MN ? make_desc(a_base + kk * 2048, BK * 128, 1024) : make_desc(a_base + kk * 32, 16, 1024);
             uint64_t bd = B_MN ? make_desc(b_base + kk * 2048, BK * 128, 1024) : make_desc(b_base + kk * 32, 16, 1024);
-            umma_f16_pair(tmem_d, ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
+            umma_f16_pair(tmem_d, ad, bd, idesc, (kb != kb0 || kk != 0) ? 1u : 0u);
           }
           umma_commit_pair(&empty[stage]);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -859,7 +910,10 @@ gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
     const uint32_t leader_tempty0 = mapa(smem_u32(&tempty[0]), 0);
     const uint32_t leader_tempty1 = mapa(smem_u32(&tempty[1]), 0);
     int local = 0;
-    for (int t = pair; t < num_tiles; t += npairs, ++local) {
+    SegIter it(args, pair, npairs, num_tiles, nk);
+    int t, kb0, kb1;
+    const int ew = warp - 2;   // epilogue warp: (quad, half) sub-block, the same in every pair
+    for (; it.next(t, kb0, kb1); ++local) {
       int mb, nb;
       tile_coords(t, tiles_m, tiles_n, mb, nb);
       const int acc = local & 1;
@@ -869,6 +923,38 @@ gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
       const int row0 = mb * 2 * BM + (int)cta * BM + quad * 32;
       const int row = row0 + lane;
       const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + acc * BN;
+      if (!SWIGLU && kb0 > 0) {
+        // stream-K tail: this warp's 32 x BN/2 fp32 sub-block of the partial sum into
+        // the pair's workspace slot, then publish it (the head owner finishes the tile)
+        float* dst = args.sk_ws + ((((int64_t)pair * 2 + cta) * BM + quad * 32 + lane) * BN);
+#pragma unroll 1
+        for (int c = half * (BN / 2); c < (half + 1) * (BN / 2); c += 32) {
+          float v[32];
+          tmem_ld32(taddr + c, v);
+#pragma unroll
+          for (int j = 0; j < 32; j += 4)
+            __stcg(reinterpret_cast<float4*>(dst + c + j), make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]));
+        }
+        __threadfence();
+        __syncwarp();
+        if (lane == 0) st_release_u32(args.sk_flags + ((int64_t)pair * 2 + cta) * EPI_WARPS2 + ew, args.sk_epoch);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(acc ? leader_tempty1 : leader_tempty0);
+        continue;
+      }
+      const bool sk_head = !SWIGLU && kb1 < nk;   // head of a cut tile: add pair + 1's tail partial
+      const float* part = nullptr;
+      if (sk_head) {
+        if (lane == 0) {
+          const uint32_t* fl = args.sk_flags + ((int64_t)(pair + 1) * 2 + cta) * EPI_WARPS2 + ew;
+          const long long t0 = clock64();
+          while (ld_acquire_u32(fl) != args.sk_epoch)
+            if (clock64() - t0 > 40000000000LL) __trap();
+        }
+        __syncwarp();
+        part = args.sk_ws + ((((int64_t)(pair + 1) * 2 + cta) * BM + quad * 32 + lane) * BN);
+      }
       if (SWIGLU) {
         constexpr int W = BNH / 2;   // features per warp
 #pragma unroll 1
@@ -895,6 +981,13 @@ gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
         for (int c = half * W; c < (half + 1) * W; c += 32) {
           float v[32];
           tmem_ld32(taddr + c, v);
+          if (sk_head) {
+#pragma unroll
+            for (int j = 0; j < 32; j += 4) {
+              const float4 q = __ldcg(reinterpret_cast<const float4*>(part + c + j));
+              v[j] += q.x; v[j + 1] += q.y; v[j + 2] += q.z; v[j + 3] += q.w;
+            }
+          }
           if (args.tma) {
             if (nb * BN + c < args.N) {
               if (eiter >= 1) {
@@ -1090,7 +1183,7 @@ static bm_status launch2(const CUtensorMap& ma, const CUtensorMap& mb, const CUt
   }
   const int tiles = ceil_div(ea.M, 2 * BM) * (SWIGLU ? ceil_div(ea.f, BN / 2) : ceil_div(ea.N, BN));
   const int pairs = gemm_sm_budget() / 2;
-  const int grid = 2 * (tiles < pairs ? tiles : pairs);
+  const int grid = 2 * (tiles < pairs ? tiles : pairs);   // stream-K: tiles >= pairs, every pair busy
   BM_CUDA_TRY(launch_k(gemm2_kernel<BN, A_MN, B_MN, SWIGLU>, dim3(grid), dim3(NUM_THREADS2), C::SMEM, st, ma, mb, mc,
                        mc2, ea));
   count_launch();
@@ -1108,6 +1201,18 @@ static bm_status dispatch_majors2(bool a_mn, bool b_mn, const CUtensorMap& ma, c
 }
 
 }  // namespace tc
+
+// Workspace layout: [0, SK_FLAG_BYTES) stream-K ready flags (zeroed once per
+// workspace, then only written with launch-unique epochs), then either split-K
+// partial tiles (1-CTA kernel) or stream-K tail partials (CTA-pair kernel).
+constexpr int64_t SK_FLAG_BYTES = 64 << 10;
+static std::mutex g_sk_mu;
+static std::unordered_set<const void*> g_sk_ready;   // workspaces whose flag region is zeroed
+static uint32_t g_sk_epoch = 0;
+static int g_stream_k = [] {
+  const char* e = getenv("BM_STREAM_K");
+  return e ? (e[0] == '1' ? 1 : 0) : 0;   // opt-in: measured slower
+}();
 
 // 0 = auto (CTA pairs for large contractions), 1 = force 1-CTA, 2 = force CTA pairs
 static int g_gemm_mode = [] {
@@ -1165,6 +1270,26 @@ bm_status gemm_bf16_tc(int M, int N, int K, const void* A, int64_t lda, int a_ma
     else BM_TRY(make_map(A, M, K, lda, BK, &ma));
     if (b_major == 0) BM_TRY(make_map(B, K, N, ldb, BN2 / 2, &mb));
     else BM_TRY(make_map(B, N, K, ldb, BK, &mb));
+    // stream-K when whole-tile waves would leave > 5 % of the pairs idle (e.g. the
+    // C2 d = 2048 contractions: 128 tiles on 74 pairs = 1.73 waves -> 2)
+    const int pairs = gemm_sm_budget() / 2;
+    const int64_t tiles2 = (int64_t)ceil_div(M, 2 * BM) * ceil_div(N, BN2);
+    const int64_t waves = (tiles2 + pairs - 1) / pairs;
+    const int64_t sk_need = SK_FLAG_BYTES + (int64_t)pairs * 2 * BM * BN2 * 4;
+    if (g_stream_k && ws && ws_bytes >= sk_need && BN2 == 256 && tiles2 >= pairs && tiles2 % pairs != 0 &&
+        (double)tiles2 / (double)(waves * pairs) < 0.95 && (int64_t)ceil_div(K, BK) >= 2) {
+      {
+        std::lock_guard<std::mutex> lk(g_sk_mu);
+        if (!g_sk_ready.count(ws)) {
+          BM_CUDA_TRY(cudaMemsetAsync(ws, 0, SK_FLAG_BYTES, st));
+          g_sk_ready.insert(ws);
+        }
+        ea.sk_epoch = ++g_sk_epoch;
+      }
+      ea.sk = 1;
+      ea.sk_flags = reinterpret_cast<uint32_t*>(ws);
+      ea.sk_ws = reinterpret_cast<float*>(reinterpret_cast<char*>(ws) + SK_FLAG_BYTES);
+    }
     if (BN2 == 256) return dispatch_majors2<256>(amn, bmn, ma, mb, mc, ea, st);
     return dispatch_majors2<128>(amn, bmn, ma, mb, mc, ea, st);
   }
@@ -1181,10 +1306,12 @@ bm_status gemm_bf16_tc(int M, int N, int K, const void* A, int64_t lda, int a_ma
   // partial tiles in the caller's workspace, summed in split order)
   const int tiles = tm * ceil_div(N, BN);
   const int nk = ceil_div(K, BK);
-  if (ws && tiles < num_sms() / 2 && nk >= 4 && N % 4 == 0 &&
+  if (ws && ws_bytes > SK_FLAG_BYTES && tiles < num_sms() / 2 && nk >= 4 && N % 4 == 0 &&
       (epi == BM_EPI_STORE || epi == BM_EPI_ADD || epi == BM_EPI_ACCUM)) {
     int splits = std::min(8, std::min(num_sms() / tiles, nk / 2));
     const int mpad = tm * BM;
+    ws = reinterpret_cast<char*>(ws) + SK_FLAG_BYTES;   // keep the stream-K flag region intact
+    ws_bytes -= SK_FLAG_BYTES;
     while (splits > 1 && (int64_t)splits * mpad * N * 4 > ws_bytes) --splits;
     if (splits > 1) {
       const int kb_per = ceil_div(nk, splits);

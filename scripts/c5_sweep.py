@@ -27,6 +27,7 @@ def main():
     ap.add_argument("--config", default="C2")
     ap.add_argument("--ms", default="8,16,32,64,128,256")
     ap.add_argument("--steps", type=int, default=2)
+    ap.add_argument("--strategy", default="bigmac", choices=["bigmac", "compute_efficient", "memory_efficient"])
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -44,9 +45,13 @@ def main():
         cfg = get_config(args.config, P=world, M=M, V=1)
         torch.cuda.empty_cache()
         torch.cuda.reset_peak_memory_stats()
-        rt = Runtime(cfg, "bf16", rank=rank, world=world, group=group)
+        kw = {"bigmac": {}, "compute_efficient": {"warmup_units": M // world},
+              "memory_efficient": {"enc_place": "entry_stage", "gen_place": "last_stage"}}[args.strategy]
+        rt = Runtime(cfg, "bf16", rank=rank, world=world, group=group, sched_kw=kw)
         rt.init_random_weights(1)
+        mem0 = torch.cuda.memory_allocated()
         db = rt.device_batch(make_batch(cfg))
+        batch_bytes = torch.cuda.memory_allocated() - mem0   # resident inputs (grow with M)
         rt.step(db)
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -65,7 +70,8 @@ def main():
             dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
         stash = rt.stash_peak()
         if rank == 0:
-            print(json.dumps({"config": args.config, "P": world, "M": M, "global_batch": M,
+            print(json.dumps({"config": args.config, "strategy": args.strategy, "P": world, "M": M, "global_batch": M,
+                              "work_bytes_rank0": rt.sizes.work_bytes, "input_batch_bytes_rank0": batch_bytes,
                               "samples_per_s": M / (t[0].item() / 1e3), "ms_per_step": t[0].item(),
                               "peak_hbm_gb_per_gpu_max": t[1].item(),
                               "rank0_stash_bytes_enc_llm_gen": stash,

@@ -67,7 +67,36 @@ def test_gemm_store_f32(L, M, N, K, a_mn, b_mn, dtype, mode):
     assert err <= tol, (err, tol)
 
 
-@pytest.mark.parametrize("M,N,K", [(300, 200, 104), (257, 513, 136), (1024, 768, 512), (554, 384, 1536)])
+@pytest.mark.parametrize("M,N,K", [(2560, 2048, 512), (4096, 2048, 1024), (2304, 4352, 320)])
+@pytest.mark.parametrize("a_mn,b_mn", [(0, 0), (0, 1), (1, 1), (1, 0)])
+def test_gemm_stream_k(L, M, N, K, a_mn, b_mn):
+    """CTA-pair GEMMs whose whole-tile waves would leave pairs idle (80 / 128 / 153
+    256x256 tiles on 74 pairs) run stream-K: tiles cut between two pairs, the tail's
+    fp32 partial added by the head owner.  Checked against the fp64 product."""
+    L.call("bm_k_gemm_mode", 2)
+    rng = np.random.default_rng(M + N + K + 3 * a_mn + b_mn)
+    A, B = rnd(rng, M, K), rnd(rng, N, K)
+    Ad = dev(A.T.copy() if a_mn else A, BF16)
+    Bd = dev(B.T.copy() if b_mn else B, BF16)
+    C = torch.full((M, N), 7.0, device="cuda", dtype=torch.float32)
+    L.call("bm_k_gemm", BF16, M, N, K, Ad.data_ptr(), M if a_mn else K, a_mn, Bd.data_ptr(), N if b_mn else K, b_mn,
+           C.data_ptr(), N, F32, 0, None, 0, 1.0, None)
+    torch.cuda.synchronize()
+    L.call("bm_k_gemm_mode", 0)
+    ref = A @ B.T
+    err = np.abs(host(C) - ref).max()
+    assert err <= 1e-5 * np.sqrt(K) * max(1.0, np.abs(ref).max()), err
+    # deterministic: a rerun reproduces every bit
+    C2 = torch.zeros_like(C)
+    L.call("bm_k_gemm_mode", 2)
+    L.call("bm_k_gemm", BF16, M, N, K, Ad.data_ptr(), M if a_mn else K, a_mn, Bd.data_ptr(), N if b_mn else K, b_mn,
+           C2.data_ptr(), N, F32, 0, None, 0, 1.0, None)
+    torch.cuda.synchronize()
+    L.call("bm_k_gemm_mode", 0)
+    assert torch.equal(C, C2)
+
+
+@pytest.mark.parametrize("M,N,K", [(300, 200, 104), (257, 513, 136), (1024, 768, 512), (554, 384, 1536), (4096, 2048, 640)])
 @pytest.mark.parametrize("epi", ["bf16_store", "bf16_add", "f32_accum"])
 @pytest.mark.parametrize("mode", [1, 2])
 def test_gemm_epilogues(L, M, N, K, epi, mode):
