@@ -348,9 +348,10 @@ struct bm_ctx {
   std::vector<int> consumer_kind;      // per op index: kind of the first compute op after it
   // GEMM timing (bench roofline): event pairs around every GEMM, two pools by step parity
   bool timing = false;
-  // fused SwiGLU GEMM epilogues (bm_k_gemm_swiglu / _dswiglu); off by default: measured
-  // slower than GEMM + the separate vectorised kernel (profiles/r01/gemm_bench_v4)
-  bool fuse_swiglu = getenv("BM_FUSE_SWIGLU") != nullptr;
+  // fused SwiGLU GEMM epilogues (bm_k_gemm_swiglu / _dswiglu); on by default: C2 step
+  // 48.6 vs 47.5 samples/s with the separate kernels (profiles/r01/bench_n1_fuse*.log);
+  // BM_FUSE_SWIGLU=0 selects GEMM + the vectorised elementwise kernel
+  bool fuse_swiglu = !(getenv("BM_FUSE_SWIGLU") && getenv("BM_FUSE_SWIGLU")[0] == '0');
   bool peer_copy_ce = !(getenv("BM_PEER_COPY") && std::string(getenv("BM_PEER_COPY")) == "sm");
   int peer_copy_ctas = getenv("BM_PEER_COPY_CTAS") ? std::atoi(getenv("BM_PEER_COPY_CTAS")) : 32;
   bool spin_wait = getenv("BM_WAIT") && std::string(getenv("BM_WAIT")) == "spin";
