@@ -267,6 +267,9 @@ def main():
     ap.add_argument("--microbatches", type=int, default=0, help="per-replica M (default 16 P)")
     ap.add_argument("--last-stage-layers", type=int, default=-1,
                     help="LLM layers of the last stage (bigmac.h); -1 = balance the LM head (HEAD_LAYERS), 0 = uniform")
+    ap.add_argument("--warmup-units", type=int, default=-1,
+                    help="BigMac W (encoder units in flight); -1: 2 at P = 1 (lets the encoder stream overlap "
+                         "the next microbatch), else 0 = W* (DESIGN.md R4)")
     ap.add_argument("--stage-layers", default="", help="explicit LLM layers per stage, e.g. 4,5,4,3 (bigmac.h)")
     ap.add_argument("--stages", type=int, default=0, help="pipeline stages P (default min(N, 4)); D = N / P replicas")
     ap.add_argument("--dtype", default="bf16")
@@ -302,7 +305,8 @@ def main():
     cfg, P, D = workload(args, N)
     if args.warmup < 3:
         raise SystemExit("--warmup must be >= 3")
-    sched_kw = {"bigmac": {}, "compute_efficient": {"warmup_units": cfg.M // P},
+    W = args.warmup_units if args.warmup_units >= 0 else (2 if P == 1 else 0)
+    sched_kw = {"bigmac": {"warmup_units": W}, "compute_efficient": {"warmup_units": cfg.M // P},
                 "memory_efficient": {"enc_place": "entry_stage", "gen_place": "last_stage"}}[args.strategy]
     split = stage_split(args, cfg, P)
     n_last = 0 if split else last_stage_layers(args, cfg, P)
@@ -453,6 +457,7 @@ def main():
             "scaling": "strong" if args.microbatches else "weak",
             "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
             "config": dict(config_dict(cfg, P, D), strategy=args.strategy, head_place=head_place_name(args, N),
+                           warmup_units=rt.sched.stats(0).w_star if W == 0 else W,
                            last_stage_layers=n_last, stage_layers=split),
             "roofline": roofline, "step_roofline": step_roof,
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches_all, "clocks": clocks,

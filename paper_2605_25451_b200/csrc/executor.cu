@@ -281,7 +281,8 @@ struct bm_ctx {
   char *dwork[2] = {nullptr, nullptr}, *bout[2] = {nullptr, nullptr}, *dh = nullptr, *dgu = nullptr, *dxn = nullptr;
   float* part = nullptr;
   float* part_gen = nullptr;  // RMSNorm-backward partials of the generator stream (no sharing across streams)
-  char *ws = nullptr, *ws_gen = nullptr;  // split-K workspaces of the two compute streams
+  float* part_enc = nullptr;  // ... and of the encoder stream
+  char *ws = nullptr, *ws_gen = nullptr, *ws_enc = nullptr;  // split-K workspaces of the three compute streams
   int64_t ws_bytes = 0;
   void* cur_ws = nullptr;
   // BM_DEBUG_PROGRESS=1: each stream writes the index of the last op it finished
@@ -342,6 +343,15 @@ struct bm_ctx {
   // soon as their inputs exist instead of queueing behind the rank's LLM op
   cudaStream_t gen_st = nullptr;
   bool use_gen_stream = false;
+  // encoder stream (BM_ENC_DP_UNIT): EncFwd / EncBwd run beside the LLM so their small,
+  // latency-bound kernels fill SMs the LLM GEMMs leave idle (partial last waves);
+  // ordered against the LLM by events: F(mb, 0) waits for EncFwd's output, EncBwd for
+  // B(mb, 0)'s embedding gradient, B's next write of emb_local for EncBwd's read
+  cudaStream_t enc_st = nullptr;
+  bool use_enc_stream = false;
+  std::vector<cudaEvent_t> enc_fwd_ev;   // per encoder stash slot: EncFwd output ready
+  cudaEvent_t emb_ready_ev = nullptr, emb_free_ev = nullptr;
+  bool emb_free_pending = false;
   cudaEvent_t hn_ev = nullptr, gen_done_ev = nullptr;
   bool gen_done_pending = false;
   std::map<int, int> own_gout;   // last rank: mb -> gout slot holding its own shard's dX
@@ -392,6 +402,11 @@ bm_ctx::~bm_ctx() {
   for (auto s_ : comm_st)
     if (s_) cudaStreamDestroy(s_);
   if (gen_st) cudaStreamDestroy(gen_st);
+  if (enc_st) cudaStreamDestroy(enc_st);
+  for (auto e : enc_fwd_ev)
+    if (e) cudaEventDestroy(e);
+  if (emb_ready_ev) cudaEventDestroy(emb_ready_ev);
+  if (emb_free_ev) cudaEventDestroy(emb_free_ev);
   if (hn_ev) cudaEventDestroy(hn_ev);
   if (gen_done_ev) cudaEventDestroy(gen_done_ev);
   for (auto e : evpool)
@@ -523,12 +538,14 @@ static void work_layout(bm_ctx& c, char* base) {
   const int wmax = std::max(std::max(m.d, m.d_e), m.d_g);
   c.part = (float*)b.take(rmsnorm_bwd_scratch_floats(std::max(S, (int64_t)m.max_n_mod), wmax) * 4);
   c.part_gen = (float*)b.take(rmsnorm_bwd_scratch_floats(std::max(c.gen_rows, 1), m.d_g) * 4);
+  c.part_enc = (float*)b.take(rmsnorm_bwd_scratch_floats(std::max(m.max_n_mod, 1), m.d_e) * 4);
   {
     const int64_t rows = ((int64_t)std::max(m.max_n_mod, c.gen_rows) + 127) / 128 * 128;
     const int64_t cols = std::max<int64_t>({m.d, m.d_e, m.f_e, m.d_g, m.f_g, m.d_in + 8});
     c.ws_bytes = std::min<int64_t>(64ll << 20, 8 * rows * cols * 4);
     c.ws = b.take(c.ws_bytes);
     c.ws_gen = b.take(c.ws_bytes);
+    c.ws_enc = b.take(c.ws_bytes);
   }
   c.embscr = b.take(embed_bwd_scratch_bytes(m.S));
   if (c.head_dp) {
@@ -578,7 +595,9 @@ static bm_status timed_gemm(bm_ctx& c, int M, int N, int K, const void* A, int64
                             int64_t ldb, int bm_, void* C, int64_t ldc, int cdt, int epi, const void* R, int64_t ldr,
                             int f = 0) {
   void* ws = c.cur_ws;
-  if (!c.timing || M <= 0 || N <= 0 || K <= 0)
+  // the roofline's dominant kernel: GEMMs on the compute stream (side-stream GEMMs
+  // overlap them, so their event spans would double-count device time)
+  if (!c.timing || M <= 0 || N <= 0 || K <= 0 || c.st != c.st_main)
     return gemm(c.dtype, M, N, K, A, lda, am, B, ldb, bm_, C, ldc, cdt, epi, R, ldr, 1.f, c.st, f, ws, c.ws_bytes);
   const int pool = (int)(c.step & 1);
   auto& ev = c.tev[pool];
@@ -709,6 +728,7 @@ static void dbg_launch_hook(cudaStream_t st, const void* kern) {
   int slot = -1;
   if (st == c->st_main) slot = 0;
   else if (st == c->gen_st) slot = 1;
+  else if (st == c->enc_st) slot = 2 + c->P;
   else
     for (int q = 0; q < c->P; ++q)
       if (q != c->rank && st == c->comm_st[q]) slot = 2 + q;
@@ -737,6 +757,7 @@ static cudaEvent_t trace_event(bm_ctx& c) {
 static int stream_slot(const bm_ctx& c, cudaStream_t st) {
   if (st == c.st_main) return 0;
   if (st == c.gen_st) return 1;
+  if (st == c.enc_st) return 2 + c.P;
   for (int q = 0; q < c.P; ++q)
     if (q != c.rank && st == c.comm_st[q]) return 2 + q;
   return 0;
@@ -848,6 +869,8 @@ static bm_status op_llm_fwd(bm_ctx& c, const bm_op& o, const RecvState& rs) {
   // stage input (P:297 embed_preprocess at the entry stage)
   if (s == 0) {
     const int n_mod = c.n_mod[mb];
+    if (c.use_enc_stream && mb % c.P == 0)   // this rank's own encoder output (EncFwd on the encoder stream)
+      BM_CUDA_TRY(cudaStreamWaitEvent(c.st, c.enc_fwd_ev[(mb / c.P) % c.n_enc_slots], 0));
     const char* emb = c.enc_entry      ? c.enc[mb % c.n_enc_slots].out
                       : (mb % c.P == 0) ? c.enc[(mb / c.P) % c.n_enc_slots].out
                                         : recv_slot(c, mb % c.P, BM_PAY_EMB, rs.ops.at(0)->seq);
@@ -990,7 +1013,14 @@ static bm_status op_llm_bwd(bm_ctx& c, const bm_op& o, const RecvState& rs) {
     const int n_mod = c.n_mod[mb];
     BM_TRY(TY(c, embed_bwd<bf16>(m.S, m.d, n_mod, c.ids + (int64_t)mb * S, (const bf16*)c.bout[b], G_(c, "llm.embed"), c.embscr, c.st),
               embed_bwd<float>(m.S, m.d, n_mod, c.ids + (int64_t)mb * S, (const float*)c.bout[b], G_(c, "llm.embed"), c.embscr, c.st)));
-    if (c.enc_entry || mb % c.P == 0) BM_TRY(d2d(c, c.emb_local, c.bout[b], (int64_t)n_mod * d * es));
+    if (c.enc_entry || mb % c.P == 0) {
+      if (c.emb_free_pending) {   // the previous EncBwd (encoder stream) has read emb_local
+        BM_CUDA_TRY(cudaStreamWaitEvent(c.st, c.emb_free_ev, 0));
+        c.emb_free_pending = false;
+      }
+      BM_TRY(d2d(c, c.emb_local, c.bout[b], (int64_t)n_mod * d * es));
+      if (c.use_enc_stream) BM_CUDA_TRY(cudaEventRecord(c.emb_ready_ev, c.st));
+    }
   } else if ((s - 1) % c.P == c.rank) {
     BM_TRY(d2d(c, c.llm[c.llm_live.at({mb, ch - 1})].gin, c.bout[b], S * d * es));
   }
@@ -1283,6 +1313,14 @@ bm_status bm_ctx_create(const bm_model_cfg* mc, const bm_schedule* s, int32_t ra
   // generator ops run on a high-priority stream whenever there is a generator: they
   // start when Hn (final norm) of F(m, V-1) exists and overlap the LM head / CE
   c->use_gen_stream = c->has_gen && !(getenv("BM_GEN_STREAM") && getenv("BM_GEN_STREAM")[0] == '0');
+  // on by default at P = 1 (C2: 50.7 vs 48.6 samples/s with W = 2); at P > 1 the encoder
+  // kernels would compete with LLM ops on other ranks' critical path (N = 2: 89.1 vs 90.6),
+  // so BM_ENC_STREAM=1 / 0 forces it on / off
+  {
+    const char* e = getenv("BM_ENC_STREAM");
+    const bool want = e ? e[0] == '1' : c->P == 1;
+    c->use_enc_stream = c->has_enc && !c->enc_entry && want;
+  }
   *out = c;
   return BM_OK;
 }
@@ -1331,6 +1369,13 @@ bm_status bm_ctx_bind(bm_ctx* c, const bm_buffers* b) {
     for (int i = 0; i < 2; ++i) {
       BM_CUDA_TRY(cudaEventCreateWithFlags(&c->bout_ev[i], cudaEventDisableTiming));
       BM_CUDA_TRY(cudaEventCreateWithFlags(&c->gout_ev[i], cudaEventDisableTiming));
+    }
+    if (c->use_enc_stream) {
+      BM_CUDA_TRY(cudaStreamCreateWithFlags(&c->enc_st, cudaStreamNonBlocking));
+      c->enc_fwd_ev.assign(c->n_enc_slots, nullptr);
+      for (auto& e : c->enc_fwd_ev) BM_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      BM_CUDA_TRY(cudaEventCreateWithFlags(&c->emb_ready_ev, cudaEventDisableTiming));
+      BM_CUDA_TRY(cudaEventCreateWithFlags(&c->emb_free_ev, cudaEventDisableTiming));
     }
     if (c->use_gen_stream) {
       int least = 0, greatest = 0;
@@ -1499,6 +1544,8 @@ bm_status bm_step(bm_ctx* c, const bm_batch* b, void* stream) {
     for (int r = 0; r < x.P; ++r)
       if (r != x.rank) BM_CUDA_TRY(cudaStreamWaitEvent(x.comm_st[r], e, 0));
     if (x.use_gen_stream) BM_CUDA_TRY(cudaStreamWaitEvent(x.gen_st, e, 0));
+    if (x.use_enc_stream) BM_CUDA_TRY(cudaStreamWaitEvent(x.enc_st, e, 0));
+    x.emb_free_pending = false;
   }
   x.gen_done_pending = false;
   x.own_gout.clear();
@@ -1532,13 +1579,14 @@ bm_status bm_step(bm_ctx* c, const bm_batch* b, void* stream) {
     switch (o.kind) {
       case BM_OP_RECV: {
         const bool on_gen = x.use_gen_stream && x.consumer_kind[i] == BM_OP_GEN_FWD;
-        BM_TRY(do_recv_wait(x, o, on_gen ? x.gen_st : main_st));
-        if (x.debug_progress)
-          drv().write32((CUstream)(on_gen ? x.gen_st : main_st), (CUdeviceptr)(x.progress + 16 * (on_gen ? 1 : 0)),
-                        (uint32_t)i + 1, 0);
+        const bool on_enc = x.use_enc_stream && x.consumer_kind[i] == BM_OP_ENC_BWD;
+        cudaStream_t wst = on_gen ? x.gen_st : (on_enc ? x.enc_st : main_st);
+        BM_TRY(do_recv_wait(x, o, wst));
+        if (x.debug_progress && !on_enc)
+          drv().write32((CUstream)wst, (CUdeviceptr)(x.progress + 16 * (on_gen ? 1 : 0)), (uint32_t)i + 1, 0);
         if (x.tracing) {
-          cudaEvent_t e = trace_mark(x, on_gen ? x.gen_st : main_st);
-          x.trace.push_back({(int32_t)i, (int32_t)o.kind, on_gen ? 1 : 0, o.mb, e, e});
+          cudaEvent_t e = trace_mark(x, wst);
+          x.trace.push_back({(int32_t)i, (int32_t)o.kind, stream_slot(x, wst), o.mb, e, e});
         }
         rs.ops.push_back(&o);
         continue;
@@ -1553,7 +1601,8 @@ bm_status bm_step(bm_ctx* c, const bm_batch* b, void* stream) {
     }
     x.producer_ev = nullptr;
     const bool gen_op = o.kind == BM_OP_GEN_FWD || o.kind == BM_OP_GEN_BWD;
-    cudaStream_t op_st = (gen_op && x.use_gen_stream) ? x.gen_st : main_st;
+    const bool enc_op = o.kind == BM_OP_ENC_FWD || o.kind == BM_OP_ENC_BWD;
+    cudaStream_t op_st = (gen_op && x.use_gen_stream) ? x.gen_st : ((enc_op && x.use_enc_stream) ? x.enc_st : main_st);
     if (!gen_op && x.gen_done_pending && o.kind == BM_OP_LLM_BWD && o.chunk == x.V - 1 && x.rank == x.P - 1) {
       // the last stage's backward consumes the generator-input gradients (own shard added in place)
       BM_CUDA_TRY(cudaStreamWaitEvent(main_st, x.gen_done_ev, 0));
@@ -1564,13 +1613,26 @@ bm_status bm_step(bm_ctx* c, const bm_batch* b, void* stream) {
     x.st = op_st;
     x.producer_st = op_st;
     float* part_main = x.part;
-    if (op_st != main_st) x.part = x.part_gen;
-    x.cur_ws = (op_st != main_st) ? x.ws_gen : x.ws;
+    if (op_st == x.gen_st && op_st != main_st) x.part = x.part_gen;
+    if (op_st == x.enc_st && op_st != main_st) x.part = x.part_enc;
+    x.cur_ws = op_st == main_st ? x.ws : (op_st == x.gen_st ? x.ws_gen : x.ws_enc);
     set_sm_reserve((op_st == main_st && x.use_gen_stream && x.rank != x.P - 1) ? x.gen_reserve_sms : 0);
     cudaEvent_t tr_a = x.tracing ? trace_mark(x, op_st) : nullptr;
     switch (o.kind) {
-      case BM_OP_ENC_FWD: BM_TRY(op_enc_fwd(x, o)); live_enc += enc_unit_bytes; break;
-      case BM_OP_ENC_BWD: BM_TRY(op_enc_bwd(x, o, rs)); live_enc -= enc_unit_bytes; break;
+      case BM_OP_ENC_FWD:
+        BM_TRY(op_enc_fwd(x, o));
+        if (x.use_enc_stream) BM_CUDA_TRY(cudaEventRecord(x.enc_fwd_ev[o.unit % x.n_enc_slots], x.enc_st));
+        live_enc += enc_unit_bytes;
+        break;
+      case BM_OP_ENC_BWD:
+        if (x.use_enc_stream && x.rank == 0) BM_CUDA_TRY(cudaStreamWaitEvent(x.enc_st, x.emb_ready_ev, 0));
+        BM_TRY(op_enc_bwd(x, o, rs));
+        if (x.use_enc_stream && x.rank == 0) {   // emb_local read: B's next copy may overwrite it
+          BM_CUDA_TRY(cudaEventRecord(x.emb_free_ev, x.enc_st));
+          x.emb_free_pending = true;
+        }
+        live_enc -= enc_unit_bytes;
+        break;
       case BM_OP_LLM_FWD:
         BM_TRY(op_llm_fwd(x, o, rs));
         live_llm += llm_unit_bytes;
@@ -1615,6 +1677,11 @@ bm_status bm_step(bm_ctx* c, const bm_batch* b, void* stream) {
   if (x.use_gen_stream) {
     cudaEvent_t e = next_event(x);
     BM_CUDA_TRY(cudaEventRecord(e, x.gen_st));
+    BM_CUDA_TRY(cudaStreamWaitEvent(main_st, e, 0));
+  }
+  if (x.use_enc_stream) {   // encoder gradients complete before the DP allreduce
+    cudaEvent_t e = next_event(x);
+    BM_CUDA_TRY(cudaEventRecord(e, x.enc_st));
     BM_CUDA_TRY(cudaStreamWaitEvent(main_st, e, 0));
   }
   x.producer_st = nullptr;

@@ -67,7 +67,7 @@ def main():
         events = []
         for r, recs in enumerate(allt):
             for x in recs:
-                tid = STREAMS.get(x["stream"], f"comm->{x['stream'] - 2}")
+                tid = STREAMS.get(x["stream"], "encoder" if x["stream"] == 2 + world else f"comm->{x['stream'] - 2}")
                 name = x["kind"] if x["mb"] < 0 else f"{x['kind']} mb{x['mb']}"
                 dur = max(x["t1"] - x["t0"], 0.001)
                 events.append({"name": name, "ph": "X", "pid": f"rank {r}", "tid": tid,
@@ -77,7 +77,7 @@ def main():
             json.dump({"traceEvents": events, "displayTimeUnit": "ms"}, f)
         summ = []
         for r, recs in enumerate(allt):
-            comp = sorted([x for x in recs if x["stream"] in (0, 1) and x["kind"] not in ("Recv",)],
+            comp = sorted([x for x in recs if x["stream"] in (0, 1, 2 + world) and x["kind"] not in ("Recv",)],
                           key=lambda x: x["t0"])
             main = [x for x in comp if x["stream"] == 0]
             end = max(x["t1"] for x in recs)
@@ -85,7 +85,7 @@ def main():
             for x in recs:
                 if x["kind"] == "Recv":
                     continue
-                k = STREAMS.get(x["stream"], "comm")
+                k = STREAMS.get(x["stream"], "encoder" if x["stream"] == 2 + world else "comm")
                 busy[k] = busy.get(k, 0.0) + (x["t1"] - x["t0"])
             gaps = []
             prev = 0.0

@@ -73,7 +73,8 @@ def test_step_single_gpu(oracle_cache, dtype, M, V):
     rt.close()
 
 
-@pytest.mark.parametrize("kw", [{"enc_place": "entry_stage", "gen_place": "last_stage"}, {"warmup_units": 4}])
+@pytest.mark.parametrize("kw", [{"enc_place": "entry_stage", "gen_place": "last_stage"}, {"warmup_units": 4},
+                                {"warmup_units": 2}])
 def test_step_single_gpu_baselines(oracle_cache, kw):
     from paper_2605_25451_b200.runtime import Runtime
     cfg = get_config("C1", P=1, M=4, V=1)
