@@ -18,6 +18,8 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -s $((3*N)
     --log-file gpurun_out/launches_v3.csv $CMD > gpurun_out/ncu_launches.log 2>&1 || echo "launch list failed"
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:gemm2 -s 40 -c 4 \
     -o gpurun_out/prof_gemm_v3 $CMD > gpurun_out/ncu_full_gemm.log 2>&1 || echo "gemm capture failed"
-timeout 900 ncu --set full --clock-control none -k "regex:rmsnorm|swiglu|ce_row|colsum|embed_segsum|gelu|splitk" -s 200 -c 16 \
-    -o gpurun_out/prof_ew_v3 $CMD > gpurun_out/ncu_full_ew.log 2>&1 || echo "elementwise capture failed"
+# HBM-bound kernels at C2 LLM shapes, one launch each (scripts/prof_elementwise.py)
+python scripts/prof_elementwise.py --json gpurun_out/elementwise_v3.jsonl > gpurun_out/prof_ew_plain.log 2>&1 || echo "elementwise plain run failed"
+timeout 900 ncu --set full --clock-control none -k "regex:rmsnorm|swiglu|ce_row|sum_scale|gelu|embed" \
+    -o gpurun_out/prof_ew_v3 python scripts/prof_elementwise.py --iters 1 --warm 0 > gpurun_out/ncu_full_ew.log 2>&1 || echo "elementwise capture failed"
 ls -la gpurun_out | tail -8
