@@ -9,6 +9,8 @@
 #include <cfloat>
 
 #include <vector>
+#include <cub/block/block_radix_sort.cuh>
+#include <cub/block/block_scan.cuh>
 #include "common.cuh"
 
 namespace bm {
@@ -421,6 +423,56 @@ __global__ void embed_sort_kernel(int S, int n_mod, const int32_t* __restrict__ 
   }
 }
 
+// Same output as embed_sort_kernel (order = text positions sorted by id, equal
+// ids in position order; seg = segment starts; scratch[0] = #segments) with a
+// stable CUB block radix sort of (id, position) pairs: ITEMS * 1024 >= S - n_mod.
+template <int ITEMS>
+__global__ void __launch_bounds__(1024) embed_radix_sort_kernel(int S, int n_mod, const int32_t* __restrict__ ids,
+                                                                int32_t* __restrict__ scratch) {
+  pdl_enter();
+  using Sort = cub::BlockRadixSort<unsigned, 1024, ITEMS, int>;
+  using Scan = cub::BlockScan<int, 1024>;
+  __shared__ union {
+    typename Sort::TempStorage sort;
+    typename Scan::TempStorage scan;
+  } tmp;
+  __shared__ unsigned last_key[1024];
+  const int cnt = S - n_mod;
+  unsigned key[ITEMS];
+  int pos[ITEMS];
+#pragma unroll
+  for (int k = 0; k < ITEMS; ++k) {   // blocked arrangement: thread t holds items [t ITEMS, (t+1) ITEMS)
+    const int i = threadIdx.x * ITEMS + k;
+    key[k] = i < cnt ? (unsigned)ids[n_mod + i] : 0xffffffffu;
+    pos[k] = n_mod + i;
+  }
+  Sort(tmp.sort).Sort(key, pos);   // stable: equal ids stay in position order
+  last_key[threadIdx.x] = key[ITEMS - 1];
+  __syncthreads();
+  int32_t* order = scratch + 1;
+  int32_t* seg = scratch + 1 + S;
+  bool head[ITEMS];
+  int local = 0;
+#pragma unroll
+  for (int k = 0; k < ITEMS; ++k) {
+    const int i = threadIdx.x * ITEMS + k;
+    const unsigned prev = k > 0 ? key[k - 1] : (threadIdx.x > 0 ? last_key[threadIdx.x - 1] : 0u);
+    head[k] = i < cnt && (i == 0 || key[k] != prev);
+    local += head[k] ? 1 : 0;
+    if (i < cnt) order[i] = pos[k];
+  }
+  int base = 0, total = 0;
+  __syncthreads();   // tmp.sort -> tmp.scan
+  Scan(tmp.scan).ExclusiveSum(local, base, total);
+#pragma unroll
+  for (int k = 0; k < ITEMS; ++k)
+    if (head[k]) seg[base++] = threadIdx.x * ITEMS + k;
+  if (threadIdx.x == 0) {
+    scratch[0] = total;
+    seg[total] = cnt;
+  }
+}
+
 template <typename T>
 __global__ void embed_segsum_kernel(int S, int d, const int32_t* __restrict__ ids, const T* __restrict__ dX,
                                     const int32_t* __restrict__ scratch, float* __restrict__ dT) {
@@ -430,14 +482,26 @@ __global__ void embed_segsum_kernel(int S, int d, const int32_t* __restrict__ id
   const int32_t* seg = scratch + 1 + S;
   const int warps = blockDim.x / 32;
   const int lane = threadIdx.x % 32;
+  constexpr int N = V16<T>::N;   // d % N == 0 (embed_bwd checks)
   for (int s = blockIdx.x * warps + threadIdx.x / 32; s < nseg; s += gridDim.x * warps) {
     const int i0 = seg[s], i1 = seg[s + 1];
     const int id = ids[order[i0]];
     float* dst = dT + (int64_t)id * d;
-    for (int c = lane; c < d; c += 32) {
-      float acc = 0.f;
-      for (int i = i0; i < i1; ++i) acc += to_f(dX[(int64_t)order[i] * d + c]);
-      dst[c] += acc;
+    for (int c = lane * N; c < d; c += 32 * N) {
+      float acc[N];
+#pragma unroll
+      for (int j = 0; j < N; ++j) acc[j] = 0.f;
+      for (int i = i0; i < i1; ++i) {   // segment members in position order (deterministic)
+        const V16<T> v = vload(dX + (int64_t)order[i] * d + c);
+#pragma unroll
+        for (int j = 0; j < N; ++j) acc[j] += v.get(j);
+      }
+#pragma unroll
+      for (int j = 0; j < N; j += 4) {
+        float4 o = *reinterpret_cast<float4*>(dst + c + j);
+        o.x += acc[j]; o.y += acc[j + 1]; o.z += acc[j + 2]; o.w += acc[j + 3];
+        *reinterpret_cast<float4*>(dst + c + j) = o;
+      }
     }
   }
 }
@@ -755,7 +819,11 @@ bm_status embed_bwd(int S, int d, int n_mod, const int32_t* ids, const T* dX, fl
     BM_CUDA_TRY(cudaFuncSetAttribute(embed_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 16384 * 8));
     attr = true;
   }
-  BM_CUDA_TRY(launch_k(embed_sort_kernel, dim3(1), dim3(1024), smem, st, S, n_mod, ids, reinterpret_cast<int32_t*>(scratch)));
+  BM_CHECK_ARG(d % V16<T>::N == 0, "embed width must be a multiple of the vector width");
+  int32_t* sc = reinterpret_cast<int32_t*>(scratch);
+  if (cnt <= 4096) BM_CUDA_TRY(launch_k(embed_radix_sort_kernel<4>, dim3(1), dim3(1024), 0, st, S, n_mod, ids, sc));
+  else if (cnt <= 8192) BM_CUDA_TRY(launch_k(embed_radix_sort_kernel<8>, dim3(1), dim3(1024), 0, st, S, n_mod, ids, sc));
+  else BM_CUDA_TRY(launch_k(embed_sort_kernel, dim3(1), dim3(1024), smem, st, S, n_mod, ids, sc));
   BM_CUDA_TRY(launch_k(embed_segsum_kernel<T>, dim3(ceil_div(cnt, 8)), dim3(256), 0, st, S, d, ids, dX, reinterpret_cast<int32_t*>(scratch), dT));
   count_launch(2);
   BM_CUDA_TRY(cudaGetLastError());
@@ -881,7 +949,8 @@ void preload_elementwise(std::vector<const void*>& v) {
                         (const void*)cast_kernel<float, float>, (const void*)cast_kernel<bf16, bf16>,
                         (const void*)colsum_accum_kernel, (const void*)colsum2_accum_kernel, (const void*)copy16_kernel,
                         (const void*)copy1_kernel, (const void*)zero16_kernel, (const void*)zero1_kernel,
-                        (const void*)spin_wait_kernel, (const void*)embed_sort_kernel, (const void*)sum_scale_kernel})
+                        (const void*)spin_wait_kernel, (const void*)embed_sort_kernel, (const void*)sum_scale_kernel,
+                        (const void*)embed_radix_sort_kernel<4>, (const void*)embed_radix_sort_kernel<8>})
     v.push_back(f);
 }
 

@@ -186,7 +186,9 @@ def test_swiglu_gelu(L, dtype):
 
 
 @pytest.mark.parametrize("dtype", [BF16, F32])
-@pytest.mark.parametrize("S,d,n_mod,vocab", [(128, 128, 40, 256), (4096, 256, 700, 1000), (64, 64, 64, 50)])
+@pytest.mark.parametrize("S,d,n_mod,vocab", [(128, 128, 40, 256), (4096, 256, 700, 1000), (64, 64, 64, 50),
+                                             (4096, 2048, 554, 32000), (8192, 128, 300, 500), (8192, 64, 0, 40000),
+                                             (16384, 64, 100, 3000)])
 def test_embed(L, dtype, S, d, n_mod, vocab):
     rng = np.random.default_rng(4)
     table = rnd(rng, vocab, d)
