@@ -431,7 +431,7 @@ def main():
             traffic = json.load(open(tpath)).get("dram_bytes_per_launch")
         except Exception:
             traffic = None
-    roofline = {"bound": "tensor", "kernel": "bm::tc::gemm_kernel (tcgen05.mma kind::f16, TMA, TMEM)",
+    roofline = {"bound": "tensor", "kernel": "bm::tc::gemm2_kernel / gemm_kernel on the compute stream (tcgen05.mma kind::f16, TMA, TMEM; CTA pairs for the LLM contractions)",
                 "achieved": achieved, "peak": sustained, "unit": "TFLOP/s", "frac": achieved / sustained,
                 "peak_source": f"{peak_src} bf16_tflops_sustained (GEMMs timed inside a long step)",
                 "traffic": traffic, "launches": n_gemm_all,

@@ -1,0 +1,67 @@
+"""Host-side logic of bench.py (no GPU): the workload each N runs, the layer
+partition rules, the algorithmic FLOP count against SURVEY.md §8(d)'s table,
+and the reference arm's JSON line (the oracle timed on a tiny sample)."""
+import argparse
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import bench  # noqa: E402
+
+
+def ns(**kw):
+    d = dict(config="C2", microbatches=0, stages=0, last_stage_layers=-1, stage_layers="")
+    d.update(kw)
+    return argparse.Namespace(**d)
+
+
+@pytest.mark.parametrize("N,P,D,M", [(1, 1, 1, 16), (2, 2, 1, 32), (4, 4, 1, 64), (8, 4, 2, 64)])
+def test_workload_ladder(N, P, D, M):
+    # SURVEY §8(d) GPU ladder: P = G up to 4 stages, then pipeline replicas; 16 microbatches per GPU
+    cfg, p, d = bench.workload(ns(), N)
+    assert (p, d, cfg.M, cfg.V) == (P, D, M, 1)
+    assert cfg.M * d == 16 * N
+    cfg3, p3, _ = bench.workload(ns(config="C3"), 4)
+    assert (cfg3.V, p3, cfg3.M % p3) == (2, 4, 0)
+
+
+def test_layer_partition_rules():
+    a = ns()
+    for N, expect in [(2, 7), (4, 3), (8, 3)]:
+        cfg, P, _ = bench.workload(a, N)
+        assert bench.last_stage_layers(a, cfg, P) == expect
+    cfg, P, _ = bench.workload(a, 4)
+    split = bench.stage_split(a, cfg, P)
+    assert sum(split) == cfg.L and len(split) == P
+    assert bench.stage_split(ns(stage_layers="5,4,4,3"), cfg, P) == [5, 4, 4, 3]
+    assert bench.last_stage_layers(a, *bench.workload(a, 1)[:2]) == 0
+
+
+def test_step_flops_matches_survey_table():
+    # FLOP per microbatch at the mean modality / generation rows:
+    # C2 21.3 TF (LLM 93.0 %), C4 220.4 TF (LLM 96.5 %)
+    from synth import get_config
+    for name, n_mean, total, llm_share in [("C2", 554, 21.3e12, 0.930), ("C4", 1385, 220.4e12, 0.965)]:
+        cfg = get_config(name, P=1, M=1)
+        f = bench.step_flops(cfg, [n_mean], [n_mean])
+        llm = 6.0 * cfg.S * 3 * cfg.d * cfg.f * cfg.L
+        assert abs(f - total) / total < 0.01, (name, f)
+        assert abs(llm / f - llm_share) < 0.005, (name, llm / f)
+
+
+def test_reference_arm_json_line():
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--steps", "1",
+                        "--warmup", "0", "--ref-rows", "64"], capture_output=True, text=True, timeout=300, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-2000:]
+    line = json.loads([x for x in r.stdout.splitlines() if x.startswith("{")][-1])
+    for k in ("impl", "metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+              "scaling", "vs_baseline", "dtype", "data", "config", "cpu_baseline", "e2e"):
+        assert k in line, k
+    assert line["impl"] == "reference" and line["value"] > 0
+    assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["cpu_baseline"]["kind"] == "oracle"
+    assert line["config"]["workload"].startswith("C2")
