@@ -31,6 +31,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--head", default="auto", choices=["auto", "last_stage", "dp_shard"])
     ap.add_argument("--last-stage-layers", type=int, default=0)
+    ap.add_argument("--stage-layers", default="", help="explicit LLM layers per stage, e.g. 4,4,5,3")
     ap.add_argument("--out", default="gpurun_out/trace.json")
     a = ap.parse_args()
     rank, world = int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
@@ -45,7 +46,8 @@ def main():
     kw = {"bigmac": {}, "compute_efficient": {"warmup_units": cfg.M // world},
           "memory_efficient": {"enc_place": "entry_stage", "gen_place": "last_stage"}}[a.strategy]
     rt = Runtime(cfg, "bf16", rank=rank, world=world, group=group, sched_kw=kw, head_place=a.head,
-                 last_stage_layers=a.last_stage_layers)
+                 last_stage_layers=a.last_stage_layers,
+                 stage_layers=[int(v) for v in a.stage_layers.split(",")] if a.stage_layers else None)
     rt.init_random_weights(1)
     db = rt.device_batch(make_batch(cfg))
     for _ in range(a.warmup):
@@ -101,7 +103,11 @@ def main():
             idle_by_next = {}
             for g in gaps:
                 idle_by_next[g[1]] = idle_by_next.get(g[1], 0.0) + g[0]
+            # compute-stream idle as a fraction of the step vs the 1F1B closed form
+            # (P-1)/(MV+P-1): the measured idle also holds stage imbalance
             summ.append({"rank": r, "step_ms": end, "busy_ms": busy,
+                         "compute_idle_frac": sum(g[0] for g in gaps) / end if end > 0 else None,
+                         "bubble_bound_1f1b": (world - 1) / (a.M * a.V + world - 1),
                          "compute_idle_ms": sum(g[0] for g in gaps),
                          "op_ms_by_kind": per_kind,
                          "op_mean_ms": {k: per_kind[k] / n_kind[k] for k in per_kind},
