@@ -1,8 +1,8 @@
 """Executor stream semantics are deadlock-free (CPU).
 
-tests/tools/stream_sim.py replays bm_step's enqueue logic (compute, generator
-and per-peer comm streams; data/credit flag waits; producer, Hn, copy-done and
-generator-done events; the step-end allreduce barrier) as FIFO streams on the
+tests/tools/stream_sim.py replays bm_step's enqueue logic (compute, generator,
+encoder and per-peer comm streams; data/credit flag waits; producer, Hn,
+copy-done, generator-done, encoder-output and embedding-gradient events; the step-end allreduce barrier) as FIFO streams on the
 schedule the oracle builds, and runs them to completion.  A stuck stream means
 the executor adds a dependency cycle that the schedule's own acyclicity check
 (oracle/schedule.py size_rings) does not see."""
@@ -21,7 +21,7 @@ PLACEMENTS = [{}, {"gen_place": "last_stage"}, {"enc_place": "entry_stage", "gen
 
 
 @pytest.mark.parametrize("P,M,V", CASES)
-@pytest.mark.parametrize("kw", PLACEMENTS + [{"warmup": "M/P"}])
+@pytest.mark.parametrize("kw", PLACEMENTS + [{"warmup": "M/P"}, {"warmup_units": 2}, {"warmup_units": 3}])
 def test_no_executor_deadlock(P, M, V, kw):
     kw = dict(kw)
     if kw.pop("warmup", None):
@@ -31,4 +31,7 @@ def test_no_executor_deadlock(P, M, V, kw):
     except S.ScheduleError:
         pytest.skip("configuration rejected by the builder")
     stuck = simulate(sched, steps=2)
+    assert not stuck, stuck
+    # encoder stream forced on at any P (BM_ENC_STREAM=1); the default has it at P = 1
+    stuck = simulate(sched, steps=2, use_enc_stream=True)
     assert not stuck, stuck

@@ -8,11 +8,14 @@ from oracle import schedule as S
 KIND_OF = {"EncFwd": 0, "EncBwd": 1, "LlmFwd": 2, "LlmBwd": 3, "GenFwd": 4, "GenBwd": 5}
 
 
-def simulate(sched, steps=2, use_gen_stream=None, verbose=False):
+def simulate(sched, steps=2, use_gen_stream=None, use_enc_stream=None, verbose=False):
     cfg = sched.cfg
     P, V = cfg.stages, cfg.vchunks
     if use_gen_stream is None:
         use_gen_stream = cfg.gen_place != "none"
+    if use_enc_stream is None:   # executor default: on at P = 1 (BM_ENC_STREAM forces it)
+        use_enc_stream = P == 1
+    use_enc_stream = use_enc_stream and cfg.enc_place == "dp_unit"
     rings = sched.rings
     nmsg = {}
     for r in range(P):
@@ -62,6 +65,11 @@ def simulate(sched, steps=2, use_gen_stream=None, verbose=False):
                     wait_ev(r, f"comm{q}", e0)
             if use_gen_stream:
                 wait_ev(r, "gen", e0)
+            if use_enc_stream:
+                wait_ev(r, "enc", e0)
+            enc_slots = max(sched.stats[r].peak_enc_units, 1)
+            emb_free_pending = False
+            cur_gb = 0
             producer_ev, producer_st = None, "main"
             bsel = gsel = 0
             bout_pending = [None, None]
@@ -72,7 +80,8 @@ def simulate(sched, steps=2, use_gen_stream=None, verbose=False):
             for i, o in enumerate(ops):
                 if o.kind == "Recv":
                     consumer = next(x for x in ops[i + 1:] if x.kind not in ("Send", "Recv"))
-                    sname = "gen" if (use_gen_stream and consumer.kind == "GenFwd") else "main"
+                    sname = "gen" if (use_gen_stream and consumer.kind == "GenFwd") else (
+                        "enc" if (use_enc_stream and consumer.kind == "EncBwd") else "main")
                     ch = (o.peer, r, o.payload)
                     st(r, sname).append(("wait_flag", ("data", ch), step * nmsg[ch] + o.seq + 1))
                     continue
@@ -101,7 +110,8 @@ def simulate(sched, steps=2, use_gen_stream=None, verbose=False):
                     continue
                 producer_ev = None
                 gen_op = o.kind in ("GenFwd", "GenBwd")
-                op_st = "gen" if (gen_op and use_gen_stream) else "main"
+                enc_op = o.kind in ("EncFwd", "EncBwd")
+                op_st = "gen" if (gen_op and use_gen_stream) else ("enc" if (enc_op and use_enc_stream) else "main")
                 if (not gen_op and gen_done_pending and o.kind == "LlmBwd" and o.chunk == V - 1 and r == P - 1):
                     wait_ev(r, "main", f"r{r}gendone")
                     gen_done_pending = False
@@ -115,17 +125,28 @@ def simulate(sched, steps=2, use_gen_stream=None, verbose=False):
                         wait_ev(r, "main", bout_pending[b])
                         bout_pending[b] = None
                     last_ring, last_idx = 0, b
-                elif o.kind == "GenBwd":
+                elif o.kind == "GenFwd":
+                    # GenFwd picks the microbatch's gout slot ([dHn head rows | generator dX])
                     b = gsel
                     gsel ^= 1
-                    last_ring, last_idx = 1, b
+                    cur_gb = b
                     if gout_pending[b]:
                         wait_ev(r, op_st, gout_pending[b])
                         gout_pending[b] = None
+                elif o.kind == "GenBwd":
+                    last_ring, last_idx = 1, cur_gb
                 elif o.kind == "EncFwd":
                     last_ring = -1
                 elif o.kind == "LlmFwd":
                     last_ring = -1
+                own_enc_mb = r == 0 and o.chunk == 0 and o.mb % P == 0   # F/B at stage 0 of this rank's encoder mb
+                if use_enc_stream and o.kind == "LlmFwd" and own_enc_mb:
+                    wait_ev(r, "main", f"r{r}encfwd{(o.mb // P) % enc_slots}")
+                if o.kind == "LlmBwd" and own_enc_mb and emb_free_pending:
+                    wait_ev(r, "main", f"r{r}embfree")   # the last EncBwd read the embedding gradient
+                    emb_free_pending = False
+                if use_enc_stream and o.kind == "EncBwd" and r == 0:
+                    wait_ev(r, "enc", f"r{r}embready")
                 if o.kind == "LlmBwd" and o.chunk == V - 1 and r == P - 1 and o.mb in own_gout:
                     # own generator shard's dX added from gout; the slot is free after this op
                     st(r, op_st).append(("kernel", (r, i, o.kind, o.mb)))
@@ -137,6 +158,13 @@ def simulate(sched, steps=2, use_gen_stream=None, verbose=False):
                     st(r, op_st).append(("kernel", (r, i, o.kind, o.mb)))
                 if o.kind == "LlmFwd" and cfg.gen_place != "none" and o.chunk == V - 1 and r == P - 1:
                     rec(r, "main", f"r{r}hn")
+                if use_enc_stream and o.kind == "EncFwd":
+                    rec(r, "enc", f"r{r}encfwd{o.unit % enc_slots}")
+                if use_enc_stream and o.kind == "LlmBwd" and own_enc_mb:
+                    rec(r, "main", f"r{r}embready")
+                if use_enc_stream and o.kind == "EncBwd" and r == 0:
+                    rec(r, "enc", f"r{r}embfree")
+                    emb_free_pending = True
                 if o.kind == "GenBwd" and r == P - 1:
                     own_gout[o.mb] = last_idx
                 if o.kind == "GenBwd" and use_gen_stream and r == P - 1:
@@ -154,6 +182,10 @@ def simulate(sched, steps=2, use_gen_stream=None, verbose=False):
             if use_gen_stream:
                 e = new_ev(r)
                 rec(r, "gen", e)
+                wait_ev(r, "main", e)
+            if use_enc_stream:
+                e = new_ev(r)
+                rec(r, "enc", e)
                 wait_ev(r, "main", e)
         # allreduce barrier: every rank's main stream reaches it
         for r in range(P):
