@@ -69,6 +69,7 @@ struct EpiArgs {
   float* sk_ws;          // fp32 tail partials: [npairs][2 CTAs][128 rows][BN]
   uint32_t* sk_flags;    // [npairs][2 CTAs][8 epilogue warps], = sk_epoch when a partial is ready
   uint32_t sk_epoch;     // unique per launch on this flag set
+  int group;             // raster group (m-tiles per n sweep) of the CTA-pair kernel
 };
 
 // ---------------------------------------------------------------- PTX helpers
@@ -220,9 +221,8 @@ __host__ __device__ constexpr uint32_t make_idesc(int N, bool a_mn, bool b_mn, i
          | ((uint32_t)(M >> 4) << 24); // M / 16
 }
 
-__device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int& mb, int& nb) {
-  // grouped raster: 8 m-tiles share each n sweep for L2 reuse of B
-  const int G = 8;
+__device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int& mb, int& nb, int G = 8) {
+  // grouped raster: G m-tiles share each n sweep for L2 reuse of B
   int per_group = G * tiles_n;
   int group = t / per_group;
   int first_m = group * G;
@@ -843,7 +843,7 @@ gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
       int t, kb0, kb1;
       while (it.next(t, kb0, kb1)) {
         int mb, nb;
-        tile_coords(t, tiles_m, tiles_n, mb, nb);
+        tile_coords(t, tiles_m, tiles_n, mb, nb, args.group);
         const int m0 = mb * 2 * BM + (int)cta * BM;
         // SwiGLU pairing: CTA 0 loads gate rows [nb*BNH, +BNH), CTA 1 the matching up rows
         const int n0 = SWIGLU ? (nb * BNH + (int)cta * args.f) : (nb * BN + (int)cta * BNH);
@@ -915,7 +915,7 @@ gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
     const int ew = warp - 2;   // epilogue warp: (quad, half) sub-block, the same in every pair
     for (; it.next(t, kb0, kb1); ++local) {
       int mb, nb;
-      tile_coords(t, tiles_m, tiles_n, mb, nb);
+      tile_coords(t, tiles_m, tiles_n, mb, nb, args.group);
       const int acc = local & 1;
       const uint32_t acc_phase = (local >> 1) & 1;
       mbar_wait(&tfull[acc], acc_phase);
@@ -1209,6 +1209,11 @@ constexpr int64_t SK_FLAG_BYTES = 64 << 10;
 static std::mutex g_sk_mu;
 static std::unordered_set<const void*> g_sk_ready;   // workspaces whose flag region is zeroed
 static uint32_t g_sk_epoch = 0;
+static int g_raster_group = [] {   // BM_GEMM_GROUP: measurement override of the pair raster
+  const char* e = getenv("BM_GEMM_GROUP");
+  const int v = e ? atoi(e) : 8;
+  return v >= 1 ? v : 8;
+}();
 static int g_stream_k = [] {
   const char* e = getenv("BM_STREAM_K");
   return e ? (e[0] == '1' ? 1 : 0) : 0;   // opt-in: measured slower
@@ -1231,6 +1236,7 @@ bm_status gemm_bf16_tc(int M, int N, int K, const void* A, int64_t lda, int a_ma
                "A/B must be 16-byte aligned");
   const bool amn = a_major != 0, bmn = b_major != 0;
   EpiArgs ea{M, N, K, Cp, ldc, c_dtype == BM_F32 ? 1 : 0, epi, R, ldr, alpha, f, 0, 1, 1 << 30, 0};
+  ea.group = g_raster_group;
   CUtensorMap ma, mb, mc, mc2;
   std::memset(&mc, 0, sizeof(mc));
   std::memset(&mc2, 0, sizeof(mc2));

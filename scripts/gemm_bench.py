@@ -41,6 +41,8 @@ def main():
         ("C2 down fwd+res", 4096, 2048, 8192, 0, 0, "add"),
         ("C2 down dgrad", 4096, 8192, 2048, 0, 1, "store"),
         ("C2 gate_up wgrad", 16384, 2048, 4096, 1, 1, "accum"),
+        ("C2 gate_up dgrad", 4096, 2048, 16384, 0, 1, "store"),
+        ("C2 down wgrad", 2048, 8192, 4096, 1, 1, "accum"),
         ("C2 head fwd", 3500, 32000, 2048, 0, 0, "store"),
         ("8192^3", 8192, 8192, 8192, 0, 0, "store"),
         ("C4 gate_up fwd", 8192, 22016, 4096, 0, 0, "store"),
