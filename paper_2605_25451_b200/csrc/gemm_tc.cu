@@ -70,6 +70,11 @@ struct EpiArgs {
   uint32_t* sk_flags;    // [npairs][2 CTAs][8 epilogue warps], = sk_epoch when a partial is ready
   uint32_t sk_epoch;     // unique per launch on this flag set
   int group;             // raster group (m-tiles per n sweep) of the CTA-pair kernel
+  // sk == 2 (DP + split remainder): the first dp_tiles tiles round-robin as whole
+  // tiles; the other rem tiles are cut into ksplit k-ranges, pieces ordered
+  // k-range-major (piece i: range i / rem of remainder tile i % rem) and dealt
+  // round-robin, so concurrent pieces read the same k-range of A and B
+  int dp_tiles, rem, ksplit;
 };
 
 // ---------------------------------------------------------------- PTX helpers
@@ -240,13 +245,34 @@ __device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int
 struct SegIter {
   int sk, nk, num_tiles, step, t;
   int64_t g, g1;
+  int dp, rem, ks, piece;   // sk == 2
+  int q = -1, tr = -1;      // sk == 2: k-range index and remainder tile of the last piece (-1: whole tile)
   __device__ SegIter(const EpiArgs& a, int pair, int npairs, int tiles, int nk_)
-      : sk(a.sk), nk(nk_), num_tiles(tiles), step(npairs), t(pair) {
+      : sk(a.sk), nk(nk_), num_tiles(tiles), step(npairs), t(pair), dp(a.dp_tiles), rem(a.rem), ks(a.ksplit),
+        piece(pair) {
     const int64_t tot = (int64_t)tiles * nk_;
     g = tot * pair / npairs;
     g1 = tot * (pair + 1) / npairs;
   }
   __device__ bool next(int& tile, int& kb0, int& kb1) {
+    if (sk == 2) {
+      if (t < dp) {
+        tile = t;
+        kb0 = 0;
+        kb1 = nk;
+        t += step;
+        q = tr = -1;
+        return true;
+      }
+      if (piece >= rem * ks) return false;
+      q = piece / rem;
+      tr = piece % rem;
+      tile = dp + tr;
+      kb0 = (int)((int64_t)q * nk / ks);
+      kb1 = (int)((int64_t)(q + 1) * nk / ks);
+      piece += step;
+      return true;
+    }
     if (!sk) {
       if (t >= num_tiles) return false;
       tile = t;
@@ -923,10 +949,14 @@ gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
       const int row0 = mb * 2 * BM + (int)cta * BM + quad * 32;
       const int row = row0 + lane;
       const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + acc * BN;
-      if (!SWIGLU && kb0 > 0) {
-        // stream-K tail: this warp's 32 x BN/2 fp32 sub-block of the partial sum into
-        // the pair's workspace slot, then publish it (the head owner finishes the tile)
-        float* dst = args.sk_ws + ((((int64_t)pair * 2 + cta) * BM + quad * 32 + lane) * BN);
+      // partial-sum producers: stream-K tails (slot = this pair) and split-remainder
+      // pieces before the last k-range (slot = tr * (ksplit - 1) + q)
+      const bool piece_part = args.sk == 2 && it.q >= 0 && it.q < args.ksplit - 1;
+      if (!SWIGLU && ((args.sk == 1 && kb0 > 0) || piece_part)) {
+        // this warp's 32 x BN/2 fp32 sub-block of the partial sum into the slot, then
+        // publish it (the owner of the tile's last piece finishes the tile)
+        const int64_t pslot = piece_part ? (int64_t)it.tr * (args.ksplit - 1) + it.q : pair;
+        float* dst = args.sk_ws + (((pslot * 2 + cta) * BM + quad * 32 + lane) * BN);
 #pragma unroll 1
         for (int c = half * (BN / 2); c < (half + 1) * (BN / 2); c += 32) {
           float v[32];
@@ -937,23 +967,30 @@ gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
         }
         __threadfence();
         __syncwarp();
-        if (lane == 0) st_release_u32(args.sk_flags + ((int64_t)pair * 2 + cta) * EPI_WARPS2 + ew, args.sk_epoch);
+        if (lane == 0) st_release_u32(args.sk_flags + (pslot * 2 + cta) * EPI_WARPS2 + ew, args.sk_epoch);
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive_cluster(acc ? leader_tempty1 : leader_tempty0);
         continue;
       }
-      const bool sk_head = !SWIGLU && kb1 < nk;   // head of a cut tile: add pair + 1's tail partial
+      // consumers: a stream-K head adds pair + 1's tail; the last piece of a split
+      // remainder tile adds the tile's ksplit - 1 partials in k-range order
+      const bool sk_head = !SWIGLU && args.sk == 1 && kb1 < nk;
+      const bool piece_last = !SWIGLU && args.sk == 2 && it.q == args.ksplit - 1;
+      const int nparts = sk_head ? 1 : (piece_last ? args.ksplit - 1 : 0);
+      const int64_t pslot0 = sk_head ? (int64_t)(pair + 1) : (int64_t)it.tr * (args.ksplit - 1);
       const float* part = nullptr;
-      if (sk_head) {
+      if (nparts > 0) {
         if (lane == 0) {
-          const uint32_t* fl = args.sk_flags + ((int64_t)(pair + 1) * 2 + cta) * EPI_WARPS2 + ew;
-          const long long t0 = clock64();
-          while (ld_acquire_u32(fl) != args.sk_epoch)
-            if (clock64() - t0 > 40000000000LL) __trap();
+          for (int j = 0; j < nparts; ++j) {
+            const uint32_t* fl = args.sk_flags + ((pslot0 + j) * 2 + cta) * EPI_WARPS2 + ew;
+            const long long t0 = clock64();
+            while (ld_acquire_u32(fl) != args.sk_epoch)
+              if (clock64() - t0 > 40000000000LL) __trap();
+          }
         }
         __syncwarp();
-        part = args.sk_ws + ((((int64_t)(pair + 1) * 2 + cta) * BM + quad * 32 + lane) * BN);
+        part = args.sk_ws + (((pslot0 * 2 + cta) * BM + quad * 32 + lane) * BN);
       }
       if (SWIGLU) {
         constexpr int W = BNH / 2;   // features per warp
@@ -981,10 +1018,11 @@ gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
         for (int c = half * W; c < (half + 1) * W; c += 32) {
           float v[32];
           tmem_ld32(taddr + c, v);
-          if (sk_head) {
+          for (int pj = 0; pj < nparts; ++pj) {   // fixed order: deterministic
+            const float* pp = part + (int64_t)pj * 2 * BM * BN;
 #pragma unroll
             for (int j = 0; j < 32; j += 4) {
-              const float4 q = __ldcg(reinterpret_cast<const float4*>(part + c + j));
+              const float4 q = __ldcg(reinterpret_cast<const float4*>(pp + c + j));
               v[j] += q.x; v[j + 1] += q.y; v[j + 2] += q.z; v[j + 3] += q.w;
             }
           }
@@ -1214,6 +1252,10 @@ static int g_raster_group = [] {   // BM_GEMM_GROUP: measurement override of the
   const int v = e ? atoi(e) : 8;
   return v >= 1 ? v : 8;
 }();
+static int g_split_rem = [] {   // BM_SPLIT_REM=1: DP + split-remainder schedule (opt-in: measured slower)
+  const char* e = getenv("BM_SPLIT_REM");
+  return e ? (e[0] == '1' ? 1 : 0) : 0;
+}();
 static int g_stream_k = [] {
   const char* e = getenv("BM_STREAM_K");
   return e ? (e[0] == '1' ? 1 : 0) : 0;   // opt-in: measured slower
@@ -1282,7 +1324,36 @@ bm_status gemm_bf16_tc(int M, int N, int K, const void* A, int64_t lda, int a_ma
     const int64_t tiles2 = (int64_t)ceil_div(M, 2 * BM) * ceil_div(N, BN2);
     const int64_t waves = (tiles2 + pairs - 1) / pairs;
     const int64_t sk_need = SK_FLAG_BYTES + (int64_t)pairs * 2 * BM * BN2 * 4;
-    if (g_stream_k && ws && ws_bytes >= sk_need && BN2 == 256 && tiles2 >= pairs && tiles2 % pairs != 0 &&
+    // DP + split remainder (opt-in): whole-tile waves, then the remainder tiles cut
+    // into s k-ranges with s minimising ceil(rem s / pairs) / s (ties: smaller s)
+    const int nkb = ceil_div(K, BK);
+    const int64_t dp_t = tiles2 / pairs * pairs, rem_t = tiles2 - dp_t;
+    int best_s = 1;
+    double best = 1.0;
+    for (int sp = 2; sp <= 4 && sp <= nkb && rem_t > 0; ++sp) {   // s <= 4 bounds the partial traffic
+      const double r = (double)((rem_t * sp + pairs - 1) / pairs) / sp;
+      if (r < best - 1e-9) { best = r; best_s = sp; }
+    }
+    const int64_t hy_need = SK_FLAG_BYTES + rem_t * (best_s - 1) * 2 * BM * BN2 * 4;
+    const bool hybrid = g_split_rem && g_stream_k == 0 && ws && BN2 == 256 && tiles2 >= pairs && rem_t > 0 &&
+                        best <= 0.9 && best_s <= nkb && ws_bytes >= hy_need &&
+                        rem_t * (best_s - 1) * 2 * EPI_WARPS2 * 4 <= SK_FLAG_BYTES;
+    if (hybrid) {
+      {
+        std::lock_guard<std::mutex> lk(g_sk_mu);
+        if (!g_sk_ready.count(ws)) {
+          BM_CUDA_TRY(cudaMemsetAsync(ws, 0, SK_FLAG_BYTES, st));
+          g_sk_ready.insert(ws);
+        }
+        ea.sk_epoch = ++g_sk_epoch;
+      }
+      ea.sk = 2;
+      ea.dp_tiles = (int)dp_t;
+      ea.rem = (int)rem_t;
+      ea.ksplit = best_s;
+      ea.sk_flags = reinterpret_cast<uint32_t*>(ws);
+      ea.sk_ws = reinterpret_cast<float*>(reinterpret_cast<char*>(ws) + SK_FLAG_BYTES);
+    } else if (g_stream_k && ws && ws_bytes >= sk_need && BN2 == 256 && tiles2 >= pairs && tiles2 % pairs != 0 &&
         (double)tiles2 / (double)(waves * pairs) < 0.95 && (int64_t)ceil_div(K, BK) >= 2) {
       {
         std::lock_guard<std::mutex> lk(g_sk_mu);
