@@ -23,6 +23,7 @@
 #include <unordered_map>
 #include <unordered_set>
 #include <mutex>
+#include <string>
 #include <vector>
 
 #include "common.cuh"
@@ -75,6 +76,7 @@ struct EpiArgs {
   // k-range-major (piece i: range i / rem of remainder tile i % rem) and dealt
   // round-robin, so concurrent pieces read the same k-range of A and B
   int dp_tiles, rem, ksplit;
+  int mbar_cluster;      // 1: .acquire.cluster barrier waits (default); 0: BM_MBAR_SCOPE=cta
 };
 
 // ---------------------------------------------------------------- PTX helpers
@@ -88,26 +90,45 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
-__device__ __forceinline__ bool mbar_try(uint32_t addr, uint32_t parity) {
+// try_wait with the default .acquire.cta semantics (as CUTLASS's barrier waits):
+// the guarded data moves through the async proxy (TMA, tcgen05) whose completion
+// the barrier itself tracks, so no cluster-scope acquire -- which the compiler
+// implements as an L1 invalidation (CCTL.IVALL) on every poll -- is needed.
+// cluster_scope = 1 (default) uses .acquire.cluster; BM_MBAR_SCOPE=cta selects the
+// CTA-scope form (parity-tested, no measurable step difference: 47.8-48.0 both,
+// profiles/r01/bench_n1_mbar_*.log).
+__device__ __forceinline__ bool mbar_try(uint32_t addr, uint32_t parity, int cluster_scope) {
   uint32_t ok;
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n"
-      "selp.u32 %0, 1, 0, p;\n"
-      "}\n"
-      : "=r"(ok)
-      : "r"(addr), "r"(parity)
-      : "memory");
+  if (cluster_scope) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, p;\n"
+        "}\n"
+        : "=r"(ok)
+        : "r"(addr), "r"(parity)
+        : "memory");
+  } else {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, p;\n"
+        "}\n"
+        : "=r"(ok)
+        : "r"(addr), "r"(parity)
+        : "memory");
+  }
   return ok != 0;
 }
 // Wait for the phase with `parity`; a protocol bug traps after ~20 s instead of
 // hanging the GPU.
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity, int cluster_scope = 0) {
   const uint32_t a = smem_u32(bar);
-  if (mbar_try(a, parity)) return;
+  if (mbar_try(a, parity, cluster_scope)) return;
   const long long t0 = clock64();
-  while (!mbar_try(a, parity)) {
+  while (!mbar_try(a, parity, cluster_scope)) {
     if (clock64() - t0 > 40000000000LL) __trap();
   }
 }
@@ -675,7 +696,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
         const int m0 = mb * BM, n0 = nb * BN;
         const int kb_lo = sp * args.kb_per, kb_hi = min(nk_all, kb_lo + args.kb_per);
         for (int kb = kb_lo; kb < kb_hi; ++kb) {
-          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_wait(&empty[stage], phase ^ 1, args.mbar_cluster);
           mbar_expect_tx(&full[stage], C::STAGE_BYTES);
           uint8_t* a_dst = smA + stage * C::A_BYTES;
           uint8_t* b_dst = smB + stage * C::B_BYTES;
@@ -706,13 +727,13 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
       for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++local) {
         const int acc = local & 1;
         const uint32_t acc_phase = (local >> 1) & 1;
-        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        mbar_wait(&tempty[acc], acc_phase ^ 1, args.mbar_cluster);
         tc_fence_after();
         const uint32_t tmem_d = tmem_base + acc * BN;
         const int sp = t / base_tiles;
         const int kb_lo = sp * args.kb_per, kb_hi = min(nk_all, kb_lo + args.kb_per);
         for (int kb = kb_lo; kb < kb_hi; ++kb) {
-          mbar_wait(&full[stage], phase);
+          mbar_wait(&full[stage], phase, args.mbar_cluster);
           tc_fence_after();
           const uint32_t a_base = smem_u32(smA + stage * C::A_BYTES);
           const uint32_t b_base = smem_u32(smB + stage * C::B_BYTES);
@@ -746,7 +767,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
       tile_coords(t - sp * base_tiles, tiles_m, tiles_n, mb, nb);
       const int acc = local & 1;
       const uint32_t acc_phase = (local >> 1) & 1;
-      mbar_wait(&tfull[acc], acc_phase);
+      mbar_wait(&tfull[acc], acc_phase, args.mbar_cluster);
       tc_fence_after();
       const int row0 = mb * BM + quad * 32;
       const int row = row0 + lane;
@@ -874,7 +895,7 @@ gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
         // SwiGLU pairing: CTA 0 loads gate rows [nb*BNH, +BNH), CTA 1 the matching up rows
         const int n0 = SWIGLU ? (nb * BNH + (int)cta * args.f) : (nb * BN + (int)cta * BNH);
         for (int kb = kb0; kb < kb1; ++kb) {
-          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_wait(&empty[stage], phase ^ 1, args.mbar_cluster);
           if (cta == 0) mbar_expect_tx(&full[stage], 2 * C::STAGE_BYTES);
           const uint32_t lbar = mapa(smem_u32(&full[stage]), 0);
           uint8_t* a_dst = smA + stage * C::A_BYTES;
@@ -907,11 +928,11 @@ gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
       for (; it.next(t, kb0, kb1); ++local) {
         const int acc = local & 1;
         const uint32_t acc_phase = (local >> 1) & 1;
-        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        mbar_wait(&tempty[acc], acc_phase ^ 1, args.mbar_cluster);
         tc_fence_after();
         const uint32_t tmem_d = tmem_base + acc * BN;
         for (int kb = kb0; kb < kb1; ++kb) {
-          mbar_wait(&full[stage], phase);
+          mbar_wait(&full[stage], phase, args.mbar_cluster);
           tc_fence_after();
           const uint32_t a_base = smem_u32(smA + stage * C::A_BYTES);
           const uint32_t b_base = smem_u32(smB + stage * C::B_BYTES);
@@ -944,7 +965,7 @@ gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
       tile_coords(t, tiles_m, tiles_n, mb, nb, args.group);
       const int acc = local & 1;
       const uint32_t acc_phase = (local >> 1) & 1;
-      mbar_wait(&tfull[acc], acc_phase);
+      mbar_wait(&tfull[acc], acc_phase, args.mbar_cluster);
       tc_fence_after();
       const int row0 = mb * 2 * BM + (int)cta * BM + quad * 32;
       const int row = row0 + lane;
@@ -1252,6 +1273,10 @@ static int g_raster_group = [] {   // BM_GEMM_GROUP: measurement override of the
   const int v = e ? atoi(e) : 8;
   return v >= 1 ? v : 8;
 }();
+static int g_mbar_cluster = [] {   // default: the fully validated .acquire.cluster waits
+  const char* e = getenv("BM_MBAR_SCOPE");
+  return e && std::string(e) == "cta" ? 0 : 1;
+}();
 static int g_split_rem = [] {   // BM_SPLIT_REM=1: DP + split-remainder schedule (opt-in: measured slower)
   const char* e = getenv("BM_SPLIT_REM");
   return e ? (e[0] == '1' ? 1 : 0) : 0;
@@ -1279,6 +1304,7 @@ bm_status gemm_bf16_tc(int M, int N, int K, const void* A, int64_t lda, int a_ma
   const bool amn = a_major != 0, bmn = b_major != 0;
   EpiArgs ea{M, N, K, Cp, ldc, c_dtype == BM_F32 ? 1 : 0, epi, R, ldr, alpha, f, 0, 1, 1 << 30, 0};
   ea.group = g_raster_group;
+  ea.mbar_cluster = g_mbar_cluster;
   CUtensorMap ma, mb, mc, mc2;
   std::memset(&mc, 0, sizeof(mc));
   std::memset(&mc2, 0, sizeof(mc2));
