@@ -77,6 +77,7 @@ struct EpiArgs {
   // round-robin, so concurrent pieces read the same k-range of A and B
   int dp_tiles, rem, ksplit;
   int mbar_cluster;      // 1: .acquire.cluster barrier waits (default); 0: BM_MBAR_SCOPE=cta
+  int sk_tma;            // partials written by TMA stores through tmC2 (swizzled smem staging)
 };
 
 // ---------------------------------------------------------------- PTX helpers
@@ -977,17 +978,46 @@ gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
         // this warp's 32 x BN/2 fp32 sub-block of the partial sum into the slot, then
         // publish it (the owner of the tile's last piece finishes the tile)
         const int64_t pslot = piece_part ? (int64_t)it.tr * (args.ksplit - 1) + it.q : pair;
-        float* dst = args.sk_ws + (((pslot * 2 + cta) * BM + quad * 32 + lane) * BN);
+        if (args.sk_tma) {
+          // coalesced: swizzled 32 x 32 fp32 staging + TMA store into the workspace
+          // viewed as [slots * 2 * 128 rows, BN] (the normal epilogue's path)
+          const int prow = (int)((pslot * 2 + cta) * BM + quad * 32);
 #pragma unroll 1
-        for (int c = half * (BN / 2); c < (half + 1) * (BN / 2); c += 32) {
-          float v[32];
-          tmem_ld32(taddr + c, v);
+          for (int c = half * (BN / 2); c < (half + 1) * (BN / 2); c += 32) {
+            float v[32];
+            tmem_ld32(taddr + c, v);
+            if (eiter >= 1) {
+              if (lane == 0) bulk_wait_read0();
+              __syncwarp();
+            }
+            stage_f32(slot, lane, v);
+            fence_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_2d(&tmC2, slot, c, prow);
+              bulk_commit();
+            }
+            ++eiter;
+          }
+          if (lane == 0) {   // stores performed, then visible to the owner's generic loads
+            bulk_wait_all();
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+            __threadfence();
+          }
+          __syncwarp();
+        } else {
+          float* dst = args.sk_ws + (((pslot * 2 + cta) * BM + quad * 32 + lane) * BN);
+#pragma unroll 1
+          for (int c = half * (BN / 2); c < (half + 1) * (BN / 2); c += 32) {
+            float v[32];
+            tmem_ld32(taddr + c, v);
 #pragma unroll
-          for (int j = 0; j < 32; j += 4)
-            __stcg(reinterpret_cast<float4*>(dst + c + j), make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]));
+            for (int j = 0; j < 32; j += 4)
+              __stcg(reinterpret_cast<float4*>(dst + c + j), make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]));
+          }
+          __threadfence();
+          __syncwarp();
         }
-        __threadfence();
-        __syncwarp();
         if (lane == 0) st_release_u32(args.sk_flags + (pslot * 2 + cta) * EPI_WARPS2 + ew, args.sk_epoch);
         tc_fence_before();
         __syncwarp();
@@ -1252,11 +1282,13 @@ static bm_status launch2(const CUtensorMap& ma, const CUtensorMap& mb, const CUt
 
 template <int BN>
 static bm_status dispatch_majors2(bool a_mn, bool b_mn, const CUtensorMap& ma, const CUtensorMap& mb,
-                                  const CUtensorMap& mc, const EpiArgs& ea, cudaStream_t st) {
-  if (!a_mn && !b_mn) return launch2<BN, false, false>(ma, mb, mc, mc, ea, st);
-  if (!a_mn && b_mn) return launch2<BN, false, true>(ma, mb, mc, mc, ea, st);
-  if (a_mn && b_mn) return launch2<BN, true, true>(ma, mb, mc, mc, ea, st);
-  return launch2<BN, true, false>(ma, mb, mc, mc, ea, st);
+                                  const CUtensorMap& mc, const EpiArgs& ea, cudaStream_t st,
+                                  const CUtensorMap* mc2 = nullptr) {
+  const CUtensorMap& m2 = mc2 ? *mc2 : mc;   // second map: the split-remainder partial workspace
+  if (!a_mn && !b_mn) return launch2<BN, false, false>(ma, mb, mc, m2, ea, st);
+  if (!a_mn && b_mn) return launch2<BN, false, true>(ma, mb, mc, m2, ea, st);
+  if (a_mn && b_mn) return launch2<BN, true, true>(ma, mb, mc, m2, ea, st);
+  return launch2<BN, true, false>(ma, mb, mc, m2, ea, st);
 }
 
 }  // namespace tc
@@ -1276,6 +1308,10 @@ static int g_raster_group = [] {   // BM_GEMM_GROUP: measurement override of the
 static int g_mbar_cluster = [] {   // default: the fully validated .acquire.cluster waits
   const char* e = getenv("BM_MBAR_SCOPE");
   return e && std::string(e) == "cta" ? 0 : 1;
+}();
+static int g_sk_tma = [] {   // BM_SK_TMA=0: per-lane partial stores instead of TMA stores
+  const char* e = getenv("BM_SK_TMA");
+  return e ? (e[0] == '0' ? 0 : 1) : 1;
 }();
 static int g_split_rem = [] {   // BM_SPLIT_REM=1: DP + split-remainder schedule (opt-in: measured slower)
   const char* e = getenv("BM_SPLIT_REM");
@@ -1350,6 +1386,8 @@ bm_status gemm_bf16_tc(int M, int N, int K, const void* A, int64_t lda, int a_ma
     const int64_t tiles2 = (int64_t)ceil_div(M, 2 * BM) * ceil_div(N, BN2);
     const int64_t waves = (tiles2 + pairs - 1) / pairs;
     const int64_t sk_need = SK_FLAG_BYTES + (int64_t)pairs * 2 * BM * BN2 * 4;
+    CUtensorMap mws2;
+    bool have_mws2 = false;
     // DP + split remainder (opt-in): whole-tile waves, then the remainder tiles cut
     // into s k-ranges with s minimising ceil(rem s / pairs) / s (ties: smaller s)
     const int nkb = ceil_div(K, BK);
@@ -1379,6 +1417,11 @@ bm_status gemm_bf16_tc(int M, int N, int K, const void* A, int64_t lda, int a_ma
       ea.ksplit = best_s;
       ea.sk_flags = reinterpret_cast<uint32_t*>(ws);
       ea.sk_ws = reinterpret_cast<float*>(reinterpret_cast<char*>(ws) + SK_FLAG_BYTES);
+      if (g_sk_tma) {
+        BM_TRY(make_map_k(ea.sk_ws, (uint64_t)BN2, (uint64_t)rem_t * (best_s - 1) * 2 * BM, BN2, 32, 2, &mws2));
+        ea.sk_tma = 1;
+        have_mws2 = true;
+      }
     } else if (g_stream_k && ws && ws_bytes >= sk_need && BN2 == 256 && tiles2 >= pairs && tiles2 % pairs != 0 &&
         (double)tiles2 / (double)(waves * pairs) < 0.95 && (int64_t)ceil_div(K, BK) >= 2) {
       {
@@ -1393,7 +1436,7 @@ bm_status gemm_bf16_tc(int M, int N, int K, const void* A, int64_t lda, int a_ma
       ea.sk_flags = reinterpret_cast<uint32_t*>(ws);
       ea.sk_ws = reinterpret_cast<float*>(reinterpret_cast<char*>(ws) + SK_FLAG_BYTES);
     }
-    if (BN2 == 256) return dispatch_majors2<256>(amn, bmn, ma, mb, mc, ea, st);
+    if (BN2 == 256) return dispatch_majors2<256>(amn, bmn, ma, mb, mc, ea, st, have_mws2 ? &mws2 : nullptr);
     return dispatch_majors2<128>(amn, bmn, ma, mb, mc, ea, st);
   }
   // 1-CTA tiles: the largest BN that still gives ~a full wave of CTAs (small
