@@ -13,7 +13,12 @@
 // Runtime buffers are stash slots keyed by (mb, chunk) for the
 // LLM, by unit for the encoder, one for the generator.  DP gradients of the
 // encoder/projector/generator are accumulated locally and summed once at the
-// end of the step with NCCL.
+// end of the step with NCCL; with D pipeline replicas
+// (bm_ctx_init_replicas) the LLM stage gradients are also summed over the
+// stage's replicas.  Streams per rank: the caller's compute stream (LLM ops),
+// a high-priority generator stream (GenFwd/GenBwd, started at Hn-ready), an
+// encoder stream (EncFwd/EncBwd; default at P = 1) and one comm stream per
+// peer; cross-stream order is carried by events and device flags only.
 #include <dlfcn.h>
 
 #include <algorithm>
