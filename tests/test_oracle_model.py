@@ -178,3 +178,26 @@ def test_interpreter_baseline_strategies(P, M, V, enc, gen, W):
     assert abs(loss2 - loss) <= 1e-12 * abs(loss)
     for k in G:
         assert np.linalg.norm(G2[k] - G[k]) <= 1e-12 * max(np.linalg.norm(G[k]), 1e-30), k
+
+
+@pytest.mark.parametrize("D", [2, 3])
+def test_replica_global_batch_is_mean_of_replicas(D):
+    """Reading R15 (pipeline replicas): D replicas of M microbatches each compute
+    the global-batch step.  L over the M*D-microbatch batch equals the mean of the
+    D replica losses, and every gradient the mean of the replica gradients -- the
+    sum the GPU path forms with scale 1/(M D) and an allreduce over replicas."""
+    from synth import slice_batch
+    M = 2
+    cfg_g = get_config("C1", P=1, M=M * D, V=1)
+    W, Bg = make_weights(cfg_g), make_batch(cfg_g)
+    Lg, per_g, Gg = om.step_fp64(cfg_g, W, Bg)
+    Ls, Gs = [], []
+    for k in range(D):
+        Lk, per_k, Gk = om.step_fp64(get_config("C1", P=1, M=M, V=1), W, slice_batch(Bg, k * M, (k + 1) * M))
+        assert per_k == per_g[k * M:(k + 1) * M]          # per-microbatch terms are the replica's own
+        Ls.append(Lk)
+        Gs.append(Gk)
+    assert abs(Lg - np.mean(Ls)) <= 1e-12 * abs(Lg)
+    for name in Gg:
+        mean = sum(G[name] for G in Gs) / D
+        assert np.allclose(Gg[name], mean, rtol=1e-10, atol=1e-14), name
