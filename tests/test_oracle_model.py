@@ -201,3 +201,33 @@ def test_replica_global_batch_is_mean_of_replicas(D):
     for name in Gg:
         mean = sum(G[name] for G in Gs) / D
         assert np.allclose(Gg[name], mean, rtol=1e-10, atol=1e-14), name
+
+
+@pytest.mark.parametrize("P", [2, 3, 4])
+def test_head_dp_shards_reproduce_full_head(P):
+    """Reading R14 (DP-sharded LM head): text rows split into P shards
+    [n_mod + floor(r n_text / P), n_mod + floor((r+1) n_text / P)); each shard's CE
+    mean scaled by n_shard / n_text (the full-microbatch denominator) sums to the
+    full CE, and each shard's dHn rows and head gradient (dce = n_shard / n_text)
+    reassemble the unsharded backward exactly (up to fp64 rounding)."""
+    cfg = get_config("C1", P=1, M=1, V=1)
+    W = om.to_f64(make_weights(cfg))
+    rng = np.random.default_rng(7)
+    S, n_mod = cfg.S, 37
+    H = rng.standard_normal((S, cfg.d))
+    labels = rng.integers(0, cfg.vocab, size=S)
+    Hn, ce, cache = om.head_fwd(W, cfg, H, labels, n_mod)
+    G_full = {}
+    dHn_full = om.head_bwd_logits(W, cfg, cache, 1.0, G_full)
+    n_text = S - n_mod
+    ce_sum, G_sh, dHn_sh = 0.0, {}, np.zeros_like(dHn_full)
+    for r in range(P):
+        lo = n_mod + (r * n_text) // P
+        hi = n_mod + ((r + 1) * n_text) // P
+        _, ce_r, cache_r = om.head_fwd(W, cfg, H[:hi], labels[:hi], lo)   # CE mean over rows [lo, hi)
+        ce_sum += ce_r * (hi - lo) / n_text
+        d = om.head_bwd_logits(W, cfg, cache_r, (hi - lo) / n_text, G_sh)
+        dHn_sh[lo:hi] = d[lo:hi]
+    assert abs(ce_sum - ce) <= 1e-12 * abs(ce)
+    assert np.allclose(dHn_sh, dHn_full, rtol=1e-12, atol=1e-15)
+    assert np.allclose(G_sh["llm.head"], G_full["llm.head"], rtol=1e-10, atol=1e-15)
