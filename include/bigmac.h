@@ -250,6 +250,31 @@ bm_status bm_ctx_init_nccl(bm_ctx* c, const uint8_t id[128], int32_t nranks, int
 bm_status bm_ctx_init_replicas(bm_ctx* c, int32_t D, int32_t replica, const uint8_t id_world[128],
                                const uint8_t id_stage[128]);
 
+/* Step-end sums over peer memory instead of NCCL.
+ * The library sums the DP parameters' gradients over all P * D processes, each
+ * stage's LLM gradients over its D replicas (D > 1), the per-microbatch loss
+ * terms over the pipeline and the global-batch loss over everyone, by reading
+ * the peers' gradient buffers and peer-sum blocks directly through CUDA IPC:
+ * reduce-scatter (process i sums chunk i in process order -- deterministic),
+ * all-gather (chunk copies), separated by device-flag barriers
+ * (cuStreamWriteValue32 / cuStreamWaitValue32) on the compute stream.
+ * Use it when NCCL cannot form the group -- several processes on ONE device
+ * (NCCL rejects duplicate GPUs; the single-GPU multi-rank parity fixture) --
+ * or to compare with NCCL.  Replaces bm_ctx_init_nccl / bm_ctx_init_replicas
+ * (calling both is BM_E_INVALID).
+ *   D, replica      pipeline replicas as in bm_ctx_init_replicas (D = 1: one pipeline)
+ *   comm_handles    [P D][64] bm_ipc_export handles of every process's `comm`
+ *                   buffer, process g = replica * P + stage (own entry ignored)
+ *   comm_offsets    [P D] their byte offsets
+ *   grad_handles    [P D][64] handles of every process's `grads` buffer
+ *   grad_offsets    [P D]
+ * Call after bm_ctx_bind and after opening every pipeline peer with
+ * bm_ctx_open_peer.  P D <= 64.  Errors: BM_E_INVALID, BM_E_STATE (order),
+ * BM_E_CUDA (IPC open failed). */
+bm_status bm_ctx_init_peer_sum(bm_ctx* c, int32_t D, int32_t replica, const uint8_t* comm_handles,
+                               const int64_t* comm_offsets, const uint8_t* grad_handles,
+                               const int64_t* grad_offsets);
+
 /* One step's inputs.  If on_host != 0 the array pointers are host pointers
  * and bm_step copies them to the device inside the step (end-to-end path).
  * Row counts are always host arrays.  All ranks receive the full batch. */

@@ -102,6 +102,8 @@ SIGNATURES = {
     "bm_nccl_unique_id": [C.POINTER(C.c_uint8)],
     "bm_ctx_init_nccl": [_P, C.POINTER(C.c_uint8), _I32, _I32],
     "bm_ctx_init_replicas": [_P, _I32, _I32, C.POINTER(C.c_uint8), C.POINTER(C.c_uint8)],
+    "bm_ctx_init_peer_sum": [_P, _I32, _I32, C.POINTER(C.c_uint8), C.POINTER(_I64), C.POINTER(C.c_uint8),
+                             C.POINTER(_I64)],
     "bm_step": [_P, C.POINTER(Batch), _P],
     "bm_ctx_loss_ptr": [_P, C.POINTER(_P)],
     "bm_ctx_launch_count": [_P, C.POINTER(_I64)],

@@ -254,6 +254,45 @@ struct MlpSlot {  // encoder (L_e blocks) or generator (L_g blocks)
   char *a1 = nullptr, *p1 = nullptr, *out = nullptr, *dout = nullptr;
 };
 
+// process-wide registry of opened CUDA-IPC handles: one mapping per exported
+// allocation (two buffers of a peer may share one caching-allocator segment,
+// and a handle must not be opened twice in one process)
+struct IpcKey {
+  std::array<uint8_t, 64> h;
+  bool operator<(const IpcKey& o) const { return h < o.h; }
+};
+static std::map<IpcKey, std::pair<void*, int>>& ipc_reg() {
+  static std::map<IpcKey, std::pair<void*, int>> m;
+  return m;
+}
+static bm_status ipc_open(const uint8_t handle[64], void** base) {
+  IpcKey k;
+  std::memcpy(k.h.data(), handle, 64);
+  auto it = ipc_reg().find(k);
+  if (it != ipc_reg().end()) {
+    it->second.second += 1;
+    *base = it->second.first;
+    return BM_OK;
+  }
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, 64);
+  void* p = nullptr;
+  BM_CUDA_TRY(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+  ipc_reg()[k] = {p, 1};
+  *base = p;
+  return BM_OK;
+}
+static void ipc_close(void* base) {
+  for (auto it = ipc_reg().begin(); it != ipc_reg().end(); ++it)
+    if (it->second.first == base) {
+      if (--it->second.second == 0) {
+        cudaIpcCloseMemHandle(base);
+        ipc_reg().erase(it);
+      }
+      return;
+    }
+}
+
 }  // namespace bm
 
 using namespace bm;
@@ -276,6 +315,7 @@ struct bm_ctx {
   std::vector<Chan> chans;
   std::map<std::tuple<int, int, int>, int> chan_idx;
   std::vector<int64_t> comm_size;  // per rank
+  std::vector<int64_t> sum_off;    // per rank: peer-sum block in its comm buffer
   // op annotations
   std::vector<std::vector<int>> release_of;  // op index -> recv op indices released after it
   // work layout
@@ -324,6 +364,12 @@ struct bm_ctx {
   ncclComm_t nc_world = nullptr;   // all P * D processes: DP parameters
   ncclComm_t nc_stage = nullptr;   // the D processes of this stage: its LLM parameters
   float gscale = 1.f;              // per-sample gradient scale 1 / (M D)
+  // step-end sums over peer memory instead of NCCL (bm_ctx_init_peer_sum):
+  // process g = replica * P + stage; its peer-sum block and grad buffer as mapped here
+  bool psum = false;
+  std::vector<char*> ps_comm;
+  std::vector<float*> ps_grad;
+  std::vector<void*> ipc_bases;    // mappings to release (registry references)
   int64_t step = 0;
   int64_t launches = 0;
   int64_t stash_peak[3] = {0, 0, 0};
@@ -428,8 +474,7 @@ bm_ctx::~bm_ctx() {
     if (bout_ev[i]) cudaEventDestroy(bout_ev[i]);
     if (gout_ev[i]) cudaEventDestroy(gout_ev[i]);
   }
-  for (size_t r = 0; r < peer.size(); ++r)
-    if (peer[r] && (int)r != rank) cudaIpcCloseMemHandle(peer[r]);
+  for (void* b : ipc_bases) ipc_close(b);
   if (nc && nccl().ok) nccl().CommDestroy(nc);
   if (nc_world && nccl().ok) nccl().CommDestroy(nc_world);
   if (nc_stage && nccl().ok) nccl().CommDestroy(nc_stage);
@@ -478,8 +523,15 @@ static void comm_layout(bm_ctx& c) {
     ch.data_off = data_cur[ch.dst];
     data_cur[ch.dst] += ch.K * ch.slot_bytes;
   }
-  for (int r = 0; r < c.P; ++r) c.comm_size[r] = align_up(std::max<int64_t>(data_cur[r], 256), 256);
+  // peer-sum block (bm_ctx_init_peer_sum): one barrier flag per source process
+  // (BM_MAX_SUM_PEERS x 64 B) + the raw loss terms [2M] the peers read
+  c.sum_off.assign(c.P, 0);
+  for (int r = 0; r < c.P; ++r) {
+    c.sum_off[r] = align_up(data_cur[r], 256);
+    c.comm_size[r] = align_up(c.sum_off[r] + 64 * BM_MAX_SUM_PEERS + (2 * (int64_t)c.M + 1) * 4, 256);
+  }
 }
+
 
 struct Bump {
   char* base;
@@ -1229,6 +1281,75 @@ static bm_status do_release(bm_ctx& c, const bm_op& o, cudaStream_t on) {
   return BM_OK;
 }
 
+// ------------------------------------------------------------------ step-end sums over peer memory
+// barrier over all P D processes: write v into this process's flag slot at every
+// process, then wait until every process has written >= v into ours
+static bm_status psum_barrier(bm_ctx& c, uint32_t v) {
+  const int world = (int)c.ps_comm.size(), me = c.replica * c.P + c.rank;
+  for (int g = 0; g < world; ++g) {
+    CUresult r = drv().write32((CUstream)c.st, (CUdeviceptr)(c.ps_comm[g] + 64 * me), v, 0);
+    if (r != CUDA_SUCCESS) { set_error("cuStreamWriteValue32 (sum barrier) failed " + std::to_string((int)r)); return BM_E_CUDA; }
+  }
+  for (int g = 0; g < world; ++g)
+    if (g != me) BM_TRY(wait_flag(c, c.st, c.ps_comm[me] + 64 * g, v, "sum barrier"));
+  return BM_OK;
+}
+
+// chunk q of n over [0, count): 4-element (16-byte) aligned boundaries
+static void chunk_of(int64_t count, int n, int q, int64_t* lo, int64_t* hi) {
+  const int64_t n4 = (count + 3) / 4;
+  *lo = std::min(count, (n4 * q / n) * 4);
+  *hi = std::min(count, (n4 * (q + 1) / n) * 4);
+}
+
+// reduce-scatter of [off, off + count) of the gradient buffers over `group`
+// (process indices): this process sums chunk me_idx in group order, in place
+static bm_status psum_reduce_scatter(bm_ctx& c, const std::vector<int>& group, int me_idx, int64_t off, int64_t count) {
+  int64_t lo, hi;
+  chunk_of(count, (int)group.size(), me_idx, &lo, &hi);
+  if (hi <= lo) return BM_OK;
+  PeerSrc s{};
+  for (size_t q = 0; q < group.size(); ++q) s.p[q] = c.ps_grad[group[q]] + off + lo;
+  return peer_sum(s, (int)group.size(), c.G + off + lo, hi - lo, c.st);
+}
+// all-gather: copy every other member's reduced chunk
+static bm_status psum_all_gather(bm_ctx& c, const std::vector<int>& group, int me_idx, int64_t off, int64_t count) {
+  for (size_t q = 0; q < group.size(); ++q) {
+    if ((int)q == me_idx) continue;
+    int64_t lo, hi;
+    chunk_of(count, (int)group.size(), (int)q, &lo, &hi);
+    if (hi > lo)
+      BM_CUDA_TRY(cudaMemcpyAsync(c.G + off + lo, c.ps_grad[group[q]] + off + lo, (size_t)(hi - lo) * 4,
+                                  cudaMemcpyDeviceToDevice, c.st));
+  }
+  return BM_OK;
+}
+
+// DP parameters over every process, the stage's LLM parameters over its D replicas,
+// loss terms over the pipeline, the global-batch loss over everyone (A18)
+static bm_status peer_finalize(bm_ctx& x) {
+  const int world = x.P * x.D, me = x.replica * x.P + x.rank;
+  const uint32_t base = (uint32_t)(x.step * 4);
+  float* raw = (float*)(x.ps_comm[me] + 64 * BM_MAX_SUM_PEERS);
+  BM_CUDA_TRY(cudaMemcpyAsync(raw, x.loss, (size_t)2 * x.M * 4, cudaMemcpyDeviceToDevice, x.st));
+  BM_TRY(psum_barrier(x, base + 1));   // every gradient and loss term of the step is final
+  std::vector<int> all(world), stage(x.D), pipe(x.P);
+  for (int g = 0; g < world; ++g) all[g] = g;
+  for (int k = 0; k < x.D; ++k) stage[k] = k * x.P + x.rank;
+  for (int r = 0; r < x.P; ++r) pipe[r] = x.replica * x.P + r;
+  BM_TRY(psum_reduce_scatter(x, all, me, 0, x.dp_elems));
+  if (x.D > 1) BM_TRY(psum_reduce_scatter(x, stage, x.replica, x.dp_elems, x.total_elems - x.dp_elems));
+  PeerSrc sp{}, sw{};
+  for (int r = 0; r < x.P; ++r) sp.p[r] = (const float*)(x.ps_comm[pipe[r]] + 64 * BM_MAX_SUM_PEERS);
+  for (int g = 0; g < world; ++g) sw.p[g] = (const float*)(x.ps_comm[g] + 64 * BM_MAX_SUM_PEERS);
+  BM_TRY(peer_loss(sp, x.P, sw, world, x.M, 1.f / ((float)x.M * (float)x.D), x.loss, x.st));
+  BM_TRY(psum_barrier(x, base + 2));   // every owned chunk is reduced
+  BM_TRY(psum_all_gather(x, all, me, 0, x.dp_elems));
+  if (x.D > 1) BM_TRY(psum_all_gather(x, stage, x.replica, x.dp_elems, x.total_elems - x.dp_elems));
+  BM_TRY(psum_barrier(x, base + 3));   // nobody reads this step's buffers any more
+  return BM_OK;
+}
+
 }  // namespace bm
 
 // ================================================================ C ABI
@@ -1417,11 +1538,50 @@ bm_status bm_ipc_export(const void* dptr, uint8_t handle[64], int64_t* offset) {
 bm_status bm_ctx_open_peer(bm_ctx* c, int32_t peer, const uint8_t handle[64], int64_t offset) {
   BM_CHECK_ARG(c && handle && c->bound, "bind the context before opening peers");
   BM_CHECK_ARG(peer >= 0 && peer < c->P && peer != c->rank, "bad peer rank");
-  cudaIpcMemHandle_t h;
-  std::memcpy(&h, handle, 64);
+  BM_CHECK_ARG(!c->peer[peer], "peer already opened");
   void* p = nullptr;
-  BM_CUDA_TRY(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+  BM_TRY(ipc_open(handle, &p));
+  c->ipc_bases.push_back(p);
   c->peer[peer] = (char*)p + offset;
+  return BM_OK;
+}
+
+bm_status bm_ctx_init_peer_sum(bm_ctx* c, int32_t D, int32_t replica, const uint8_t* comm_handles,
+                               const int64_t* comm_offsets, const uint8_t* grad_handles, const int64_t* grad_offsets) {
+  BM_CHECK_ARG(c && comm_handles && comm_offsets && grad_handles && grad_offsets, "null argument");
+  BM_CHECK_ARG(c->bound, "bind the context before bm_ctx_init_peer_sum");
+  BM_CHECK_ARG(D >= 1 && replica >= 0 && replica < D, "replica out of range");
+  BM_CHECK_ARG((int64_t)c->P * D <= BM_MAX_SUM_PEERS, "too many processes for the peer sum");
+  BM_CHECK_ARG(!c->psum && !c->nc && !c->nc_world && !c->nc_stage, "step-end sums already initialised");
+  for (int r = 0; r < c->P; ++r)
+    BM_CHECK_ARG(c->peer[r], "open the pipeline peers (bm_ctx_open_peer) before bm_ctx_init_peer_sum");
+  const int world = c->P * D, me = replica * c->P + c->rank;
+  c->ps_comm.assign(world, nullptr);
+  c->ps_grad.assign(world, nullptr);
+  for (int g = 0; g < world; ++g) {
+    const int stage = g % c->P;
+    if (g == me) {
+      c->ps_comm[g] = c->comm + c->sum_off[stage];
+      c->ps_grad[g] = c->G;
+      continue;
+    }
+    if (g / c->P == replica) {
+      c->ps_comm[g] = c->peer[stage] + c->sum_off[stage];
+    } else {
+      void* p = nullptr;
+      BM_TRY(ipc_open(comm_handles + 64 * (size_t)g, &p));
+      c->ipc_bases.push_back(p);
+      c->ps_comm[g] = (char*)p + comm_offsets[g] + c->sum_off[stage];
+    }
+    void* p = nullptr;
+    BM_TRY(ipc_open(grad_handles + 64 * (size_t)g, &p));
+    c->ipc_bases.push_back(p);
+    c->ps_grad[g] = (float*)((char*)p + grad_offsets[g]);
+  }
+  c->D = D;
+  c->replica = replica;
+  c->gscale = 1.f / ((float)c->M * (float)D);
+  c->psum = true;
   return BM_OK;
 }
 
@@ -1484,11 +1644,11 @@ bm_status bm_step(bm_ctx* c, const bm_batch* b, void* stream) {
       set_error("peer " + std::to_string(r) + " not opened");
       return BM_E_STATE;
     }
-  if (c->P > 1 && !c->nc) {
-    set_error("NCCL not initialised (bm_ctx_init_nccl) for P > 1");
+  if (c->P > 1 && !c->nc && !c->psum) {
+    set_error("step-end sums not initialised (bm_ctx_init_nccl or bm_ctx_init_peer_sum) for P > 1");
     return BM_E_STATE;
   }
-  if (c->D > 1 && (!c->nc_world || !c->nc_stage)) {
+  if (c->D > 1 && !c->psum && (!c->nc_world || !c->nc_stage)) {
     set_error("replica communicators not initialised (bm_ctx_init_replicas)");
     return BM_E_STATE;
   }
@@ -1700,7 +1860,9 @@ bm_status bm_step(bm_ctx* c, const bm_batch* b, void* stream) {
   // finalize: DP gradient sum + loss terms
   cudaEvent_t tr_tail = x.tracing ? trace_mark(x, x.st) : nullptr;
   static const bool no_allreduce = getenv("BM_DEBUG_NO_ALLREDUCE") != nullptr;   // hang triage only
-  if (!no_allreduce && (x.P > 1 || x.D > 1)) {
+  if (x.psum && !no_allreduce) {
+    BM_TRY(peer_finalize(x));
+  } else if (!no_allreduce && (x.P > 1 || x.D > 1)) {
     // DP parameters over every process (the replica's pipeline group when D = 1),
     // this stage's LLM parameters over its D replicas, loss terms over the pipeline
     BM_NCCL_TRY(nccl().GroupStart());
@@ -1713,8 +1875,8 @@ bm_status bm_step(bm_ctx* c, const bm_batch* b, void* stream) {
     BM_NCCL_TRY(nccl().GroupEnd());
   }
   // L = (1/M) sum of the replica's terms; with replicas, the mean of the D replica losses
-  BM_TRY(loss_finalize(x.M, x.loss, 1.f / ((float)x.M * (float)x.D), x.st));
-  if (x.D > 1 && !no_allreduce)
+  if (!x.psum || no_allreduce) BM_TRY(loss_finalize(x.M, x.loss, 1.f / ((float)x.M * (float)x.D), x.st));
+  if (x.D > 1 && !no_allreduce && !x.psum)
     BM_NCCL_TRY(nccl().AllReduce(x.loss + 2 * x.M, x.loss + 2 * x.M, 1, ncclFloat32, ncclSum, x.nc_stage, x.st));
   if (x.tracing) {
     x.trace_last = trace_mark(x, x.st);

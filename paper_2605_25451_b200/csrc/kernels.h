@@ -50,4 +50,15 @@ bm_status spin_wait(const uint32_t* flag, uint32_t v, cudaStream_t st);
 // loss[2M] = scale * sum(loss[0 .. 2M))
 bm_status loss_finalize(int M, float* loss, float scale, cudaStream_t st);
 
+// step-end sums over CUDA-IPC peer memory (peer_sum.cu)
+#define BM_MAX_SUM_PEERS 64
+struct PeerSrc {
+  const float* p[BM_MAX_SUM_PEERS];
+};
+// dst[0:count) = sum_{q<n} s.p[q][0:count) in q order (dst may alias a source)
+bm_status peer_sum(const PeerSrc& s, int n, float* dst, int64_t count, cudaStream_t st);
+// loss[0:2M) = sum over the np pipeline sources; loss[2M] = scale * sum of all nw sources' terms
+bm_status peer_loss(const PeerSrc& pipe, int np, const PeerSrc& world, int nw, int M, float scale, float* loss,
+                    cudaStream_t st);
+
 }  // namespace bm

@@ -79,6 +79,7 @@ bm_status gemm(int dtype, int M, int N, int K, const void* A, int64_t lda, int a
 void preload_elementwise(std::vector<const void*>& v);
 void preload_simt(std::vector<const void*>& v);
 void preload_tc(std::vector<const void*>& v);
+void preload_peer_sum(std::vector<const void*>& v);
 // Load every kernel of the library onto the current device now.  Under CUDA lazy
 // module loading (the default) a kernel is loaded at its first launch, and that
 // load blocks while another stream of the context is parked on a cross-GPU flag
@@ -89,6 +90,7 @@ bm_status preload_kernels() {
   preload_elementwise(v);
   preload_simt(v);
   preload_tc(v);
+  preload_peer_sum(v);
   for (const void* f : v) {
     cudaFuncAttributes a;
     BM_CUDA_TRY(cudaFuncGetAttributes(&a, f));

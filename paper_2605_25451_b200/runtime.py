@@ -44,7 +44,8 @@ def exchange(group, P: int, D: int, global_rank: int, payload, new_id):
     (payloads of the P stages of this process's replica, in stage order,
      {"pipe": id of this replica's pipeline group (P > 1),
       "world": id of the all-process group (D > 1),
-      "stage": id of this stage's replica group (D > 1)}).
+      "stage": id of this stage's replica group (D > 1)},
+     payloads of all P * D processes).
     Ids are made by one member of each group (new_id() -> bytes): the pipeline's
     stage 0, process 0, and replica 0's process of the stage."""
     import torch.distributed as dist
@@ -57,7 +58,17 @@ def exchange(group, P: int, D: int, global_rank: int, payload, new_id):
     base = replica * P
     peers = [allp[base + q][0] for q in range(P)]
     ids = {"pipe": allp[base][1]["pipe"], "world": allp[0][1]["world"], "stage": allp[stage][1]["stage"]}
-    return peers, ids
+    return peers, ids, [a[0] for a in allp]
+
+
+def sum_mode(uuids) -> str:
+    """Step-end sums (A18): "nccl" when every process has its own GPU, "peer" (the
+    library's IPC reduce, bm_ctx_init_peer_sum) when two processes share a device
+    -- NCCL rejects duplicate GPUs.  BM_STEP_SUM=nccl|peer forces one."""
+    forced = os.environ.get("BM_STEP_SUM", "auto")
+    if forced in ("nccl", "peer"):
+        return forced
+    return "peer" if len(set(uuids)) < len(uuids) else "nccl"
 
 
 def _round8(x):
@@ -135,23 +146,37 @@ class Runtime:
         group, and with D > 1 the all-process and per-stage NCCL groups."""
         import torch.distributed as dist
         P, D = self.P, self.D
-        hb = (C.c_uint8 * 64)()
-        off = C.c_int64()
-        L.call("bm_ipc_export", self.comm_ptr, hb, C.byref(off))
+
+        def export(ptr):
+            hb = (C.c_uint8 * 64)()
+            off = C.c_int64()
+            L.call("bm_ipc_export", ptr, hb, C.byref(off))
+            return bytes(hb), off.value
 
         def new_id():
             nid = (C.c_uint8 * 128)()
             L.call("bm_nccl_unique_id", nid)
             return bytes(nid)
-        peers, ids = exchange(group, P, D, self.global_rank, (bytes(hb), off.value), new_id)
-        for q, (hbytes, o) in enumerate(peers):
+        uuid = str(torch.cuda.get_device_properties(self.device).uuid)
+        mine = (export(self.comm_ptr), export(self.g_ptr), uuid)
+        peers, ids, allp = exchange(group, P, D, self.global_rank, mine, new_id)
+        for q, ((hbytes, o), _, _) in enumerate(peers):
             if q != self.rank:
                 L.call("bm_ctx_open_peer", self.ctx, q, (C.c_uint8 * 64).from_buffer_copy(hbytes), o)
+        self.sum_mode = sum_mode([a[2] for a in allp])
         as_c = lambda b: (C.c_uint8 * 128).from_buffer_copy(b)  # noqa: E731
-        if P > 1:
-            L.call("bm_ctx_init_nccl", self.ctx, as_c(ids["pipe"]), P, self.rank)
-        if D > 1:
-            L.call("bm_ctx_init_replicas", self.ctx, D, self.replica, as_c(ids["world"]), as_c(ids["stage"]))
+        if self.sum_mode == "peer":
+            n = P * D
+            ch = (C.c_uint8 * (64 * n)).from_buffer_copy(b"".join(a[0][0] for a in allp))
+            co = (C.c_int64 * n)(*[a[0][1] for a in allp])
+            gh = (C.c_uint8 * (64 * n)).from_buffer_copy(b"".join(a[1][0] for a in allp))
+            go = (C.c_int64 * n)(*[a[1][1] for a in allp])
+            L.call("bm_ctx_init_peer_sum", self.ctx, D, self.replica, ch, co, gh, go)
+        else:
+            if P > 1:
+                L.call("bm_ctx_init_nccl", self.ctx, as_c(ids["pipe"]), P, self.rank)
+            if D > 1:
+                L.call("bm_ctx_init_replicas", self.ctx, D, self.replica, as_c(ids["world"]), as_c(ids["stage"]))
         dist.barrier(group=group)
 
     # ------------------------------------------------------------------ weights / grads

@@ -7,5 +7,5 @@ and `paper_2605_25451_b200/` import it; neither imports the other.
 """
 from .configs import CONFIGS, ModelShape, get_config  # noqa: F401
 from .gen import (  # noqa: F401
-    bf16_round, make_batch, make_weights, param_specs, slice_batch, Batch,
+    bf16_round, edge_counts, edge_shape, make_batch, make_weights, param_specs, slice_batch, Batch,
 )

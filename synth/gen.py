@@ -116,12 +116,19 @@ def _draw_counts(rng, law, M, S):
     return np.clip(n, 1, S).astype(np.int64)
 
 
-def make_batch(cfg: ModelShape, seed: int | None = None, M: int | None = None) -> Batch:
+def make_batch(cfg: ModelShape, seed: int | None = None, M: int | None = None, n_mod=None, n_gen=None) -> Batch:
+    """Seeded synthetic batch.  n_mod / n_gen: explicit per-microbatch row counts
+    (edge cases: 0 modality rows, n_mod = S -- no text rows --, fewer generator rows
+    than ranks, modality and generator rows overlapping) instead of the laws."""
     seed = cfg.data_seed if seed is None else seed
     M = cfg.M if M is None else M
     rng = np.random.Generator(np.random.PCG64(seed))
-    n_mod = _draw_counts(rng, cfg.n_mod_law, M, cfg.S)
-    n_gen = _draw_counts(rng, cfg.n_gen_law, M, cfg.S)
+    drawn_mod = _draw_counts(rng, cfg.n_mod_law, M, cfg.S)
+    drawn_gen = _draw_counts(rng, cfg.n_gen_law, M, cfg.S)
+    n_mod = drawn_mod if n_mod is None else np.asarray(n_mod, np.int64)
+    n_gen = drawn_gen if n_gen is None else np.asarray(n_gen, np.int64)
+    assert len(n_mod) == M and len(n_gen) == M
+    assert all(0 <= x <= cfg.S for x in n_mod) and all(1 <= x <= cfg.S for x in n_gen)
     patches, targets = [], []
     ids = np.empty((M, cfg.S), np.int32)
     labels = np.empty((M, cfg.S), np.int32)
@@ -131,6 +138,23 @@ def make_batch(cfg: ModelShape, seed: int | None = None, M: int | None = None) -
         labels[m] = rng.integers(0, cfg.vocab, size=cfg.S)
         targets.append(bf16_round(rng.standard_normal((int(n_gen[m]), cfg.d_t), dtype=np.float32)))
     return Batch(n_mod=n_mod, n_gen=n_gen, patches=patches, ids=ids, labels=labels, targets=targets)
+
+
+def edge_counts(cfg: ModelShape, M: int):
+    """The method's degenerate row counts, cycled over M microbatches: no modality
+    rows, modality rows filling the sequence (no CE rows), a few modality rows with
+    the generator reading the whole sequence (modality, CE and generator rows
+    overlap), fewer generator rows than a 4-stage pipeline has ranks (empty
+    generator shards).  Returns (n_mod, n_gen)."""
+    S = cfg.S
+    mods = [0, S, 17, 60]
+    gens = [1, 3, S, 2]
+    return [mods[m % 4] for m in range(M)], [gens[m % 4] for m in range(M)]
+
+
+def edge_shape(cfg: ModelShape) -> ModelShape:
+    """cfg with row-count laws spanning [0, S] so the buffers admit every edge count."""
+    return cfg.replace(n_mod_law=("uniform", 0, cfg.S), n_gen_law=("uniform", 1, cfg.S))
 
 
 def slice_batch(b: Batch, lo: int, hi: int) -> Batch:

@@ -21,7 +21,7 @@ import torch.distributed as dist
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
-from synth import get_config, make_batch, make_weights, slice_batch  # noqa: E402
+from synth import edge_counts, edge_shape, get_config, make_batch, make_weights, slice_batch  # noqa: E402
 
 
 def main():
@@ -30,12 +30,23 @@ def main():
     rank = int(os.environ["RANK"])
     world = int(os.environ["WORLD_SIZE"])
     assert world == P * D, (world, P, D)
-    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", rank)))
+    # BM_TEST_ONE_GPU=1: every rank on cuda:0 (the single-GPU multi-rank fixture: CUDA
+    # IPC works between processes of one device; the step-end sums then run over peer
+    # memory, bm_ctx_init_peer_sum, because NCCL rejects duplicate devices)
+    one_gpu = os.environ.get("BM_TEST_ONE_GPU") == "1"
+    torch.cuda.set_device(0 if one_gpu else int(os.environ.get("LOCAL_RANK", rank)))
     dist.init_process_group("gloo")
     from paper_2605_25451_b200.runtime import Runtime
+    edge = "edge" in gen.split("+")
+    gen = "+".join(t for t in gen.split("+") if t != "edge")
     cfg = get_config(name, P=P, M=M, V=V)
     cfg_global = get_config(name, P=P, M=M * D, V=V)
-    W, B_global = make_weights(cfg), make_batch(cfg_global)
+    if edge:   # degenerate row counts (synth.edge_counts), buffers sized for [0, S]
+        cfg, cfg_global = edge_shape(cfg), edge_shape(cfg_global)
+        n_mod, n_gen = edge_counts(cfg_global, M * D)
+        W, B_global = make_weights(cfg), make_batch(cfg_global, n_mod=n_mod, n_gen=n_gen)
+    else:
+        W, B_global = make_weights(cfg), make_batch(cfg_global)
     replica = rank // P
     B = slice_batch(B_global, replica * M, (replica + 1) * M)
     # strategy spec: "<gen_place>", "entry_stage+<gen_place>" (memory-efficient baseline),
@@ -102,7 +113,7 @@ def main():
         if missing:
             print("missing grads", missing)
             ok = False
-        print("PARITY OK" if ok else "PARITY FAIL", loss, loss_ref)
+        print("PARITY OK" if ok else "PARITY FAIL", loss, loss_ref, "sum_mode", rt.sum_mode)
     dist.barrier()
     rt.close()
     dist.destroy_process_group()

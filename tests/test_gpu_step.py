@@ -2,7 +2,8 @@
 against the fp64 oracle: loss, per-microbatch loss terms and every parameter
 gradient, normwise relative error <= 1e-4 (fp32) / 2e-2 (bf16) -- the
 tolerances north_star fixes.  Single-GPU cases run the P = 1 pipeline; the
-multi-GPU cases (P = 2, 4) launch one process per GPU via torchrun."""
+multi-rank cases (P = 2, 4, replicas) launch one process per rank via torchrun --
+one per GPU when the box has enough GPUs, else all on cuda:0 (_torchrun)."""
 import os
 import subprocess
 import sys
@@ -30,6 +31,18 @@ def oracle_cache():
     return {}
 
 
+@pytest.fixture
+def gemm_mode(request):
+    """bm_k_gemm_mode for the test: 0 = auto (C1 sizes take the 1-CTA kernels),
+    2 = CTA pairs everywhere -- the kernels the C2 / C4 bench runs for the LLM
+    contractions (pair DSWIGLU down dgrad, pair reduce-add wgrad, pair residual add)."""
+    from paper_2605_25451_b200 import _lib as L
+    mode = getattr(request, "param", 0)
+    L.call("bm_k_gemm_mode", mode)
+    yield mode
+    L.call("bm_k_gemm_mode", 0)
+
+
 def reference(cache, cfg):
     key = (cfg.P, cfg.M, cfg.V, cfg.name)
     if key not in cache:
@@ -38,9 +51,9 @@ def reference(cache, cfg):
     return cache[key]
 
 
-@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("dtype,gemm_mode", [("f32", 0), ("bf16", 0), ("bf16", 2)], indirect=["gemm_mode"])
 @pytest.mark.parametrize("M,V", [(4, 1), (4, 2), (1, 1), (6, 1)])
-def test_step_single_gpu(oracle_cache, dtype, M, V):
+def test_step_single_gpu(oracle_cache, dtype, M, V, gemm_mode):
     from paper_2605_25451_b200.runtime import Runtime
     cfg = get_config("C1", P=1, M=M, V=V)
     W, B, (loss_ref, per_ref, G_ref) = reference(oracle_cache, cfg)
@@ -134,6 +147,32 @@ def test_step_single_gpu_uneven_partition(oracle_cache, dtype):
     rt.close()
 
 
+@pytest.mark.parametrize("cfg_name", ["C1", "C1M"])
+@pytest.mark.parametrize("dtype,gemm_mode", [("f32", 0), ("bf16", 0), ("bf16", 2)], indirect=["gemm_mode"])
+def test_step_edge_batches_single_gpu(cfg_name, dtype, gemm_mode):
+    """Degenerate microbatches (synth.edge_counts): n_mod = 0, n_mod = S (no CE rows),
+    generator rows spanning the sequence (overlapping modality and CE rows)."""
+    from synth import edge_counts, edge_shape
+    from paper_2605_25451_b200.runtime import Runtime
+    cfg = edge_shape(get_config(cfg_name, P=1, M=4, V=1))
+    n_mod, n_gen = edge_counts(cfg, 4)
+    W, B = make_weights(cfg), make_batch(cfg, n_mod=n_mod, n_gen=n_gen)
+    loss_ref, per_ref, G_ref = om.step_fp64(cfg, W, B)
+    rt = Runtime(cfg, dtype)
+    rt.load_weights(W)
+    rt.step(rt.device_batch(B))
+    torch.cuda.synchronize()
+    loss, ce, mse = rt.losses()
+    tol = TOL[dtype]
+    assert abs(loss - loss_ref) <= tol * abs(loss_ref)
+    assert ce[1] == 0.0   # n_mod = S: no CE rows
+    assert rel(ce, np.array([a for a, _ in per_ref])) <= tol
+    assert rel(mse, np.array([b for _, b in per_ref])) <= tol
+    bad = {n: rel(rt.grad(n), G_ref[n]) for n in rt.names()}
+    assert not {k: v for k, v in bad.items() if v > tol}, bad
+    rt.close()
+
+
 def test_trace_records_every_op():
     """bm_ctx_trace_get: one record per compute op / receive (+ the tail), in the
     rank's op order on each stream, with non-decreasing times; tracing does not
@@ -164,9 +203,9 @@ def test_trace_records_every_op():
     rt.close()
 
 
-@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("dtype,gemm_mode", [("f32", 0), ("bf16", 0), ("bf16", 2)], indirect=["gemm_mode"])
 @pytest.mark.parametrize("M,V", [(4, 1), (4, 2)])
-def test_step_single_gpu_medium(oracle_cache, dtype, M, V):
+def test_step_single_gpu_medium(oracle_cache, dtype, M, V, gemm_mode):
     # C1M: several tiles per GEMM dimension, ragged row counts (60..200 modality rows)
     from paper_2605_25451_b200.runtime import Runtime
     cfg = get_config("C1M", P=1, M=M, V=V)
@@ -184,11 +223,20 @@ def test_step_single_gpu_medium(oracle_cache, dtype, M, V):
     rt.close()
 
 
-def _torchrun(nproc, *args, timeout=600):
+def _torchrun(nproc, *args, timeout=600, env=None):
+    """Launch mp_step.py on nproc ranks.  With fewer GPUs than ranks every rank runs
+    on cuda:0 (BM_TEST_ONE_GPU=1): stage-boundary copies, credit rings, gather /
+    scatter handoffs go through CUDA IPC within the device, and the step-end sums
+    through the library's peer-memory reduce (NCCL rejects duplicate GPUs), so the
+    cross-rank half of the step is verified on a 1-GPU box too."""
+    e = dict(os.environ)
+    if torch.cuda.device_count() < nproc:
+        e["BM_TEST_ONE_GPU"] = "1"
+    e.update(env or {})
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
            "--master-addr", "127.0.0.1", "--master-port", str(29500 + nproc), os.path.join(ROOT, "tests", "mp_step.py"),
            *map(str, args)]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout, cwd=ROOT)
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout, cwd=ROOT, env=e)
     assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-4000:]
     return r.stdout
 
@@ -198,18 +246,15 @@ def _torchrun(nproc, *args, timeout=600):
                                            (2, 4, 1, "f32", "dp_shard+head_dp"), (2, 8, 2, "bf16", "dp_shard+head_dp"),
                                            (2, 4, 1, "f32", "dp_shard+last1"), (2, 4, 1, "bf16", "dp_shard+last3"), (2, 4, 1, "f32", "dp_shard+split1-3"),
                                            (2, 4, 1, "f32", "entry_stage+last_stage"),
-                                           (2, 4, 1, "bf16", "ce")])
+                                           (2, 4, 1, "bf16", "ce"), (2, 4, 1, "bf16", "dp_shard+edge"),
+                                           (2, 8, 2, "f32", "dp_shard+edge")])
 def test_step_two_gpus(P, M, V, dtype, gen):
-    if torch.cuda.device_count() < P:
-        pytest.skip(f"needs {P} GPUs")
     out = _torchrun(P, "C1", P, M, V, dtype, gen)
     assert "PARITY OK" in out, out
 
 
 @pytest.mark.parametrize("cfg_name,P,M,V,dtype", [("C1M", 2, 4, 1, "bf16"), ("C1M", 2, 4, 2, "f32")])
 def test_step_two_gpus_medium(cfg_name, P, M, V, dtype):
-    if torch.cuda.device_count() < P:
-        pytest.skip(f"needs {P} GPUs")
     out = _torchrun(P, cfg_name, P, M, V, dtype, "dp_shard")
     assert "PARITY OK" in out, out
 
@@ -217,12 +262,11 @@ def test_step_two_gpus_medium(cfg_name, P, M, V, dtype):
 @pytest.mark.parametrize("P,M,V,dtype,gen", [(4, 8, 1, "f32", "dp_shard"), (4, 8, 1, "bf16", "dp_shard"),
                                            (4, 16, 1, "bf16", "dp_shard"), (4, 16, 1, "bf16", "ce"),
                                            (4, 16, 1, "f32", "entry_stage+last_stage"), (4, 16, 1, "f32", "ce"),
-                                           (4, 8, 1, "bf16", "dp_shard+head_dp")])
+                                           (4, 8, 1, "bf16", "dp_shard+head_dp"), (4, 4, 1, "f32", "dp_shard+edge"),
+                                           (4, 8, 1, "bf16", "dp_shard+edge"), (4, 8, 1, "bf16", "last_stage+edge")])
 def test_step_four_gpus(P, M, V, dtype, gen):
     # "ce" (W = M / P) once deadlocked: a copy-engine send parked on a credit wait
     # blocked another stream's copy in a shared copy channel
-    if torch.cuda.device_count() < P:
-        pytest.skip(f"needs {P} GPUs")
     out = _torchrun(P, "C1", P, M, V, dtype, gen, timeout=240)
     assert "PARITY OK" in out, out
 
@@ -230,15 +274,27 @@ def test_step_four_gpus(P, M, V, dtype, gen):
 @pytest.mark.parametrize("P,D,M,V,dtype", [(1, 2, 4, 1, "f32"), (1, 2, 4, 1, "bf16")])
 def test_step_replicas_two_gpus(P, D, M, V, dtype):
     # D pipeline replicas: DP params over all processes, LLM params per stage
-    if torch.cuda.device_count() < P * D:
-        pytest.skip(f"needs {P * D} GPUs")
     out = _torchrun(P * D, "C1", P, M, V, dtype, "dp_shard", D)
     assert "PARITY OK" in out, out
 
 
 @pytest.mark.parametrize("P,D,M,V,dtype", [(2, 2, 4, 1, "f32"), (2, 2, 4, 1, "bf16"), (2, 2, 8, 2, "f32")])
 def test_step_replicas_four_gpus(P, D, M, V, dtype):
-    if torch.cuda.device_count() < P * D:
-        pytest.skip(f"needs {P * D} GPUs")
     out = _torchrun(P * D, "C1", P, M, V, dtype, "dp_shard", D, timeout=300)
+    assert "PARITY OK" in out, out
+
+
+@pytest.mark.parametrize("P,D,M,V,dtype,gen", [(2, 1, 4, 1, "f32", "dp_shard"), (2, 2, 4, 1, "f32", "dp_shard")])
+def test_step_peer_sum_forced(P, D, M, V, dtype, gen):
+    """The library's peer-memory step-end sum (bm_ctx_init_peer_sum) also on
+    distinct GPUs (BM_STEP_SUM=peer), where NCCL would otherwise be used."""
+    out = _torchrun(P * D, "C1", P, M, V, dtype, gen, D, env={"BM_STEP_SUM": "peer"})
+    assert "PARITY OK" in out and "sum_mode peer" in out, out
+
+
+@pytest.mark.parametrize("P,D,M,V,dtype", [(2, 1, 4, 1, "bf16"), (2, 1, 8, 2, "bf16"), (2, 2, 4, 1, "bf16")])
+def test_step_multirank_cta_pairs(P, D, M, V, dtype):
+    """BM_GEMM_MODE=2: every bf16 contraction on the CTA-pair kernel (the bench's
+    LLM path) across the stage boundaries and replicas."""
+    out = _torchrun(P * D, "C1M", P, M, V, dtype, "dp_shard", D, env={"BM_GEMM_MODE": "2"})
     assert "PARITY OK" in out, out

@@ -83,7 +83,8 @@ def _replica_worker(rank, world, P, port, q):
         def new_id():
             cnt[0] += 1
             return f"id-{rank}-{cnt[0]}".encode()
-        peers, ids = exchange(None, P, world // P, rank, f"ipc-{rank}", new_id)
+        peers, ids, allp = exchange(None, P, world // P, rank, f"ipc-{rank}", new_id)
+        assert allp == [f"ipc-{g}" for g in range(world)], allp
         got = [None] * world
         dist.all_gather_object(got, (peers, ids))
         dist.barrier()
@@ -121,3 +122,18 @@ def test_replica_exchange_groups(world, P):
         assert len({got[k * P][1]["pipe"] for k in range(D)}) == D
     if D > 1:
         assert len({got[s][1]["stage"] for s in range(P)}) == P
+
+
+def test_sum_mode_selection(monkeypatch):
+    """Step-end sums: NCCL when every process owns a GPU, the library's peer-memory
+    sum when two processes share one (NCCL rejects duplicate devices), forced by
+    BM_STEP_SUM."""
+    from paper_2605_25451_b200.runtime import sum_mode
+    monkeypatch.delenv("BM_STEP_SUM", raising=False)
+    assert sum_mode(["a", "b", "c", "d"]) == "nccl"
+    assert sum_mode(["a", "a"]) == "peer"
+    assert sum_mode(["a", "b", "a", "b"]) == "peer"
+    monkeypatch.setenv("BM_STEP_SUM", "peer")
+    assert sum_mode(["a", "b"]) == "peer"
+    monkeypatch.setenv("BM_STEP_SUM", "nccl")
+    assert sum_mode(["a", "a"]) == "nccl"

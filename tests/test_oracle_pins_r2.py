@@ -506,3 +506,41 @@ def test_interpreter_on_bench_schedules(P, M, V, L):
     assert abs(loss2 - loss) <= 1e-12 * abs(loss)
     for k in G:
         assert np.linalg.norm(G2[k] - G[k]) <= 1e-12 * max(np.linalg.norm(G[k]), 1e-30), k
+
+
+# =========================================================================== degenerate batches
+@pytest.mark.parametrize("P,M,V", [(1, 4, 1), (4, 4, 1), (2, 8, 2)])
+def test_edge_batches_interpreter_and_closed_forms(P, M, V):
+    # the method's degenerate microbatches (synth.edge_counts): n_mod = 0, n_mod = S (no
+    # CE rows: CE_m = 0 by reading R8's mean over an empty set), generator rows covering
+    # the whole sequence, n_gen < P (empty generator shards); the interpreter (per-rank
+    # shards, gather / scatter of empty messages) equals the sequential definition
+    from synth import edge_counts, edge_shape, get_config, make_batch, make_weights
+    from oracle import interp
+    from oracle import model as om
+    cfg = edge_shape(get_config("C1", P=P, M=M, V=V))
+    n_mod, n_gen = edge_counts(cfg, M)
+    W, B = make_weights(cfg), make_batch(cfg, n_mod=n_mod, n_gen=n_gen)
+    loss, per, G = om.step_fp64(cfg, W, B)
+    for m in range(M):
+        if n_mod[m] == cfg.S:
+            assert per[m][0] == 0.0
+    assert all(np.isfinite(v).all() for v in G.values())
+    sched = S.build(S.SchedCfg(P, M, V, llm_sched=cfg.llm_sched))
+    loss2, per2, G2, _ = interp.run(sched, cfg, W, B)
+    assert abs(loss2 - loss) <= 1e-12 * abs(loss)
+    for k in G:
+        assert np.linalg.norm(G2[k] - G[k]) <= 1e-12 * max(np.linalg.norm(G[k]), 1e-30), k
+
+
+def test_no_modality_rows_gives_zero_encoder_gradients():
+    # with n_mod = 0 in every microbatch the encoder and projector never touch the loss:
+    # their gradients are exactly zero (the embedding is all text rows)
+    from synth import edge_shape, get_config, make_batch, make_weights
+    from oracle import model as om
+    cfg = edge_shape(get_config("C1", P=1, M=2))
+    W, B = make_weights(cfg), make_batch(cfg, n_mod=[0, 0], n_gen=[5, 9])
+    _, _, G = om.step_fp64(cfg, W, B)
+    for k, v in G.items():
+        if k.startswith("enc."):
+            assert not np.any(v), k
