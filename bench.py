@@ -116,31 +116,6 @@ class ClockSampler:
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def cpu_oracle_sample(cfg, rows=512, repeats=1):
-    """Time the fp64 oracle on a bounded sample: one LLM layer fwd+bwd on `rows`
-    rows of one microbatch at the workload's (d, f).  Returns (sec, flops, cores)."""
-    import numpy as np
-    from oracle import model as om
-    try:
-        from threadpoolctl import threadpool_info
-        cores = max([i.get("num_threads", 1) for i in threadpool_info()] or [1])
-    except Exception:
-        cores = os.cpu_count() or 1
-    rng = np.random.default_rng(0)
-    W = {"llm.layer0.norm": np.ones(cfg.d),
-         "llm.layer0.gate_up": rng.standard_normal((2 * cfg.f, cfg.d)) * 0.02,
-         "llm.layer0.down": rng.standard_normal((cfg.d, cfg.f)) * 0.02}
-    x = rng.standard_normal((rows, cfg.d))
-    dy = rng.standard_normal((rows, cfg.d))
-    t0 = time.perf_counter()
-    for _ in range(repeats):
-        y, caches = om.llm_layers_fwd(W, cfg, [0], x)
-        G = {}
-        om.llm_layers_bwd(W, cfg, [0], caches, dy, G)
-    dt = (time.perf_counter() - t0) / repeats
-    return dt, 18.0 * rows * cfg.d * cfg.f, cores
-
-
 def stages_of(args, N):
     P = args.stages or min(N, 4)
     if N % P:
@@ -226,7 +201,8 @@ def head_place_name(args, N):
 
 
 def run_reference(args):
-    """The oracle as it stands, on the host cores (the reference arm for this tier)."""
+    """The oracle as it stands, on the host cores (the reference arm for this tier):
+    each step one bounded sample (oracle_microbatch_sample) of the workload."""
     rank = int(os.environ.get("RANK", "0"))
     N = args.gpus
     if rank != 0:
@@ -234,19 +210,19 @@ def run_reference(args):
     cfg, P, D = workload(args, N)
     batch = global_batch(cfg, D)
     F = step_flops(cfg, batch.n_mod, batch.n_gen)
-    rows = args.ref_rows
-    for _ in range(args.warmup):
-        cpu_oracle_sample(cfg, rows)
+    from synth import get_config
+    for _ in range(args.warmup):   # untimed: warms the interpreter / BLAS on a small case
+        oracle_microbatch_sample(get_config("C1"), 1, 1)
     ts = []
     for _ in range(args.steps):
-        dt, fl, cores = cpu_oracle_sample(cfg, rows)
+        dt, fl, cores = oracle_microbatch_sample(cfg, args.ref_layers, args.ref_seq_div)
         ts.append((dt, fl))
     sec = sum(t for t, _ in ts)
     flops = sum(f for _, f in ts)
-    rate = flops / sec
-    value = rate / (F / (cfg.M * D))
-    sample = (f"per step: oracle (numpy fp64) fwd+bwd of one LLM layer on {rows} rows of a {cfg.name} microbatch "
-              f"(d={cfg.d}, f={cfg.f}); samples/s extrapolated by the step's algorithmic FLOPs per sample")
+    value = flops / sec / (F / (cfg.M * D))
+    sample = (f"per step: oracle (numpy fp64 step_fp64) fwd+bwd of one {cfg.name} microbatch with "
+              f"{args.ref_layers} of {cfg.L} LLM layers and S/{args.ref_seq_div} positions; samples/s scaled by the step's "
+              f"algorithmic FLOPs per sample")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": N,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * sec / args.steps,
             "higher_is_better": True, "scaling": "strong" if args.microbatches else "weak", "vs_baseline": None,
@@ -255,6 +231,226 @@ def run_reference(args):
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def oracle_microbatch_sample(cfg, layers=1, seq_div=2):
+    """The oracle as it stands on a bounded sample of the workload: one microbatch
+    (encoder, embed, LLM, final norm, LM head + CE, generator + MSE, and the whole
+    backward) of the workload's widths with `layers` LLM layers instead of L and
+    S / seq_div sequence positions.  Returns (seconds, algorithmic FLOPs of the
+    sample, cores)."""
+    from synth import make_batch, make_weights
+    from oracle import model as om
+    try:
+        from threadpoolctl import threadpool_info
+        cores = max([i.get("num_threads", 1) for i in threadpool_info()] or [1])
+    except Exception:
+        cores = os.cpu_count() or 1
+    scfg = cfg.replace(L=layers, M=1, P=1, V=1, llm_sched="1f1b", S=cfg.S // seq_div)
+    W, B = make_weights(scfg), make_batch(scfg)
+    t0 = time.perf_counter()
+    om.step_fp64(scfg, W, B)
+    dt = time.perf_counter() - t0
+    return dt, step_flops(scfg, B.n_mod, B.n_gen), cores
+
+
+def step_hbm_bytes(cfg, n_mod, n_gen, es=2):
+    """Algorithmic HBM bytes of one step, summed over all GPUs:
+    every kernel reads its inputs and writes its outputs once; weights are read
+    once per microbatch and fwd / bwd pass, fp32 weight gradients are read-modified-
+    written once per microbatch (TMA reduce-add).  Per microbatch and LLM layer:
+      fwd  norm (x -> xn) 2Sd; gate_up (xn, W -> gu, h) S(d + 3f) + 2df;
+           down (h, W, x -> x') S(f + 2d) + df                         (x es)
+      bwd  down dgrad+dswiglu (dy, W, gu -> dgu) S(d + 4f) + df; down wgrad
+           (dy, h) S(d + f) + 8df/es; gate_up dgrad (dgu, W -> dxn) S(2f + d) + 2df;
+           gate_up wgrad (dgu, xn) S(2f + d) + 16df/es; norm bwd (dxn, x, dres -> dx) 4Sd
+    plus the LM head (logits written and read twice by CE fwd+bwd) on the text rows
+    and the encoder / generator blocks on their rows (same per-row counts)."""
+    S, d, f, L, V = cfg.S, cfg.d, cfg.f, cfg.L, cfg.vocab
+    tot = 0.0
+    for nm, ng in zip(n_mod, n_gen):
+        per_layer = (2 * S * d + S * (d + 3 * f) + 2 * d * f + S * (f + 2 * d) + d * f +
+                     S * (d + 4 * f) + d * f + S * (d + f) + 8 * d * f / es + S * (2 * f + d) + 2 * d * f +
+                     S * (2 * f + d) + 16 * d * f / es + 4 * S * d) * es
+        nt = S - nm
+        head = (nt * d + V * d + 3 * nt * V + nt * d + V * d + nt * d + 2 * V * d * 4 / es) * es
+        def mlp(n, dm, fm, Lb):
+            return Lb * (2 * n * dm + n * (dm + 2 * fm) + 2 * dm * fm + n * (fm + 2 * dm)) * 3 * es
+        enc = mlp(nm, cfg.d_e, cfg.f_e, cfg.L_e) + 3 * nm * (cfg.d_in + cfg.d_e + 2 * d) * es
+        gen = mlp(ng, cfg.d_g, cfg.f_g, cfg.L_g) + 3 * ng * (d + cfg.d_g + cfg.d_t) * es
+        tot += L * per_layer + head + enc + gen + 2 * S * d * es   # + embedding gather / scatter
+    return tot
+
+
+def bubble_from_trace(recs):
+    """Compute-stream (LLM) idle fraction of one traced step on one rank:
+    1 - |union of compute-op intervals on stream 0| / step span (origin -> tail end)."""
+    end = max((x["t1"] for x in recs), default=0.0)
+    iv = sorted((x["t0"], x["t1"]) for x in recs if x["stream"] == 0 and x["kind"] not in ("Tail", "Recv"))
+    busy, cur0, cur1 = 0.0, None, None
+    for a, b in iv:
+        if cur1 is None or a > cur1:
+            if cur1 is not None:
+                busy += cur1 - cur0
+            cur0, cur1 = a, b
+        else:
+            cur1 = max(cur1, b)
+    if cur1 is not None:
+        busy += cur1 - cur0
+    return (1.0 - busy / end) if end > 0 else None, end
+
+
+class Ctx:
+    """Process-group helpers (gloo side group; device timing stays on CUDA events)."""
+
+    def __init__(self, world, group):
+        self.world, self.group = world, group
+
+    def barrier(self):
+        if self.world > 1:
+            import torch.distributed as dist
+            dist.barrier(group=self.group)
+
+    def reduce(self, v, op):
+        if self.world == 1:
+            return v
+        import torch
+        import torch.distributed as dist
+        t = torch.tensor([float(v)], dtype=torch.float64)
+        dist.all_reduce(t, op=op, group=self.group)
+        return float(t.item())
+
+    def max(self, v):
+        import torch.distributed as dist
+        return self.reduce(v, dist.ReduceOp.MAX)
+
+    def sum(self, v):
+        import torch.distributed as dist
+        return self.reduce(v, dist.ReduceOp.SUM)
+
+    def gather(self, obj):
+        if self.world == 1:
+            return [obj]
+        import torch.distributed as dist
+        out = [None] * self.world
+        dist.all_gather_object(out, obj, group=self.group)
+        return out
+
+
+def make_runtime(args, cfg, P, rank, world, group, strategy="bigmac"):
+    from paper_2605_25451_b200.runtime import Runtime
+    W = args.warmup_units if args.warmup_units >= 0 else (2 if P == 1 else 0)
+    sched_kw = {"bigmac": {"warmup_units": W}, "compute_efficient": {"warmup_units": cfg.M // P},
+                "memory_efficient": {"enc_place": "entry_stage", "gen_place": "last_stage"}}[strategy]
+    split = stage_split(args, cfg, P)
+    n_last = 0 if split else last_stage_layers(args, cfg, P)
+    rt = Runtime(cfg, args.dtype, rank=rank, world=world, group=group, sched_kw=sched_kw, head_place=args.head,
+                 last_stage_layers=n_last, stage_layers=split)
+    rt.init_random_weights(seed=1)
+    return rt, W, split, n_last
+
+
+def timed_steps(rt, db, cx, steps, warmup):
+    """W untimed steps, then `steps` steps between CUDA events on the caller's stream,
+    barrier + synchronize on both sides; returns max-over-ranks milliseconds."""
+    import torch
+    stream = torch.cuda.current_stream()
+    for _ in range(warmup):
+        rt.step(db)
+    torch.cuda.synchronize()
+    cx.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        rt.step(db)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    cx.barrier()
+    return cx.max(e0.elapsed_time(e1))
+
+
+def measure_bubble(rt, db, cx, P, cfg):
+    """One traced step (CUDA events around every op): per-rank compute-stream idle
+    fraction against the 1F1B closed form (P - 1) / (M V + P - 1)."""
+    import torch
+    cx.barrier()
+    rt.set_trace(True)
+    rt.step(db)
+    torch.cuda.synchronize()
+    tr = rt.trace()
+    rt.set_trace(False)
+    frac, span = bubble_from_trace(tr)
+    per = cx.gather(frac)
+    return {"measured_max": max(per), "per_rank": per, "bound": (P - 1) / (cfg.M * cfg.V + P - 1),
+            "how": "1 - busy/step of the LLM compute stream from a per-op CUDA-event trace of one step "
+                   "(max over ranks); bound = 1F1B closed form (P-1)/(MV+P-1)"}
+
+
+def free_runtime(rt):
+    import torch
+    rt.close()
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+
+
+def run_secondary(args, cx, rank, world, name, cfg, P, D, steps, warmup, with_bubble=True):
+    """A second configuration in the same process (C4 at N = 1, BASELINE's C2 M = 16 at
+    N > 1): samples/s, step roofline, bubble, peak HBM."""
+    import torch
+    from synth import slice_batch
+    torch.cuda.empty_cache()
+    torch.cuda.reset_peak_memory_stats()
+    rt, W, split, n_last = make_runtime(args, cfg, P, rank, world, cx.group)
+    gbatch = global_batch(cfg, D)
+    replica = rank // P
+    db = rt.device_batch(slice_batch(gbatch, replica * cfg.M, (replica + 1) * cfg.M))
+    ms = timed_steps(rt, db, cx, steps, warmup)
+    out = {"workload": config_dict(cfg, P, D)["workload"], "global_batch": cfg.M * D, "steps": steps,
+           "warmup": warmup, "ms_per_step": ms / steps, "value": cfg.M * D * steps / (ms / 1e3), "unit": UNIT,
+           "tokens_per_s": cfg.M * D * cfg.S * steps / (ms / 1e3)}
+    peaks, _ = load_peaks()
+    F = step_flops(cfg, gbatch.n_mod, gbatch.n_gen)
+    t_roof = F / (world * peaks["bf16_tflops"] * 1e12) * 1e3
+    out["step_roofline"] = {"flops_per_step": F, "t_roof_ms": t_roof, "frac": t_roof / (ms / steps)}
+    if with_bubble:
+        out["bubble"] = measure_bubble(rt, db, cx, P, cfg)
+    out["peak_hbm_gb_per_gpu"] = cx.max(torch.cuda.max_memory_allocated()) / 1e9
+    out["stash_peak_bytes_rank0_enc_llm_gen"] = rt.stash_peak()
+    out["config"] = {"stages": P, "replicas": D, "microbatches": cfg.M, "warmup_units": W, "stage_layers": split,
+                     "last_stage_layers": n_last}
+    free_runtime(rt)
+    del db
+    return out
+
+
+def run_sweep(args, cx, rank, world, P, ms_list):
+    """Peak HBM per GPU and samples/s vs global batch (C5's claim: the
+    encoder / generator stash is fixed by the schedule -- W units, one generator shard --
+    and the LLM in-flight depth by 1F1B, so peak HBM grows only with the resident inputs)."""
+    import torch
+    from synth import get_config, make_batch
+    out = []
+    for M in ms_list:
+        if M % P:
+            continue
+        cfg = get_config(args.config, P=P, M=M, V=1)
+        torch.cuda.empty_cache()
+        torch.cuda.reset_peak_memory_stats()
+        rt, W, _, _ = make_runtime(args, cfg, P, rank, world, cx.group)
+        mem0 = torch.cuda.memory_allocated()
+        db = rt.device_batch(make_batch(cfg))
+        batch_bytes = torch.cuda.memory_allocated() - mem0
+        ms = timed_steps(rt, db, cx, 1, 1)
+        st = rt.sched.stats(rt.rank)
+        out.append({"M": M, "global_batch": M, "samples_per_s": M / (ms / 1e3), "ms_per_step": ms,
+                    "peak_hbm_gb_per_gpu": cx.max(torch.cuda.max_memory_allocated()) / 1e9,
+                    "resident_input_gb_rank0": cx.max(batch_bytes if rank == 0 else 0) / 1e9,
+                    "stash_peak_bytes_rank0_enc_llm_gen": rt.stash_peak(), "peak_enc_units": st.peak_enc_units,
+                    "peak_llm_inflight": st.peak_llm_inflight, "peak_gen_shards": st.peak_gen_shards})
+        free_runtime(rt)
+        del db
+    return out
 
 
 def main():
@@ -275,7 +471,12 @@ def main():
     ap.add_argument("--dtype", default="bf16")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--ref-rows", type=int, default=512)
+    ap.add_argument("--no-extra", action="store_true", help="skip the secondary config (C4 at N = 1, M = 16 per "
+                                                             "replica at N > 1) and the batch sweep")
+    ap.add_argument("--sweep", default="8,16,32,64,128,256", help="global batches of the peak-HBM sweep ('' = off)")
+    ap.add_argument("--c4-steps", type=int, default=2)
+    ap.add_argument("--ref-layers", type=int, default=1, help="LLM layers of the oracle sample")
+    ap.add_argument("--ref-seq-div", type=int, default=2, help="the oracle sample runs S / this positions")
     ap.add_argument("--head", default="auto", choices=["auto", "last_stage", "dp_shard"],
                     help="LM head + CE placement (bigmac.h bm_head_place): auto = last_stage (the paper's "
                          "Megatron placement), dp_shard = DP-sharded with the generator")
@@ -299,43 +500,18 @@ def main():
     if world > 1:
         dist.init_process_group("cpu:gloo,cuda:nccl", device_id=torch.device("cuda", local))
         group = dist.new_group(backend="gloo")
+    cx = Ctx(world, group)
 
-    from synth import slice_batch
-    from paper_2605_25451_b200.runtime import Runtime
+    from synth import get_config, slice_batch
     cfg, P, D = workload(args, N)
     if args.warmup < 3:
         raise SystemExit("--warmup must be >= 3")
-    W = args.warmup_units if args.warmup_units >= 0 else (2 if P == 1 else 0)
-    sched_kw = {"bigmac": {"warmup_units": W}, "compute_efficient": {"warmup_units": cfg.M // P},
-                "memory_efficient": {"enc_place": "entry_stage", "gen_place": "last_stage"}}[args.strategy]
-    split = stage_split(args, cfg, P)
-    n_last = 0 if split else last_stage_layers(args, cfg, P)
-    rt = Runtime(cfg, args.dtype, rank=rank, world=world, group=group, sched_kw=sched_kw, head_place=args.head,
-                 last_stage_layers=n_last, stage_layers=split)
-    rt.init_random_weights(seed=1)
+    rt, W, split, n_last = make_runtime(args, cfg, P, rank, world, group, args.strategy)
     gbatch = global_batch(cfg, D)
     replica = rank // P
     batch = slice_batch(gbatch, replica * cfg.M, (replica + 1) * cfg.M)
     db = rt.device_batch(batch)
     stream = torch.cuda.current_stream()
-
-    def barrier():
-        if world > 1:
-            dist.barrier(group=group)
-
-    def max_over_ranks(v):
-        if world == 1:
-            return v
-        t = torch.tensor([v], dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
-        return float(t.item())
-
-    def sum_over_ranks(v):
-        if world == 1:
-            return v
-        t = torch.tensor([v], dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
-        return float(t.item())
 
     # ---------------- warmup
     for _ in range(args.warmup):
@@ -351,19 +527,17 @@ def main():
     clk = ClockSampler(uuid)
     clk.start()
     time.sleep(0.3)
-    barrier()
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(args.steps):
-        rt.step(db)
-    e1.record(stream)
-    torch.cuda.synchronize()
-    barrier()
+    ms_max = timed_steps(rt, db, cx, args.steps, 0)
     clocks = clk.stop()
-    ms = e0.elapsed_time(e1)
     launches = rt.launch_count() * args.steps
-    # instrumented pass (not part of `value`): a CUDA-event pair around every GEMM
+    ms_per_step = ms_max / args.steps
+    samples = cfg.M * D * args.steps
+    value = samples / (ms_max / 1000.0)
+    loss, _, _ = rt.losses()
+    peak_alloc = cx.max(float(torch.cuda.max_memory_allocated()))
+    stash = rt.stash_peak()
+
+    # instrumented passes (not part of `value`): a CUDA-event pair around every GEMM
     # launch and every NVLink copy, on the stream each runs on -> roofline + NVLink
     rt.set_timing(True)
     n_inst = max(2, min(args.steps, 5))
@@ -373,14 +547,7 @@ def main():
     n_gemm, gemm_flops, gemm_ms = rt.gemm_stats()
     n_msgs, comm_bytes, comm_ms = rt.comm_stats()
     rt.set_timing(False)
-    barrier()
-    ms_max = max_over_ranks(ms)
-    ms_per_step = ms_max / args.steps
-    samples = cfg.M * D * args.steps
-    value = samples / (ms_max / 1000.0)
-    loss, _, _ = rt.losses()
-    peak_alloc = max_over_ranks(float(torch.cuda.max_memory_allocated()))
-    stash = rt.stash_peak()
+    bubble = measure_bubble(rt, db, cx, P, cfg)
 
     # ---------------- end-to-end: host inputs copied in, loss read back, every step
     e2e = None
@@ -390,7 +557,7 @@ def main():
         for _ in range(2):
             rt.step(hb)
             float(lt[2 * cfg.M].item())
-        barrier()
+        cx.barrier()
         torch.cuda.synchronize()
         f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         f0.record(stream)
@@ -399,57 +566,88 @@ def main():
             float(lt[2 * cfg.M].item())   # device -> host read of the step's loss
         f1.record(stream)
         torch.cuda.synchronize()
-        barrier()
-        ems = max_over_ranks(f0.elapsed_time(f1))
-        h2d = sum_over_ranks(hb.h2d_bytes)
+        cx.barrier()
+        ems = cx.max(f0.elapsed_time(f1))
+        h2d = cx.sum(hb.h2d_bytes)
         e2e = {"value": cfg.M * D * args.steps / (ems / 1000.0), "unit": UNIT,
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(4 * world),
                "ms_per_step": ems / args.steps}
 
-    launches_all = int(sum_over_ranks(launches))
-    comm_bytes_all = sum_over_ranks(comm_bytes)
-    comm_ms_all = sum_over_ranks(comm_ms)
-    n_msgs_all = int(sum_over_ranks(n_msgs))
-    gemm_flops_all = sum_over_ranks(gemm_flops)
-    gemm_ms_all = sum_over_ranks(gemm_ms)
-    n_gemm_all = int(sum_over_ranks(n_gemm))
+    launches_all = int(cx.sum(launches))
+    comm_bytes_all = cx.sum(comm_bytes)
+    comm_bytes_max = cx.max(comm_bytes)
+    comm_ms_all = cx.sum(comm_ms)
+    n_msgs_all = int(cx.sum(n_msgs))
+    gemm_flops_all = cx.sum(gemm_flops)
+    gemm_ms_all = cx.sum(gemm_ms)
+    n_gemm_all = int(cx.sum(n_gemm))
+    sum_mode = getattr(rt, "sum_mode", None)
+    free_runtime(rt)
+    del db
+
+    # ---------------- secondary configuration and the batch sweep
+    extra = {}
+    if not args.no_extra:
+        if N == 1:
+            # the largest single-GPU workload: C4 (7B-shaped LLM, S = 8192) at P = 1, M = 64
+            c4 = get_config("C4", P=1, M=64, V=1)
+            extra["c4_single_gpu"] = run_secondary(args, cx, rank, world, "C4", c4, 1, 1, args.c4_steps, 1)
+        elif args.config == "C2" and not args.microbatches:
+            # BASELINE.json configs[1]: 16 microbatches per pipeline (global batch 16 D)
+            c2 = get_config("C2", P=P, M=16, V=1)
+            extra["c2_m16_per_replica"] = run_secondary(args, cx, rank, world, "C2", c2, P, D, max(3, args.steps // 2), 3)
+        if args.sweep:
+            extra["batch_sweep"] = {"config": f"{args.config} model, P = {P}, bigmac, 1 timed step per M",
+                                    "points": run_sweep(args, cx, rank, world, P,
+                                                        [int(x) for x in args.sweep.split(",") if x])}
 
     if rank != 0:
-        if world > 1:
-            dist.barrier(group=group)
-        rt.close()
+        cx.barrier()
         return
 
     peaks, peak_src = load_peaks()
     F = step_flops(cfg, gbatch.n_mod, gbatch.n_gen)
     sustained = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
     achieved = gemm_flops_all / (gemm_ms_all / 1000.0) / 1e12 if gemm_ms_all > 0 else 0.0
-    traffic = None
-    tpath = os.path.join(ROOT, "profiles", "gemm_traffic.json")
-    if os.path.exists(tpath):
-        try:
-            traffic = json.load(open(tpath)).get("dram_bytes_per_launch")
-        except Exception:
-            traffic = None
+    traffic, traffic_src = None, None
+    for tpath in (os.path.join(ROOT, "profiles", "r02", "gemm_traffic.json"),
+                  os.path.join(ROOT, "profiles", "gemm_traffic.json")):
+        if os.path.exists(tpath):
+            try:
+                tj = json.load(open(tpath))
+                traffic, traffic_src = tj.get("dram_bytes_per_launch"), os.path.relpath(tpath, ROOT) + ": " + \
+                    str(tj.get("source", ""))
+                break
+            except Exception:
+                pass
     roofline = {"bound": "tensor", "kernel": "bm::tc::gemm2_kernel / gemm_kernel on the compute stream (tcgen05.mma kind::f16, TMA, TMEM; CTA pairs for the LLM contractions)",
                 "achieved": achieved, "peak": sustained, "unit": "TFLOP/s", "frac": achieved / sustained,
                 "peak_source": f"{peak_src} bf16_tflops_sustained (GEMMs timed inside a long step)",
-                "traffic": traffic, "launches": n_gemm_all,
+                "traffic": traffic, "traffic_source": traffic_src, "launches": n_gemm_all,
                 "gemm_share_of_step": (gemm_ms_all / world / n_inst) / ms_per_step if ms_per_step > 0 else None,
                 "measured_over": f"{n_inst} instrumented steps after the timed region (event pair per GEMM)",
                 "flops_per_launch": gemm_flops_all / max(n_gemm_all, 1),
                 "avg_launch_ms": gemm_ms_all / max(n_gemm_all, 1)}
-    t_roof_ms = F / (N * peaks["bf16_tflops"] * 1e12) * 1e3
+    hbm_all = step_hbm_bytes(cfg, gbatch.n_mod, gbatch.n_gen)
+    t_flop = F / (N * peaks["bf16_tflops"] * 1e12) * 1e3
+    t_hbm = hbm_all / N / (peaks["hbm_gbs"] * 1e9) * 1e3
+    nvl_per_gpu = comm_bytes_max / n_inst if world > 1 else 0.0
+    t_nvl = nvl_per_gpu / 900e9 * 1e3
+    t_roof_ms = max(t_flop, t_hbm, t_nvl)
     step_roof = {"flops_per_step": F, "t_roof_ms": t_roof_ms, "frac": t_roof_ms / ms_per_step,
-                 "peak_tflops": peaks["bf16_tflops"], "bubble_bound": (P - 1) / (cfg.M * cfg.V + P - 1)}
+                 "terms_ms": {"tensor": t_flop, "hbm": t_hbm, "nvlink": t_nvl},
+                 "hbm_bytes_per_step_all_gpus": hbm_all, "nvlink_bytes_per_step_max_gpu": nvl_per_gpu,
+                 "peaks": {"bf16_tflops": peaks["bf16_tflops"], "hbm_gbs": peaks["hbm_gbs"], "nvlink_gbs": 900.0},
+                 "bound": max((t_flop, "tensor"), (t_hbm, "hbm"), (t_nvl, "nvlink"))[1],
+                 "bubble_bound": (P - 1) / (cfg.M * cfg.V + P - 1)}
 
     cpu = None
     if not args.no_cpu and N == 1:
-        dt, fl, cores = cpu_oracle_sample(cfg, rows=2048)
-        rate = fl / dt
-        cpu = {"value": rate / (F / (cfg.M * D)), "unit": UNIT, "cores": cores, "kind": "oracle",
-               "sample": f"oracle (numpy fp64) fwd+bwd of one LLM layer on 2048 rows of a {cfg.name} microbatch "
-                         f"({dt:.1f} s); samples/s extrapolated by the step's algorithmic FLOPs per sample"}
+        dt, fl, cores = oracle_microbatch_sample(cfg, args.ref_layers, args.ref_seq_div)
+        cpu = {"value": fl / dt / (F / (cfg.M * D)), "unit": UNIT, "cores": cores, "kind": "oracle",
+               "sample": f"oracle (numpy fp64 step_fp64) fwd+bwd of one {cfg.name} microbatch with "
+                         f"{args.ref_layers} of {cfg.L} LLM layers and S/{args.ref_seq_div} positions ({dt:.1f} s, "
+                         f"{fl / 1e12:.2f} TFLOP); samples/s scaled by the step's algorithmic FLOPs per sample"}
 
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": N, "steps": args.steps,
             "strategy": args.strategy,
@@ -457,9 +655,8 @@ def main():
             "scaling": "strong" if args.microbatches else "weak",
             "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
             "config": dict(config_dict(cfg, P, D), strategy=args.strategy, head_place=head_place_name(args, N),
-                           warmup_units=rt.sched.stats(0).w_star if W == 0 else W,
-                           last_stage_layers=n_last, stage_layers=split),
-            "roofline": roofline, "step_roofline": step_roof,
+                           warmup_units=W, last_stage_layers=n_last, stage_layers=split, step_sum=sum_mode),
+            "roofline": roofline, "step_roofline": step_roof, "bubble": bubble,
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches_all, "clocks": clocks,
             "nvlink": ({"bytes_per_step_all_ranks": comm_bytes_all / n_inst,
                         "messages_per_step": n_msgs_all / n_inst,
@@ -470,10 +667,9 @@ def main():
             "tokens_per_s": cfg.M * D * cfg.S * args.steps / (ms_max / 1000.0),
             "peak_hbm_gb_per_gpu": peak_alloc / 1e9, "stash_peak_bytes_rank0": stash,
             "loss": loss}
+    line.update(extra)
     print(json.dumps(line), flush=True)
-    if world > 1:
-        dist.barrier(group=group)
-    rt.close()
+    cx.barrier()
 
 
 if __name__ == "__main__":

@@ -215,11 +215,17 @@ typedef struct {
   void* grads;     /* device, grad_bytes (zeroed by bm_step)                     */
   void* work;      /* device, work_bytes                                         */
   void* comm;      /* device, comm_bytes (zeroed by the caller before binding)   */
+  /* the caller's allocation sizes in bytes; bm_ctx_bind returns BM_E_OOM if any
+   * is smaller than bm_ctx_sizes_get's requirement */
+  int64_t weight_bytes, grad_bytes, work_bytes, comm_bytes;
 } bm_buffers;
 
 /* Create the per-rank executor for `rank` of schedule s (s must outlive ctx). */
 bm_status bm_ctx_create(const bm_model_cfg* mc, const bm_schedule* s, int32_t rank, bm_ctx** out);
 bm_status bm_ctx_sizes_get(const bm_ctx* c, bm_ctx_sizes* out);
+/* Binds the caller's buffers (256-byte aligned, sizes >= bm_ctx_sizes_get).
+ * Errors: BM_E_INVALID (null / misaligned), BM_E_OOM (a buffer is too small; the
+ * message names it and both sizes), BM_E_CUDA. */
 bm_status bm_ctx_bind(bm_ctx* c, const bm_buffers* b);
 
 /* Peer memory (CUDA IPC over NVLink).  Export any device pointer as a 64-byte
@@ -295,6 +301,17 @@ typedef struct {
  * Asynchronous.  Zeroes grads, runs the rank's op list, allreduces DP grads
  * and the loss terms, and leaves the results in the bound buffers. */
 bm_status bm_step(bm_ctx* c, const bm_batch* batch, void* stream);
+
+/* Wait for the step most recently enqueued by bm_step to finish, at most
+ * timeout_ms milliseconds (<= 0: wait forever).  Returns BM_OK when it finished.
+ * BM_E_TIMEOUT when it did not: the step's device work is blocked on a flag a
+ * peer never wrote (a peer died, or the ranks' step counts drifted).  The
+ * message then names the first op of this rank whose receive (data flag) or
+ * send (ring credit) condition is unmet -- op index, kind, peer, payload,
+ * microbatch, the flag value and the value waited for -- or the step-end sum
+ * barrier.  The device work stays enqueued: the caller is expected to abort
+ * (destroying the CUDA context frees the GPU).  BM_E_CUDA on a device error. */
+bm_status bm_step_wait(bm_ctx* c, int64_t timeout_ms);
 
 /* Device pointer to float[2*M + 1]: per-mb CE, per-mb MSE (sums over ranks
  * after bm_step), and the step loss L = (1/M) sum (CE_m + MSE_m). */

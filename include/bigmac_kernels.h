@@ -52,9 +52,39 @@ bm_status bm_k_gemm_swiglu(int32_t M, int32_t f, int32_t K, const void* X, int64
 /* LLM down-projection data gradient with the SwiGLU backward fused into the
  * epilogue:  dh = dY W_down ([M, K] x [K, f], W_down [K, f] row-major, ldw),
  * then dgu = [dh*u*s*(1 + g(1-s)), dh*g*s] with s = sigmoid(g), g|u from gu
- * [M, 2f];  writes dgu [M, 2f] (dh is never stored). */
+ * [M, 2f];  writes dgu [M, 2f] (dh is never stored).  f % 32 == 0 (32-column
+ * output chunks; BM_E_INVALID otherwise -- the executor then runs the GEMM and
+ * bm_k_swiglu_bwd separately). */
 bm_status bm_k_gemm_dswiglu(int32_t M, int32_t f, int32_t K, const void* dY, int64_t lddy,
                             const void* W, int64_t ldw, const void* gu, void* dgu, void* stream);
+
+/* One bf16 contraction of a grouped launch, arguments as bm_k_gemm (epilogue
+ * BM_EPI_DSWIGLU: the fused SwiGLU backward of bm_k_gemm_dswiglu, with N = f,
+ * C = dgu [M, 2f], R = gu [M, 2f]; f is ignored otherwise). */
+typedef struct {
+  int32_t M, N, K;
+  const void* A;
+  int64_t lda;
+  int32_t a_major;
+  const void* B;
+  int64_t ldb;
+  int32_t b_major;
+  void* C;
+  int64_t ldc;
+  int32_t c_dtype, epilogue;
+  const void* R;
+  int64_t ldr;
+  float alpha;
+  int32_t f;
+} bm_gemm_desc;
+/* n (1..2) independent bf16 contractions -- a Linear's data and weight gradient --
+ * in ONE persistent CTA-pair tcgen05 launch: every pair processes whole 256 x 256
+ * tiles of either problem on a host-computed longest-processing-time schedule (a
+ * tile's cost = its K / 64 blocks), so neither problem's last wave leaves pairs
+ * idle.  Shapes that do not fit the pair kernel (M or N < 256, misaligned
+ * operands, or too few tiles in auto mode) run as separate bm_k_gemm launches.
+ * Outputs must not overlap.  Errors: BM_E_INVALID, BM_E_CUDA. */
+bm_status bm_k_gemm_group(const bm_gemm_desc* descs, int32_t n, void* stream);
 
 /* Tuning / testing knob for the bf16 GEMM tile scheme: 0 = auto (CTA-pair
  * cta_group::2 256xBN tiles when M >= 512, N >= 256, K >= 256; 128xBN 1-CTA
@@ -107,8 +137,9 @@ bm_status bm_k_add(int32_t dtype, int64_t n, const void* a, const void* b, void*
 bm_status bm_k_cast(int32_t src_dtype, int32_t dst_dtype, int64_t n, const void* src, void* dst, void* stream);
 /* Byte copy / zero fill on SMs (16-byte vectors when dst, src and bytes are 16-byte
  * aligned).  dst may be a peer GPU's IPC-mapped buffer (NVLink stores).  The
- * executor moves every byte inside a step with these kernels, never with a
- * copy-engine memcpy.  max_ctas <= 0: the elementwise grid (8 CTAs per SM). */
+ * executor's stage-boundary sends use a copy-engine cudaMemcpyAsync by default
+ * (no SM time taken from the GEMMs); BM_PEER_COPY=sm selects this kernel
+ * instead.  max_ctas <= 0: the elementwise grid (8 CTAs per SM). */
 bm_status bm_k_copy(void* dst, const void* src, int64_t bytes, int32_t max_ctas, void* stream);
 bm_status bm_k_zero(void* dst, int64_t bytes, void* stream);
 

@@ -66,7 +66,16 @@ class CtxSizes(C.Structure):
 
 
 class Buffers(C.Structure):
-    _fields_ = [("weights", C.c_void_p), ("grads", C.c_void_p), ("work", C.c_void_p), ("comm", C.c_void_p)]
+    _fields_ = [("weights", C.c_void_p), ("grads", C.c_void_p), ("work", C.c_void_p), ("comm", C.c_void_p),
+                ("weight_bytes", C.c_int64), ("grad_bytes", C.c_int64), ("work_bytes", C.c_int64),
+                ("comm_bytes", C.c_int64)]
+
+
+class GemmDesc(C.Structure):
+    _fields_ = [("M", C.c_int32), ("N", C.c_int32), ("K", C.c_int32), ("A", C.c_void_p), ("lda", C.c_int64),
+                ("a_major", C.c_int32), ("B", C.c_void_p), ("ldb", C.c_int64), ("b_major", C.c_int32),
+                ("C", C.c_void_p), ("ldc", C.c_int64), ("c_dtype", C.c_int32), ("epilogue", C.c_int32),
+                ("R", C.c_void_p), ("ldr", C.c_int64), ("alpha", C.c_float), ("f", C.c_int32)]
 
 
 class TraceRec(C.Structure):
@@ -105,6 +114,7 @@ SIGNATURES = {
     "bm_ctx_init_peer_sum": [_P, _I32, _I32, C.POINTER(C.c_uint8), C.POINTER(_I64), C.POINTER(C.c_uint8),
                              C.POINTER(_I64)],
     "bm_step": [_P, C.POINTER(Batch), _P],
+    "bm_step_wait": [_P, _I64],
     "bm_ctx_loss_ptr": [_P, C.POINTER(_P)],
     "bm_ctx_launch_count": [_P, C.POINTER(_I64)],
     "bm_ctx_stash_peak": [_P, C.POINTER(_I64)],
@@ -118,6 +128,7 @@ SIGNATURES = {
     # bigmac_kernels.h
     "bm_k_gemm": [_I32, _I32, _I32, _I32, _P, _I64, _I32, _P, _I64, _I32, _P, _I64, _I32, _I32, _P, _I64, _F, _P],
     "bm_k_gemm_mode": [_I32],
+    "bm_k_gemm_group": [C.POINTER(GemmDesc), _I32, _P],
     "bm_k_gemm_swiglu": [_I32, _I32, _I32, _P, _I64, _P, _I64, _P, _P, _P],
     "bm_k_gemm_dswiglu": [_I32, _I32, _I32, _P, _I64, _P, _I64, _P, _P, _P],
     "bm_k_rmsnorm_fwd": [_I32, _I32, _I32, _P, _P, _P, _P, _P],

@@ -23,6 +23,8 @@
 
 #include <algorithm>
 #include <array>
+#include <chrono>
+#include <thread>
 #include <cstdio>
 #include <cstring>
 #include <map>
@@ -371,6 +373,7 @@ struct bm_ctx {
   std::vector<float*> ps_grad;
   std::vector<void*> ipc_bases;    // mappings to release (registry references)
   int64_t step = 0;
+  cudaEvent_t done_ev = nullptr;   // recorded at the end of every bm_step (bm_step_wait)
   int64_t launches = 0;
   int64_t stash_peak[3] = {0, 0, 0};
   // per-step state
@@ -459,6 +462,7 @@ bm_ctx::~bm_ctx() {
   if (emb_ready_ev) cudaEventDestroy(emb_ready_ev);
   if (emb_free_ev) cudaEventDestroy(emb_free_ev);
   if (hn_ev) cudaEventDestroy(hn_ev);
+  if (done_ev) cudaEventDestroy(done_ev);
   if (gen_done_ev) cudaEventDestroy(gen_done_ev);
   for (auto e : evpool)
     if (e) cudaEventDestroy(e);
@@ -675,6 +679,54 @@ static bm_status timed_gemm(bm_ctx& c, int M, int N, int K, const void* A, int64
   c.tshape[pool].push_back({M, N, K, epi});
   return BM_OK;
 }
+// independent contractions (a Linear's data and weight gradient) in one grouped
+// CTA-pair launch (gemm_bf16_tc_group: LPT tile schedule, no wave tail per GEMM);
+// BM_GEMM_GROUP_BWD=0 launches them one by one
+static const bool g_group_bwd = !(getenv("BM_GEMM_GROUP_BWD") && getenv("BM_GEMM_GROUP_BWD")[0] == '0');
+static bm_status timed_group(bm_ctx& c, GemmSpec* sp, int n) {
+  if (c.dtype != BM_BF16 || n == 1 || !g_group_bwd) {
+    for (int i = 0; i < n; ++i) {
+      const GemmSpec& q = sp[i];
+      BM_TRY(timed_gemm(c, q.M, q.N, q.K, q.A, q.lda, q.a_major, q.B, q.ldb, q.b_major, q.C, q.ldc, q.c_dtype, q.epi,
+                        q.R, q.ldr, q.f));
+    }
+    return BM_OK;
+  }
+  for (int i = 0; i < n; ++i) {
+    sp[i].ws = c.cur_ws;
+    sp[i].ws_bytes = c.ws_bytes;
+  }
+  if (!c.timing || c.st != c.st_main) return gemm_bf16_tc_group(sp, n, c.st);
+  const int pool = (int)(c.step & 1);
+  auto& ev = c.tev[pool];
+  if (c.tev_used[pool] + 2 > ev.size()) {
+    for (int k = 0; k < 256; ++k) {
+      cudaEvent_t e;
+      BM_CUDA_TRY(cudaEventCreate(&e));
+      ev.push_back(e);
+    }
+  }
+  cudaEvent_t e0 = ev[c.tev_used[pool]], e1 = ev[c.tev_used[pool] + 1];
+  c.tev_used[pool] += 2;
+  BM_CUDA_TRY(cudaEventRecord(e0, c.st));
+  BM_TRY(gemm_bf16_tc_group(sp, n, c.st));
+  BM_CUDA_TRY(cudaEventRecord(e1, c.st));
+  double fl = 0;
+  for (int i = 0; i < n; ++i) fl += 2.0 * sp[i].M * sp[i].N * sp[i].K;
+  c.tflop_pending[pool] += fl;
+  c.gemm_count_pending[pool] += 1;
+  c.tshape[pool].push_back({sp[0].M, sp[0].N, sp[0].K, 100 + sp[1].epi});
+  return BM_OK;
+}
+// GemmSpec of a Linear's weight gradient dW[out, in] += dY^T X (fp32 TMA reduce-add)
+static GemmSpec spec_wgrad(int n, int in, int out, const void* dY, const void* X, int64_t ldx, float* dW, int64_t ldw) {
+  return GemmSpec{out, in, n, dY, out, 1, X, ldx, 1, dW, ldw, BM_F32, BM_EPI_ACCUM, nullptr, 0, 1.f, 0, nullptr, 0};
+}
+// ... its data gradient dX[n, in] = dY W
+static GemmSpec spec_dgrad(const bm_ctx& c, int n, int in, int out, const void* dY, const void* Wt, int64_t ldw,
+                           void* dX, int64_t lddx) {
+  return GemmSpec{n, in, out, dY, out, 0, Wt, ldw, 1, dX, lddx, c.dtype, BM_EPI_STORE, nullptr, 0, 1.f, 0, nullptr, 0};
+}
 // fold a finished pool's event pairs into the totals (blocks until they completed)
 static bm_status harvest_comm(bm_ctx& c, int pool) {
   auto& ev = c.cev[pool];
@@ -742,7 +794,9 @@ static bm_status lin_gate_up(bm_ctx& c, const void* xn, const void* Wgu, int64_t
 static bm_status lin_down_dgrad_swiglu(bm_ctx& c, const void* dy, const void* Wd, int64_t ldw, const void* gu,
                                        void* dh_scratch, void* dgu) {
   const auto& m = c.mc;
-  if (c.fuse_swiglu && c.dtype == BM_BF16)
+  // the fused epilogue stores 32-column chunks of dg and du; with f % 32 != 0 the last dg
+  // chunk's store would spill into du's first columns, so those widths take the split path
+  if (c.fuse_swiglu && c.dtype == BM_BF16 && m.f % 32 == 0)
     return timed_gemm(c, m.S, m.f, m.d, dy, m.d, 0, Wd, ldw, 1, dgu, 2 * m.f, BM_BF16, BM_EPI_DSWIGLU, gu, 2 * m.f, m.f);
   BM_TRY(timed_gemm(c, m.S, m.f, m.d, dy, m.d, 0, Wd, ldw, 1, dh_scratch, m.f, c.dtype, BM_EPI_STORE, nullptr, 0));
   return c.dtype == BM_BF16 ? swiglu_bwd<bf16>(m.S, m.f, (const bf16*)dh_scratch, (const bf16*)gu, (bf16*)dgu, c.st)
@@ -1054,11 +1108,23 @@ static bm_status op_llm_bwd(bm_ctx& c, const bm_op& o, const RecvState& rs) {
     const int l = l0 + j;
     char* out = (j == 0) ? c.bout[b] : (cur == c.dwork[0] ? c.dwork[1] : c.dwork[0]);
     snprintf(nm, sizeof nm, "llm.layer%d.down", l);
-    BM_TRY(lin_wgrad(c, m.S, m.f, m.d, cur, sl.h[j], m.f, G_(c, nm), LD_(c, nm)));
-    BM_TRY(lin_down_dgrad_swiglu(c, cur, P_(c, nm), LD_(c, nm), sl.gu[j], c.dh, c.dgu));
+    if (c.fuse_swiglu && c.dtype == BM_BF16 && m.f % 32 == 0) {
+      // down wgrad + down dgrad with the SwiGLU backward in its epilogue: one grouped launch
+      GemmSpec sp[2] = {spec_wgrad(m.S, m.f, m.d, cur, sl.h[j], m.f, G_(c, nm), LD_(c, nm)),
+                        GemmSpec{(int)m.S, m.f, m.d, cur, m.d, 0, P_(c, nm), LD_(c, nm), 1, c.dgu, 2 * (int64_t)m.f,
+                                 BM_BF16, BM_EPI_DSWIGLU, sl.gu[j], 2 * (int64_t)m.f, 1.f, m.f, nullptr, 0}};
+      BM_TRY(timed_group(c, sp, 2));
+    } else {
+      BM_TRY(lin_wgrad(c, m.S, m.f, m.d, cur, sl.h[j], m.f, G_(c, nm), LD_(c, nm)));
+      BM_TRY(lin_down_dgrad_swiglu(c, cur, P_(c, nm), LD_(c, nm), sl.gu[j], c.dh, c.dgu));
+    }
     snprintf(nm, sizeof nm, "llm.layer%d.gate_up", l);
-    BM_TRY(lin_wgrad(c, m.S, m.d, 2 * m.f, c.dgu, sl.xn[j], m.d, G_(c, nm), LD_(c, nm)));
-    BM_TRY(lin_dgrad(c, m.S, m.d, 2 * m.f, c.dgu, P_(c, nm), LD_(c, nm), c.dxn, m.d));
+    {
+      // gate_up dgrad + gate_up wgrad: one grouped launch
+      GemmSpec sp[2] = {spec_dgrad(c, m.S, m.d, 2 * m.f, c.dgu, P_(c, nm), LD_(c, nm), c.dxn, m.d),
+                        spec_wgrad(m.S, m.d, 2 * m.f, c.dgu, sl.xn[j], m.d, G_(c, nm), LD_(c, nm))};
+      BM_TRY(timed_group(c, sp, 2));
+    }
     snprintf(nm, sizeof nm, "llm.layer%d.norm", l);
     BM_TRY(norm_bwd(c, m.S, m.d, c.dxn, sl.x[j], P_(c, nm), sl.rstd[j], cur, out, G_(c, nm)));
     cur = out;
@@ -1464,6 +1530,17 @@ bm_status bm_ctx_bind(bm_ctx* c, const bm_buffers* b) {
   BM_CHECK_ARG(c && b && b->weights && b->grads && b->work && b->comm, "null buffer");
   for (const void* p : {b->weights, b->grads, b->work, b->comm})
     BM_CHECK_ARG((reinterpret_cast<uintptr_t>(p) & 255) == 0, "buffers must be 256-byte aligned");
+  {
+    const int64_t need[4] = {c->total_elems * (int64_t)c->es, c->total_elems * 4, c->work_bytes, c->comm_size[c->rank]};
+    const int64_t have[4] = {b->weight_bytes, b->grad_bytes, b->work_bytes, b->comm_bytes};
+    static const char* nm[4] = {"weights", "grads", "work", "comm"};
+    for (int i = 0; i < 4; ++i)
+      if (have[i] < need[i]) {
+        set_error(std::string("buffer '") + nm[i] + "' is " + std::to_string(have[i]) + " bytes, the context needs " +
+                  std::to_string(need[i]));
+        return BM_E_OOM;
+      }
+  }
   // every kernel loaded before the first step (lazy loading stalls behind flag waits)
   BM_TRY(preload_kernels());
   c->W = (char*)b->weights;
@@ -1510,6 +1587,7 @@ bm_status bm_ctx_bind(bm_ctx* c, const bm_buffers* b) {
       BM_CUDA_TRY(cudaEventCreateWithFlags(&c->gen_done_ev, cudaEventDisableTiming));
     }
     if (c->has_gen) BM_CUDA_TRY(cudaEventCreateWithFlags(&c->hn_ev, cudaEventDisableTiming));
+    BM_CUDA_TRY(cudaEventCreateWithFlags(&c->done_ev, cudaEventDisableTiming));
   }
   if (!drv().wait32 || !drv().write32) {
     set_error("cuStreamWaitValue32/cuStreamWriteValue32 unavailable");
@@ -1882,9 +1960,75 @@ bm_status bm_step(bm_ctx* c, const bm_batch* b, void* stream) {
     x.trace_last = trace_mark(x, x.st);
     x.trace.push_back({-1, -1, 0, -1, tr_tail, x.trace_last});
   }
+  BM_CUDA_TRY(cudaEventRecord(x.done_ev, x.st));
   x.step += 1;
   x.launches = launch_count() - launches0;
   return BM_OK;
+}
+
+// first unmet wait of this rank's step `stp` (op order), read from a host copy of its flags
+static std::string blocked_op(const bm_ctx& c, int64_t stp, const std::vector<uint32_t>& fl) {
+  static const char* PN[] = {"act", "grad", "emb", "embgrad", "genin", "gengrad"};
+  static const char* KN[] = {"EncFwd", "EncBwd", "LlmFwd", "LlmBwd", "GenFwd", "GenBwd", "Send", "Recv"};
+  const auto& ops = c.s->ranks[c.rank];
+  for (size_t i = 0; i < ops.size(); ++i) {
+    const bm_op& o = ops[i];
+    if (o.kind != BM_OP_RECV && o.kind != BM_OP_SEND) continue;
+    const bool recv = o.kind == BM_OP_RECV;
+    const auto key = recv ? std::make_tuple((int)o.peer, c.rank, (int)o.payload) : std::make_tuple(c.rank, (int)o.peer, (int)o.payload);
+    const Chan& ch = c.chans[c.chan_idx.at(key)];
+    if (!recv && o.seq < ch.K) continue;   // a free slot: no credit wait
+    const uint32_t base = (uint32_t)(stp * ch.nmsg);
+    const uint32_t want = recv ? base + (uint32_t)o.seq + 1 : base + (uint32_t)(o.seq - ch.K) + 1;
+    const uint32_t have = fl[(size_t)(recv ? ch.flag_off : ch.credit_off) / 4];
+    if ((int32_t)(have - want) < 0)
+      return "rank " + std::to_string(c.rank) + " blocked at op " + std::to_string(i) + " (" + KN[o.kind] + " " +
+             PN[o.payload] + (recv ? " from " : " to ") + "rank " + std::to_string(o.peer) + ", mb " +
+             std::to_string(o.mb) + ", seq " + std::to_string(o.seq) + "): " + (recv ? "data" : "credit") +
+             " flag " + std::to_string(have) + " < " + std::to_string(want);
+  }
+  if (c.psum) {
+    const int world = (int)c.ps_comm.size(), me = c.replica * c.P + c.rank;
+    const uint32_t want = (uint32_t)(stp * 4 + 3);
+    const size_t sb = (size_t)c.sum_off[c.rank] / 4;
+    for (int g = 0; g < world; ++g)
+      if (g != me && (int32_t)(fl[sb + 16 * g] - want) < 0)
+        return "rank " + std::to_string(c.rank) + " blocked in the step-end sum barrier: process " + std::to_string(g) +
+               " flag " + std::to_string(fl[sb + 16 * g]) + " < " + std::to_string(want);
+  }
+  return "rank " + std::to_string(c.rank) + ": every receive / credit / barrier flag is satisfied (blocked in a kernel "
+         "or a collective)";
+}
+
+bm_status bm_step_wait(bm_ctx* c, int64_t timeout_ms) {
+  BM_CHECK_ARG(c && c->bound, "bound context required");
+  if (c->step == 0 || !c->done_ev) return BM_OK;
+  const auto t0 = std::chrono::steady_clock::now();
+  for (;;) {
+    const cudaError_t e = cudaEventQuery(c->done_ev);
+    if (e == cudaSuccess) return BM_OK;
+    if (e != cudaErrorNotReady) BM_CUDA_TRY(e);
+    const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    if (timeout_ms > 0 && ms > (double)timeout_ms) break;
+    std::this_thread::sleep_for(std::chrono::microseconds(200));
+  }
+  // diagnose from a host copy of this rank's flags (private stream, bounded wait)
+  std::string why = "flags unreadable (the copy did not complete within 2 s)";
+  const size_t bytes = (size_t)c->comm_size[c->rank];
+  std::vector<uint32_t> fl(bytes / 4 + 1, 0);
+  cudaStream_t s = nullptr;
+  if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) == cudaSuccess) {
+    if (cudaMemcpyAsync(fl.data(), c->comm, bytes, cudaMemcpyDeviceToHost, s) == cudaSuccess) {
+      const auto t1 = std::chrono::steady_clock::now();
+      while (cudaStreamQuery(s) == cudaErrorNotReady &&
+             std::chrono::steady_clock::now() - t1 < std::chrono::seconds(2))
+        std::this_thread::sleep_for(std::chrono::milliseconds(1));
+      if (cudaStreamQuery(s) == cudaSuccess) why = blocked_op(*c, c->step - 1, fl);
+    }
+    cudaStreamDestroy(s);   // released once its copy completes
+  }
+  set_error("step " + std::to_string(c->step - 1) + " did not finish within " + std::to_string(timeout_ms) + " ms: " + why);
+  return BM_E_TIMEOUT;
 }
 
 bm_status bm_ctx_loss_ptr(const bm_ctx* c, const float** dptr) {

@@ -27,6 +27,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "kernels.h"
 
 namespace bm {
 int gemm_mode();
@@ -64,20 +65,8 @@ struct EpiArgs {
   int splits;      // split-K factor (1-CTA kernel); > 1: fp32 partials to the workspace map
   int kb_per;      // K blocks per split
   int mpad;        // workspace rows per split (M rounded up to the tile height)
-  // stream-K (CTA-pair kernel, sk != 0): pair p runs the k-iterations
-  // [p T / npairs, (p+1) T / npairs) of the T = tiles * nk (tile, k-block) sequence
-  int sk;
-  float* sk_ws;          // fp32 tail partials: [npairs][2 CTAs][128 rows][BN]
-  uint32_t* sk_flags;    // [npairs][2 CTAs][8 epilogue warps], = sk_epoch when a partial is ready
-  uint32_t sk_epoch;     // unique per launch on this flag set
-  int group;             // raster group (m-tiles per n sweep) of the CTA-pair kernel
-  // sk == 2 (DP + split remainder): the first dp_tiles tiles round-robin as whole
-  // tiles; the other rem tiles are cut into ksplit k-ranges, pieces ordered
-  // k-range-major (piece i: range i / rem of remainder tile i % rem) and dealt
-  // round-robin, so concurrent pieces read the same k-range of A and B
-  int dp_tiles, rem, ksplit;
-  int mbar_cluster;      // 1: .acquire.cluster barrier waits (default); 0: BM_MBAR_SCOPE=cta
-  int sk_tma;            // partials written by TMA stores through tmC2 (swizzled smem staging)
+  int group;       // raster group (m-tiles per n sweep) of the CTA-pair kernel
+  int mbar_cluster;  // 1: .acquire.cluster barrier waits (default); 0: BM_MBAR_SCOPE=cta
 };
 
 // ---------------------------------------------------------------- PTX helpers
@@ -257,67 +246,6 @@ __device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int
   int r = t % per_group;
   mb = first_m + r % gm;
   nb = r / gm;
-}
-
-// The (tile, k-block range) segments of one CTA pair: round-robin whole tiles,
-// or (stream-K) the pair's contiguous share of the tile-major k-iteration
-// sequence.  With tiles >= pairs a share spans >= nk iterations, so a tile is
-// cut at most once: its head [0, kb1) ends the share of pair p and its tail
-// [kb1, nk) starts the share of pair p + 1.
-struct SegIter {
-  int sk, nk, num_tiles, step, t;
-  int64_t g, g1;
-  int dp, rem, ks, piece;   // sk == 2
-  int q = -1, tr = -1;      // sk == 2: k-range index and remainder tile of the last piece (-1: whole tile)
-  __device__ SegIter(const EpiArgs& a, int pair, int npairs, int tiles, int nk_)
-      : sk(a.sk), nk(nk_), num_tiles(tiles), step(npairs), t(pair), dp(a.dp_tiles), rem(a.rem), ks(a.ksplit),
-        piece(pair) {
-    const int64_t tot = (int64_t)tiles * nk_;
-    g = tot * pair / npairs;
-    g1 = tot * (pair + 1) / npairs;
-  }
-  __device__ bool next(int& tile, int& kb0, int& kb1) {
-    if (sk == 2) {
-      if (t < dp) {
-        tile = t;
-        kb0 = 0;
-        kb1 = nk;
-        t += step;
-        q = tr = -1;
-        return true;
-      }
-      if (piece >= rem * ks) return false;
-      q = piece / rem;
-      tr = piece % rem;
-      tile = dp + tr;
-      kb0 = (int)((int64_t)q * nk / ks);
-      kb1 = (int)((int64_t)(q + 1) * nk / ks);
-      piece += step;
-      return true;
-    }
-    if (!sk) {
-      if (t >= num_tiles) return false;
-      tile = t;
-      kb0 = 0;
-      kb1 = nk;
-      t += step;
-      return true;
-    }
-    if (g >= g1) return false;
-    tile = (int)(g / nk);
-    kb0 = (int)(g % nk);
-    kb1 = (int)min((int64_t)nk, (int64_t)kb0 + (g1 - g));
-    g += kb1 - kb0;
-    return true;
-  }
-};
-__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
-  uint32_t v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release_u32(uint32_t* p, uint32_t v) {
-  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
@@ -825,17 +753,119 @@ template <int BN, bool SWI = false> struct Cfg2 {
   static constexpr int A_BYTES = 128 * BK * 2;                 // 16 KB
   static constexpr int B_BYTES = (BN / 2) * BK * 2;            // 16 KB (BN = 256)
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  // staging slots per epilogue warp: with 2, a chunk's TMA stores read one while the
+  // next chunk is staged in the other (wait_group.read 1); with 1, read 0
+  // (measured: 2 slots with 5 stages gains 1.5 % on the SwiGLU-backward dgrad and
+  // loses 3-4 % on the fp32 wgrads, so the non-SwiGLU kernels keep 1 slot, 6 stages)
+  static constexpr int NSLOT = 1;
   static constexpr int STAGES = SWI ? 5 : ((BN == 256) ? 6 : 8);
   static constexpr int TMEM_COLS = 2 * BN;
-  static constexpr int EPI_SLOT = SWI ? 6144 : 4096;           // one staging slot per epilogue warp
-  static constexpr int EPI_BYTES = EPI_WARPS2 * EPI_SLOT;
+  static constexpr int EPI_SLOT = SWI ? 6144 : 4096;           // staging slot of one epilogue warp
+  static constexpr int EPI_BYTES = EPI_WARPS2 * NSLOT * EPI_SLOT;
   static constexpr int SMEM = STAGES * STAGE_BYTES + EPI_BYTES + 1024 + 256;
 };
 
-template <int BN, bool A_MN, bool B_MN, bool SWIGLU>
+// One problem of a (grouped) CTA-pair launch: operand / output maps, epilogue,
+// operand majors and tile grid.  Several independent contractions (a Linear's
+// data- and weight-gradient) can share one persistent launch.
+struct alignas(64) PairProblem {
+  CUtensorMap tmA, tmB, tmC, tmC2;   // tmC2: SwiGLU h output
+  EpiArgs ea;
+  int a_mn, b_mn;
+  int tiles_m, tiles_n, nk;
+};
+constexpr int MAX_PAIR_PROBLEMS = 2;
+struct alignas(64) PairGroup {
+  PairProblem prob[MAX_PAIR_PROBLEMS];
+  int nprob;
+  int tiles0;           // tiles of problem 0 (round-robin item t < tiles0: problem 0)
+  int total_tiles;
+  const int* work;      // optional static schedule: items of pair p = work[work_off[p] .. work_off[p+1])
+  const int* work_off;  //   item = (problem << 24) | tile
+};
+
+// The work items of one CTA pair: round-robin over the concatenated tile lists,
+// or the host-computed schedule (longest-processing-time list scheduling).
+struct PairIter {
+  const PairGroup& g;
+  int pos, end, step;
+  __device__ PairIter(const PairGroup& g_, int pair, int npairs) : g(g_) {
+    if (g.work) {
+      pos = g.work_off[pair];
+      end = g.work_off[pair + 1];
+      step = 1;
+    } else {
+      pos = pair;
+      end = g.total_tiles;
+      step = npairs;
+    }
+  }
+  __device__ bool next(int& prob, int& tile) {
+    if (pos >= end) return false;
+    if (g.work) {
+      const int it = g.work[pos];
+      prob = it >> 24;
+      tile = it & 0xFFFFFF;
+    } else {
+      prob = pos >= g.tiles0 ? 1 : 0;
+      tile = pos - (prob ? g.tiles0 : 0);
+    }
+    pos += step;
+    return true;
+  }
+};
+
+// 32 g and 32 u values (bf16) of one row for the fused SwiGLU-backward epilogue,
+// loaded ahead of the accumulator (they do not depend on the MMA result)
+struct GU32 {
+  uint4 g[4], u[4];
+};
+__device__ __forceinline__ void load_gu(const EpiArgs& a, int row, int col0, GU32& x) {
+  if (row < a.M && col0 < a.N) {
+    const bf16* gu = reinterpret_cast<const bf16*>(a.R) + (int64_t)row * a.ldr + col0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      x.g[j] = __ldg(reinterpret_cast<const uint4*>(gu + 8 * j));
+      x.u[j] = __ldg(reinterpret_cast<const uint4*>(gu + a.f + 8 * j));
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) x.g[j] = x.u[j] = make_uint4(0, 0, 0, 0);
+  }
+}
+// dg = dh u s (1 + g (1 - s)) -> w, du = dh g s -> v (in place of dh), s = sigmoid(g)
+__device__ __forceinline__ void dswiglu_math(float alpha, float* v, float* w, const GU32& x) {
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const float g = __bfloat162float(reinterpret_cast<const bf16*>(&x.g[j])[q]);
+      const float u = __bfloat162float(reinterpret_cast<const bf16*>(&x.u[j])[q]);
+      const float d = alpha * v[8 * j + q], sg = sigmoidf_(g);
+      w[8 * j + q] = d * u * sg * (1.f + g * (1.f - sg));
+      v[8 * j + q] = d * g * sg;
+    }
+  }
+}
+// TMA stores of a full 32-column chunk: dg -> cols [col0, +32), du -> cols [f + col0, +32)
+__device__ __forceinline__ void store_dswiglu_tma(const EpiArgs& a, const CUtensorMap* tmC, uint32_t slot, int lane,
+                                                  int row0, int col0, const float* dg, const float* du) {
+  stage_bf16(slot, lane, dg);
+  stage_bf16(slot + 2048, lane, du);
+  fence_async_smem();
+  __syncwarp();
+  if (lane == 0) {
+    tma_store_2d(tmC, slot, col0, row0);
+    tma_store_2d(tmC, slot + 2048, a.f + col0, row0);
+    bulk_commit();
+  }
+}
+
+// AM / BM_: operand majors fixed at compile time (0 K-major, 1 MN-major) for
+// single-problem launches, or -1: read per problem at run time (grouped launches)
+template <int BN, bool SWIGLU, int AM = -1, int BMJ = -1>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS2, 1)
-gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-             const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmC2, EpiArgs args) {
+gemm2_kernel(const __grid_constant__ PairGroup g) {
   using C = Cfg2<BN, SWIGLU>;
   constexpr int STAGES = C::STAGES;
   constexpr int BNH = BN / 2;
@@ -853,11 +883,8 @@ gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
   const uint32_t cta = cluster_rank();
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
-  const int tiles_m = (args.M + 2 * BM - 1) / (2 * BM);
-  const int tiles_n = SWIGLU ? (args.f + BNH - 1) / BNH : (args.N + BN - 1) / BN;
-  const int num_tiles = tiles_m * tiles_n;
-  const int nk = (args.K + BK - 1) / BK;
   const int pair = blockIdx.x / 2, npairs = gridDim.x / 2;
+  const int mbc = g.prob[0].ea.mbar_cluster;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -869,8 +896,10 @@ gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
       mbar_init(&tempty[s], 2 * EPI_WARPS2);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    tma_prefetch(&tmA);
-    tma_prefetch(&tmB);
+    for (int p = 0; p < g.nprob; ++p) {
+      tma_prefetch(&g.prob[p].tmA);
+      tma_prefetch(&g.prob[p].tmB);
+    }
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
@@ -887,32 +916,39 @@ gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      SegIter it(args, pair, npairs, num_tiles, nk);
-      int t, kb0, kb1;
-      while (it.next(t, kb0, kb1)) {
+      PairIter it(g, pair, npairs);
+      int pi, t;
+      while (it.next(pi, t)) {
+        // per-tile scalars into registers: the barrier waits below invalidate L1
+        // (acquire.cluster), so re-reading parameters inside the k-loop would go to L2
+        const PairProblem& pr = g.prob[pi];
+        const CUtensorMap* mA = &pr.tmA;
+        const CUtensorMap* mB = &pr.tmB;
+        const int nk = pr.nk;
+        const bool amn = AM >= 0 ? AM != 0 : pr.a_mn != 0, bmn = BMJ >= 0 ? BMJ != 0 : pr.b_mn != 0;
         int mb, nb;
-        tile_coords(t, tiles_m, tiles_n, mb, nb, args.group);
+        tile_coords(t, pr.tiles_m, pr.tiles_n, mb, nb, pr.ea.group);
         const int m0 = mb * 2 * BM + (int)cta * BM;
         // SwiGLU pairing: CTA 0 loads gate rows [nb*BNH, +BNH), CTA 1 the matching up rows
-        const int n0 = SWIGLU ? (nb * BNH + (int)cta * args.f) : (nb * BN + (int)cta * BNH);
-        for (int kb = kb0; kb < kb1; ++kb) {
-          mbar_wait(&empty[stage], phase ^ 1, args.mbar_cluster);
+        const int n0 = SWIGLU ? (nb * BNH + (int)cta * pr.ea.f) : (nb * BN + (int)cta * BNH);
+        for (int kb = 0; kb < nk; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1, mbc);
           if (cta == 0) mbar_expect_tx(&full[stage], 2 * C::STAGE_BYTES);
           const uint32_t lbar = mapa(smem_u32(&full[stage]), 0);
           uint8_t* a_dst = smA + stage * C::A_BYTES;
           uint8_t* b_dst = smB + stage * C::B_BYTES;
           const int k0 = kb * BK;
-          if (A_MN) {
+          if (amn) {
 #pragma unroll
-            for (int j = 0; j < BM / 64; ++j) tma_load_2d_pair(a_dst + j * (BK * 128), &tmA, lbar, m0 + 64 * j, k0);
+            for (int j = 0; j < BM / 64; ++j) tma_load_2d_pair(a_dst + j * (BK * 128), mA, lbar, m0 + 64 * j, k0);
           } else {
-            tma_load_2d_pair(a_dst, &tmA, lbar, k0, m0);
+            tma_load_2d_pair(a_dst, mA, lbar, k0, m0);
           }
-          if (B_MN) {
+          if (bmn) {
 #pragma unroll
-            for (int j = 0; j < BNH / 64; ++j) tma_load_2d_pair(b_dst + j * (BK * 128), &tmB, lbar, n0 + 64 * j, k0);
+            for (int j = 0; j < BNH / 64; ++j) tma_load_2d_pair(b_dst + j * (BK * 128), mB, lbar, n0 + 64 * j, k0);
           } else {
-            tma_load_2d_pair(b_dst, &tmB, lbar, k0, n0);
+            tma_load_2d_pair(b_dst, mB, lbar, k0, n0);
           }
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
@@ -920,28 +956,31 @@ gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
     }
   } else if (warp == 1) {
     if (cta == 0 && lane == 0) {
-      constexpr uint32_t idesc = make_idesc(BN, A_MN, B_MN, 2 * BM);
       int stage = 0;
       uint32_t phase = 0;
       int local = 0;
-      SegIter it(args, pair, npairs, num_tiles, nk);
-      int t, kb0, kb1;
-      for (; it.next(t, kb0, kb1); ++local) {
+      PairIter it(g, pair, npairs);
+      int pi, t;
+      for (; it.next(pi, t); ++local) {
+        const PairProblem& pr = g.prob[pi];
+        const bool amn = AM >= 0 ? AM != 0 : pr.a_mn != 0, bmn = BMJ >= 0 ? BMJ != 0 : pr.b_mn != 0;
+        const int nk = pr.nk;
+        const uint32_t idesc = make_idesc(BN, amn, bmn, 2 * BM);
         const int acc = local & 1;
         const uint32_t acc_phase = (local >> 1) & 1;
-        mbar_wait(&tempty[acc], acc_phase ^ 1, args.mbar_cluster);
+        mbar_wait(&tempty[acc], acc_phase ^ 1, mbc);
         tc_fence_after();
         const uint32_t tmem_d = tmem_base + acc * BN;
-        for (int kb = kb0; kb < kb1; ++kb) {
-          mbar_wait(&full[stage], phase, args.mbar_cluster);
+        for (int kb = 0; kb < nk; ++kb) {
+          mbar_wait(&full[stage], phase, mbc);
           tc_fence_after();
           const uint32_t a_base = smem_u32(smA + stage * C::A_BYTES);
           const uint32_t b_base = smem_u32(smB + stage * C::B_BYTES);
 #pragma unroll
           for (int kk = 0; kk < BK / 16; ++kk) {
-            uint64_t ad = A_MN ? make_desc(a_base + kk * 2048, BK * 128, 1024) : make_desc(a_base + kk * 32, 16, 1024);
-            uint64_t bd = B_MN ? make_desc(b_base + kk * 2048, BK * 128, 1024) : make_desc(b_base + kk * 32, 16, 1024);
-            umma_f16_pair(tmem_d, ad, bd, idesc, (kb != kb0 || kk != 0) ? 1u : 0u);
+            uint64_t ad = amn ? make_desc(a_base + kk * 2048, BK * 128, 1024) : make_desc(a_base + kk * 32, 16, 1024);
+            uint64_t bd = bmn ? make_desc(b_base + kk * 2048, BK * 128, 1024) : make_desc(b_base + kk * 32, 16, 1024);
+            umma_f16_pair(tmem_d, ad, bd, idesc, (kb != 0 || kk != 0) ? 1u : 0u);
           }
           umma_commit_pair(&empty[stage]);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -953,141 +992,91 @@ gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
     // epilogue warps 2..9: TMEM lane quadrant = warp % 4, column half = (warp - 2) / 4
     const int quad = warp & 3;
     const int half = (warp - 2) / 4;
-    const uint32_t slot = smem_u32(smE) + (uint32_t)((warp - 2) * C::EPI_SLOT);
+    const uint32_t slot0 = smem_u32(smE) + (uint32_t)((warp - 2) * C::NSLOT * C::EPI_SLOT);
+    uint32_t slot = slot0;
     int eiter = 0;
     const uint32_t leader_tempty0 = mapa(smem_u32(&tempty[0]), 0);
     const uint32_t leader_tempty1 = mapa(smem_u32(&tempty[1]), 0);
     int local = 0;
-    SegIter it(args, pair, npairs, num_tiles, nk);
-    int t, kb0, kb1;
-    const int ew = warp - 2;   // epilogue warp: (quad, half) sub-block, the same in every pair
-    for (; it.next(t, kb0, kb1); ++local) {
+    PairIter it(g, pair, npairs);
+    int pi, t;
+    for (; it.next(pi, t); ++local) {
+      const PairProblem& pr = g.prob[pi];
+      const EpiArgs ea = pr.ea;   // into registers (see the producer)
+      const CUtensorMap* mC = &pr.tmC;
+      const CUtensorMap* mC2 = &pr.tmC2;
       int mb, nb;
-      tile_coords(t, tiles_m, tiles_n, mb, nb, args.group);
+      tile_coords(t, pr.tiles_m, pr.tiles_n, mb, nb, ea.group);
       const int acc = local & 1;
       const uint32_t acc_phase = (local >> 1) & 1;
-      mbar_wait(&tfull[acc], acc_phase, args.mbar_cluster);
-      tc_fence_after();
       const int row0 = mb * 2 * BM + (int)cta * BM + quad * 32;
       const int row = row0 + lane;
       const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + acc * BN;
-      // partial-sum producers: stream-K tails (slot = this pair) and split-remainder
-      // pieces before the last k-range (slot = tr * (ksplit - 1) + q)
-      const bool piece_part = args.sk == 2 && it.q >= 0 && it.q < args.ksplit - 1;
-      if (!SWIGLU && ((args.sk == 1 && kb0 > 0) || piece_part)) {
-        // this warp's 32 x BN/2 fp32 sub-block of the partial sum into the slot, then
-        // publish it (the owner of the tile's last piece finishes the tile)
-        const int64_t pslot = piece_part ? (int64_t)it.tr * (args.ksplit - 1) + it.q : pair;
-        if (args.sk_tma) {
-          // coalesced: swizzled 32 x 32 fp32 staging + TMA store into the workspace
-          // viewed as [slots * 2 * 128 rows, BN] (the normal epilogue's path)
-          const int prow = (int)((pslot * 2 + cta) * BM + quad * 32);
-#pragma unroll 1
-          for (int c = half * (BN / 2); c < (half + 1) * (BN / 2); c += 32) {
-            float v[32];
-            tmem_ld32(taddr + c, v);
-            if (eiter >= 1) {
-              if (lane == 0) bulk_wait_read0();
-              __syncwarp();
-            }
-            stage_f32(slot, lane, v);
-            fence_async_smem();
-            __syncwarp();
-            if (lane == 0) {
-              tma_store_2d(&tmC2, slot, c, prow);
-              bulk_commit();
-            }
-            ++eiter;
-          }
-          if (lane == 0) {   // stores performed, then visible to the owner's generic loads
-            bulk_wait_all();
-            asm volatile("fence.proxy.async.global;" ::: "memory");
-            __threadfence();
-          }
-          __syncwarp();
-        } else {
-          float* dst = args.sk_ws + (((pslot * 2 + cta) * BM + quad * 32 + lane) * BN);
-#pragma unroll 1
-          for (int c = half * (BN / 2); c < (half + 1) * (BN / 2); c += 32) {
-            float v[32];
-            tmem_ld32(taddr + c, v);
-#pragma unroll
-            for (int j = 0; j < 32; j += 4)
-              __stcg(reinterpret_cast<float4*>(dst + c + j), make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]));
-          }
-          __threadfence();
-          __syncwarp();
-        }
-        if (lane == 0) st_release_u32(args.sk_flags + (pslot * 2 + cta) * EPI_WARPS2 + ew, args.sk_epoch);
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive_cluster(acc ? leader_tempty1 : leader_tempty0);
-        continue;
-      }
-      // consumers: a stream-K head adds pair + 1's tail; the last piece of a split
-      // remainder tile adds the tile's ksplit - 1 partials in k-range order
-      const bool sk_head = !SWIGLU && args.sk == 1 && kb1 < nk;
-      const bool piece_last = !SWIGLU && args.sk == 2 && it.q == args.ksplit - 1;
-      const int nparts = sk_head ? 1 : (piece_last ? args.ksplit - 1 : 0);
-      const int64_t pslot0 = sk_head ? (int64_t)(pair + 1) : (int64_t)it.tr * (args.ksplit - 1);
-      const float* part = nullptr;
-      if (nparts > 0) {
-        if (lane == 0) {
-          for (int j = 0; j < nparts; ++j) {
-            const uint32_t* fl = args.sk_flags + ((pslot0 + j) * 2 + cta) * EPI_WARPS2 + ew;
-            const long long t0 = clock64();
-            while (ld_acquire_u32(fl) != args.sk_epoch)
-              if (clock64() - t0 > 40000000000LL) __trap();
-          }
-        }
-        __syncwarp();
-        part = args.sk_ws + (((pslot0 * 2 + cta) * BM + quad * 32 + lane) * BN);
-      }
       if (SWIGLU) {
+        mbar_wait(&tfull[acc], acc_phase, mbc);
+        tc_fence_after();
         constexpr int W = BNH / 2;   // features per warp
 #pragma unroll 1
         for (int c = half * W; c < (half + 1) * W; c += 32) {
           float vg[32], vu[32];
           tmem_ld32(taddr + c, vg);
           tmem_ld32(taddr + BNH + c, vu);
-          if (args.tma) {
-            if (nb * BNH + c < args.f) {
+          if (ea.tma) {
+            if (nb * BNH + c < ea.f) {
               if (eiter >= 1) {
                 if (lane == 0) bulk_wait_read0();
                 __syncwarp();
               }
-              epi_swiglu_tma(args, &tmC, &tmC2, slot, lane, row0, nb * BNH + c, vg, vu);
+              epi_swiglu_tma(ea, mC, mC2, slot, lane, row0, nb * BNH + c, vg, vu);
               ++eiter;
             }
-          } else if (row < args.M) {
-            epilogue_swiglu(args, row, nb * BNH + c, vg, vu);
+          } else if (row < ea.M) {
+            epilogue_swiglu(ea, row, nb * BNH + c, vg, vu);
           }
         }
       } else {
         constexpr int W = BN / 2;    // columns per warp
+        const int cbeg = half * W, cend = (half + 1) * W;
+        const bool dsw = ea.epi == BM_EPI_DSWIGLU && ea.tma;
+        GU32 gu;
+        if (dsw) load_gu(ea, row, nb * BN + cbeg, gu);   // ahead of the accumulator
+        mbar_wait(&tfull[acc], acc_phase, mbc);
+        tc_fence_after();
 #pragma unroll 1
-        for (int c = half * W; c < (half + 1) * W; c += 32) {
+        for (int c = cbeg; c < cend; c += 32) {
           float v[32];
           tmem_ld32(taddr + c, v);
-          for (int pj = 0; pj < nparts; ++pj) {   // fixed order: deterministic
-            const float* pp = part + (int64_t)pj * 2 * BM * BN;
-#pragma unroll
-            for (int j = 0; j < 32; j += 4) {
-              const float4 q = __ldcg(reinterpret_cast<const float4*>(pp + c + j));
-              v[j] += q.x; v[j + 1] += q.y; v[j + 2] += q.z; v[j + 3] += q.w;
-            }
-          }
-          if (args.tma) {
-            if (nb * BN + c < args.N) {
-              if (eiter >= 1) {
-                if (lane == 0) bulk_wait_read0();
+          if (dsw) {
+            float w[32];
+            dswiglu_math(ea.alpha, v, w, gu);
+            if (c + 32 < cend) load_gu(ea, row, nb * BN + c + 32, gu);   // next chunk, in flight during the stores
+            if (nb * BN + c < ea.N) {
+              slot = slot0 + (uint32_t)((eiter % C::NSLOT) * C::EPI_SLOT);
+              if (eiter >= C::NSLOT) {
+                if (lane == 0) {
+                  if (C::NSLOT == 2) bulk_wait_read1();
+                  else bulk_wait_read0();
+                }
                 __syncwarp();
               }
-              epi_chunk_tma(args, &tmC, slot, lane, row0, nb * BN + c, v);
+              store_dswiglu_tma(ea, mC, slot, lane, row0, nb * BN + c, w, v);
               ++eiter;
             }
-          } else if (row < args.M) {
-            epilogue_row(args, row, nb * BN + c, v);
+          } else if (ea.tma) {
+            if (nb * BN + c < ea.N) {
+              slot = slot0 + (uint32_t)((eiter % C::NSLOT) * C::EPI_SLOT);
+              if (eiter >= C::NSLOT) {
+                if (lane == 0) {
+                  if (C::NSLOT == 2) bulk_wait_read1();
+                  else bulk_wait_read0();
+                }
+                __syncwarp();
+              }
+              epi_chunk_tma(ea, mC, slot, lane, row0, nb * BN + c, v);
+              ++eiter;
+            }
+          } else if (row < ea.M) {
+            epilogue_row(ea, row, nb * BN + c, v);
           }
         }
       }
@@ -1260,46 +1249,34 @@ static bm_status dispatch_majors(bool a_mn, bool b_mn, const CUtensorMap& ma, co
 }
 
 
-template <int BN, bool A_MN, bool B_MN, bool SWIGLU = false>
-static bm_status launch2(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc, const CUtensorMap& mc2,
-                         const EpiArgs& ea, cudaStream_t st) {
+template <int BN, bool SWIGLU = false, int AM = -1, int BMJ = -1>
+static bm_status launch2(const PairGroup& g, int tiles, cudaStream_t st) {
   using C = Cfg2<BN, SWIGLU>;
   static bool attr_set = false;
   if (!attr_set) {
-    BM_CUDA_TRY(cudaFuncSetAttribute(gemm2_kernel<BN, A_MN, B_MN, SWIGLU>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    BM_CUDA_TRY(cudaFuncSetAttribute(gemm2_kernel<BN, SWIGLU, AM, BMJ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      C::SMEM));
     attr_set = true;
   }
-  const int tiles = ceil_div(ea.M, 2 * BM) * (SWIGLU ? ceil_div(ea.f, BN / 2) : ceil_div(ea.N, BN));
   const int pairs = gemm_sm_budget() / 2;
-  const int grid = 2 * (tiles < pairs ? tiles : pairs);   // stream-K: tiles >= pairs, every pair busy
-  BM_CUDA_TRY(launch_k(gemm2_kernel<BN, A_MN, B_MN, SWIGLU>, dim3(grid), dim3(NUM_THREADS2), C::SMEM, st, ma, mb, mc,
-                       mc2, ea));
+  const int grid = 2 * (tiles < pairs ? tiles : pairs);
+  BM_CUDA_TRY(launch_k(gemm2_kernel<BN, SWIGLU, AM, BMJ>, dim3(grid), dim3(NUM_THREADS2), C::SMEM, st, g));
   count_launch();
   BM_CUDA_TRY(cudaGetLastError());
   return BM_OK;
 }
-
+// single-problem launch with the operand majors as template constants
 template <int BN>
-static bm_status dispatch_majors2(bool a_mn, bool b_mn, const CUtensorMap& ma, const CUtensorMap& mb,
-                                  const CUtensorMap& mc, const EpiArgs& ea, cudaStream_t st,
-                                  const CUtensorMap* mc2 = nullptr) {
-  const CUtensorMap& m2 = mc2 ? *mc2 : mc;   // second map: the split-remainder partial workspace
-  if (!a_mn && !b_mn) return launch2<BN, false, false>(ma, mb, mc, m2, ea, st);
-  if (!a_mn && b_mn) return launch2<BN, false, true>(ma, mb, mc, m2, ea, st);
-  if (a_mn && b_mn) return launch2<BN, true, true>(ma, mb, mc, m2, ea, st);
-  return launch2<BN, true, false>(ma, mb, mc, m2, ea, st);
+static bm_status launch2_static(const PairGroup& g, int tiles, cudaStream_t st) {
+  const int a = g.prob[0].a_mn, b = g.prob[0].b_mn;
+  if (!a && !b) return launch2<BN, false, 0, 0>(g, tiles, st);
+  if (!a && b) return launch2<BN, false, 0, 1>(g, tiles, st);
+  if (a && b) return launch2<BN, false, 1, 1>(g, tiles, st);
+  return launch2<BN, false, 1, 0>(g, tiles, st);
 }
 
 }  // namespace tc
 
-// Workspace layout: [0, SK_FLAG_BYTES) stream-K ready flags (zeroed once per
-// workspace, then only written with launch-unique epochs), then either split-K
-// partial tiles (1-CTA kernel) or stream-K tail partials (CTA-pair kernel).
-constexpr int64_t SK_FLAG_BYTES = 64 << 10;
-static std::mutex g_sk_mu;
-static std::unordered_set<const void*> g_sk_ready;   // workspaces whose flag region is zeroed
-static uint32_t g_sk_epoch = 0;
 static int g_raster_group = [] {   // BM_GEMM_GROUP: measurement override of the pair raster
   const char* e = getenv("BM_GEMM_GROUP");
   const int v = e ? atoi(e) : 8;
@@ -1309,26 +1286,67 @@ static int g_mbar_cluster = [] {   // default: the fully validated .acquire.clus
   const char* e = getenv("BM_MBAR_SCOPE");
   return e && std::string(e) == "cta" ? 0 : 1;
 }();
-static int g_sk_tma = [] {   // BM_SK_TMA=0: per-lane partial stores instead of TMA stores
-  const char* e = getenv("BM_SK_TMA");
-  return e ? (e[0] == '0' ? 0 : 1) : 1;
-}();
-static int g_split_rem = [] {   // BM_SPLIT_REM=1: DP + split-remainder schedule (opt-in: measured slower)
-  const char* e = getenv("BM_SPLIT_REM");
-  return e ? (e[0] == '1' ? 1 : 0) : 0;
-}();
-static int g_stream_k = [] {
-  const char* e = getenv("BM_STREAM_K");
-  return e ? (e[0] == '1' ? 1 : 0) : 0;   // opt-in: measured slower
-}();
-
 // 0 = auto (CTA pairs for large contractions), 1 = force 1-CTA, 2 = force CTA pairs
 static int g_gemm_mode = [] {
   const char* e = getenv("BM_GEMM_MODE");
   return e ? (e[0] == '1' ? 1 : (e[0] == '2' ? 2 : 0)) : 0;
 }();
 int gemm_mode() { return g_gemm_mode; }
+// BM_GEMM_GROUP_INTERLEAVE=0: keep each pair's grouped tiles problem by problem (measurement)
+static int g_group_interleave = [] {
+  const char* e = getenv("BM_GEMM_GROUP_INTERLEAVE");
+  return e && e[0] == '0' ? 0 : 1;
+}();
+// BM_GEMM_GROUP_RR=1: grouped pair launches deal tiles round-robin instead of the LPT schedule (measurement)
+static int g_group_rr = [] {
+  const char* e = getenv("BM_GEMM_GROUP_RR");
+  return e && e[0] == '1' ? 1 : 0;
+}();
 void set_gemm_mode(int m) { g_gemm_mode = m; }
+
+// fills the epilogue arguments and the output map of one contraction
+static bm_status prepare_out(int M, int N, int K, void* Cp, int64_t ldc, int c_dtype, int epi, const void* R,
+                             int64_t ldr, float alpha, int f, tc::EpiArgs* ea, CUtensorMap* mc) {
+  using namespace tc;
+  *ea = EpiArgs{M, N, K, Cp, ldc, c_dtype == BM_F32 ? 1 : 0, epi, R, ldr, alpha, f, 0, 1, 1 << 30, 0, 8, 1};
+  ea->group = g_raster_group;
+  ea->mbar_cluster = g_mbar_cluster;
+  std::memset(mc, 0, sizeof(*mc));
+  const int ces = c_dtype == BM_F32 ? 4 : 2;
+  if (epi == BM_EPI_DSWIGLU) {
+    BM_CHECK_ARG(c_dtype == BM_BF16 && N == f && f % 32 == 0 && ldc >= 2 * f && ldr >= 2 * f &&
+                     (reinterpret_cast<uintptr_t>(R) & 15) == 0 && ldr % 8 == 0,
+                 "DSWIGLU epilogue: bf16, N = f, f % 32 == 0, C/R are [M, 2f], 16-byte aligned");
+    if (tma_out_ok(Cp, ldc, 2)) {
+      BM_TRY(make_map_k(Cp, 2 * (uint64_t)f, M, ldc, 32, 1, mc));
+      ea->tma = 1;
+    }
+  } else if (tma_out_ok(Cp, ldc, ces)) {
+    BM_TRY(make_map_k(Cp, (uint64_t)N, M, ldc, 32, c_dtype == BM_F32 ? 2 : 1, mc));
+    ea->tma = 1;
+  }
+  return BM_OK;
+}
+
+// one CTA-pair problem (256 x BN2 tiles) of a (grouped) pair launch
+static bm_status pair_problem(int M, int N, int K, const void* A, int64_t lda, int a_major, const void* B,
+                              int64_t ldb, int b_major, void* Cp, int64_t ldc, int c_dtype, int epi, const void* R,
+                              int64_t ldr, float alpha, int f, int BN2, tc::PairProblem* pr) {
+  using namespace tc;
+  std::memset(pr, 0, sizeof(*pr));
+  BM_TRY(prepare_out(M, N, K, Cp, ldc, c_dtype, epi, R, ldr, alpha, f, &pr->ea, &pr->tmC));
+  pr->tmC2 = pr->tmC;
+  if (a_major == 0) BM_TRY(make_map(A, K, M, lda, BM, &pr->tmA));
+  else BM_TRY(make_map(A, M, K, lda, BK, &pr->tmA));
+  if (b_major == 0) BM_TRY(make_map(B, K, N, ldb, BN2 / 2, &pr->tmB));
+  else BM_TRY(make_map(B, N, K, ldb, BK, &pr->tmB));
+  pr->a_mn = a_major != 0;
+  pr->b_mn = b_major != 0;
+  pr->tiles_m = ceil_div(M, 2 * BM);
+  pr->tiles_n = ceil_div(N, BN2);
+  pr->nk = ceil_div(K, BK);
+  return BM_OK;
+}
 
 bm_status gemm_bf16_tc(int M, int N, int K, const void* A, int64_t lda, int a_major, const void* B, int64_t ldb,
                        int b_major, void* Cp, int64_t ldc, int c_dtype, int epi, const void* R, int64_t ldr,
@@ -1338,36 +1356,30 @@ bm_status gemm_bf16_tc(int M, int N, int K, const void* A, int64_t lda, int a_ma
   BM_CHECK_ARG((reinterpret_cast<uintptr_t>(A) & 15) == 0 && (reinterpret_cast<uintptr_t>(B) & 15) == 0,
                "A/B must be 16-byte aligned");
   const bool amn = a_major != 0, bmn = b_major != 0;
-  EpiArgs ea{M, N, K, Cp, ldc, c_dtype == BM_F32 ? 1 : 0, epi, R, ldr, alpha, f, 0, 1, 1 << 30, 0};
-  ea.group = g_raster_group;
-  ea.mbar_cluster = g_mbar_cluster;
-  CUtensorMap ma, mb, mc, mc2;
-  std::memset(&mc, 0, sizeof(mc));
-  std::memset(&mc2, 0, sizeof(mc2));
-  const int ces = c_dtype == BM_F32 ? 4 : 2;
   if (epi == BM_EPI_SWIGLU) {
     // gate/up GEMM with fused SwiGLU: always CTA pairs, BN = 256 (128 gate + 128 up features)
     BM_CHECK_ARG(b_major == 0 && c_dtype == BM_BF16 && N == 2 * f && f % 128 == 0, "SWIGLU epilogue: K-major B, bf16, N = 2f, f % 128 == 0");
-    if (a_major == 0) BM_TRY(make_map(A, K, M, lda, BM, &ma));
-    else BM_TRY(make_map(A, M, K, lda, BK, &ma));
-    BM_TRY(make_map(B, K, N, ldb, 128, &mb));
+    PairGroup g;
+    std::memset(&g, 0, sizeof(g));
+    PairProblem& pr = g.prob[0];
+    pr.ea = EpiArgs{M, N, K, Cp, ldc, 0, epi, R, ldr, alpha, f, 0, 1, 1 << 30, 0, g_raster_group, g_mbar_cluster};
+    if (a_major == 0) BM_TRY(make_map(A, K, M, lda, BM, &pr.tmA));
+    else BM_TRY(make_map(A, M, K, lda, BK, &pr.tmA));
+    BM_TRY(make_map(B, K, N, ldb, 128, &pr.tmB));
     if (tma_out_ok(Cp, ldc, 2) && tma_out_ok(R, ldr, 2)) {
-      BM_TRY(make_map_k(Cp, 2 * (uint64_t)f, M, ldc, 32, 1, &mc));
-      BM_TRY(make_map_k(R, (uint64_t)f, M, ldr, 32, 1, &mc2));
-      ea.tma = 1;
+      BM_TRY(make_map_k(Cp, 2 * (uint64_t)f, M, ldc, 32, 1, &pr.tmC));
+      BM_TRY(make_map_k(R, (uint64_t)f, M, ldr, 32, 1, &pr.tmC2));
+      pr.ea.tma = 1;
     }
-    if (a_major == 0) return launch2<256, false, false, true>(ma, mb, mc, mc2, ea, st);
-    return launch2<256, true, false, true>(ma, mb, mc, mc2, ea, st);
-  }
-  if (epi == BM_EPI_DSWIGLU) {
-    BM_CHECK_ARG(c_dtype == BM_BF16 && N == f && ldc >= 2 * f && ldr >= 2 * f, "DSWIGLU epilogue: bf16, N = f, C/R are [M, 2f]");
-    if (tma_out_ok(Cp, ldc, 2)) {
-      BM_TRY(make_map_k(Cp, 2 * (uint64_t)f, M, ldc, 32, 1, &mc));
-      ea.tma = 1;
-    }
-  } else if (tma_out_ok(Cp, ldc, ces)) {
-    BM_TRY(make_map_k(Cp, (uint64_t)N, M, ldc, 32, c_dtype == BM_F32 ? 2 : 1, &mc));
-    ea.tma = 1;
+    pr.a_mn = a_major != 0;
+    pr.b_mn = 0;
+    pr.tiles_m = ceil_div(M, 2 * BM);
+    pr.tiles_n = ceil_div(f, 128);
+    pr.nk = ceil_div(K, BK);
+    g.nprob = 1;
+    g.tiles0 = g.total_tiles = pr.tiles_m * pr.tiles_n;
+    if (a_major == 0) return launch2<256, true, 0, 0>(g, g.total_tiles, st);
+    return launch2<256, true, 1, 0>(g, g.total_tiles, st);
   }
   // CTA pairs for the large contractions (enough 256-row tiles to fill the
   // machine), 1-CTA tiles otherwise
@@ -1376,69 +1388,18 @@ bm_status gemm_bf16_tc(int M, int N, int K, const void* A, int64_t lda, int a_ma
   const bool pair = mode == 2 || (mode == 0 && M >= 256 && N >= 256 && K >= 256 && pair_tiles >= num_sms() / 2);
   if (pair) {
     const int BN2 = (N >= 256) ? 256 : 128;
-    if (a_major == 0) BM_TRY(make_map(A, K, M, lda, BM, &ma));
-    else BM_TRY(make_map(A, M, K, lda, BK, &ma));
-    if (b_major == 0) BM_TRY(make_map(B, K, N, ldb, BN2 / 2, &mb));
-    else BM_TRY(make_map(B, N, K, ldb, BK, &mb));
-    // stream-K when whole-tile waves would leave > 5 % of the pairs idle (e.g. the
-    // C2 d = 2048 contractions: 128 tiles on 74 pairs = 1.73 waves -> 2)
-    const int pairs = gemm_sm_budget() / 2;
-    const int64_t tiles2 = (int64_t)ceil_div(M, 2 * BM) * ceil_div(N, BN2);
-    const int64_t waves = (tiles2 + pairs - 1) / pairs;
-    const int64_t sk_need = SK_FLAG_BYTES + (int64_t)pairs * 2 * BM * BN2 * 4;
-    CUtensorMap mws2;
-    bool have_mws2 = false;
-    // DP + split remainder (opt-in): whole-tile waves, then the remainder tiles cut
-    // into s k-ranges with s minimising ceil(rem s / pairs) / s (ties: smaller s)
-    const int nkb = ceil_div(K, BK);
-    const int64_t dp_t = tiles2 / pairs * pairs, rem_t = tiles2 - dp_t;
-    int best_s = 1;
-    double best = 1.0;
-    for (int sp = 2; sp <= 4 && sp <= nkb && rem_t > 0; ++sp) {   // s <= 4 bounds the partial traffic
-      const double r = (double)((rem_t * sp + pairs - 1) / pairs) / sp;
-      if (r < best - 1e-9) { best = r; best_s = sp; }
-    }
-    const int64_t hy_need = SK_FLAG_BYTES + rem_t * (best_s - 1) * 2 * BM * BN2 * 4;
-    const bool hybrid = g_split_rem && g_stream_k == 0 && ws && BN2 == 256 && tiles2 >= pairs && rem_t > 0 &&
-                        best <= 0.9 && best_s <= nkb && ws_bytes >= hy_need &&
-                        rem_t * (best_s - 1) * 2 * EPI_WARPS2 * 4 <= SK_FLAG_BYTES;
-    if (hybrid) {
-      {
-        std::lock_guard<std::mutex> lk(g_sk_mu);
-        if (!g_sk_ready.count(ws)) {
-          BM_CUDA_TRY(cudaMemsetAsync(ws, 0, SK_FLAG_BYTES, st));
-          g_sk_ready.insert(ws);
-        }
-        ea.sk_epoch = ++g_sk_epoch;
-      }
-      ea.sk = 2;
-      ea.dp_tiles = (int)dp_t;
-      ea.rem = (int)rem_t;
-      ea.ksplit = best_s;
-      ea.sk_flags = reinterpret_cast<uint32_t*>(ws);
-      ea.sk_ws = reinterpret_cast<float*>(reinterpret_cast<char*>(ws) + SK_FLAG_BYTES);
-      if (g_sk_tma) {
-        BM_TRY(make_map_k(ea.sk_ws, (uint64_t)BN2, (uint64_t)rem_t * (best_s - 1) * 2 * BM, BN2, 32, 2, &mws2));
-        ea.sk_tma = 1;
-        have_mws2 = true;
-      }
-    } else if (g_stream_k && ws && ws_bytes >= sk_need && BN2 == 256 && tiles2 >= pairs && tiles2 % pairs != 0 &&
-        (double)tiles2 / (double)(waves * pairs) < 0.95 && (int64_t)ceil_div(K, BK) >= 2) {
-      {
-        std::lock_guard<std::mutex> lk(g_sk_mu);
-        if (!g_sk_ready.count(ws)) {
-          BM_CUDA_TRY(cudaMemsetAsync(ws, 0, SK_FLAG_BYTES, st));
-          g_sk_ready.insert(ws);
-        }
-        ea.sk_epoch = ++g_sk_epoch;
-      }
-      ea.sk = 1;
-      ea.sk_flags = reinterpret_cast<uint32_t*>(ws);
-      ea.sk_ws = reinterpret_cast<float*>(reinterpret_cast<char*>(ws) + SK_FLAG_BYTES);
-    }
-    if (BN2 == 256) return dispatch_majors2<256>(amn, bmn, ma, mb, mc, ea, st, have_mws2 ? &mws2 : nullptr);
-    return dispatch_majors2<128>(amn, bmn, ma, mb, mc, ea, st);
+    PairGroup g;
+    std::memset(&g, 0, sizeof(g));
+    BM_TRY(pair_problem(M, N, K, A, lda, a_major, B, ldb, b_major, Cp, ldc, c_dtype, epi, R, ldr, alpha, f, BN2,
+                        &g.prob[0]));
+    g.nprob = 1;
+    g.tiles0 = g.total_tiles = g.prob[0].tiles_m * g.prob[0].tiles_n;
+    if (BN2 == 256) return launch2_static<256>(g, g.total_tiles, st);
+    return launch2_static<128>(g, g.total_tiles, st);
   }
+  EpiArgs ea;
+  CUtensorMap ma, mb, mc;
+  BM_TRY(prepare_out(M, N, K, Cp, ldc, c_dtype, epi, R, ldr, alpha, f, &ea, &mc));
   // 1-CTA tiles: the largest BN that still gives ~a full wave of CTAs (small
   // encoder / generator contractions have only a few 128-row tiles)
   int BN = (N <= 64) ? 64 : (N <= 128 ? 128 : 256);
@@ -1452,12 +1413,10 @@ bm_status gemm_bf16_tc(int M, int N, int K, const void* A, int64_t lda, int a_ma
   // partial tiles in the caller's workspace, summed in split order)
   const int tiles = tm * ceil_div(N, BN);
   const int nk = ceil_div(K, BK);
-  if (ws && ws_bytes > SK_FLAG_BYTES && tiles < num_sms() / 2 && nk >= 4 && N % 4 == 0 &&
+  if (ws && ws_bytes > 0 && tiles < num_sms() / 2 && nk >= 4 && N % 4 == 0 &&
       (epi == BM_EPI_STORE || epi == BM_EPI_ADD || epi == BM_EPI_ACCUM)) {
     int splits = std::min(8, std::min(num_sms() / tiles, nk / 2));
     const int mpad = tm * BM;
-    ws = reinterpret_cast<char*>(ws) + SK_FLAG_BYTES;   // keep the stream-K flag region intact
-    ws_bytes -= SK_FLAG_BYTES;
     while (splits > 1 && (int64_t)splits * mpad * N * 4 > ws_bytes) --splits;
     if (splits > 1) {
       const int kb_per = ceil_div(nk, splits);
@@ -1487,6 +1446,127 @@ bm_status gemm_bf16_tc(int M, int N, int K, const void* A, int64_t lda, int a_ma
   return dispatch_majors<256>(amn, bmn, ma, mb, mc, ea, st);
 }
 
+// ---------------------------------------------------------------- grouped pair launches
+// Static schedule of several independent contractions on the CTA pairs:
+// longest-processing-time list scheduling with a tile's cost = its k-blocks
+// (every 256 x 256 tile of a problem costs the same), problems with longer
+// tiles first, each problem's tiles in raster order.  Cached per shape set.
+struct WorkKey {
+  std::vector<int> k;
+  bool operator==(const WorkKey& o) const { return k == o.k; }
+};
+struct WorkKeyHash {
+  size_t operator()(const WorkKey& w) const {
+    size_t h = 0;
+    for (int v : w.k) h = h * 1000003u ^ (size_t)v;
+    return h;
+  }
+};
+static std::mutex g_work_mu;
+static std::unordered_map<WorkKey, std::pair<int*, int*>, WorkKeyHash> g_work;
+
+static bm_status pair_schedule(const tc::PairGroup& g, int pairs, const int** work, const int** work_off) {
+  WorkKey key;
+  key.k.push_back(pairs);
+  for (int p = 0; p < g.nprob; ++p) {
+    key.k.push_back(g.prob[p].tiles_m);
+    key.k.push_back(g.prob[p].tiles_n);
+    key.k.push_back(g.prob[p].nk);
+  }
+  std::lock_guard<std::mutex> lk(g_work_mu);
+  auto it = g_work.find(key);
+  if (it == g_work.end()) {
+    std::vector<int> order(g.nprob);
+    for (int p = 0; p < g.nprob; ++p) order[p] = p;
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return g.prob[a].nk > g.prob[b].nk; });
+    std::vector<std::vector<int>> per(pairs);
+    std::vector<int64_t> load(pairs, 0);
+    for (int p : order) {
+      const int tiles = g.prob[p].tiles_m * g.prob[p].tiles_n;
+      for (int t = 0; t < tiles; ++t) {
+        int best = 0;
+        for (int q = 1; q < pairs; ++q)
+          if (load[q] < load[best]) best = q;   // ties: lowest pair (deterministic)
+        per[best].push_back((p << 24) | t);
+        load[best] += g.prob[p].nk;
+      }
+    }
+    // alternate the problems within each pair's list (same set of tiles, same load):
+    // a tile with a heavy epilogue (fused SwiGLU backward, fp32 reduce-add) then runs
+    // its epilogue under the next tile's mainloop of the other problem
+    if (g_group_interleave && g.nprob == 2) {
+      for (auto& lst : per) {
+        std::vector<int> a, b, m;
+        for (int it : lst) ((it >> 24) == order[0] ? a : b).push_back(it);
+        size_t i = 0, j = 0;
+        while (i < a.size() || j < b.size()) {
+          if (i < a.size()) m.push_back(a[i++]);
+          if (j < b.size()) m.push_back(b[j++]);
+        }
+        lst.swap(m);
+      }
+    }
+    std::vector<int> flat, off(pairs + 1, 0);
+    for (int q = 0; q < pairs; ++q) {
+      off[q] = (int)flat.size();
+      flat.insert(flat.end(), per[q].begin(), per[q].end());
+    }
+    off[pairs] = (int)flat.size();
+    int *dw = nullptr, *doff = nullptr;
+    BM_CUDA_TRY(cudaMalloc(&dw, std::max<size_t>(flat.size(), 1) * sizeof(int)));
+    BM_CUDA_TRY(cudaMalloc(&doff, off.size() * sizeof(int)));
+    BM_CUDA_TRY(cudaMemcpy(dw, flat.data(), flat.size() * sizeof(int), cudaMemcpyHostToDevice));
+    BM_CUDA_TRY(cudaMemcpy(doff, off.data(), off.size() * sizeof(int), cudaMemcpyHostToDevice));
+    it = g_work.emplace(key, std::make_pair(dw, doff)).first;
+  }
+  *work = it->second.first;
+  *work_off = it->second.second;
+  return BM_OK;
+}
+
+bm_status gemm_bf16_tc_group(const GemmSpec* sp, int n, cudaStream_t st) {
+  using namespace tc;
+  BM_CHECK_ARG(n >= 1 && n <= MAX_PAIR_PROBLEMS, "group of 1..2 contractions");
+  const int mode = gemm_mode();
+  bool ok = mode != 1;
+  int64_t ptiles = 0;
+  for (int i = 0; i < n; ++i) {
+    const GemmSpec& s = sp[i];
+    BM_CHECK_ARG(s.M > 0 && s.N > 0 && s.K > 0, "grouped GEMM: empty contraction");
+    ok = ok && s.epi != BM_EPI_SWIGLU && s.N >= 256 && s.M >= 256 && s.K >= 64 && s.lda % 8 == 0 &&
+         s.ldb % 8 == 0 && (reinterpret_cast<uintptr_t>(s.A) & 15) == 0 && (reinterpret_cast<uintptr_t>(s.B) & 15) == 0;
+    ptiles += (int64_t)ceil_div(s.M, 2 * BM) * ceil_div(s.N, 256);
+  }
+  // auto mode: like single launches, CTA pairs only when the group fills the machine
+  ok = ok && (mode == 2 || ptiles >= num_sms() / 2);
+  if (!ok || n == 1) {   // not pair-shaped: one launch per contraction
+    for (int i = 0; i < n; ++i) {
+      const GemmSpec& s = sp[i];
+      BM_TRY(gemm_bf16_tc(s.M, s.N, s.K, s.A, s.lda, s.a_major, s.B, s.ldb, s.b_major, s.C, s.ldc, s.c_dtype, s.epi,
+                          s.R, s.ldr, s.alpha, st, s.f, s.ws, s.ws_bytes));
+    }
+    return BM_OK;
+  }
+  PairGroup g;
+  std::memset(&g, 0, sizeof(g));
+  int tiles = 0;
+  for (int i = 0; i < n; ++i) {
+    const GemmSpec& s = sp[i];
+    BM_TRY(pair_problem(s.M, s.N, s.K, s.A, s.lda, s.a_major, s.B, s.ldb, s.b_major, s.C, s.ldc, s.c_dtype, s.epi, s.R,
+                        s.ldr, s.alpha, s.f, 256, &g.prob[i]));
+    tiles += g.prob[i].tiles_m * g.prob[i].tiles_n;
+  }
+  g.nprob = n;
+  g.tiles0 = g.prob[0].tiles_m * g.prob[0].tiles_n;
+  g.total_tiles = tiles;
+  const int pairs = std::min(gemm_sm_budget() / 2, tiles);
+  if (!g_group_rr) BM_TRY(pair_schedule(g, pairs, &g.work, &g.work_off));
+  bool b_all_mn = true;
+  for (int i = 0; i < n; ++i) b_all_mn = b_all_mn && g.prob[i].b_mn;
+  if (b_all_mn) return launch2<256, false, -1, 1>(g, tiles, st);   // a Linear's dgrad + wgrad: B MN-major
+  return launch2<256>(g, tiles, st);
+}
+
 // every tcgen05 GEMM instantiation the dispatcher can launch (bm::preload_kernels)
 template <int BN>
 static void preload_bn(std::vector<const void*>& v) {
@@ -1495,21 +1575,18 @@ static void preload_bn(std::vector<const void*>& v) {
                         (const void*)gemm_kernel<BN, true, true>, (const void*)gemm_kernel<BN, true, false>})
     v.push_back(f);
 }
-template <int BN>
-static void preload_bn2(std::vector<const void*>& v) {
-  using namespace tc;
-  for (const void* f : {(const void*)gemm2_kernel<BN, false, false, false>, (const void*)gemm2_kernel<BN, false, true, false>,
-                        (const void*)gemm2_kernel<BN, true, true, false>, (const void*)gemm2_kernel<BN, true, false, false>})
-    v.push_back(f);
-}
 void preload_tc(std::vector<const void*>& v) {
   preload_bn<64>(v);
   preload_bn<128>(v);
   preload_bn<256>(v);
-  preload_bn2<128>(v);
-  preload_bn2<256>(v);
-  v.push_back((const void*)tc::gemm2_kernel<256, false, false, true>);
-  v.push_back((const void*)tc::gemm2_kernel<256, true, false, true>);
+  v.push_back((const void*)tc::gemm2_kernel<256, false>);   // grouped (run-time majors)
+  v.push_back((const void*)tc::gemm2_kernel<256, false, -1, 1>);
+  for (const void* f : {(const void*)tc::gemm2_kernel<128, false, 0, 0>, (const void*)tc::gemm2_kernel<128, false, 0, 1>,
+                        (const void*)tc::gemm2_kernel<128, false, 1, 1>, (const void*)tc::gemm2_kernel<128, false, 1, 0>,
+                        (const void*)tc::gemm2_kernel<256, false, 0, 0>, (const void*)tc::gemm2_kernel<256, false, 0, 1>,
+                        (const void*)tc::gemm2_kernel<256, false, 1, 1>, (const void*)tc::gemm2_kernel<256, false, 1, 0>,
+                        (const void*)tc::gemm2_kernel<256, true, 0, 0>, (const void*)tc::gemm2_kernel<256, true, 1, 0>})
+    v.push_back(f);
   v.push_back((const void*)tc::splitk_reduce_kernel);
 }
 

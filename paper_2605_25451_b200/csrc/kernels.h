@@ -12,6 +12,29 @@ bm_status gemm_bf16_tc(int M, int N, int K, const void* A, int64_t lda, int a_ma
 bm_status gemm_f32_simt(int M, int N, int K, const float* A, int64_t lda, int a_major, const float* B, int64_t ldb,
                         int b_major, float* C, int64_t ldc, int epi, const float* R, int64_t ldr, float alpha,
                         cudaStream_t st);
+// one contraction C = epilogue(alpha A B^T) (gemm_bf16_tc's arguments)
+struct GemmSpec {
+  int M, N, K;
+  const void* A;
+  int64_t lda;
+  int a_major;
+  const void* B;
+  int64_t ldb;
+  int b_major;
+  void* C;
+  int64_t ldc;
+  int c_dtype, epi;
+  const void* R;
+  int64_t ldr;
+  float alpha;
+  int f;
+  void* ws;
+  int64_t ws_bytes;
+};
+// independent bf16 contractions (n <= 2, e.g. a Linear's data and weight gradient) in
+// ONE persistent CTA-pair launch on a longest-processing-time tile schedule; shapes
+// that do not fit the pair kernel fall back to one gemm_bf16_tc launch each
+bm_status gemm_bf16_tc_group(const GemmSpec* specs, int n, cudaStream_t st);
 // dtype-dispatching GEMM (bf16 -> tcgen05, fp32 -> exact FFMA)
 bm_status gemm(int dtype, int M, int N, int K, const void* A, int64_t lda, int a_major, const void* B, int64_t ldb,
                int b_major, void* C, int64_t ldc, int c_dtype, int epi, const void* R, int64_t ldr, float alpha,

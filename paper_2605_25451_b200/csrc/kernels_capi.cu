@@ -142,6 +142,15 @@ bm_status bm_k_gemm_swiglu(int32_t M, int32_t f, int32_t K, const void* X, int64
               ST(stream), f);
 }
 
+bm_status bm_k_gemm_group(const bm_gemm_desc* d, int32_t n, void* stream) {
+  BM_CHECK_ARG(d && n >= 1 && n <= 2, "1..2 descriptors");
+  GemmSpec sp[2];
+  for (int i = 0; i < n; ++i)
+    sp[i] = GemmSpec{d[i].M, d[i].N, d[i].K, d[i].A, d[i].lda, d[i].a_major, d[i].B, d[i].ldb, d[i].b_major, d[i].C,
+                     d[i].ldc, d[i].c_dtype, d[i].epilogue, d[i].R, d[i].ldr, d[i].alpha, d[i].f, nullptr, 0};
+  return gemm_bf16_tc_group(sp, n, ST(stream));
+}
+
 bm_status bm_k_gemm_dswiglu(int32_t M, int32_t f, int32_t K, const void* dY, int64_t lddy, const void* W, int64_t ldw,
                             const void* gu, void* dgu, void* stream) {
   return gemm(BM_BF16, M, f, K, dY, lddy, 0, W, ldw, 1, dgu, 2 * (int64_t)f, BM_BF16, BM_EPI_DSWIGLU, gu,

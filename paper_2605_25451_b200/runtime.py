@@ -116,13 +116,13 @@ class Runtime:
             n = max(int(nbytes), 256)
             t = (torch.zeros if zero else torch.empty)(n + 256, dtype=torch.uint8, device=self.device)
             off = (-t.data_ptr()) % 256
-            return t, t.data_ptr() + off
+            return t, t.data_ptr() + off, n
 
-        self._w, self.w_ptr = alloc(sz.weight_bytes)
-        self._g, self.g_ptr = alloc(sz.grad_bytes)
-        self._work, self.work_ptr = alloc(sz.work_bytes)
-        self._comm, self.comm_ptr = alloc(sz.comm_bytes, zero=True)
-        bufs = L.Buffers(self.w_ptr, self.g_ptr, self.work_ptr, self.comm_ptr)
+        self._w, self.w_ptr, wb = alloc(sz.weight_bytes)
+        self._g, self.g_ptr, gb = alloc(sz.grad_bytes)
+        self._work, self.work_ptr, kb = alloc(sz.work_bytes)
+        self._comm, self.comm_ptr, cb = alloc(sz.comm_bytes, zero=True)
+        bufs = L.Buffers(self.w_ptr, self.g_ptr, self.work_ptr, self.comm_ptr, wb, gb, kb, cb)
         L.call("bm_ctx_bind", self.ctx, C.byref(bufs))
         # parameter table
         n, tot, dp = C.c_int32(), C.c_int64(), C.c_int64()
@@ -335,6 +335,11 @@ class Runtime:
         self._stream.wait_stream(cur)
         L.call("bm_step", self.ctx, C.byref(db.struct), C.c_void_p(self._stream.cuda_stream))
         cur.wait_stream(self._stream)
+
+    def step_wait(self, timeout_s: float = 0.0):
+        """Block until the last step finished; BigMacError(E_TIMEOUT) naming the blocked
+        op if it did not within timeout_s seconds (<= 0: no limit)."""
+        L.call("bm_step_wait", self.ctx, int(timeout_s * 1000))
 
     def loss_tensor(self) -> torch.Tensor:
         p = C.c_void_p()

@@ -3,6 +3,7 @@ between iterations) next to cuBLAS (torch.matmul) for context.
 
     python scripts/gemm_bench.py [--json out.json]
 """
+import ctypes
 import json
 import os
 import sys
@@ -104,7 +105,38 @@ def main():
         L.call("bm_k_gemm", 0, S, f, d, dY.data_ptr(), d, 0, Wd.data_ptr(), f, 1, dh.data_ptr(), f, 0, 0, None, 0, 1.0, None)
         L.call("bm_k_swiglu_bwd", 0, S, f, dh.data_ptr(), gu.data_ptr(), dgu.data_ptr(), None)
 
-    for name, fn, fl in [("gate_up+swiglu fused", fused_fwd, 2.0 * S * 2 * f * d),
+    # a Linear's backward: weight + data gradient in one grouped launch vs two launches
+    dW_gu = torch.zeros((2 * f, d), device="cuda", dtype=torch.float32)
+    dW_d = torch.zeros((d, f), device="cuda", dtype=torch.float32)
+    dxn = torch.empty((S, d), device="cuda", dtype=torch.bfloat16)
+    hh = torch.randn((S, f), device="cuda").to(torch.bfloat16)
+    D = L.GemmDesc
+    down_w = D(d, f, S, dY.data_ptr(), d, 1, hh.data_ptr(), f, 1, dW_d.data_ptr(), f, 1, 1, None, 0, 1.0, 0)
+    down_dg = D(S, f, d, dY.data_ptr(), d, 0, Wd.data_ptr(), f, 1, dgu.data_ptr(), 2 * f, 0, 4, gu.data_ptr(), 2 * f, 1.0, f)
+    gu_dg = D(S, d, 2 * f, dgu.data_ptr(), 2 * f, 0, Wgu.data_ptr(), d, 1, dxn.data_ptr(), d, 0, 0, None, 0, 1.0, 0)
+    gu_w = D(2 * f, d, S, dgu.data_ptr(), 2 * f, 1, X.data_ptr(), d, 1, dW_gu.data_ptr(), d, 1, 1, None, 0, 1.0, 0)
+    down_pair = (D * 2)(down_w, down_dg)
+    gu_pair = (D * 2)(gu_dg, gu_w)
+
+    def down_grouped():
+        L.call("bm_k_gemm_group", down_pair, 2, None)
+
+    def down_separate():
+        L.call("bm_k_gemm_group", down_pair, 1, None)
+        L.call("bm_k_gemm_group", ctypes.byref(down_dg), 1, None)
+
+    def gu_grouped():
+        L.call("bm_k_gemm_group", gu_pair, 2, None)
+
+    def gu_separate():
+        L.call("bm_k_gemm_group", gu_pair, 1, None)
+        L.call("bm_k_gemm_group", ctypes.byref(gu_w), 1, None)
+
+    for name, fn, fl in [("down bwd grouped (wgrad + dgrad/dswiglu)", down_grouped, 4.0 * S * f * d),
+                         ("down bwd separate", down_separate, 4.0 * S * f * d),
+                         ("gate_up bwd grouped (dgrad + wgrad)", gu_grouped, 8.0 * S * f * d),
+                         ("gate_up bwd separate", gu_separate, 8.0 * S * f * d),
+                         ("gate_up+swiglu fused", fused_fwd, 2.0 * S * 2 * f * d),
                          ("gate_up + swiglu kernel", unfused_fwd, 2.0 * S * 2 * f * d),
                          ("down dgrad+dswiglu fused", fused_bwd, 2.0 * S * f * d),
                          ("down dgrad + swiglu_bwd kernel", unfused_bwd, 2.0 * S * f * d)]:

@@ -1,11 +1,21 @@
-"""One rank of a multi-GPU parity run (launched by tests/test_gpu_step.py via torchrun).
+"""Ranks of a multi-rank parity run (launched by tests/test_gpu_step.py via torchrun).
 
-usage: mp_step.py CONFIG P M V DTYPE GEN_PLACE[+head_dp][+last<n>] [D]
-D > 1: D pipeline replicas of P stages (world = P D); replica k runs microbatches
-[kM, (k+1)M) of one global batch of M D microbatches, and every gradient is
-compared with the oracle's gradient of that global batch.
-Every rank runs bm_step on its own GPU; rank 0 gathers all gradients and
-compares them with the fp64 oracle (normwise rel tol 1e-4 fp32 / 2e-2 bf16).
+usage: mp_step.py CASE [CASE ...]
+  CASE = CONFIG:P:M:V:DTYPE:SPEC:D[:FLAGS]   (FLAGS comma-separated: peer, gm2)
+Every case runs in the same processes, one after the other (one process start
+and CUDA context per rank for the whole batch).  world = P D for every case.
+D > 1: D pipeline replicas of P stages; replica k runs microbatches [kM, (k+1)M)
+of one global batch of M D microbatches, and every gradient is compared with the
+oracle's gradient of that global batch.  Rank 0 gathers all gradients and
+compares them with the fp64 oracle (normwise rel tol 1e-4 fp32 / 2e-2 bf16),
+printing one line "CASE <case> PARITY OK|FAIL ..." per case.
+SPEC: "<gen_place>", "entry_stage+<gen_place>" (memory-efficient baseline), "ce"
+(compute-efficient baseline: all encoder forwards first, W = M / P); modifiers
+"+head_dp" (LM head + CE DP-sharded with the generator), "+last<n>"
+(last_stage_layers = n), "+split<a>-<b>-..." (explicit stage_layers), "+edge"
+(degenerate row counts, synth.edge_counts).
+FLAGS: peer = force the library's peer-memory step-end sum (BM_STEP_SUM=peer);
+gm2 = every bf16 contraction on the CTA-pair GEMM (bm_k_gemm_mode 2).
 """
 import os
 
@@ -13,6 +23,8 @@ import os
 # stream parked on a credit wait must not block unrelated streams sharing its queue
 os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 import sys
+import time
+import traceback
 
 import numpy as np
 import torch
@@ -24,38 +36,11 @@ sys.path.insert(0, ROOT)
 from synth import edge_counts, edge_shape, get_config, make_batch, make_weights, slice_batch  # noqa: E402
 
 
-def main():
-    name, P, M, V, dtype, gen = sys.argv[1], int(sys.argv[2]), int(sys.argv[3]), int(sys.argv[4]), sys.argv[5], sys.argv[6]
-    D = int(sys.argv[7]) if len(sys.argv) > 7 else 1
-    rank = int(os.environ["RANK"])
-    world = int(os.environ["WORLD_SIZE"])
-    assert world == P * D, (world, P, D)
-    # BM_TEST_ONE_GPU=1: every rank on cuda:0 (the single-GPU multi-rank fixture: CUDA
-    # IPC works between processes of one device; the step-end sums then run over peer
-    # memory, bm_ctx_init_peer_sum, because NCCL rejects duplicate devices)
-    one_gpu = os.environ.get("BM_TEST_ONE_GPU") == "1"
-    torch.cuda.set_device(0 if one_gpu else int(os.environ.get("LOCAL_RANK", rank)))
-    dist.init_process_group("gloo")
-    from paper_2605_25451_b200.runtime import Runtime
-    edge = "edge" in gen.split("+")
-    gen = "+".join(t for t in gen.split("+") if t != "edge")
-    cfg = get_config(name, P=P, M=M, V=V)
-    cfg_global = get_config(name, P=P, M=M * D, V=V)
-    if edge:   # degenerate row counts (synth.edge_counts), buffers sized for [0, S]
-        cfg, cfg_global = edge_shape(cfg), edge_shape(cfg_global)
-        n_mod, n_gen = edge_counts(cfg_global, M * D)
-        W, B_global = make_weights(cfg), make_batch(cfg_global, n_mod=n_mod, n_gen=n_gen)
-    else:
-        W, B_global = make_weights(cfg), make_batch(cfg_global)
-    replica = rank // P
-    B = slice_batch(B_global, replica * M, (replica + 1) * M)
-    # strategy spec: "<gen_place>", "entry_stage+<gen_place>" (memory-efficient baseline),
-    # "ce" (compute-efficient baseline: all encoder forwards first, W = M / P);
-    # "<gen_place>+head_dp": the LM head + CE DP-sharded with the generator (BM_HEAD_DP_SHARD)
-    # "...+last<n>": last_stage_layers = n (uneven LLM layer partition, bigmac.h)
-    # "...+split<a>-<b>-...": explicit stage_layers
+def parse_spec(spec, M, P):
     head, last, split = "auto", 0, None
-    toks = gen.split("+")
+    toks = spec.split("+")
+    edge = "edge" in toks
+    toks = [t for t in toks if t != "edge"]
     for t in toks:
         if t.startswith("split"):
             split = [int(x) for x in t[5:].split("-")]
@@ -72,51 +57,122 @@ def main():
         kw = {"enc_place": "entry_stage", "gen_place": gen.split("+")[1]}
     else:
         kw = {"gen_place": gen}
+    return kw, head, last, split, edge
+
+
+def run_case(case, rank, world):
+    from paper_2605_25451_b200 import _lib as L
+    from paper_2605_25451_b200.runtime import Runtime
+    parts = case.split(":")
+    name, P, M, V, dtype, spec, D = parts[0], int(parts[1]), int(parts[2]), int(parts[3]), parts[4], parts[5], int(parts[6])
+    flags = parts[7].split(",") if len(parts) > 7 and parts[7] else []
+    assert world == P * D, (case, world)
+    kw, head, last, split, edge = parse_spec(spec, M, P)
+    cfg = get_config(name, P=P, M=M, V=V)
+    cfg_global = get_config(name, P=P, M=M * D, V=V)
+    if edge:   # degenerate row counts, buffers sized for [0, S]
+        cfg, cfg_global = edge_shape(cfg), edge_shape(cfg_global)
+        n_mod, n_gen = edge_counts(cfg_global, M * D)
+        W, B_global = make_weights(cfg), make_batch(cfg_global, n_mod=n_mod, n_gen=n_gen)
+    else:
+        W, B_global = make_weights(cfg), make_batch(cfg_global)
+    replica = rank // P
+    B = slice_batch(B_global, replica * M, (replica + 1) * M)
+    os.environ["BM_STEP_SUM"] = "peer" if "peer" in flags else "auto"
+    L.call("bm_k_gemm_mode", 2 if "gm2" in flags else 0)
     rt = Runtime(cfg, dtype, rank=rank, world=world, sched_kw=kw, head_place=head, last_stage_layers=last,
                  stage_layers=split)
     rt.load_weights(W)
     db = rt.device_batch(B)
     for _ in range(2):
         rt.step(db)
+    rt.step_wait(300.0)   # a hang becomes BM_E_TIMEOUT naming the blocked op
     torch.cuda.synchronize()
     loss, ce, mse = rt.losses()
     grads = {n: rt.grad(n) for n in rt.names()}
-    kinds = {n: rt.params[n][4] for n in rt.names()}
     allg = [None] * world
-    dist.gather_object((grads, kinds, loss, ce, mse), allg if rank == 0 else None, dst=0)
+    dist.gather_object((grads, loss, ce, mse), allg if rank == 0 else None, dst=0)
     if rank == 0:
         from oracle import model as om
         loss_ref, per_ref, G_ref = om.step_fp64(cfg_global, W, B_global)
         tol = 1e-4 if dtype == "f32" else 2e-2
-        ok = True
-        for r, (g, k, l_, c_, m_) in enumerate(allg):
+        msgs = []
+        for r, (g, l_, c_, m_) in enumerate(allg):
             if abs(l_ - loss_ref) > tol * abs(loss_ref):
-                print(f"rank {r} loss {l_} vs {loss_ref}")
-                ok = False
+                msgs.append(f"rank {r} loss {l_} vs {loss_ref}")
             q = r // P   # replica: its own microbatches' loss terms
             ce_ref = np.array([x for x, _ in per_ref[q * M:(q + 1) * M]])
             mse_ref = np.array([y for _, y in per_ref[q * M:(q + 1) * M]])
             if (np.linalg.norm(c_ - ce_ref) > tol * np.linalg.norm(ce_ref) or
                     np.linalg.norm(m_ - mse_ref) > tol * max(np.linalg.norm(mse_ref), 1e-30)):
-                print(f"rank {r} per-microbatch loss terms differ")
-                ok = False
+                msgs.append(f"rank {r} per-microbatch loss terms differ")
             for n, v in g.items():
                 ref = G_ref[n]
                 e = np.linalg.norm(v - ref) / max(np.linalg.norm(ref), 1e-30)
                 if e > tol:
-                    print(f"rank {r} grad {n} rel err {e:.3e}")
-                    ok = False
+                    msgs.append(f"rank {r} grad {n} rel err {e:.3e}")
         seen = set()
-        for g, _, _, _, _ in allg:
+        for g, _, _, _ in allg:
             seen |= set(g)
         missing = set(G_ref) - seen
         if missing:
-            print("missing grads", missing)
-            ok = False
-        print("PARITY OK" if ok else "PARITY FAIL", loss, loss_ref, "sum_mode", rt.sum_mode)
+            msgs.append(f"missing grads {sorted(missing)}")
+        verdict = "PARITY OK" if not msgs else "PARITY FAIL"
+        print(f"CASE {case} {verdict} loss {loss:.6f} oracle {loss_ref:.6f} sum_mode {rt.sum_mode} "
+              f"{'; '.join(msgs[:8])}", flush=True)
     dist.barrier()
     rt.close()
+    dist.barrier()
+
+
+def hang_case(rank, world):
+    """bm_step_wait: rank 1 skips its second step, so rank 0's second step blocks on a
+    flag that never comes; rank 0 must get BM_E_TIMEOUT naming the blocked op."""
+    from paper_2605_25451_b200 import _lib as L
+    from paper_2605_25451_b200.runtime import Runtime
+    cfg = get_config("C1", P=2, M=4, V=1)
+    rt = Runtime(cfg, "f32", rank=rank, world=world)
+    rt.load_weights(make_weights(cfg))
+    db = rt.device_batch(make_batch(cfg))
+    rt.step(db)
+    rt.step_wait(60.0)
+    dist.barrier()
+    if rank == 1:
+        time.sleep(25)      # keep the comm buffers mapped while rank 0 times out
+        os._exit(0)
+    rt.step(db)
+    try:
+        rt.step_wait(3.0)
+        print("CASE hang NO TIMEOUT", flush=True)
+    except L.BigMacError as e:
+        ok = e.code == 10 and "blocked at op" in str(e)
+        print(f"CASE hang {'TIMEOUT OK' if ok else 'TIMEOUT BAD'} {e}", flush=True)
+    os._exit(0)   # the blocked device work dies with the context
+
+
+def main():
+    cases = sys.argv[1:]
+    rank = int(os.environ["RANK"])
+    world = int(os.environ["WORLD_SIZE"])
+    # BM_TEST_ONE_GPU=1: every rank on cuda:0 (the single-GPU multi-rank fixture: CUDA
+    # IPC works between processes of one device; the step-end sums then run over peer
+    # memory, bm_ctx_init_peer_sum, because NCCL rejects duplicate devices)
+    one_gpu = os.environ.get("BM_TEST_ONE_GPU") == "1"
+    torch.cuda.set_device(0 if one_gpu else int(os.environ.get("LOCAL_RANK", rank)))
+    dist.init_process_group("gloo")
+    if cases == ["hang"]:
+        hang_case(rank, world)
+    failed = False
+    for case in cases:
+        try:
+            run_case(case, rank, world)
+        except Exception:
+            failed = True
+            if rank == 0:
+                print(f"CASE {case} PARITY ERROR {traceback.format_exc()[-1500:]!r}", flush=True)
+            break   # the group's collective state is unknown after an exception
     dist.destroy_process_group()
+    sys.exit(1 if failed else 0)
 
 
 if __name__ == "__main__":

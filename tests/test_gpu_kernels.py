@@ -69,10 +69,10 @@ def test_gemm_store_f32(L, M, N, K, a_mn, b_mn, dtype, mode):
 
 @pytest.mark.parametrize("M,N,K", [(2560, 2048, 512), (4096, 2048, 1024), (2304, 4352, 320)])
 @pytest.mark.parametrize("a_mn,b_mn", [(0, 0), (0, 1), (1, 1), (1, 0)])
-def test_gemm_stream_k(L, M, N, K, a_mn, b_mn):
-    """CTA-pair GEMMs whose whole-tile waves would leave pairs idle (80 / 128 / 153
-    256x256 tiles on 74 pairs) run stream-K: tiles cut between two pairs, the tail's
-    fp32 partial added by the head owner.  Checked against the fp64 product."""
+def test_gemm_pairs_partial_last_wave(L, M, N, K, a_mn, b_mn):
+    """CTA-pair GEMMs whose last wave of whole 256x256 tiles leaves pairs idle
+    (80 / 128 / 153 tiles on 74 pairs), every operand-major combination (runtime
+    majors of the pair kernel), against the fp64 product; bitwise deterministic."""
     L.call("bm_k_gemm_mode", 2)
     rng = np.random.default_rng(M + N + K + 3 * a_mn + b_mn)
     A, B = rnd(rng, M, K), rnd(rng, N, K)
@@ -286,3 +286,63 @@ def test_gemm_fused_swiglu(L, M, f, K):
     dh = dY @ Wdown
     dgu_ref = om.swiglu_bwd(dh, gu_out, f)
     assert np.abs(host(dgu) - dgu_ref).max() <= 1e-2 * max(1e-3, np.abs(dgu_ref).max())
+
+
+# grouped CTA-pair launches (bm_k_gemm_group): a Linear's weight gradient (fp32 TMA
+# reduce-add, A and B MN-major) and data gradient (bf16 store or the fused SwiGLU
+# backward, B MN-major) in one persistent launch on the LPT tile schedule
+GROUP_CASES = [
+    # (S rows, in, out, dgrad epilogue, gemm mode)
+    (4096, 2048, 8192, "store", 0),     # C2 gate_up-like: long-K dgrad + short-K wgrad
+    (4096, 8192, 2048, "dswiglu", 0),   # C2 down-like: dgrad with the SwiGLU backward
+    (520, 384, 640, "dswiglu", 2),      # ragged: partial m / n tiles, forced pairs
+    (768, 1280, 512, "store", 2),
+    (1000, 512, 2048, "store", 0),      # auto mode, too few tiles: separate 1-CTA launches
+]
+
+
+@pytest.mark.parametrize("S,n_in,n_out,dg_epi,mode", GROUP_CASES)
+def test_gemm_group_dgrad_wgrad(L, S, n_in, n_out, dg_epi, mode):
+    L.call("bm_k_gemm_mode", mode)
+    rng = np.random.default_rng(S + n_in + n_out)
+    dY = rnd(rng, S, n_out)                     # [S, out]
+    X = rnd(rng, S, n_in, scale=0.5)             # [S, in]
+    Wt = rnd(rng, n_out, n_in, scale=0.05)       # [out, in]
+    dYd, Xd, Wd = dev(dY, BF16), dev(X, BF16), dev(Wt, BF16)
+    dW0 = rnd(rng, n_out, n_in)
+    dW = torch.tensor(dW0, device="cuda", dtype=torch.float32)
+    D = L.GemmDesc
+    wgrad = D(n_out, n_in, S, dYd.data_ptr(), n_out, 1, Xd.data_ptr(), n_in, 1, dW.data_ptr(), n_in, F32, 1, None, 0,
+              1.0, 0)
+    if dg_epi == "store":
+        dX = torch.zeros((S, n_in), device="cuda", dtype=torch.bfloat16)
+        dgrad = D(S, n_in, n_out, dYd.data_ptr(), n_out, 0, Wd.data_ptr(), n_in, 1, dX.data_ptr(), n_in, BF16, 0, None,
+                  0, 1.0, 0)
+    else:   # the down projection's dgrad: N = f = n_in, C = dgu [S, 2f], R = gu [S, 2f]
+        f = n_in
+        gu_h = rnd(rng, S, 2 * f)
+        gu = dev(gu_h, BF16)
+        dX = torch.zeros((S, 2 * f), device="cuda", dtype=torch.bfloat16)
+        dgrad = D(S, f, n_out, dYd.data_ptr(), n_out, 0, Wd.data_ptr(), n_in, 1, dX.data_ptr(), 2 * f, BF16, 4,
+                  gu.data_ptr(), 2 * f, 1.0, f)
+    arr = (D * 2)(dgrad, wgrad)
+    L.call("bm_k_gemm_group", arr, 2, None)
+    torch.cuda.synchronize()
+    first = (dW.clone(), dX.clone())
+    L.call("bm_k_gemm_mode", 0)
+    dW_ref = dW0 + dY.T @ X
+    tol = 1e-5 * np.sqrt(S) * max(1.0, np.abs(dY.T @ X).max())
+    assert np.abs(host(dW) - dW_ref).max() <= tol
+    dh = dY @ Wt
+    if dg_epi == "store":
+        assert np.all(np.abs(host(dX) - dh) <= 2.0 ** -8 * np.abs(dh) + 1e-4 * np.sqrt(n_out))
+    else:
+        ref = om.swiglu_bwd(dh, gu_h, n_in)
+        assert np.all(np.abs(host(dX) - ref) <= 2.0 ** -7 * np.abs(ref) + 1e-3 * np.abs(ref).max())
+    # deterministic: rerun from the same initial dW reproduces every bit
+    dW.copy_(torch.tensor(dW0, device="cuda", dtype=torch.float32))
+    L.call("bm_k_gemm_mode", mode)
+    L.call("bm_k_gemm_group", arr, 2, None)
+    torch.cuda.synchronize()
+    L.call("bm_k_gemm_mode", 0)
+    assert torch.equal(first[0], dW) and torch.equal(first[1], dX)
