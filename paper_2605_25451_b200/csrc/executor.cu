@@ -680,9 +680,12 @@ static bm_status timed_gemm(bm_ctx& c, int M, int N, int K, const void* A, int64
   return BM_OK;
 }
 // independent contractions (a Linear's data and weight gradient) in one grouped
-// CTA-pair launch (gemm_bf16_tc_group: LPT tile schedule, no wave tail per GEMM);
-// BM_GEMM_GROUP_BWD=0 launches them one by one
-static const bool g_group_bwd = !(getenv("BM_GEMM_GROUP_BWD") && getenv("BM_GEMM_GROUP_BWD")[0] == '0');
+// CTA-pair launch (gemm_bf16_tc_group: LPT tile schedule, no wave tail per GEMM)
+// (opt-in BM_GEMM_GROUP_BWD=1: standalone it is even with two launches and in the C2
+// step 0.8 % slower -- the power-capped clock rises when a launch's last wave leaves
+// pairs idle, so the wave tail the grouping removes costs less than its count
+// suggests; profiles/r02/ab_group_bwd.log)
+static const bool g_group_bwd = getenv("BM_GEMM_GROUP_BWD") && getenv("BM_GEMM_GROUP_BWD")[0] == '1';
 static bm_status timed_group(bm_ctx& c, GemmSpec* sp, int n) {
   if (c.dtype != BM_BF16 || n == 1 || !g_group_bwd) {
     for (int i = 0; i < n; ++i) {

@@ -364,9 +364,15 @@ class Runtime:
         return list(a)
 
     def close(self):
+        """Destroy the context and release its device buffers (the caller must not use
+        views such as grads_t / weights_t afterwards)."""
         if getattr(self, "ctx", None):
+            torch.cuda.synchronize(self.device)
             L.lib().bm_ctx_destroy(self.ctx)
             self.ctx = None
+            for k in ("_w", "_g", "_work", "_comm", "weights_t", "grads_t", "_stream"):
+                if hasattr(self, k):
+                    setattr(self, k, None)
 
     def __del__(self):
         try:
