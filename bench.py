@@ -337,6 +337,21 @@ class Ctx:
         return out
 
 
+def gen_exclude(args, cfg, P, split, strategy):
+    """bigmac.h gen_exclude: "auto" keeps the DP-sharded generator off the stage that
+    holds the most LLM layers when the partition is uneven (it paces the pipeline;
+    DESIGN.md R20), "none" = 0, else a comma list of ranks."""
+    if args.gen_exclude == "none" or P == 1 or strategy == "memory_efficient" or args.head == "dp_shard":
+        return 0
+    if args.gen_exclude != "auto":
+        return sum(1 << int(r) for r in args.gen_exclude.split(","))
+    if not split or len(split) != P:
+        return 0
+    mx = max(split)
+    heavy = [r for r, n in enumerate(split) if n == mx]
+    return (1 << heavy[0]) if len(heavy) == 1 else 0
+
+
 def make_runtime(args, cfg, P, rank, world, group, strategy="bigmac"):
     from paper_2605_25451_b200.runtime import Runtime
     W = args.warmup_units if args.warmup_units >= 0 else (2 if P == 1 else 0)
@@ -345,7 +360,8 @@ def make_runtime(args, cfg, P, rank, world, group, strategy="bigmac"):
     split = stage_split(args, cfg, P)
     n_last = 0 if split else last_stage_layers(args, cfg, P)
     rt = Runtime(cfg, args.dtype, rank=rank, world=world, group=group, sched_kw=sched_kw, head_place=args.head,
-                 last_stage_layers=n_last, stage_layers=split)
+                 last_stage_layers=n_last, stage_layers=split, fsdp=args.fsdp,
+                 gen_exclude=gen_exclude(args, cfg, P, split, strategy))
     rt.init_random_weights(seed=1)
     return rt, W, split, n_last
 
@@ -480,6 +496,10 @@ def main():
     ap.add_argument("--head", default="auto", choices=["auto", "last_stage", "dp_shard"],
                     help="LM head + CE placement (bigmac.h bm_head_place): auto = last_stage (the paper's "
                          "Megatron placement), dp_shard = DP-sharded with the generator")
+    ap.add_argument("--fsdp", default="off", choices=["off", "pull", "allgather"],
+                    help="encoder / generator parameters: replicated (off), FSDP with BigMac's one-sided pull, "
+                         "or FSDP with the all-gather baseline (bigmac.h bm_fsdp_mode, P:401-426)")
+    ap.add_argument("--gen-exclude", default="auto", help="ranks that take no generator rows: auto | none | r,r")
     ap.add_argument("--strategy", default="bigmac", choices=["bigmac", "compute_efficient", "memory_efficient"],
                     help="bigmac (default); the paper's baselines on the same executor (P:129-156)")
     args = ap.parse_args()
@@ -582,6 +602,9 @@ def main():
     gemm_ms_all = cx.sum(gemm_ms)
     n_gemm_all = int(cx.sum(n_gemm))
     sum_mode = getattr(rt, "sum_mode", None)
+    fsdp_info = {"mode": args.fsdp, "weight_bytes_per_gpu_max": cx.max(rt.w_elems * rt.es),
+                 "weight_bytes_replicated": rt.total_elems * rt.es,
+                 "pull_bytes_per_step_max_gpu": cx.max(rt.pull_bytes())}
     free_runtime(rt)
     del db
 
@@ -655,8 +678,9 @@ def main():
             "scaling": "strong" if args.microbatches else "weak",
             "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
             "config": dict(config_dict(cfg, P, D), strategy=args.strategy, head_place=head_place_name(args, N),
-                           warmup_units=W, last_stage_layers=n_last, stage_layers=split, step_sum=sum_mode),
-            "roofline": roofline, "step_roofline": step_roof, "bubble": bubble,
+                           warmup_units=W, last_stage_layers=n_last, stage_layers=split, step_sum=sum_mode,
+                           gen_exclude=gen_exclude(args, cfg, P, split, args.strategy)),
+            "roofline": roofline, "step_roofline": step_roof, "bubble": bubble, "fsdp": fsdp_info,
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches_all, "clocks": clocks,
             "nvlink": ({"bytes_per_step_all_ranks": comm_bytes_all / n_inst,
                         "messages_per_step": n_msgs_all / n_inst,

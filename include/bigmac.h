@@ -145,7 +145,9 @@ typedef struct {
   int32_t max_n_mod, max_n_gen;   /* upper bounds on per-sample row counts     */
   int32_t head_place;             /* bm_head_place                             */
   int32_t last_stage_layers;      /* LLM layers of the last virtual stage; 0 = uniform (below) */
-  int32_t reserved[6];            /* must be zero                              */
+  int32_t fsdp;                   /* bm_fsdp_mode of the encoder / generator parameters */
+  int32_t gen_exclude;            /* bit mask of ranks that take no generator rows (below) */
+  int32_t reserved[4];            /* must be zero                              */
   int32_t stage_layers[BM_MAX_VSTAGES]; /* explicit partition (below); all 0 = unset */
 } bm_model_cfg;
 
@@ -159,6 +161,14 @@ typedef struct {
  * (L - n) mod (P V - 1) stages one layer more.  Requires 1 <= n and
  * L - n >= P V - 1 (every stage holds a layer).  Uneven splits balance the
  * head's cost; op lists do not depend on the partition. */
+
+/* gen_exclude (BM_GEN_DP_SHARD): rank r with bit r set takes no generator rows;
+ * microbatch m's n_gen rows are split into equal shards over the other ranks in
+ * rank order.  The generator is token-wise, so any row partition computes the same
+ * loss and gradients (reading R20); excluding the busiest pipeline stage keeps the
+ * generator's kernels off the stage that paces the pipeline.  Op lists are
+ * unchanged (an excluded rank's GenFwd / GenBwd are empty, its genin / gengrad
+ * messages carry no rows). */
 
 /* Where the final-norm output's LM head + cross-entropy (fwd and bwd) run.
  * BM_HEAD_LAST_STAGE: in F(m, V-1) on rank P-1, as in the paper's Megatron
@@ -176,6 +186,28 @@ typedef struct {
  *   head shard competes with that rank's running LLM op, and the last stage
  *   waits for it -- profiles/r01/traces/trace_n2_m32_*.summary.json). */
 typedef enum { BM_HEAD_AUTO = 0, BM_HEAD_LAST_STAGE = 1, BM_HEAD_DP_SHARD = 2 } bm_head_place;
+
+/* Encoder / generator parameters under FSDP.
+ * BM_FSDP_OFF: every rank holds them in full (plain data parallelism; gradients
+ *   summed at step end).
+ * BM_FSDP_PULL: BigMac's one-sided pull.  The DP parameters (the prefix
+ *   [0, dp_elems) of the parameter space) are sharded over the P ranks of the
+ *   pipeline: rank r stores only elements [lo_r, hi_r) (bm_ctx_dp_shard; 4-element
+ *   aligned near-equal chunks) at the start of its weights buffer, followed by its
+ *   LLM parameters.  Every encoder / generator op materialises its parameters block
+ *   by block (patch, each residual block, projector; generator in / blocks / out)
+ *   into two bucket slots, reading each shard directly from its owner's weights
+ *   buffer over NVLink (CUDA IPC, copy engine on a pull stream) while the previous
+ *   block computes -- the owners take no part, so ranks proceed on their own
+ *   schedules (no all-gather barrier).  Gradients are accumulated locally and
+ *   reduce-scattered at step end: after bm_step only this rank's shard of the DP
+ *   gradients is valid (all of it under the NCCL step-end sum, which all-reduces).
+ * BM_FSDP_ALLGATHER: the paper's baseline: the same buckets, but each pull is
+ *   preceded by a barrier of the pipeline group on the op's stream -- FSDP's
+ *   all-gather synchronisation point -- and runs on that stream.
+ *   Requires BM_ENC_DP_UNIT and BM_GEN_DP_SHARD (every rank in every op).
+ * FSDP needs D = 1 and a head that is not DP-sharded. */
+typedef enum { BM_FSDP_OFF = 0, BM_FSDP_PULL = 1, BM_FSDP_ALLGATHER = 2 } bm_fsdp_mode;
 
 /* Parameter kinds: DP parameters (encoder, projector, generator) are summed
  * over ranks at step end; LLM parameters belong to one stage. */
@@ -233,6 +265,17 @@ bm_status bm_ctx_bind(bm_ctx* c, const bm_buffers* b);
  * bm_ctx_open_peer (their `comm` buffer).  Exchange is done by the caller. */
 bm_status bm_ipc_export(const void* dptr, uint8_t handle[64], int64_t* offset);
 bm_status bm_ctx_open_peer(bm_ctx* c, int32_t peer, const uint8_t handle[64], int64_t offset);
+
+/* FSDP (bm_model_cfg.fsdp != BM_FSDP_OFF): map the pipeline peers' weights buffers
+ * (bm_ipc_export handles [P][64] and byte offsets [P], own entry ignored) for the
+ * one-sided pulls.  Call after bm_ctx_bind.  Errors: BM_E_INVALID, BM_E_CUDA. */
+bm_status bm_ctx_init_fsdp(bm_ctx* c, const uint8_t* weight_handles, const int64_t* weight_offsets);
+/* This rank's shard [*lo, *hi) of the DP parameter elements (the whole prefix
+ * [0, dp_elems) without FSDP).  Its weights buffer stores element e of the shard
+ * at element e - lo; LLM parameter element e (>= dp_elems) at e - dp_elems + (hi - lo). */
+bm_status bm_ctx_dp_shard(const bm_ctx* c, int64_t* lo, int64_t* hi);
+/* Bytes this rank pulled from peers' shards during its last bm_step (FSDP). */
+bm_status bm_ctx_pull_bytes(const bm_ctx* c, int64_t* bytes);
 
 /* Data-parallel gradient sum over the P ranks (NCCL).  Rank 0 creates
  * the id, the caller broadcasts it. */

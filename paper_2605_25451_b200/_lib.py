@@ -22,6 +22,7 @@ LLM_SCHED = {"1f1b": 0, "interleaved": 1}
 ENC_PLACE = {"none": 0, "dp_unit": 1, "entry_stage": 2}
 GEN_PLACE = {"none": 0, "dp_shard": 1, "last_stage": 2}
 HEAD_PLACE = {"auto": 0, "last_stage": 1, "dp_shard": 2}
+FSDP = {"off": 0, "pull": 1, "allgather": 2}
 
 
 class BigMacError(RuntimeError):
@@ -51,8 +52,8 @@ class SchedStats(C.Structure):
 class ModelCfg(C.Structure):
     _fields_ = [(n, C.c_int32) for n in ("S", "d_in", "d_e", "f_e", "L_e", "d", "f", "L", "vocab",
                                          "d_g", "f_g", "L_g", "d_t", "dtype", "max_n_mod", "max_n_gen",
-                                         "head_place", "last_stage_layers")] + \
-               [("reserved", C.c_int32 * 6), ("stage_layers", C.c_int32 * 32)]
+                                         "head_place", "last_stage_layers", "fsdp", "gen_exclude")] + \
+               [("reserved", C.c_int32 * 4), ("stage_layers", C.c_int32 * 32)]
 
 
 class ParamInfo(C.Structure):
@@ -111,6 +112,9 @@ SIGNATURES = {
     "bm_nccl_unique_id": [C.POINTER(C.c_uint8)],
     "bm_ctx_init_nccl": [_P, C.POINTER(C.c_uint8), _I32, _I32],
     "bm_ctx_init_replicas": [_P, _I32, _I32, C.POINTER(C.c_uint8), C.POINTER(C.c_uint8)],
+    "bm_ctx_init_fsdp": [_P, C.POINTER(C.c_uint8), C.POINTER(_I64)],
+    "bm_ctx_dp_shard": [_P, C.POINTER(_I64), C.POINTER(_I64)],
+    "bm_ctx_pull_bytes": [_P, C.POINTER(_I64)],
     "bm_ctx_init_peer_sum": [_P, _I32, _I32, C.POINTER(C.c_uint8), C.POINTER(_I64), C.POINTER(C.c_uint8),
                              C.POINTER(_I64)],
     "bm_step": [_P, C.POINTER(Batch), _P],

@@ -114,6 +114,13 @@ struct PEntry {
 
 static int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
 static int round8(int x) { return (x + 7) / 8 * 8; }
+// chunk q of n over [0, count): 4-element (16-byte) aligned boundaries (FSDP shards,
+// peer-sum reduce-scatter chunks)
+static void chunk_of(int64_t count, int n, int q, int64_t* lo, int64_t* hi) {
+  const int64_t n4 = (count + 3) / 4;
+  *lo = std::min(count, (n4 * q / n) * 4);
+  *hi = std::min(count, (n4 * (q + 1) / n) * 4);
+}
 
 static bm_status check_model(const bm_model_cfg& mc, const bm_sched_cfg& sc) {
   BM_CHECK_ARG(mc.S > 0 && mc.d > 0 && mc.f > 0 && mc.L > 0 && mc.vocab > 0, "bad LLM dims");
@@ -143,6 +150,17 @@ static bm_status check_model(const bm_model_cfg& mc, const bm_sched_cfg& sc) {
   BM_CHECK_ARG(mc.head_place >= BM_HEAD_AUTO && mc.head_place <= BM_HEAD_DP_SHARD, "bad head_place");
   BM_CHECK_ARG(mc.head_place != BM_HEAD_DP_SHARD || sc.gen_place == BM_GEN_DP_SHARD,
                "BM_HEAD_DP_SHARD rides on the DP-sharded generator ops (gen_place = BM_GEN_DP_SHARD)");
+  BM_CHECK_ARG(mc.fsdp >= BM_FSDP_OFF && mc.fsdp <= BM_FSDP_ALLGATHER, "bad fsdp mode");
+  {
+    const uint32_t all = sc.stages >= 32 ? 0xFFFFFFFFu : ((1u << sc.stages) - 1u);
+    BM_CHECK_ARG(((uint32_t)mc.gen_exclude & ~all) == 0 && ((uint32_t)mc.gen_exclude & all) != all,
+                 "gen_exclude: a bit mask of ranks < P that leaves at least one rank");
+    BM_CHECK_ARG(!mc.gen_exclude || (sc.gen_place == BM_GEN_DP_SHARD && mc.head_place != BM_HEAD_DP_SHARD),
+                 "gen_exclude applies to the DP-sharded generator (without the DP-sharded head)");
+  }
+  BM_CHECK_ARG(!mc.fsdp || mc.head_place != BM_HEAD_DP_SHARD, "FSDP shards the encoder / generator only (not the DP-sharded head)");
+  BM_CHECK_ARG(mc.fsdp != BM_FSDP_ALLGATHER || (sc.enc_place == BM_ENC_DP_UNIT && sc.gen_place == BM_GEN_DP_SHARD),
+               "the FSDP all-gather baseline needs every rank in every encoder / generator op (DP unit, DP shard)");
   return BM_OK;
 }
 
@@ -235,6 +253,25 @@ static std::vector<PEntry> param_layout(const bm_model_cfg& mc, const bm_sched_c
 }
 
 // ------------------------------------------------------------------ context
+// peer-sum block of a comm buffer (offsets in bytes)
+constexpr int64_t SUMBLK_FSDP = 64 * BM_MAX_SUM_PEERS;                 // FSDP barrier flags [2][64] x 64 B
+constexpr int64_t SUMBLK_LOSS = SUMBLK_FSDP + 2 * 64 * BM_MAX_SUM_PEERS;  // raw loss terms
+
+// FSDP (bm_model_cfg.fsdp): the encoder / generator parameters are sharded over the P
+// ranks; a chain of parameter buckets (one per block, in use order) is materialised
+// into two slots before use by pulling every shard from its owner
+struct PullChain {
+  std::vector<std::pair<int64_t, int64_t>> blocks;   // [lo, hi) DP element range per block
+  char* slot[2] = {nullptr, nullptr};
+  cudaEvent_t ready[2] = {nullptr, nullptr}, freed[2] = {nullptr, nullptr};
+  bool freed_pending[2] = {false, false};
+  cudaStream_t st = nullptr;   // pull stream (one-sided pull); the op stream itself for all-gather
+  std::vector<int> seq;        // block ids of the current op, in use order
+  int64_t cur_lo = 0, cur_hi = 0;   // block acquired last (parameter lookups resolve into it)
+  char* cur = nullptr;
+  uint32_t bar = 0;            // all-gather barriers issued on this chain (same on every rank)
+};
+
 struct Chan {
   int src, dst, pay, K, nmsg;
   int64_t slot_bytes;
@@ -312,6 +349,7 @@ struct bm_ctx {
   bool enc_entry = false;  // memory-efficient baseline: encoder as the entry stage's first layers
   bool head_dp = false;    // LM head + CE DP-sharded with the generator (bm_head_place)
   int n_enc_slots = 0, n_llm_slots = 0, gen_rows = 0;
+  int gen_rows_max = 0;    // largest generator shard of any rank (message slot sizes, same on every rank)
   int head_rows = 0;       // max text rows of one head shard (head_dp)
   // comm layout
   std::vector<Chan> chans;
@@ -372,6 +410,13 @@ struct bm_ctx {
   std::vector<char*> ps_comm;
   std::vector<float*> ps_grad;
   std::vector<void*> ipc_bases;    // mappings to release (registry references)
+  // FSDP (bm_model_cfg.fsdp): own shard [dp_lo, dp_hi) of the DP elements; the weights
+  // buffer holds it at element 0, the LLM parameters after it
+  int fsdp = 0;
+  int64_t dp_lo = 0, dp_hi = 0;
+  std::vector<char*> peer_w;       // pipeline peers' weight buffers (bm_ctx_init_fsdp)
+  PullChain chain[2];              // 0 encoder (+ projector), 1 generator
+  int64_t pull_bytes = 0;          // bytes pulled from peers in the last step
   int64_t step = 0;
   cudaEvent_t done_ev = nullptr;   // recorded at the end of every bm_step (bm_step_wait)
   int64_t launches = 0;
@@ -463,6 +508,13 @@ bm_ctx::~bm_ctx() {
   if (emb_free_ev) cudaEventDestroy(emb_free_ev);
   if (hn_ev) cudaEventDestroy(hn_ev);
   if (done_ev) cudaEventDestroy(done_ev);
+  for (auto& ch : chain) {
+    for (int i = 0; i < 2; ++i) {
+      if (ch.ready[i]) cudaEventDestroy(ch.ready[i]);
+      if (ch.freed[i]) cudaEventDestroy(ch.freed[i]);
+    }
+    if (ch.st) cudaStreamDestroy(ch.st);
+  }
   if (gen_done_ev) cudaEventDestroy(gen_done_ev);
   for (auto e : evpool)
     if (e) cudaEventDestroy(e);
@@ -499,7 +551,7 @@ static int64_t payload_rows_max(const bm_ctx& c, int pay) {
     case BM_PAY_GRAD: return c.mc.S;
     case BM_PAY_EMB:
     case BM_PAY_EMBGRAD: return c.mc.max_n_mod;
-    default: return c.gen_rows + c.head_rows;   // genin / gengrad: [head rows | generator rows]
+    default: return c.gen_rows_max + c.head_rows;   // genin / gengrad: [head rows | generator rows]
   }
 }
 
@@ -527,12 +579,13 @@ static void comm_layout(bm_ctx& c) {
     ch.data_off = data_cur[ch.dst];
     data_cur[ch.dst] += ch.K * ch.slot_bytes;
   }
-  // peer-sum block (bm_ctx_init_peer_sum): one barrier flag per source process
-  // (BM_MAX_SUM_PEERS x 64 B) + the raw loss terms [2M] the peers read
+  // peer-sum block: one step-end barrier flag per source process (bm_ctx_init_peer_sum),
+  // two FSDP all-gather barrier flag sets (bm_model_cfg.fsdp = BM_FSDP_ALLGATHER; encoder
+  // and generator chains), then the raw loss terms [2M] the peers read
   c.sum_off.assign(c.P, 0);
   for (int r = 0; r < c.P; ++r) {
     c.sum_off[r] = align_up(data_cur[r], 256);
-    c.comm_size[r] = align_up(c.sum_off[r] + 64 * BM_MAX_SUM_PEERS + (2 * (int64_t)c.M + 1) * 4, 256);
+    c.comm_size[r] = align_up(c.sum_off[r] + SUMBLK_LOSS + (2 * (int64_t)c.M + 1) * 4, 256);
   }
 }
 
@@ -630,6 +683,12 @@ static void work_layout(bm_ctx& c, char* base) {
   c.g_dxn = b.take(ng * m.d_g * es);
   for (int i = 0; i < 2; ++i) c.gout[i] = b.take((ng + c.head_rows) * d * es);
   c.emb_local = b.take(n * d * es);
+  if (c.fsdp)   // two bucket slots per chain, each the largest block of that chain
+    for (auto& ch : c.chain) {
+      int64_t mx = 1;
+      for (auto& bl : ch.blocks) mx = std::max(mx, bl.second - bl.first);
+      for (int i = 0; i < 2; ++i) ch.slot[i] = b.take(mx * es);
+    }
   c.loss = (float*)b.take((2 * (int64_t)c.M + 1) * 4);
   c.progress = (uint32_t*)b.take((2 + c.P) * 64);
   // host-batch staging
@@ -644,7 +703,13 @@ static void work_layout(bm_ctx& c, char* base) {
 // ------------------------------------------------------------------ helpers
 static inline char* P_(bm_ctx& c, const char* name) {
   auto it = c.pidx.find(name);
-  return it == c.pidx.end() ? nullptr : c.W + c.params[it->second].off * c.es;
+  if (it == c.pidx.end()) return nullptr;
+  const int64_t off = c.params[it->second].off;
+  if (!c.fsdp) return c.W + off * c.es;
+  if (off >= c.dp_elems) return c.W + (off - c.dp_elems + (c.dp_hi - c.dp_lo)) * c.es;   // LLM parameter
+  for (auto& ch : c.chain)   // DP parameter: inside the bucket acquired last on its chain
+    if (off >= ch.cur_lo && off < ch.cur_hi) return ch.cur + (off - ch.cur_lo) * c.es;
+  return nullptr;
 }
 static inline float* G_(bm_ctx& c, const char* name) {
   auto it = c.pidx.find(name);
@@ -882,11 +947,24 @@ static cudaEvent_t trace_mark(bm_ctx& c, cudaStream_t st) {
   return e;
 }
 
+// generator row shard of rank r: equal shards over the ranks not in
+// bm_model_cfg.gen_exclude (in rank order), empty on the excluded ranks
 static void shard_rows(const bm_ctx& c, int m, int r, int* lo, int* hi) {
   const int n = c.n_gen[m];
   if (c.gen_last) { *lo = 0; *hi = n; return; }
-  *lo = (int)(((int64_t)r * n) / c.P);
-  *hi = (int)(((int64_t)(r + 1) * n) / c.P);
+  const uint32_t ex = (uint32_t)c.mc.gen_exclude;
+  int k = 0, nk = 0;   // r's index among the included ranks, their count
+  for (int q = 0; q < c.P; ++q)
+    if (!((ex >> q) & 1u)) {
+      if (q < r) ++k;
+      ++nk;
+    }
+  if ((ex >> r) & 1u) {
+    *lo = *hi = (int)(((int64_t)k * n) / nk);
+    return;
+  }
+  *lo = (int)(((int64_t)k * n) / nk);
+  *hi = (int)(((int64_t)(k + 1) * n) / nk);
 }
 
 // head shard r of microbatch m (head_dp): absolute rows of the text range [n_mod, S)
@@ -897,10 +975,92 @@ static void head_rows_of(const bm_ctx& c, int m, int r, int* lo, int* hi) {
   *hi = n_mod + (int)(((int64_t)(r + 1) * n_text) / c.P);
 }
 
+static bm_status wait_flag(bm_ctx& c, cudaStream_t on, char* flag, uint32_t v, const char* what);
+// ------------------------------------------------------------------ FSDP one-sided pull
+// barrier of the pipeline group on stream `on` (all-gather baseline): every rank must
+// reach the same bucket before any proceeds -- FSDP's synchronisation point
+static bm_status fsdp_barrier(bm_ctx& c, int k, cudaStream_t on) {
+  PullChain& ch = c.chain[k];
+  const uint32_t v = ++ch.bar;
+  for (int q = 0; q < c.P; ++q) {
+    char* f = c.peer[q] + c.sum_off[q] + SUMBLK_FSDP + (int64_t)(k * BM_MAX_SUM_PEERS + c.rank) * 64;
+    CUresult r = drv().write32((CUstream)on, (CUdeviceptr)f, v, 0);
+    if (r != CUDA_SUCCESS) { set_error("cuStreamWriteValue32 (fsdp barrier) failed"); return BM_E_CUDA; }
+  }
+  for (int q = 0; q < c.P; ++q)
+    if (q != c.rank)
+      BM_TRY(wait_flag(c, on, c.comm + c.sum_off[c.rank] + SUMBLK_FSDP + (int64_t)(k * BM_MAX_SUM_PEERS + q) * 64, v,
+                       "fsdp all-gather"));
+  return BM_OK;
+}
+// materialise block seq[j] of chain k into slot j % 2: the shard of every owner q is
+// read from q's weight buffer (own shard locally) -- no participation of the owners
+static bm_status fsdp_issue(bm_ctx& c, int k, int j, cudaStream_t op_st) {
+  PullChain& ch = c.chain[k];
+  const int s = j & 1;
+  cudaStream_t st = c.fsdp == BM_FSDP_ALLGATHER ? op_st : ch.st;
+  if (ch.freed_pending[s]) {   // the op that read this slot last has finished with it
+    if (st != op_st) BM_CUDA_TRY(cudaStreamWaitEvent(st, ch.freed[s], 0));
+    ch.freed_pending[s] = false;
+  }
+  if (c.fsdp == BM_FSDP_ALLGATHER) BM_TRY(fsdp_barrier(c, k, st));
+  const auto bl = ch.blocks[ch.seq[j]];
+  for (int q = 0; q < c.P; ++q) {
+    int64_t qlo, qhi;
+    chunk_of(c.dp_elems, c.P, q, &qlo, &qhi);
+    const int64_t a = std::max(bl.first, qlo), e = std::min(bl.second, qhi);
+    if (e <= a) continue;
+    const char* src = (q == c.rank ? c.W : c.peer_w[q]) + (a - qlo) * c.es;
+    BM_CUDA_TRY(cudaMemcpyAsync(ch.slot[s] + (a - bl.first) * c.es, src, (size_t)(e - a) * c.es,
+                                cudaMemcpyDeviceToDevice, st));
+    if (q != c.rank) c.pull_bytes += (e - a) * c.es;
+  }
+  BM_CUDA_TRY(cudaEventRecord(ch.ready[s], st));
+  return BM_OK;
+}
+// an op starts using chain k with blocks `seq` in this order: prefetch the first two
+static bm_status fsdp_begin(bm_ctx& c, int k, std::vector<int> seq, cudaStream_t op_st) {
+  if (!c.fsdp) return BM_OK;
+  PullChain& ch = c.chain[k];
+  // (no wait on op_st: weights are constant within a step, so a pull may run ahead;
+  // slot reuse is ordered by the freed events of the slot's last reader)
+  ch.seq = std::move(seq);
+  for (int j = 0; j < 2 && j < (int)ch.seq.size(); ++j) BM_TRY(fsdp_issue(c, k, j, op_st));
+  return BM_OK;
+}
+// block seq[j] is needed now on op_st: wait for its pull; parameter lookups resolve into it
+static bm_status fsdp_acquire(bm_ctx& c, int k, int j, cudaStream_t op_st) {
+  if (!c.fsdp) return BM_OK;
+  PullChain& ch = c.chain[k];
+  if (c.fsdp != BM_FSDP_ALLGATHER) BM_CUDA_TRY(cudaStreamWaitEvent(op_st, ch.ready[j & 1], 0));
+  ch.cur = ch.slot[j & 1];
+  ch.cur_lo = ch.blocks[ch.seq[j]].first;
+  ch.cur_hi = ch.blocks[ch.seq[j]].second;
+  return BM_OK;
+}
+// block seq[j]'s kernels are enqueued: its slot is free once they ran; pull seq[j + 2]
+static bm_status fsdp_release(bm_ctx& c, int k, int j, cudaStream_t op_st) {
+  if (!c.fsdp) return BM_OK;
+  PullChain& ch = c.chain[k];
+  BM_CUDA_TRY(cudaEventRecord(ch.freed[j & 1], op_st));
+  ch.freed_pending[j & 1] = true;
+  ch.cur_lo = ch.cur_hi = 0;
+  if (j + 2 < (int)ch.seq.size()) BM_TRY(fsdp_issue(c, k, j + 2, op_st));
+  return BM_OK;
+}
+static std::vector<int> fsdp_order(int nblocks, bool reverse) {
+  std::vector<int> v(nblocks);
+  for (int i = 0; i < nblocks; ++i) v[i] = reverse ? nblocks - 1 - i : i;
+  return v;
+}
+
 // ------------------------------------------------------------------ residual MLP blocks (encoder / generator)
-static bm_status mlp_blocks_fwd(bm_ctx& c, MlpSlot& sl, const char* prefix, int Lb, int n, int dm, int fm) {
+// k: FSDP chain, j0: position of block 0 in the op's block sequence (forward order)
+static bm_status mlp_blocks_fwd(bm_ctx& c, MlpSlot& sl, const char* prefix, int Lb, int n, int dm, int fm, int k = 0,
+                                int j0 = 0) {
   char nm[64];
   for (int i = 0; i < Lb; ++i) {
+    BM_TRY(fsdp_acquire(c, k, j0 + i, c.st));
     snprintf(nm, sizeof nm, "%s.blk%d.norm", prefix, i);
     BM_TRY(norm_fwd(c, n, dm, sl.E[i], P_(c, nm), sl.xn[i], sl.rstd[i]));
     snprintf(nm, sizeof nm, "%s.blk%d.fc1", prefix, i);
@@ -908,14 +1068,17 @@ static bm_status mlp_blocks_fwd(bm_ctx& c, MlpSlot& sl, const char* prefix, int 
     BM_TRY(gelu_f(c, (int64_t)n * fm, sl.a[i], sl.z[i]));
     snprintf(nm, sizeof nm, "%s.blk%d.fc2", prefix, i);
     BM_TRY(lin_fwd(c, n, fm, dm, sl.z[i], fm, P_(c, nm), LD_(c, nm), sl.E[i + 1], BM_EPI_ADD, sl.E[i]));
+    BM_TRY(fsdp_release(c, k, j0 + i, c.st));
   }
   return BM_OK;
 }
 // dE (n x dm) in/out, updated in place through the blocks in reverse
+// blocks in reverse; block i is at position j0 + (Lb - 1 - i) of the op's sequence
 static bm_status mlp_blocks_bwd(bm_ctx& c, MlpSlot& sl, const char* prefix, int Lb, int n, int dm, int fm, char* dE,
-                                char* dz, char* da, char* dxn) {
+                                char* dz, char* da, char* dxn, int k = 0, int j0 = 0) {
   char nm[64];
   for (int i = Lb - 1; i >= 0; --i) {
+    BM_TRY(fsdp_acquire(c, k, j0 + (Lb - 1 - i), c.st));
     snprintf(nm, sizeof nm, "%s.blk%d.fc2", prefix, i);
     BM_TRY(lin_wgrad(c, n, fm, dm, dE, sl.z[i], fm, G_(c, nm), LD_(c, nm)));
     BM_TRY(lin_dgrad(c, n, fm, dm, dE, P_(c, nm), LD_(c, nm), dz, fm));
@@ -925,6 +1088,7 @@ static bm_status mlp_blocks_bwd(bm_ctx& c, MlpSlot& sl, const char* prefix, int 
     BM_TRY(lin_dgrad(c, n, dm, fm, da, P_(c, nm), LD_(c, nm), dxn, dm));
     snprintf(nm, sizeof nm, "%s.blk%d.norm", prefix, i);
     BM_TRY(norm_bwd(c, n, dm, dxn, sl.E[i], P_(c, nm), sl.rstd[i], dE, dE, G_(c, nm)));
+    BM_TRY(fsdp_release(c, k, j0 + (Lb - 1 - i), c.st));
   }
   return BM_OK;
 }
@@ -943,11 +1107,17 @@ static bm_status op_enc_fwd(bm_ctx& c, const bm_op& o) {
   const auto& m = c.mc;
   const int mb = o.mb, n = c.n_mod[mb];
   MlpSlot& sl = c.enc[o.unit % c.n_enc_slots];
+  const int nb = m.L_e + 2;   // FSDP buckets: patch, the L_e blocks, projector
+  BM_TRY(fsdp_begin(c, 0, fsdp_order(nb, false), c.st));
+  BM_TRY(fsdp_acquire(c, 0, 0, c.st));
   BM_TRY(lin_fwd(c, n, m.d_in, m.d_e, c.mb_patches[mb], c.ld_patch, P_(c, "enc.patch"), LD_(c, "enc.patch"), sl.E[0]));
-  BM_TRY(mlp_blocks_fwd(c, sl, "enc", m.L_e, n, m.d_e, m.f_e));
+  BM_TRY(fsdp_release(c, 0, 0, c.st));
+  BM_TRY(mlp_blocks_fwd(c, sl, "enc", m.L_e, n, m.d_e, m.f_e, 0, 1));
+  BM_TRY(fsdp_acquire(c, 0, nb - 1, c.st));
   BM_TRY(lin_fwd(c, n, m.d_e, m.d, sl.E[m.L_e], m.d_e, P_(c, "enc.proj1"), LD_(c, "enc.proj1"), sl.a1));
   BM_TRY(gelu_f(c, (int64_t)n * m.d, sl.a1, sl.p1));
   BM_TRY(lin_fwd(c, n, m.d, m.d, sl.p1, m.d, P_(c, "enc.proj2"), LD_(c, "enc.proj2"), sl.out));
+  BM_TRY(fsdp_release(c, 0, nb - 1, c.st));
   c.last_src = sl.out;
   c.last_src_ring = -1;
   return BM_OK;
@@ -958,13 +1128,19 @@ static bm_status op_enc_bwd(bm_ctx& c, const bm_op& o, const RecvState& rs) {
   const int mb = o.mb, n = c.n_mod[mb];
   MlpSlot& sl = c.enc[o.unit % c.n_enc_slots];
   const char* dout = c.rank == 0 ? c.emb_local : recv_slot(c, 0, BM_PAY_EMBGRAD, rs.ops.at(0)->seq);
+  const int nb = m.L_e + 2;   // FSDP buckets in reverse: projector, blocks L_e-1..0, patch
+  BM_TRY(fsdp_begin(c, 0, fsdp_order(nb, true), c.st));
+  BM_TRY(fsdp_acquire(c, 0, 0, c.st));
   BM_TRY(lin_wgrad(c, n, m.d, m.d, dout, sl.p1, m.d, G_(c, "enc.proj2"), LD_(c, "enc.proj2")));
   BM_TRY(lin_dgrad(c, n, m.d, m.d, dout, P_(c, "enc.proj2"), LD_(c, "enc.proj2"), c.e_dp, m.d));
   BM_TRY(gelu_b(c, (int64_t)n * m.d, c.e_dp, sl.a1, c.e_da));
   BM_TRY(lin_wgrad(c, n, m.d_e, m.d, c.e_da, sl.E[m.L_e], m.d_e, G_(c, "enc.proj1"), LD_(c, "enc.proj1")));
   BM_TRY(lin_dgrad(c, n, m.d_e, m.d, c.e_da, P_(c, "enc.proj1"), LD_(c, "enc.proj1"), c.e_dE, m.d_e));
-  BM_TRY(mlp_blocks_bwd(c, sl, "enc", m.L_e, n, m.d_e, m.f_e, c.e_dE, c.e_dz, c.e_da, c.e_dxn));
+  BM_TRY(fsdp_release(c, 0, 0, c.st));
+  BM_TRY(mlp_blocks_bwd(c, sl, "enc", m.L_e, n, m.d_e, m.f_e, c.e_dE, c.e_dz, c.e_da, c.e_dxn, 0, 1));
+  BM_TRY(fsdp_acquire(c, 0, nb - 1, c.st));   // the patch embedding (weight gradient only)
   BM_TRY(lin_wgrad(c, n, m.d_in, m.d_e, c.e_dE, c.mb_patches[mb], c.ld_patch, G_(c, "enc.patch"), LD_(c, "enc.patch")));
+  BM_TRY(fsdp_release(c, 0, nb - 1, c.st));
   return BM_OK;
 }
 
@@ -1192,9 +1368,15 @@ static bm_status op_gen_fwd(bm_ctx& c, const bm_op& o, const RecvState& rs) {
   if (n <= 0) return BM_OK;
   const char* X = own ? c.genin_src[c.rank] : slot + (int64_t)nh * row;
   MlpSlot& sl = c.gen;
+  const int nb = m.L_g + 2;   // FSDP buckets: in-projection, the L_g blocks, out-projection
+  BM_TRY(fsdp_begin(c, 1, fsdp_order(nb, false), c.st));
+  BM_TRY(fsdp_acquire(c, 1, 0, c.st));
   BM_TRY(lin_fwd(c, n, m.d, m.d_g, X, m.d, P_(c, "gen.in"), LD_(c, "gen.in"), sl.E[0]));
-  BM_TRY(mlp_blocks_fwd(c, sl, "gen", m.L_g, n, m.d_g, m.f_g));
+  BM_TRY(fsdp_release(c, 1, 0, c.st));
+  BM_TRY(mlp_blocks_fwd(c, sl, "gen", m.L_g, n, m.d_g, m.f_g, 1, 1));
+  BM_TRY(fsdp_acquire(c, 1, nb - 1, c.st));
   BM_TRY(lin_fwd(c, n, m.d_g, m.d_t, sl.E[m.L_g], m.d_g, P_(c, "gen.out"), LD_(c, "gen.out"), sl.out));
+  BM_TRY(fsdp_release(c, 1, nb - 1, c.st));
   const char* t = c.mb_targets[mb] + (int64_t)lo * m.d_t * c.es;
   const float denom = (float)c.n_gen[mb] * m.d_t;
   BM_TRY(TY(c, mse_fwd_bwd<bf16>(n, m.d_t, (const bf16*)sl.out, (const bf16*)t, denom, c.gscale, 1.f, c.loss + c.M + mb, (bf16*)sl.dout, c.st),
@@ -1216,15 +1398,21 @@ static bm_status op_gen_bwd(bm_ctx& c, const bm_op& o, const char* X) {
   c.last_src_idx = b;
   if (c.rank == c.P - 1) c.own_gout[mb] = b;
   if (n <= 0) return BM_OK;
+  const int nb = m.L_g + 2;   // FSDP buckets in reverse
+  BM_TRY(fsdp_begin(c, 1, fsdp_order(nb, true), c.st));
+  BM_TRY(fsdp_acquire(c, 1, 0, c.st));
   BM_TRY(lin_wgrad(c, n, m.d_g, m.d_t, sl.dout, sl.E[m.L_g], m.d_g, G_(c, "gen.out"), LD_(c, "gen.out")));
   BM_TRY(lin_dgrad(c, n, m.d_g, m.d_t, sl.dout, P_(c, "gen.out"), LD_(c, "gen.out"), c.g_dG, m.d_g));
-  BM_TRY(mlp_blocks_bwd(c, sl, "gen", m.L_g, n, m.d_g, m.f_g, c.g_dG, c.g_dz, c.g_da, c.g_dxn));
+  BM_TRY(fsdp_release(c, 1, 0, c.st));
+  BM_TRY(mlp_blocks_bwd(c, sl, "gen", m.L_g, n, m.d_g, m.f_g, c.g_dG, c.g_dz, c.g_da, c.g_dxn, 1, 1));
+  BM_TRY(fsdp_acquire(c, 1, nb - 1, c.st));
   BM_TRY(lin_wgrad(c, n, m.d, m.d_g, c.g_dG, X, m.d, G_(c, "gen.in"), LD_(c, "gen.in")));
   // dX of this shard into the gout ring: sent to the last stage, or (own shard on
   // the last stage) added into dHn by B(mb, V-1) -- never written into dHn here,
   // where the LM-head dgrad of the same rows may still be running on the compute stream
   BM_TRY(lin_dgrad(c, n, m.d, m.d_g, c.g_dG, P_(c, "gen.in"), LD_(c, "gen.in"),
                    c.gout[b] + (int64_t)(hhi - hlo) * m.d * c.es, m.d));
+  BM_TRY(fsdp_release(c, 1, nb - 1, c.st));
   return BM_OK;
 }
 
@@ -1364,13 +1552,6 @@ static bm_status psum_barrier(bm_ctx& c, uint32_t v) {
   return BM_OK;
 }
 
-// chunk q of n over [0, count): 4-element (16-byte) aligned boundaries
-static void chunk_of(int64_t count, int n, int q, int64_t* lo, int64_t* hi) {
-  const int64_t n4 = (count + 3) / 4;
-  *lo = std::min(count, (n4 * q / n) * 4);
-  *hi = std::min(count, (n4 * (q + 1) / n) * 4);
-}
-
 // reduce-scatter of [off, off + count) of the gradient buffers over `group`
 // (process indices): this process sums chunk me_idx in group order, in place
 static bm_status psum_reduce_scatter(bm_ctx& c, const std::vector<int>& group, int me_idx, int64_t off, int64_t count) {
@@ -1399,7 +1580,7 @@ static bm_status psum_all_gather(bm_ctx& c, const std::vector<int>& group, int m
 static bm_status peer_finalize(bm_ctx& x) {
   const int world = x.P * x.D, me = x.replica * x.P + x.rank;
   const uint32_t base = (uint32_t)(x.step * 4);
-  float* raw = (float*)(x.ps_comm[me] + 64 * BM_MAX_SUM_PEERS);
+  float* raw = (float*)(x.ps_comm[me] + SUMBLK_LOSS);
   BM_CUDA_TRY(cudaMemcpyAsync(raw, x.loss, (size_t)2 * x.M * 4, cudaMemcpyDeviceToDevice, x.st));
   BM_TRY(psum_barrier(x, base + 1));   // every gradient and loss term of the step is final
   std::vector<int> all(world), stage(x.D), pipe(x.P);
@@ -1409,11 +1590,13 @@ static bm_status peer_finalize(bm_ctx& x) {
   BM_TRY(psum_reduce_scatter(x, all, me, 0, x.dp_elems));
   if (x.D > 1) BM_TRY(psum_reduce_scatter(x, stage, x.replica, x.dp_elems, x.total_elems - x.dp_elems));
   PeerSrc sp{}, sw{};
-  for (int r = 0; r < x.P; ++r) sp.p[r] = (const float*)(x.ps_comm[pipe[r]] + 64 * BM_MAX_SUM_PEERS);
-  for (int g = 0; g < world; ++g) sw.p[g] = (const float*)(x.ps_comm[g] + 64 * BM_MAX_SUM_PEERS);
+  for (int r = 0; r < x.P; ++r) sp.p[r] = (const float*)(x.ps_comm[pipe[r]] + SUMBLK_LOSS);
+  for (int g = 0; g < world; ++g) sw.p[g] = (const float*)(x.ps_comm[g] + SUMBLK_LOSS);
   BM_TRY(peer_loss(sp, x.P, sw, world, x.M, 1.f / ((float)x.M * (float)x.D), x.loss, x.st));
   BM_TRY(psum_barrier(x, base + 2));   // every owned chunk is reduced
-  BM_TRY(psum_all_gather(x, all, me, 0, x.dp_elems));
+  // FSDP keeps only the own shard of the DP gradients (reduce-scatter; the chunks are
+  // the weight shards, chunk_of over the pipeline group)
+  if (!x.fsdp) BM_TRY(psum_all_gather(x, all, me, 0, x.dp_elems));
   if (x.D > 1) BM_TRY(psum_all_gather(x, stage, x.replica, x.dp_elems, x.total_elems - x.dp_elems));
   BM_TRY(psum_barrier(x, base + 3));   // nobody reads this step's buffers any more
   return BM_OK;
@@ -1482,10 +1665,47 @@ bm_status bm_ctx_create(const bm_model_cfg* mc, const bm_schedule* s, int32_t ra
   const bm_sched_stats& st = s->stats[rank];
   c->n_llm_slots = std::max(st.peak_llm_inflight, 1);
   c->n_enc_slots = std::max(st.peak_enc_units, 1);
-  c->gen_rows = c->gen_last ? (rank == c->P - 1 ? mc->max_n_gen : 0) : (mc->max_n_gen + c->P - 1) / c->P;
-  if (!c->has_gen) c->gen_rows = 0;
+  {
+    int nk = 0;
+    for (int q = 0; q < c->P; ++q) nk += !(((uint32_t)mc->gen_exclude >> q) & 1u);
+    const bool ex = ((uint32_t)mc->gen_exclude >> rank) & 1u;
+    c->gen_rows = c->gen_last ? (rank == c->P - 1 ? mc->max_n_gen : 0) : (ex ? 0 : (mc->max_n_gen + nk - 1) / nk);
+    c->gen_rows_max = c->gen_last ? mc->max_n_gen : (mc->max_n_gen + nk - 1) / nk;
+  }
+  if (!c->has_gen) c->gen_rows = c->gen_rows_max = 0;
   c->head_dp = head_dp(*mc, s->cfg);
   c->head_rows = c->head_dp ? (mc->S + c->P - 1) / c->P : 0;
+  c->fsdp = mc->fsdp;
+  if (c->fsdp) {
+    chunk_of(c->dp_elems, c->P, rank, &c->dp_lo, &c->dp_hi);
+    // bucket chains: [patch] [blk0] .. [blk L_e-1] [proj1 proj2]; [gen.in] [blk0] .. [gen.out]
+    auto range = [&](std::initializer_list<std::string> names) {
+      int64_t lo = INT64_MAX, hi = 0;
+      for (const auto& n : names) {
+        const PEntry& e = c->params[c->pidx.at(n)];
+        lo = std::min(lo, e.off);
+        hi = std::max(hi, e.off + (int64_t)e.rows * e.ld);
+      }
+      return std::make_pair(lo, hi);
+    };
+    auto& ce = c->chain[0].blocks;
+    ce.push_back(range({"enc.patch"}));
+    for (int i = 0; i < mc->L_e; ++i) {
+      const std::string p = "enc.blk" + std::to_string(i);
+      ce.push_back(range({p + ".norm", p + ".fc1", p + ".fc2"}));
+    }
+    ce.push_back(range({"enc.proj1", "enc.proj2"}));
+    auto& cg = c->chain[1].blocks;
+    cg.push_back(range({"gen.in"}));
+    for (int i = 0; i < mc->L_g; ++i) {
+      const std::string p = "gen.blk" + std::to_string(i);
+      cg.push_back(range({p + ".norm", p + ".fc1", p + ".fc2"}));
+    }
+    cg.push_back(range({"gen.out"}));
+  } else {
+    c->dp_lo = 0;
+    c->dp_hi = c->dp_elems;
+  }
   comm_layout(*c);
   work_layout(*c, nullptr);
   // release annotations: Recv at i is released after the compute op j (genin: the following GenBwd)
@@ -1522,7 +1742,8 @@ bm_status bm_ctx_create(const bm_model_cfg* mc, const bm_schedule* s, int32_t ra
 
 bm_status bm_ctx_sizes_get(const bm_ctx* c, bm_ctx_sizes* out) {
   BM_CHECK_ARG(c && out, "null argument");
-  out->weight_bytes = c->total_elems * (int64_t)c->es;
+  // FSDP: this rank's shard of the DP parameters, then its LLM parameters
+  out->weight_bytes = (c->total_elems - c->dp_elems + (c->dp_hi - c->dp_lo)) * (int64_t)c->es;
   out->grad_bytes = c->total_elems * 4;
   out->work_bytes = c->work_bytes;
   out->comm_bytes = c->comm_size[c->rank];
@@ -1534,7 +1755,8 @@ bm_status bm_ctx_bind(bm_ctx* c, const bm_buffers* b) {
   for (const void* p : {b->weights, b->grads, b->work, b->comm})
     BM_CHECK_ARG((reinterpret_cast<uintptr_t>(p) & 255) == 0, "buffers must be 256-byte aligned");
   {
-    const int64_t need[4] = {c->total_elems * (int64_t)c->es, c->total_elems * 4, c->work_bytes, c->comm_size[c->rank]};
+    const int64_t need[4] = {(c->total_elems - c->dp_elems + (c->dp_hi - c->dp_lo)) * (int64_t)c->es,
+                             c->total_elems * 4, c->work_bytes, c->comm_size[c->rank]};
     const int64_t have[4] = {b->weight_bytes, b->grad_bytes, b->work_bytes, b->comm_bytes};
     static const char* nm[4] = {"weights", "grads", "work", "comm"};
     for (int i = 0; i < 4; ++i)
@@ -1591,7 +1813,17 @@ bm_status bm_ctx_bind(bm_ctx* c, const bm_buffers* b) {
     }
     if (c->has_gen) BM_CUDA_TRY(cudaEventCreateWithFlags(&c->hn_ev, cudaEventDisableTiming));
     BM_CUDA_TRY(cudaEventCreateWithFlags(&c->done_ev, cudaEventDisableTiming));
+    if (c->fsdp)
+      for (auto& ch : c->chain) {
+        BM_CUDA_TRY(cudaStreamCreateWithFlags(&ch.st, cudaStreamNonBlocking));
+        for (int i = 0; i < 2; ++i) {
+          BM_CUDA_TRY(cudaEventCreateWithFlags(&ch.ready[i], cudaEventDisableTiming));
+          BM_CUDA_TRY(cudaEventCreateWithFlags(&ch.freed[i], cudaEventDisableTiming));
+        }
+      }
   }
+  c->peer_w.assign(c->P, nullptr);
+  c->peer_w[c->rank] = c->W;
   if (!drv().wait32 || !drv().write32) {
     set_error("cuStreamWaitValue32/cuStreamWriteValue32 unavailable");
     return BM_E_CUDA;
@@ -1627,6 +1859,32 @@ bm_status bm_ctx_open_peer(bm_ctx* c, int32_t peer, const uint8_t handle[64], in
   return BM_OK;
 }
 
+bm_status bm_ctx_init_fsdp(bm_ctx* c, const uint8_t* weight_handles, const int64_t* weight_offsets) {
+  BM_CHECK_ARG(c && weight_handles && weight_offsets, "null argument");
+  BM_CHECK_ARG(c->bound && c->fsdp, "bind an FSDP context (bm_model_cfg.fsdp) first");
+  for (int q = 0; q < c->P; ++q) {
+    if (q == c->rank || c->peer_w[q]) continue;
+    void* p = nullptr;
+    BM_TRY(ipc_open(weight_handles + 64 * (size_t)q, &p));
+    c->ipc_bases.push_back(p);
+    c->peer_w[q] = (char*)p + weight_offsets[q];
+  }
+  return BM_OK;
+}
+
+bm_status bm_ctx_dp_shard(const bm_ctx* c, int64_t* lo, int64_t* hi) {
+  BM_CHECK_ARG(c && lo && hi, "null argument");
+  *lo = c->dp_lo;
+  *hi = c->dp_hi;
+  return BM_OK;
+}
+
+bm_status bm_ctx_pull_bytes(const bm_ctx* c, int64_t* bytes) {
+  BM_CHECK_ARG(c && bytes, "null argument");
+  *bytes = c->pull_bytes;
+  return BM_OK;
+}
+
 bm_status bm_ctx_init_peer_sum(bm_ctx* c, int32_t D, int32_t replica, const uint8_t* comm_handles,
                                const int64_t* comm_offsets, const uint8_t* grad_handles, const int64_t* grad_offsets) {
   BM_CHECK_ARG(c && comm_handles && comm_offsets && grad_handles && grad_offsets, "null argument");
@@ -1634,6 +1892,7 @@ bm_status bm_ctx_init_peer_sum(bm_ctx* c, int32_t D, int32_t replica, const uint
   BM_CHECK_ARG(D >= 1 && replica >= 0 && replica < D, "replica out of range");
   BM_CHECK_ARG((int64_t)c->P * D <= BM_MAX_SUM_PEERS, "too many processes for the peer sum");
   BM_CHECK_ARG(!c->psum && !c->nc && !c->nc_world && !c->nc_stage, "step-end sums already initialised");
+  BM_CHECK_ARG(!c->fsdp || D == 1, "FSDP shards over one pipeline's ranks (D = 1)");
   for (int r = 0; r < c->P; ++r)
     BM_CHECK_ARG(c->peer[r], "open the pipeline peers (bm_ctx_open_peer) before bm_ctx_init_peer_sum");
   const int world = c->P * D, me = replica * c->P + c->rank;
@@ -1697,6 +1956,7 @@ bm_status bm_ctx_init_replicas(bm_ctx* c, int32_t D, int32_t replica, const uint
   BM_CHECK_ARG(c && id_world && id_stage, "null argument");
   BM_CHECK_ARG(D >= 1 && replica >= 0 && replica < D, "replica out of range");
   BM_CHECK_ARG(!c->nc_world && !c->nc_stage, "replicas already initialised");
+  BM_CHECK_ARG(!c->fsdp || D == 1, "FSDP shards over one pipeline's ranks (D = 1)");
   if (!nccl().ok) {
     set_error("libnccl.so.2 not loadable");
     return BM_E_NCCL;
@@ -1725,6 +1985,12 @@ bm_status bm_step(bm_ctx* c, const bm_batch* b, void* stream) {
       set_error("peer " + std::to_string(r) + " not opened");
       return BM_E_STATE;
     }
+  if (c->fsdp)
+    for (int r = 0; r < c->P; ++r)
+      if (!c->peer_w[r]) {
+        set_error("FSDP: peer " + std::to_string(r) + "'s weight shard not opened (bm_ctx_init_fsdp)");
+        return BM_E_STATE;
+      }
   if (c->P > 1 && !c->nc && !c->psum) {
     set_error("step-end sums not initialised (bm_ctx_init_nccl or bm_ctx_init_peer_sum) for P > 1");
     return BM_E_STATE;
@@ -1795,6 +2061,7 @@ bm_status bm_step(bm_ctx* c, const bm_batch* b, void* stream) {
   }
   x.gen_done_pending = false;
   x.own_gout.clear();
+  x.pull_bytes = 0;
   cudaStream_t main_st = x.st;
   x.st_main = main_st;
   if (x.tracing) {

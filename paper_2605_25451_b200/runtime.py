@@ -23,7 +23,8 @@ from . import schedule as BS
 
 
 def model_cfg(shape, dtype: str, max_n_mod: int | None = None, max_n_gen: int | None = None,
-              head_place: str = "auto", last_stage_layers: int = 0, stage_layers=None) -> L.ModelCfg:
+              head_place: str = "auto", last_stage_layers: int = 0, stage_layers=None, fsdp: str = "off",
+              gen_exclude: int = 0) -> L.ModelCfg:
     mc = L.ModelCfg()
     mc.S, mc.d_in, mc.d_e, mc.f_e, mc.L_e = shape.S, shape.d_in, shape.d_e, shape.f_e, shape.L_e
     mc.d, mc.f, mc.L, mc.vocab = shape.d, shape.f, shape.L, shape.vocab
@@ -33,6 +34,8 @@ def model_cfg(shape, dtype: str, max_n_mod: int | None = None, max_n_gen: int | 
     mc.max_n_gen = max_n_gen if max_n_gen is not None else min(shape.n_gen_law[2], shape.S)
     mc.head_place = L.HEAD_PLACE[head_place]
     mc.last_stage_layers = last_stage_layers
+    mc.fsdp = L.FSDP[fsdp]
+    mc.gen_exclude = gen_exclude
     for i, n in enumerate(stage_layers or ()):
         mc.stage_layers[i] = n
     return mc
@@ -84,7 +87,7 @@ class DeviceBatch:
 
 class Runtime:
     def __init__(self, shape, dtype="bf16", rank=0, world=1, group=None, device=None, sched_kw=None,
-                 head_place="auto", last_stage_layers=0, stage_layers=None):
+                 head_place="auto", last_stage_layers=0, stage_layers=None, fsdp="off", gen_exclude=0):
         self.shape = shape
         self.dtype = dtype
         self.world = world
@@ -100,8 +103,9 @@ class Runtime:
         self._stream = None   # own compute stream (created on first step)
         kw = dict(sched_kw or {})
         self.sched = BS.build(self.P, self.M, self.V, **kw)
+        self.fsdp = fsdp
         self.mc = model_cfg(shape, dtype, head_place=head_place, last_stage_layers=last_stage_layers,
-                            stage_layers=stage_layers)
+                            stage_layers=stage_layers, fsdp=fsdp, gen_exclude=gen_exclude)
         h = C.c_void_p()
         L.call("bm_ctx_create", C.byref(self.mc), self.sched.handle, rank, C.byref(h))
         self.ctx = h.value
@@ -135,7 +139,11 @@ class Runtime:
             pi = L.ParamInfo()
             L.call("bm_param_info_get", C.byref(self.mc), C.byref(scfg), rank, i, C.byref(pi))
             self.params[pi.name.decode()] = (pi.rows, pi.cols, pi.ld, pi.offset, pi.kind)
-        self.weights_t = self._w[(self.w_ptr - self._w.data_ptr()):][: self.total_elems * self.es].view(tdt)
+        lo, hi = C.c_int64(), C.c_int64()
+        L.call("bm_ctx_dp_shard", self.ctx, C.byref(lo), C.byref(hi))
+        self.dp_lo, self.dp_hi = lo.value, hi.value   # FSDP: this rank's shard of the DP elements
+        self.w_elems = self.total_elems - self.dp_elems + (self.dp_hi - self.dp_lo)
+        self.weights_t = self._w[(self.w_ptr - self._w.data_ptr()):][: self.w_elems * self.es].view(tdt)
         self.grads_t = self._g[(self.g_ptr - self._g.data_ptr()):][: self.total_elems * 4].view(torch.float32)
         if world > 1:
             self._connect(group)
@@ -158,11 +166,15 @@ class Runtime:
             L.call("bm_nccl_unique_id", nid)
             return bytes(nid)
         uuid = str(torch.cuda.get_device_properties(self.device).uuid)
-        mine = (export(self.comm_ptr), export(self.g_ptr), uuid)
+        mine = (export(self.comm_ptr), export(self.g_ptr), uuid, export(self.w_ptr))
         peers, ids, allp = exchange(group, P, D, self.global_rank, mine, new_id)
-        for q, ((hbytes, o), _, _) in enumerate(peers):
+        for q, ((hbytes, o), _, _, _) in enumerate(peers):
             if q != self.rank:
                 L.call("bm_ctx_open_peer", self.ctx, q, (C.c_uint8 * 64).from_buffer_copy(hbytes), o)
+        if self.fsdp != "off":   # one-sided pulls read the pipeline peers' weight shards
+            wh = (C.c_uint8 * (64 * P)).from_buffer_copy(b"".join(x[3][0] for x in peers))
+            wo = (C.c_int64 * P)(*[x[3][1] for x in peers])
+            L.call("bm_ctx_init_fsdp", self.ctx, wh, wo)
         self.sum_mode = sum_mode([a[2] for a in allp])
         as_c = lambda b: (C.c_uint8 * 128).from_buffer_copy(b)  # noqa: E731
         if self.sum_mode == "peer":
@@ -180,6 +192,13 @@ class Runtime:
         dist.barrier(group=group)
 
     # ------------------------------------------------------------------ weights / grads
+    def _physical(self, flat):
+        """Logical parameter vector -> this rank's weights buffer layout (bigmac.h
+        bm_ctx_dp_shard: the DP shard [dp_lo, dp_hi) first, then the LLM parameters)."""
+        if self.dp_lo == 0 and self.dp_hi == self.dp_elems:
+            return flat
+        return torch.cat([flat[self.dp_lo:self.dp_hi], flat[self.dp_elems:]])
+
     def load_weights(self, weights: dict):
         """weights: {name: float32 array} (synth.make_weights); only this rank's params are used."""
         flat = torch.zeros(self.total_elems, dtype=torch.float32)
@@ -187,7 +206,7 @@ class Runtime:
             w = np.asarray(weights[name], np.float32).reshape(rows, cols)
             view = flat[off:off + rows * ld].view(rows, ld)
             view[:, :cols] = torch.from_numpy(w)
-        self.weights_t.copy_(flat.to(self.device).to(self.tdtype))
+        self.weights_t.copy_(self._physical(flat).to(self.device).to(self.tdtype))
         torch.cuda.synchronize(self.device)
 
     def init_random_weights(self, seed: int = 1, std: float = 0.02):
@@ -198,17 +217,29 @@ class Runtime:
         gen = torch.Generator(device=self.device)
         depth = {"enc": sh.L_e, "llm": sh.L, "gen": sh.L_g}
         self.weights_t.zero_()
-        for name, (rows, cols, ld, off, _) in self.params.items():
-            view = self.weights_t[off:off + rows * ld].view(rows, ld)
+        sharded = not (self.dp_lo == 0 and self.dp_hi == self.dp_elems)
+        for name, (rows, cols, ld, off, kind) in self.params.items():
+            if sharded and kind == 0:   # FSDP: generate in full, keep the owned slice
+                full = torch.zeros(rows * ld, dtype=self.tdtype, device=self.device)
+                view = full.view(rows, ld)
+            elif sharded:
+                o = off - self.dp_elems + (self.dp_hi - self.dp_lo)
+                view = self.weights_t[o:o + rows * ld].view(rows, ld)
+            else:
+                view = self.weights_t[off:off + rows * ld].view(rows, ld)
             if cols == 1:
                 view.fill_(1.0)
-                continue
-            gen.manual_seed(seed * 1000003 + zlib.crc32(name.encode()))  # DP replicas identical on every rank
-            scale = std
-            if name.endswith((".fc2", ".down")):
-                scale = std / (2.0 * depth[name.split(".")[0]]) ** 0.5
-            w = torch.randn((rows, cols), generator=gen, device=self.device, dtype=torch.float32) * scale
-            view[:, :cols] = w.to(self.tdtype)
+            else:
+                gen.manual_seed(seed * 1000003 + zlib.crc32(name.encode()))  # DP replicas identical on every rank
+                scale = std
+                if name.endswith((".fc2", ".down")):
+                    scale = std / (2.0 * depth[name.split(".")[0]]) ** 0.5
+                w = torch.randn((rows, cols), generator=gen, device=self.device, dtype=torch.float32) * scale
+                view[:, :cols] = w.to(self.tdtype)
+            if sharded and kind == 0:
+                a, b = max(off, self.dp_lo), min(off + rows * ld, self.dp_hi)
+                if b > a:
+                    self.weights_t[a - self.dp_lo:b - self.dp_lo].copy_(full[a - off:b - off])
         torch.cuda.synchronize(self.device)
 
     def set_timing(self, on: bool):
@@ -335,6 +366,12 @@ class Runtime:
         self._stream.wait_stream(cur)
         L.call("bm_step", self.ctx, C.byref(db.struct), C.c_void_p(self._stream.cuda_stream))
         cur.wait_stream(self._stream)
+
+    def pull_bytes(self) -> int:
+        """Bytes pulled from peers' FSDP shards in the last step."""
+        n = C.c_int64()
+        L.call("bm_ctx_pull_bytes", self.ctx, C.byref(n))
+        return n.value
 
     def step_wait(self, timeout_s: float = 0.0):
         """Block until the last step finished; BigMacError(E_TIMEOUT) naming the blocked

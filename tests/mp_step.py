@@ -13,7 +13,9 @@ SPEC: "<gen_place>", "entry_stage+<gen_place>" (memory-efficient baseline), "ce"
 (compute-efficient baseline: all encoder forwards first, W = M / P); modifiers
 "+head_dp" (LM head + CE DP-sharded with the generator), "+last<n>"
 (last_stage_layers = n), "+split<a>-<b>-..." (explicit stage_layers), "+edge"
-(degenerate row counts, synth.edge_counts).
+(degenerate row counts, synth.edge_counts), "+fsdp" / "+fsdpag" (FSDP with the
+one-sided pull / the all-gather baseline), "+genx<mask>" (ranks in the bit mask take
+no generator rows).
 FLAGS: peer = force the library's peer-memory step-end sum (BM_STEP_SUM=peer);
 gm2 = every bf16 contraction on the CTA-pair GEMM (bm_k_gemm_mode 2).
 """
@@ -40,7 +42,9 @@ def parse_spec(spec, M, P):
     head, last, split = "auto", 0, None
     toks = spec.split("+")
     edge = "edge" in toks
-    toks = [t for t in toks if t != "edge"]
+    fsdp = "pull" if "fsdp" in toks else ("allgather" if "fsdpag" in toks else "off")
+    genx = sum(int(t[4:]) for t in toks if t.startswith("genx"))
+    toks = [t for t in toks if t not in ("edge", "fsdp", "fsdpag") and not t.startswith("genx")]
     for t in toks:
         if t.startswith("split"):
             split = [int(x) for x in t[5:].split("-")]
@@ -57,7 +61,7 @@ def parse_spec(spec, M, P):
         kw = {"enc_place": "entry_stage", "gen_place": gen.split("+")[1]}
     else:
         kw = {"gen_place": gen}
-    return kw, head, last, split, edge
+    return kw, head, last, split, edge, fsdp, genx
 
 
 def run_case(case, rank, world):
@@ -67,7 +71,7 @@ def run_case(case, rank, world):
     name, P, M, V, dtype, spec, D = parts[0], int(parts[1]), int(parts[2]), int(parts[3]), parts[4], parts[5], int(parts[6])
     flags = parts[7].split(",") if len(parts) > 7 and parts[7] else []
     assert world == P * D, (case, world)
-    kw, head, last, split, edge = parse_spec(spec, M, P)
+    kw, head, last, split, edge, fsdp, genx = parse_spec(spec, M, P)
     cfg = get_config(name, P=P, M=M, V=V)
     cfg_global = get_config(name, P=P, M=M * D, V=V)
     if edge:   # degenerate row counts, buffers sized for [0, S]
@@ -81,7 +85,7 @@ def run_case(case, rank, world):
     os.environ["BM_STEP_SUM"] = "peer" if "peer" in flags else "auto"
     L.call("bm_k_gemm_mode", 2 if "gm2" in flags else 0)
     rt = Runtime(cfg, dtype, rank=rank, world=world, sched_kw=kw, head_place=head, last_stage_layers=last,
-                 stage_layers=split)
+                 stage_layers=split, fsdp=fsdp, gen_exclude=genx)
     rt.load_weights(W)
     db = rt.device_batch(B)
     for _ in range(2):
@@ -90,14 +94,36 @@ def run_case(case, rank, world):
     torch.cuda.synchronize()
     loss, ce, mse = rt.losses()
     grads = {n: rt.grad(n) for n in rt.names()}
+    meta = {"params": dict(rt.params), "shard": (rt.dp_lo, rt.dp_hi), "w_elems": rt.w_elems,
+            "total": rt.total_elems, "pull": rt.pull_bytes()}
     allg = [None] * world
-    dist.gather_object((grads, loss, ce, mse), allg if rank == 0 else None, dst=0)
+    dist.gather_object((grads, loss, ce, mse, meta), allg if rank == 0 else None, dst=0)
     if rank == 0:
         from oracle import model as om
         loss_ref, per_ref, G_ref = om.step_fp64(cfg_global, W, B_global)
         tol = 1e-4 if dtype == "f32" else 2e-2
         msgs = []
-        for r, (g, l_, c_, m_) in enumerate(allg):
+        if fsdp != "off":
+            # FSDP: rank r's DP gradients are valid on its shard [lo_r, hi_r) of the DP
+            # elements only (reduce-scatter); stitch the shards into full DP gradients
+            stitched = {}
+            for g, _, _, _, meta in allg:
+                lo, hi = meta["shard"]
+                for n, (rows, cols, ld, off, kind) in meta["params"].items():
+                    if kind != 0:
+                        continue
+                    e = off + np.arange(rows)[:, None] * ld + np.arange(cols)[None, :]
+                    own = ((e >= lo) & (e < hi)).reshape(g[n].shape)
+                    tgt = stitched.setdefault(n, np.full(g[n].shape, np.nan))
+                    tgt[own] = g[n][own]
+            for g, _, _, _, meta in allg:
+                for n in stitched:
+                    g[n] = stitched[n]
+                if P > 1 and not meta["w_elems"] < meta["total"]:
+                    msgs.append("FSDP weights buffer is not sharded")
+            if P > 1 and not any(meta["pull"] > 0 for *_, meta in allg):
+                msgs.append("FSDP pulled no bytes from peers")
+        for r, (g, l_, c_, m_, _) in enumerate(allg):
             if abs(l_ - loss_ref) > tol * abs(loss_ref):
                 msgs.append(f"rank {r} loss {l_} vs {loss_ref}")
             q = r // P   # replica: its own microbatches' loss terms
@@ -112,7 +138,7 @@ def run_case(case, rank, world):
                 if e > tol:
                     msgs.append(f"rank {r} grad {n} rel err {e:.3e}")
         seen = set()
-        for g, _, _, _ in allg:
+        for g, *_ in allg:
             seen |= set(g)
         missing = set(G_ref) - seen
         if missing:

@@ -262,6 +262,10 @@ MR_CASES = [
     ("C1", 2, 4, 1, "bf16", "dp_shard+edge", 1, ""), ("C1", 2, 8, 2, "f32", "dp_shard+edge", 1, ""),
     # every bf16 contraction on the CTA-pair GEMM (the bench's LLM kernels)
     ("C1M", 2, 4, 1, "bf16", "dp_shard", 1, "gm2"), ("C1M", 2, 8, 2, "bf16", "dp_shard", 1, "gm2"),
+    # FSDP: one-sided pull (also with the last-stage generator), all-gather baseline
+    ("C1", 2, 4, 1, "f32", "dp_shard+fsdp", 1, ""), ("C1", 2, 8, 2, "bf16", "dp_shard+fsdp", 1, ""),
+    ("C1", 2, 4, 1, "f32", "last_stage+fsdp", 1, ""), ("C1", 2, 4, 1, "f32", "dp_shard+fsdpag", 1, ""),
+    ("C1M", 2, 4, 1, "bf16", "dp_shard+fsdp", 1, "gm2"), ("C1", 2, 4, 1, "f32", "dp_shard+genx2", 1, ""),
     # pipeline replicas (R15)
     ("C1", 1, 4, 1, "f32", "dp_shard", 2, ""), ("C1", 1, 4, 1, "bf16", "dp_shard", 2, ""),
     # the peer-memory step-end sum forced (also where NCCL would be used)
@@ -273,6 +277,11 @@ MR_CASES = [
     ("C1", 4, 8, 1, "bf16", "dp_shard+head_dp", 1, ""), ("C1", 4, 4, 1, "f32", "dp_shard+edge", 1, ""),
     ("C1", 4, 8, 1, "bf16", "dp_shard+edge", 1, ""), ("C1", 4, 8, 1, "bf16", "last_stage+edge", 1, ""),
     ("C1M", 4, 8, 1, "bf16", "dp_shard", 1, "gm2"),
+    # generator rows kept off a rank (bigmac.h gen_exclude, reading R20)
+    ("C1", 4, 8, 1, "f32", "dp_shard+genx4", 1, ""), ("C1", 4, 8, 1, "bf16", "dp_shard+genx9+edge", 1, ""),
+    # FSDP of the encoder / generator: one-sided pull, and the all-gather baseline
+    ("C1", 4, 8, 1, "f32", "dp_shard+fsdpag", 1, ""), ("C1M", 4, 8, 1, "bf16", "dp_shard+fsdp", 1, ""),
+    ("C1", 4, 8, 1, "f32", "dp_shard+fsdp", 1, ""),
     # P = 2 x D = 2
     ("C1", 2, 4, 1, "f32", "dp_shard", 2, ""), ("C1", 2, 4, 1, "bf16", "dp_shard", 2, ""),
     ("C1", 2, 8, 2, "f32", "dp_shard", 2, ""), ("C1", 2, 4, 1, "f32", "dp_shard", 2, "peer"),
@@ -315,3 +324,23 @@ def test_step_wait_timeout_names_blocked_op():
     receive handles; SURVEY §8(b) flag-wait timeout)."""
     out = _torchrun(2, ["hang"], timeout=300)
     assert "TIMEOUT OK" in out.get("hang", ""), out
+
+
+@pytest.mark.parametrize("fsdp,dtype", [("pull", "f32"), ("pull", "bf16"), ("allgather", "f32")])
+def test_step_single_gpu_fsdp(oracle_cache, fsdp, dtype):
+    """FSDP at P = 1 (the shard is everything): the bucket chain (two slots per chain,
+    pulls on the pull stream, parameter lookups into the acquired block) reproduces
+    the plain step."""
+    from paper_2605_25451_b200.runtime import Runtime
+    cfg = get_config("C1M", P=1, M=4, V=1)
+    W, B, (loss_ref, per_ref, G_ref) = reference(oracle_cache, cfg)
+    rt = Runtime(cfg, dtype, fsdp=fsdp)
+    rt.load_weights(W)
+    rt.step(rt.device_batch(B))
+    torch.cuda.synchronize()
+    loss, _, _ = rt.losses()
+    tol = TOL[dtype]
+    assert abs(loss - loss_ref) <= tol * abs(loss_ref)
+    bad = {n: rel(rt.grad(n), G_ref[n]) for n in rt.names()}
+    assert not {k: v for k, v in bad.items() if v > tol}, bad
+    rt.close()

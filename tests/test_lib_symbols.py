@@ -132,3 +132,40 @@ def test_layer_partition_examples_and_errors():
     with pytest.raises(L.BigMacError):       # the DP-sharded head rides on DP-sharded generator ops
         L.call("bm_param_count", C.byref(mc), C.byref(BS.make_cfg(2, 4, 1, gen_place="last_stage")), 0,
                C.byref(n), C.byref(tot), C.byref(dp))
+
+
+@pytest.mark.parametrize("P", [1, 2, 4])
+def test_fsdp_shards_partition_the_dp_parameters(P):
+    """FSDP (bm_model_cfg.fsdp), host logic only: the ranks' shards
+    [lo_r, hi_r) tile the DP parameter prefix exactly once, each rank's weights buffer
+    shrinks by the unowned DP elements, and the unsupported combinations are rejected."""
+    from synth import get_config
+    from paper_2605_25451_b200 import _lib as L
+    from paper_2605_25451_b200 import schedule as BS
+    from paper_2605_25451_b200.runtime import model_cfg
+    cfg = get_config("C1", P=P, M=2 * P, V=1)
+    sched = BS.build(P, 2 * P, 1)
+    shards, sizes = [], []
+    for r in range(P):
+        out = []
+        for mode in ("off", "pull"):
+            mc = model_cfg(cfg, "bf16", fsdp=mode)
+            h = C.c_void_p()
+            L.call("bm_ctx_create", C.byref(mc), sched.handle, r, C.byref(h))
+            sz = L.CtxSizes()
+            L.call("bm_ctx_sizes_get", h, C.byref(sz))
+            lo, hi = C.c_int64(), C.c_int64()
+            L.call("bm_ctx_dp_shard", h, C.byref(lo), C.byref(hi))
+            out.append((sz.weight_bytes, lo.value, hi.value))
+            L.lib().bm_ctx_destroy(h)
+        (w_off, lo0, hi0), (w_fsdp, lo, hi) = out
+        dp = hi0 - lo0
+        assert lo0 == 0 and dp > 0
+        assert w_off - w_fsdp == (dp - (hi - lo)) * 2
+        shards.append((lo, hi))
+    assert shards[0][0] == 0 and shards[-1][1] == dp
+    assert all(shards[i][1] == shards[i + 1][0] for i in range(P - 1))
+    assert all(lo % 4 == 0 for lo, _ in shards)
+    mc = model_cfg(cfg, "bf16", fsdp="pull", head_place="dp_shard")
+    h = C.c_void_p()
+    assert L.lib().bm_ctx_create(C.byref(mc), sched.handle, 0, C.byref(h)) == 1   # BM_E_INVALID

@@ -544,3 +544,35 @@ def test_no_modality_rows_gives_zero_encoder_gradients():
     for k, v in G.items():
         if k.startswith("enc."):
             assert not np.any(v), k
+
+
+# =========================================================================== reading R20
+@pytest.mark.parametrize("parts", [[0, 40, 40, 97], [0, 97], [0, 0, 13, 97], [0, 30, 60, 97, 97]])
+def test_generator_row_partition_invariance(parts):
+    # R20: the generator is token-wise, so running it on any partition of a microbatch's
+    # n_gen rows (empty parts included) with the full-microbatch MSE denominator and
+    # summing the parts' losses and gradients gives the unsharded result (up to fp64
+    # summation order) -- what gen_exclude relies on
+    from synth import get_config, make_weights
+    from oracle import model as om
+    cfg = get_config("C1")
+    W = om.to_f64(make_weights(cfg))
+    rng = np.random.default_rng(7)
+    n = parts[-1]
+    X = rng.standard_normal((n, cfg.d))
+    t = rng.standard_normal((n, cfg.d_t))
+    denom = float(n * cfg.d_t)
+    G_full = {}
+    mse, cache = om.gen_fwd(W, cfg, X, t, denom)
+    dX = om.gen_bwd(W, cfg, cache, 1.0, G_full)
+    G_sum, mse_sum, dX_parts = {}, 0.0, []
+    for a, b in zip(parts[:-1], parts[1:]):
+        if b == a:
+            continue
+        m, c = om.gen_fwd(W, cfg, X[a:b], t[a:b], denom)
+        mse_sum += m
+        dX_parts.append(om.gen_bwd(W, cfg, c, 1.0, G_sum))
+    assert abs(mse_sum - mse) <= 1e-12 * abs(mse)
+    assert np.allclose(np.concatenate(dX_parts), dX, rtol=1e-12, atol=1e-15)
+    for k in G_full:
+        assert np.linalg.norm(G_sum[k] - G_full[k]) <= 1e-12 * np.linalg.norm(G_full[k]), k
