@@ -92,6 +92,12 @@ __device__ __forceinline__ float gelu_grad(float a) {
 }
 
 // ------------------------------------------------------------------ RMSNorm
+// BM_RMS_WIDE=0: the round-1 kernels (two reads of x in the forward, per-warp-row
+// fused backward for wide rows) -- measurement only
+static int g_rms_wide = [] {   // BM_RMS_WIDE=0: the per-warp-row fused kernel for wide rows too (measurement)
+  const char* e = getenv("BM_RMS_WIDE");
+  return e && e[0] == '0' ? 0 : 1;
+}();
 template <typename T>
 __global__ void rmsnorm_fwd_kernel(int rows, int cols, const T* __restrict__ x, const T* __restrict__ g,
                                    T* __restrict__ y, float* __restrict__ rstd) {
@@ -117,6 +123,49 @@ __global__ void rmsnorm_fwd_kernel(int rows, int cols, const T* __restrict__ x, 
 #pragma unroll
     for (int i = 0; i < N; ++i) o.set(i, v.get(i) * r * gv.get(i));
     vstore(yr + c, o);
+  }
+}
+
+// warp per row with the row held in registers (CH 16-byte vectors per lane, all loads
+// in flight at once; x is read from HBM once)
+template <typename T, int CH>
+__global__ void __launch_bounds__(256)
+rmsnorm_fwd_reg_kernel(int rows, int cols, const T* __restrict__ x, const T* __restrict__ g, T* __restrict__ y,
+                       float* __restrict__ rstd) {
+  pdl_enter();
+  constexpr int N = V16<T>::N;
+  const int row = blockIdx.x * 8 + threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  if (row >= rows) return;
+  const T* xr = x + (int64_t)row * cols;
+  V16<T> v[CH];
+  float ss = 0.f;
+#pragma unroll
+  for (int k = 0; k < CH; ++k) {
+    const int c = (k * 32 + lane) * N;
+    if (c < cols) v[k] = vload(xr + c);
+  }
+#pragma unroll
+  for (int k = 0; k < CH; ++k) {
+    const int c = (k * 32 + lane) * N;
+    if (c < cols) {
+#pragma unroll
+      for (int i = 0; i < N; ++i) { const float f = v[k].get(i); ss += f * f; }
+    }
+  }
+  ss = warp_sum(ss);
+  const float r = rsqrtf(ss / cols + RMS_EPS);
+  if (lane == 0) rstd[row] = r;
+  T* yr = y + (int64_t)row * cols;
+#pragma unroll
+  for (int k = 0; k < CH; ++k) {
+    const int c = (k * 32 + lane) * N;
+    if (c < cols) {
+      V16<T> gv = vload(g + c), o;
+#pragma unroll
+      for (int i = 0; i < N; ++i) o.set(i, v[k].get(i) * r * gv.get(i));
+      vstore(yr + c, o);
+    }
   }
 }
 
@@ -706,12 +755,127 @@ template <typename T>
 bm_status rmsnorm_fwd(int rows, int cols, const T* x, const T* g, T* y, float* rstd, cudaStream_t st) {
   if (rows <= 0) return BM_OK;
   BM_CHECK_ARG(cols % V16<T>::N == 0, "rmsnorm cols must be a multiple of the vector width");
+  const int ch = ceil_div(cols, 32 * V16<T>::N);
+  const dim3 grid(ceil_div(rows, 8));
+  if (g_rms_wide && ch <= 16) {   // row in registers (BM_RMS_WIDE=0: the two-read kernel)
+    if (ch <= 2) BM_CUDA_TRY(launch_k(rmsnorm_fwd_reg_kernel<T, 2>, grid, dim3(256), 0, st, rows, cols, x, g, y, rstd));
+    else if (ch <= 4) BM_CUDA_TRY(launch_k(rmsnorm_fwd_reg_kernel<T, 4>, grid, dim3(256), 0, st, rows, cols, x, g, y, rstd));
+    else if (ch <= 8) BM_CUDA_TRY(launch_k(rmsnorm_fwd_reg_kernel<T, 8>, grid, dim3(256), 0, st, rows, cols, x, g, y, rstd));
+    else BM_CUDA_TRY(launch_k(rmsnorm_fwd_reg_kernel<T, 16>, grid, dim3(256), 0, st, rows, cols, x, g, y, rstd));
+    count_launch();
+    BM_CUDA_TRY(cudaGetLastError());
+    return BM_OK;
+  }
   BM_CUDA_TRY(launch_k(rmsnorm_fwd_kernel<T>, dim3(ceil_div(rows, 8)), dim3(256), 0, st, rows, cols, x, g, y, rstd));
   count_launch();
   BM_CUDA_TRY(cudaGetLastError());
   return BM_OK;
 }
 // rows per block of the fused backward: ~2 waves of blocks over the 148 SMs
+// Wide rows (cols >= 256 vectors): the block's 256 threads split a row's columns
+// (CH 16-byte vectors per thread), so each thread keeps only CH x N gain-gradient
+// accumulators and a group of 4 rows' dy / x in registers between the two passes
+// (no re-read): pass 1 forms the 4 row dot products (warp sums -> smem -> fixed-order
+// block sums), pass 2 writes dx.  High occupancy instead of 64 accumulators per lane.
+template <typename T, int CH>
+__global__ void __launch_bounds__(256)
+rmsnorm_bwd_wide_kernel(int rows, int cols, int rows_per_block, const T* __restrict__ dy, const T* __restrict__ x,
+                        const T* __restrict__ g, const float* __restrict__ rstd, const T* dres, T* dx,
+                        float* __restrict__ partial) {
+  pdl_enter();
+  constexpr int N = V16<T>::N, RG = 4;
+  __shared__ float red[2][RG][8];
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  float acc[CH][N];
+  V16<T> gv[CH];
+#pragma unroll
+  for (int k = 0; k < CH; ++k) {
+    const int c = (k * 256 + threadIdx.x) * N;
+    if (c < cols) gv[k] = vload(g + c);
+#pragma unroll
+    for (int i = 0; i < N; ++i) acc[k][i] = 0.f;
+  }
+  const int r0 = blockIdx.x * rows_per_block;
+  const int r1 = min(rows, r0 + rows_per_block);
+  int par = 0;
+  for (int rb = r0; rb < r1; rb += RG, par ^= 1) {
+    V16<T> dv[RG][CH], xv[RG][CH];
+    float rs[RG];
+#pragma unroll
+    for (int j = 0; j < RG; ++j) {
+      const int row = rb + j;
+      rs[j] = row < r1 ? rstd[row] : 0.f;
+      float dot = 0.f;
+#pragma unroll
+      for (int k = 0; k < CH; ++k) {
+        const int c = (k * 256 + threadIdx.x) * N;
+        if (row < r1 && c < cols) {
+          const int64_t off = (int64_t)row * cols + c;
+          dv[j][k] = vload(dy + off);
+          xv[j][k] = vload(x + off);
+#pragma unroll
+          for (int i = 0; i < N; ++i) {
+            const float xh = xv[j][k].get(i) * rs[j];
+            dot += dv[j][k].get(i) * gv[k].get(i) * xh;
+            acc[k][i] += dv[j][k].get(i) * xh;
+          }
+        }
+      }
+      dot = warp_sum(dot);
+      if (lane == 0) red[par][j][warp] = dot;
+    }
+    __syncthreads();   // red[par] complete; red[par ^ 1] is free for the next group
+#pragma unroll
+    for (int j = 0; j < RG; ++j) {
+      const int row = rb + j;
+      if (row >= r1) continue;
+      float dot = 0.f;
+#pragma unroll
+      for (int w = 0; w < 8; ++w) dot += red[par][j][w];   // fixed order: deterministic
+      dot /= cols;
+#pragma unroll
+      for (int k = 0; k < CH; ++k) {
+        const int c = (k * 256 + threadIdx.x) * N;
+        if (c < cols) {
+          const int64_t off = (int64_t)row * cols + c;
+          V16<T> o, rv;
+          if (dres) rv = vload(dres + off);
+#pragma unroll
+          for (int i = 0; i < N; ++i) {
+            float v = rs[j] * (dv[j][k].get(i) * gv[k].get(i) - xv[j][k].get(i) * rs[j] * dot);
+            if (dres) v += rv.get(i);
+            o.set(i, v);
+          }
+          vstore(dx + off, o);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < CH; ++k) {
+    const int c = (k * 256 + threadIdx.x) * N;
+    if (c < cols) {
+#pragma unroll
+      for (int i = 0; i < N; ++i) partial[(int64_t)blockIdx.x * cols + c + i] = acc[k][i];
+    }
+  }
+}
+template <typename T, int CH>
+static bm_status launch_rms_bwd_wide(int rows, int cols, const T* dy, const T* x, const T* g, const float* rstd,
+                                     const T* dres, T* dx, float* dg, float* partial, cudaStream_t st) {
+  // ~4 blocks per SM, rows per block a multiple of the 4-row group
+  int rb = ceil_div(rows, 4 * num_sms());
+  rb = rb < 4 ? 4 : (rb + 3) / 4 * 4;
+  const int nb = ceil_div(rows, rb);
+  BM_CUDA_TRY(launch_k(rmsnorm_bwd_wide_kernel<T, CH>, dim3(nb), dim3(256), 0, st, rows, cols, rb, dy, x, g, rstd, dres,
+                       dx, partial));
+  BM_CUDA_TRY(launch_k(colsum2_accum_kernel, dim3(ceil_div(cols, 32)), dim3(256), 0, st, nb, cols, partial, dg));
+  count_launch(2);
+  BM_CUDA_TRY(cudaGetLastError());
+  return BM_OK;
+}
+
+
 static int rb_rows(int rows) {
   int rb = ceil_div(rows, 2 * num_sms());
   rb = (rb + 7) / 8 * 8;
@@ -742,6 +906,12 @@ bm_status rmsnorm_bwd(int rows, int cols, const T* dy, const T* x, const T* g, c
   constexpr int N = V16<T>::N;
   BM_CHECK_ARG(cols % N == 0, "rmsnorm cols must be a multiple of the vector width");
   const int ch = ceil_div(cols, 32 * N);  // vector chunks per lane
+  const int wide = ceil_div(cols, 256 * N);   // vector chunks per thread of a 256-thread row split
+  if (g_rms_wide && cols >= 256 * N && wide <= 4 && cols % (256 * N) == 0) {
+    if (wide == 1) return launch_rms_bwd_wide<T, 1>(rows, cols, dy, x, g, rstd, dres, dx, dg, partial, st);
+    if (wide == 2) return launch_rms_bwd_wide<T, 2>(rows, cols, dy, x, g, rstd, dres, dx, dg, partial, st);
+    return launch_rms_bwd_wide<T, 4>(rows, cols, dy, x, g, rstd, dres, dx, dg, partial, st);
+  }
   if (ch <= 16 && cols <= 6144) {
     if (ch <= 1) return launch_rms_bwd_fused<T, 1>(rows, cols, dy, x, g, rstd, dres, dx, dg, partial, st);
     if (ch <= 2) return launch_rms_bwd_fused<T, 2>(rows, cols, dy, x, g, rstd, dres, dx, dg, partial, st);
@@ -916,7 +1086,7 @@ BM_INST(bf16)
 BM_INST(float)
 
 int64_t rmsnorm_bwd_scratch_floats(int rows, int cols) {
-  const int64_t fused = (int64_t)ceil_div(rows, 8) * cols;
+  const int64_t fused = (int64_t)std::max(ceil_div(rows, 8), ceil_div(rows, 4)) * cols;
   const int64_t split = (int64_t)dg_chunks(rows) * cols;
   return fused > split ? fused : split;
 }
@@ -936,6 +1106,10 @@ static void preload_t(std::vector<const void*>& v) {
                         (const void*)rmsnorm_dg_partial_kernel<T>, (const void*)rmsnorm_bwd_fused_kernel<T, 1>,
                         (const void*)rmsnorm_bwd_fused_kernel<T, 2>, (const void*)rmsnorm_bwd_fused_kernel<T, 4>,
                         (const void*)rmsnorm_bwd_fused_kernel<T, 8>, (const void*)rmsnorm_bwd_fused_kernel<T, 16>,
+                        (const void*)rmsnorm_bwd_wide_kernel<T, 1>, (const void*)rmsnorm_bwd_wide_kernel<T, 2>,
+                        (const void*)rmsnorm_bwd_wide_kernel<T, 4>, (const void*)rmsnorm_fwd_reg_kernel<T, 2>,
+                        (const void*)rmsnorm_fwd_reg_kernel<T, 4>, (const void*)rmsnorm_fwd_reg_kernel<T, 8>,
+                        (const void*)rmsnorm_fwd_reg_kernel<T, 16>,
                         (const void*)swiglu_fwd_kernel<T>, (const void*)swiglu_bwd_kernel<T>,
                         (const void*)gelu_fwd_kernel<T>, (const void*)gelu_bwd_kernel<T>, (const void*)add_kernel<T>,
                         (const void*)embed_fwd_kernel<T>, (const void*)embed_segsum_kernel<T>,

@@ -14,7 +14,8 @@ timeout 1500 ncu --metrics gpu__time_duration.sum --clock-control none -s $((3*N
     --log-file gpurun_out/launches_r02.csv $CMD > gpurun_out/ncu_launches.log 2>&1 || echo "launch list failed"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:gemm2 -s 100 -c 6 \
     -o gpurun_out/prof_gemm_r02 $CMD > gpurun_out/ncu_full_gemm.log 2>&1 || echo "gemm capture failed"
-python scripts/prof_elementwise.py --json gpurun_out/elementwise_r02.jsonl > gpurun_out/prof_ew_plain.log 2>&1 || echo "elementwise plain run failed"
+python scripts/prof_elementwise.py --json gpurun_out/elementwise_r02.jsonl > gpurun_out/prof_ew_timed.log 2>&1 || echo "elementwise timed run failed"
+python scripts/prof_elementwise.py --iters 1 --warm 0 > gpurun_out/prof_ew_plain.log 2>&1 &&
 timeout 900 ncu --set full --clock-control none -k "regex:rmsnorm|swiglu|ce_row|gelu|embed" \
     -o gpurun_out/prof_ew_r02 python scripts/prof_elementwise.py --iters 1 --warm 0 > gpurun_out/ncu_full_ew.log 2>&1 || echo "elementwise capture failed"
 ls -la gpurun_out | tail -8

@@ -131,8 +131,11 @@ def test_gemm_epilogues(L, M, N, K, epi, mode):
 
 
 @pytest.mark.parametrize("dtype", [BF16, F32])
-@pytest.mark.parametrize("rows,cols", [(1, 64), (37, 128), (300, 2048)])
+@pytest.mark.parametrize("rows,cols", [(1, 64), (37, 128), (300, 2048), (4096, 2048), (1003, 4096), (5, 1024),
+                                       (130, 6144)])
 def test_rmsnorm(L, dtype, rows, cols):
+    # cols 2048 / 4096 (bf16) and 1024 / 2048 / 4096 (fp32) take the wide-row backward
+    # (a 256-thread row split, ragged 4-row groups), 6144 / 64 / 128 the per-warp-row one
     rng = np.random.default_rng(2)
     x = rnd(rng, rows, cols, scale=2.0)
     g = rnd(rng, cols, scale=0.5) + 1.0
@@ -156,6 +159,13 @@ def test_rmsnorm(L, dtype, rows, cols):
     assert np.abs(host(rstd) - rs[:, 0]).max() <= 1e-5 * np.abs(rs).max()
     assert np.abs(host(dx) - (dxr + dres)).max() <= tol * np.abs(dxr + dres).max()
     assert np.abs(host(dg) - (dgr + 0.25)).max() <= 1e-4 * max(1, np.abs(dgr).max())
+    # deterministic: a rerun reproduces dx and the gain gradient bit for bit
+    dx2 = torch.empty_like(xd)
+    dg2 = torch.full((cols,), 0.25, device="cuda", dtype=torch.float32)
+    L.call("bm_k_rmsnorm_bwd", dtype, rows, cols, dyd.data_ptr(), xd.data_ptr(), gd.data_ptr(), rstd.data_ptr(),
+           dresd.data_ptr(), dx2.data_ptr(), dg2.data_ptr(), part.data_ptr(), None)
+    torch.cuda.synchronize()
+    assert torch.equal(dx, dx2) and torch.equal(dg, dg2)
 
 
 @pytest.mark.parametrize("dtype", [BF16, F32])
