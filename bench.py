@@ -337,19 +337,34 @@ class Ctx:
         return out
 
 
-def gen_exclude(args, cfg, P, split, strategy):
-    """bigmac.h gen_exclude: "auto" keeps the DP-sharded generator off the stage that
-    holds the most LLM layers when the partition is uneven (it paces the pipeline;
-    DESIGN.md R20), "none" = 0, else a comma list of ranks."""
-    if args.gen_exclude == "none" or P == 1 or strategy == "memory_efficient" or args.head == "dp_shard":
-        return 0
-    if args.gen_exclude != "auto":
-        return sum(1 << int(r) for r in args.gen_exclude.split(","))
+def pacing_stage_mask(split, P):
+    """Bit of the stage holding the most LLM layers when the partition is uneven and
+    that stage is unique (it paces the pipeline), else 0."""
     if not split or len(split) != P:
         return 0
     mx = max(split)
     heavy = [r for r, n in enumerate(split) if n == mx]
     return (1 << heavy[0]) if len(heavy) == 1 else 0
+
+
+def gen_exclude(args, cfg, P, split, strategy):
+    """bigmac.h gen_exclude: "auto" keeps the DP-sharded generator off the pacing stage
+    (R20), "none" = 0, else a comma list of ranks."""
+    if args.gen_exclude == "none" or P == 1 or strategy == "memory_efficient" or args.head == "dp_shard":
+        return 0
+    if args.gen_exclude != "auto":
+        return sum(1 << int(r) for r in args.gen_exclude.split(","))
+    return pacing_stage_mask(split, P)
+
+
+def enc_exclude(args, cfg, P, split, strategy):
+    """bm_sched_cfg.enc_exclude: "auto" moves the pacing stage's encoder microbatches to
+    the next lower stage (R22), "none" = 0, else a comma list of ranks."""
+    if args.enc_exclude == "none" or P == 1 or strategy == "memory_efficient":
+        return 0
+    if args.enc_exclude != "auto":
+        return sum(1 << int(r) for r in args.enc_exclude.split(","))
+    return pacing_stage_mask(split, P)
 
 
 def make_runtime(args, cfg, P, rank, world, group, strategy="bigmac"):
@@ -359,6 +374,9 @@ def make_runtime(args, cfg, P, rank, world, group, strategy="bigmac"):
                 "memory_efficient": {"enc_place": "entry_stage", "gen_place": "last_stage"}}[strategy]
     split = stage_split(args, cfg, P)
     n_last = 0 if split else last_stage_layers(args, cfg, P)
+    ex = enc_exclude(args, cfg, P, split, strategy)
+    if ex:
+        sched_kw = dict(sched_kw, enc_exclude=ex)
     rt = Runtime(cfg, args.dtype, rank=rank, world=world, group=group, sched_kw=sched_kw, head_place=args.head,
                  last_stage_layers=n_last, stage_layers=split, fsdp=args.fsdp,
                  gen_exclude=gen_exclude(args, cfg, P, split, strategy))
@@ -500,6 +518,7 @@ def main():
                     help="encoder / generator parameters: replicated (off), FSDP with BigMac's one-sided pull, "
                          "or FSDP with the all-gather baseline (bigmac.h bm_fsdp_mode, P:401-426)")
     ap.add_argument("--gen-exclude", default="auto", help="ranks that take no generator rows: auto | none | r,r")
+    ap.add_argument("--enc-exclude", default="auto", help="ranks that run no encoder microbatch: auto | none | r,r")
     ap.add_argument("--strategy", default="bigmac", choices=["bigmac", "compute_efficient", "memory_efficient"],
                     help="bigmac (default); the paper's baselines on the same executor (P:129-156)")
     args = ap.parse_args()
@@ -679,7 +698,8 @@ def main():
             "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
             "config": dict(config_dict(cfg, P, D), strategy=args.strategy, head_place=head_place_name(args, N),
                            warmup_units=W, last_stage_layers=n_last, stage_layers=split, step_sum=sum_mode,
-                           gen_exclude=gen_exclude(args, cfg, P, split, args.strategy)),
+                           gen_exclude=gen_exclude(args, cfg, P, split, args.strategy),
+                           enc_exclude=enc_exclude(args, cfg, P, split, args.strategy)),
             "roofline": roofline, "step_roofline": step_roof, "bubble": bubble, "fsdp": fsdp_info,
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches_all, "clocks": clocks,
             "nvlink": ({"bytes_per_step_all_ranks": comm_bytes_all / n_inst,

@@ -87,8 +87,15 @@ typedef struct {
   int32_t cost_fwd;      /* >= 1                         */
   int32_t cost_bwd;      /* >= 1                         */
   int32_t ring_slack;    /* >= 0                         */
-  int32_t reserved[6];   /* must be zero                 */
+  int32_t enc_exclude;   /* bit mask of ranks that run no encoder microbatch (below) */
+  int32_t reserved[5];   /* must be zero                 */
 } bm_sched_cfg;
+/* enc_exclude (BM_ENC_DP_UNIT): unit u's microbatch uP + r runs on rank r,
+ * unless r is in the mask: then on the nearest lower rank not in it, cyclically
+ * (reading R22).  That rank runs two (or more) EncFwd / EncBwd ops per
+ * unit, in microbatch order, and sends / receives their emb / embgrad messages;
+ * the masked ranks run none.  Used to keep the encoder off the pipeline stage
+ * that paces the step. */
 
 /* One operator of a rank's list.  -1 marks an absent field.
  *   EncFwd/EncBwd: mb = unit*P + rank, unit

@@ -16,7 +16,7 @@ import numpy as np
 
 from . import model as om
 from .schedule import (ENC_FWD, ENC_BWD, LLM_FWD, LLM_BWD, GEN_FWD, GEN_BWD, SEND, RECV,
-                       COMPUTE_KINDS, vstage)
+                       COMPUTE_KINDS, enc_owner, vstage)
 
 
 class InterpError(Exception):
@@ -71,7 +71,7 @@ def run(sched, cfg, weights, batch):
         m = op.mb
         if op.kind == ENC_FWD:
             E, cache = om.encoder_fwd(W, cfg, np.asarray(batch.patches[m], np.float64))
-            enc_stash[r][op.unit] = (cache, E)
+            enc_stash[r][m] = (cache, E)
             if r == 0:
                 local[r][("emb", m)] = E
             return {"emb": E}
@@ -80,7 +80,7 @@ def run(sched, cfg, weights, batch):
                 dE = local[r].pop(("embgrad", m))
             else:
                 dE = take(r, "embgrad", m)[0]
-            cache, _ = enc_stash[r].pop(op.unit)
+            cache, _ = enc_stash[r].pop(m)
             om.encoder_bwd(W, cfg, cache, dE, G[r])
             if r == 0:
                 local[r].pop(("emb", m), None)
@@ -92,7 +92,7 @@ def run(sched, cfg, weights, batch):
                 n_mod = int(batch.n_mod[m])
                 if sc.enc_place == "none":
                     raise InterpError("encoder placement 'none' unsupported by the interpreter")
-                own = m % P == 0 or sc.enc_place == "entry_stage"
+                own = enc_owner(sc, m) == 0 if sc.enc_place == "dp_unit" else True
                 emb = local[r][("emb", m)] if own else take(r, "emb", m)[0]
                 x = om.embed_fwd(W, batch.ids[m], emb, n_mod)
             elif (s - 1) % P == r:
@@ -148,7 +148,7 @@ def run(sched, cfg, weights, batch):
             out = {}
             if s == 0:
                 dE = om.embed_bwd(cfg, dx, batch.ids[m], int(batch.n_mod[m]), G[r])
-                if m % P == 0 or sc.enc_place == "entry_stage":
+                if sc.enc_place == "entry_stage" or enc_owner(sc, m) == 0:
                     local[r][("embgrad", m)] = dE
                 out["embgrad"] = dE
             else:

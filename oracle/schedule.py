@@ -55,6 +55,7 @@ class SchedCfg:
     cost_fwd: int = 1           # cut-timeline cost ratio, default 1:2
     cost_bwd: int = 2
     ring_slack: int = 1         # extra receive slots per channel above the minimum
+    enc_exclude: int = 0        # bit mask of ranks running no encoder microbatches (DESIGN R22)
 
 
 @dataclass
@@ -102,6 +103,23 @@ def validate(cfg: SchedCfg) -> None:
     if M % P != 0:
         # units of pp_size micro-batches (partition_microbatches P:248)
         raise ScheduleError(E_REMAINDER, f"M={M} is not a multiple of P={P}")
+    if cfg.enc_exclude:
+        full = (1 << P) - 1
+        if cfg.enc_exclude < 0 or cfg.enc_exclude & ~full or cfg.enc_exclude == full:
+            raise ScheduleError(E_INVALID, "enc_exclude: a mask of ranks < P leaving at least one rank")
+        if cfg.enc_place != "dp_unit":
+            raise ScheduleError(E_INVALID, "enc_exclude applies to the DP encoder units")
+
+
+def enc_owner(cfg: SchedCfg, m: int) -> int:
+    """Rank that runs microbatch m's encoder (P:195, reading R3: mb uP+r on rank r);
+    a rank in enc_exclude hands its microbatch to the nearest lower rank not in the
+    mask, cyclically (reading R22)."""
+    P = cfg.stages
+    r = m % P
+    while (cfg.enc_exclude >> r) & 1:
+        r = (r - 1) % P
+    return r
 
 
 # ----------------------------------------------------------------------------
@@ -218,10 +236,15 @@ def nest(cfg: SchedCfg, base, times):
 
     lists = [[] for _ in range(P)]
     nxt = 0
+
+    def unit_ops(kind, u):   # the unit's encoder microbatches on every rank, each rank in mb order
+        for r in range(P):
+            for m in range(u * P, u * P + P):
+                if enc_owner(cfg, m) == r:
+                    lists[r].append(Op(kind, mb=m, unit=u))
     if enc:
         for u in range(min(W, n_u)):
-            for r in range(P):
-                lists[r].append(Op(ENC_FWD, mb=u * P + r, unit=u))
+            unit_ops(ENC_FWD, u)
         nxt = min(W, n_u)
     for _, cls, _, ev in events:
         if cls == 2:
@@ -244,11 +267,9 @@ def nest(cfg: SchedCfg, base, times):
                 lists[r].append(Op(GEN_BWD, mb=m))
         else:
             u = ev[1]
-            for r in range(P):
-                lists[r].append(Op(ENC_BWD, mb=u * P + r, unit=u))
+            unit_ops(ENC_BWD, u)
             if nxt < n_u:
-                for r in range(P):
-                    lists[r].append(Op(ENC_FWD, mb=nxt * P + r, unit=nxt))
+                unit_ops(ENC_FWD, nxt)
                 nxt += 1
     return lists, W
 
@@ -263,8 +284,8 @@ def _recvs_before(cfg: SchedCfg, r: int, op: Op):
         s = vstage(P, r, op.chunk)
         if s > 0 and (s - 1) % P != r:
             out.append(Op(RECV, mb=op.mb, chunk=op.chunk, peer=(s - 1) % P, payload="act"))
-        if s == 0 and cfg.enc_place == "dp_unit" and op.mb % P != 0:
-            out.append(Op(RECV, mb=op.mb, unit=op.mb // P, peer=op.mb % P, payload="emb"))
+        if s == 0 and cfg.enc_place == "dp_unit" and enc_owner(cfg, op.mb) != 0:
+            out.append(Op(RECV, mb=op.mb, unit=op.mb // P, peer=enc_owner(cfg, op.mb), payload="emb"))
     elif op.kind == LLM_BWD:
         s = vstage(P, r, op.chunk)
         if s < P * V - 1 and (s + 1) % P != r:
@@ -295,8 +316,8 @@ def _sends_after(cfg: SchedCfg, r: int, op: Op):
         s = vstage(P, r, op.chunk)
         if s > 0 and (s - 1) % P != r:
             out.append(Op(SEND, mb=op.mb, chunk=op.chunk, peer=(s - 1) % P, payload="grad"))
-        if s == 0 and cfg.enc_place == "dp_unit" and op.mb % P != 0:
-            out.append(Op(SEND, mb=op.mb, unit=op.mb // P, peer=op.mb % P, payload="embgrad"))
+        if s == 0 and cfg.enc_place == "dp_unit" and enc_owner(cfg, op.mb) != 0:
+            out.append(Op(SEND, mb=op.mb, unit=op.mb // P, peer=enc_owner(cfg, op.mb), payload="embgrad"))
     elif op.kind == ENC_FWD and r != 0 and cfg.enc_place == "dp_unit":
         out.append(Op(SEND, mb=op.mb, unit=op.unit, peer=0, payload="emb"))
     elif op.kind == GEN_BWD and cfg.gen_place == "dp_shard" and r != P - 1:
@@ -484,7 +505,7 @@ def compute_deps(cfg: SchedCfg, r: int, op: Op):
         if s > 0:
             deps.append(((s - 1) % P, LLM_FWD, op.mb, (s - 1) // P))
         elif cfg.enc_place == "dp_unit":
-            deps.append((op.mb % P, ENC_FWD, op.mb, -1))
+            deps.append((enc_owner(cfg, op.mb), ENC_FWD, op.mb, -1))
         elif cfg.enc_place == "entry_stage":
             deps.append((0, ENC_FWD, op.mb, -1))
     elif op.kind == LLM_BWD:

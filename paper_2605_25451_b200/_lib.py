@@ -35,7 +35,7 @@ class SchedCfg(C.Structure):
     _fields_ = [("stages", C.c_int32), ("microbatches", C.c_int32), ("vchunks", C.c_int32),
                 ("warmup_units", C.c_int32), ("llm_sched", C.c_int32), ("enc_place", C.c_int32),
                 ("gen_place", C.c_int32), ("cost_fwd", C.c_int32), ("cost_bwd", C.c_int32),
-                ("ring_slack", C.c_int32), ("reserved", C.c_int32 * 6)]
+                ("ring_slack", C.c_int32), ("enc_exclude", C.c_int32), ("reserved", C.c_int32 * 5)]
 
 
 class Op(C.Structure):

@@ -362,6 +362,11 @@ struct bm_ctx {
   int64_t work_bytes = 0;
   std::vector<LlmSlot> llm;
   std::vector<MlpSlot> enc;
+  // encoder stash slot of each live EncFwd (by microbatch): slots are taken round-robin,
+  // which is safe because EncBwd frees them in EncFwd order (units in order, a unit's
+  // microbatches in order) and there are peak_enc_units of them
+  std::map<int, int> enc_slot_of;
+  int enc_next = 0;
   MlpSlot gen;
   char *dwork[2] = {nullptr, nullptr}, *bout[2] = {nullptr, nullptr}, *dh = nullptr, *dgu = nullptr, *dxn = nullptr;
   float* part = nullptr;
@@ -1106,7 +1111,10 @@ struct RecvState {  // the Recv ops seen since the last compute op (consumer inp
 static bm_status op_enc_fwd(bm_ctx& c, const bm_op& o) {
   const auto& m = c.mc;
   const int mb = o.mb, n = c.n_mod[mb];
-  MlpSlot& sl = c.enc[o.unit % c.n_enc_slots];
+  const int es_slot = c.enc_next;
+  c.enc_next = (c.enc_next + 1) % c.n_enc_slots;
+  c.enc_slot_of[mb] = es_slot;
+  MlpSlot& sl = c.enc[es_slot];
   const int nb = m.L_e + 2;   // FSDP buckets: patch, the L_e blocks, projector
   BM_TRY(fsdp_begin(c, 0, fsdp_order(nb, false), c.st));
   BM_TRY(fsdp_acquire(c, 0, 0, c.st));
@@ -1126,7 +1134,8 @@ static bm_status op_enc_fwd(bm_ctx& c, const bm_op& o) {
 static bm_status op_enc_bwd(bm_ctx& c, const bm_op& o, const RecvState& rs) {
   const auto& m = c.mc;
   const int mb = o.mb, n = c.n_mod[mb];
-  MlpSlot& sl = c.enc[o.unit % c.n_enc_slots];
+  MlpSlot& sl = c.enc[c.enc_slot_of.at(mb)];
+  c.enc_slot_of.erase(mb);
   const char* dout = c.rank == 0 ? c.emb_local : recv_slot(c, 0, BM_PAY_EMBGRAD, rs.ops.at(0)->seq);
   const int nb = m.L_e + 2;   // FSDP buckets in reverse: projector, blocks L_e-1..0, patch
   BM_TRY(fsdp_begin(c, 0, fsdp_order(nb, true), c.st));
@@ -1159,11 +1168,10 @@ static bm_status op_llm_fwd(bm_ctx& c, const bm_op& o, const RecvState& rs) {
   // stage input (P:297 embed_preprocess at the entry stage)
   if (s == 0) {
     const int n_mod = c.n_mod[mb];
-    if (c.use_enc_stream && mb % c.P == 0)   // this rank's own encoder output (EncFwd on the encoder stream)
-      BM_CUDA_TRY(cudaStreamWaitEvent(c.st, c.enc_fwd_ev[(mb / c.P) % c.n_enc_slots], 0));
-    const char* emb = c.enc_entry      ? c.enc[mb % c.n_enc_slots].out
-                      : (mb % c.P == 0) ? c.enc[(mb / c.P) % c.n_enc_slots].out
-                                        : recv_slot(c, mb % c.P, BM_PAY_EMB, rs.ops.at(0)->seq);
+    const int owner = c.enc_entry ? 0 : sched::enc_owner(c.sc, mb);
+    if (c.use_enc_stream && owner == 0)   // this rank's own encoder output (EncFwd on the encoder stream)
+      BM_CUDA_TRY(cudaStreamWaitEvent(c.st, c.enc_fwd_ev[c.enc_slot_of.at(mb)], 0));
+    const char* emb = owner == 0 ? c.enc[c.enc_slot_of.at(mb)].out : recv_slot(c, owner, BM_PAY_EMB, rs.ops.at(0)->seq);
     BM_TRY(TY(c, embed_fwd<bf16>(m.S, m.d, n_mod, c.ids + (int64_t)mb * S, (const bf16*)P_(c, "llm.embed"), (const bf16*)emb, (bf16*)sl.x[0], c.st),
               embed_fwd<float>(m.S, m.d, n_mod, c.ids + (int64_t)mb * S, (const float*)P_(c, "llm.embed"), (const float*)emb, (float*)sl.x[0], c.st)));
   } else if ((s - 1) % c.P == c.rank) {
@@ -1315,7 +1323,7 @@ static bm_status op_llm_bwd(bm_ctx& c, const bm_op& o, const RecvState& rs) {
     const int n_mod = c.n_mod[mb];
     BM_TRY(TY(c, embed_bwd<bf16>(m.S, m.d, n_mod, c.ids + (int64_t)mb * S, (const bf16*)c.bout[b], G_(c, "llm.embed"), c.embscr, c.st),
               embed_bwd<float>(m.S, m.d, n_mod, c.ids + (int64_t)mb * S, (const float*)c.bout[b], G_(c, "llm.embed"), c.embscr, c.st)));
-    if (c.enc_entry || mb % c.P == 0) {
+    if (c.enc_entry || sched::enc_owner(c.sc, mb) == 0) {
       if (c.emb_free_pending) {   // the previous EncBwd (encoder stream) has read emb_local
         BM_CUDA_TRY(cudaStreamWaitEvent(c.st, c.emb_free_ev, 0));
         c.emb_free_pending = false;
@@ -2062,6 +2070,8 @@ bm_status bm_step(bm_ctx* c, const bm_batch* b, void* stream) {
   x.gen_done_pending = false;
   x.own_gout.clear();
   x.pull_bytes = 0;
+  x.enc_slot_of.clear();
+  x.enc_next = 0;
   cudaStream_t main_st = x.st;
   x.st_main = main_st;
   if (x.tracing) {
@@ -2134,7 +2144,7 @@ bm_status bm_step(bm_ctx* c, const bm_batch* b, void* stream) {
     switch (o.kind) {
       case BM_OP_ENC_FWD:
         BM_TRY(op_enc_fwd(x, o));
-        if (x.use_enc_stream) BM_CUDA_TRY(cudaEventRecord(x.enc_fwd_ev[o.unit % x.n_enc_slots], x.enc_st));
+        if (x.use_enc_stream) BM_CUDA_TRY(cudaEventRecord(x.enc_fwd_ev[x.enc_slot_of.at(o.mb)], x.enc_st));
         live_enc += enc_unit_bytes;
         break;
       case BM_OP_ENC_BWD:

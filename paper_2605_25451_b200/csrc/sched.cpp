@@ -63,9 +63,24 @@ static void validate(const bm_sched_cfg& c) {
     throw Fail{BM_E_INVALID, "unknown enc_place"};
   if (c.gen_place != BM_GEN_NONE && c.gen_place != BM_GEN_DP_SHARD && c.gen_place != BM_GEN_LAST_STAGE)
     throw Fail{BM_E_INVALID, "unknown gen_place"};
-  for (int i = 0; i < 6; ++i)
+  for (int i = 0; i < 5; ++i)
     if (c.reserved[i] != 0) throw Fail{BM_E_INVALID, "reserved fields must be zero"};
   if (M % P != 0) throw Fail{BM_E_REMAINDER, "M=" + std::to_string(M) + " is not a multiple of P=" + std::to_string(P)};
+  if (c.enc_exclude) {
+    const int64_t full = (P >= 31) ? -1 : (((int64_t)1 << P) - 1);
+    if (c.enc_exclude < 0 || (P < 31 && ((int64_t)c.enc_exclude & ~full)) || (int64_t)c.enc_exclude == full)
+      throw Fail{BM_E_INVALID, "enc_exclude: a mask of ranks < P leaving at least one rank"};
+    if (c.enc_place != BM_ENC_DP_UNIT) throw Fail{BM_E_INVALID, "enc_exclude applies to the DP encoder units"};
+  }
+}
+
+// rank running microbatch m's encoder: m % P (reading R3), or, if that rank is in
+// enc_exclude, the nearest lower rank not in the mask, cyclically (reading R22)
+int enc_owner(const bm_sched_cfg& c, int m) {
+  const int P = c.stages;
+  int r = m % P;
+  while ((c.enc_exclude >> r) & 1) r = (r - 1 + P) % P;
+  return r;
 }
 
 // ---------------------------------------------------------------- LLM base lists
@@ -186,9 +201,14 @@ static std::vector<std::vector<bm_op>> nest(const bm_sched_cfg& c, const std::ve
   });
   std::vector<std::vector<bm_op>> lists(P);
   int nxt = 0;
+  // the unit's encoder microbatches on every rank, each rank in microbatch order
+  auto unit_ops = [&](int kind, int u) {
+    for (int r = 0; r < P; ++r)
+      for (int m = u * P; m < u * P + P; ++m)
+        if (enc_owner(c, m) == r) lists[r].push_back(mk(kind, m, -1, u));
+  };
   if (enc) {
-    for (int u = 0; u < std::min(W, n_u); ++u)
-      for (int r = 0; r < P; ++r) lists[r].push_back(mk(BM_OP_ENC_FWD, u * P + r, -1, u));
+    for (int u = 0; u < std::min(W, n_u); ++u) unit_ops(BM_OP_ENC_FWD, u);
     nxt = std::min(W, n_u);
   }
   for (const Ev& e : ev) {
@@ -214,9 +234,9 @@ static std::vector<std::vector<bm_op>> nest(const bm_sched_cfg& c, const std::ve
       }
     } else {
       const int u = e.idx;
-      for (int r = 0; r < P; ++r) lists[r].push_back(mk(BM_OP_ENC_BWD, u * P + r, -1, u));
+      unit_ops(BM_OP_ENC_BWD, u);
       if (nxt < n_u) {
-        for (int r = 0; r < P; ++r) lists[r].push_back(mk(BM_OP_ENC_FWD, nxt * P + r, -1, nxt));
+        unit_ops(BM_OP_ENC_FWD, nxt);
         ++nxt;
       }
     }
@@ -232,8 +252,8 @@ static void recvs_before(const bm_sched_cfg& c, int r, const bm_op& o, std::vect
   if (o.kind == BM_OP_LLM_FWD) {
     const int s = o.chunk * P + r;
     if (s > 0 && (s - 1) % P != r) out.push_back(mk(BM_OP_RECV, o.mb, o.chunk, -1, (s - 1) % P, BM_PAY_ACT));
-    if (s == 0 && c.enc_place == BM_ENC_DP_UNIT && o.mb % P != 0)
-      out.push_back(mk(BM_OP_RECV, o.mb, -1, o.mb / P, o.mb % P, BM_PAY_EMB));
+    if (s == 0 && c.enc_place == BM_ENC_DP_UNIT && enc_owner(c, o.mb) != 0)
+      out.push_back(mk(BM_OP_RECV, o.mb, -1, o.mb / P, enc_owner(c, o.mb), BM_PAY_EMB));
   } else if (o.kind == BM_OP_LLM_BWD) {
     const int s = o.chunk * P + r;
     if (s < P * V - 1 && (s + 1) % P != r) out.push_back(mk(BM_OP_RECV, o.mb, o.chunk, -1, (s + 1) % P, BM_PAY_GRAD));
@@ -258,8 +278,8 @@ static void sends_after(const bm_sched_cfg& c, int r, const bm_op& o, std::vecto
   } else if (o.kind == BM_OP_LLM_BWD) {
     const int s = o.chunk * P + r;
     if (s > 0 && (s - 1) % P != r) out.push_back(mk(BM_OP_SEND, o.mb, o.chunk, -1, (s - 1) % P, BM_PAY_GRAD));
-    if (s == 0 && c.enc_place == BM_ENC_DP_UNIT && o.mb % P != 0)
-      out.push_back(mk(BM_OP_SEND, o.mb, -1, o.mb / P, o.mb % P, BM_PAY_EMBGRAD));
+    if (s == 0 && c.enc_place == BM_ENC_DP_UNIT && enc_owner(c, o.mb) != 0)
+      out.push_back(mk(BM_OP_SEND, o.mb, -1, o.mb / P, enc_owner(c, o.mb), BM_PAY_EMBGRAD));
   } else if (o.kind == BM_OP_ENC_FWD && r != 0 && c.enc_place == BM_ENC_DP_UNIT) {
     out.push_back(mk(BM_OP_SEND, o.mb, -1, o.unit, 0, BM_PAY_EMB));
   } else if (o.kind == BM_OP_GEN_BWD && c.gen_place == BM_GEN_DP_SHARD && r != P - 1) {
@@ -370,7 +390,7 @@ static void verify_deps(const bm_sched_cfg& c, const std::vector<std::vector<bm_
       if (o.kind == BM_OP_LLM_FWD) {
         const int s = o.chunk * P + r;
         if (s > 0) dep((s - 1) % P, BM_OP_LLM_FWD, o.mb, (s - 1) / P, me);
-        else if (c.enc_place == BM_ENC_DP_UNIT) dep(o.mb % P, BM_OP_ENC_FWD, o.mb, -1, me);
+        else if (c.enc_place == BM_ENC_DP_UNIT) dep(enc_owner(c, o.mb), BM_OP_ENC_FWD, o.mb, -1, me);
         else if (c.enc_place == BM_ENC_ENTRY_STAGE) dep(0, BM_OP_ENC_FWD, o.mb, -1, me);
       } else if (o.kind == BM_OP_LLM_BWD) {
         const int s = o.chunk * P + r;

@@ -13,3 +13,10 @@ struct bm_schedule {
   std::vector<bm_sched_stats> stats;
   std::map<std::tuple<int, int, int>, std::pair<int, int>> rings;  // (src,dst,payload) -> (K, nmsg)
 };
+
+namespace bm {
+namespace sched {
+// rank that runs microbatch m's encoder (bm_sched_cfg.enc_exclude; R3, R22)
+int enc_owner(const bm_sched_cfg& c, int m);
+}  // namespace sched
+}  // namespace bm

@@ -50,7 +50,7 @@ class Sched:
 
 
 def make_cfg(P, M, V=1, warmup_units=0, llm_sched=None, enc_place="dp_unit", gen_place="dp_shard",
-             cost_fwd=1, cost_bwd=2, ring_slack=1) -> L.SchedCfg:
+             cost_fwd=1, cost_bwd=2, ring_slack=1, enc_exclude=0) -> L.SchedCfg:
     if llm_sched is None:
         llm_sched = "1f1b" if V == 1 else "interleaved"
     c = L.SchedCfg()
@@ -59,6 +59,7 @@ def make_cfg(P, M, V=1, warmup_units=0, llm_sched=None, enc_place="dp_unit", gen
     c.enc_place = L.ENC_PLACE[enc_place]
     c.gen_place = L.GEN_PLACE[gen_place]
     c.cost_fwd, c.cost_bwd, c.ring_slack = cost_fwd, cost_bwd, ring_slack
+    c.enc_exclude = enc_exclude
     return c
 
 

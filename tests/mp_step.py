@@ -15,7 +15,7 @@ SPEC: "<gen_place>", "entry_stage+<gen_place>" (memory-efficient baseline), "ce"
 (last_stage_layers = n), "+split<a>-<b>-..." (explicit stage_layers), "+edge"
 (degenerate row counts, synth.edge_counts), "+fsdp" / "+fsdpag" (FSDP with the
 one-sided pull / the all-gather baseline), "+genx<mask>" (ranks in the bit mask take
-no generator rows).
+no generator rows), "+encx<mask>" (ranks in the mask run no encoder microbatch).
 FLAGS: peer = force the library's peer-memory step-end sum (BM_STEP_SUM=peer);
 gm2 = every bf16 contraction on the CTA-pair GEMM (bm_k_gemm_mode 2).
 """
@@ -44,7 +44,8 @@ def parse_spec(spec, M, P):
     edge = "edge" in toks
     fsdp = "pull" if "fsdp" in toks else ("allgather" if "fsdpag" in toks else "off")
     genx = sum(int(t[4:]) for t in toks if t.startswith("genx"))
-    toks = [t for t in toks if t not in ("edge", "fsdp", "fsdpag") and not t.startswith("genx")]
+    encx = sum(int(t[4:]) for t in toks if t.startswith("encx"))
+    toks = [t for t in toks if t not in ("edge", "fsdp", "fsdpag") and not t.startswith(("genx", "encx"))]
     for t in toks:
         if t.startswith("split"):
             split = [int(x) for x in t[5:].split("-")]
@@ -61,6 +62,8 @@ def parse_spec(spec, M, P):
         kw = {"enc_place": "entry_stage", "gen_place": gen.split("+")[1]}
     else:
         kw = {"gen_place": gen}
+    if encx:
+        kw["enc_exclude"] = encx
     return kw, head, last, split, edge, fsdp, genx
 
 

@@ -266,6 +266,7 @@ MR_CASES = [
     ("C1", 2, 4, 1, "f32", "dp_shard+fsdp", 1, ""), ("C1", 2, 8, 2, "bf16", "dp_shard+fsdp", 1, ""),
     ("C1", 2, 4, 1, "f32", "last_stage+fsdp", 1, ""), ("C1", 2, 4, 1, "f32", "dp_shard+fsdpag", 1, ""),
     ("C1M", 2, 4, 1, "bf16", "dp_shard+fsdp", 1, "gm2"), ("C1", 2, 4, 1, "f32", "dp_shard+genx2", 1, ""),
+    ("C1", 2, 8, 2, "f32", "dp_shard+encx2", 1, ""), ("C1", 2, 4, 1, "bf16", "dp_shard+encx1+edge", 1, ""),
     # pipeline replicas (R15)
     ("C1", 1, 4, 1, "f32", "dp_shard", 2, ""), ("C1", 1, 4, 1, "bf16", "dp_shard", 2, ""),
     # the peer-memory step-end sum forced (also where NCCL would be used)
@@ -279,6 +280,9 @@ MR_CASES = [
     ("C1M", 4, 8, 1, "bf16", "dp_shard", 1, "gm2"),
     # generator rows kept off a rank (bigmac.h gen_exclude, reading R20)
     ("C1", 4, 8, 1, "f32", "dp_shard+genx4", 1, ""), ("C1", 4, 8, 1, "bf16", "dp_shard+genx9+edge", 1, ""),
+    # encoder microbatches moved off ranks (bm_sched_cfg.enc_exclude, reading R22)
+    ("C1", 4, 8, 1, "f32", "dp_shard+encx4", 1, ""), ("C1", 4, 8, 1, "bf16", "dp_shard+encx4+genx4", 1, ""),
+    ("C1", 4, 8, 1, "f32", "dp_shard+encx1", 1, ""), ("C1M", 4, 8, 1, "bf16", "dp_shard+encx6+fsdp", 1, ""),
     # FSDP of the encoder / generator: one-sided pull, and the all-gather baseline
     ("C1", 4, 8, 1, "f32", "dp_shard+fsdpag", 1, ""), ("C1M", 4, 8, 1, "bf16", "dp_shard+fsdp", 1, ""),
     ("C1", 4, 8, 1, "f32", "dp_shard+fsdp", 1, ""),

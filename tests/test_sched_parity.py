@@ -23,7 +23,8 @@ def both(P, M, V, **kw):
 @pytest.mark.parametrize("kw", [{}, {"cost_fwd": 1, "cost_bwd": 1}, {"gen_place": "last_stage"},
                                 {"gen_place": "none", "ring_slack": 0}, {"warmup_units": 3},
                                 {"enc_place": "entry_stage", "gen_place": "last_stage"},
-                                {"enc_place": "entry_stage", "gen_place": "dp_shard"}])
+                                {"enc_place": "entry_stage", "gen_place": "dp_shard"},
+                                {"enc_exclude": 1}, {"enc_exclude": 4}, {"enc_exclude": 6, "gen_place": "last_stage"}])
 def test_serialization_identical(P, M, V, kw):
     try:
         o = S.build(S.SchedCfg(P, M, V, llm_sched="1f1b" if V == 1 else "interleaved", **kw))
