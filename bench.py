@@ -477,7 +477,8 @@ def run_sweep(args, cx, rank, world, P, ms_list):
         batch_bytes = torch.cuda.memory_allocated() - mem0
         ms = timed_steps(rt, db, cx, 1, 1)
         st = rt.sched.stats(rt.rank)
-        out.append({"M": M, "global_batch": M, "samples_per_s": M / (ms / 1e3), "ms_per_step": ms,
+        D = world // P
+        out.append({"M": M, "global_batch": M * D, "samples_per_s": M * D / (ms / 1e3), "ms_per_step": ms,
                     "peak_hbm_gb_per_gpu": cx.max(torch.cuda.max_memory_allocated()) / 1e9,
                     "resident_input_gb_rank0": cx.max(batch_bytes if rank == 0 else 0) / 1e9,
                     "stash_peak_bytes_rank0_enc_llm_gen": rt.stash_peak(), "peak_enc_units": st.peak_enc_units,
@@ -611,6 +612,7 @@ def main():
         e2e = {"value": cfg.M * D * args.steps / (ems / 1000.0), "unit": UNIT,
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(4 * world),
                "ms_per_step": ems / args.steps}
+        del lt, hb   # lt views the work buffer: keep the later configurations' peak HBM clean
 
     launches_all = int(cx.sum(launches))
     comm_bytes_all = cx.sum(comm_bytes)
@@ -639,7 +641,8 @@ def main():
             c2 = get_config("C2", P=P, M=16, V=1)
             extra["c2_m16_per_replica"] = run_secondary(args, cx, rank, world, "C2", c2, P, D, max(3, args.steps // 2), 3)
         if args.sweep:
-            extra["batch_sweep"] = {"config": f"{args.config} model, P = {P}, bigmac, 1 timed step per M",
+            extra["batch_sweep"] = {"config": f"{args.config} model, P = {P} x D = {D}, bigmac, 1 timed step per "
+                                              f"per-replica M",
                                     "points": run_sweep(args, cx, rank, world, P,
                                                         [int(x) for x in args.sweep.split(",") if x])}
 

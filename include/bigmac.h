@@ -264,7 +264,10 @@ bm_status bm_ctx_create(const bm_model_cfg* mc, const bm_schedule* s, int32_t ra
 bm_status bm_ctx_sizes_get(const bm_ctx* c, bm_ctx_sizes* out);
 /* Binds the caller's buffers (256-byte aligned, sizes >= bm_ctx_sizes_get).
  * Errors: BM_E_INVALID (null / misaligned), BM_E_OOM (a buffer is too small; the
- * message names it and both sizes), BM_E_CUDA. */
+ * message names it and both sizes), BM_E_STATE (P > 1 and the environment variable
+ * CUDA_DEVICE_MAX_CONNECTIONS unset or < P + 6: every stream of the rank needs its
+ * own hardware queue, and it must be set before the CUDA context exists),
+ * BM_E_CUDA. */
 bm_status bm_ctx_bind(bm_ctx* c, const bm_buffers* b);
 
 /* Peer memory (CUDA IPC over NVLink).  Export any device pointer as a 64-byte

@@ -92,8 +92,8 @@ __device__ __forceinline__ float gelu_grad(float a) {
 }
 
 // ------------------------------------------------------------------ RMSNorm
-// BM_RMS_WIDE=0: the round-1 kernels (two reads of x in the forward, per-warp-row
-// fused backward for wide rows) -- measurement only
+// BM_RMS_WIDE=0: the per-warp-row fused backward for wide rows too (measurement only;
+// a register-resident forward was measured and dropped: 16.3 vs 12.4 us at 4096 x 2048)
 static int g_rms_wide = [] {   // BM_RMS_WIDE=0: the per-warp-row fused kernel for wide rows too (measurement)
   const char* e = getenv("BM_RMS_WIDE");
   return e && e[0] == '0' ? 0 : 1;
@@ -123,49 +123,6 @@ __global__ void rmsnorm_fwd_kernel(int rows, int cols, const T* __restrict__ x, 
 #pragma unroll
     for (int i = 0; i < N; ++i) o.set(i, v.get(i) * r * gv.get(i));
     vstore(yr + c, o);
-  }
-}
-
-// warp per row with the row held in registers (CH 16-byte vectors per lane, all loads
-// in flight at once; x is read from HBM once)
-template <typename T, int CH>
-__global__ void __launch_bounds__(256)
-rmsnorm_fwd_reg_kernel(int rows, int cols, const T* __restrict__ x, const T* __restrict__ g, T* __restrict__ y,
-                       float* __restrict__ rstd) {
-  pdl_enter();
-  constexpr int N = V16<T>::N;
-  const int row = blockIdx.x * 8 + threadIdx.x / 32;
-  const int lane = threadIdx.x % 32;
-  if (row >= rows) return;
-  const T* xr = x + (int64_t)row * cols;
-  V16<T> v[CH];
-  float ss = 0.f;
-#pragma unroll
-  for (int k = 0; k < CH; ++k) {
-    const int c = (k * 32 + lane) * N;
-    if (c < cols) v[k] = vload(xr + c);
-  }
-#pragma unroll
-  for (int k = 0; k < CH; ++k) {
-    const int c = (k * 32 + lane) * N;
-    if (c < cols) {
-#pragma unroll
-      for (int i = 0; i < N; ++i) { const float f = v[k].get(i); ss += f * f; }
-    }
-  }
-  ss = warp_sum(ss);
-  const float r = rsqrtf(ss / cols + RMS_EPS);
-  if (lane == 0) rstd[row] = r;
-  T* yr = y + (int64_t)row * cols;
-#pragma unroll
-  for (int k = 0; k < CH; ++k) {
-    const int c = (k * 32 + lane) * N;
-    if (c < cols) {
-      V16<T> gv = vload(g + c), o;
-#pragma unroll
-      for (int i = 0; i < N; ++i) o.set(i, v[k].get(i) * r * gv.get(i));
-      vstore(yr + c, o);
-    }
   }
 }
 
@@ -236,6 +193,26 @@ colsum2_accum_kernel(int nchunk, int cols, const float* __restrict__ partial, fl
     float s = 0.f;
 #pragma unroll
     for (int q = 0; q < 8; ++q) s += sh[q][threadIdx.x];
+    out[c] += s;
+  }
+}
+// 32 columns x 32 row groups per block (1024 threads): the wide backward's many
+// partial rows summed with 4x the memory parallelism of colsum2; fixed order
+__global__ void __launch_bounds__(1024)
+colsum32_accum_kernel(int nchunk, int cols, const float* __restrict__ partial, float* __restrict__ out) {
+  pdl_enter();
+  __shared__ float sh[32][33];
+  const int c = blockIdx.x * 32 + (threadIdx.x & 31);
+  const int g = threadIdx.x >> 5;
+  float acc = 0.f;
+  if (c < cols)
+    for (int k = g; k < nchunk; k += 32) acc += partial[(int64_t)k * cols + c];
+  sh[g][threadIdx.x & 31] = acc;
+  __syncthreads();
+  if (g == 0 && c < cols) {
+    float s = 0.f;
+#pragma unroll
+    for (int q = 0; q < 32; ++q) s += sh[q][threadIdx.x];
     out[c] += s;
   }
 }
@@ -755,17 +732,6 @@ template <typename T>
 bm_status rmsnorm_fwd(int rows, int cols, const T* x, const T* g, T* y, float* rstd, cudaStream_t st) {
   if (rows <= 0) return BM_OK;
   BM_CHECK_ARG(cols % V16<T>::N == 0, "rmsnorm cols must be a multiple of the vector width");
-  const int ch = ceil_div(cols, 32 * V16<T>::N);
-  const dim3 grid(ceil_div(rows, 8));
-  if (g_rms_wide && ch <= 16) {   // row in registers (BM_RMS_WIDE=0: the two-read kernel)
-    if (ch <= 2) BM_CUDA_TRY(launch_k(rmsnorm_fwd_reg_kernel<T, 2>, grid, dim3(256), 0, st, rows, cols, x, g, y, rstd));
-    else if (ch <= 4) BM_CUDA_TRY(launch_k(rmsnorm_fwd_reg_kernel<T, 4>, grid, dim3(256), 0, st, rows, cols, x, g, y, rstd));
-    else if (ch <= 8) BM_CUDA_TRY(launch_k(rmsnorm_fwd_reg_kernel<T, 8>, grid, dim3(256), 0, st, rows, cols, x, g, y, rstd));
-    else BM_CUDA_TRY(launch_k(rmsnorm_fwd_reg_kernel<T, 16>, grid, dim3(256), 0, st, rows, cols, x, g, y, rstd));
-    count_launch();
-    BM_CUDA_TRY(cudaGetLastError());
-    return BM_OK;
-  }
   BM_CUDA_TRY(launch_k(rmsnorm_fwd_kernel<T>, dim3(ceil_div(rows, 8)), dim3(256), 0, st, rows, cols, x, g, y, rstd));
   count_launch();
   BM_CUDA_TRY(cudaGetLastError());
@@ -869,7 +835,7 @@ static bm_status launch_rms_bwd_wide(int rows, int cols, const T* dy, const T* x
   const int nb = ceil_div(rows, rb);
   BM_CUDA_TRY(launch_k(rmsnorm_bwd_wide_kernel<T, CH>, dim3(nb), dim3(256), 0, st, rows, cols, rb, dy, x, g, rstd, dres,
                        dx, partial));
-  BM_CUDA_TRY(launch_k(colsum2_accum_kernel, dim3(ceil_div(cols, 32)), dim3(256), 0, st, nb, cols, partial, dg));
+  BM_CUDA_TRY(launch_k(colsum32_accum_kernel, dim3(ceil_div(cols, 32)), dim3(1024), 0, st, nb, cols, partial, dg));
   count_launch(2);
   BM_CUDA_TRY(cudaGetLastError());
   return BM_OK;
@@ -1107,9 +1073,7 @@ static void preload_t(std::vector<const void*>& v) {
                         (const void*)rmsnorm_bwd_fused_kernel<T, 2>, (const void*)rmsnorm_bwd_fused_kernel<T, 4>,
                         (const void*)rmsnorm_bwd_fused_kernel<T, 8>, (const void*)rmsnorm_bwd_fused_kernel<T, 16>,
                         (const void*)rmsnorm_bwd_wide_kernel<T, 1>, (const void*)rmsnorm_bwd_wide_kernel<T, 2>,
-                        (const void*)rmsnorm_bwd_wide_kernel<T, 4>, (const void*)rmsnorm_fwd_reg_kernel<T, 2>,
-                        (const void*)rmsnorm_fwd_reg_kernel<T, 4>, (const void*)rmsnorm_fwd_reg_kernel<T, 8>,
-                        (const void*)rmsnorm_fwd_reg_kernel<T, 16>,
+                        (const void*)rmsnorm_bwd_wide_kernel<T, 4>,
                         (const void*)swiglu_fwd_kernel<T>, (const void*)swiglu_bwd_kernel<T>,
                         (const void*)gelu_fwd_kernel<T>, (const void*)gelu_bwd_kernel<T>, (const void*)add_kernel<T>,
                         (const void*)embed_fwd_kernel<T>, (const void*)embed_segsum_kernel<T>,
@@ -1121,7 +1085,8 @@ void preload_elementwise(std::vector<const void*>& v) {
   preload_t<float>(v);
   for (const void* f : {(const void*)cast_kernel<float, bf16>, (const void*)cast_kernel<bf16, float>,
                         (const void*)cast_kernel<float, float>, (const void*)cast_kernel<bf16, bf16>,
-                        (const void*)colsum_accum_kernel, (const void*)colsum2_accum_kernel, (const void*)copy16_kernel,
+                        (const void*)colsum_accum_kernel, (const void*)colsum2_accum_kernel,
+                        (const void*)colsum32_accum_kernel, (const void*)copy16_kernel,
                         (const void*)copy1_kernel, (const void*)zero16_kernel, (const void*)zero1_kernel,
                         (const void*)spin_wait_kernel, (const void*)embed_sort_kernel, (const void*)sum_scale_kernel,
                         (const void*)embed_radix_sort_kernel<4>, (const void*)embed_radix_sort_kernel<8>})

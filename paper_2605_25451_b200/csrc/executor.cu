@@ -1836,6 +1836,18 @@ bm_status bm_ctx_bind(bm_ctx* c, const bm_buffers* b) {
     set_error("cuStreamWaitValue32/cuStreamWriteValue32 unavailable");
     return BM_E_CUDA;
   }
+  if (c->P > 1) {
+    // every stream of the rank (compute, generator, encoder, P-1 comm, 2 FSDP pull, NCCL)
+    // needs its own hardware queue: a comm stream parked on a credit wait must not
+    // block an unrelated stream sharing its queue (a deadlock observed in round 1)
+    const char* e = getenv("CUDA_DEVICE_MAX_CONNECTIONS");
+    const int need = c->P + 6;
+    if (!e || std::atoi(e) < need) {
+      set_error("CUDA_DEVICE_MAX_CONNECTIONS must be >= " + std::to_string(need) +
+                " (set before the CUDA context is created) for a multi-rank context");
+      return BM_E_STATE;
+    }
+  }
   c->bound = true;
   return BM_OK;
 }

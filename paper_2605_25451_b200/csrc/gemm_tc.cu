@@ -1292,6 +1292,12 @@ static int g_gemm_mode = [] {
   return e ? (e[0] == '1' ? 1 : (e[0] == '2' ? 2 : 0)) : 0;
 }();
 int gemm_mode() { return g_gemm_mode; }
+// split-K of the small 1-CTA GEMMs only when a tile has at least this many k-blocks
+// (BM_SPLITK_MIN_NK; 0 disables split-K; each split launch adds a reduce kernel)
+static int g_splitk_min_nk = [] {
+  const char* e = getenv("BM_SPLITK_MIN_NK");
+  return e ? atoi(e) : 4;
+}();
 // BM_GEMM_GROUP_INTERLEAVE=0: keep each pair's grouped tiles problem by problem (measurement)
 static int g_group_interleave = [] {
   const char* e = getenv("BM_GEMM_GROUP_INTERLEAVE");
@@ -1413,7 +1419,7 @@ bm_status gemm_bf16_tc(int M, int N, int K, const void* A, int64_t lda, int a_ma
   // partial tiles in the caller's workspace, summed in split order)
   const int tiles = tm * ceil_div(N, BN);
   const int nk = ceil_div(K, BK);
-  if (ws && ws_bytes > 0 && tiles < num_sms() / 2 && nk >= 4 && N % 4 == 0 &&
+  if (g_splitk_min_nk > 0 && ws && ws_bytes > 0 && tiles < num_sms() / 2 && nk >= g_splitk_min_nk && N % 4 == 0 &&
       (epi == BM_EPI_STORE || epi == BM_EPI_ADD || epi == BM_EPI_ACCUM)) {
     int splits = std::min(8, std::min(num_sms() / tiles, nk / 2));
     const int mpad = tm * BM;

@@ -12,6 +12,8 @@ and the compute-stream idle gaps, attributed to the op that followed them.
 import argparse
 import json
 import os
+
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")   # before the CUDA context (executor.cu)
 import sys
 
 import torch
