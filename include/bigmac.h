@@ -47,7 +47,10 @@ typedef enum {
   BM_E_TIMEOUT = 10
 } bm_status;
 
-typedef enum { BM_LLM_1F1B = 0, BM_LLM_INTERLEAVED = 1 } bm_llm_sched;
+/* BM_LLM_ZB_H1: zero-bubble ZB-H1 (the schedule class P:552-556 names as the
+ * extension; construction DESIGN.md R23): each backward is split into B (input
+ * gradient, BM_OP_LLM_BWD) and W (weight gradient, BM_OP_LLM_W); V must be 1. */
+typedef enum { BM_LLM_1F1B = 0, BM_LLM_INTERLEAVED = 1, BM_LLM_ZB_H1 = 2 } bm_llm_sched;
 /* BM_ENC_DP_UNIT: BigMac (units of P microbatches, one per rank).
  * BM_ENC_ENTRY_STAGE: memory-efficient baseline (Fig. 3): the
  * encoder runs as the entry stage's first layers -- EncFwd(m) right before
@@ -58,7 +61,8 @@ typedef enum { BM_GEN_NONE = 0, BM_GEN_DP_SHARD = 1, BM_GEN_LAST_STAGE = 2 } bm_
 
 typedef enum {
   BM_OP_ENC_FWD = 0, BM_OP_ENC_BWD = 1, BM_OP_LLM_FWD = 2, BM_OP_LLM_BWD = 3,
-  BM_OP_GEN_FWD = 4, BM_OP_GEN_BWD = 5, BM_OP_SEND = 6, BM_OP_RECV = 7
+  BM_OP_GEN_FWD = 4, BM_OP_GEN_BWD = 5, BM_OP_SEND = 6, BM_OP_RECV = 7,
+  BM_OP_LLM_W = 8   /* weight-gradient half of an LLM backward (BM_LLM_ZB_H1 only) */
 } bm_op_kind;   /* compute vs communication operators */
 
 typedef enum {
@@ -75,7 +79,9 @@ typedef enum {
  * warmup_units == 0 selects W* (the minimal dependency-safe warmup, R4).
  * cost_fwd:cost_bwd is the cut-timeline cost ratio that defines "columns"
  * (R1), default 1:2.  ring_slack adds receive slots
- * above the minimal deadlock-free ring size. */
+ * above the minimal deadlock-free ring size.  cost_wgrad (BM_LLM_ZB_H1 only) is
+ * the W share of cost_bwd (B costs cost_bwd - cost_wgrad); 0 selects
+ * cost_bwd / 2; B and W must both cost >= 1, else BM_E_INVALID. */
 typedef struct {
   int32_t stages;        /* P >= 1                       */
   int32_t microbatches;  /* M >= 1, M % P == 0           */
@@ -88,7 +94,8 @@ typedef struct {
   int32_t cost_bwd;      /* >= 1                         */
   int32_t ring_slack;    /* >= 0                         */
   int32_t enc_exclude;   /* bit mask of ranks that run no encoder microbatch (below) */
-  int32_t reserved[5];   /* must be zero                 */
+  int32_t cost_wgrad;    /* >= 0; zero-bubble W cost (0 => cost_bwd / 2) */
+  int32_t reserved[4];   /* must be zero                 */
 } bm_sched_cfg;
 /* enc_exclude (BM_ENC_DP_UNIT): unit u's microbatch uP + r runs on rank r,
  * unless r is in the mask: then on the nearest lower rank not in it, cyclically
@@ -99,7 +106,7 @@ typedef struct {
 
 /* One operator of a rank's list.  -1 marks an absent field.
  *   EncFwd/EncBwd: mb = unit*P + rank, unit
- *   LlmFwd/LlmBwd: mb, chunk
+ *   LlmFwd/LlmBwd/LlmW: mb, chunk
  *   GenFwd/GenBwd: mb (row shard = rank under BM_GEN_DP_SHARD)
  *   Send/Recv:     mb, chunk (act/grad), unit (emb/embgrad), peer, payload,
  *                  slot (= seq mod ring size), seq (per-channel message index) */
@@ -112,7 +119,7 @@ typedef struct {
   int32_t warmup_units;       /* W used                                            */
   int32_t peak_enc_units;     /* max live EncFwd-EncBwd on this rank (<= W) */
   int32_t peak_gen_shards;    /* max live GenFwd-GenBwd (1)                */
-  int32_t peak_llm_inflight;  /* max live LLM F-B (unchanged LLM schedule)  */
+  int32_t peak_llm_inflight;  /* max live LLM F-B (F-W under ZB-H1)        */
   int32_t n_ops;              /* ops incl. comm on this rank                       */
   int64_t llm_idle_cost_units;/* makespan - busy in the cut-timeline DES           */
   int64_t makespan_cost_units;

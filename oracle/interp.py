@@ -15,7 +15,7 @@ from __future__ import annotations
 import numpy as np
 
 from . import model as om
-from .schedule import (ENC_FWD, ENC_BWD, LLM_FWD, LLM_BWD, GEN_FWD, GEN_BWD, SEND, RECV,
+from .schedule import (ENC_FWD, ENC_BWD, LLM_FWD, LLM_BWD, GEN_FWD, GEN_BWD, SEND, RECV, LLM_W,
                        COMPUTE_KINDS, enc_owner, vstage)
 
 
@@ -121,7 +121,8 @@ def run(sched, cfg, weights, batch):
         if op.kind == LLM_BWD:
             c = op.chunk
             s = vstage(P, r, c)
-            ent = llm_stash[r].pop((m, c))
+            zb = sc.llm_sched == "zb_h1"      # B = input gradient; stash kept until W (R23)
+            ent = llm_stash[r][(m, c)] if zb else llm_stash[r].pop((m, c))
             if s == P * V - 1:
                 dHn = ent["dHn"].copy()
                 n_gen = int(batch.n_gen[m])
@@ -144,7 +145,10 @@ def run(sched, cfg, weights, batch):
                 dy = local[r].pop(("grad", m, s + 1))
             else:
                 dy = take(r, "grad", m)[0]
-            dx = om.llm_layers_bwd(W, cfg, om.stage_layers(cfg, s), ent["caches"], dy, G[r])
+            if zb:
+                ent["defer"] = []
+            dx = om.llm_layers_bwd(W, cfg, om.stage_layers(cfg, s), ent["caches"], dy, G[r],
+                                   ent.get("defer"))
             out = {}
             if s == 0:
                 dE = om.embed_bwd(cfg, dx, batch.ids[m], int(batch.n_mod[m]), G[r])
@@ -156,6 +160,10 @@ def run(sched, cfg, weights, batch):
                     local[r][("grad", m, s)] = dx
                 out["grad"] = dx
             return out
+        if op.kind == LLM_W:
+            ent = llm_stash[r].pop((m, op.chunk))
+            om.llm_wgrad(ent.pop("defer"), G[r])
+            return {}
         if op.kind == GEN_FWD:
             lo, hi = shard(m, r)
             if r == P - 1:

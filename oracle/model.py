@@ -159,19 +159,33 @@ def llm_layers_fwd(W, cfg, layers, x):
     return x, caches
 
 
-def llm_layers_bwd(W, cfg, layers, caches, dy, G):
+def llm_layers_bwd(W, cfg, layers, caches, dy, G, defer=None):
+    """Backward of llm_layers_fwd.  With `defer` (a list; zero-bubble B/W split,
+    DESIGN.md R23) the two weight-gradient products dY^T X are appended to it as
+    (name, dY, X) instead of accumulated; llm_wgrad applies them later."""
+    def wgrad(name, dY, X):
+        if defer is None:
+            _acc(G, name, dY.T @ X)
+        else:
+            defer.append((name, dY, X))
     for l, c in zip(reversed(layers), reversed(caches)):
         p = f"llm.layer{l}"
         x, xn, rstd, gu, h = c
-        _acc(G, p + ".down", dy.T @ h)
+        wgrad(p + ".down", dy, h)
         dh = dy @ W[p + ".down"]
         dgu = swiglu_bwd(dh, gu, cfg.f)
-        _acc(G, p + ".gate_up", dgu.T @ xn)
+        wgrad(p + ".gate_up", dgu, xn)
         dxn = dgu @ W[p + ".gate_up"]
         dx, dg = rmsnorm_bwd(dxn, x, W[p + ".norm"], rstd)
         _acc(G, p + ".norm", dg)
         dy = dy + dx
     return dy
+
+
+def llm_wgrad(defer, G):
+    """The W half of a zero-bubble backward: the deferred dY^T X products."""
+    for name, dY, X in defer:
+        _acc(G, name, dY.T @ X)
 
 
 # ----------------------------------------------------------------------------

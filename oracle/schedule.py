@@ -7,6 +7,8 @@ Plain, slow, step-by-step implementation of BigMac's scheduler:
   insert_comm_ops
   deadlock_check        P:317 (+ credit-ring sizing)
   order property
+  zero-bubble base      P:552-556 names zero-bubble pipeline parallelism (Qi et al.)
+                        as the next LLM schedule class; ZB-H1 built as in DESIGN.md R23
 Every reading of an ambiguous passage is listed in DESIGN.md "Readings".
 """
 from __future__ import annotations
@@ -25,9 +27,12 @@ class ScheduleError(Exception):
 
 
 # op kinds and payloads (names are the serialization tokens)
-ENC_FWD, ENC_BWD, LLM_FWD, LLM_BWD, GEN_FWD, GEN_BWD, SEND, RECV = (
-    "EncFwd", "EncBwd", "LlmFwd", "LlmBwd", "GenFwd", "GenBwd", "Send", "Recv")
-COMPUTE_KINDS = (ENC_FWD, ENC_BWD, LLM_FWD, LLM_BWD, GEN_FWD, GEN_BWD)
+ENC_FWD, ENC_BWD, LLM_FWD, LLM_BWD, GEN_FWD, GEN_BWD, SEND, RECV, LLM_W = (
+    "EncFwd", "EncBwd", "LlmFwd", "LlmBwd", "GenFwd", "GenBwd", "Send", "Recv", "LlmW")
+# LLM_W: the weight-gradient half of an LLM backward (zero-bubble schedules, R23);
+# under zb_h1 LLM_BWD computes only the input gradient
+COMPUTE_KINDS = (ENC_FWD, ENC_BWD, LLM_FWD, LLM_BWD, GEN_FWD, GEN_BWD, LLM_W)
+LLM_KIND = {"F": LLM_FWD, "B": LLM_BWD, "W": LLM_W}
 PAYLOADS = ("act", "grad", "emb", "embgrad", "genin", "gengrad")
 
 
@@ -49,13 +54,14 @@ class SchedCfg:
     microbatches: int           # M  (microbatch_num)
     vchunks: int = 1            # V  (vpp size)
     warmup_units: int = 0       # W; 0 => W*
-    llm_sched: str = "1f1b"     # "1f1b" | "interleaved"
+    llm_sched: str = "1f1b"     # "1f1b" | "interleaved" | "zb_h1" (R23)
     enc_place: str = "dp_unit"  # "none" | "dp_unit" | "entry_stage"
     gen_place: str = "dp_shard" # "none" | "dp_shard" | "last_stage"
     cost_fwd: int = 1           # cut-timeline cost ratio, default 1:2
     cost_bwd: int = 2
     ring_slack: int = 1         # extra receive slots per channel above the minimum
     enc_exclude: int = 0        # bit mask of ranks running no encoder microbatches (DESIGN R22)
+    cost_wgrad: int = 0         # zb_h1: W's share of cost_bwd; 0 => cost_bwd // 2 (R23)
 
 
 @dataclass
@@ -94,8 +100,15 @@ def validate(cfg: SchedCfg) -> None:
         raise ScheduleError(E_INVALID, "1F1B requires V == 1")
     if cfg.llm_sched == "interleaved" and V < 2:
         raise ScheduleError(E_INVALID, "interleaved 1F1B requires V >= 2")
-    if cfg.llm_sched not in ("1f1b", "interleaved"):
+    if cfg.llm_sched not in ("1f1b", "interleaved", "zb_h1"):
         raise ScheduleError(E_INVALID, "unknown llm_sched")
+    if cfg.cost_wgrad < 0:
+        raise ScheduleError(E_INVALID, "cost_wgrad must be >= 0")
+    if cfg.llm_sched == "zb_h1":
+        if V != 1:
+            raise ScheduleError(E_INVALID, "ZB-H1 requires V == 1")
+        if not 1 <= wgrad_cost(cfg) < cfg.cost_bwd:
+            raise ScheduleError(E_INVALID, "ZB-H1 needs 1 <= W cost < cost_bwd (B and W both >= 1)")
     if cfg.enc_place not in ("none", "dp_unit", "entry_stage"):
         raise ScheduleError(E_INVALID, "unknown enc_place")
     if cfg.gen_place not in ("none", "dp_shard", "last_stage"):
@@ -109,6 +122,11 @@ def validate(cfg: SchedCfg) -> None:
             raise ScheduleError(E_INVALID, "enc_exclude: a mask of ranks < P leaving at least one rank")
         if cfg.enc_place != "dp_unit":
             raise ScheduleError(E_INVALID, "enc_exclude applies to the DP encoder units")
+
+
+def wgrad_cost(cfg: SchedCfg) -> int:
+    """Cost of the W half of a backward under zb_h1 (the B half costs cost_bwd - W)."""
+    return cfg.cost_wgrad if cfg.cost_wgrad > 0 else cfg.cost_bwd // 2
 
 
 def enc_owner(cfg: SchedCfg, m: int) -> int:
@@ -153,6 +171,82 @@ def llm_base_schedule(P: int, M: int, V: int):
     return out
 
 
+def zb_h1_schedule(P: int, M: int, cf: int, cb: int, cw: int):
+    """Per-rank lists of ('F'|'B'|'W', mb, 0) for the ZB-H1 zero-bubble schedule
+    (R23; P:552-556 points to Qi et al.'s zero-bubble pipelines).
+    The backward is split into B (input gradient, cost cb) and W (weight
+    gradient, cost cw).  Every rank keeps the 1F1B order of its F and B ops
+    (warmup min(P-r-1, M)) and holds at most P microbatches between F and W (the
+    1F1B peak of rank 0, so no rank needs more activation memory than 1F1B's
+    busiest one).  Built by simulating the ranks in time order; a rank free at
+    time t does, in this order of preference:
+      1. its next F if P microbatches are held -> the oldest pending W instead;
+      2. its next F/B if its producer has finished by t;
+      3. the oldest pending W if it ends no later than the earliest time the
+         next F/B can start (the producer's end if it is scheduled, else the
+         producer rank's free time plus the producer's cost), so a W fills
+         idle time without delaying the F/B chain;
+      4. nothing until t + 1.
+    After its last B it runs the pending W's oldest first."""
+    fb = []
+    for r in range(P):
+        w = min(P - r - 1, M)
+        ops = [("F", m) for m in range(w)]
+        for i in range(M - w):
+            ops += [("F", w + i), ("B", i)]
+        ops += [("B", i) for i in range(M - w, M)]
+        fb.append(ops)
+    end = {}
+    lists = [[] for _ in range(P)]
+    t = [0] * P
+    ptr = [0] * P
+    pending = [deque() for _ in range(P)]
+    held = [0] * P
+    active = set(range(P))
+
+    def run_w(r):
+        m = pending[r].popleft()
+        lists[r].append(("W", m, 0))
+        end[(r, "W", m)] = t[r] + cw
+        t[r] += cw
+        held[r] -= 1
+
+    while active:
+        r = min(active, key=lambda x: (t[x], x))   # every other rank is free at >= t[r]
+        if ptr[r] == len(fb[r]):
+            if pending[r]:
+                run_w(r)
+            else:
+                active.discard(r)
+            continue
+        k, m = fb[r][ptr[r]]
+        if k == "F" and held[r] >= P:
+            run_w(r)
+            continue
+        dep = None
+        if k == "F" and r > 0:
+            dep, dep_cost = (r - 1, "F", m), cf
+        if k == "B" and r < P - 1:
+            dep, dep_cost = (r + 1, "B", m), cb
+        if dep is None or (dep in end and end[dep] <= t[r]):
+            lists[r].append((k, m, 0))
+            end[(r, k, m)] = t[r] + (cf if k == "F" else cb)
+            t[r] = end[(r, k, m)]
+            ptr[r] += 1
+            if k == "F":
+                held[r] += 1
+            else:
+                pending[r].append(m)
+        else:
+            q = dep[0]
+            earliest = end[dep] if dep in end else max(t[r], t[q]) + dep_cost
+            if pending[r] and t[r] + cw <= earliest:
+                run_w(r)
+            else:
+                t[r] += 1
+    return lists
+
+
 def vstage(P: int, rank: int, chunk: int) -> int:
     return chunk * P + rank
 
@@ -160,10 +254,11 @@ def vstage(P: int, rank: int, chunk: int) -> int:
 # ----------------------------------------------------------------------------
 # 3. cut timeline: integer DES of the LLM lists
 # ----------------------------------------------------------------------------
-def des_llm(base, P: int, V: int, cf: int, cb: int):
+def des_llm(base, P: int, V: int, cf: int, cb: int, cw: int = 0):
     """start/end of every LLM op with per-rank program order and data deps
-    F(m,s) <- F(m,s-1),  B(m,s) <- B(m,s+1) (and F(m,s) by program order).
-    Returns {(r, 'F'|'B', m, c): (start, end)}; raises E_DEPENDENCY on stall."""
+    F(m,s) <- F(m,s-1),  B(m,s) <- B(m,s+1) (and F(m,s) by program order;
+    W(m,s), zb_h1 only, follows B(m,s) by program order and costs cw).
+    Returns {(r, 'F'|'B'|'W', m, c): (start, end)}; raises E_DEPENDENCY on stall."""
     times = {}
     ptr = [0] * P
     free = [0] * P
@@ -182,7 +277,7 @@ def des_llm(base, P: int, V: int, cf: int, cb: int):
                 if dep is not None and dep not in times:
                     break
                 st = max(free[r], times[dep][1] if dep is not None else 0)
-                en = st + (cf if k == "F" else cb)
+                en = st + {"F": cf, "B": cb, "W": cw}[k]
                 times[(r, k, m, c)] = (st, en)
                 free[r] = en
                 ptr[r] += 1
@@ -256,7 +351,7 @@ def nest(cfg: SchedCfg, base, times):
             # stage's first layers -- EncFwd(m) right before F(m,0), EncBwd(m) right after B(m,0)
             if entry and k == "F" and r == 0 and c == 0:
                 lists[r].append(Op(ENC_FWD, mb=m, unit=m))
-            lists[r].append(Op(LLM_FWD if k == "F" else LLM_BWD, mb=m, chunk=c))
+            lists[r].append(Op(LLM_KIND[k], mb=m, chunk=c))
             if entry and k == "B" and r == 0 and c == 0:
                 lists[r].append(Op(ENC_BWD, mb=m, unit=m))
         elif cls == 0:
@@ -517,6 +612,8 @@ def compute_deps(cfg: SchedCfg, r: int, op: Op):
             deps += [(q, GEN_BWD, op.mb, -1) for q in range(P)]
         elif cfg.gen_place == "last_stage":
             deps.append((P - 1, GEN_BWD, op.mb, -1))
+    elif op.kind == LLM_W:
+        deps.append((r, LLM_BWD, op.mb, op.chunk))
     elif op.kind == ENC_BWD:
         deps.append((r, ENC_FWD, op.mb, -1))
         deps.append((0, LLM_BWD, op.mb, 0))
@@ -528,7 +625,7 @@ def compute_deps(cfg: SchedCfg, r: int, op: Op):
 
 
 def _ckey(r, op):
-    return (r, op.kind, op.mb, op.chunk if op.kind in (LLM_FWD, LLM_BWD) else -1)
+    return (r, op.kind, op.mb, op.chunk if op.kind in (LLM_FWD, LLM_BWD, LLM_W) else -1)
 
 
 def verify_dependencies(cfg: SchedCfg, lists):
@@ -593,8 +690,8 @@ def verify_dependencies(cfg: SchedCfg, lists):
 
 
 def llm_subsequence(ops):
-    return [("F" if o.kind == LLM_FWD else "B", o.mb, o.chunk)
-            for o in ops if o.kind in (LLM_FWD, LLM_BWD)]
+    name = {v: k for k, v in LLM_KIND.items()}
+    return [(name[o.kind], o.mb, o.chunk) for o in ops if o.kind in name]
 
 
 def peak_window(ops, open_kind, close_kind) -> int:
@@ -631,8 +728,14 @@ def order_property(cfg: SchedCfg, ops0):
 def build(cfg: SchedCfg) -> Schedule:
     validate(cfg)
     P, M, V = cfg.stages, cfg.microbatches, cfg.vchunks
-    base = llm_base_schedule(P, M, V)
-    times = des_llm(base, P, V, cfg.cost_fwd, cfg.cost_bwd)
+    if cfg.llm_sched == "zb_h1":
+        cw = wgrad_cost(cfg)
+        cb = cfg.cost_bwd - cw
+        base = zb_h1_schedule(P, M, cfg.cost_fwd, cb, cw)
+    else:
+        cw, cb = 0, cfg.cost_bwd
+        base = llm_base_schedule(P, M, V)
+    times = des_llm(base, P, V, cfg.cost_fwd, cb, cw)
     lists, W = nest(cfg, base, times)
     viol = verify_dependencies(cfg, lists)
     if viol:
@@ -653,12 +756,14 @@ def build(cfg: SchedCfg) -> Schedule:
         for (src, dst, p), K in rings.items():
             if dst == r:
                 rs[p] = max(rs[p], K)
+        # a microbatch's stage activations live from F until B (until W under zb_h1)
+        close = LLM_W if cfg.llm_sched == "zb_h1" else LLM_BWD
         inflight = cur = 0
         for o in lists[r]:
             if o.kind == LLM_FWD:
                 cur += 1
                 inflight = max(inflight, cur)
-            elif o.kind == LLM_BWD:
+            elif o.kind == close:
                 cur -= 1
         stats.append(Stats(
             w_star=ws, warmup_units=W if cfg.enc_place == "dp_unit" else 0,

@@ -16,9 +16,9 @@ STATUS = {0: "OK", 1: "E_INVALID", 2: "E_REMAINDER", 3: "E_WARMUP", 4: "E_DEPEND
           6: "E_CUDA", 7: "E_NCCL", 8: "E_OOM", 9: "E_STATE", 10: "E_TIMEOUT"}
 BF16, F32 = 0, 1
 EPI_STORE, EPI_ACCUM, EPI_ADD = 0, 1, 2
-OP_KINDS = ["EncFwd", "EncBwd", "LlmFwd", "LlmBwd", "GenFwd", "GenBwd", "Send", "Recv"]
+OP_KINDS = ["EncFwd", "EncBwd", "LlmFwd", "LlmBwd", "GenFwd", "GenBwd", "Send", "Recv", "LlmW"]
 PAYLOADS = ["act", "grad", "emb", "embgrad", "genin", "gengrad"]
-LLM_SCHED = {"1f1b": 0, "interleaved": 1}
+LLM_SCHED = {"1f1b": 0, "interleaved": 1, "zb_h1": 2}
 ENC_PLACE = {"none": 0, "dp_unit": 1, "entry_stage": 2}
 GEN_PLACE = {"none": 0, "dp_shard": 1, "last_stage": 2}
 HEAD_PLACE = {"auto": 0, "last_stage": 1, "dp_shard": 2}
@@ -35,7 +35,8 @@ class SchedCfg(C.Structure):
     _fields_ = [("stages", C.c_int32), ("microbatches", C.c_int32), ("vchunks", C.c_int32),
                 ("warmup_units", C.c_int32), ("llm_sched", C.c_int32), ("enc_place", C.c_int32),
                 ("gen_place", C.c_int32), ("cost_fwd", C.c_int32), ("cost_bwd", C.c_int32),
-                ("ring_slack", C.c_int32), ("enc_exclude", C.c_int32), ("reserved", C.c_int32 * 5)]
+                ("ring_slack", C.c_int32), ("enc_exclude", C.c_int32), ("cost_wgrad", C.c_int32),
+                ("reserved", C.c_int32 * 4)]
 
 
 class Op(C.Structure):

@@ -1,6 +1,7 @@
 // sched.cpp -- host schedule builder: BigMac's pipeline scheduler.
 //
-//   get_llm_schedule   Megatron-style 1F1B / interleaved 1F1B lists
+//   get_llm_schedule   Megatron-style 1F1B / interleaved 1F1B lists,
+//                      or ZB-H1 zero-bubble lists with B/W split (R23)
 //   columns            cut timeline = integer DES of the LLM lists with the
 //                      cost_fwd:cost_bwd ratio (R1)
 //   build_schedule     W warmup encoder units, then a sweep over LLM op starts
@@ -17,6 +18,7 @@
 // Output is bit-identical to oracle/schedule.py (tests/test_sched_parity.py).
 #include <algorithm>
 #include <cstring>
+#include <deque>
 #include <map>
 #include <set>
 #include <string>
@@ -39,10 +41,14 @@ struct Fail {
   std::string msg;
 };
 
+enum { LF = 0, LB = 1, LW = 2 };  // F, B (input gradient under ZB-H1), W (weight gradient)
 struct LOp {
-  bool bwd;
+  int k;
   int mb, chunk;
 };
+static const int LLM_OPK[3] = {BM_OP_LLM_FWD, BM_OP_LLM_BWD, BM_OP_LLM_W};
+
+static int wgrad_cost(const bm_sched_cfg& c) { return c.cost_wgrad > 0 ? c.cost_wgrad : c.cost_bwd / 2; }
 
 static bm_op mk(int kind, int mb = -1, int chunk = -1, int unit = -1, int peer = -1, int payload = -1) {
   bm_op o;
@@ -58,12 +64,19 @@ static void validate(const bm_sched_cfg& c) {
     throw Fail{BM_E_INVALID, "costs must be >= 1 and ring_slack >= 0"};
   if (c.llm_sched == BM_LLM_1F1B && V != 1) throw Fail{BM_E_INVALID, "1F1B requires V == 1"};
   if (c.llm_sched == BM_LLM_INTERLEAVED && V < 2) throw Fail{BM_E_INVALID, "interleaved 1F1B requires V >= 2"};
-  if (c.llm_sched != BM_LLM_1F1B && c.llm_sched != BM_LLM_INTERLEAVED) throw Fail{BM_E_INVALID, "unknown llm_sched"};
+  if (c.llm_sched != BM_LLM_1F1B && c.llm_sched != BM_LLM_INTERLEAVED && c.llm_sched != BM_LLM_ZB_H1)
+    throw Fail{BM_E_INVALID, "unknown llm_sched"};
+  if (c.cost_wgrad < 0) throw Fail{BM_E_INVALID, "cost_wgrad must be >= 0"};
+  if (c.llm_sched == BM_LLM_ZB_H1) {
+    if (V != 1) throw Fail{BM_E_INVALID, "ZB-H1 requires V == 1"};
+    const int cw = wgrad_cost(c);
+    if (cw < 1 || cw >= c.cost_bwd) throw Fail{BM_E_INVALID, "ZB-H1 needs 1 <= W cost < cost_bwd (B and W both >= 1)"};
+  }
   if (c.enc_place != BM_ENC_NONE && c.enc_place != BM_ENC_DP_UNIT && c.enc_place != BM_ENC_ENTRY_STAGE)
     throw Fail{BM_E_INVALID, "unknown enc_place"};
   if (c.gen_place != BM_GEN_NONE && c.gen_place != BM_GEN_DP_SHARD && c.gen_place != BM_GEN_LAST_STAGE)
     throw Fail{BM_E_INVALID, "unknown gen_place"};
-  for (int i = 0; i < 5; ++i)
+  for (int i = 0; i < 4; ++i)
     if (c.reserved[i] != 0) throw Fail{BM_E_INVALID, "reserved fields must be zero"};
   if (M % P != 0) throw Fail{BM_E_REMAINDER, "M=" + std::to_string(M) + " is not a multiple of P=" + std::to_string(P)};
   if (c.enc_exclude) {
@@ -91,14 +104,14 @@ static std::vector<std::vector<LOp>> base_lists(int P, int M, int V) {
     int w;
     if (V == 1) {
       w = std::min(P - r - 1, M);
-      for (int m = 0; m < M; ++m) { fwd.push_back({false, m, 0}); bwd.push_back({true, m, 0}); }
+      for (int m = 0; m < M; ++m) { fwd.push_back({LF, m, 0}); bwd.push_back({LB, m, 0}); }
     } else {
       w = std::min(2 * (P - r - 1) + (V - 1) * P, M * V);
       for (int k = 0; k < M * V; ++k) {
         const int g = k / (P * V), j = k % (P * V);
         const int c = j / P, m = g * P + (j % P);
-        fwd.push_back({false, m, c});
-        bwd.push_back({true, m, V - 1 - c});
+        fwd.push_back({LF, m, c});
+        bwd.push_back({LB, m, V - 1 - c});
       }
     }
     const int total = (int)fwd.size();
@@ -110,16 +123,73 @@ static std::vector<std::vector<LOp>> base_lists(int P, int M, int V) {
   return out;
 }
 
+// ZB-H1 (R23): 1F1B order of F and B per rank, at most P microbatches
+// held between F and W; ranks simulated in time order, a free rank preferring
+// (1) the oldest pending W if its next op is an F and P are held, (2) its next
+// F/B if the producer has finished, (3) the oldest pending W if it ends no later
+// than the earliest start of that F/B (producer's end, or producer rank's free
+// time + producer cost if unscheduled), (4) waiting one unit.
+static std::vector<std::vector<LOp>> zb_h1_lists(int P, int M, int cf, int cb, int cw) {
+  std::vector<std::vector<LOp>> fb(P), out(P);
+  for (int r = 0; r < P; ++r) {
+    const int w = std::min(P - r - 1, M);
+    for (int m = 0; m < w; ++m) fb[r].push_back({LF, m, 0});
+    for (int i = 0; i < M - w; ++i) { fb[r].push_back({LF, w + i, 0}); fb[r].push_back({LB, i, 0}); }
+    for (int i = M - w; i < M; ++i) fb[r].push_back({LB, i, 0});
+  }
+  std::vector<int64_t> endF((size_t)P * M, -1), endB((size_t)P * M, -1), t(P, 0);
+  std::vector<size_t> ptr(P, 0);
+  std::vector<int> held(P, 0);
+  std::vector<std::deque<int>> pending(P);
+  std::vector<bool> active(P, true);
+  int n_active = P;
+  auto run_w = [&](int r) {
+    const int m = pending[r].front();
+    pending[r].pop_front();
+    out[r].push_back({LW, m, 0});
+    t[r] += cw;
+    --held[r];
+  };
+  while (n_active) {
+    int r = -1;
+    for (int x = 0; x < P; ++x)
+      if (active[x] && (r < 0 || t[x] < t[r])) r = x;
+    if (ptr[r] == fb[r].size()) {
+      if (!pending[r].empty()) run_w(r);
+      else { active[r] = false; --n_active; }
+      continue;
+    }
+    const LOp o = fb[r][ptr[r]];
+    if (o.k == LF && held[r] >= P) { run_w(r); continue; }
+    int64_t dep = 0;  // 0: no producer; -1: producer not scheduled yet
+    int q = -1, qcost = 0;
+    if (o.k == LF && r > 0) { q = r - 1; qcost = cf; dep = endF[(size_t)q * M + o.mb]; }
+    if (o.k == LB && r < P - 1) { q = r + 1; qcost = cb; dep = endB[(size_t)q * M + o.mb]; }
+    if (dep >= 0 && dep <= t[r]) {
+      out[r].push_back(o);
+      t[r] += (o.k == LF) ? cf : cb;
+      if (o.k == LF) { endF[(size_t)r * M + o.mb] = t[r]; ++held[r]; }
+      else { endB[(size_t)r * M + o.mb] = t[r]; pending[r].push_back(o.mb); }
+      ++ptr[r];
+    } else {
+      const int64_t earliest = dep >= 0 ? dep : std::max(t[r], t[q]) + qcost;
+      if (!pending[r].empty() && t[r] + cw <= earliest) run_w(r);
+      else ++t[r];
+    }
+  }
+  return out;
+}
+
 struct Times {
   int P, M, V;
-  std::vector<int64_t> st, en;  // index(r, bwd, m, c)
-  size_t idx(int r, bool b, int m, int c) const { return (((size_t)r * 2 + (b ? 1 : 0)) * M + m) * V + c; }
+  std::vector<int64_t> st, en;  // index(r, kind, m, c)
+  size_t idx(int r, int k, int m, int c) const { return (((size_t)r * 3 + k) * M + m) * V + c; }
 };
 
-static Times des_llm(const std::vector<std::vector<LOp>>& base, int P, int M, int V, int cf, int cb) {
+static Times des_llm(const std::vector<std::vector<LOp>>& base, int P, int M, int V, int cf, int cb, int cw) {
   Times T{P, M, V, {}, {}};
-  T.st.assign((size_t)P * 2 * M * V, -1);
-  T.en.assign((size_t)P * 2 * M * V, -1);
+  T.st.assign((size_t)P * 3 * M * V, -1);
+  T.en.assign((size_t)P * 3 * M * V, -1);
   std::vector<size_t> ptr(P, 0);
   std::vector<int64_t> freet(P, 0);
   size_t remaining = 0;
@@ -132,19 +202,19 @@ static Times des_llm(const std::vector<std::vector<LOp>>& base, int P, int M, in
         const int s = o.chunk * P + r;
         int64_t dep_end = 0;
         bool has = false;
-        if (!o.bwd && s > 0) {
-          const size_t d = T.idx((s - 1) % P, false, o.mb, (s - 1) / P);
+        if (o.k == LF && s > 0) {
+          const size_t d = T.idx((s - 1) % P, LF, o.mb, (s - 1) / P);
           if (T.en[d] < 0) break;
           dep_end = T.en[d]; has = true;
         }
-        if (o.bwd && s < P * V - 1) {
-          const size_t d = T.idx((s + 1) % P, true, o.mb, (s + 1) / P);
+        if (o.k == LB && s < P * V - 1) {
+          const size_t d = T.idx((s + 1) % P, LB, o.mb, (s + 1) / P);
           if (T.en[d] < 0) break;
           dep_end = T.en[d]; has = true;
         }
         const int64_t start = std::max(freet[r], has ? dep_end : (int64_t)0);
-        const int64_t end = start + (o.bwd ? cb : cf);
-        const size_t me = T.idx(r, o.bwd, o.mb, o.chunk);
+        const int64_t end = start + (o.k == LF ? cf : o.k == LB ? cb : cw);
+        const size_t me = T.idx(r, o.k, o.mb, o.chunk);
         T.st[me] = start; T.en[me] = end;
         freet[r] = end;
         ++ptr[r]; --remaining; prog = true;
@@ -156,15 +226,15 @@ static Times des_llm(const std::vector<std::vector<LOp>>& base, int P, int M, in
 }
 
 static int w_star(const std::vector<LOp>& base0, int P, int M) {
-  std::map<std::tuple<bool, int, int>, int> pos;
-  for (int i = 0; i < (int)base0.size(); ++i) pos[{base0[i].bwd, base0[i].mb, base0[i].chunk}] = i;
+  std::map<std::tuple<int, int, int>, int> pos;
+  for (int i = 0; i < (int)base0.size(); ++i) pos[{base0[i].k, base0[i].mb, base0[i].chunk}] = i;
   const int n_u = M / P;
   int best = 1;
   for (int i = 0; i < n_u; ++i) {
-    const int g = pos[{true, i * P + P - 1, 0}];
+    const int g = pos[{LB, i * P + P - 1, 0}];
     int cnt = 0;
     for (int j = i; j < n_u; ++j)
-      if (pos[{false, j * P, 0}] < g) ++cnt;
+      if (pos[{LF, j * P, 0}] < g) ++cnt;
     best = std::max(best, cnt);
   }
   return best;
@@ -188,12 +258,12 @@ static std::vector<std::vector<bm_op>> nest(const bm_sched_cfg& c, const std::ve
   for (int r = 0; r < P; ++r)
     for (int i = 0; i < (int)base[r].size(); ++i) {
       const LOp& o = base[r][i];
-      ev.push_back({T.st[T.idx(r, o.bwd, o.mb, o.chunk)], 2, r, r, i});
+      ev.push_back({T.st[T.idx(r, o.k, o.mb, o.chunk)], 2, r, r, i});
     }
   if (c.gen_place != BM_GEN_NONE)
-    for (int m = 0; m < M; ++m) ev.push_back({T.en[T.idx(P - 1, false, m, V - 1)], 0, m, 0, m});
+    for (int m = 0; m < M; ++m) ev.push_back({T.en[T.idx(P - 1, LF, m, V - 1)], 0, m, 0, m});
   if (enc)
-    for (int u = 0; u < n_u; ++u) ev.push_back({T.en[T.idx(0, true, u * P + P - 1, 0)], 1, u, 0, u});
+    for (int u = 0; u < n_u; ++u) ev.push_back({T.en[T.idx(0, LB, u * P + P - 1, 0)], 1, u, 0, u});
   std::sort(ev.begin(), ev.end(), [](const Ev& a, const Ev& b) {
     if (a.t != b.t) return a.t < b.t;
     if (a.cls != b.cls) return a.cls < b.cls;
@@ -214,13 +284,13 @@ static std::vector<std::vector<bm_op>> nest(const bm_sched_cfg& c, const std::ve
   for (const Ev& e : ev) {
     if (e.cls == 2) {
       const LOp& o = base[e.r][e.idx];
-      if (enc && !o.bwd && e.r == 0 && o.chunk == 0 && o.mb / P >= nxt)
+      if (enc && o.k == LF && e.r == 0 && o.chunk == 0 && o.mb / P >= nxt)
         throw Fail{BM_E_WARMUP, "W=" + std::to_string(W) + " too small: F(" + std::to_string(o.mb) +
                                     ",0)@0 precedes EncFwd(" + std::to_string(o.mb / P) + ")"};
       // memory-efficient baseline: the encoder is the entry stage's first layers
-      if (entry && !o.bwd && e.r == 0 && o.chunk == 0) lists[0].push_back(mk(BM_OP_ENC_FWD, o.mb, -1, o.mb));
-      lists[e.r].push_back(mk(o.bwd ? BM_OP_LLM_BWD : BM_OP_LLM_FWD, o.mb, o.chunk));
-      if (entry && o.bwd && e.r == 0 && o.chunk == 0) lists[0].push_back(mk(BM_OP_ENC_BWD, o.mb, -1, o.mb));
+      if (entry && o.k == LF && e.r == 0 && o.chunk == 0) lists[0].push_back(mk(BM_OP_ENC_FWD, o.mb, -1, o.mb));
+      lists[e.r].push_back(mk(LLM_OPK[o.k], o.mb, o.chunk));
+      if (entry && o.k == LB && e.r == 0 && o.chunk == 0) lists[0].push_back(mk(BM_OP_ENC_BWD, o.mb, -1, o.mb));
     } else if (e.cls == 0) {
       const int m = e.idx;
       if (c.gen_place == BM_GEN_DP_SHARD) {
@@ -245,7 +315,7 @@ static std::vector<std::vector<bm_op>> nest(const bm_sched_cfg& c, const std::ve
 }
 
 // ---------------------------------------------------------------- comm insertion
-static bool is_compute(int k) { return k <= BM_OP_GEN_BWD; }
+static bool is_compute(int k) { return k <= BM_OP_GEN_BWD || k == BM_OP_LLM_W; }
 
 static void recvs_before(const bm_sched_cfg& c, int r, const bm_op& o, std::vector<bm_op>& out) {
   const int P = c.stages, V = c.vchunks;
@@ -367,7 +437,8 @@ static void verify_deps(const bm_sched_cfg& c, const std::vector<std::vector<bm_
   const int P = c.stages, V = c.vchunks;
   std::map<std::tuple<int, int, int, int>, int> nid;  // (rank, kind, mb, chunk)
   auto key = [](int r, const bm_op& o) {
-    return std::make_tuple(r, o.kind, o.mb, (o.kind == BM_OP_LLM_FWD || o.kind == BM_OP_LLM_BWD) ? o.chunk : -1);
+    const bool llm = o.kind == BM_OP_LLM_FWD || o.kind == BM_OP_LLM_BWD || o.kind == BM_OP_LLM_W;
+    return std::make_tuple(r, o.kind, o.mb, llm ? o.chunk : -1);
   };
   int n = 0;
   for (int r = 0; r < P; ++r)
@@ -398,6 +469,8 @@ static void verify_deps(const bm_sched_cfg& c, const std::vector<std::vector<bm_
         if (s < P * V - 1) dep((s + 1) % P, BM_OP_LLM_BWD, o.mb, (s + 1) / P, me);
         else if (c.gen_place == BM_GEN_DP_SHARD) for (int q = 0; q < P; ++q) dep(q, BM_OP_GEN_BWD, o.mb, -1, me);
         else if (c.gen_place == BM_GEN_LAST_STAGE) dep(P - 1, BM_OP_GEN_BWD, o.mb, -1, me);
+      } else if (o.kind == BM_OP_LLM_W) {
+        dep(r, BM_OP_LLM_BWD, o.mb, o.chunk, me);
       } else if (o.kind == BM_OP_ENC_BWD) {
         dep(r, BM_OP_ENC_FWD, o.mb, -1, me);
         dep(0, BM_OP_LLM_BWD, o.mb, 0, me);
@@ -424,16 +497,18 @@ static int peak_window(const std::vector<bm_op>& ops, int open_k, int close_k) {
 static bm_schedule* build(const bm_sched_cfg& c) {
   validate(c);
   const int P = c.stages, M = c.microbatches, V = c.vchunks;
-  auto base = base_lists(P, M, V);
-  Times T = des_llm(base, P, M, V, c.cost_fwd, c.cost_bwd);
+  const bool zb = c.llm_sched == BM_LLM_ZB_H1;
+  const int cw = zb ? wgrad_cost(c) : 0, cb = c.cost_bwd - cw;
+  auto base = zb ? zb_h1_lists(P, M, c.cost_fwd, cb, cw) : base_lists(P, M, V);
+  Times T = des_llm(base, P, M, V, c.cost_fwd, cb, cw);
   int W = 0;
   auto lists = nest(c, base, T, W);
   verify_deps(c, lists);
   for (int r = 0; r < P; ++r) {  // LLM order preserved
     size_t k = 0;
     for (auto& o : lists[r]) {
-      if (o.kind != BM_OP_LLM_FWD && o.kind != BM_OP_LLM_BWD) continue;
-      if (k >= base[r].size() || base[r][k].bwd != (o.kind == BM_OP_LLM_BWD) || base[r][k].mb != o.mb ||
+      if (o.kind != BM_OP_LLM_FWD && o.kind != BM_OP_LLM_BWD && o.kind != BM_OP_LLM_W) continue;
+      if (k >= base[r].size() || LLM_OPK[base[r][k].k] != o.kind || base[r][k].mb != o.mb ||
           base[r][k].chunk != o.chunk)
         throw Fail{BM_E_DEPENDENCY, "LLM order changed"};
       ++k;
@@ -499,10 +574,11 @@ static bm_schedule* build(const bm_sched_cfg& c) {
     st.warmup_units = enc ? W : 0;
     st.peak_enc_units = peak_window(lists[r], BM_OP_ENC_FWD, BM_OP_ENC_BWD);
     st.peak_gen_shards = peak_window(lists[r], BM_OP_GEN_FWD, BM_OP_GEN_BWD);
-    st.peak_llm_inflight = peak_window(lists[r], BM_OP_LLM_FWD, BM_OP_LLM_BWD);
+    // stage activations live from F until B (until W under ZB-H1)
+    st.peak_llm_inflight = peak_window(lists[r], BM_OP_LLM_FWD, zb ? BM_OP_LLM_W : BM_OP_LLM_BWD);
     st.n_ops = (int)s->ranks[r].size();
     int64_t busy = 0;
-    for (auto& o : base[r]) busy += o.bwd ? c.cost_bwd : c.cost_fwd;
+    for (auto& o : base[r]) busy += o.k == LF ? c.cost_fwd : o.k == LB ? cb : cw;
     st.llm_idle_cost_units = makespan - busy;
     st.makespan_cost_units = makespan;
     for (auto& kv : s->rings)
@@ -519,7 +595,7 @@ static bm_schedule* build(const bm_sched_cfg& c) {
 }  // namespace bm
 
 // ================================================================ C ABI
-static const char* KIND_NAMES[] = {"EncFwd", "EncBwd", "LlmFwd", "LlmBwd", "GenFwd", "GenBwd", "Send", "Recv"};
+static const char* KIND_NAMES[] = {"EncFwd", "EncBwd", "LlmFwd", "LlmBwd", "GenFwd", "GenBwd", "Send", "Recv", "LlmW"};
 static const char* PAY_NAMES[] = {"act", "grad", "emb", "embgrad", "genin", "gengrad"};
 
 extern "C" {

@@ -7,7 +7,7 @@ from dataclasses import dataclass
 from . import _lib as L
 
 # bm_op_kind names (include/bigmac.h)
-KINDS = ("EncFwd", "EncBwd", "LlmFwd", "LlmBwd", "GenFwd", "GenBwd", "Send", "Recv")
+KINDS = ("EncFwd", "EncBwd", "LlmFwd", "LlmBwd", "GenFwd", "GenBwd", "Send", "Recv", "LlmW")
 PAYLOADS = ("act", "grad", "emb", "embgrad", "genin", "gengrad")
 
 
@@ -50,7 +50,7 @@ class Sched:
 
 
 def make_cfg(P, M, V=1, warmup_units=0, llm_sched=None, enc_place="dp_unit", gen_place="dp_shard",
-             cost_fwd=1, cost_bwd=2, ring_slack=1, enc_exclude=0) -> L.SchedCfg:
+             cost_fwd=1, cost_bwd=2, ring_slack=1, enc_exclude=0, cost_wgrad=0) -> L.SchedCfg:
     if llm_sched is None:
         llm_sched = "1f1b" if V == 1 else "interleaved"
     c = L.SchedCfg()
@@ -60,6 +60,7 @@ def make_cfg(P, M, V=1, warmup_units=0, llm_sched=None, enc_place="dp_unit", gen
     c.gen_place = L.GEN_PLACE[gen_place]
     c.cost_fwd, c.cost_bwd, c.ring_slack = cost_fwd, cost_bwd, ring_slack
     c.enc_exclude = enc_exclude
+    c.cost_wgrad = cost_wgrad
     return c
 
 

@@ -66,3 +66,44 @@ def test_golden_file():
     path = os.path.join(os.path.dirname(__file__), "golden", "sched_P4_M8_V2.tsv")
     with open(path) as f:
         assert BS.build(4, 8, 2).serialize() == f.read()
+
+
+ZB_GRID = [(P, M) for P in (1, 2, 3, 4, 8) for M in (P, 2 * P, 8 * P)] + [(4, 64), (8, 64), (8, 256)]
+
+
+@pytest.mark.parametrize("P,M", ZB_GRID)
+@pytest.mark.parametrize("kw", [{}, {"cost_fwd": 2, "cost_bwd": 4, "cost_wgrad": 1}, {"cost_fwd": 1, "cost_bwd": 3},
+                                {"gen_place": "last_stage"}, {"gen_place": "none", "ring_slack": 0},
+                                {"enc_place": "entry_stage", "gen_place": "last_stage"}, {"enc_exclude": 1}])
+def test_zb_h1_serialization_identical(P, M, kw):
+    """ZB-H1 (reading R23): the C++ builder's B/W split lists equal the oracle's."""
+    try:
+        o = S.build(S.SchedCfg(P, M, 1, llm_sched="zb_h1", **kw))
+    except S.ScheduleError as e:
+        with pytest.raises(L.BigMacError) as ce:
+            BS.build(P, M, 1, llm_sched="zb_h1", **kw)
+        assert ce.value.code == e.code
+        return
+    c = BS.build(P, M, 1, llm_sched="zb_h1", **kw)
+    assert c.serialize() == S.serialize(o)
+    for r in range(P):
+        st, so = c.stats(r), o.stats[r]
+        assert (st.w_star, st.peak_enc_units, st.peak_gen_shards, st.peak_llm_inflight, st.n_ops,
+                st.llm_idle_cost_units, st.makespan_cost_units) == \
+            (so.w_star, so.peak_enc_units, so.peak_gen_shards, so.peak_llm_inflight, so.n_ops,
+             so.llm_idle_cost_units, so.makespan_cost_units)
+
+
+@pytest.mark.parametrize("kw", [{"cost_bwd": 1}, {"cost_bwd": 2, "cost_wgrad": 2}, {"cost_wgrad": -1}])
+def test_zb_h1_invalid_costs(kw):
+    with pytest.raises(S.ScheduleError) as e:
+        S.build(S.SchedCfg(4, 8, 1, llm_sched="zb_h1", **kw))
+    with pytest.raises(L.BigMacError) as ce:
+        BS.build(4, 8, 1, llm_sched="zb_h1", **kw)
+    assert ce.value.code == e.value.code == 1
+
+
+def test_zb_h1_requires_v1():
+    with pytest.raises(L.BigMacError) as e:
+        BS.build(2, 4, 2, llm_sched="zb_h1")
+    assert e.value.code == 1
