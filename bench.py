@@ -129,7 +129,19 @@ def workload(args, N):
     P = stages_of(args, N)
     base = get_config(args.config)
     cfg = get_config(args.config, P=P, M=args.microbatches or base.M * P, V=base.V)
+    if getattr(args, "llm_sched", "auto") == "zb_h1":
+        if cfg.V != 1:
+            raise SystemExit("--llm-sched zb_h1 needs a V = 1 config")
+        cfg = cfg.replace(llm_sched="zb_h1")
     return cfg, P, N // P
+
+
+def bubble_bound(cfg, P):
+    """Closed-form LLM bubble: 1F1B / interleaved (P-1)/(MV+P-1); ZB-H1 with
+    F:B:W = 1:1:1 (P-1)/(3M+P-1) (reading R23)."""
+    if cfg.llm_sched == "zb_h1":
+        return (P - 1) / (3 * cfg.M + P - 1)
+    return (P - 1) / (cfg.M * cfg.V + P - 1)
 
 
 # LM head + CE of one microbatch on the last stage, in LLM-layer (fwd+bwd) equivalents,
@@ -182,7 +194,8 @@ SHAPES = {"C2": ("ViT-S", "1B", "small"), "C3": ("ViT-S", "1B", "small"), "C4": 
 def config_dict(cfg, P, D):
     rep_txt = f" x {D} pipeline replicas" if D > 1 else ""
     enc, llm, gen = SHAPES.get(cfg.name, ("synthetic", "synthetic", "synthetic"))
-    sched = "1F1B" if cfg.V == 1 else f"interleaved 1F1B ({cfg.V} chunks/stage)"
+    sched = ("ZB-H1 zero-bubble (B/W split)" if cfg.llm_sched == "zb_h1" else
+             "1F1B" if cfg.V == 1 else f"interleaved 1F1B ({cfg.V} chunks/stage)")
     return {"workload": f"{cfg.name}: {enc}-shaped encoder (d_e={cfg.d_e}, L_e={cfg.L_e}) + {llm}-shaped LLM "
                         f"(d={cfg.d}, f={cfg.f}, L={cfg.L}, vocab={cfg.vocab}) + {gen}-shaped generator (d_g={cfg.d_g}, "
                         f"L_g={cfg.L_g}); nested pipeline P={P} stages{rep_txt}, M={cfg.M} microbatches per replica, "
@@ -372,6 +385,7 @@ def make_runtime(args, cfg, P, rank, world, group, strategy="bigmac"):
     W = args.warmup_units if args.warmup_units >= 0 else (2 if P == 1 else 0)
     sched_kw = {"bigmac": {"warmup_units": W}, "compute_efficient": {"warmup_units": cfg.M // P},
                 "memory_efficient": {"enc_place": "entry_stage", "gen_place": "last_stage"}}[strategy]
+    sched_kw = dict(sched_kw, llm_sched=cfg.llm_sched)
     split = stage_split(args, cfg, P)
     n_last = 0 if split else last_stage_layers(args, cfg, P)
     ex = enc_exclude(args, cfg, P, split, strategy)
@@ -416,9 +430,9 @@ def measure_bubble(rt, db, cx, P, cfg):
     rt.set_trace(False)
     frac, span = bubble_from_trace(tr)
     per = cx.gather(frac)
-    return {"measured_max": max(per), "per_rank": per, "bound": (P - 1) / (cfg.M * cfg.V + P - 1),
+    return {"measured_max": max(per), "per_rank": per, "bound": bubble_bound(cfg, P),
             "how": "1 - busy/step of the LLM compute stream from a per-op CUDA-event trace of one step "
-                   "(max over ranks); bound = 1F1B closed form (P-1)/(MV+P-1)"}
+                   "(max over ranks); bound = closed form: 1F1B (P-1)/(MV+P-1), ZB-H1 (P-1)/(3M+P-1)"}
 
 
 def free_runtime(rt):
@@ -520,6 +534,8 @@ def main():
                          "or FSDP with the all-gather baseline (bigmac.h bm_fsdp_mode, P:401-426)")
     ap.add_argument("--gen-exclude", default="auto", help="ranks that take no generator rows: auto | none | r,r")
     ap.add_argument("--enc-exclude", default="auto", help="ranks that run no encoder microbatch: auto | none | r,r")
+    ap.add_argument("--llm-sched", default="auto", choices=["auto", "zb_h1"],
+                    help="LLM base schedule: auto = 1F1B (V = 1) / interleaved (V > 1); zb_h1 = ZB-H1 zero-bubble")
     ap.add_argument("--strategy", default="bigmac", choices=["bigmac", "compute_efficient", "memory_efficient"],
                     help="bigmac (default); the paper's baselines on the same executor (P:129-156)")
     args = ap.parse_args()
@@ -684,7 +700,7 @@ def main():
                  "hbm_bytes_per_step_all_gpus": hbm_all, "nvlink_bytes_per_step_max_gpu": nvl_per_gpu,
                  "peaks": {"bf16_tflops": peaks["bf16_tflops"], "hbm_gbs": peaks["hbm_gbs"], "nvlink_gbs": 900.0},
                  "bound": max((t_flop, "tensor"), (t_hbm, "hbm"), (t_nvl, "nvlink"))[1],
-                 "bubble_bound": (P - 1) / (cfg.M * cfg.V + P - 1)}
+                 "bubble_bound": bubble_bound(cfg, P)}
 
     cpu = None
     if not args.no_cpu and N == 1:

@@ -113,6 +113,7 @@ struct PEntry {
 };
 
 static int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+static bool is_comm(int k) { return k == BM_OP_SEND || k == BM_OP_RECV; }
 static int round8(int x) { return (x + 7) / 8 * 8; }
 // chunk q of n over [0, count): 4-element (16-byte) aligned boundaries (FSDP shards,
 // peer-sum reduce-scatter chunks)
@@ -282,6 +283,7 @@ struct Chan {
 
 struct LlmSlot {
   std::vector<char*> x, xn, gu, h;
+  std::vector<char*> wdy, wdgu;   // ZB-H1: per layer dY and dgu kept from B for W (R23)
   std::vector<float*> rstd;
   char *gin = nullptr, *Hn = nullptr, *dHn = nullptr;
   float* rstd_f = nullptr;
@@ -466,6 +468,7 @@ struct bm_ctx {
   // 48.6 vs 47.5 samples/s with the separate kernels (profiles/r01/bench_n1_fuse*.log);
   // BM_FUSE_SWIGLU=0 selects GEMM + the vectorised elementwise kernel
   bool fuse_swiglu = !(getenv("BM_FUSE_SWIGLU") && getenv("BM_FUSE_SWIGLU")[0] == '0');
+  bool zb = false;         // BM_LLM_ZB_H1: LLM_BWD = input gradient, LLM_W = weight gradients
   bool peer_copy_ce = !(getenv("BM_PEER_COPY") && std::string(getenv("BM_PEER_COPY")) == "sm");
   int peer_copy_ctas = getenv("BM_PEER_COPY_CTAS") ? std::atoi(getenv("BM_PEER_COPY_CTAS")) : 32;
   bool spin_wait = getenv("BM_WAIT") && std::string(getenv("BM_WAIT")) == "spin";
@@ -621,6 +624,13 @@ static void work_layout(bm_ctx& c, char* base) {
       sl.h[j] = b.take(S * f * es);
     }
     sl.gin = b.take(S * d * es);
+    if (c.zb) {   // the weight-gradient operands B leaves for W
+      sl.wdy.resize(c.lps); sl.wdgu.resize(c.lps);
+      for (int j = 0; j < c.lps; ++j) {
+        sl.wdy[j] = b.take(S * d * es);
+        sl.wdgu[j] = b.take(S * 2 * f * es);
+      }
+    }
     if (last_rank) {
       sl.Hn = b.take(S * d * es);
       sl.dHn = b.take(S * d * es);
@@ -1273,9 +1283,10 @@ static bm_status op_llm_bwd(bm_ctx& c, const bm_op& o, const RecvState& rs) {
       c.gout_pending[og->second] = true;
       c.own_gout.erase(og);
     }
-    BM_TRY(norm_bwd(c, m.S, m.d, sl.dHn, sl.x[sl.nl], P_(c, "llm.final_norm"), sl.rstd_f, nullptr, c.dwork[0],
+    char* top = (c.zb && sl.nl > 0) ? sl.wdy[sl.nl - 1] : c.dwork[0];
+    BM_TRY(norm_bwd(c, m.S, m.d, sl.dHn, sl.x[sl.nl], P_(c, "llm.final_norm"), sl.rstd_f, nullptr, top,
                     G_(c, "llm.final_norm")));
-    cur = c.dwork[0];
+    cur = top;
   } else if ((s + 1) % c.P == c.rank) {
     cur = sl.gin;
   } else {
@@ -1291,7 +1302,21 @@ static bm_status op_llm_bwd(bm_ctx& c, const bm_op& o, const RecvState& rs) {
   char nm[64];
   int l0, nl;
   stage_layers(m, c.P * c.V, s, &l0, &nl);
-  for (int j = nl - 1; j >= 0; --j) {
+  if (c.zb) {
+    // ZB-H1 B: input gradient only; every layer's dY and dgu stay in the slot for W (R23)
+    if (nl > 0 && cur != sl.wdy[nl - 1]) BM_TRY(d2d(c, sl.wdy[nl - 1], cur, S * d * es));
+    for (int j = nl - 1; j >= 0; --j) {
+      const int l = l0 + j;
+      char* out = (j == 0) ? c.bout[b] : sl.wdy[j - 1];
+      snprintf(nm, sizeof nm, "llm.layer%d.down", l);
+      BM_TRY(lin_down_dgrad_swiglu(c, sl.wdy[j], P_(c, nm), LD_(c, nm), sl.gu[j], c.dh, sl.wdgu[j]));
+      snprintf(nm, sizeof nm, "llm.layer%d.gate_up", l);
+      BM_TRY(lin_dgrad(c, m.S, m.d, 2 * m.f, sl.wdgu[j], P_(c, nm), LD_(c, nm), c.dxn, m.d));
+      snprintf(nm, sizeof nm, "llm.layer%d.norm", l);
+      BM_TRY(norm_bwd(c, m.S, m.d, c.dxn, sl.x[j], P_(c, nm), sl.rstd[j], sl.wdy[j], out, G_(c, nm)));
+    }
+  }
+  for (int j = c.zb ? -1 : nl - 1; j >= 0; --j) {
     const int l = l0 + j;
     char* out = (j == 0) ? c.bout[b] : (cur == c.dwork[0] ? c.dwork[1] : c.dwork[0]);
     snprintf(nm, sizeof nm, "llm.layer%d.down", l);
@@ -1334,7 +1359,30 @@ static bm_status op_llm_bwd(bm_ctx& c, const bm_op& o, const RecvState& rs) {
   } else if ((s - 1) % c.P == c.rank) {
     BM_TRY(d2d(c, c.llm[c.llm_live.at({mb, ch - 1})].gin, c.bout[b], S * d * es));
   }
-  c.llm_live.erase({mb, ch});
+  if (!c.zb) {   // under ZB-H1 the stash lives until W
+    c.llm_live.erase({mb, ch});
+    c.llm_free.push_back(slot);
+  }
+  return BM_OK;
+}
+
+// ZB-H1 W (R23): the two weight-gradient GEMMs of every layer, dW += dY^T X with the
+// operands B left in the slot (down: dY, h; gate_up: dgu, xn); then the slot is free
+static bm_status op_llm_w(bm_ctx& c, const bm_op& o) {
+  const auto& m = c.mc;
+  const int slot = c.llm_live.at({o.mb, o.chunk});
+  LlmSlot& sl = c.llm[slot];
+  int l0, nl;
+  stage_layers(m, c.P * c.V, o.chunk * c.P + c.rank, &l0, &nl);
+  char nd[64], ng[64];
+  for (int j = nl - 1; j >= 0; --j) {
+    snprintf(nd, sizeof nd, "llm.layer%d.down", l0 + j);
+    snprintf(ng, sizeof ng, "llm.layer%d.gate_up", l0 + j);
+    GemmSpec sp[2] = {spec_wgrad(m.S, m.f, m.d, sl.wdy[j], sl.h[j], m.f, G_(c, nd), LD_(c, nd)),
+                      spec_wgrad(m.S, m.d, 2 * m.f, sl.wdgu[j], sl.xn[j], m.d, G_(c, ng), LD_(c, ng))};
+    BM_TRY(timed_group(c, sp, 2));
+  }
+  c.llm_live.erase({o.mb, o.chunk});
   c.llm_free.push_back(slot);
   return BM_OK;
 }
@@ -1671,7 +1719,8 @@ bm_status bm_ctx_create(const bm_model_cfg* mc, const bm_schedule* s, int32_t ra
     return BM_E_INVALID;
   }
   const bm_sched_stats& st = s->stats[rank];
-  c->n_llm_slots = std::max(st.peak_llm_inflight, 1);
+  c->zb = s->cfg.llm_sched == BM_LLM_ZB_H1;
+  c->n_llm_slots = std::max(st.peak_llm_inflight, 1);   // F..B (F..W under ZB-H1)
   c->n_enc_slots = std::max(st.peak_enc_units, 1);
   {
     int nk = 0;
@@ -1722,7 +1771,7 @@ bm_status bm_ctx_create(const bm_model_cfg* mc, const bm_schedule* s, int32_t ra
   for (size_t i = 0; i < ops.size(); ++i) {
     if (ops[i].kind != BM_OP_RECV) continue;
     size_t j = i + 1;
-    while (ops[j].kind > BM_OP_GEN_BWD) ++j;
+    while (is_comm(ops[j].kind)) ++j;
     if (ops[i].payload == BM_PAY_GENIN)
       while (ops[j].kind != BM_OP_GEN_BWD) ++j;
     c->release_of[j].push_back((int)i);
@@ -1730,7 +1779,7 @@ bm_status bm_ctx_create(const bm_model_cfg* mc, const bm_schedule* s, int32_t ra
   c->consumer_kind.assign(ops.size(), -1);
   for (size_t i = 0; i < ops.size(); ++i) {
     size_t j = i;
-    while (j < ops.size() && ops[j].kind > BM_OP_GEN_BWD) ++j;
+    while (j < ops.size() && is_comm(ops[j].kind)) ++j;
     c->consumer_kind[i] = j < ops.size() ? ops[j].kind : -1;
   }
   // generator ops run on a high-priority stream whenever there is a generator: they
@@ -2101,7 +2150,7 @@ bm_status bm_step(bm_ctx* c, const bm_batch* b, void* stream) {
   const char* gen_x = nullptr;
   int64_t live_enc = 0, live_llm = 0, live_gen = 0;
   const int64_t enc_unit_bytes = (int64_t)m.max_n_mod * (m.d_e * (m.L_e + 1) + m.L_e * (m.d_e + 2 * m.f_e) + 3 * m.d) * x.es;
-  const int64_t llm_unit_bytes = (int64_t)m.S * (x.lps * (2 * m.d + 3 * m.f) + m.d) * x.es;
+  const int64_t llm_unit_bytes = (int64_t)m.S * (x.lps * (2 * m.d + 3 * m.f + (x.zb ? m.d + 2 * m.f : 0)) + m.d) * x.es;
   const int64_t gen_unit_bytes = (int64_t)x.gen_rows * (m.d_g * (m.L_g + 1) + m.L_g * (m.d_g + 2 * m.f_g) + 2 * m.d_t) * x.es;
   for (int k = 0; k < 3; ++k) x.stash_peak[k] = 0;
   for (size_t i = 0; i < ops.size(); ++i) {
@@ -2172,7 +2221,11 @@ bm_status bm_step(bm_ctx* c, const bm_batch* b, void* stream) {
         BM_TRY(op_llm_fwd(x, o, rs));
         live_llm += llm_unit_bytes;
         break;
-      case BM_OP_LLM_BWD: BM_TRY(op_llm_bwd(x, o, rs)); live_llm -= llm_unit_bytes; break;
+      case BM_OP_LLM_BWD:
+        BM_TRY(op_llm_bwd(x, o, rs));
+        if (!x.zb) live_llm -= llm_unit_bytes;
+        break;
+      case BM_OP_LLM_W: BM_TRY(op_llm_w(x, o)); live_llm -= llm_unit_bytes; break;
       case BM_OP_GEN_FWD:
         gen_x = nullptr;
         if (x.rank != x.P - 1 && !rs.ops.empty()) {

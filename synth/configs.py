@@ -98,7 +98,7 @@ def get_config(name: str, **overrides) -> ModelShape:
     cfg = CONFIGS[name]
     if overrides:
         cfg = cfg.replace(**overrides)
-    if cfg.V == 1 and cfg.llm_sched != "1f1b":
+    if cfg.V == 1 and cfg.llm_sched not in ("1f1b", "zb_h1"):
         cfg = cfg.replace(llm_sched="1f1b")
     if cfg.V >= 2 and cfg.llm_sched != "interleaved":
         cfg = cfg.replace(llm_sched="interleaved")

@@ -15,7 +15,8 @@ SPEC: "<gen_place>", "entry_stage+<gen_place>" (memory-efficient baseline), "ce"
 (last_stage_layers = n), "+split<a>-<b>-..." (explicit stage_layers), "+edge"
 (degenerate row counts, synth.edge_counts), "+fsdp" / "+fsdpag" (FSDP with the
 one-sided pull / the all-gather baseline), "+genx<mask>" (ranks in the bit mask take
-no generator rows), "+encx<mask>" (ranks in the mask run no encoder microbatch).
+no generator rows), "+encx<mask>" (ranks in the mask run no encoder microbatch),
+"+zb" (ZB-H1 zero-bubble LLM schedule, B/W split, reading R23).
 FLAGS: peer = force the library's peer-memory step-end sum (BM_STEP_SUM=peer);
 gm2 = every bf16 contraction on the CTA-pair GEMM (bm_k_gemm_mode 2).
 """
@@ -45,7 +46,8 @@ def parse_spec(spec, M, P):
     fsdp = "pull" if "fsdp" in toks else ("allgather" if "fsdpag" in toks else "off")
     genx = sum(int(t[4:]) for t in toks if t.startswith("genx"))
     encx = sum(int(t[4:]) for t in toks if t.startswith("encx"))
-    toks = [t for t in toks if t not in ("edge", "fsdp", "fsdpag") and not t.startswith(("genx", "encx"))]
+    zb = "zb" in toks
+    toks = [t for t in toks if t not in ("edge", "fsdp", "fsdpag", "zb") and not t.startswith(("genx", "encx"))]
     for t in toks:
         if t.startswith("split"):
             split = [int(x) for x in t[5:].split("-")]
@@ -64,6 +66,8 @@ def parse_spec(spec, M, P):
         kw = {"gen_place": gen}
     if encx:
         kw["enc_exclude"] = encx
+    if zb:
+        kw["llm_sched"] = "zb_h1"
     return kw, head, last, split, edge, fsdp, genx
 
 

@@ -88,3 +88,14 @@ def test_step_hbm_bytes_is_below_the_flop_term_at_c2():
     assert b / 6555e9 < f / 1664.4e12
     # weights are read per microbatch: bytes grow linearly in M
     assert abs(bench.step_hbm_bytes(cfg, [554] * 4, [554] * 4) - 4 * b) < 1e-6 * b
+
+
+def test_zb_h1_workload_and_bubble_bound():
+    cfg, P, D = bench.workload(ns(llm_sched="zb_h1"), 4)
+    assert (cfg.llm_sched, P, D, cfg.M) == ("zb_h1", 4, 1, 64)
+    assert bench.bubble_bound(cfg, P) == pytest.approx(3 / (3 * 64 + 3))
+    ref, _, _ = bench.workload(ns(), 4)
+    assert bench.bubble_bound(ref, P) == pytest.approx(3 / 67)
+    assert "ZB-H1" in bench.config_dict(cfg, P, D)["workload"]
+    with pytest.raises(SystemExit):
+        bench.workload(ns(config="C3", llm_sched="zb_h1"), 4)

@@ -223,6 +223,33 @@ def test_step_single_gpu_medium(oracle_cache, dtype, M, V, gemm_mode):
     rt.close()
 
 
+@pytest.mark.parametrize("cfg_name,dtype,gemm_mode", [("C1", "f32", 0), ("C1", "bf16", 0), ("C1M", "f32", 0),
+                                                     ("C1M", "bf16", 2)], indirect=["gemm_mode"])
+def test_step_single_gpu_zb_h1(oracle_cache, cfg_name, dtype, gemm_mode):
+    """ZB-H1 base schedule (reading R23) at P = 1: LLM_BWD computes only the input
+    gradient and leaves dY / dgu per layer in the stash slot, LLM_W runs the weight
+    gradient GEMMs -- same loss and gradients as the oracle."""
+    from paper_2605_25451_b200.runtime import Runtime
+    cfg = get_config(cfg_name, P=1, M=4, V=1)
+    W, B, (loss_ref, per_ref, G_ref) = reference(oracle_cache, cfg)
+    rt = Runtime(cfg, dtype, sched_kw={"llm_sched": "zb_h1"})
+    assert any(o[0] == 8 for o in rt.sched.ops(0))          # BM_OP_LLM_W present
+    rt.load_weights(W)
+    db = rt.device_batch(B)
+    rt.step(db)
+    torch.cuda.synchronize()
+    loss, ce, mse = rt.losses()
+    tol = TOL[dtype]
+    assert abs(loss - loss_ref) <= tol * abs(loss_ref)
+    bad = {n: rel(rt.grad(n), G_ref[n]) for n in rt.names()}
+    assert not {k: v for k, v in bad.items() if v > tol}, bad
+    g1 = rt.grads_t.clone()
+    rt.step(db)
+    torch.cuda.synchronize()
+    assert torch.equal(g1, rt.grads_t)
+    rt.close()
+
+
 def _torchrun(nproc, cases, timeout=900):
     """Launch mp_step.py on nproc ranks for a batch of cases.  With fewer GPUs than
     ranks every rank runs on cuda:0 (BM_TEST_ONE_GPU=1): stage-boundary copies,
@@ -286,6 +313,12 @@ MR_CASES = [
     # FSDP of the encoder / generator: one-sided pull, and the all-gather baseline
     ("C1", 4, 8, 1, "f32", "dp_shard+fsdpag", 1, ""), ("C1M", 4, 8, 1, "bf16", "dp_shard+fsdp", 1, ""),
     ("C1", 4, 8, 1, "f32", "dp_shard+fsdp", 1, ""),
+    # ZB-H1 zero-bubble base schedule (B = input gradient, W = weight gradients; R23)
+    ("C1", 2, 4, 1, "f32", "dp_shard+zb", 1, ""), ("C1", 2, 4, 1, "bf16", "dp_shard+zb", 1, ""),
+    ("C1M", 2, 4, 1, "bf16", "dp_shard+zb", 1, "gm2"), ("C1", 2, 4, 1, "f32", "entry_stage+last_stage+zb", 1, ""),
+    ("C1", 4, 8, 1, "f32", "dp_shard+zb", 1, ""), ("C1", 4, 16, 1, "bf16", "dp_shard+zb", 1, ""),
+    ("C1", 4, 8, 1, "f32", "last_stage+zb+edge", 1, ""), ("C1M", 4, 8, 1, "bf16", "dp_shard+zb+fsdp", 1, "gm2"),
+    ("C1", 2, 4, 1, "f32", "dp_shard+zb", 2, ""),
     # P = 2 x D = 2
     ("C1", 2, 4, 1, "f32", "dp_shard", 2, ""), ("C1", 2, 4, 1, "bf16", "dp_shard", 2, ""),
     ("C1", 2, 8, 2, "f32", "dp_shard", 2, ""), ("C1", 2, 4, 1, "f32", "dp_shard", 2, "peer"),
