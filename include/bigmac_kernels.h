@@ -90,6 +90,11 @@ bm_status bm_k_gemm_group(const bm_gemm_desc* descs, int32_t n, void* stream);
  * cta_group::2 256xBN tiles when M >= 512, N >= 256, K >= 256; 128xBN 1-CTA
  * tiles otherwise), 1 = always 1-CTA, 2 = always CTA pairs.  Process-wide. */
 bm_status bm_k_gemm_mode(int32_t mode);
+/* Pair-tile width of the CTA-pair GEMM: 0 = 256 x 256 tiles (two TMEM accumulators,
+ * the epilogue of one tile overlaps the next tile's MMAs), 1 = 256 x 512 tiles
+ * whenever N >= 512 (one 512-column accumulator; a quarter less L2 -> SMEM traffic
+ * per FLOP), 2 = auto (256 x 512 when N >= 512 and K >= 4096).  Process-wide. */
+bm_status bm_k_gemm_bn512(int32_t mode);
 
 /* RMSNorm y = x * rstd * g, rstd = 1/sqrt(mean(x^2) + 1e-5); rstd saved (fp32 [rows]). */
 bm_status bm_k_rmsnorm_fwd(int32_t dtype, int32_t rows, int32_t cols, const void* x,

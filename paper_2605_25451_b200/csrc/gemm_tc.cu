@@ -749,17 +749,21 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
 // ============================================================================
 constexpr int EPI_WARPS2 = 8;   // CTA-pair kernel: two epilogue warps per TMEM lane quadrant
 constexpr int NUM_THREADS2 = 64 + 32 * EPI_WARPS2;
+// BN = 512 (pair tile 256 x 512, each CTA 128 x 512): a quarter less L2 -> SMEM
+// traffic per FLOP than 256 x 256 (cuBLAS's tile on these shapes), at the price of a
+// single TMEM accumulator (512 columns): the MMA waits for the epilogue between tiles
 template <int BN, bool SWI = false> struct Cfg2 {
   static constexpr int A_BYTES = 128 * BK * 2;                 // 16 KB
-  static constexpr int B_BYTES = (BN / 2) * BK * 2;            // 16 KB (BN = 256)
+  static constexpr int B_BYTES = (BN / 2) * BK * 2;            // 16 KB (BN = 256), 32 KB (BN = 512)
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   // staging slots per epilogue warp: with 2, a chunk's TMA stores read one while the
   // next chunk is staged in the other (wait_group.read 1); with 1, read 0
   // (measured: 2 slots with 5 stages gains 1.5 % on the SwiGLU-backward dgrad and
   // loses 3-4 % on the fp32 wgrads, so the non-SwiGLU kernels keep 1 slot, 6 stages)
   static constexpr int NSLOT = 1;
-  static constexpr int STAGES = SWI ? 5 : ((BN == 256) ? 6 : 8);
-  static constexpr int TMEM_COLS = 2 * BN;
+  static constexpr int STAGES = SWI ? 5 : (BN == 512 ? 4 : ((BN == 256) ? 6 : 8));
+  static constexpr int NACC = BN == 512 ? 1 : 2;               // TMEM accumulator buffers
+  static constexpr int TMEM_COLS = NACC * BN;
   static constexpr int EPI_SLOT = SWI ? 6144 : 4096;           // staging slot of one epilogue warp
   static constexpr int EPI_BYTES = EPI_WARPS2 * NSLOT * EPI_SLOT;
   static constexpr int SMEM = STAGES * STAGE_BYTES + EPI_BYTES + 1024 + 256;
@@ -944,7 +948,21 @@ gemm2_kernel(const __grid_constant__ PairGroup g) {
           } else {
             tma_load_2d_pair(a_dst, mA, lbar, k0, m0);
           }
-          if (bmn) {
+          if (BN == 512) {
+            // two 128-row halves, half h = global columns [nb*512 + h*256, +256) of the pair
+            // (CTA c holds rows [c*128, +128) of each half), so TMEM columns map contiguously
+            const int nh = nb * BN + (int)cta * 128;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              if (bmn) {
+#pragma unroll
+                for (int j = 0; j < 2; ++j)
+                  tma_load_2d_pair(b_dst + h * 16384 + j * (BK * 128), mB, lbar, nh + h * 256 + 64 * j, k0);
+              } else {
+                tma_load_2d_pair(b_dst + h * 16384, mB, lbar, k0, nh + h * 256);
+              }
+            }
+          } else if (bmn) {
 #pragma unroll
             for (int j = 0; j < BNH / 64; ++j) tma_load_2d_pair(b_dst + j * (BK * 128), mB, lbar, n0 + 64 * j, k0);
           } else {
@@ -965,9 +983,9 @@ gemm2_kernel(const __grid_constant__ PairGroup g) {
         const PairProblem& pr = g.prob[pi];
         const bool amn = AM >= 0 ? AM != 0 : pr.a_mn != 0, bmn = BMJ >= 0 ? BMJ != 0 : pr.b_mn != 0;
         const int nk = pr.nk;
-        const uint32_t idesc = make_idesc(BN, amn, bmn, 2 * BM);
-        const int acc = local & 1;
-        const uint32_t acc_phase = (local >> 1) & 1;
+        const uint32_t idesc = make_idesc(BN == 512 ? 256 : BN, amn, bmn, 2 * BM);
+        const int acc = C::NACC == 2 ? (local & 1) : 0;
+        const uint32_t acc_phase = C::NACC == 2 ? ((local >> 1) & 1) : (local & 1);
         mbar_wait(&tempty[acc], acc_phase ^ 1, mbc);
         tc_fence_after();
         const uint32_t tmem_d = tmem_base + acc * BN;
@@ -979,8 +997,12 @@ gemm2_kernel(const __grid_constant__ PairGroup g) {
 #pragma unroll
           for (int kk = 0; kk < BK / 16; ++kk) {
             uint64_t ad = amn ? make_desc(a_base + kk * 2048, BK * 128, 1024) : make_desc(a_base + kk * 32, 16, 1024);
-            uint64_t bd = bmn ? make_desc(b_base + kk * 2048, BK * 128, 1024) : make_desc(b_base + kk * 32, 16, 1024);
-            umma_f16_pair(tmem_d, ad, bd, idesc, (kb != 0 || kk != 0) ? 1u : 0u);
+#pragma unroll
+            for (int h = 0; h < (BN == 512 ? 2 : 1); ++h) {   // BN = 512: two N = 256 MMAs sharing A
+              const uint32_t bh = b_base + h * 16384;
+              uint64_t bd = bmn ? make_desc(bh + kk * 2048, BK * 128, 1024) : make_desc(bh + kk * 32, 16, 1024);
+              umma_f16_pair(tmem_d + h * 256, ad, bd, idesc, (kb != 0 || kk != 0) ? 1u : 0u);
+            }
           }
           umma_commit_pair(&empty[stage]);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -1007,8 +1029,8 @@ gemm2_kernel(const __grid_constant__ PairGroup g) {
       const CUtensorMap* mC2 = &pr.tmC2;
       int mb, nb;
       tile_coords(t, pr.tiles_m, pr.tiles_n, mb, nb, ea.group);
-      const int acc = local & 1;
-      const uint32_t acc_phase = (local >> 1) & 1;
+      const int acc = C::NACC == 2 ? (local & 1) : 0;
+      const uint32_t acc_phase = C::NACC == 2 ? ((local >> 1) & 1) : (local & 1);
       const int row0 = mb * 2 * BM + (int)cta * BM + quad * 32;
       const int row = row0 + lane;
       const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + acc * BN;
@@ -1309,6 +1331,23 @@ static int g_group_rr = [] {
   return e && e[0] == '1' ? 1 : 0;
 }();
 void set_gemm_mode(int m) { g_gemm_mode = m; }
+// 256 x 512 pair tiles (BM_GEMM_BN512: 0 = never, 1 = every pair GEMM with N >= 512,
+// default 2 = when the K loop is long enough to amortise the epilogue the single TMEM
+// accumulator cannot overlap: K >= 8192, or K >= 4096 with a bf16 output.  Measured
+// (profiles/r02/bn512/): C2 down fwd (K 8192) +7 %, gate_up dgrad (K 16384) +10 %,
+// 8192^3 +8.5 %, C4 gate_up fwd (K 4096) +5 %; K = 2048 -2..-11 %, the fp32
+// reduce-add C2 gate_up wgrad (K 4096) -10 %)
+static int g_bn512 = [] {
+  const char* e = getenv("BM_GEMM_BN512");
+  return e ? atoi(e) : 2;
+}();
+void set_gemm_bn512(int m) { g_bn512 = m; }
+static bool use_bn512(int M, int N, int K, int c_dtype) {
+  (void)M;
+  if (N < 512 || g_bn512 == 0) return false;
+  if (g_bn512 == 1) return true;
+  return K >= 8192 || (K >= 4096 && c_dtype == BM_BF16);
+}
 
 // fills the epilogue arguments and the output map of one contraction
 static bm_status prepare_out(int M, int N, int K, void* Cp, int64_t ldc, int c_dtype, int epi, const void* R,
@@ -1344,7 +1383,7 @@ static bm_status pair_problem(int M, int N, int K, const void* A, int64_t lda, i
   pr->tmC2 = pr->tmC;
   if (a_major == 0) BM_TRY(make_map(A, K, M, lda, BM, &pr->tmA));
   else BM_TRY(make_map(A, M, K, lda, BK, &pr->tmA));
-  if (b_major == 0) BM_TRY(make_map(B, K, N, ldb, BN2 / 2, &pr->tmB));
+  if (b_major == 0) BM_TRY(make_map(B, K, N, ldb, BN2 == 512 ? 128 : BN2 / 2, &pr->tmB));
   else BM_TRY(make_map(B, N, K, ldb, BK, &pr->tmB));
   pr->a_mn = a_major != 0;
   pr->b_mn = b_major != 0;
@@ -1393,13 +1432,14 @@ bm_status gemm_bf16_tc(int M, int N, int K, const void* A, int64_t lda, int a_ma
   const int64_t pair_tiles = (int64_t)ceil_div(M, 2 * BM) * ceil_div(N, 256);
   const bool pair = mode == 2 || (mode == 0 && M >= 256 && N >= 256 && K >= 256 && pair_tiles >= num_sms() / 2);
   if (pair) {
-    const int BN2 = (N >= 256) ? 256 : 128;
+    const int BN2 = (N >= 256) ? (use_bn512(M, N, K, c_dtype) ? 512 : 256) : 128;
     PairGroup g;
     std::memset(&g, 0, sizeof(g));
     BM_TRY(pair_problem(M, N, K, A, lda, a_major, B, ldb, b_major, Cp, ldc, c_dtype, epi, R, ldr, alpha, f, BN2,
                         &g.prob[0]));
     g.nprob = 1;
     g.tiles0 = g.total_tiles = g.prob[0].tiles_m * g.prob[0].tiles_n;
+    if (BN2 == 512) return launch2_static<512>(g, g.total_tiles, st);
     if (BN2 == 256) return launch2_static<256>(g, g.total_tiles, st);
     return launch2_static<128>(g, g.total_tiles, st);
   }

@@ -110,7 +110,7 @@ using namespace bm;
     return BM_E_INVALID;                                      \
   } while (0)
 
-namespace bm { void set_gemm_mode(int m); }
+namespace bm { void set_gemm_mode(int m); void set_gemm_bn512(int m); }
 
 extern "C" {
 
@@ -119,6 +119,12 @@ const char* bm_last_error(void) { return get_error(); }
 bm_status bm_k_gemm_mode(int32_t mode) {
   BM_CHECK_ARG(mode >= 0 && mode <= 2, "mode must be 0 (auto), 1 (1-CTA) or 2 (CTA pair)");
   bm::set_gemm_mode(mode);
+  return BM_OK;
+}
+
+bm_status bm_k_gemm_bn512(int32_t mode) {
+  BM_CHECK_ARG(mode >= 0 && mode <= 2, "mode must be 0 (never), 1 (always) or 2 (auto)");
+  bm::set_gemm_bn512(mode);
   return BM_OK;
 }
 

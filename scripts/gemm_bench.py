@@ -47,6 +47,13 @@ def main():
         ("C2 head fwd", 3500, 32000, 2048, 0, 0, "store"),
         ("8192^3", 8192, 8192, 8192, 0, 0, "store"),
         ("C4 gate_up fwd", 8192, 22016, 4096, 0, 0, "store"),
+        ("C4 down fwd+res", 8192, 4096, 11008, 0, 0, "add"),
+        ("C4 down dgrad", 8192, 11008, 4096, 0, 1, "store"),
+        ("C4 gate_up wgrad", 22016, 4096, 8192, 1, 1, "accum"),
+        ("C4 gate_up dgrad", 8192, 4096, 22016, 0, 1, "store"),
+        ("C4 down wgrad", 4096, 11008, 8192, 1, 1, "accum"),
+        ("C2 head dgrad", 3500, 2048, 32000, 0, 1, "store"),
+        ("C2 head wgrad", 32000, 2048, 3500, 1, 1, "accum"),
         ("enc fc1 n=554", 554, 1536, 384, 0, 0, "store"),
     ]
     out = []
