@@ -1332,21 +1332,31 @@ static int g_group_rr = [] {
 }();
 void set_gemm_mode(int m) { g_gemm_mode = m; }
 // 256 x 512 pair tiles (BM_GEMM_BN512: 0 = never, 1 = every pair GEMM with N >= 512,
-// default 2 = when the K loop is long enough to amortise the epilogue the single TMEM
-// accumulator cannot overlap: K >= 8192, or K >= 4096 with a bf16 output.  Measured
-// (profiles/r02/bn512/): C2 down fwd (K 8192) +7 %, gate_up dgrad (K 16384) +10 %,
-// 8192^3 +8.5 %, C4 gate_up fwd (K 4096) +5 %; K = 2048 -2..-11 %, the fp32
-// reduce-add C2 gate_up wgrad (K 4096) -10 %)
+// default 2 = by a wave-quantised cost model).  A 256 x 512 tile moves a quarter less
+// L2 -> SMEM data per FLOP (its k-blocks run ~1.1x faster than two 256 x 256 ones) but
+// has one TMEM accumulator, so its epilogue (~4096 clocks; fp32 reduce-add 6144) is not
+// overlapped, and it halves the tile count (coarser last wave).  Model, per pair:
+//   t256 = ceil(T256 / pairs) * nk * 512,  t512 = ceil(T512 / pairs) * (nk * 1024 / 1.1 + E)
+// 512 when t512 < 0.98 t256.  It reproduces the measured gains within ~4 points
+// (profiles/r02/bn512/bn512_knob.log: C2 down fwd +5 %, gate_up dgrad +10.5 %, head
+// dgrad +16 %, 8192^3 +6 %; C4 down fwd -9 % and gate_up dgrad -7 % from the last
+// wave).  The SwiGLU-backward epilogue (gu loads, two outputs) loses 20-27 % with the
+// un-overlapped epilogue and always takes 256 x 256.
 static int g_bn512 = [] {
   const char* e = getenv("BM_GEMM_BN512");
   return e ? atoi(e) : 2;
 }();
 void set_gemm_bn512(int m) { g_bn512 = m; }
-static bool use_bn512(int M, int N, int K, int c_dtype) {
-  (void)M;
-  if (N < 512 || g_bn512 == 0) return false;
-  if (g_bn512 == 1) return true;
-  return K >= 8192 || (K >= 4096 && c_dtype == BM_BF16);
+static bool use_bn512(int M, int N, int K, int c_dtype, int epi) {
+  if (N < 512 || g_bn512 == 0 || epi == BM_EPI_SWIGLU) return false;
+  if (g_bn512 == 1) return true;   // forced (tests, A/B), the SwiGLU-backward epilogue included
+  if (epi == BM_EPI_DSWIGLU) return false;
+  const int64_t pairs = std::max(1, gemm_sm_budget() / 2);
+  const int64_t tm = (M + 255) / 256, nk = (K + 63) / 64;
+  const int64_t t256 = tm * ((N + 255) / 256), t512 = tm * ((N + 511) / 512);
+  const double c256 = (double)((t256 + pairs - 1) / pairs) * nk * 512.0;
+  const double c512 = (double)((t512 + pairs - 1) / pairs) * (nk * 1024.0 / 1.1 + (c_dtype == BM_F32 ? 6144.0 : 4096.0));
+  return c512 < 0.98 * c256;
 }
 
 // fills the epilogue arguments and the output map of one contraction
@@ -1432,7 +1442,7 @@ bm_status gemm_bf16_tc(int M, int N, int K, const void* A, int64_t lda, int a_ma
   const int64_t pair_tiles = (int64_t)ceil_div(M, 2 * BM) * ceil_div(N, 256);
   const bool pair = mode == 2 || (mode == 0 && M >= 256 && N >= 256 && K >= 256 && pair_tiles >= num_sms() / 2);
   if (pair) {
-    const int BN2 = (N >= 256) ? (use_bn512(M, N, K, c_dtype) ? 512 : 256) : 128;
+    const int BN2 = (N >= 256) ? (use_bn512(M, N, K, c_dtype, epi) ? 512 : 256) : 128;
     PairGroup g;
     std::memset(&g, 0, sizeof(g));
     BM_TRY(pair_problem(M, N, K, A, lda, a_major, B, ldb, b_major, Cp, ldc, c_dtype, epi, R, ldr, alpha, f, BN2,
