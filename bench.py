@@ -156,8 +156,48 @@ HEAD_LAYERS = 1.7
 DEFAULT_SPLIT = {("C2", 4): [4, 4, 5, 3]}
 
 
+def unit_partition(cfg, P):
+    """Partition of the 2L half-layer units (bigmac.h stage_halves, R24) over
+    the P V virtual stages minimising the slowest stage, then the sum of squared stage
+    costs: unit costs A_l = 2, B_l = 1 (thirds of a layer: gate_up is 2/3 of its FLOPs),
+    the last stage also runs the LM head + CE (HEAD_LAYERS layers)."""
+    PV, n = P * cfg.V, 2 * cfg.L
+    pre = [0]
+    for u in range(n):
+        pre.append(pre[-1] + (2 if u % 2 == 0 else 1))
+    head = 3 * HEAD_LAYERS
+    best = {0: (0.0, 0.0, [])}          # units covered -> (max, sum of squares, parts)
+    for s in range(PV):
+        nxt = {}
+        for u0, (mx, sq, parts) in best.items():
+            hi = n if s == PV - 1 else n - (PV - s - 1)
+            for u1 in range(u0 + 1, hi + 1):
+                if s == PV - 1 and u1 != n:
+                    continue
+                c = pre[u1] - pre[u0] + (head if s == PV - 1 else 0)
+                key = (max(mx, c), sq + c * c)
+                if u1 not in nxt or key < nxt[u1][:2]:
+                    nxt[u1] = (key[0], key[1], parts + [u1 - u0])
+        best = nxt
+    return best[n][2]
+
+
+def unit_costs(cfg, units):
+    """Per-stage cost (layer equivalents) of a half-layer-unit partition, head included."""
+    out, u = [], 0
+    for s, k in enumerate(units):
+        c = sum(2 if x % 2 == 0 else 1 for x in range(u, u + k)) / 3.0
+        out.append(c + (HEAD_LAYERS if s == len(units) - 1 else 0.0))
+        u += k
+    return out
+
+
 def stage_split(args, cfg, P):
-    """Explicit stage_layers (bigmac.h) or None."""
+    """Explicit stage_layers (bigmac.h) or None; in half-layer units with --partition halves."""
+    if getattr(args, "partition", "layers") == "halves" and P * cfg.V > 1:
+        if args.stage_layers:
+            return [int(x) for x in args.stage_layers.split(",")]
+        return unit_partition(cfg, P)
     if args.stage_layers:
         return [int(x) for x in args.stage_layers.split(",")]
     if args.last_stage_layers >= 0:
@@ -350,14 +390,21 @@ class Ctx:
         return out
 
 
-def pacing_stage_mask(split, P):
-    """Bit of the stage holding the most LLM layers when the partition is uneven and
-    that stage is unique (it paces the pipeline), else 0."""
+def pacing_stage_mask(split, P, costs=None):
+    """Bits of the stages holding the most LLM work (layers, or `costs` of a half-layer
+    partition; they pace the pipeline) when the partition is uneven, else 0."""
     if not split or len(split) != P:
         return 0
-    mx = max(split)
-    heavy = [r for r, n in enumerate(split) if n == mx]
-    return (1 << heavy[0]) if len(heavy) == 1 else 0
+    w = costs if costs is not None else split
+    mx = max(w)
+    if min(w) >= mx - 1e-9:
+        return 0
+    return sum(1 << r for r, n in enumerate(w) if n >= mx - 1e-9)
+
+
+def _pacing(args, cfg, P, split):
+    halves = getattr(args, "partition", "layers") == "halves"
+    return pacing_stage_mask(split, P, unit_costs(cfg, split) if (halves and split) else None)
 
 
 def gen_exclude(args, cfg, P, split, strategy):
@@ -367,7 +414,7 @@ def gen_exclude(args, cfg, P, split, strategy):
         return 0
     if args.gen_exclude != "auto":
         return sum(1 << int(r) for r in args.gen_exclude.split(","))
-    return pacing_stage_mask(split, P)
+    return _pacing(args, cfg, P, split)
 
 
 def enc_exclude(args, cfg, P, split, strategy):
@@ -377,7 +424,7 @@ def enc_exclude(args, cfg, P, split, strategy):
         return 0
     if args.enc_exclude != "auto":
         return sum(1 << int(r) for r in args.enc_exclude.split(","))
-    return pacing_stage_mask(split, P)
+    return _pacing(args, cfg, P, split)
 
 
 def make_runtime(args, cfg, P, rank, world, group, strategy="bigmac"):
@@ -393,7 +440,8 @@ def make_runtime(args, cfg, P, rank, world, group, strategy="bigmac"):
         sched_kw = dict(sched_kw, enc_exclude=ex)
     rt = Runtime(cfg, args.dtype, rank=rank, world=world, group=group, sched_kw=sched_kw, head_place=args.head,
                  last_stage_layers=n_last, stage_layers=split, fsdp=args.fsdp,
-                 gen_exclude=gen_exclude(args, cfg, P, split, strategy))
+                 gen_exclude=gen_exclude(args, cfg, P, split, strategy),
+                 stage_halves=bool(split) and getattr(args, "partition", "layers") == "halves")
     rt.init_random_weights(seed=1)
     return rt, W, split, n_last
 
@@ -534,6 +582,9 @@ def main():
                          "or FSDP with the all-gather baseline (bigmac.h bm_fsdp_mode, P:401-426)")
     ap.add_argument("--gen-exclude", default="auto", help="ranks that take no generator rows: auto | none | r,r")
     ap.add_argument("--enc-exclude", default="auto", help="ranks that run no encoder microbatch: auto | none | r,r")
+    ap.add_argument("--partition", default="layers", choices=["layers", "halves"],
+                    help="LLM stage partition: whole layers (DEFAULT_SPLIT / last_stage_layers) or half-layer units "
+                         "(stage boundaries inside layers, bigmac.h stage_halves)")
     ap.add_argument("--llm-sched", default="auto", choices=["auto", "zb_h1"],
                     help="LLM base schedule: auto = 1F1B (V = 1) / interleaved (V > 1); zb_h1 = ZB-H1 zero-bubble")
     ap.add_argument("--strategy", default="bigmac", choices=["bigmac", "compute_efficient", "memory_efficient"],

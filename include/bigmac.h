@@ -161,7 +161,8 @@ typedef struct {
   int32_t last_stage_layers;      /* LLM layers of the last virtual stage; 0 = uniform (below) */
   int32_t fsdp;                   /* bm_fsdp_mode of the encoder / generator parameters */
   int32_t gen_exclude;            /* bit mask of ranks that take no generator rows (below) */
-  int32_t reserved[4];            /* must be zero                              */
+  int32_t stage_halves;           /* 1: stage_layers counts half-layer units (below) */
+  int32_t reserved[3];            /* must be zero                              */
   int32_t stage_layers[BM_MAX_VSTAGES]; /* explicit partition (below); all 0 = unset */
 } bm_model_cfg;
 
@@ -174,7 +175,15 @@ typedef struct {
  * P V - 1 stages split the remaining L - n as evenly as possible, the first
  * (L - n) mod (P V - 1) stages one layer more.  Requires 1 <= n and
  * L - n >= P V - 1 (every stage holds a layer).  Uneven splits balance the
- * head's cost; op lists do not depend on the partition. */
+ * head's cost; op lists do not depend on the partition.
+ * stage_halves = 1 (with stage_layers set): each layer l is two units, A_l =
+ * RMSNorm + gate_up GEMM + SwiGLU and B_l = down GEMM + residual (2/3 and 1/3 of
+ * its FLOPs), and stage_layers[s] counts units (every entry >= 1, sum = 2 L), so a
+ * stage boundary may fall inside a layer: the stage-boundary message is then
+ * [x_l | h_l] (S x (d + f)) forward and [dx_{l+1} | dh_l] backward, and layer l's
+ * norm / gate_up live on the earlier stage, its down on the later one (DESIGN.md
+ * reading R24).  The first virtual stage cannot start and the last cannot end
+ * inside a layer. */
 
 /* gen_exclude (BM_GEN_DP_SHARD): rank r with bit r set takes no generator rows;
  * microbatch m's n_gen rows are split into equal shards over the other ranks in

@@ -129,15 +129,17 @@ static bm_status check_model(const bm_model_cfg& mc, const bm_sched_cfg& sc) {
   BM_CHECK_ARG(mc.d_g > 0 && mc.f_g > 0 && mc.L_g >= 0 && mc.d_t > 0, "bad generator dims");
   BM_CHECK_ARG(mc.dtype == BM_BF16 || mc.dtype == BM_F32, "dtype must be bf16 or fp32");
   const int PV = sc.stages * sc.vchunks;
+  BM_CHECK_ARG(mc.stage_halves == 0 || (mc.stage_halves == 1 && mc.stage_layers[0] != 0),
+               "stage_halves = 1 needs an explicit stage_layers partition (in half-layer units)");
   if (mc.stage_layers[0] != 0) {
     BM_CHECK_ARG(PV <= BM_MAX_VSTAGES, "explicit stage_layers needs P*V <= BM_MAX_VSTAGES");
     int sum = 0;
     for (int s = 0; s < PV; ++s) {
-      BM_CHECK_ARG(mc.stage_layers[s] >= 1, "stage_layers: every virtual stage needs >= 1 layer");
+      BM_CHECK_ARG(mc.stage_layers[s] >= 1, "stage_layers: every virtual stage needs >= 1 layer (unit)");
       sum += mc.stage_layers[s];
     }
     for (int s = PV; s < BM_MAX_VSTAGES; ++s) BM_CHECK_ARG(mc.stage_layers[s] == 0, "stage_layers beyond P*V must be 0");
-    BM_CHECK_ARG(sum == mc.L, "stage_layers must sum to L");
+    BM_CHECK_ARG(sum == (mc.stage_halves ? 2 * mc.L : mc.L), "stage_layers must sum to L (2 L half-layer units)");
   } else if (mc.last_stage_layers == 0)
     BM_CHECK_ARG(mc.L % (sc.stages * sc.vchunks) == 0, "L must be a multiple of P*V (or set last_stage_layers)");
   else
@@ -187,14 +189,34 @@ static void stage_layers(const bm_model_cfg& mc, int PV, int s, int* l0, int* n)
   *n = q + (s < r ? 1 : 0);
   *l0 = s * q + std::min(s, r);
 }
+// The LLM span of virtual stage s: layers [l0, l0 + nl).  With stage_halves
+// (bigmac.h; R24) the first layer may hold only its B half (down +
+// residual: b_first) and the last only its A half (norm + gate_up + SwiGLU: a_last).
+struct Span {
+  int l0 = 0, nl = 0;
+  bool b_first = false, a_last = false;
+  bool has_a(int j) const { return !(b_first && j == 0); }
+  bool has_b(int j) const { return !(a_last && j == nl - 1); }
+};
+static Span stage_span(const bm_model_cfg& mc, int PV, int s) {
+  Span sp;
+  if (mc.stage_halves) {
+    int u0 = 0;
+    for (int i = 0; i < s; ++i) u0 += mc.stage_layers[i];
+    const int u1 = u0 + mc.stage_layers[s];
+    sp.l0 = u0 / 2;
+    sp.nl = (u1 + 1) / 2 - sp.l0;
+    sp.b_first = (u0 & 1) != 0;
+    sp.a_last = (u1 & 1) != 0;
+    return sp;
+  }
+  stage_layers(mc, PV, s, &sp.l0, &sp.nl);
+  return sp;
+}
 // most layers of one virtual stage held by `rank` (stash slot depth)
 static int max_stage_layers(const bm_model_cfg& mc, int P, int V, int rank) {
   int mx = 0;
-  for (int c = 0; c < V; ++c) {
-    int l0, n;
-    stage_layers(mc, P * V, c * P + rank, &l0, &n);
-    mx = std::max(mx, n);
-  }
+  for (int c = 0; c < V; ++c) mx = std::max(mx, stage_span(mc, P * V, c * P + rank).nl);
   return mx;
 }
 
@@ -236,13 +258,14 @@ static std::vector<PEntry> param_layout(const bm_model_cfg& mc, const bm_sched_c
   const int P = sc.stages, V = sc.vchunks;
   if (rank == 0) add("llm.embed", mc.vocab, mc.d, BM_PARAM_LLM);
   for (int c = 0; c < V; ++c) {
-    int l0, nl;
-    stage_layers(mc, P * V, c * P + rank, &l0, &nl);
-    for (int l = l0; l < l0 + nl; ++l) {
-      const std::string p = "llm.layer" + std::to_string(l);
-      add(p + ".norm", mc.d, 1, BM_PARAM_LLM);
-      add(p + ".gate_up", 2 * mc.f, mc.d, BM_PARAM_LLM);
-      add(p + ".down", mc.d, mc.f, BM_PARAM_LLM);
+    const Span sp = stage_span(mc, P * V, c * P + rank);
+    for (int j = 0; j < sp.nl; ++j) {
+      const std::string p = "llm.layer" + std::to_string(sp.l0 + j);
+      if (sp.has_a(j)) {
+        add(p + ".norm", mc.d, 1, BM_PARAM_LLM);
+        add(p + ".gate_up", 2 * mc.f, mc.d, BM_PARAM_LLM);
+      }
+      if (sp.has_b(j)) add(p + ".down", mc.d, mc.f, BM_PARAM_LLM);
     }
   }
   if (rank == P - 1) {
@@ -288,6 +311,7 @@ struct LlmSlot {
   char *gin = nullptr, *Hn = nullptr, *dHn = nullptr;
   float* rstd_f = nullptr;
   int nl = 0;   // layers of the virtual stage the slot currently stashes
+  Span sp;      // ... and its span (half layers at the ends, stage_halves)
 };
 struct MlpSlot {  // encoder (L_e blocks) or generator (L_g blocks)
   std::vector<char*> E, xn, a, z;
@@ -469,6 +493,7 @@ struct bm_ctx {
   // BM_FUSE_SWIGLU=0 selects GEMM + the vectorised elementwise kernel
   bool fuse_swiglu = !(getenv("BM_FUSE_SWIGLU") && getenv("BM_FUSE_SWIGLU")[0] == '0');
   bool zb = false;         // BM_LLM_ZB_H1: LLM_BWD = input gradient, LLM_W = weight gradients
+  int64_t mid_cols = 0;    // f if some stage boundary falls inside a layer (stage_halves), else 0
   bool peer_copy_ce = !(getenv("BM_PEER_COPY") && std::string(getenv("BM_PEER_COPY")) == "sm");
   int peer_copy_ctas = getenv("BM_PEER_COPY_CTAS") ? std::atoi(getenv("BM_PEER_COPY_CTAS")) : 32;
   bool spin_wait = getenv("BM_WAIT") && std::string(getenv("BM_WAIT")) == "spin";
@@ -563,6 +588,13 @@ static int64_t payload_rows_max(const bm_ctx& c, int pay) {
   }
 }
 
+// stage-boundary message after virtual stage b: x (S x d), or [x_l | h_l] / [dx | dh]
+// (S x (d + f)) when the boundary falls inside layer l (stage_halves, R24)
+static int64_t boundary_bytes(const bm_ctx& c, int b) {
+  const bool mid = stage_span(c.mc, c.P * c.V, b).a_last;
+  return (int64_t)c.mc.S * (c.mc.d + (mid ? c.mc.f : 0)) * c.es;
+}
+
 static void comm_layout(bm_ctx& c) {
   c.comm_size.assign(c.P, 0);
   std::vector<int64_t> flag_cur(c.P, 0);
@@ -573,7 +605,8 @@ static void comm_layout(bm_ctx& c) {
     ch.pay = std::get<2>(kv.first);
     ch.K = kv.second.first;
     ch.nmsg = kv.second.second;
-    ch.slot_bytes = align_up(payload_rows_max(c, ch.pay) * c.mc.d * (int64_t)c.es, 256);
+    const int64_t width = (ch.pay == BM_PAY_ACT || ch.pay == BM_PAY_GRAD) ? c.mc.d + c.mid_cols : c.mc.d;
+    ch.slot_bytes = align_up(payload_rows_max(c, ch.pay) * width * (int64_t)c.es, 256);
     ch.flag_off = flag_cur[ch.dst];
     flag_cur[ch.dst] += 64;
     ch.credit_off = flag_cur[ch.src];
@@ -616,14 +649,16 @@ static void work_layout(bm_ctx& c, char* base) {
   c.llm.assign(c.n_llm_slots, LlmSlot());
   for (auto& sl : c.llm) {
     sl.x.resize(c.lps + 1); sl.xn.resize(c.lps); sl.gu.resize(c.lps); sl.h.resize(c.lps); sl.rstd.resize(c.lps);
-    for (int j = 0; j <= c.lps; ++j) sl.x[j] = b.take(S * d * es);
     for (int j = 0; j < c.lps; ++j) {
+      // x_j and h_j back to back: [x_l | h_l] is the message of a boundary inside layer l
+      sl.x[j] = b.take(S * (d + f) * es);
+      sl.h[j] = sl.x[j] + S * d * es;
       sl.xn[j] = b.take(S * d * es);
       sl.rstd[j] = (float*)b.take(S * 4);
       sl.gu[j] = b.take(S * 2 * f * es);
-      sl.h[j] = b.take(S * f * es);
     }
-    sl.gin = b.take(S * d * es);
+    sl.x[c.lps] = b.take(S * d * es);
+    sl.gin = b.take(S * (d + c.mid_cols) * es);
     if (c.zb) {   // the weight-gradient operands B leaves for W
       sl.wdy.resize(c.lps); sl.wdgu.resize(c.lps);
       for (int j = 0; j < c.lps; ++j) {
@@ -660,7 +695,7 @@ static void work_layout(bm_ctx& c, char* base) {
   if (c.has_gen && c.gen_rows > 0) mlp_slot(c.gen, c.gen_rows, m.d_g, m.f_g, m.L_g, 0, false, m.d_t);
   // LLM scratch
   for (int i = 0; i < 2; ++i) c.dwork[i] = b.take(S * d * es);
-  for (int i = 0; i < 2; ++i) c.bout[i] = b.take(S * d * es);
+  for (int i = 0; i < 2; ++i) c.bout[i] = b.take(S * (d + c.mid_cols) * es);
   c.dh = b.take(S * f * es);
   c.dgu = b.take(S * 2 * f * es);
   c.dxn = b.take(S * d * es);
@@ -1185,25 +1220,31 @@ static bm_status op_llm_fwd(bm_ctx& c, const bm_op& o, const RecvState& rs) {
     BM_TRY(TY(c, embed_fwd<bf16>(m.S, m.d, n_mod, c.ids + (int64_t)mb * S, (const bf16*)P_(c, "llm.embed"), (const bf16*)emb, (bf16*)sl.x[0], c.st),
               embed_fwd<float>(m.S, m.d, n_mod, c.ids + (int64_t)mb * S, (const float*)P_(c, "llm.embed"), (const float*)emb, (float*)sl.x[0], c.st)));
   } else if ((s - 1) % c.P == c.rank) {
-    const int prev = c.llm_live.at({mb, ch - 1});
-    BM_TRY(d2d(c, sl.x[0], c.llm[prev].x[c.llm[prev].nl], S * d * es));
+    // a boundary inside layer l brings [x_l | h_l] into x[0] (h[0] follows x[0])
+    const LlmSlot& pv = c.llm[c.llm_live.at({mb, ch - 1})];
+    BM_TRY(d2d(c, sl.x[0], pv.sp.a_last ? pv.x[pv.nl - 1] : pv.x[pv.nl], boundary_bytes(c, s - 1)));
   } else {
-    BM_TRY(d2d(c, sl.x[0], recv_slot(c, (s - 1) % c.P, BM_PAY_ACT, rs.ops.at(0)->seq), S * d * es));
+    BM_TRY(d2d(c, sl.x[0], recv_slot(c, (s - 1) % c.P, BM_PAY_ACT, rs.ops.at(0)->seq), boundary_bytes(c, s - 1)));
   }
-  int l0, nl;
-  stage_layers(m, c.P * c.V, s, &l0, &nl);
+  const Span sp = stage_span(m, c.P * c.V, s);
+  const int nl = sp.nl;
   sl.nl = nl;
+  sl.sp = sp;
   char nm[64];
   for (int j = 0; j < nl; ++j) {
-    const int l = l0 + j;
-    snprintf(nm, sizeof nm, "llm.layer%d.norm", l);
-    BM_TRY(norm_fwd(c, m.S, m.d, sl.x[j], P_(c, nm), sl.xn[j], sl.rstd[j]));
-    snprintf(nm, sizeof nm, "llm.layer%d.gate_up", l);
-    BM_TRY(lin_gate_up(c, sl.xn[j], P_(c, nm), LD_(c, nm), sl.gu[j], sl.h[j]));
-    snprintf(nm, sizeof nm, "llm.layer%d.down", l);
-    BM_TRY(lin_fwd(c, m.S, m.f, m.d, sl.h[j], m.f, P_(c, nm), LD_(c, nm), sl.x[j + 1], BM_EPI_ADD, sl.x[j]));
+    const int l = sp.l0 + j;
+    if (sp.has_a(j)) {   // A_l: RMSNorm -> gate_up GEMM with SwiGLU
+      snprintf(nm, sizeof nm, "llm.layer%d.norm", l);
+      BM_TRY(norm_fwd(c, m.S, m.d, sl.x[j], P_(c, nm), sl.xn[j], sl.rstd[j]));
+      snprintf(nm, sizeof nm, "llm.layer%d.gate_up", l);
+      BM_TRY(lin_gate_up(c, sl.xn[j], P_(c, nm), LD_(c, nm), sl.gu[j], sl.h[j]));
+    }
+    if (sp.has_b(j)) {   // B_l: down GEMM + residual
+      snprintf(nm, sizeof nm, "llm.layer%d.down", l);
+      BM_TRY(lin_fwd(c, m.S, m.f, m.d, sl.h[j], m.f, P_(c, nm), LD_(c, nm), sl.x[j + 1], BM_EPI_ADD, sl.x[j]));
+    }
   }
-  c.last_src = sl.x[nl];
+  c.last_src = sp.a_last ? sl.x[nl - 1] : sl.x[nl];   // [x_l | h_l] when the stage ends inside layer l
   c.last_src_ring = -1;
   if (s == c.P * c.V - 1) {
     // last stage: final norm, LM head + CE (fwd and bwd through the head), generator inputs
@@ -1300,42 +1341,72 @@ static bm_status op_llm_bwd(bm_ctx& c, const bm_op& o, const RecvState& rs) {
     c.bout_pending[b] = false;
   }
   char nm[64];
-  int l0, nl;
-  stage_layers(m, c.P * c.V, s, &l0, &nl);
+  const Span sp = sl.sp;
+  const int l0 = sp.l0, nl = sp.nl;
+  // a stage ending inside layer l receives [dx_{l+1} | dh_l] (cur, cur + S d): only A_l's
+  // backward runs here; one starting inside layer l sends [dx_{l+1} | dh_l] (R24)
+  auto swiglu_bwd_of = [&](const char* dh, const char* gu, char* dgu) -> bm_status {
+    return TY(c, swiglu_bwd<bf16>(m.S, m.f, (const bf16*)dh, (const bf16*)gu, (bf16*)dgu, c.st),
+              swiglu_bwd<float>(m.S, m.f, (const float*)dh, (const float*)gu, (float*)dgu, c.st));
+  };
   if (c.zb) {
     // ZB-H1 B: input gradient only; every layer's dY and dgu stay in the slot for W (R23)
-    if (nl > 0 && cur != sl.wdy[nl - 1]) BM_TRY(d2d(c, sl.wdy[nl - 1], cur, S * d * es));
+    if (nl > 0 && sp.has_b(nl - 1) && cur != sl.wdy[nl - 1]) BM_TRY(d2d(c, sl.wdy[nl - 1], cur, S * d * es));
     for (int j = nl - 1; j >= 0; --j) {
       const int l = l0 + j;
       char* out = (j == 0) ? c.bout[b] : sl.wdy[j - 1];
-      snprintf(nm, sizeof nm, "llm.layer%d.down", l);
-      BM_TRY(lin_down_dgrad_swiglu(c, sl.wdy[j], P_(c, nm), LD_(c, nm), sl.gu[j], c.dh, sl.wdgu[j]));
+      if (!sp.has_a(j)) {   // B_l only (j = 0): send [dx_{l+1} | dh_l]
+        snprintf(nm, sizeof nm, "llm.layer%d.down", l);
+        BM_TRY(lin_dgrad(c, m.S, m.f, m.d, sl.wdy[j], P_(c, nm), LD_(c, nm), out + S * d * es, m.f));
+        BM_TRY(d2d(c, out, sl.wdy[j], S * d * es));
+        continue;
+      }
+      const char* resid = sl.wdy[j];
+      if (!sp.has_b(j)) {   // A_l only (j = nl - 1): dgu from the received dh
+        BM_TRY(swiglu_bwd_of(cur + S * d * es, sl.gu[j], sl.wdgu[j]));
+        resid = cur;
+      } else {
+        snprintf(nm, sizeof nm, "llm.layer%d.down", l);
+        BM_TRY(lin_down_dgrad_swiglu(c, sl.wdy[j], P_(c, nm), LD_(c, nm), sl.gu[j], c.dh, sl.wdgu[j]));
+      }
       snprintf(nm, sizeof nm, "llm.layer%d.gate_up", l);
       BM_TRY(lin_dgrad(c, m.S, m.d, 2 * m.f, sl.wdgu[j], P_(c, nm), LD_(c, nm), c.dxn, m.d));
       snprintf(nm, sizeof nm, "llm.layer%d.norm", l);
-      BM_TRY(norm_bwd(c, m.S, m.d, c.dxn, sl.x[j], P_(c, nm), sl.rstd[j], sl.wdy[j], out, G_(c, nm)));
+      BM_TRY(norm_bwd(c, m.S, m.d, c.dxn, sl.x[j], P_(c, nm), sl.rstd[j], resid, out, G_(c, nm)));
     }
   }
   for (int j = c.zb ? -1 : nl - 1; j >= 0; --j) {
     const int l = l0 + j;
     char* out = (j == 0) ? c.bout[b] : (cur == c.dwork[0] ? c.dwork[1] : c.dwork[0]);
-    snprintf(nm, sizeof nm, "llm.layer%d.down", l);
-    if (c.fuse_swiglu && c.dtype == BM_BF16 && m.f % 32 == 0) {
-      // down wgrad + down dgrad with the SwiGLU backward in its epilogue: one grouped launch
-      GemmSpec sp[2] = {spec_wgrad(m.S, m.f, m.d, cur, sl.h[j], m.f, G_(c, nm), LD_(c, nm)),
-                        GemmSpec{(int)m.S, m.f, m.d, cur, m.d, 0, P_(c, nm), LD_(c, nm), 1, c.dgu, 2 * (int64_t)m.f,
-                                 BM_BF16, BM_EPI_DSWIGLU, sl.gu[j], 2 * (int64_t)m.f, 1.f, m.f, nullptr, 0}};
-      BM_TRY(timed_group(c, sp, 2));
-    } else {
+    if (!sp.has_a(j)) {   // B_l only (j = 0): down wgrad, dh = dY W_down, send [dY | dh]
+      snprintf(nm, sizeof nm, "llm.layer%d.down", l);
       BM_TRY(lin_wgrad(c, m.S, m.f, m.d, cur, sl.h[j], m.f, G_(c, nm), LD_(c, nm)));
-      BM_TRY(lin_down_dgrad_swiglu(c, cur, P_(c, nm), LD_(c, nm), sl.gu[j], c.dh, c.dgu));
+      BM_TRY(lin_dgrad(c, m.S, m.f, m.d, cur, P_(c, nm), LD_(c, nm), out + S * d * es, m.f));
+      BM_TRY(d2d(c, out, cur, S * d * es));
+      cur = out;
+      continue;
+    }
+    if (!sp.has_b(j)) {   // A_l only (j = nl - 1): dgu = SwiGLU backward of the received dh
+      BM_TRY(swiglu_bwd_of(cur + S * d * es, sl.gu[j], c.dgu));
+    } else {
+      snprintf(nm, sizeof nm, "llm.layer%d.down", l);
+      if (c.fuse_swiglu && c.dtype == BM_BF16 && m.f % 32 == 0) {
+        // down wgrad + down dgrad with the SwiGLU backward in its epilogue: one grouped launch
+        GemmSpec gs[2] = {spec_wgrad(m.S, m.f, m.d, cur, sl.h[j], m.f, G_(c, nm), LD_(c, nm)),
+                          GemmSpec{(int)m.S, m.f, m.d, cur, m.d, 0, P_(c, nm), LD_(c, nm), 1, c.dgu, 2 * (int64_t)m.f,
+                                   BM_BF16, BM_EPI_DSWIGLU, sl.gu[j], 2 * (int64_t)m.f, 1.f, m.f, nullptr, 0}};
+        BM_TRY(timed_group(c, gs, 2));
+      } else {
+        BM_TRY(lin_wgrad(c, m.S, m.f, m.d, cur, sl.h[j], m.f, G_(c, nm), LD_(c, nm)));
+        BM_TRY(lin_down_dgrad_swiglu(c, cur, P_(c, nm), LD_(c, nm), sl.gu[j], c.dh, c.dgu));
+      }
     }
     snprintf(nm, sizeof nm, "llm.layer%d.gate_up", l);
     {
       // gate_up dgrad + gate_up wgrad: one grouped launch
-      GemmSpec sp[2] = {spec_dgrad(c, m.S, m.d, 2 * m.f, c.dgu, P_(c, nm), LD_(c, nm), c.dxn, m.d),
+      GemmSpec gs[2] = {spec_dgrad(c, m.S, m.d, 2 * m.f, c.dgu, P_(c, nm), LD_(c, nm), c.dxn, m.d),
                         spec_wgrad(m.S, m.d, 2 * m.f, c.dgu, sl.xn[j], m.d, G_(c, nm), LD_(c, nm))};
-      BM_TRY(timed_group(c, sp, 2));
+      BM_TRY(timed_group(c, gs, 2));
     }
     snprintf(nm, sizeof nm, "llm.layer%d.norm", l);
     BM_TRY(norm_bwd(c, m.S, m.d, c.dxn, sl.x[j], P_(c, nm), sl.rstd[j], cur, out, G_(c, nm)));
@@ -1357,7 +1428,7 @@ static bm_status op_llm_bwd(bm_ctx& c, const bm_op& o, const RecvState& rs) {
       if (c.use_enc_stream) BM_CUDA_TRY(cudaEventRecord(c.emb_ready_ev, c.st));
     }
   } else if ((s - 1) % c.P == c.rank) {
-    BM_TRY(d2d(c, c.llm[c.llm_live.at({mb, ch - 1})].gin, c.bout[b], S * d * es));
+    BM_TRY(d2d(c, c.llm[c.llm_live.at({mb, ch - 1})].gin, c.bout[b], boundary_bytes(c, s - 1)));
   }
   if (!c.zb) {   // under ZB-H1 the stash lives until W
     c.llm_live.erase({mb, ch});
@@ -1372,15 +1443,16 @@ static bm_status op_llm_w(bm_ctx& c, const bm_op& o) {
   const auto& m = c.mc;
   const int slot = c.llm_live.at({o.mb, o.chunk});
   LlmSlot& sl = c.llm[slot];
-  int l0, nl;
-  stage_layers(m, c.P * c.V, o.chunk * c.P + c.rank, &l0, &nl);
+  const Span sp = sl.sp;
   char nd[64], ng[64];
-  for (int j = nl - 1; j >= 0; --j) {
-    snprintf(nd, sizeof nd, "llm.layer%d.down", l0 + j);
-    snprintf(ng, sizeof ng, "llm.layer%d.gate_up", l0 + j);
-    GemmSpec sp[2] = {spec_wgrad(m.S, m.f, m.d, sl.wdy[j], sl.h[j], m.f, G_(c, nd), LD_(c, nd)),
-                      spec_wgrad(m.S, m.d, 2 * m.f, sl.wdgu[j], sl.xn[j], m.d, G_(c, ng), LD_(c, ng))};
-    BM_TRY(timed_group(c, sp, 2));
+  for (int j = sp.nl - 1; j >= 0; --j) {
+    snprintf(nd, sizeof nd, "llm.layer%d.down", sp.l0 + j);
+    snprintf(ng, sizeof ng, "llm.layer%d.gate_up", sp.l0 + j);
+    GemmSpec gs[2];
+    int n = 0;
+    if (sp.has_b(j)) gs[n++] = spec_wgrad(m.S, m.f, m.d, sl.wdy[j], sl.h[j], m.f, G_(c, nd), LD_(c, nd));
+    if (sp.has_a(j)) gs[n++] = spec_wgrad(m.S, m.d, 2 * m.f, sl.wdgu[j], sl.xn[j], m.d, G_(c, ng), LD_(c, ng));
+    BM_TRY(timed_group(c, gs, n));
   }
   c.llm_live.erase({o.mb, o.chunk});
   c.llm_free.push_back(slot);
@@ -1473,11 +1545,12 @@ static bm_status op_gen_bwd(bm_ctx& c, const bm_op& o, const char* X) {
 }
 
 // ------------------------------------------------------------------ comm ops
+// bytes of a message this rank sends (src_rank_for_shard: the shard's rank for genin / gengrad)
 static int64_t payload_bytes(const bm_ctx& c, const bm_op& o, int src_rank_for_shard) {
   const int64_t row = (int64_t)c.mc.d * c.es;
   switch (o.payload) {
-    case BM_PAY_ACT:
-    case BM_PAY_GRAD: return c.mc.S * row;
+    case BM_PAY_ACT: return boundary_bytes(c, o.chunk * c.P + c.rank);
+    case BM_PAY_GRAD: return boundary_bytes(c, o.chunk * c.P + c.rank - 1);
     case BM_PAY_EMB:
     case BM_PAY_EMBGRAD: return c.n_mod[o.mb] * row;
     default: {   // genin / gengrad: [head rows | generator rows] of the shard's rank
@@ -1720,6 +1793,8 @@ bm_status bm_ctx_create(const bm_model_cfg* mc, const bm_schedule* s, int32_t ra
   }
   const bm_sched_stats& st = s->stats[rank];
   c->zb = s->cfg.llm_sched == BM_LLM_ZB_H1;
+  for (int b = 0; b + 1 < c->P * c->V; ++b)
+    if (stage_span(*mc, c->P * c->V, b).a_last) c->mid_cols = mc->f;
   c->n_llm_slots = std::max(st.peak_llm_inflight, 1);   // F..B (F..W under ZB-H1)
   c->n_enc_slots = std::max(st.peak_enc_units, 1);
   {

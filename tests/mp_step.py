@@ -16,7 +16,8 @@ SPEC: "<gen_place>", "entry_stage+<gen_place>" (memory-efficient baseline), "ce"
 (degenerate row counts, synth.edge_counts), "+fsdp" / "+fsdpag" (FSDP with the
 one-sided pull / the all-gather baseline), "+genx<mask>" (ranks in the bit mask take
 no generator rows), "+encx<mask>" (ranks in the mask run no encoder microbatch),
-"+zb" (ZB-H1 zero-bubble LLM schedule, B/W split, reading R23).
+"+zb" (ZB-H1 zero-bubble LLM schedule, B/W split, reading R23), "+halves<a>-<b>-..."
+(explicit partition in half-layer units, stage boundaries inside layers, reading R24).
 FLAGS: peer = force the library's peer-memory step-end sum (BM_STEP_SUM=peer);
 gm2 = every bf16 contraction on the CTA-pair GEMM (bm_k_gemm_mode 2).
 """
@@ -48,10 +49,13 @@ def parse_spec(spec, M, P):
     encx = sum(int(t[4:]) for t in toks if t.startswith("encx"))
     zb = "zb" in toks
     toks = [t for t in toks if t not in ("edge", "fsdp", "fsdpag", "zb") and not t.startswith(("genx", "encx"))]
+    halves = False
     for t in toks:
         if t.startswith("split"):
             split = [int(x) for x in t[5:].split("-")]
-    toks = [t for t in toks if not t.startswith("split")]
+        if t.startswith("halves"):   # explicit partition in half-layer units (stage_halves, R24)
+            split, halves = [int(x) for x in t[6:].split("-")], True
+    toks = [t for t in toks if not t.startswith(("split", "halves"))]
     if "head_dp" in toks:
         head = "dp_shard"
     for t in toks:
@@ -68,7 +72,7 @@ def parse_spec(spec, M, P):
         kw["enc_exclude"] = encx
     if zb:
         kw["llm_sched"] = "zb_h1"
-    return kw, head, last, split, edge, fsdp, genx
+    return kw, head, last, split, edge, fsdp, genx, halves
 
 
 def run_case(case, rank, world):
@@ -78,7 +82,7 @@ def run_case(case, rank, world):
     name, P, M, V, dtype, spec, D = parts[0], int(parts[1]), int(parts[2]), int(parts[3]), parts[4], parts[5], int(parts[6])
     flags = parts[7].split(",") if len(parts) > 7 and parts[7] else []
     assert world == P * D, (case, world)
-    kw, head, last, split, edge, fsdp, genx = parse_spec(spec, M, P)
+    kw, head, last, split, edge, fsdp, genx, halves = parse_spec(spec, M, P)
     cfg = get_config(name, P=P, M=M, V=V)
     cfg_global = get_config(name, P=P, M=M * D, V=V)
     if edge:   # degenerate row counts, buffers sized for [0, S]
@@ -92,7 +96,7 @@ def run_case(case, rank, world):
     os.environ["BM_STEP_SUM"] = "peer" if "peer" in flags else "auto"
     L.call("bm_k_gemm_mode", 2 if "gm2" in flags else 0)
     rt = Runtime(cfg, dtype, rank=rank, world=world, sched_kw=kw, head_place=head, last_stage_layers=last,
-                 stage_layers=split, fsdp=fsdp, gen_exclude=genx)
+                 stage_layers=split, fsdp=fsdp, gen_exclude=genx, stage_halves=halves)
     rt.load_weights(W)
     db = rt.device_batch(B)
     for _ in range(2):

@@ -99,3 +99,26 @@ def test_zb_h1_workload_and_bubble_bound():
     assert "ZB-H1" in bench.config_dict(cfg, P, D)["workload"]
     with pytest.raises(SystemExit):
         bench.workload(ns(config="C3", llm_sched="zb_h1"), 4)
+
+
+def test_half_layer_unit_partition():
+    """--partition halves (bigmac.h stage_halves, R24): 2L units split over P V stages,
+    the slowest stage (A = 2/3, B = 1/3 layer, head on the last) minimised."""
+    from synth import get_config
+    cfg = get_config("C2", P=4, M=64)
+    u = bench.unit_partition(cfg, 4)
+    assert sum(u) == 2 * cfg.L and min(u) >= 1
+    costs = bench.unit_costs(cfg, u)
+    assert max(costs) < 5.0 - 1e-9                 # beats the best whole-layer split (4, 4, 5, 3)
+    assert max(costs) == pytest.approx(14 / 3)
+    # brute force over every 4-way split of the 32 units
+    import itertools
+    best = min(max(bench.unit_costs(cfg, [a, b - a, c - b, 32 - c]))
+               for a, b, c in itertools.combinations(range(1, 32), 3))
+    assert max(costs) == pytest.approx(best)
+    assert bench.pacing_stage_mask(u, 4, costs) == 0b0101
+    assert bench.pacing_stage_mask([4, 4, 5, 3], 4) == 0b0100
+    assert bench.pacing_stage_mask([4, 4, 4, 4], 4) == 0
+    a = ns(partition="halves", llm_sched="auto")
+    assert bench.stage_split(a, cfg, 4) == u
+    assert bench.stage_split(a, cfg.replace(P=1), 1) is None or cfg.V > 1

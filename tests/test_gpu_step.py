@@ -319,6 +319,11 @@ MR_CASES = [
     ("C1", 4, 8, 1, "f32", "dp_shard+zb", 1, ""), ("C1", 4, 16, 1, "bf16", "dp_shard+zb", 1, ""),
     ("C1", 4, 8, 1, "f32", "last_stage+zb+edge", 1, ""), ("C1M", 4, 8, 1, "bf16", "dp_shard+zb+fsdp", 1, "gm2"),
     ("C1", 2, 4, 1, "f32", "dp_shard+zb", 2, ""),
+    # stage boundaries inside layers (half-layer units, R24): [x | h] / [dx | dh] messages
+    ("C1", 2, 4, 1, "f32", "dp_shard+halves3-5", 1, ""), ("C1", 2, 4, 1, "bf16", "dp_shard+halves5-3", 1, ""),
+    ("C1M", 2, 4, 1, "bf16", "dp_shard+halves3-5", 1, "gm2"), ("C1", 2, 4, 1, "f32", "dp_shard+halves3-5+zb", 1, ""),
+    ("C1", 2, 8, 2, "f32", "dp_shard+halves1-3-2-2", 1, ""), ("C1", 4, 8, 1, "f32", "dp_shard+halves3-2-2-1", 1, ""),
+    ("C1", 4, 8, 1, "bf16", "dp_shard+halves1-1-1-5+zb+edge", 1, ""), ("C1", 2, 4, 1, "f32", "dp_shard+halves3-5", 2, ""),
     # P = 2 x D = 2
     ("C1", 2, 4, 1, "f32", "dp_shard", 2, ""), ("C1", 2, 4, 1, "bf16", "dp_shard", 2, ""),
     ("C1", 2, 8, 2, "f32", "dp_shard", 2, ""), ("C1", 2, 4, 1, "f32", "dp_shard", 2, "peer"),

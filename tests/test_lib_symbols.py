@@ -169,3 +169,51 @@ def test_fsdp_shards_partition_the_dp_parameters(P):
     mc = model_cfg(cfg, "bf16", fsdp="pull", head_place="dp_shard")
     h = C.c_void_p()
     assert L.lib().bm_ctx_create(C.byref(mc), sched.handle, 0, C.byref(h)) == 1   # BM_E_INVALID
+
+
+@pytest.mark.parametrize("P,V,units", [(2, 1, [3, 5]), (2, 1, [5, 3]), (4, 1, [3, 2, 2, 1]), (2, 2, [1, 3, 2, 2]),
+                                       (4, 1, [1, 1, 1, 5])])
+def test_param_layout_half_layer_units(P, V, units):
+    """stage_halves (bigmac.h, reading R24): unit 2l = layer l's norm + gate_up, unit
+    2l + 1 = its down; every rank holds exactly the parameters of its units, each
+    LLM parameter lives on one rank."""
+    from synth import get_config
+    from paper_2605_25451_b200 import _lib as L
+    from paper_2605_25451_b200 import schedule as BS
+    from paper_2605_25451_b200.runtime import model_cfg
+    cfg = get_config("C1", P=P, M=2 * P, V=V)
+    assert sum(units) == 2 * cfg.L
+    mc = model_cfg(cfg, "bf16", stage_layers=units, stage_halves=True)
+    sc = BS.make_cfg(P, 2 * P, V)
+    owner = {}
+    for rank in range(P):
+        n, tot, dp = C.c_int32(), C.c_int64(), C.c_int64()
+        L.call("bm_param_count", C.byref(mc), C.byref(sc), rank, C.byref(n), C.byref(tot), C.byref(dp))
+        for i in range(n.value):
+            pi = L.ParamInfo()
+            L.call("bm_param_info_get", C.byref(mc), C.byref(sc), rank, i, C.byref(pi))
+            nm = pi.name.decode()
+            if nm.startswith("llm.layer"):
+                assert nm not in owner, nm
+                owner[nm] = rank
+    for s in range(P * V):
+        rank = s % P
+        for u in range(sum(units[:s]), sum(units[:s + 1])):
+            l, half = divmod(u, 2)
+            names = [f"llm.layer{l}.down"] if half else [f"llm.layer{l}.norm", f"llm.layer{l}.gate_up"]
+            for nm in names:
+                assert owner.pop(nm) == rank, (nm, s)
+    assert not owner
+
+
+def test_half_layer_units_errors():
+    from synth import get_config
+    from paper_2605_25451_b200 import _lib as L
+    from paper_2605_25451_b200 import schedule as BS
+    from paper_2605_25451_b200.runtime import model_cfg
+    cfg = get_config("C1", P=2, M=4, V=1)
+    n, tot, dp = C.c_int32(), C.c_int64(), C.c_int64()
+    for bad in ([4, 3], [8, 0], None):       # sum != 2L, empty stage, no explicit partition
+        mc = model_cfg(cfg, "bf16", stage_layers=bad, stage_halves=True)
+        with pytest.raises(L.BigMacError):
+            L.call("bm_param_count", C.byref(mc), C.byref(BS.make_cfg(2, 4, 1)), 0, C.byref(n), C.byref(tot), C.byref(dp))
