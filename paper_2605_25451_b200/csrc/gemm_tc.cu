@@ -67,6 +67,7 @@ struct EpiArgs {
   int mpad;        // workspace rows per split (M rounded up to the tile height)
   int group;       // raster group (m-tiles per n sweep) of the CTA-pair kernel
   int mbar_cluster;  // 1: .acquire.cluster barrier waits (default); 0: BM_MBAR_SCOPE=cta
+  int prefetch = 1;  // pair epilogue: L2-prefetch the tile's g / u / residual rows (BM_EPI_PREFETCH=0: off)
 };
 
 // ---------------------------------------------------------------- PTX helpers
@@ -246,6 +247,10 @@ __device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int
   int r = t % per_group;
   mb = first_m + r % gm;
   nb = r / gm;
+}
+
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
 
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
@@ -1060,6 +1065,19 @@ gemm2_kernel(const __grid_constant__ PairGroup g) {
         constexpr int W = BN / 2;    // columns per warp
         const int cbeg = half * W, cend = (half + 1) * W;
         const bool dsw = ea.epi == BM_EPI_DSWIGLU && ea.tma;
+        // the epilogue's global reads (g / u of the SwiGLU backward, the residual R) for the
+        // whole tile into L2 while the MMAs still run: the chunk loads then hit L2 instead of
+        // waiting on HBM with one chunk in flight per warp
+        if (ea.prefetch && (dsw || ea.epi == BM_EPI_ADD) && row < ea.M) {
+          const int col0 = nb * BN + cbeg;
+          const int ces = (ea.epi == BM_EPI_ADD && ea.c_f32) ? 4 : 2;
+          const char* r = reinterpret_cast<const char*>(ea.R) + ((int64_t)row * ea.ldr + col0) * ces;
+          const int nbytes = min(cend - cbeg, ea.N - col0) * ces;
+          for (int o = 0; o < nbytes; o += 128) {
+            prefetch_l2(r + o);
+            if (dsw) prefetch_l2(r + (int64_t)ea.f * 2 + o);
+          }
+        }
         GU32 gu;
         if (dsw) load_gu(ea, row, nb * BN + cbeg, gu);   // ahead of the accumulator
         mbar_wait(&tfull[acc], acc_phase, mbc);
@@ -1304,6 +1322,10 @@ static int g_raster_group = [] {   // BM_GEMM_GROUP: measurement override of the
   const int v = e ? atoi(e) : 8;
   return v >= 1 ? v : 8;
 }();
+static int g_epi_prefetch = [] {
+  const char* e = getenv("BM_EPI_PREFETCH");
+  return e && e[0] == '0' ? 0 : 1;
+}();
 static int g_mbar_cluster = [] {   // default: the fully validated .acquire.cluster waits
   const char* e = getenv("BM_MBAR_SCOPE");
   return e && std::string(e) == "cta" ? 0 : 1;
@@ -1366,6 +1388,7 @@ static bm_status prepare_out(int M, int N, int K, void* Cp, int64_t ldc, int c_d
   *ea = EpiArgs{M, N, K, Cp, ldc, c_dtype == BM_F32 ? 1 : 0, epi, R, ldr, alpha, f, 0, 1, 1 << 30, 0, 8, 1};
   ea->group = g_raster_group;
   ea->mbar_cluster = g_mbar_cluster;
+  ea->prefetch = g_epi_prefetch;
   std::memset(mc, 0, sizeof(*mc));
   const int ces = c_dtype == BM_F32 ? 4 : 2;
   if (epi == BM_EPI_DSWIGLU) {
