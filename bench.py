@@ -402,9 +402,21 @@ def pacing_stage_mask(split, P, costs=None):
     return sum(1 << r for r, n in enumerate(w) if n >= mx - 1e-9)
 
 
+def lightest_only_mask(costs):
+    """Bits of every stage except the lightest one(s): with a half-layer partition the
+    encoder and generator run only where the LLM leaves the most room (C2, N = 4:
+    188.5 vs 180.2 samples/s for excluding only the heaviest stages,
+    profiles/r02/zb/ab_place_n4.log)."""
+    mn = min(costs)
+    if max(costs) <= mn + 1e-9:
+        return 0
+    return sum(1 << r for r, c in enumerate(costs) if c > mn + 1e-9)
+
+
 def _pacing(args, cfg, P, split):
-    halves = getattr(args, "partition", "layers") == "halves"
-    return pacing_stage_mask(split, P, unit_costs(cfg, split) if (halves and split) else None)
+    if getattr(args, "partition", "layers") == "halves" and split and len(split) == P:
+        return lightest_only_mask(unit_costs(cfg, split))
+    return pacing_stage_mask(split, P)
 
 
 def gen_exclude(args, cfg, P, split, strategy):
@@ -514,6 +526,7 @@ def run_secondary(args, cx, rank, world, name, cfg, P, D, steps, warmup, with_bu
     out["peak_hbm_gb_per_gpu"] = cx.max(torch.cuda.max_memory_allocated()) / 1e9
     out["stash_peak_bytes_rank0_enc_llm_gen"] = rt.stash_peak()
     out["config"] = {"stages": P, "replicas": D, "microbatches": cfg.M, "warmup_units": W, "stage_layers": split,
+                     "partition": getattr(args, "partition", "layers"), "llm_sched": cfg.llm_sched,
                      "last_stage_layers": n_last}
     free_runtime(rt)
     del db
@@ -582,7 +595,7 @@ def main():
                          "or FSDP with the all-gather baseline (bigmac.h bm_fsdp_mode, P:401-426)")
     ap.add_argument("--gen-exclude", default="auto", help="ranks that take no generator rows: auto | none | r,r")
     ap.add_argument("--enc-exclude", default="auto", help="ranks that run no encoder microbatch: auto | none | r,r")
-    ap.add_argument("--partition", default="layers", choices=["layers", "halves"],
+    ap.add_argument("--partition", default="halves", choices=["layers", "halves"],
                     help="LLM stage partition: whole layers (DEFAULT_SPLIT / last_stage_layers) or half-layer units "
                          "(stage boundaries inside layers, bigmac.h stage_halves)")
     ap.add_argument("--llm-sched", default="auto", choices=["auto", "zb_h1"],
@@ -707,6 +720,10 @@ def main():
             # BASELINE.json configs[1]: 16 microbatches per pipeline (global batch 16 D)
             c2 = get_config("C2", P=P, M=16, V=1)
             extra["c2_m16_per_replica"] = run_secondary(args, cx, rank, world, "C2", c2, P, D, max(3, args.steps // 2), 3)
+        if N > 1 and cfg.V == 1 and cfg.llm_sched != "zb_h1":
+            # the same workload on the ZB-H1 zero-bubble base schedule (reading R23)
+            extra["zb_h1"] = run_secondary(args, cx, rank, world, cfg.name, cfg.replace(llm_sched="zb_h1"), P, D,
+                                           max(3, args.steps // 2), 3)
         if args.sweep:
             extra["batch_sweep"] = {"config": f"{args.config} model, P = {P} x D = {D}, bigmac, 1 timed step per "
                                               f"per-replica M",
@@ -768,6 +785,7 @@ def main():
             "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
             "config": dict(config_dict(cfg, P, D), strategy=args.strategy, head_place=head_place_name(args, N),
                            warmup_units=W, last_stage_layers=n_last, stage_layers=split, step_sum=sum_mode,
+                           partition=args.partition,
                            gen_exclude=gen_exclude(args, cfg, P, split, args.strategy),
                            enc_exclude=enc_exclude(args, cfg, P, split, args.strategy)),
             "roofline": roofline, "step_roofline": step_roof, "bubble": bubble, "fsdp": fsdp_info,
