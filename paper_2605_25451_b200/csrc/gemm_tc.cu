@@ -67,7 +67,7 @@ struct EpiArgs {
   int mpad;        // workspace rows per split (M rounded up to the tile height)
   int group;       // raster group (m-tiles per n sweep) of the CTA-pair kernel
   int mbar_cluster;  // 1: .acquire.cluster barrier waits (default); 0: BM_MBAR_SCOPE=cta
-  int prefetch = 1;  // pair epilogue: L2-prefetch the tile's g / u / residual rows (BM_EPI_PREFETCH=0: off)
+  int prefetch = 1;  // pair epilogue: L2-prefetch the tile's g / u rows (BM_EPI_PREFETCH=0: off)
 };
 
 // ---------------------------------------------------------------- PTX helpers
@@ -1065,17 +1065,18 @@ gemm2_kernel(const __grid_constant__ PairGroup g) {
         constexpr int W = BN / 2;    // columns per warp
         const int cbeg = half * W, cend = (half + 1) * W;
         const bool dsw = ea.epi == BM_EPI_DSWIGLU && ea.tma;
-        // the epilogue's global reads (g / u of the SwiGLU backward, the residual R) for the
-        // whole tile into L2 while the MMAs still run: the chunk loads then hit L2 instead of
-        // waiting on HBM with one chunk in flight per warp
-        if (ea.prefetch && (dsw || ea.epi == BM_EPI_ADD) && row < ea.M) {
+        // the epilogue's global reads (g / u of the SwiGLU backward) for the whole tile into
+        // L2 while the MMAs still run: the chunk loads then hit L2 instead of waiting on HBM
+        // with one chunk in flight per warp
+        // (SwiGLU backward only: standalone +1.5 % at C2, +5 % at C4 shapes; the residual
+        // add's R lost 2 %; profiles/r02/bn512/pf_gemm.log)
+        if (ea.prefetch && dsw && row < ea.M) {
           const int col0 = nb * BN + cbeg;
-          const int ces = (ea.epi == BM_EPI_ADD && ea.c_f32) ? 4 : 2;
-          const char* r = reinterpret_cast<const char*>(ea.R) + ((int64_t)row * ea.ldr + col0) * ces;
-          const int nbytes = min(cend - cbeg, ea.N - col0) * ces;
+          const char* r = reinterpret_cast<const char*>(ea.R) + ((int64_t)row * ea.ldr + col0) * 2;
+          const int nbytes = min(cend - cbeg, ea.N - col0) * 2;
           for (int o = 0; o < nbytes; o += 128) {
             prefetch_l2(r + o);
-            if (dsw) prefetch_l2(r + (int64_t)ea.f * 2 + o);
+            prefetch_l2(r + (int64_t)ea.f * 2 + o);
           }
         }
         GU32 gu;
