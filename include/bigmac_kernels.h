@@ -95,6 +95,10 @@ bm_status bm_k_gemm_mode(int32_t mode);
  * whenever N >= 512 (one 512-column accumulator; a quarter less L2 -> SMEM traffic
  * per FLOP), 2 = auto (256 x 512 when N >= 512 and K >= 4096).  Process-wide. */
 bm_status bm_k_gemm_bn512(int32_t mode);
+/* 1: single-problem 256 x 256 CTA-pair GEMMs run as clusters of two pairs (four CTAs)
+ * that share the A tile by TMA multicast (each CTA loads half of its 128 A rows for
+ * both pairs); 0 (default): one pair per cluster.  Process-wide. */
+bm_status bm_k_gemm_cl4(int32_t on);
 
 /* RMSNorm y = x * rstd * g, rstd = 1/sqrt(mean(x^2) + 1e-5); rstd saved (fp32 [rows]). */
 bm_status bm_k_rmsnorm_fwd(int32_t dtype, int32_t rows, int32_t cols, const void* x,
