@@ -34,6 +34,10 @@ def main():
     ap.add_argument("--head", default="auto", choices=["auto", "last_stage", "dp_shard"])
     ap.add_argument("--last-stage-layers", type=int, default=0)
     ap.add_argument("--stage-layers", default="", help="explicit LLM layers per stage, e.g. 4,4,5,3")
+    ap.add_argument("--halves", action="store_true", help="--stage-layers in half-layer units (stage_halves)")
+    ap.add_argument("--gen-exclude", type=int, default=0, help="bit mask (bigmac.h gen_exclude)")
+    ap.add_argument("--enc-exclude", type=int, default=0, help="bit mask (bm_sched_cfg.enc_exclude)")
+    ap.add_argument("--llm-sched", default="auto", choices=["auto", "zb_h1"])
     ap.add_argument("--out", default="gpurun_out/trace.json")
     a = ap.parse_args()
     rank, world = int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
@@ -45,11 +49,17 @@ def main():
     from synth import get_config, make_batch
     from paper_2605_25451_b200.runtime import Runtime
     cfg = get_config(a.config, P=world, M=a.M, V=a.V)
+    if a.llm_sched == "zb_h1":
+        cfg = cfg.replace(llm_sched="zb_h1")
     kw = {"bigmac": {}, "compute_efficient": {"warmup_units": cfg.M // world},
           "memory_efficient": {"enc_place": "entry_stage", "gen_place": "last_stage"}}[a.strategy]
+    kw = dict(kw, llm_sched=cfg.llm_sched)
+    if a.enc_exclude:
+        kw["enc_exclude"] = a.enc_exclude
     rt = Runtime(cfg, "bf16", rank=rank, world=world, group=group, sched_kw=kw, head_place=a.head,
                  last_stage_layers=a.last_stage_layers,
-                 stage_layers=[int(v) for v in a.stage_layers.split(",")] if a.stage_layers else None)
+                 stage_layers=[int(v) for v in a.stage_layers.split(",")] if a.stage_layers else None,
+                 gen_exclude=a.gen_exclude, stage_halves=a.halves)
     rt.init_random_weights(1)
     db = rt.device_batch(make_batch(cfg))
     for _ in range(a.warmup):
