@@ -99,6 +99,10 @@ bm_status bm_k_gemm_bn512(int32_t mode);
  * that share the A tile by TMA multicast (each CTA loads half of its 128 A rows for
  * both pairs); 0 (default): one pair per cluster.  Process-wide. */
 bm_status bm_k_gemm_cl4(int32_t on);
+/* 1 (default): 256 x 256 CTA-pair GEMMs step K in 128-deep blocks (two 64-wide
+ * swizzled sub-tiles per operand, three 64 KB stages); 0: 64-deep blocks, six
+ * stages.  Process-wide. */
+bm_status bm_k_gemm_bk128(int32_t on);
 
 /* RMSNorm y = x * rstd * g, rstd = 1/sqrt(mean(x^2) + 1e-5); rstd saved (fp32 [rows]). */
 bm_status bm_k_rmsnorm_fwd(int32_t dtype, int32_t rows, int32_t cols, const void* x,

@@ -767,16 +767,18 @@ constexpr int NUM_THREADS2 = 64 + 32 * EPI_WARPS2;
 // BN = 512 (pair tile 256 x 512, each CTA 128 x 512): a quarter less L2 -> SMEM
 // traffic per FLOP than 256 x 256 (cuBLAS's tile on these shapes), at the price of a
 // single TMEM accumulator (512 columns): the MMA waits for the epilogue between tiles
-template <int BN, bool SWI = false> struct Cfg2 {
-  static constexpr int A_BYTES = 128 * BK * 2;                 // 16 KB
-  static constexpr int B_BYTES = (BN / 2) * BK * 2;            // 16 KB (BN = 256), 32 KB (BN = 512)
+// BKP = 128: 128-deep K blocks (two 64-wide swizzle sub-tiles per operand, 64 KB stages,
+// 3 stages) -- twice the MMAs per barrier round trip, same bytes per FLOP.
+template <int BN, bool SWI = false, int BKP = 64> struct Cfg2 {
+  static constexpr int A_BYTES = 128 * BKP * 2;                // 16 KB (BKP = 64)
+  static constexpr int B_BYTES = (BN / 2) * BKP * 2;           // 16 KB (BN = 256), 32 KB (BN = 512)
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   // staging slots per epilogue warp: with 2, a chunk's TMA stores read one while the
   // next chunk is staged in the other (wait_group.read 1); with 1, read 0
   // (measured: 2 slots with 5 stages gains 1.5 % on the SwiGLU-backward dgrad and
   // loses 3-4 % on the fp32 wgrads, so the non-SwiGLU kernels keep 1 slot, 6 stages)
   static constexpr int NSLOT = 1;
-  static constexpr int STAGES = SWI ? 5 : (BN == 512 ? 4 : ((BN == 256) ? 6 : 8));
+  static constexpr int STAGES = SWI ? 5 : (BKP == 128 ? 3 : (BN == 512 ? 4 : ((BN == 256) ? 6 : 8)));
   static constexpr int NACC = BN == 512 ? 1 : 2;               // TMEM accumulator buffers
   static constexpr int TMEM_COLS = NACC * BN;
   static constexpr int EPI_SLOT = SWI ? 6144 : 4096;           // staging slot of one epilogue warp
@@ -887,10 +889,12 @@ __device__ __forceinline__ void store_dswiglu_tma(const EpiArgs& a, const CUtens
 // CTA loads 64 of its 128 A rows and multicasts them to its counterpart in the other
 // pair (a quarter less L2 -> SMEM traffic per FLOP, keeping the two TMEM accumulators);
 // a stage is free when both pairs' MMAs have read it (empty barriers count two commits).
-template <int BN, bool SWIGLU, int AM = -1, int BMJ = -1, int CL = 2>
+template <int BN, bool SWIGLU, int AM = -1, int BMJ = -1, int CL = 2, int BKP = 64>
 __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NUM_THREADS2, 1)
 gemm2_kernel(const __grid_constant__ PairGroup g) {
-  using C = Cfg2<BN, SWIGLU>;
+  static_assert(BKP == 64 || (BN == 256 && CL == 2 && !SWIGLU), "BKP = 128: plain 256 x 256 pair tiles only");
+  constexpr int NSUB = BKP / 64;   // 64-wide swizzle sub-tiles per K block
+  using C = Cfg2<BN, SWIGLU, BKP>;
   constexpr int STAGES = C::STAGES;
   constexpr int BNH = BN / 2;
   extern __shared__ uint8_t smem_raw[];
@@ -968,16 +972,17 @@ gemm2_kernel(const __grid_constant__ PairGroup g) {
           const uint32_t lbar = mapa(smem_u32(&full[stage]), lead);
           uint8_t* a_dst = smA + stage * C::A_BYTES;
           uint8_t* b_dst = smB + stage * C::B_BYTES;
-          const int k0 = kb * BK;
+          const int k0 = kb * BKP;
           if (CL == 4) {
             // rows [64 pq, +64) of this CTA's A half, to itself and its counterpart
             if (amn) tma_load_2d_pair_mc(a_dst + pq * (BK * 128), mA, lbar, m0 + 64 * (int)pq, k0, mc_mask);
             else tma_load_2d_pair_mc(a_dst + pq * (64 * 128), mA, lbar, k0, m0 + 64 * (int)pq, mc_mask);
           } else if (amn) {
 #pragma unroll
-            for (int j = 0; j < BM / 64; ++j) tma_load_2d_pair(a_dst + j * (BK * 128), mA, lbar, m0 + 64 * j, k0);
+            for (int j = 0; j < BM / 64; ++j) tma_load_2d_pair(a_dst + j * (BKP * 128), mA, lbar, m0 + 64 * j, k0);
           } else {
-            tma_load_2d_pair(a_dst, mA, lbar, k0, m0);
+#pragma unroll
+            for (int q = 0; q < NSUB; ++q) tma_load_2d_pair(a_dst + q * (BM * 128), mA, lbar, k0 + 64 * q, m0);
           }
           if (BN == 512) {
             // two 128-row halves, half h = global columns [nb*512 + h*256, +256) of the pair
@@ -995,9 +1000,10 @@ gemm2_kernel(const __grid_constant__ PairGroup g) {
             }
           } else if (bmn) {
 #pragma unroll
-            for (int j = 0; j < BNH / 64; ++j) tma_load_2d_pair(b_dst + j * (BK * 128), mB, lbar, n0 + 64 * j, k0);
+            for (int j = 0; j < BNH / 64; ++j) tma_load_2d_pair(b_dst + j * (BKP * 128), mB, lbar, n0 + 64 * j, k0);
           } else {
-            tma_load_2d_pair(b_dst, mB, lbar, k0, n0);
+#pragma unroll
+            for (int q = 0; q < NSUB; ++q) tma_load_2d_pair(b_dst + q * (BNH * 128), mB, lbar, k0 + 64 * q, n0);
           }
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
@@ -1026,12 +1032,15 @@ gemm2_kernel(const __grid_constant__ PairGroup g) {
           const uint32_t a_base = smem_u32(smA + stage * C::A_BYTES);
           const uint32_t b_base = smem_u32(smB + stage * C::B_BYTES);
 #pragma unroll
-          for (int kk = 0; kk < BK / 16; ++kk) {
-            uint64_t ad = amn ? make_desc(a_base + kk * 2048, BK * 128, 1024) : make_desc(a_base + kk * 32, 16, 1024);
+          for (int kk = 0; kk < BKP / 16; ++kk) {
+            const int q = kk / 4, w = kk % 4;   // K-major: sub-tile q, 16-deep step w within it
+            uint64_t ad = amn ? make_desc(a_base + kk * 2048, BKP * 128, 1024)
+                              : make_desc(a_base + q * (BM * 128) + w * 32, 16, 1024);
 #pragma unroll
             for (int h = 0; h < (BN == 512 ? 2 : 1); ++h) {   // BN = 512: two N = 256 MMAs sharing A
               const uint32_t bh = b_base + h * 16384;
-              uint64_t bd = bmn ? make_desc(bh + kk * 2048, BK * 128, 1024) : make_desc(bh + kk * 32, 16, 1024);
+              uint64_t bd = bmn ? make_desc(bh + kk * 2048, BKP * 128, 1024)
+                                : make_desc(bh + q * (BNH * 128) + w * 32, 16, 1024);
               umma_f16_pair(tmem_d + h * 256, ad, bd, idesc, (kb != 0 || kk != 0) ? 1u : 0u);
             }
           }
@@ -1317,39 +1326,39 @@ static bm_status dispatch_majors(bool a_mn, bool b_mn, const CUtensorMap& ma, co
 }
 
 
-template <int BN, bool SWIGLU = false, int AM = -1, int BMJ = -1, int CL = 2>
+template <int BN, bool SWIGLU = false, int AM = -1, int BMJ = -1, int CL = 2, int BKP = 64>
 static bm_status launch2(const PairGroup& g, int tiles, cudaStream_t st) {
-  using C = Cfg2<BN, SWIGLU>;
+  using C = Cfg2<BN, SWIGLU, BKP>;
   static bool attr_set = false;
   static int max_clusters = 0;   // CL = 4: clusters of two pairs that fit at once (GPC shapes)
   if (!attr_set) {
-    BM_CUDA_TRY(cudaFuncSetAttribute(gemm2_kernel<BN, SWIGLU, AM, BMJ, CL>,
+    BM_CUDA_TRY(cudaFuncSetAttribute(gemm2_kernel<BN, SWIGLU, AM, BMJ, CL, BKP>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
     if (CL == 4) {
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3(num_sms() / 4 * 4);
       cfg.blockDim = dim3(NUM_THREADS2);
       cfg.dynamicSmemBytes = C::SMEM;
-      BM_CUDA_TRY(cudaOccupancyMaxActiveClusters(&max_clusters, gemm2_kernel<BN, SWIGLU, AM, BMJ, CL>, &cfg));
+      BM_CUDA_TRY(cudaOccupancyMaxActiveClusters(&max_clusters, gemm2_kernel<BN, SWIGLU, AM, BMJ, CL, BKP>, &cfg));
     }
     attr_set = true;
   }
   // tiles = work items: pair tiles (CL = 2) or cluster tiles (CL = 4)
   const int slots = CL == 4 ? std::min(max_clusters, gemm_sm_budget() / 4) : gemm_sm_budget() / 2;
   const int grid = CL * (tiles < slots ? tiles : std::max(slots, 1));
-  BM_CUDA_TRY(launch_k(gemm2_kernel<BN, SWIGLU, AM, BMJ, CL>, dim3(grid), dim3(NUM_THREADS2), C::SMEM, st, g));
+  BM_CUDA_TRY(launch_k(gemm2_kernel<BN, SWIGLU, AM, BMJ, CL, BKP>, dim3(grid), dim3(NUM_THREADS2), C::SMEM, st, g));
   count_launch();
   BM_CUDA_TRY(cudaGetLastError());
   return BM_OK;
 }
 // single-problem launch with the operand majors as template constants
-template <int BN, int CL = 2>
+template <int BN, int CL = 2, int BKP = 64>
 static bm_status launch2_static(const PairGroup& g, int tiles, cudaStream_t st) {
   const int a = g.prob[0].a_mn, b = g.prob[0].b_mn;
-  if (!a && !b) return launch2<BN, false, 0, 0, CL>(g, tiles, st);
-  if (!a && b) return launch2<BN, false, 0, 1, CL>(g, tiles, st);
-  if (a && b) return launch2<BN, false, 1, 1, CL>(g, tiles, st);
-  return launch2<BN, false, 1, 0, CL>(g, tiles, st);
+  if (!a && !b) return launch2<BN, false, 0, 0, CL, BKP>(g, tiles, st);
+  if (!a && b) return launch2<BN, false, 0, 1, CL, BKP>(g, tiles, st);
+  if (a && b) return launch2<BN, false, 1, 1, CL, BKP>(g, tiles, st);
+  return launch2<BN, false, 1, 0, CL, BKP>(g, tiles, st);
 }
 
 }  // namespace tc
@@ -1413,6 +1422,17 @@ static int g_cl4 = [] {
   return e ? atoi(e) : 0;
 }();
 void set_gemm_cl4(int m) { g_cl4 = m; }
+// 128-deep K blocks for 256 x 256 pair tiles (default; BM_GEMM_BK128=0: 64-deep, 6 stages).
+// Twice the MMAs per full-barrier round trip at the same bytes per FLOP: standalone
+// +3..+14 % on the 256-wide C2 / C4 contractions (C4 head wgrad -8 %), C2 step 50.5 ->
+// 51.6 samples/s, in-step GEMM 0.84 -> 0.86 (profiles/r02/bn512/bk128_*.log).  The
+// SwiGLU-forward kernel keeps 64-deep blocks (its 48 KB epilogue staging leaves room
+// for two 64 KB stages only).
+static int g_bk128 = [] {
+  const char* e = getenv("BM_GEMM_BK128");
+  return e ? atoi(e) : 1;
+}();
+void set_gemm_bk128(int m) { g_bk128 = m; }
 static bool use_bn512(int M, int N, int K, int c_dtype, int epi) {
   if (N < 512 || g_bn512 == 0 || epi == BM_EPI_SWIGLU) return false;
   if (g_bn512 == 1) return true;   // forced (tests, A/B), the SwiGLU-backward epilogue included
@@ -1527,8 +1547,16 @@ bm_status gemm_bf16_tc(int M, int N, int K, const void* A, int64_t lda, int a_ma
       pr.tiles_n = ceil_div(pr.tiles_n, 2);
       if (a_major == 0) BM_TRY(make_map(A, K, M, lda, 64, &pr.tmA));
     }
+    const bool bk128 = g_bk128 != 0 && BN2 == 256 && !cl4;
+    if (bk128) {   // MN-major operands as 64 x 128 boxes; 128-deep K blocks
+      PairProblem& pr = g.prob[0];
+      if (a_major != 0) BM_TRY(make_map(A, M, K, lda, 128, &pr.tmA));
+      if (b_major != 0) BM_TRY(make_map(B, N, K, ldb, 128, &pr.tmB));
+      pr.nk = ceil_div(K, 128);
+    }
     g.tiles0 = g.total_tiles = g.prob[0].tiles_m * g.prob[0].tiles_n;
     if (cl4) return launch2_static<256, 4>(g, g.total_tiles, st);
+    if (bk128) return launch2_static<256, 2, 128>(g, g.total_tiles, st);
     if (BN2 == 512) return launch2_static<512>(g, g.total_tiles, st);
     if (BN2 == 256) return launch2_static<256>(g, g.total_tiles, st);
     return launch2_static<128>(g, g.total_tiles, st);

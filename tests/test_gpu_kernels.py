@@ -502,3 +502,68 @@ def test_gemm_fused_swiglu_cluster4(L, M, f, K):
     finally:
         L.call("bm_k_gemm_cl4", 0)
         L.call("bm_k_gemm_mode", 0)
+
+
+@pytest.mark.parametrize("M,N,K", [(512, 512, 64), (2560, 2048, 512), (1000, 1000, 640), (4096, 2304, 1000),
+                                   (304, 1280, 200)])
+@pytest.mark.parametrize("a_mn,b_mn", [(0, 0), (0, 1), (1, 1), (1, 0)])
+@pytest.mark.parametrize("epi", ["f32_store", "bf16_add", "f32_accum", "dswiglu"])
+@pytest.mark.parametrize("bk", [128, 64])
+def test_gemm_pairs_bk128(L, M, N, K, a_mn, b_mn, epi, bk):
+    """128-deep (default) and 64-deep K blocks on 256 x 256 pair tiles (bm_k_gemm_bk128):
+    every operand major, K tails that end inside a block or a sub-tile, four epilogues;
+    bitwise equal to a rerun."""
+    L.call("bm_k_gemm_mode", 2)
+    L.call("bm_k_gemm_bn512", 0)
+    L.call("bm_k_gemm_bk128", 1 if bk == 128 else 0)
+    try:
+        rng = np.random.default_rng(M + 3 * N + 5 * K + 7 * a_mn + b_mn)
+        if epi == "dswiglu":
+            if a_mn or not b_mn or N % 32:
+                pytest.skip("the SwiGLU backward is dY (K-major) x W_down (MN-major), f % 32 == 0")
+            f = N
+            gu, dY, Wd = rnd(rng, M, 2 * f), rnd(rng, M, K), rnd(rng, K, f, scale=0.1)
+            gud, dYd, Wdd = dev(gu, BF16), dev(dY, BF16), dev(Wd, BF16)
+            outs = []
+            for _ in range(2):
+                dgu = torch.zeros((M, 2 * f), device="cuda", dtype=torch.bfloat16)
+                L.call("bm_k_gemm_dswiglu", M, f, K, dYd.data_ptr(), K, Wdd.data_ptr(), f, gud.data_ptr(),
+                       dgu.data_ptr(), None)
+                torch.cuda.synchronize()
+                outs.append(dgu)
+            ref = om.swiglu_bwd(dY @ Wd, gu, f)
+            assert np.abs(host(outs[0]) - ref).max() <= 1e-2 * max(1e-3, np.abs(ref).max())
+            assert torch.equal(outs[0], outs[1])
+            return
+        A, B, R = rnd(rng, M, K), rnd(rng, N, K), rnd(rng, M, N)
+        Ad = dev(A.T.copy() if a_mn else A, BF16)
+        Bd = dev(B.T.copy() if b_mn else B, BF16)
+        ref = A @ B.T * 0.5
+        outs = []
+        for _ in range(2):
+            if epi == "f32_store":
+                C = torch.full((M, N), 7.0, device="cuda", dtype=torch.float32)
+                args = (C.data_ptr(), N, F32, 0, None, 0)
+            elif epi == "bf16_add":
+                C = torch.zeros((M, N), device="cuda", dtype=torch.bfloat16)
+                Rd = dev(R, BF16)
+                args = (C.data_ptr(), N, BF16, 2, Rd.data_ptr(), N)
+            else:
+                C = dev(R, F32)
+                args = (C.data_ptr(), N, F32, 1, None, 0)
+            L.call("bm_k_gemm", BF16, M, N, K, Ad.data_ptr(), M if a_mn else K, a_mn, Bd.data_ptr(),
+                   N if b_mn else K, b_mn, *args, 0.5, None)
+            torch.cuda.synchronize()
+            outs.append(C)
+        out = host(outs[0])
+        if epi != "f32_store":
+            ref = ref + R
+        if epi == "bf16_add":
+            assert np.all(np.abs(out - ref) <= 2.0 ** -8 * np.abs(ref) + 1e-4 * np.sqrt(K))
+        else:
+            assert np.abs(out - ref).max() <= 1e-5 * np.sqrt(K) * max(1.0, np.abs(ref).max())
+        assert torch.equal(outs[0], outs[1])
+    finally:
+        L.call("bm_k_gemm_bk128", 1)
+        L.call("bm_k_gemm_mode", 0)
+        L.call("bm_k_gemm_bn512", 2)
