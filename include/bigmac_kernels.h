@@ -103,6 +103,10 @@ bm_status bm_k_gemm_cl4(int32_t on);
  * swizzled sub-tiles per operand, three 64 KB stages); 0: 64-deep blocks, six
  * stages.  Process-wide. */
 bm_status bm_k_gemm_bk128(int32_t on);
+/* 1: the gate/up GEMM with the fused SwiGLU epilogue also steps K in 128-deep blocks
+ * (three 64 KB stages; 4 KB epilogue staging per warp, [g | u] stored before h;
+ * default); 0: 64-deep blocks, five stages.  Takes effect with bm_k_gemm_bk128(1). */
+bm_status bm_k_gemm_swiglu_bk128(int32_t on);
 
 /* RMSNorm y = x * rstd * g, rstd = 1/sqrt(mean(x^2) + 1e-5); rstd saved (fp32 [rows]). */
 bm_status bm_k_rmsnorm_fwd(int32_t dtype, int32_t rows, int32_t cols, const void* x,

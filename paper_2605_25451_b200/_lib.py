@@ -137,6 +137,7 @@ SIGNATURES = {
     "bm_k_gemm_bn512": [_I32],
     "bm_k_gemm_cl4": [_I32],
     "bm_k_gemm_bk128": [_I32],
+    "bm_k_gemm_swiglu_bk128": [_I32],
     "bm_k_gemm_group": [C.POINTER(GemmDesc), _I32, _P],
     "bm_k_gemm_swiglu": [_I32, _I32, _I32, _P, _I64, _P, _I64, _P, _P, _P],
     "bm_k_gemm_dswiglu": [_I32, _I32, _I32, _P, _I64, _P, _I64, _P, _P, _P],

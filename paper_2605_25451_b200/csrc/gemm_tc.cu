@@ -426,6 +426,39 @@ __device__ __forceinline__ void epi_swiglu_tma(const EpiArgs& a, const CUtensorM
   }
 }
 
+// the same with a 4 KB staging slot: [g | u] first, then h once the TMA engine has read them
+__device__ __forceinline__ void epi_swiglu_tma_4k(const EpiArgs& a, const CUtensorMap* tmGU, const CUtensorMap* tmH,
+                                                  uint32_t slot, int lane, int row0, int j0, const float* vg,
+                                                  const float* vu) {
+  float g[32], u[32], h[32];
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    const float gr = __bfloat162float(__float2bfloat16_rn(a.alpha * vg[j]));
+    const float ur = __bfloat162float(__float2bfloat16_rn(a.alpha * vu[j]));
+    g[j] = gr;
+    u[j] = ur;
+    h[j] = gr * sigmoidf_(gr) * ur;
+  }
+  stage_bf16(slot, lane, g);
+  stage_bf16(slot + 2048, lane, u);
+  fence_async_smem();
+  __syncwarp();
+  if (lane == 0) {
+    tma_store_2d(tmGU, slot, j0, row0);
+    tma_store_2d(tmGU, slot + 2048, a.f + j0, row0);
+    bulk_commit();
+    bulk_wait_read0();
+  }
+  __syncwarp();
+  stage_bf16(slot, lane, h);
+  fence_async_smem();
+  __syncwarp();
+  if (lane == 0) {
+    tma_store_2d(tmH, slot, j0, row0);
+    bulk_commit();
+  }
+}
+
 __device__ __forceinline__ void epilogue_row(const EpiArgs& a, int row, int col0, const float* v) {
   // one thread writes up to 32 consecutive columns of one row
   const int ncols = min(32, a.N - col0);
@@ -778,10 +811,10 @@ template <int BN, bool SWI = false, int BKP = 64> struct Cfg2 {
   // (measured: 2 slots with 5 stages gains 1.5 % on the SwiGLU-backward dgrad and
   // loses 3-4 % on the fp32 wgrads, so the non-SwiGLU kernels keep 1 slot, 6 stages)
   static constexpr int NSLOT = 1;
-  static constexpr int STAGES = SWI ? 5 : (BKP == 128 ? 3 : (BN == 512 ? 4 : ((BN == 256) ? 6 : 8)));
+  static constexpr int STAGES = SWI ? (BKP == 128 ? 3 : 5) : (BKP == 128 ? 3 : (BN == 512 ? 4 : ((BN == 256) ? 6 : 8)));
   static constexpr int NACC = BN == 512 ? 1 : 2;               // TMEM accumulator buffers
   static constexpr int TMEM_COLS = NACC * BN;
-  static constexpr int EPI_SLOT = SWI ? 6144 : 4096;           // staging slot of one epilogue warp
+  static constexpr int EPI_SLOT = (SWI && BKP == 64) ? 6144 : 4096;   // staging slot of one epilogue warp
   static constexpr int EPI_BYTES = EPI_WARPS2 * NSLOT * EPI_SLOT;
   static constexpr int SMEM = STAGES * STAGE_BYTES + EPI_BYTES + 1024 + 256;
 };
@@ -892,7 +925,7 @@ __device__ __forceinline__ void store_dswiglu_tma(const EpiArgs& a, const CUtens
 template <int BN, bool SWIGLU, int AM = -1, int BMJ = -1, int CL = 2, int BKP = 64>
 __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NUM_THREADS2, 1)
 gemm2_kernel(const __grid_constant__ PairGroup g) {
-  static_assert(BKP == 64 || (BN == 256 && CL == 2 && !SWIGLU), "BKP = 128: plain 256 x 256 pair tiles only");
+  static_assert(BKP == 64 || (BN == 256 && CL == 2), "BKP = 128: 256 x 256 pair tiles, one pair per cluster");
   constexpr int NSUB = BKP / 64;   // 64-wide swizzle sub-tiles per K block
   using C = Cfg2<BN, SWIGLU, BKP>;
   constexpr int STAGES = C::STAGES;
@@ -1090,7 +1123,8 @@ gemm2_kernel(const __grid_constant__ PairGroup g) {
                 if (lane == 0) bulk_wait_read0();
                 __syncwarp();
               }
-              epi_swiglu_tma(ea, mC, mC2, slot, lane, row0, nb * BNH + c, vg, vu);
+              if (C::EPI_SLOT == 4096) epi_swiglu_tma_4k(ea, mC, mC2, slot, lane, row0, nb * BNH + c, vg, vu);
+              else epi_swiglu_tma(ea, mC, mC2, slot, lane, row0, nb * BNH + c, vg, vu);
               ++eiter;
             }
           } else if (row < ea.M) {
@@ -1399,6 +1433,17 @@ static int g_group_rr = [] {
   return e && e[0] == '1' ? 1 : 0;
 }();
 void set_gemm_mode(int m) { g_gemm_mode = m; }
+// 128-deep K blocks for 256 x 256 pair tiles (default; BM_GEMM_BK128=0: 64-deep, 6 stages).
+// Twice the MMAs per full-barrier round trip at the same bytes per FLOP: standalone
+// +3..+14 % on the 256-wide C2 / C4 contractions (C4 head wgrad -8 %), C2 step 50.5 ->
+// 51.6 samples/s, in-step GEMM 0.84 -> 0.86 (profiles/r02/bn512/bk128_*.log).  The
+// SwiGLU-forward kernel keeps 64-deep blocks (its 48 KB epilogue staging leaves room
+// for two 64 KB stages only, so it stages [g | u] and h through 4 KB, see below).
+static int g_bk128 = [] {
+  const char* e = getenv("BM_GEMM_BK128");
+  return e ? atoi(e) : 1;
+}();
+void set_gemm_bk128(int m) { g_bk128 = m; }
 // 256 x 512 pair tiles (BM_GEMM_BN512: 0 = never, 1 = every pair GEMM with N >= 512,
 // default 2 = by a wave-quantised cost model).  A 256 x 512 tile moves a quarter less
 // L2 -> SMEM data per FLOP (its k-blocks run ~1.1x faster than two 256 x 256 ones) but
@@ -1422,17 +1467,16 @@ static int g_cl4 = [] {
   return e ? atoi(e) : 0;
 }();
 void set_gemm_cl4(int m) { g_cl4 = m; }
-// 128-deep K blocks for 256 x 256 pair tiles (default; BM_GEMM_BK128=0: 64-deep, 6 stages).
-// Twice the MMAs per full-barrier round trip at the same bytes per FLOP: standalone
-// +3..+14 % on the 256-wide C2 / C4 contractions (C4 head wgrad -8 %), C2 step 50.5 ->
-// 51.6 samples/s, in-step GEMM 0.84 -> 0.86 (profiles/r02/bn512/bk128_*.log).  The
-// SwiGLU-forward kernel keeps 64-deep blocks (its 48 KB epilogue staging leaves room
-// for two 64 KB stages only).
-static int g_bk128 = [] {
-  const char* e = getenv("BM_GEMM_BK128");
+
+// ... for the SwiGLU-forward kernel too (default; three 64 KB stages, 4 KB epilogue
+// staging per warp, [g | u] and h stored one after the other): standalone +5.9 % (C2) /
+// +5.6 % (C4), C2 step 51.1 -> 51.6 samples/s (profiles/r02/bn512/swbk_*.log);
+// BM_GEMM_SWIGLU_BK128=0: 64-deep blocks, five stages, 6 KB staging
+static int g_swiglu_bk128 = [] {
+  const char* e = getenv("BM_GEMM_SWIGLU_BK128");
   return e ? atoi(e) : 1;
 }();
-void set_gemm_bk128(int m) { g_bk128 = m; }
+void set_gemm_swiglu_bk128(int m) { g_swiglu_bk128 = m; }
 static bool use_bn512(int M, int N, int K, int c_dtype, int epi) {
   if (N < 512 || g_bn512 == 0 || epi == BM_EPI_SWIGLU) return false;
   if (g_bn512 == 1) return true;   // forced (tests, A/B), the SwiGLU-backward epilogue included
@@ -1441,7 +1485,11 @@ static bool use_bn512(int M, int N, int K, int c_dtype, int epi) {
   const int64_t tm = (M + 255) / 256, nk = (K + 63) / 64;
   const int64_t t256 = tm * ((N + 255) / 256), t512 = tm * ((N + 511) / 512);
   const double c256 = (double)((t256 + pairs - 1) / pairs) * nk * 512.0;
-  const double c512 = (double)((t512 + pairs - 1) / pairs) * (nk * 1024.0 / 1.1 + (c_dtype == BM_F32 ? 6144.0 : 4096.0));
+  // per-FLOP k-block speed of 256 x 512 over 256 x 256 tiles: 1.1 against 64-deep K blocks,
+  // 1.03 against the 128-deep ones (most of the gain was the halved barrier round trips
+  // per FLOP, which 128-deep blocks also get; profiles/r02/bn512/bn512_v2_knob.log)
+  const double g = g_bk128 ? 1.03 : 1.1;
+  const double c512 = (double)((t512 + pairs - 1) / pairs) * (nk * 1024.0 / g + (c_dtype == BM_F32 ? 6144.0 : 4096.0));
   return c512 < 0.98 * c256;
 }
 
@@ -1506,8 +1554,9 @@ bm_status gemm_bf16_tc(int M, int N, int K, const void* A, int64_t lda, int a_ma
     PairProblem& pr = g.prob[0];
     pr.ea = EpiArgs{M, N, K, Cp, ldc, 0, epi, R, ldr, alpha, f, 0, 1, 1 << 30, 0, g_raster_group, g_mbar_cluster};
     const bool cl4 = g_cl4 != 0;
+    const bool bk128 = g_bk128 != 0 && g_swiglu_bk128 != 0 && !cl4;
     if (a_major == 0) BM_TRY(make_map(A, K, M, lda, cl4 ? 64 : BM, &pr.tmA));
-    else BM_TRY(make_map(A, M, K, lda, BK, &pr.tmA));
+    else BM_TRY(make_map(A, M, K, lda, bk128 ? 128 : BK, &pr.tmA));
     BM_TRY(make_map(B, K, N, ldb, 128, &pr.tmB));
     if (tma_out_ok(Cp, ldc, 2) && tma_out_ok(R, ldr, 2)) {
       BM_TRY(make_map_k(Cp, 2 * (uint64_t)f, M, ldc, 32, 1, &pr.tmC));
@@ -1519,12 +1568,16 @@ bm_status gemm_bf16_tc(int M, int N, int K, const void* A, int64_t lda, int a_ma
     pr.tiles_m = ceil_div(M, 2 * BM);
     pr.tiles_n = ceil_div(f, 128);
     if (cl4) pr.tiles_n = ceil_div(pr.tiles_n, 2);   // cluster tiles: n blocks 2j, 2j + 1
-    pr.nk = ceil_div(K, BK);
+    pr.nk = ceil_div(K, bk128 ? 128 : BK);
     g.nprob = 1;
     g.tiles0 = g.total_tiles = pr.tiles_m * pr.tiles_n;
     if (cl4) {
       if (a_major == 0) return launch2<256, true, 0, 0, 4>(g, g.total_tiles, st);
       return launch2<256, true, 1, 0, 4>(g, g.total_tiles, st);
+    }
+    if (bk128) {
+      if (a_major == 0) return launch2<256, true, 0, 0, 2, 128>(g, g.total_tiles, st);
+      return launch2<256, true, 1, 0, 2, 128>(g, g.total_tiles, st);
     }
     if (a_major == 0) return launch2<256, true, 0, 0>(g, g.total_tiles, st);
     return launch2<256, true, 1, 0>(g, g.total_tiles, st);

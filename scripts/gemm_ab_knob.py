@@ -46,10 +46,11 @@ def bench(fn, flush, iters=7):
 def main():
     rounds = int(sys.argv[1]) if len(sys.argv) > 1 else 4
     knob = sys.argv[2] if len(sys.argv) > 2 else "bn512"
-    fn_knob = {"bn512": "bm_k_gemm_bn512", "cl4": "bm_k_gemm_cl4", "bk128": "bm_k_gemm_bk128"}[knob]
+    fn_knob = {"bn512": "bm_k_gemm_bn512", "cl4": "bm_k_gemm_cl4", "bk128": "bm_k_gemm_bk128",
+               "swiglu_bk128": "bm_k_gemm_swiglu_bk128"}[knob]
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     L.call("bm_k_gemm_mode", 2)
-    if knob in ("cl4", "bk128"):
+    if knob in ("cl4", "bk128", "swiglu_bk128"):
         L.call("bm_k_gemm_bn512", 2)
     for name, M, N, K, amn, bmn, epi in SHAPES:
         A = torch.randn((K, M) if amn else (M, K), device="cuda").to(torch.bfloat16)
@@ -88,7 +89,8 @@ def main():
         print(json.dumps(row), flush=True)
     L.call("bm_k_gemm_bn512", 2)
     L.call("bm_k_gemm_cl4", 0)
-    L.call("bm_k_gemm_bk128", 0)
+    L.call("bm_k_gemm_bk128", 1)
+    L.call("bm_k_gemm_swiglu_bk128", 1)
     L.call("bm_k_gemm_mode", 0)
 
 

@@ -567,3 +567,26 @@ def test_gemm_pairs_bk128(L, M, N, K, a_mn, b_mn, epi, bk):
         L.call("bm_k_gemm_bk128", 1)
         L.call("bm_k_gemm_mode", 0)
         L.call("bm_k_gemm_bn512", 2)
+
+
+@pytest.mark.parametrize("M,f,K", [(300, 384, 128), (2048, 1024, 256), (4096, 2048, 2000), (1, 128, 64)])
+@pytest.mark.parametrize("bk", [128, 64])
+def test_gemm_fused_swiglu_bk128(L, M, f, K, bk):
+    """gate/up GEMM + SwiGLU epilogue with 128-deep K blocks and 4 KB staging (default)
+    and with 64-deep blocks and 6 KB staging."""
+    L.call("bm_k_gemm_swiglu_bk128", 1 if bk == 128 else 0)
+    try:
+        rng = np.random.default_rng(3 * f + K)
+        X, Wgu = rnd(rng, M, K), rnd(rng, 2 * f, K, scale=0.1)
+        Xd, Wd = dev(X, BF16), dev(Wgu, BF16)
+        gu = torch.zeros((M, 2 * f), device="cuda", dtype=torch.bfloat16)
+        h = torch.zeros((M, f), device="cuda", dtype=torch.bfloat16)
+        L.call("bm_k_gemm_swiglu", M, f, K, Xd.data_ptr(), K, Wd.data_ptr(), K, gu.data_ptr(), h.data_ptr(), None)
+        torch.cuda.synchronize()
+        gu_ref = X @ Wgu.T
+        gu_out = host(gu)
+        assert np.all(np.abs(gu_out - gu_ref) <= 2.0 ** -8 * np.abs(gu_ref) + 1e-4 * np.sqrt(K))
+        h_ref = om.swiglu(gu_out, f)
+        assert np.abs(host(h) - h_ref).max() <= 1e-2 * max(1e-3, np.abs(h_ref).max())
+    finally:
+        L.call("bm_k_gemm_swiglu_bk128", 1)
