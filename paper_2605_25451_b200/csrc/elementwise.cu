@@ -765,7 +765,7 @@ rmsnorm_bwd_wide_kernel(int rows, int cols, int rows_per_block, const T* __restr
   const int r1 = min(rows, r0 + rows_per_block);
   int par = 0;
   for (int rb = r0; rb < r1; rb += RG, par ^= 1) {
-    V16<T> dv[RG][CH], xv[RG][CH], rv[RG][CH];
+    V16<T> dv[RG][CH], xv[RG][CH];
     float rs[RG];
 #pragma unroll
     for (int j = 0; j < RG; ++j) {
@@ -779,7 +779,6 @@ rmsnorm_bwd_wide_kernel(int rows, int cols, int rows_per_block, const T* __restr
           const int64_t off = (int64_t)row * cols + c;
           dv[j][k] = vload(dy + off);
           xv[j][k] = vload(x + off);
-          if (dres) rv[j][k] = vload(dres + off);   // with dy / x: one memory round trip per group
 #pragma unroll
           for (int i = 0; i < N; ++i) {
             const float xh = xv[j][k].get(i) * rs[j];
@@ -805,11 +804,12 @@ rmsnorm_bwd_wide_kernel(int rows, int cols, int rows_per_block, const T* __restr
         const int c = (k * 256 + threadIdx.x) * N;
         if (c < cols) {
           const int64_t off = (int64_t)row * cols + c;
-          V16<T> o;
+          V16<T> o, rv;
+          if (dres) rv = vload(dres + off);
 #pragma unroll
           for (int i = 0; i < N; ++i) {
             float v = rs[j] * (dv[j][k].get(i) * gv[k].get(i) - xv[j][k].get(i) * rs[j] * dot);
-            if (dres) v += rv[j][k].get(i);
+            if (dres) v += rv.get(i);
             o.set(i, v);
           }
           vstore(dx + off, o);
