@@ -404,9 +404,8 @@ def pacing_stage_mask(split, P, costs=None):
 
 def lightest_only_mask(costs):
     """Bits of every stage except the lightest one(s): with a half-layer partition the
-    encoder and generator run only where the LLM leaves the most room (C2, N = 4:
-    188.5 vs 180.2 samples/s for excluding only the heaviest stages,
-    profiles/r02/zb/ab_place_n4.log)."""
+    generator runs only where the LLM leaves the most room (C2, N = 4: 188.2–188.5 vs
+    180.2 samples/s for excluding only the heaviest stages, profiles/r02/zb/ab_place_n4.log)."""
     mn = min(costs)
     if max(costs) <= mn + 1e-9:
         return 0
@@ -436,6 +435,11 @@ def enc_exclude(args, cfg, P, split, strategy):
         return 0
     if args.enc_exclude != "auto":
         return sum(1 << int(r) for r in args.enc_exclude.split(","))
+    if getattr(args, "partition", "layers") == "halves":
+        # with a half-layer partition the encoder stays on every stage: it feeds the entry
+        # stage, and concentrating it costs more than the stage it unloads (C2, N = 2:
+        # 94.2 samples/s vs 90.4 with it on the lightest stage only; profiles/r02/zb/ab_n2.log)
+        return 0
     return _pacing(args, cfg, P, split)
 
 

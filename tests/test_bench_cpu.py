@@ -119,7 +119,8 @@ def test_half_layer_unit_partition():
     assert bench.pacing_stage_mask(u, 4, costs) == 0b0101
     assert bench.lightest_only_mask(costs) == 0b0111          # encoder / generator on the last stage only
     a = ns(partition="halves", gen_exclude="auto", enc_exclude="auto", head="auto")
-    assert bench.gen_exclude(a, cfg, 4, u, "bigmac") == 0b0111 == bench.enc_exclude(a, cfg, 4, u, "bigmac")
+    assert bench.gen_exclude(a, cfg, 4, u, "bigmac") == 0b0111
+    assert bench.enc_exclude(a, cfg, 4, u, "bigmac") == 0          # the encoder stays on every stage
     assert bench.pacing_stage_mask([4, 4, 5, 3], 4) == 0b0100
     assert bench.pacing_stage_mask([4, 4, 4, 4], 4) == 0
     a = ns(partition="halves", llm_sched="auto")
