@@ -148,6 +148,9 @@ def bubble_bound(cfg, P):
 # measured at C2 (profiles/r01/traces/trace_n2_m32_last_stage.summary.json: the last
 # stage's F(m) takes 4.27 ms vs 2.55 ms elsewhere for 8 layers whose F+B is 8.2 ms)
 HEAD_LAYERS = 1.7
+# encoder + generator of one C2 microbatch on the stage that runs them, in the same units
+# (N = 2 trace: ≈ 0.7 ms per microbatch next to ≈ 1.07 ms per layer fwd + bwd)
+ENC_GEN_LAYERS = 0.6
 
 
 # explicit partitions measured best at C2 (L = 16): stage 0 also runs the text
@@ -436,10 +439,14 @@ def enc_exclude(args, cfg, P, split, strategy):
     if args.enc_exclude != "auto":
         return sum(1 << int(r) for r in args.enc_exclude.split(","))
     if getattr(args, "partition", "layers") == "halves":
-        # with a half-layer partition the encoder stays on every stage: it feeds the entry
-        # stage, and concentrating it costs more than the stage it unloads (C2, N = 2:
-        # 94.2 samples/s vs 90.4 with it on the lightest stage only; profiles/r02/zb/ab_n2.log)
-        return 0
+        # the encoder joins the generator on the lightest stage only when that stage has
+        # room for both (slack >= ENC_GEN_LAYERS): C2 N = 4 (slack 0.64) 188.5 vs 180.9
+        # samples/s with it everywhere; C2 N = 2 (slack 0.3) 94.2 everywhere vs 90.4
+        # (profiles/r02/zb/ab_place_n4.log, ab_n2.log, final/bench_n4_final.log)
+        if not split or len(split) != P:
+            return 0
+        costs = unit_costs(cfg, split)
+        return lightest_only_mask(costs) if max(costs) - min(costs) >= ENC_GEN_LAYERS else 0
     return _pacing(args, cfg, P, split)
 
 

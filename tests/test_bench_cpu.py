@@ -120,7 +120,11 @@ def test_half_layer_unit_partition():
     assert bench.lightest_only_mask(costs) == 0b0111          # encoder / generator on the last stage only
     a = ns(partition="halves", gen_exclude="auto", enc_exclude="auto", head="auto")
     assert bench.gen_exclude(a, cfg, 4, u, "bigmac") == 0b0111
-    assert bench.enc_exclude(a, cfg, 4, u, "bigmac") == 0          # the encoder stays on every stage
+    assert bench.enc_exclude(a, cfg, 4, u, "bigmac") == 0b0111     # slack 0.64 >= ENC_GEN_LAYERS
+    c2 = get_config("C2", P=2, M=32)
+    u2 = bench.unit_partition(c2, 2)
+    assert bench.enc_exclude(a, c2, 2, u2, "bigmac") == 0           # slack 0.3: the encoder stays everywhere
+    assert bench.gen_exclude(a, c2, 2, u2, "bigmac") == 0b01
     assert bench.pacing_stage_mask([4, 4, 5, 3], 4) == 0b0100
     assert bench.pacing_stage_mask([4, 4, 4, 4], 4) == 0
     a = ns(partition="halves", llm_sched="auto")
