@@ -95,10 +95,6 @@ bm_status bm_k_gemm_mode(int32_t mode);
  * whenever N >= 512 (one 512-column accumulator; a quarter less L2 -> SMEM traffic
  * per FLOP), 2 = auto (256 x 512 when N >= 512 and K >= 4096).  Process-wide. */
 bm_status bm_k_gemm_bn512(int32_t mode);
-/* 1: single-problem 256 x 256 CTA-pair GEMMs run as clusters of two pairs (four CTAs)
- * that share the A tile by TMA multicast (each CTA loads half of its 128 A rows for
- * both pairs); 0 (default): one pair per cluster.  Process-wide. */
-bm_status bm_k_gemm_cl4(int32_t on);
 /* 1 (default): 256 x 256 CTA-pair GEMMs step K in 128-deep blocks (two 64-wide
  * swizzled sub-tiles per operand, three 64 KB stages); 0: 64-deep blocks, six
  * stages.  Process-wide. */

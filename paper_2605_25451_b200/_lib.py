@@ -135,7 +135,6 @@ SIGNATURES = {
     "bm_k_gemm": [_I32, _I32, _I32, _I32, _P, _I64, _I32, _P, _I64, _I32, _P, _I64, _I32, _I32, _P, _I64, _F, _P],
     "bm_k_gemm_mode": [_I32],
     "bm_k_gemm_bn512": [_I32],
-    "bm_k_gemm_cl4": [_I32],
     "bm_k_gemm_bk128": [_I32],
     "bm_k_gemm_swiglu_bk128": [_I32],
     "bm_k_gemm_group": [C.POINTER(GemmDesc), _I32, _P],

@@ -205,22 +205,12 @@ __device__ __forceinline__ void umma_f16_pair(uint32_t tmem_d, uint64_t adesc, u
       "}\n" ::"r"(tmem_d),
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum));
 }
-// ... multicast to the CTAs in `mask` (the same smem offset in each); the completion is
-// signalled on each destination's pair-leader barrier (cluster of two pairs)
-__device__ __forceinline__ void tma_load_2d_pair_mc(void* dst, const CUtensorMap* map, uint32_t leader_bar, int c0,
-                                                    int c1, uint16_t mask) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
-      " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(leader_bar), "r"(c0), "r"(c1), "h"(mask)
-      : "memory");
-}
-// commit: arrive on the barrier at the same offset in every CTA of `mask` (default: the pair)
-__device__ __forceinline__ void umma_commit_pair(uint64_t* bar, uint16_t mask = 0x3) {
+// commit: arrive on the barrier at the same offset in both CTAs of the pair
+__device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {
   asm volatile(
       "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
           smem_u32(bar)),
-      "h"(mask)
+      "h"((uint16_t)0x3)
       : "memory");
 }
 
@@ -917,15 +907,12 @@ __device__ __forceinline__ void store_dswiglu_tma(const EpiArgs& a, const CUtens
 
 // AM / BM_: operand majors fixed at compile time (0 K-major, 1 MN-major) for
 // single-problem launches, or -1: read per problem at run time (grouped launches)
-// CL = 2: one CTA pair per cluster.  CL = 4: two pairs per cluster walk the same
-// "cluster tiles" (one m block, n blocks 2j and 2j + 1) in lockstep and share A: each
-// CTA loads 64 of its 128 A rows and multicasts them to its counterpart in the other
-// pair (a quarter less L2 -> SMEM traffic per FLOP, keeping the two TMEM accumulators);
-// a stage is free when both pairs' MMAs have read it (empty barriers count two commits).
-template <int BN, bool SWIGLU, int AM = -1, int BMJ = -1, int CL = 2, int BKP = 64>
-__global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NUM_THREADS2, 1)
+// (Clusters of two pairs sharing A by TMA multicast were built, parity-tested and
+// measured 8-12 % slower -- DESIGN.md §7 -- and removed.)
+template <int BN, bool SWIGLU, int AM = -1, int BMJ = -1, int BKP = 64>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS2, 1)
 gemm2_kernel(const __grid_constant__ PairGroup g) {
-  static_assert(BKP == 64 || (BN == 256 && CL == 2), "BKP = 128: 256 x 256 pair tiles, one pair per cluster");
+  static_assert(BKP == 64 || BN == 256, "BKP = 128: 256 x 256 pair tiles");
   constexpr int NSUB = BKP / 64;   // 64-wide swizzle sub-tiles per K block
   using C = Cfg2<BN, SWIGLU, BKP>;
   constexpr int STAGES = C::STAGES;
@@ -941,22 +928,16 @@ gemm2_kernel(const __grid_constant__ PairGroup g) {
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
-  const uint32_t crank = cluster_rank();
-  const uint32_t cta = crank & 1;          // CTA within its pair
-  const uint32_t pq = crank >> 1;          // pair within the cluster (CL = 4)
-  const uint32_t lead = crank & ~1u;       // the pair leader's cluster rank
+  const uint32_t cta = cluster_rank();     // CTA within the pair
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
-  // work-list index: the pair (CL = 2) or the cluster (CL = 4, both pairs share it)
-  const int pair = blockIdx.x / CL, npairs = gridDim.x / CL;
+  const int pair = blockIdx.x / 2, npairs = gridDim.x / 2;
   const int mbc = g.prob[0].ea.mbar_cluster;
-  const uint16_t pair_mask = (uint16_t)(0x3u << (2 * pq));
-  const uint16_t mc_mask = (uint16_t)((1u << crank) | (1u << (crank ^ 2u)));   // CL = 4: A multicast
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], CL / 2);
+      mbar_init(&empty[s], 1);
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull[s], 1);
@@ -995,22 +976,17 @@ gemm2_kernel(const __grid_constant__ PairGroup g) {
         const bool amn = AM >= 0 ? AM != 0 : pr.a_mn != 0, bmn = BMJ >= 0 ? BMJ != 0 : pr.b_mn != 0;
         int mb, nb;
         tile_coords(t, pr.tiles_m, pr.tiles_n, mb, nb, pr.ea.group);
-        if (CL == 4) nb = 2 * nb + (int)pq;   // cluster tile -> this pair's n block
         const int m0 = mb * 2 * BM + (int)cta * BM;
         // SwiGLU pairing: CTA 0 loads gate rows [nb*BNH, +BNH), CTA 1 the matching up rows
         const int n0 = SWIGLU ? (nb * BNH + (int)cta * pr.ea.f) : (nb * BN + (int)cta * BNH);
         for (int kb = 0; kb < nk; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1, mbc);
           if (cta == 0) mbar_expect_tx(&full[stage], 2 * C::STAGE_BYTES);
-          const uint32_t lbar = mapa(smem_u32(&full[stage]), lead);
+          const uint32_t lbar = mapa(smem_u32(&full[stage]), 0);
           uint8_t* a_dst = smA + stage * C::A_BYTES;
           uint8_t* b_dst = smB + stage * C::B_BYTES;
           const int k0 = kb * BKP;
-          if (CL == 4) {
-            // rows [64 pq, +64) of this CTA's A half, to itself and its counterpart
-            if (amn) tma_load_2d_pair_mc(a_dst + pq * (BK * 128), mA, lbar, m0 + 64 * (int)pq, k0, mc_mask);
-            else tma_load_2d_pair_mc(a_dst + pq * (64 * 128), mA, lbar, k0, m0 + 64 * (int)pq, mc_mask);
-          } else if (amn) {
+          if (amn) {
 #pragma unroll
             for (int j = 0; j < BM / 64; ++j) tma_load_2d_pair(a_dst + j * (BKP * 128), mA, lbar, m0 + 64 * j, k0);
           } else {
@@ -1077,10 +1053,10 @@ gemm2_kernel(const __grid_constant__ PairGroup g) {
               umma_f16_pair(tmem_d + h * 256, ad, bd, idesc, (kb != 0 || kk != 0) ? 1u : 0u);
             }
           }
-          umma_commit_pair(&empty[stage], CL == 4 ? (uint16_t)0xF : pair_mask);
+          umma_commit_pair(&empty[stage]);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
-        umma_commit_pair(&tfull[acc], pair_mask);
+        umma_commit_pair(&tfull[acc]);
       }
     }
   } else {
@@ -1090,8 +1066,8 @@ gemm2_kernel(const __grid_constant__ PairGroup g) {
     const uint32_t slot0 = smem_u32(smE) + (uint32_t)((warp - 2) * C::NSLOT * C::EPI_SLOT);
     uint32_t slot = slot0;
     int eiter = 0;
-    const uint32_t leader_tempty0 = mapa(smem_u32(&tempty[0]), lead);
-    const uint32_t leader_tempty1 = mapa(smem_u32(&tempty[1]), lead);
+    const uint32_t leader_tempty0 = mapa(smem_u32(&tempty[0]), 0);
+    const uint32_t leader_tempty1 = mapa(smem_u32(&tempty[1]), 0);
     int local = 0;
     PairIter it(g, pair, npairs);
     int pi, t;
@@ -1102,7 +1078,6 @@ gemm2_kernel(const __grid_constant__ PairGroup g) {
       const CUtensorMap* mC2 = &pr.tmC2;
       int mb, nb;
       tile_coords(t, pr.tiles_m, pr.tiles_n, mb, nb, ea.group);
-      if (CL == 4) nb = 2 * nb + (int)pq;
       const int acc = C::NACC == 2 ? (local & 1) : 0;
       const uint32_t acc_phase = C::NACC == 2 ? ((local >> 1) & 1) : (local & 1);
       const int row0 = mb * 2 * BM + (int)cta * BM + quad * 32;
@@ -1360,39 +1335,30 @@ static bm_status dispatch_majors(bool a_mn, bool b_mn, const CUtensorMap& ma, co
 }
 
 
-template <int BN, bool SWIGLU = false, int AM = -1, int BMJ = -1, int CL = 2, int BKP = 64>
+template <int BN, bool SWIGLU = false, int AM = -1, int BMJ = -1, int BKP = 64>
 static bm_status launch2(const PairGroup& g, int tiles, cudaStream_t st) {
   using C = Cfg2<BN, SWIGLU, BKP>;
   static bool attr_set = false;
-  static int max_clusters = 0;   // CL = 4: clusters of two pairs that fit at once (GPC shapes)
   if (!attr_set) {
-    BM_CUDA_TRY(cudaFuncSetAttribute(gemm2_kernel<BN, SWIGLU, AM, BMJ, CL, BKP>,
+    BM_CUDA_TRY(cudaFuncSetAttribute(gemm2_kernel<BN, SWIGLU, AM, BMJ, BKP>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
-    if (CL == 4) {
-      cudaLaunchConfig_t cfg = {};
-      cfg.gridDim = dim3(num_sms() / 4 * 4);
-      cfg.blockDim = dim3(NUM_THREADS2);
-      cfg.dynamicSmemBytes = C::SMEM;
-      BM_CUDA_TRY(cudaOccupancyMaxActiveClusters(&max_clusters, gemm2_kernel<BN, SWIGLU, AM, BMJ, CL, BKP>, &cfg));
-    }
     attr_set = true;
   }
-  // tiles = work items: pair tiles (CL = 2) or cluster tiles (CL = 4)
-  const int slots = CL == 4 ? std::min(max_clusters, gemm_sm_budget() / 4) : gemm_sm_budget() / 2;
-  const int grid = CL * (tiles < slots ? tiles : std::max(slots, 1));
-  BM_CUDA_TRY(launch_k(gemm2_kernel<BN, SWIGLU, AM, BMJ, CL, BKP>, dim3(grid), dim3(NUM_THREADS2), C::SMEM, st, g));
+  const int pairs = gemm_sm_budget() / 2;
+  const int grid = 2 * (tiles < pairs ? tiles : pairs);
+  BM_CUDA_TRY(launch_k(gemm2_kernel<BN, SWIGLU, AM, BMJ, BKP>, dim3(grid), dim3(NUM_THREADS2), C::SMEM, st, g));
   count_launch();
   BM_CUDA_TRY(cudaGetLastError());
   return BM_OK;
 }
 // single-problem launch with the operand majors as template constants
-template <int BN, int CL = 2, int BKP = 64>
+template <int BN, int BKP = 64>
 static bm_status launch2_static(const PairGroup& g, int tiles, cudaStream_t st) {
   const int a = g.prob[0].a_mn, b = g.prob[0].b_mn;
-  if (!a && !b) return launch2<BN, false, 0, 0, CL, BKP>(g, tiles, st);
-  if (!a && b) return launch2<BN, false, 0, 1, CL, BKP>(g, tiles, st);
-  if (a && b) return launch2<BN, false, 1, 1, CL, BKP>(g, tiles, st);
-  return launch2<BN, false, 1, 0, CL, BKP>(g, tiles, st);
+  if (!a && !b) return launch2<BN, false, 0, 0, BKP>(g, tiles, st);
+  if (!a && b) return launch2<BN, false, 0, 1, BKP>(g, tiles, st);
+  if (a && b) return launch2<BN, false, 1, 1, BKP>(g, tiles, st);
+  return launch2<BN, false, 1, 0, BKP>(g, tiles, st);
 }
 
 }  // namespace tc
@@ -1460,13 +1426,7 @@ static int g_bn512 = [] {
   return e ? atoi(e) : 2;
 }();
 void set_gemm_bn512(int m) { g_bn512 = m; }
-// clusters of two CTA pairs sharing A by TMA multicast (BM_GEMM_CL4=1) for single-problem
-// 256 x 256 pair launches
-static int g_cl4 = [] {
-  const char* e = getenv("BM_GEMM_CL4");
-  return e ? atoi(e) : 0;
-}();
-void set_gemm_cl4(int m) { g_cl4 = m; }
+
 
 // ... for the SwiGLU-forward kernel too (default; three 64 KB stages, 4 KB epilogue
 // staging per warp, [g | u] and h stored one after the other): standalone +5.9 % (C2) /
@@ -1553,9 +1513,8 @@ bm_status gemm_bf16_tc(int M, int N, int K, const void* A, int64_t lda, int a_ma
     std::memset(&g, 0, sizeof(g));
     PairProblem& pr = g.prob[0];
     pr.ea = EpiArgs{M, N, K, Cp, ldc, 0, epi, R, ldr, alpha, f, 0, 1, 1 << 30, 0, g_raster_group, g_mbar_cluster};
-    const bool cl4 = g_cl4 != 0;
-    const bool bk128 = g_bk128 != 0 && g_swiglu_bk128 != 0 && !cl4;
-    if (a_major == 0) BM_TRY(make_map(A, K, M, lda, cl4 ? 64 : BM, &pr.tmA));
+    const bool bk128 = g_bk128 != 0 && g_swiglu_bk128 != 0;
+    if (a_major == 0) BM_TRY(make_map(A, K, M, lda, BM, &pr.tmA));
     else BM_TRY(make_map(A, M, K, lda, bk128 ? 128 : BK, &pr.tmA));
     BM_TRY(make_map(B, K, N, ldb, 128, &pr.tmB));
     if (tma_out_ok(Cp, ldc, 2) && tma_out_ok(R, ldr, 2)) {
@@ -1567,17 +1526,12 @@ bm_status gemm_bf16_tc(int M, int N, int K, const void* A, int64_t lda, int a_ma
     pr.b_mn = 0;
     pr.tiles_m = ceil_div(M, 2 * BM);
     pr.tiles_n = ceil_div(f, 128);
-    if (cl4) pr.tiles_n = ceil_div(pr.tiles_n, 2);   // cluster tiles: n blocks 2j, 2j + 1
     pr.nk = ceil_div(K, bk128 ? 128 : BK);
     g.nprob = 1;
     g.tiles0 = g.total_tiles = pr.tiles_m * pr.tiles_n;
-    if (cl4) {
-      if (a_major == 0) return launch2<256, true, 0, 0, 4>(g, g.total_tiles, st);
-      return launch2<256, true, 1, 0, 4>(g, g.total_tiles, st);
-    }
     if (bk128) {
-      if (a_major == 0) return launch2<256, true, 0, 0, 2, 128>(g, g.total_tiles, st);
-      return launch2<256, true, 1, 0, 2, 128>(g, g.total_tiles, st);
+      if (a_major == 0) return launch2<256, true, 0, 0, 128>(g, g.total_tiles, st);
+      return launch2<256, true, 1, 0, 128>(g, g.total_tiles, st);
     }
     if (a_major == 0) return launch2<256, true, 0, 0>(g, g.total_tiles, st);
     return launch2<256, true, 1, 0>(g, g.total_tiles, st);
@@ -1594,13 +1548,7 @@ bm_status gemm_bf16_tc(int M, int N, int K, const void* A, int64_t lda, int a_ma
     BM_TRY(pair_problem(M, N, K, A, lda, a_major, B, ldb, b_major, Cp, ldc, c_dtype, epi, R, ldr, alpha, f, BN2,
                         &g.prob[0]));
     g.nprob = 1;
-    const bool cl4 = g_cl4 != 0 && BN2 == 256;
-    if (cl4) {   // cluster tiles of two n blocks; A loaded as 64-row multicast halves
-      PairProblem& pr = g.prob[0];
-      pr.tiles_n = ceil_div(pr.tiles_n, 2);
-      if (a_major == 0) BM_TRY(make_map(A, K, M, lda, 64, &pr.tmA));
-    }
-    const bool bk128 = g_bk128 != 0 && BN2 == 256 && !cl4;
+    const bool bk128 = g_bk128 != 0 && BN2 == 256;
     if (bk128) {   // MN-major operands as 64 x 128 boxes; 128-deep K blocks
       PairProblem& pr = g.prob[0];
       if (a_major != 0) BM_TRY(make_map(A, M, K, lda, 128, &pr.tmA));
@@ -1608,8 +1556,7 @@ bm_status gemm_bf16_tc(int M, int N, int K, const void* A, int64_t lda, int a_ma
       pr.nk = ceil_div(K, 128);
     }
     g.tiles0 = g.total_tiles = g.prob[0].tiles_m * g.prob[0].tiles_n;
-    if (cl4) return launch2_static<256, 4>(g, g.total_tiles, st);
-    if (bk128) return launch2_static<256, 2, 128>(g, g.total_tiles, st);
+    if (bk128) return launch2_static<256, 128>(g, g.total_tiles, st);
     if (BN2 == 512) return launch2_static<512>(g, g.total_tiles, st);
     if (BN2 == 256) return launch2_static<256>(g, g.total_tiles, st);
     return launch2_static<128>(g, g.total_tiles, st);

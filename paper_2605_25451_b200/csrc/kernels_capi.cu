@@ -110,7 +110,7 @@ using namespace bm;
     return BM_E_INVALID;                                      \
   } while (0)
 
-namespace bm { void set_gemm_mode(int m); void set_gemm_bn512(int m); void set_gemm_cl4(int m); void set_gemm_bk128(int m); void set_gemm_swiglu_bk128(int m); }
+namespace bm { void set_gemm_mode(int m); void set_gemm_bn512(int m); void set_gemm_bk128(int m); void set_gemm_swiglu_bk128(int m); }
 
 extern "C" {
 
@@ -137,12 +137,6 @@ bm_status bm_k_gemm_bk128(int32_t on) {
 bm_status bm_k_gemm_swiglu_bk128(int32_t on) {
   BM_CHECK_ARG(on == 0 || on == 1, "on must be 0 or 1");
   bm::set_gemm_swiglu_bk128(on);
-  return BM_OK;
-}
-
-bm_status bm_k_gemm_cl4(int32_t on) {
-  BM_CHECK_ARG(on == 0 || on == 1, "on must be 0 or 1");
-  bm::set_gemm_cl4(on);
   return BM_OK;
 }
 

@@ -3,8 +3,8 @@ over several rounds in one process (CUDA events, L2 flushed between iterations);
 prints per shape the median TF/s over rounds of each setting.
 
     python scripts/gemm_ab_knob.py [rounds] [knob]
-knob: bn512 (bm_k_gemm_bn512 0 = 256x256 vs 1 = 256x512; default) or cl4
-(bm_k_gemm_cl4 0 vs 1, with the production bn512 auto policy)
+knob: bn512 (bm_k_gemm_bn512 0 = 256x256 vs 1 = 256x512; default), bk128 or
+swiglu_bk128 (0 vs 1, with the production bn512 auto policy)
 """
 import json
 import os
@@ -46,11 +46,11 @@ def bench(fn, flush, iters=7):
 def main():
     rounds = int(sys.argv[1]) if len(sys.argv) > 1 else 4
     knob = sys.argv[2] if len(sys.argv) > 2 else "bn512"
-    fn_knob = {"bn512": "bm_k_gemm_bn512", "cl4": "bm_k_gemm_cl4", "bk128": "bm_k_gemm_bk128",
+    fn_knob = {"bn512": "bm_k_gemm_bn512", "bk128": "bm_k_gemm_bk128",
                "swiglu_bk128": "bm_k_gemm_swiglu_bk128"}[knob]
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     L.call("bm_k_gemm_mode", 2)
-    if knob in ("cl4", "bk128", "swiglu_bk128"):
+    if knob in ("bk128", "swiglu_bk128"):
         L.call("bm_k_gemm_bn512", 2)
     for name, M, N, K, amn, bmn, epi in SHAPES:
         A = torch.randn((K, M) if amn else (M, K), device="cuda").to(torch.bfloat16)
@@ -88,7 +88,6 @@ def main():
         row["gain"] = round(row["tf_1"] / row["tf_0"] - 1, 4)
         print(json.dumps(row), flush=True)
     L.call("bm_k_gemm_bn512", 2)
-    L.call("bm_k_gemm_cl4", 0)
     L.call("bm_k_gemm_bk128", 1)
     L.call("bm_k_gemm_swiglu_bk128", 1)
     L.call("bm_k_gemm_mode", 0)

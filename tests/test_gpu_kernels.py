@@ -426,84 +426,6 @@ def test_gemm_dswiglu_bn512(L, M, f, Kd):
         L.call("bm_k_gemm_bn512", 2)
 
 
-@pytest.mark.parametrize("M,N,K", [(512, 512, 64), (2560, 2048, 512), (1000, 1000, 640), (4096, 2304, 1024),
-                                   (304, 1280, 200)])
-@pytest.mark.parametrize("a_mn,b_mn", [(0, 0), (0, 1), (1, 1), (1, 0)])
-@pytest.mark.parametrize("epi", ["f32_store", "bf16_add", "f32_accum"])
-def test_gemm_pairs_cluster4(L, M, N, K, a_mn, b_mn, epi):
-    """Clusters of two CTA pairs sharing A by TMA multicast (bm_k_gemm_cl4): every
-    operand major, odd tile columns (the second pair of the last cluster tile runs
-    off the matrix), ragged shapes, three epilogues; bitwise equal to a rerun."""
-    L.call("bm_k_gemm_mode", 2)
-    L.call("bm_k_gemm_bn512", 0)
-    L.call("bm_k_gemm_cl4", 1)
-    try:
-        rng = np.random.default_rng(M + 5 * N + K + 7 * a_mn + b_mn)
-        A, B, R = rnd(rng, M, K), rnd(rng, N, K), rnd(rng, M, N)
-        Ad = dev(A.T.copy() if a_mn else A, BF16)
-        Bd = dev(B.T.copy() if b_mn else B, BF16)
-        ref = A @ B.T * 0.5
-        outs = []
-        for _ in range(2):
-            if epi == "f32_store":
-                C = torch.full((M, N), 7.0, device="cuda", dtype=torch.float32)
-                args = (C.data_ptr(), N, F32, 0, None, 0)
-            elif epi == "bf16_add":
-                C = torch.zeros((M, N), device="cuda", dtype=torch.bfloat16)
-                Rd = dev(R, BF16)
-                args = (C.data_ptr(), N, BF16, 2, Rd.data_ptr(), N)
-            else:
-                C = dev(R, F32)
-                args = (C.data_ptr(), N, F32, 1, None, 0)
-            L.call("bm_k_gemm", BF16, M, N, K, Ad.data_ptr(), M if a_mn else K, a_mn, Bd.data_ptr(),
-                   N if b_mn else K, b_mn, *args, 0.5, None)
-            torch.cuda.synchronize()
-            outs.append(C)
-        out = host(outs[0])
-        if epi != "f32_store":
-            ref = ref + R
-        if epi == "bf16_add":
-            assert np.all(np.abs(out - ref) <= 2.0 ** -8 * np.abs(ref) + 1e-4 * np.sqrt(K))
-        else:
-            assert np.abs(out - ref).max() <= 1e-5 * np.sqrt(K) * max(1.0, np.abs(ref).max())
-        assert torch.equal(outs[0], outs[1])
-    finally:
-        L.call("bm_k_gemm_cl4", 0)
-        L.call("bm_k_gemm_mode", 0)
-        L.call("bm_k_gemm_bn512", 2)
-
-
-@pytest.mark.parametrize("M,f,K", [(300, 384, 128), (2048, 1024, 256), (4096, 2048, 2048)])
-def test_gemm_fused_swiglu_cluster4(L, M, f, K):
-    """gate/up + SwiGLU and down dgrad + SwiGLU backward on two-pair clusters."""
-    L.call("bm_k_gemm_mode", 2)
-    L.call("bm_k_gemm_cl4", 1)
-    try:
-        rng = np.random.default_rng(f + K)
-        X, Wgu = rnd(rng, M, K), rnd(rng, 2 * f, K, scale=0.1)
-        Xd, Wd = dev(X, BF16), dev(Wgu, BF16)
-        gu = torch.zeros((M, 2 * f), device="cuda", dtype=torch.bfloat16)
-        h = torch.zeros((M, f), device="cuda", dtype=torch.bfloat16)
-        L.call("bm_k_gemm_swiglu", M, f, K, Xd.data_ptr(), K, Wd.data_ptr(), K, gu.data_ptr(), h.data_ptr(), None)
-        Kd = 512
-        dY, Wdown = rnd(rng, M, Kd), rnd(rng, Kd, f, scale=0.1)
-        dYd, Wdd = dev(dY, BF16), dev(Wdown, BF16)
-        dgu = torch.zeros((M, 2 * f), device="cuda", dtype=torch.bfloat16)
-        L.call("bm_k_gemm_dswiglu", M, f, Kd, dYd.data_ptr(), Kd, Wdd.data_ptr(), f, gu.data_ptr(), dgu.data_ptr(),
-               None)
-        torch.cuda.synchronize()
-        gu_ref = X @ Wgu.T
-        gu_out = host(gu)
-        assert np.all(np.abs(gu_out - gu_ref) <= 2.0 ** -8 * np.abs(gu_ref) + 1e-4 * np.sqrt(K))
-        h_ref = om.swiglu(gu_out, f)
-        assert np.abs(host(h) - h_ref).max() <= 1e-2 * max(1e-3, np.abs(h_ref).max())
-        dgu_ref = om.swiglu_bwd(dY @ Wdown, gu_out, f)
-        assert np.abs(host(dgu) - dgu_ref).max() <= 1e-2 * max(1e-3, np.abs(dgu_ref).max())
-    finally:
-        L.call("bm_k_gemm_cl4", 0)
-        L.call("bm_k_gemm_mode", 0)
-
-
 @pytest.mark.parametrize("M,N,K", [(512, 512, 64), (2560, 2048, 512), (1000, 1000, 640), (4096, 2304, 1000),
                                    (304, 1280, 200)])
 @pytest.mark.parametrize("a_mn,b_mn", [(0, 0), (0, 1), (1, 1), (1, 0)])
