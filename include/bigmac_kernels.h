@@ -93,7 +93,9 @@ bm_status bm_k_gemm_mode(int32_t mode);
 /* Pair-tile width of the CTA-pair GEMM: 0 = 256 x 256 tiles (two TMEM accumulators,
  * the epilogue of one tile overlaps the next tile's MMAs), 1 = 256 x 512 tiles
  * whenever N >= 512 (one 512-column accumulator; a quarter less L2 -> SMEM traffic
- * per FLOP), 2 = auto (256 x 512 when N >= 512 and K >= 4096).  Process-wide. */
+ * per FLOP), 2 = auto (default: a wave-quantised cost model picks 256 x 512 where
+ * its per-FLOP gain beats the un-overlapped epilogue and the coarser last wave,
+ * never for the SwiGLU-backward epilogue; gemm_tc.cu use_bn512).  Process-wide. */
 bm_status bm_k_gemm_bn512(int32_t mode);
 /* 1 (default): 256 x 256 CTA-pair GEMMs step K in 128-deep blocks (two 64-wide
  * swizzled sub-tiles per operand, three 64 KB stages); 0: 64-deep blocks, six
