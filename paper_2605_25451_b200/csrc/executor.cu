@@ -2389,7 +2389,7 @@ bm_status bm_step(bm_ctx* c, const bm_batch* b, void* stream) {
 // first unmet wait of this rank's step `stp` (op order), read from a host copy of its flags
 static std::string blocked_op(const bm_ctx& c, int64_t stp, const std::vector<uint32_t>& fl) {
   static const char* PN[] = {"act", "grad", "emb", "embgrad", "genin", "gengrad"};
-  static const char* KN[] = {"EncFwd", "EncBwd", "LlmFwd", "LlmBwd", "GenFwd", "GenBwd", "Send", "Recv"};
+  static const char* KN[] = {"EncFwd", "EncBwd", "LlmFwd", "LlmBwd", "GenFwd", "GenBwd", "Send", "Recv", "LlmW"};
   const auto& ops = c.s->ranks[c.rank];
   for (size_t i = 0; i < ops.size(); ++i) {
     const bm_op& o = ops[i];
