@@ -596,6 +596,7 @@ def main():
                                                              "replica at N > 1) and the batch sweep")
     ap.add_argument("--sweep", default="8,16,32,64,128,256", help="global batches of the peak-HBM sweep ('' = off)")
     ap.add_argument("--c4-steps", type=int, default=2)
+    ap.add_argument("--no-c4-strong", action="store_true", help="skip the C4 strong-scaling line at N > 1")
     ap.add_argument("--ref-layers", type=int, default=1, help="LLM layers of the oracle sample")
     ap.add_argument("--ref-seq-div", type=int, default=1, help="the oracle sample runs S / this positions (1: the full sequence)")
     ap.add_argument("--head", default="auto", choices=["auto", "last_stage", "dp_shard"],
@@ -731,6 +732,11 @@ def main():
             # BASELINE.json configs[1]: 16 microbatches per pipeline (global batch 16 D)
             c2 = get_config("C2", P=P, M=16, V=1)
             extra["c2_m16_per_replica"] = run_secondary(args, cx, rank, world, "C2", c2, P, D, max(3, args.steps // 2), 3)
+        if N > 1 and args.config == "C2" and not args.microbatches and not args.no_c4_strong:
+            # SURVEY §8(d) strong-scaling ladder: the C4 model (7B-shaped LLM, S = 8192) at
+            # P = min(N, 4) stages x D replicas over one global batch of 64 microbatches
+            c4 = get_config("C4", P=P, M=64 // D, V=1)
+            extra["c4_strong"] = run_secondary(args, cx, rank, world, "C4", c4, P, D, 2, 2, with_bubble=False)
         if N > 1 and cfg.V == 1 and cfg.llm_sched != "zb_h1":
             # the same workload on the ZB-H1 zero-bubble base schedule (reading R23)
             extra["zb_h1"] = run_secondary(args, cx, rank, world, cfg.name, cfg.replace(llm_sched="zb_h1"), P, D,
