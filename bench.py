@@ -598,7 +598,7 @@ def main():
     ap.add_argument("--c4-steps", type=int, default=2)
     ap.add_argument("--no-c4-strong", action="store_true", help="skip the C4 strong-scaling line at N > 1")
     ap.add_argument("--ref-layers", type=int, default=1, help="LLM layers of the oracle sample")
-    ap.add_argument("--ref-seq-div", type=int, default=1, help="the oracle sample runs S / this positions (1: the full sequence)")
+    ap.add_argument("--ref-seq-div", type=int, default=2, help="the oracle sample runs S / this positions")
     ap.add_argument("--head", default="auto", choices=["auto", "last_stage", "dp_shard"],
                     help="LM head + CE placement (bigmac.h bm_head_place): auto = last_stage (the paper's "
                          "Megatron placement), dp_shard = DP-sharded with the generator")
