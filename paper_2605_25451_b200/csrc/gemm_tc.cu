@@ -792,9 +792,7 @@ constexpr int NUM_THREADS2 = 64 + 32 * EPI_WARPS2;
 // single TMEM accumulator (512 columns): the MMA waits for the epilogue between tiles
 // BKP = 128: 128-deep K blocks (two 64-wide swizzle sub-tiles per operand, 64 KB stages,
 // 3 stages) -- twice the MMAs per barrier round trip, same bytes per FLOP.
-// NS2: two epilogue staging slots per warp (a chunk's TMA stores read one while the next
-// chunk is staged in the other) with as many stages as still fit
-template <int BN, bool SWI = false, int BKP = 64, bool NS2 = false> struct Cfg2 {
+template <int BN, bool SWI = false, int BKP = 64> struct Cfg2 {
   static constexpr int A_BYTES = 128 * BKP * 2;                // 16 KB (BKP = 64)
   static constexpr int B_BYTES = (BN / 2) * BKP * 2;           // 16 KB (BN = 256), 32 KB (BN = 512)
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
@@ -802,9 +800,8 @@ template <int BN, bool SWI = false, int BKP = 64, bool NS2 = false> struct Cfg2 
   // next chunk is staged in the other (wait_group.read 1); with 1, read 0
   // (measured: 2 slots with 5 stages gains 1.5 % on the SwiGLU-backward dgrad and
   // loses 3-4 % on the fp32 wgrads, so the non-SwiGLU kernels keep 1 slot, 6 stages)
-  static constexpr int NSLOT = NS2 ? 2 : 1;
-  static constexpr int STAGES = NS2 ? (BKP == 128 ? 2 : 5)
-                                    : (SWI ? (BKP == 128 ? 3 : 5) : (BKP == 128 ? 3 : (BN == 512 ? 4 : ((BN == 256) ? 6 : 8))));
+  static constexpr int NSLOT = 1;
+  static constexpr int STAGES = SWI ? (BKP == 128 ? 3 : 5) : (BKP == 128 ? 3 : (BN == 512 ? 4 : ((BN == 256) ? 6 : 8)));
   static constexpr int NACC = BN == 512 ? 1 : 2;               // TMEM accumulator buffers
   static constexpr int TMEM_COLS = NACC * BN;
   static constexpr int EPI_SLOT = (SWI && BKP == 64) ? 6144 : 4096;   // staging slot of one epilogue warp
@@ -912,12 +909,12 @@ __device__ __forceinline__ void store_dswiglu_tma(const EpiArgs& a, const CUtens
 // single-problem launches, or -1: read per problem at run time (grouped launches)
 // (Clusters of two pairs sharing A by TMA multicast were built, parity-tested and
 // measured 8-12 % slower -- DESIGN.md §7 -- and removed.)
-template <int BN, bool SWIGLU, int AM = -1, int BMJ = -1, int BKP = 64, bool NS2 = false>
+template <int BN, bool SWIGLU, int AM = -1, int BMJ = -1, int BKP = 64>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS2, 1)
 gemm2_kernel(const __grid_constant__ PairGroup g) {
   static_assert(BKP == 64 || BN == 256, "BKP = 128: 256 x 256 pair tiles");
   constexpr int NSUB = BKP / 64;   // 64-wide swizzle sub-tiles per K block
-  using C = Cfg2<BN, SWIGLU, BKP, NS2>;
+  using C = Cfg2<BN, SWIGLU, BKP>;
   constexpr int STAGES = C::STAGES;
   constexpr int BNH = BN / 2;
   extern __shared__ uint8_t smem_raw[];
@@ -1338,18 +1335,18 @@ static bm_status dispatch_majors(bool a_mn, bool b_mn, const CUtensorMap& ma, co
 }
 
 
-template <int BN, bool SWIGLU = false, int AM = -1, int BMJ = -1, int BKP = 64, bool NS2 = false>
+template <int BN, bool SWIGLU = false, int AM = -1, int BMJ = -1, int BKP = 64>
 static bm_status launch2(const PairGroup& g, int tiles, cudaStream_t st) {
-  using C = Cfg2<BN, SWIGLU, BKP, NS2>;
+  using C = Cfg2<BN, SWIGLU, BKP>;
   static bool attr_set = false;
   if (!attr_set) {
-    BM_CUDA_TRY(cudaFuncSetAttribute(gemm2_kernel<BN, SWIGLU, AM, BMJ, BKP, NS2>,
+    BM_CUDA_TRY(cudaFuncSetAttribute(gemm2_kernel<BN, SWIGLU, AM, BMJ, BKP>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
     attr_set = true;
   }
   const int pairs = gemm_sm_budget() / 2;
   const int grid = 2 * (tiles < pairs ? tiles : pairs);
-  BM_CUDA_TRY(launch_k(gemm2_kernel<BN, SWIGLU, AM, BMJ, BKP, NS2>, dim3(grid), dim3(NUM_THREADS2), C::SMEM, st, g));
+  BM_CUDA_TRY(launch_k(gemm2_kernel<BN, SWIGLU, AM, BMJ, BKP>, dim3(grid), dim3(NUM_THREADS2), C::SMEM, st, g));
   count_launch();
   BM_CUDA_TRY(cudaGetLastError());
   return BM_OK;
@@ -1370,10 +1367,6 @@ static int g_raster_group = [] {   // BM_GEMM_GROUP: measurement override of the
   const char* e = getenv("BM_GEMM_GROUP");
   const int v = e ? atoi(e) : 8;
   return v >= 1 ? v : 8;
-}();
-static int g_dsw_variant = [] {
-  const char* e = getenv("BM_DSW_VARIANT");
-  return e ? atoi(e) : 0;
 }();
 static int g_epi_prefetch = [] {
   const char* e = getenv("BM_EPI_PREFETCH");
@@ -1555,18 +1548,6 @@ bm_status gemm_bf16_tc(int M, int N, int K, const void* A, int64_t lda, int a_ma
     BM_TRY(pair_problem(M, N, K, A, lda, a_major, B, ldb, b_major, Cp, ldc, c_dtype, epi, R, ldr, alpha, f, BN2,
                         &g.prob[0]));
     g.nprob = 1;
-    // SwiGLU-backward epilogue variants (BM_DSW_VARIANT: 1 = 128-deep, 2 stages, two staging
-    // slots; 2 = 64-deep, 5 stages, two slots; 0 = the common 128-deep / 1-slot kernel)
-    if (epi == BM_EPI_DSWIGLU && BN2 == 256 && g_dsw_variant && a_major == 0 && b_major == 1) {
-      PairProblem& pr = g.prob[0];
-      if (g_dsw_variant == 1) {
-        BM_TRY(make_map(B, N, K, ldb, 128, &pr.tmB));
-        pr.nk = ceil_div(K, 128);
-      }
-      g.tiles0 = g.total_tiles = pr.tiles_m * pr.tiles_n;
-      if (g_dsw_variant == 1) return launch2<256, false, 0, 1, 128, true>(g, g.total_tiles, st);
-      return launch2<256, false, 0, 1, 64, true>(g, g.total_tiles, st);
-    }
     const bool bk128 = g_bk128 != 0 && BN2 == 256;
     if (bk128) {   // MN-major operands as 64 x 128 boxes; 128-deep K blocks
       PairProblem& pr = g.prob[0];
