@@ -878,16 +878,54 @@ __device__ __forceinline__ void load_gu(const EpiArgs& a, int row, int col0, GU3
   }
 }
 // dg = dh u s (1 + g (1 - s)) -> w, du = dh g s -> v (in place of dh), s = sigmoid(g)
+// packed fp32 pairs (sm_100 FFMA2 / FMUL2): the SwiGLU-backward epilogue is issue-bound
+// (≈ 11 FP32 operations per element against the mainloop's length), so it runs its
+// arithmetic two elements per instruction
+typedef unsigned long long f32x2;
+__device__ __forceinline__ f32x2 f2(float lo, float hi) {
+  return ((f32x2)__float_as_uint(hi) << 32) | (f32x2)__float_as_uint(lo);
+}
+__device__ __forceinline__ float f2lo(f32x2 x) { return __uint_as_float((uint32_t)x); }
+__device__ __forceinline__ float f2hi(f32x2 x) { return __uint_as_float((uint32_t)(x >> 32)); }
+__device__ __forceinline__ f32x2 mul2(f32x2 a, f32x2 b) {
+  f32x2 r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ f32x2 fma2(f32x2 a, f32x2 b, f32x2 c) {
+  f32x2 r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+// two bf16 of one 32-bit word -> fp32 pair (element 2i in lo, 2i + 1 in hi)
+__device__ __forceinline__ f32x2 bf2_to_f2(uint32_t w) {
+  return f2(__uint_as_float(w << 16), __uint_as_float(w & 0xFFFF0000u));
+}
+// dg = dh u s (1 + g (1 - s)) -> w, du = dh g s -> v (in place of dh), s = sigmoid(g)
 __device__ __forceinline__ void dswiglu_math(float alpha, float* v, float* w, const GU32& x) {
+  const f32x2 al = f2(alpha, alpha), half = f2(0.5f, 0.5f), one = f2(1.f, 1.f), mone = f2(-1.f, -1.f);
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
+    const uint32_t* gw = reinterpret_cast<const uint32_t*>(&x.g[j]);
+    const uint32_t* uw = reinterpret_cast<const uint32_t*>(&x.u[j]);
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const float g = __bfloat162float(reinterpret_cast<const bf16*>(&x.g[j])[q]);
-      const float u = __bfloat162float(reinterpret_cast<const bf16*>(&x.u[j])[q]);
-      const float d = alpha * v[8 * j + q], sg = sigmoidf_(g);
-      w[8 * j + q] = d * u * sg * (1.f + g * (1.f - sg));
-      v[8 * j + q] = d * g * sg;
+    for (int q = 0; q < 4; ++q) {
+      const int e = 8 * j + 2 * q;
+      const f32x2 g = bf2_to_f2(gw[q]), u = bf2_to_f2(uw[q]);
+      const f32x2 d = mul2(al, f2(v[e], v[e + 1]));
+      const f32x2 gh = mul2(half, g);
+      float t0, t1;
+      asm("tanh.approx.f32 %0, %1;" : "=f"(t0) : "f"(f2lo(gh)));
+      asm("tanh.approx.f32 %0, %1;" : "=f"(t1) : "f"(f2hi(gh)));
+      const f32x2 sg = fma2(half, f2(t0, t1), half);       // sigmoid(g) = (1 + tanh(g / 2)) / 2
+      const f32x2 b = fma2(g, fma2(mone, sg, one), one);   // 1 + g (1 - s)
+      const f32x2 ds = mul2(d, sg);
+      const f32x2 wg = mul2(mul2(ds, u), b);
+      const f32x2 wu = mul2(ds, g);
+      w[e] = f2lo(wg);
+      w[e + 1] = f2hi(wg);
+      v[e] = f2lo(wu);
+      v[e + 1] = f2hi(wu);
     }
   }
 }
