@@ -1410,9 +1410,16 @@ static int g_epi_prefetch = [] {
   const char* e = getenv("BM_EPI_PREFETCH");
   return e && e[0] == '0' ? 0 : 1;
 }();
-static int g_mbar_cluster = [] {   // default: the fully validated .acquire.cluster waits
+// barrier polls at CTA scope by default (as CUTLASS's waits: every barrier a thread
+// polls lives in its own CTA and guards async-proxy data -- TMA bytes, tcgen05 commits,
+// TMEM ordered by tcgen05 fences -- so no cluster-scope acquire is needed, and each
+// .acquire.cluster poll costs an L1 invalidation, CCTL.IVALL: 27 % of the warp samples
+// of the SwiGLU-backward GEMM, profiles/r02/bn512/ncu_dswiglu_stalls.txt).  Standalone
+// +0.5..+2.5 %, C2 step 52.40 -> 52.55 samples/s (mbar_*.log); BM_MBAR_SCOPE=cluster
+// restores the .acquire.cluster form
+static int g_mbar_cluster = [] {
   const char* e = getenv("BM_MBAR_SCOPE");
-  return e && std::string(e) == "cta" ? 0 : 1;
+  return e && std::string(e) == "cluster" ? 1 : 0;
 }();
 // 0 = auto (CTA pairs for large contractions), 1 = force 1-CTA, 2 = force CTA pairs
 static int g_gemm_mode = [] {
