@@ -95,7 +95,9 @@ typedef struct {
   int32_t ring_slack;    /* >= 0                         */
   int32_t enc_exclude;   /* bit mask of ranks that run no encoder microbatch (below) */
   int32_t cost_wgrad;    /* >= 0; zero-bubble W cost (0 => cost_bwd / 2) */
-  int32_t reserved[4];   /* must be zero                 */
+  int32_t llm_cp;        /* LLM context-parallel degree (0 => 1; below)     */
+  int32_t enc_cp;        /* encoder context-parallel degree (0 => 1)        */
+  int32_t reserved[2];   /* must be zero                 */
 } bm_sched_cfg;
 /* enc_exclude (BM_ENC_DP_UNIT): unit u's microbatch uP + r runs on rank r,
  * unless r is in the mask: then on the nearest lower rank not in it, cyclically
@@ -103,6 +105,18 @@ typedef struct {
  * unit, in microbatch order, and sends / receives their emb / embgrad messages;
  * the masked ranks run none.  Used to keep the encoder off the pipeline stage
  * that paces the step. */
+
+/* Decoupled context parallelism (R25), schedule level:
+ * llm_cp > 1 or enc_cp > 1 builds the nested schedule for P * llm_cp ranks,
+ * rank c P + r = LLM CP index c of stage r (the llm_cp ranks of a stage run the
+ * stage's LLM list in lockstep on their sequence shards).  The encoder runs in CP
+ * groups of enc_cp consecutive ranks, one microbatch per group, so an encoder unit
+ * has P llm_cp / enc_cp microbatches (M must be a multiple: BM_E_REMAINDER); the
+ * CP-conversion all-to-all appears as emb messages from every rank of a
+ * microbatch's encoder group to every stage-0 rank (c P) and embgrad messages
+ * back.  Requires 1 <= enc_cp <= llm_cp, enc_cp | P llm_cp, enc_place NONE or
+ * DP_UNIT, gen_place NONE or LAST_STAGE, enc_exclude 0 (else BM_E_INVALID).  The
+ * executor (bm_ctx_create) runs llm_cp = enc_cp = 1 schedules only. */
 
 /* One operator of a rank's list.  -1 marks an absent field.
  *   EncFwd/EncBwd: mb = unit*P + rank, unit

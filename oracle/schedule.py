@@ -9,6 +9,9 @@ Plain, slow, step-by-step implementation of BigMac's scheduler:
   order property
   zero-bubble base      P:552-556 names zero-bubble pipeline parallelism (Qi et al.)
                         as the next LLM schedule class; ZB-H1 built as in DESIGN.md R23
+  decoupled CP          P:388-398: distinct LLM / encoder CP degrees, encoder unit of
+                        P llm_cp / enc_cp microbatches, CP-conversion all-to-all
+                        (build_cp; schedule level, R25)
 Every reading of an ambiguous passage is listed in DESIGN.md "Readings".
 """
 from __future__ import annotations
@@ -62,6 +65,8 @@ class SchedCfg:
     ring_slack: int = 1         # extra receive slots per channel above the minimum
     enc_exclude: int = 0        # bit mask of ranks running no encoder microbatches (DESIGN R22)
     cost_wgrad: int = 0         # zb_h1: W's share of cost_bwd; 0 => cost_bwd // 2 (R23)
+    llm_cp: int = 1             # LLM context-parallel degree (R25)
+    enc_cp: int = 1             # encoder context-parallel degree
 
 
 @dataclass
@@ -113,9 +118,17 @@ def validate(cfg: SchedCfg) -> None:
         raise ScheduleError(E_INVALID, "unknown enc_place")
     if cfg.gen_place not in ("none", "dp_shard", "last_stage"):
         raise ScheduleError(E_INVALID, "unknown gen_place")
-    if M % P != 0:
-        # units of pp_size micro-batches (partition_microbatches P:248)
-        raise ScheduleError(E_REMAINDER, f"M={M} is not a multiple of P={P}")
+    if cfg.llm_cp < 1 or cfg.enc_cp < 1 or cfg.enc_cp > cfg.llm_cp or (P * cfg.llm_cp) % cfg.enc_cp:
+        # the unit is enlarged from P to P llm_cp / enc_cp microbatches: enc_cp <= llm_cp
+        raise ScheduleError(E_INVALID, "need 1 <= enc_cp <= llm_cp and enc_cp dividing P * llm_cp")
+    cp = cfg.llm_cp > 1 or cfg.enc_cp > 1
+    if cp and (cfg.enc_place == "entry_stage" or cfg.gen_place == "dp_shard" or cfg.enc_exclude):
+        raise ScheduleError(E_INVALID, "decoupled CP: enc_place none / dp_unit, gen_place none / last_stage, "
+                                       "no enc_exclude")
+    unit = P * cfg.llm_cp // cfg.enc_cp
+    if M % unit != 0:
+        # units of pp_size (x llm_cp / enc_cp) micro-batches
+        raise ScheduleError(E_REMAINDER, f"M={M} is not a multiple of the encoder unit {unit}")
     if cfg.enc_exclude:
         full = (1 << P) - 1
         if cfg.enc_exclude < 0 or cfg.enc_exclude & ~full or cfg.enc_exclude == full:
@@ -727,6 +740,8 @@ def order_property(cfg: SchedCfg, ops0):
 # ----------------------------------------------------------------------------
 def build(cfg: SchedCfg) -> Schedule:
     validate(cfg)
+    if cfg.llm_cp > 1 or cfg.enc_cp > 1:
+        return build_cp(cfg)
     P, M, V = cfg.stages, cfg.microbatches, cfg.vchunks
     if cfg.llm_sched == "zb_h1":
         cw = wgrad_cost(cfg)
@@ -791,3 +806,247 @@ def serialize(sched: Schedule) -> str:
             lines.append("\t".join([str(r), str(i), o.kind, _f(o.mb), _f(o.chunk), _f(o.unit),
                                     _f(o.peer), _f(o.payload), _f(o.slot), _f(o.seq)]))
     return "\n".join(lines) + ("\n" if lines else "")
+
+
+# ----------------------------------------------------------------------------
+# decoupled context parallelism (reading R25)
+# ----------------------------------------------------------------------------
+# R = P * llm_cp ranks, rank k = c P + r (LLM CP index c, pipeline stage r): the
+# llm_cp ranks of a stage run the stage's LLM list in lockstep, each on its
+# sequence shard of every microbatch.  The encoder runs in CP groups of enc_cp
+# consecutive ranks, one microbatch per group, so an encoder unit has
+# U = P llm_cp / enc_cp microbatches: microbatch uU + e on group e.  The
+# encoder-to-LLM handoff is the CP-conversion all-to-all, expanded
+# into P2P messages: every rank of m's encoder group sends "emb" to every
+# stage-0 rank (c P) and receives "embgrad" back from each.  The generator runs
+# on the last-stage ranks on their own rows (gen_place last_stage) or not at all.
+def _stage_lists_and_times(cfg):
+    P, M, V = cfg.stages, cfg.microbatches, cfg.vchunks
+    if cfg.llm_sched == "zb_h1":
+        cw = wgrad_cost(cfg)
+        cb = cfg.cost_bwd - cw
+        base = zb_h1_schedule(P, M, cfg.cost_fwd, cb, cw)
+    else:
+        cw, cb = 0, cfg.cost_bwd
+        base = llm_base_schedule(P, M, V)
+    return base, des_llm(base, P, V, cfg.cost_fwd, cb, cw)
+
+
+def cp_encoder_ranks(cfg: SchedCfg, m: int):
+    """Ranks of microbatch m's encoder CP group."""
+    U = cfg.stages * cfg.llm_cp // cfg.enc_cp
+    e = m % U
+    return list(range(e * cfg.enc_cp, (e + 1) * cfg.enc_cp))
+
+
+def cp_stage0_ranks(cfg: SchedCfg):
+    return [c * cfg.stages for c in range(cfg.llm_cp)]
+
+
+def _nest_cp(cfg, base, times):
+    P, M, V = cfg.stages, cfg.microbatches, cfg.vchunks
+    R, U = P * cfg.llm_cp, P * cfg.llm_cp // cfg.enc_cp
+    n_u = M // U
+    enc = cfg.enc_place == "dp_unit"
+    W = (cfg.warmup_units if cfg.warmup_units > 0 else w_star(base[0], U)) if enc else 0
+    events = []
+    for k in range(R):
+        for (kd, m, c) in base[k % P]:
+            st, _ = times[(k % P, kd, m, c)]
+            events.append((st, 2, k, (k, kd, m, c)))
+    if cfg.gen_place != "none":
+        for m in range(M):
+            _, en = times[(P - 1, "F", m, V - 1)]
+            events.append((en, 0, m, ("GEN", m)))
+    if enc:
+        for u in range(n_u):
+            _, en = times[(0, "B", u * U + U - 1, 0)]
+            events.append((en, 1, u, ("ENC", u)))
+    events.sort(key=lambda e: (e[0], e[1], e[2]))
+    lists = [[] for _ in range(R)]
+
+    def unit_ops(kind, u):
+        for k in range(R):
+            for m in range(u * U, u * U + U):
+                if k in cp_encoder_ranks(cfg, m):
+                    lists[k].append(Op(kind, mb=m, unit=u))
+    nxt = 0
+    if enc:
+        for u in range(min(W, n_u)):
+            unit_ops(ENC_FWD, u)
+        nxt = min(W, n_u)
+    for _, cls, _, ev in events:
+        if cls == 2:
+            k, kd, m, c = ev
+            if enc and kd == "F" and k % P == 0 and c == 0 and m // U >= nxt:
+                raise ScheduleError(E_WARMUP, f"W={W} too small: F({m},0)@{k} precedes EncFwd({m // U})")
+            lists[k].append(Op(LLM_KIND[kd], mb=m, chunk=c))
+        elif cls == 0:
+            m = ev[1]
+            for c in range(cfg.llm_cp):
+                lists[c * P + P - 1].append(Op(GEN_FWD, mb=m))
+                lists[c * P + P - 1].append(Op(GEN_BWD, mb=m))
+        else:
+            u = ev[1]
+            unit_ops(ENC_BWD, u)
+            if nxt < n_u:
+                unit_ops(ENC_FWD, nxt)
+                nxt += 1
+    return lists, W
+
+
+def _cp_comm(cfg, k, op):
+    """(recvs before, sends after) of compute op `op` on rank k."""
+    P, V = cfg.stages, cfg.vchunks
+    c, r = divmod(k, P)
+    enc = cfg.enc_place == "dp_unit"
+    before, after = [], []
+    if op.kind in (LLM_FWD, LLM_BWD):
+        s = vstage(P, r, op.chunk)
+    if op.kind == LLM_FWD:
+        if s > 0 and (s - 1) % P != r:
+            before.append(Op(RECV, mb=op.mb, chunk=op.chunk, peer=c * P + (s - 1) % P, payload="act"))
+        if s == 0 and enc:
+            for q in cp_encoder_ranks(cfg, op.mb):
+                if q != k:
+                    before.append(Op(RECV, mb=op.mb, unit=op.mb // (P * cfg.llm_cp // cfg.enc_cp), peer=q,
+                                     payload="emb"))
+        if s < P * V - 1 and (s + 1) % P != r:
+            after.append(Op(SEND, mb=op.mb, chunk=op.chunk, peer=c * P + (s + 1) % P, payload="act"))
+    elif op.kind == LLM_BWD:
+        if s < P * V - 1 and (s + 1) % P != r:
+            before.append(Op(RECV, mb=op.mb, chunk=op.chunk, peer=c * P + (s + 1) % P, payload="grad"))
+        if s > 0 and (s - 1) % P != r:
+            after.append(Op(SEND, mb=op.mb, chunk=op.chunk, peer=c * P + (s - 1) % P, payload="grad"))
+        if s == 0 and enc:
+            for q in cp_encoder_ranks(cfg, op.mb):
+                if q != k:
+                    after.append(Op(SEND, mb=op.mb, unit=op.mb // (P * cfg.llm_cp // cfg.enc_cp), peer=q,
+                                    payload="embgrad"))
+    elif op.kind == ENC_FWD and enc:
+        for q in cp_stage0_ranks(cfg):
+            if q != k:
+                after.append(Op(SEND, mb=op.mb, unit=op.unit, peer=q, payload="emb"))
+    elif op.kind == ENC_BWD and enc:
+        for q in cp_stage0_ranks(cfg):
+            if q != k:
+                before.append(Op(RECV, mb=op.mb, unit=op.unit, peer=q, payload="embgrad"))
+    return before, after
+
+
+def _cp_deps(cfg, k, op):
+    P, V = cfg.stages, cfg.vchunks
+    c, r = divmod(k, P)
+    deps = []
+    if op.kind in (LLM_FWD, LLM_BWD, LLM_W):
+        s = vstage(P, r, op.chunk)
+    if op.kind == LLM_FWD:
+        if s > 0:
+            deps.append((c * P + (s - 1) % P, LLM_FWD, op.mb, (s - 1) // P))
+        elif cfg.enc_place == "dp_unit":
+            deps += [(q, ENC_FWD, op.mb, -1) for q in cp_encoder_ranks(cfg, op.mb)]
+    elif op.kind == LLM_BWD:
+        deps.append((k, LLM_FWD, op.mb, op.chunk))
+        if s < P * V - 1:
+            deps.append((c * P + (s + 1) % P, LLM_BWD, op.mb, (s + 1) // P))
+        elif cfg.gen_place == "last_stage":
+            deps.append((k, GEN_BWD, op.mb, -1))
+    elif op.kind == LLM_W:
+        deps.append((k, LLM_BWD, op.mb, op.chunk))
+    elif op.kind == ENC_BWD:
+        deps.append((k, ENC_FWD, op.mb, -1))
+        deps += [(q, LLM_BWD, op.mb, 0) for q in cp_stage0_ranks(cfg)]
+    elif op.kind == GEN_FWD:
+        deps.append((k, LLM_FWD, op.mb, V - 1))
+    elif op.kind == GEN_BWD:
+        deps.append((k, GEN_FWD, op.mb, -1))
+    return deps
+
+
+def _verify_with(lists, deps_fn):
+    """verify_dependencies with a given producer function (acyclic program order + data)."""
+    nid, n = {}, 0
+    comp = [[op for op in ops if op.kind in COMPUTE_KINDS] for ops in lists]
+    for k, ops in enumerate(comp):
+        for op in ops:
+            key = _ckey(k, op)
+            if key in nid:
+                return [("duplicate", key)]
+            nid[key] = n
+            n += 1
+    edges = []
+    for k, ops in enumerate(comp):
+        for i, op in enumerate(ops):
+            if i:
+                edges.append((nid[_ckey(k, ops[i - 1])], nid[_ckey(k, op)]))
+            for d in deps_fn(k, op):
+                if d not in nid:
+                    return [("missing", d, _ckey(k, op))]
+                edges.append((nid[d], nid[_ckey(k, op)]))
+    return [] if _acyclic(n, edges) else [("cycle",)]
+
+
+def build_cp(cfg: SchedCfg) -> Schedule:
+    """build() for decoupled CP (R25): nesting over P llm_cp ranks with encoder units of
+    P llm_cp / enc_cp microbatches, CP-conversion messages, rings, verification."""
+    P = cfg.stages
+    R, U = P * cfg.llm_cp, P * cfg.llm_cp // cfg.enc_cp
+    base, times = _stage_lists_and_times(cfg)
+    lists, W = _nest_cp(cfg, base, times)
+    viol = _verify_with(lists, lambda k, op: _cp_deps(cfg, k, op))
+    if viol:
+        raise ScheduleError(E_DEPENDENCY, f"dependency violation: {viol[:3]}")
+    for k in range(R):
+        if llm_subsequence(lists[k]) != [tuple(x) for x in base[k % P]]:
+            raise ScheduleError(E_DEPENDENCY, f"LLM order changed on rank {k}")
+    full = []
+    for k in range(R):
+        ops = []
+        for op in lists[k]:
+            before, after = _cp_comm(cfg, k, op)
+            ops += before + [op] + after
+        full.append(ops)
+    send_cnt, recv_cnt = {}, {}
+    for k in range(R):
+        for i, op in enumerate(full[k]):
+            if op.kind == SEND:
+                ch = (k, op.peer, op.payload)
+                full[k][i] = _with(op, seq=send_cnt.get(ch, 0))
+                send_cnt[ch] = send_cnt.get(ch, 0) + 1
+            elif op.kind == RECV:
+                ch = (op.peer, k, op.payload)
+                full[k][i] = _with(op, seq=recv_cnt.get(ch, 0))
+                recv_cnt[ch] = recv_cnt.get(ch, 0) + 1
+    if send_cnt != recv_cnt:
+        raise ScheduleError(E_DEPENDENCY, "unmatched send/recv counts")
+    rings = size_rings(cfg, full, send_cnt)
+    final = assign_slots(full, rings)
+    makespan = max(en for (_, en) in times.values())
+    enc = cfg.enc_place == "dp_unit"
+    ws = w_star(base[0], U) if enc else 0
+    close = LLM_W if cfg.llm_sched == "zb_h1" else LLM_BWD
+    stats = []
+    for k in range(R):
+        busy = sum(en - st for (rr, *_), (st, en) in times.items() if rr == k % P)
+        rs = {p: 0 for p in PAYLOADS}
+        for (src, dst, p), K in rings.items():
+            if dst == k:
+                rs[p] = max(rs[p], K)
+        inflight = cur = 0
+        for o in lists[k]:
+            if o.kind == LLM_FWD:
+                cur += 1
+                inflight = max(inflight, cur)
+            elif o.kind == close:
+                cur -= 1
+        stats.append(Stats(
+            w_star=ws, warmup_units=W if enc else 0,
+            peak_enc_units=peak_window(lists[k], ENC_FWD, ENC_BWD),
+            peak_gen_shards=peak_window(lists[k], GEN_FWD, GEN_BWD),
+            peak_llm_inflight=inflight,
+            llm_idle_cost_units=makespan - busy,
+            makespan_cost_units=makespan,
+            n_ops=len(final[k]),
+            ring_slots=rs))
+    return Schedule(cfg=cfg, ranks=final, stats=stats, rings=rings, llm_base=[base[k % P] for k in range(R)],
+                    times=times)

@@ -36,7 +36,7 @@ class SchedCfg(C.Structure):
                 ("warmup_units", C.c_int32), ("llm_sched", C.c_int32), ("enc_place", C.c_int32),
                 ("gen_place", C.c_int32), ("cost_fwd", C.c_int32), ("cost_bwd", C.c_int32),
                 ("ring_slack", C.c_int32), ("enc_exclude", C.c_int32), ("cost_wgrad", C.c_int32),
-                ("reserved", C.c_int32 * 4)]
+                ("llm_cp", C.c_int32), ("enc_cp", C.c_int32), ("reserved", C.c_int32 * 2)]
 
 
 class Op(C.Structure):

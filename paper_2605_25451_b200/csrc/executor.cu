@@ -126,6 +126,8 @@ static void chunk_of(int64_t count, int n, int q, int64_t* lo, int64_t* hi) {
 static bm_status check_model(const bm_model_cfg& mc, const bm_sched_cfg& sc) {
   BM_CHECK_ARG(mc.S > 0 && mc.d > 0 && mc.f > 0 && mc.L > 0 && mc.vocab > 0, "bad LLM dims");
   BM_CHECK_ARG(mc.d_in > 0 && mc.d_e > 0 && mc.f_e > 0 && mc.L_e >= 0, "bad encoder dims");
+  BM_CHECK_ARG(sc.llm_cp <= 1 && sc.enc_cp <= 1,
+               "decoupled-CP schedules (llm_cp / enc_cp > 1) are built and verified, not executed (DESIGN.md R25)");
   BM_CHECK_ARG(mc.d_g > 0 && mc.f_g > 0 && mc.L_g >= 0 && mc.d_t > 0, "bad generator dims");
   BM_CHECK_ARG(mc.dtype == BM_BF16 || mc.dtype == BM_F32, "dtype must be bf16 or fp32");
   const int PV = sc.stages * sc.vchunks;

@@ -76,9 +76,17 @@ static void validate(const bm_sched_cfg& c) {
     throw Fail{BM_E_INVALID, "unknown enc_place"};
   if (c.gen_place != BM_GEN_NONE && c.gen_place != BM_GEN_DP_SHARD && c.gen_place != BM_GEN_LAST_STAGE)
     throw Fail{BM_E_INVALID, "unknown gen_place"};
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < 2; ++i)
     if (c.reserved[i] != 0) throw Fail{BM_E_INVALID, "reserved fields must be zero"};
-  if (M % P != 0) throw Fail{BM_E_REMAINDER, "M=" + std::to_string(M) + " is not a multiple of P=" + std::to_string(P)};
+  const int lcp = c.llm_cp > 0 ? c.llm_cp : 1, ecp = c.enc_cp > 0 ? c.enc_cp : 1;
+  if (c.llm_cp < 0 || c.enc_cp < 0 || ecp > lcp || (P * lcp) % ecp)
+    throw Fail{BM_E_INVALID, "need 1 <= enc_cp <= llm_cp and enc_cp dividing P * llm_cp"};
+  const bool cp = lcp > 1 || ecp > 1;
+  if (cp && (c.enc_place == BM_ENC_ENTRY_STAGE || c.gen_place == BM_GEN_DP_SHARD || c.enc_exclude))
+    throw Fail{BM_E_INVALID, "decoupled CP: enc_place none / dp_unit, gen_place none / last_stage, no enc_exclude"};
+  const int unit = P * lcp / ecp;
+  if (M % unit != 0)
+    throw Fail{BM_E_REMAINDER, "M=" + std::to_string(M) + " is not a multiple of the encoder unit " + std::to_string(unit)};
   if (c.enc_exclude) {
     const int64_t full = (P >= 31) ? -1 : (((int64_t)1 << P) - 1);
     if (c.enc_exclude < 0 || (P < 31 && ((int64_t)c.enc_exclude & ~full)) || (int64_t)c.enc_exclude == full)
@@ -493,37 +501,14 @@ static int peak_window(const std::vector<bm_op>& ops, int open_k, int close_k) {
   return best;
 }
 
-// ---------------------------------------------------------------- driver
-static bm_schedule* build(const bm_sched_cfg& c) {
-  validate(c);
-  const int P = c.stages, M = c.microbatches, V = c.vchunks;
-  const bool zb = c.llm_sched == BM_LLM_ZB_H1;
-  const int cw = zb ? wgrad_cost(c) : 0, cb = c.cost_bwd - cw;
-  auto base = zb ? zb_h1_lists(P, M, c.cost_fwd, cb, cw) : base_lists(P, M, V);
-  Times T = des_llm(base, P, M, V, c.cost_fwd, cb, cw);
-  int W = 0;
-  auto lists = nest(c, base, T, W);
-  verify_deps(c, lists);
-  for (int r = 0; r < P; ++r) {  // LLM order preserved (P:209)
-    size_t k = 0;
-    for (auto& o : lists[r]) {
-      if (o.kind != BM_OP_LLM_FWD && o.kind != BM_OP_LLM_BWD && o.kind != BM_OP_LLM_W) continue;
-      if (k >= base[r].size() || LLM_OPK[base[r][k].k] != o.kind || base[r][k].mb != o.mb ||
-          base[r][k].chunk != o.chunk)
-        throw Fail{BM_E_DEPENDENCY, "LLM order changed"};
-      ++k;
-    }
-  }
-  // comm insertion + sequence numbers
-  std::vector<std::vector<bm_op>> full(P);
-  for (int r = 0; r < P; ++r)
-    for (auto& o : lists[r]) {
-      recvs_before(c, r, o, full[r]);
-      full[r].push_back(o);
-      sends_after(c, r, o, full[r]);
-    }
+// sequence numbers, ring sizing (P:317 deadlock_check), slots and statistics of a
+// schedule with comm ops; R ranks, rank r running stage r % P's LLM list
+static bm_schedule* finish_schedule(const bm_sched_cfg& c, const std::vector<std::vector<LOp>>& base, const Times& T,
+                                    const std::vector<std::vector<bm_op>>& lists, std::vector<std::vector<bm_op>>& full,
+                                    int W, int ws, bool zb, int cb, int cw, int R) {
+  const int P = c.stages;
   std::map<Chan, int> scnt, rcnt;
-  for (int r = 0; r < P; ++r)
+  for (int r = 0; r < R; ++r)
     for (auto& o : full[r]) {
       if (o.kind == BM_OP_SEND) o.seq = scnt[Chan{r, o.peer, o.payload}]++;
       else if (o.kind == BM_OP_RECV) o.seq = rcnt[Chan{o.peer, r, o.payload}]++;
@@ -553,7 +538,7 @@ static bm_schedule* build(const bm_sched_cfg& c) {
       if (K[kv.first] < kv.second) { ++K[kv.first]; grew = true; }
     if (!grew) throw Fail{BM_E_DEADLOCK, "credit rings cannot be sized"};
   }
-  for (int r = 0; r < P; ++r)
+  for (int r = 0; r < R; ++r)
     for (auto& o : full[r]) {
       if (o.kind == BM_OP_SEND) o.slot = o.seq % K[Chan{r, o.peer, o.payload}];
       else if (o.kind == BM_OP_RECV) o.slot = o.seq % K[Chan{o.peer, r, o.payload}];
@@ -566,8 +551,7 @@ static bm_schedule* build(const bm_sched_cfg& c) {
   int64_t makespan = 0;
   for (auto e : T.en) makespan = std::max(makespan, e);
   const bool enc = c.enc_place == BM_ENC_DP_UNIT;
-  const int ws = enc ? w_star(base[0], P, M) : 0;
-  for (int r = 0; r < P; ++r) {
+  for (int r = 0; r < R; ++r) {
     bm_sched_stats st;
     std::memset(&st, 0, sizeof(st));
     st.w_star = ws;
@@ -578,7 +562,7 @@ static bm_schedule* build(const bm_sched_cfg& c) {
     st.peak_llm_inflight = peak_window(lists[r], BM_OP_LLM_FWD, zb ? BM_OP_LLM_W : BM_OP_LLM_BWD);
     st.n_ops = (int)s->ranks[r].size();
     int64_t busy = 0;
-    for (auto& o : base[r]) busy += o.k == LF ? c.cost_fwd : o.k == LB ? cb : cw;
+    for (auto& o : base[r % P]) busy += o.k == LF ? c.cost_fwd : o.k == LB ? cb : cw;
     st.llm_idle_cost_units = makespan - busy;
     st.makespan_cost_units = makespan;
     for (auto& kv : s->rings)
@@ -589,6 +573,203 @@ static bm_schedule* build(const bm_sched_cfg& c) {
     s->stats.push_back(st);
   }
   return s;
+}
+
+static bm_schedule* build_cp(const bm_sched_cfg& c);
+
+// ---------------------------------------------------------------- driver
+static bm_schedule* build(const bm_sched_cfg& c) {
+  validate(c);
+  if (c.llm_cp > 1 || c.enc_cp > 1) return build_cp(c);
+  const int P = c.stages, M = c.microbatches, V = c.vchunks;
+  const bool zb = c.llm_sched == BM_LLM_ZB_H1;
+  const int cw = zb ? wgrad_cost(c) : 0, cb = c.cost_bwd - cw;
+  auto base = zb ? zb_h1_lists(P, M, c.cost_fwd, cb, cw) : base_lists(P, M, V);
+  Times T = des_llm(base, P, M, V, c.cost_fwd, cb, cw);
+  int W = 0;
+  auto lists = nest(c, base, T, W);
+  verify_deps(c, lists);
+  for (int r = 0; r < P; ++r) {  // LLM order preserved (P:209)
+    size_t k = 0;
+    for (auto& o : lists[r]) {
+      if (o.kind != BM_OP_LLM_FWD && o.kind != BM_OP_LLM_BWD && o.kind != BM_OP_LLM_W) continue;
+      if (k >= base[r].size() || LLM_OPK[base[r][k].k] != o.kind || base[r][k].mb != o.mb ||
+          base[r][k].chunk != o.chunk)
+        throw Fail{BM_E_DEPENDENCY, "LLM order changed"};
+      ++k;
+    }
+  }
+  // comm insertion + sequence numbers
+  std::vector<std::vector<bm_op>> full(P);
+  for (int r = 0; r < P; ++r)
+    for (auto& o : lists[r]) {
+      recvs_before(c, r, o, full[r]);
+      full[r].push_back(o);
+      sends_after(c, r, o, full[r]);
+    }
+  return finish_schedule(c, base, T, lists, full, W, c.enc_place == BM_ENC_DP_UNIT ? w_star(base[0], P, M) : 0, zb,
+                         cb, cw, P);
+}
+
+// ---------------------------------------------------------------- decoupled CP (R25)
+// P llm_cp ranks, rank k = cp P + stage; encoder CP groups of enc_cp consecutive ranks,
+// one microbatch each, units of U = P llm_cp / enc_cp microbatches; the
+// CP-conversion all-to-all as emb / embgrad messages between the microbatch's encoder
+// group and the stage-0 ranks.  Mirrors oracle/schedule.py build_cp.
+static bm_schedule* build_cp(const bm_sched_cfg& c) {
+  const int P = c.stages, M = c.microbatches, V = c.vchunks;
+  const int lcp = c.llm_cp > 0 ? c.llm_cp : 1, ecp = c.enc_cp > 0 ? c.enc_cp : 1;
+  const int R = P * lcp, U = R / ecp, n_u = M / U;
+  const bool zb = c.llm_sched == BM_LLM_ZB_H1;
+  const int cw = zb ? wgrad_cost(c) : 0, cb = c.cost_bwd - cw;
+  auto base = zb ? zb_h1_lists(P, M, c.cost_fwd, cb, cw) : base_lists(P, M, V);
+  Times T = des_llm(base, P, M, V, c.cost_fwd, cb, cw);
+  const bool enc = c.enc_place == BM_ENC_DP_UNIT;
+  const bool gen = c.gen_place != BM_GEN_NONE;
+  const int W = enc ? (c.warmup_units > 0 ? c.warmup_units : w_star(base[0], U, M)) : 0;
+  auto grp_lo = [&](int m) { return (m % U) * ecp; };   // encoder ranks [grp_lo, grp_lo + ecp)
+  // ---- nesting
+  struct Ev {
+    int64_t t;
+    int cls, tb, k, idx;
+  };
+  std::vector<Ev> ev;
+  for (int k = 0; k < R; ++k)
+    for (int i = 0; i < (int)base[k % P].size(); ++i) {
+      const LOp& o = base[k % P][i];
+      ev.push_back({T.st[T.idx(k % P, o.k, o.mb, o.chunk)], 2, k, k, i});
+    }
+  if (gen)
+    for (int m = 0; m < M; ++m) ev.push_back({T.en[T.idx(P - 1, LF, m, V - 1)], 0, m, 0, m});
+  if (enc)
+    for (int u = 0; u < n_u; ++u) ev.push_back({T.en[T.idx(0, LB, u * U + U - 1, 0)], 1, u, 0, u});
+  std::sort(ev.begin(), ev.end(), [](const Ev& a, const Ev& b) {
+    if (a.t != b.t) return a.t < b.t;
+    if (a.cls != b.cls) return a.cls < b.cls;
+    return a.tb < b.tb;
+  });
+  std::vector<std::vector<bm_op>> lists(R);
+  auto unit_ops = [&](int kind, int u) {
+    for (int k = 0; k < R; ++k)
+      for (int m = u * U; m < u * U + U; ++m)
+        if (k >= grp_lo(m) && k < grp_lo(m) + ecp) lists[k].push_back(mk(kind, m, -1, u));
+  };
+  int nxt = 0;
+  if (enc) {
+    for (int u = 0; u < std::min(W, n_u); ++u) unit_ops(BM_OP_ENC_FWD, u);
+    nxt = std::min(W, n_u);
+  }
+  for (const Ev& e : ev) {
+    if (e.cls == 2) {
+      const LOp& o = base[e.k % P][e.idx];
+      if (enc && o.k == LF && e.k % P == 0 && o.chunk == 0 && o.mb / U >= nxt)
+        throw Fail{BM_E_WARMUP, "W=" + std::to_string(W) + " too small: F(" + std::to_string(o.mb) + ",0)@" +
+                                    std::to_string(e.k) + " precedes EncFwd(" + std::to_string(o.mb / U) + ")"};
+      lists[e.k].push_back(mk(LLM_OPK[o.k], o.mb, o.chunk));
+    } else if (e.cls == 0) {
+      for (int cc = 0; cc < lcp; ++cc) {
+        lists[cc * P + P - 1].push_back(mk(BM_OP_GEN_FWD, e.idx));
+        lists[cc * P + P - 1].push_back(mk(BM_OP_GEN_BWD, e.idx));
+      }
+    } else {
+      unit_ops(BM_OP_ENC_BWD, e.idx);
+      if (nxt < n_u) {
+        unit_ops(BM_OP_ENC_FWD, nxt);
+        ++nxt;
+      }
+    }
+  }
+  // ---- verification: program order + data dependencies (incl. the all-to-all) acyclic
+  {
+    std::map<std::tuple<int, int, int, int>, int> nid;
+    auto key = [](int k, const bm_op& o) {
+      const bool llm = o.kind == BM_OP_LLM_FWD || o.kind == BM_OP_LLM_BWD || o.kind == BM_OP_LLM_W;
+      return std::make_tuple(k, o.kind, o.mb, llm ? o.chunk : -1);
+    };
+    int n = 0;
+    for (int k = 0; k < R; ++k)
+      for (auto& o : lists[k]) {
+        auto kk = key(k, o);
+        if (nid.count(kk)) throw Fail{BM_E_DEPENDENCY, "duplicate compute op"};
+        nid[kk] = n++;
+      }
+    std::vector<std::pair<int, int>> edges;
+    auto dep = [&](int k, int kind, int mb, int chunk, int to) {
+      auto it = nid.find(std::make_tuple(k, kind, mb, chunk));
+      if (it == nid.end()) throw Fail{BM_E_DEPENDENCY, "missing producer"};
+      edges.push_back({it->second, to});
+    };
+    for (int k = 0; k < R; ++k) {
+      const int cc = k / P, r = k % P;
+      for (size_t i = 0; i < lists[k].size(); ++i) {
+        const bm_op& o = lists[k][i];
+        const int me = nid[key(k, o)];
+        if (i) edges.push_back({nid[key(k, lists[k][i - 1])], me});
+        const int s = o.chunk * P + r;
+        if (o.kind == BM_OP_LLM_FWD) {
+          if (s > 0) dep(cc * P + (s - 1) % P, BM_OP_LLM_FWD, o.mb, (s - 1) / P, me);
+          else if (enc)
+            for (int q = grp_lo(o.mb); q < grp_lo(o.mb) + ecp; ++q) dep(q, BM_OP_ENC_FWD, o.mb, -1, me);
+        } else if (o.kind == BM_OP_LLM_BWD) {
+          dep(k, BM_OP_LLM_FWD, o.mb, o.chunk, me);
+          if (s < P * V - 1) dep(cc * P + (s + 1) % P, BM_OP_LLM_BWD, o.mb, (s + 1) / P, me);
+          else if (c.gen_place == BM_GEN_LAST_STAGE) dep(k, BM_OP_GEN_BWD, o.mb, -1, me);
+        } else if (o.kind == BM_OP_LLM_W) {
+          dep(k, BM_OP_LLM_BWD, o.mb, o.chunk, me);
+        } else if (o.kind == BM_OP_ENC_BWD) {
+          dep(k, BM_OP_ENC_FWD, o.mb, -1, me);
+          for (int c2 = 0; c2 < lcp; ++c2) dep(c2 * P, BM_OP_LLM_BWD, o.mb, 0, me);
+        } else if (o.kind == BM_OP_GEN_FWD) {
+          dep(k, BM_OP_LLM_FWD, o.mb, V - 1, me);
+        } else if (o.kind == BM_OP_GEN_BWD) {
+          dep(k, BM_OP_GEN_FWD, o.mb, -1, me);
+        }
+      }
+    }
+    if (!acyclic(n, edges, {})) throw Fail{BM_E_DEPENDENCY, "dependency cycle in the nested schedule"};
+  }
+  for (int k = 0; k < R; ++k) {  // LLM order preserved
+    size_t i = 0;
+    const auto& b = base[k % P];
+    for (auto& o : lists[k]) {
+      if (o.kind != BM_OP_LLM_FWD && o.kind != BM_OP_LLM_BWD && o.kind != BM_OP_LLM_W) continue;
+      if (i >= b.size() || LLM_OPK[b[i].k] != o.kind || b[i].mb != o.mb || b[i].chunk != o.chunk)
+        throw Fail{BM_E_DEPENDENCY, "LLM order changed"};
+      ++i;
+    }
+  }
+  // ---- comm insertion: act / grad within a CP index, CP conversion emb / embgrad
+  std::vector<std::vector<bm_op>> full(R);
+  for (int k = 0; k < R; ++k) {
+    const int cc = k / P, r = k % P;
+    for (auto& o : lists[k]) {
+      std::vector<bm_op> before, after;
+      const int s = o.chunk * P + r;
+      if (o.kind == BM_OP_LLM_FWD) {
+        if (s > 0 && (s - 1) % P != r) before.push_back(mk(BM_OP_RECV, o.mb, o.chunk, -1, cc * P + (s - 1) % P, BM_PAY_ACT));
+        if (s == 0 && enc)
+          for (int q = grp_lo(o.mb); q < grp_lo(o.mb) + ecp; ++q)
+            if (q != k) before.push_back(mk(BM_OP_RECV, o.mb, -1, o.mb / U, q, BM_PAY_EMB));
+        if (s < P * V - 1 && (s + 1) % P != r) after.push_back(mk(BM_OP_SEND, o.mb, o.chunk, -1, cc * P + (s + 1) % P, BM_PAY_ACT));
+      } else if (o.kind == BM_OP_LLM_BWD) {
+        if (s < P * V - 1 && (s + 1) % P != r) before.push_back(mk(BM_OP_RECV, o.mb, o.chunk, -1, cc * P + (s + 1) % P, BM_PAY_GRAD));
+        if (s > 0 && (s - 1) % P != r) after.push_back(mk(BM_OP_SEND, o.mb, o.chunk, -1, cc * P + (s - 1) % P, BM_PAY_GRAD));
+        if (s == 0 && enc)
+          for (int q = grp_lo(o.mb); q < grp_lo(o.mb) + ecp; ++q)
+            if (q != k) after.push_back(mk(BM_OP_SEND, o.mb, -1, o.mb / U, q, BM_PAY_EMBGRAD));
+      } else if (o.kind == BM_OP_ENC_FWD && enc) {
+        for (int c2 = 0; c2 < lcp; ++c2)
+          if (c2 * P != k) after.push_back(mk(BM_OP_SEND, o.mb, -1, o.unit, c2 * P, BM_PAY_EMB));
+      } else if (o.kind == BM_OP_ENC_BWD && enc) {
+        for (int c2 = 0; c2 < lcp; ++c2)
+          if (c2 * P != k) before.push_back(mk(BM_OP_RECV, o.mb, -1, o.unit, c2 * P, BM_PAY_EMBGRAD));
+      }
+      for (auto& x : before) full[k].push_back(x);
+      full[k].push_back(o);
+      for (auto& x : after) full[k].push_back(x);
+    }
+  }
+  return finish_schedule(c, base, T, lists, full, W, enc ? w_star(base[0], U, M) : 0, zb, cb, cw, R);
 }
 
 }  // namespace sched

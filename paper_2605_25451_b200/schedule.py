@@ -50,7 +50,7 @@ class Sched:
 
 
 def make_cfg(P, M, V=1, warmup_units=0, llm_sched=None, enc_place="dp_unit", gen_place="dp_shard",
-             cost_fwd=1, cost_bwd=2, ring_slack=1, enc_exclude=0, cost_wgrad=0) -> L.SchedCfg:
+             cost_fwd=1, cost_bwd=2, ring_slack=1, enc_exclude=0, cost_wgrad=0, llm_cp=1, enc_cp=1) -> L.SchedCfg:
     if llm_sched is None:
         llm_sched = "1f1b" if V == 1 else "interleaved"
     c = L.SchedCfg()
@@ -61,6 +61,7 @@ def make_cfg(P, M, V=1, warmup_units=0, llm_sched=None, enc_place="dp_unit", gen
     c.cost_fwd, c.cost_bwd, c.ring_slack = cost_fwd, cost_bwd, ring_slack
     c.enc_exclude = enc_exclude
     c.cost_wgrad = cost_wgrad
+    c.llm_cp, c.enc_cp = llm_cp, enc_cp
     return c
 
 
@@ -68,4 +69,4 @@ def build(P, M, V=1, **kw) -> Sched:
     cfg = make_cfg(P, M, V, **kw)
     h = C.c_void_p()
     L.call("bm_build_schedule", C.byref(cfg), C.byref(h))
-    return Sched(h.value, P)
+    return Sched(h.value, P * max(cfg.llm_cp, 1))

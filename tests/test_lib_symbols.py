@@ -217,3 +217,18 @@ def test_half_layer_units_errors():
         mc = model_cfg(cfg, "bf16", stage_layers=bad, stage_halves=True)
         with pytest.raises(L.BigMacError):
             L.call("bm_param_count", C.byref(mc), C.byref(BS.make_cfg(2, 4, 1)), 0, C.byref(n), C.byref(tot), C.byref(dp))
+
+
+def test_executor_rejects_cp_schedules():
+    """bm_ctx_create runs llm_cp = enc_cp = 1 only (the CP schedule is host-level, R25)."""
+    from synth import get_config
+    from paper_2605_25451_b200 import _lib as L
+    from paper_2605_25451_b200 import schedule as BS
+    from paper_2605_25451_b200.runtime import model_cfg
+    cfg = get_config("C1", P=2, M=8, V=1)
+    mc = model_cfg(cfg, "bf16")
+    sched = BS.build(2, 8, 1, llm_cp=2, gen_place="last_stage")
+    h = C.c_void_p()
+    with pytest.raises(L.BigMacError) as e:
+        L.call("bm_ctx_create", C.byref(mc), sched.handle, 0, C.byref(h))
+    assert e.value.code == 1 and "CP" in str(e.value)

@@ -107,3 +107,34 @@ def test_zb_h1_requires_v1():
     with pytest.raises(L.BigMacError) as e:
         BS.build(2, 4, 2, llm_sched="zb_h1")
     assert e.value.code == 1
+
+
+CP_GRID = [(4, 16, 1, 2, 1), (4, 32, 1, 2, 2), (2, 8, 1, 2, 1), (2, 8, 1, 4, 2), (4, 32, 2, 2, 1),
+           (2, 12, 1, 3, 1), (3, 12, 1, 2, 1), (2, 16, 1, 4, 1), (8, 64, 1, 2, 1), (4, 12, 1, 2, 1), (2, 8, 1, 1, 2)]
+
+
+@pytest.mark.parametrize("P,M,V,lcp,ecp", CP_GRID)
+@pytest.mark.parametrize("kw", [{"gen_place": "last_stage"}, {"gen_place": "none"}, {"enc_place": "none", "gen_place": "none"},
+                                {"gen_place": "last_stage", "llm_sched": "zb_h1"}, {"gen_place": "last_stage", "warmup_units": 3},
+                                {"gen_place": "dp_shard"}])
+def test_cp_serialization_identical(P, M, V, lcp, ecp, kw):
+    """Decoupled CP (reading R25): the C++ builder's P llm_cp-rank lists equal the oracle's."""
+    kw = dict(kw)
+    sched = kw.pop("llm_sched", "1f1b" if V == 1 else "interleaved")
+    if sched == "zb_h1" and V != 1:
+        pytest.skip("ZB-H1 needs V = 1")
+    try:
+        o = S.build(S.SchedCfg(P, M, V, llm_sched=sched, llm_cp=lcp, enc_cp=ecp, **kw))
+    except S.ScheduleError as e:
+        with pytest.raises(L.BigMacError) as ce:
+            BS.build(P, M, V, llm_sched=sched, llm_cp=lcp, enc_cp=ecp, **kw)
+        assert ce.value.code == e.code
+        return
+    c = BS.build(P, M, V, llm_sched=sched, llm_cp=lcp, enc_cp=ecp, **kw)
+    assert c.serialize() == S.serialize(o)
+    for k in range(P * lcp):
+        st, so = c.stats(k), o.stats[k]
+        assert (st.w_star, st.warmup_units, st.peak_enc_units, st.peak_gen_shards, st.peak_llm_inflight, st.n_ops,
+                st.llm_idle_cost_units, st.makespan_cost_units) == \
+            (so.w_star, so.warmup_units, so.peak_enc_units, so.peak_gen_shards, so.peak_llm_inflight, so.n_ops,
+             so.llm_idle_cost_units, so.makespan_cost_units)
