@@ -544,7 +544,7 @@ def run_secondary(args, cx, rank, world, name, cfg, P, D, steps, warmup, with_bu
     return out
 
 
-def run_sweep(args, cx, rank, world, P, ms_list):
+def run_sweep(args, cx, rank, world, P, ms_list, config=None):
     """Peak HBM per GPU and samples/s vs global batch (C5's claim: the
     encoder / generator stash is fixed by the schedule -- W units, one generator shard --
     and the LLM in-flight depth by 1F1B, so peak HBM grows only with the resident inputs)."""
@@ -554,7 +554,7 @@ def run_sweep(args, cx, rank, world, P, ms_list):
     for M in ms_list:
         if M % P:
             continue
-        cfg = get_config(args.config, P=P, M=M, V=1)
+        cfg = get_config(config or args.config, P=P, M=M, V=1)
         torch.cuda.empty_cache()
         torch.cuda.reset_peak_memory_stats()
         rt, W, _, _ = make_runtime(args, cfg, P, rank, world, cx.group)
@@ -597,6 +597,9 @@ def main():
     ap.add_argument("--sweep", default="8,16,32,64,128,256", help="global batches of the peak-HBM sweep ('' = off)")
     ap.add_argument("--c4-steps", type=int, default=2)
     ap.add_argument("--no-c4-strong", action="store_true", help="skip the C4 strong-scaling line at N > 1")
+    ap.add_argument("--c5", action="store_true", help="run the C5 sweep (default: when N >= --c5-stages)")
+    ap.add_argument("--c5-stages", type=int, default=8)
+    ap.add_argument("--c5-sweep", default="8,16,32,64,128,256", help="global batches of the C5 sweep")
     ap.add_argument("--ref-layers", type=int, default=1, help="LLM layers of the oracle sample")
     ap.add_argument("--ref-seq-div", type=int, default=2, help="the oracle sample runs S / this positions")
     ap.add_argument("--head", default="auto", choices=["auto", "last_stage", "dp_shard"],
@@ -741,6 +744,16 @@ def main():
             # the same workload on the ZB-H1 zero-bubble base schedule (reading R23)
             extra["zb_h1"] = run_secondary(args, cx, rank, world, cfg.name, cfg.replace(llm_sched="zb_h1"), P, D,
                                            max(3, args.steps // 2), 3)
+        c5p = args.c5_stages
+        if (N >= c5p or args.c5) and N % c5p == 0 and args.config == "C2" and not args.microbatches:
+            # BASELINE configs[4] (C5): the C4 model on 8 stages, global batch 8 -> 256
+            try:
+                extra["c5_sweep"] = {"config": f"C5: C4 model (7B-shaped LLM, S = 8192), P = {c5p} x D = {N // c5p}, "
+                                               f"bigmac, 1F1B, 1 timed step per M",
+                                     "points": run_sweep(args, cx, rank, world, c5p,
+                                                         [int(x) for x in args.c5_sweep.split(",") if x], "C4")}
+            except Exception as e:   # the main line must survive a failed secondary
+                extra["c5_sweep"] = {"error": repr(e)[:300]}
         if args.sweep:
             extra["batch_sweep"] = {"config": f"{args.config} model, P = {P} x D = {D}, bigmac, 1 timed step per "
                                               f"per-replica M",
