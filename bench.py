@@ -415,9 +415,16 @@ def lightest_only_mask(costs):
     return sum(1 << r for r, c in enumerate(costs) if c > mn + 1e-9)
 
 
+def rank_costs(cfg, P, split):
+    """Per-rank cost of a half-layer partition: the rank's virtual stages summed
+    (rank r holds virtual stages r, r + P, ...; interleaved V > 1)."""
+    vc = unit_costs(cfg, split)
+    return [sum(vc[s] for s in range(r, len(vc), P)) for r in range(P)]
+
+
 def _pacing(args, cfg, P, split):
-    if getattr(args, "partition", "layers") == "halves" and split and len(split) == P:
-        return lightest_only_mask(unit_costs(cfg, split))
+    if getattr(args, "partition", "layers") == "halves" and split and len(split) == P * cfg.V:
+        return lightest_only_mask(rank_costs(cfg, P, split))
     return pacing_stage_mask(split, P)
 
 
@@ -443,9 +450,9 @@ def enc_exclude(args, cfg, P, split, strategy):
         # room for both (slack >= ENC_GEN_LAYERS): C2 N = 4 (slack 0.64) 188.5 vs 180.9
         # samples/s with it everywhere; C2 N = 2 (slack 0.3) 94.2 everywhere vs 90.4
         # (profiles/r02/zb/ab_place_n4.log, ab_n2.log, final/bench_n4_final.log)
-        if not split or len(split) != P:
+        if not split or len(split) != P * cfg.V:
             return 0
-        costs = unit_costs(cfg, split)
+        costs = rank_costs(cfg, P, split)
         return lightest_only_mask(costs) if max(costs) - min(costs) >= ENC_GEN_LAYERS else 0
     return _pacing(args, cfg, P, split)
 
