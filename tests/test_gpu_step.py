@@ -329,6 +329,10 @@ MR_CASES = [
     ("C1", 4, 8, 1, "bf16", "dp_shard+halves3-2-2-1+genx7+encx7", 1, ""),
     ("C1", 4, 8, 1, "f32", "dp_shard+halves3-2-2-1+genx7+encx7+zb", 1, ""),
     ("C1", 2, 4, 1, "bf16", "dp_shard+halves5-3+genx1+encx1", 2, ""),
+    # the N = 8 bench shape: P = 4 stages x D = 2 replicas (world 8), half-layer units,
+    # encoder / generator on the lightest stage
+    ("C1", 4, 8, 1, "bf16", "dp_shard+halves3-2-2-1+genx7+encx7", 2, ""),
+    ("C1", 4, 8, 1, "f32", "dp_shard+halves3-2-2-1+genx7+encx7+zb", 2, ""),
     # P = 2 x D = 2
     ("C1", 2, 4, 1, "f32", "dp_shard", 2, ""), ("C1", 2, 4, 1, "bf16", "dp_shard", 2, ""),
     ("C1", 2, 8, 2, "f32", "dp_shard", 2, ""), ("C1", 2, 4, 1, "f32", "dp_shard", 2, "peer"),
