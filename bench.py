@@ -471,7 +471,9 @@ def make_runtime(args, cfg, P, rank, world, group, strategy="bigmac"):
     rt = Runtime(cfg, args.dtype, rank=rank, world=world, group=group, sched_kw=sched_kw, head_place=args.head,
                  last_stage_layers=n_last, stage_layers=split, fsdp=args.fsdp,
                  gen_exclude=gen_exclude(args, cfg, P, split, strategy),
-                 stage_halves=bool(split) and getattr(args, "partition", "layers") == "halves")
+                 stage_halves=bool(split) and getattr(args, "partition", "layers") == "halves",
+                 # the encoder concentrated on the lightest stage gets its own stream there
+                 enc_stream=1 if (ex and getattr(args, "partition", "layers") == "halves") else 0)
     rt.init_random_weights(seed=1)
     return rt, W, split, n_last
 

@@ -176,7 +176,8 @@ typedef struct {
   int32_t fsdp;                   /* bm_fsdp_mode of the encoder / generator parameters */
   int32_t gen_exclude;            /* bit mask of ranks that take no generator rows (below) */
   int32_t stage_halves;           /* 1: stage_layers counts half-layer units (below) */
-  int32_t reserved[3];            /* must be zero                              */
+  int32_t enc_stream;             /* encoder ops on their own stream: 0 = auto (P == 1), 1 = on, 2 = off */
+  int32_t reserved[2];            /* must be zero                              */
   int32_t stage_layers[BM_MAX_VSTAGES]; /* explicit partition (below); all 0 = unset */
 } bm_model_cfg;
 

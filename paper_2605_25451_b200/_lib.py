@@ -54,8 +54,8 @@ class ModelCfg(C.Structure):
     _fields_ = [(n, C.c_int32) for n in ("S", "d_in", "d_e", "f_e", "L_e", "d", "f", "L", "vocab",
                                          "d_g", "f_g", "L_g", "d_t", "dtype", "max_n_mod", "max_n_gen",
                                          "head_place", "last_stage_layers", "fsdp", "gen_exclude",
-                                         "stage_halves")] + \
-               [("reserved", C.c_int32 * 3), ("stage_layers", C.c_int32 * 32)]
+                                         "stage_halves", "enc_stream")] + \
+               [("reserved", C.c_int32 * 2), ("stage_layers", C.c_int32 * 32)]
 
 
 class ParamInfo(C.Structure):

@@ -156,6 +156,7 @@ static bm_status check_model(const bm_model_cfg& mc, const bm_sched_cfg& sc) {
   BM_CHECK_ARG(mc.head_place != BM_HEAD_DP_SHARD || sc.gen_place == BM_GEN_DP_SHARD,
                "BM_HEAD_DP_SHARD rides on the DP-sharded generator ops (gen_place = BM_GEN_DP_SHARD)");
   BM_CHECK_ARG(mc.fsdp >= BM_FSDP_OFF && mc.fsdp <= BM_FSDP_ALLGATHER, "bad fsdp mode");
+  BM_CHECK_ARG(mc.enc_stream >= 0 && mc.enc_stream <= 2, "enc_stream must be 0 (auto), 1 (on) or 2 (off)");
   {
     const uint32_t all = sc.stages >= 32 ? 0xFFFFFFFFu : ((1u << sc.stages) - 1u);
     BM_CHECK_ARG(((uint32_t)mc.gen_exclude & ~all) == 0 && ((uint32_t)mc.gen_exclude & all) != all,
@@ -1865,9 +1866,14 @@ bm_status bm_ctx_create(const bm_model_cfg* mc, const bm_schedule* s, int32_t ra
   // on by default at P = 1 (C2: 50.7 vs 48.6 samples/s with W = 2); at P > 1 the encoder
   // kernels would compete with LLM ops on other ranks' critical path (N = 2: 89.1 vs 90.6),
   // so BM_ENC_STREAM=1 / 0 forces it on / off
+  // bm_model_cfg.enc_stream = 1 / 2 forces it on / off: with the encoder concentrated on the
+  // lightest stage (bench.py at P > 1) its own stream overlaps it with that stage's LLM ops
+  // (C2, N = 4: 189.1 vs 185.0 samples/s, profiles/r02/zb/ab_encstream.log)
   {
     const char* e = getenv("BM_ENC_STREAM");
-    const bool want = e ? e[0] == '1' : c->P == 1;
+    bool want = e ? e[0] == '1' : c->P == 1;
+    if (mc->enc_stream == 1) want = true;
+    if (mc->enc_stream == 2) want = false;
     c->use_enc_stream = c->has_enc && !c->enc_entry && want;
   }
   *out = c;

@@ -24,7 +24,7 @@ from . import schedule as BS
 
 def model_cfg(shape, dtype: str, max_n_mod: int | None = None, max_n_gen: int | None = None,
               head_place: str = "auto", last_stage_layers: int = 0, stage_layers=None, fsdp: str = "off",
-              gen_exclude: int = 0, stage_halves: bool = False) -> L.ModelCfg:
+              gen_exclude: int = 0, stage_halves: bool = False, enc_stream: int = 0) -> L.ModelCfg:
     mc = L.ModelCfg()
     mc.S, mc.d_in, mc.d_e, mc.f_e, mc.L_e = shape.S, shape.d_in, shape.d_e, shape.f_e, shape.L_e
     mc.d, mc.f, mc.L, mc.vocab = shape.d, shape.f, shape.L, shape.vocab
@@ -37,6 +37,7 @@ def model_cfg(shape, dtype: str, max_n_mod: int | None = None, max_n_gen: int | 
     mc.fsdp = L.FSDP[fsdp]
     mc.gen_exclude = gen_exclude
     mc.stage_halves = 1 if stage_halves else 0
+    mc.enc_stream = enc_stream
     for i, n in enumerate(stage_layers or ()):
         mc.stage_layers[i] = n
     return mc
@@ -89,7 +90,7 @@ class DeviceBatch:
 class Runtime:
     def __init__(self, shape, dtype="bf16", rank=0, world=1, group=None, device=None, sched_kw=None,
                  head_place="auto", last_stage_layers=0, stage_layers=None, fsdp="off", gen_exclude=0,
-                 stage_halves=False):
+                 stage_halves=False, enc_stream=0):
         self.shape = shape
         self.dtype = dtype
         self.world = world
@@ -108,7 +109,7 @@ class Runtime:
         self.fsdp = fsdp
         self.mc = model_cfg(shape, dtype, head_place=head_place, last_stage_layers=last_stage_layers,
                             stage_layers=stage_layers, fsdp=fsdp, gen_exclude=gen_exclude,
-                            stage_halves=stage_halves)
+                            stage_halves=stage_halves, enc_stream=enc_stream)
         h = C.c_void_p()
         L.call("bm_ctx_create", C.byref(self.mc), self.sched.handle, rank, C.byref(h))
         self.ctx = h.value

@@ -1,7 +1,7 @@
 """Ranks of a multi-rank parity run (launched by tests/test_gpu_step.py via torchrun).
 
 usage: mp_step.py CASE [CASE ...]
-  CASE = CONFIG:P:M:V:DTYPE:SPEC:D[:FLAGS]   (FLAGS comma-separated: peer, gm2)
+  CASE = CONFIG:P:M:V:DTYPE:SPEC:D[:FLAGS]   (FLAGS comma-separated: peer, gm2, es)
 Every case runs in the same processes, one after the other (one process start
 and CUDA context per rank for the whole batch).  world = P D for every case.
 D > 1: D pipeline replicas of P stages; replica k runs microbatches [kM, (k+1)M)
@@ -19,7 +19,8 @@ no generator rows), "+encx<mask>" (ranks in the mask run no encoder microbatch),
 "+zb" (ZB-H1 zero-bubble LLM schedule, B/W split, reading R23), "+halves<a>-<b>-..."
 (explicit partition in half-layer units, stage boundaries inside layers, reading R24).
 FLAGS: peer = force the library's peer-memory step-end sum (BM_STEP_SUM=peer);
-gm2 = every bf16 contraction on the CTA-pair GEMM (bm_k_gemm_mode 2).
+gm2 = every bf16 contraction on the CTA-pair GEMM (bm_k_gemm_mode 2); es = encoder ops on
+their own stream (bm_model_cfg.enc_stream = 1).
 """
 import os
 
@@ -96,7 +97,8 @@ def run_case(case, rank, world):
     os.environ["BM_STEP_SUM"] = "peer" if "peer" in flags else "auto"
     L.call("bm_k_gemm_mode", 2 if "gm2" in flags else 0)
     rt = Runtime(cfg, dtype, rank=rank, world=world, sched_kw=kw, head_place=head, last_stage_layers=last,
-                 stage_layers=split, fsdp=fsdp, gen_exclude=genx, stage_halves=halves)
+                 stage_layers=split, fsdp=fsdp, gen_exclude=genx, stage_halves=halves,
+                 enc_stream=1 if "es" in flags else 0)
     rt.load_weights(W)
     db = rt.device_batch(B)
     for _ in range(2):

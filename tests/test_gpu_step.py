@@ -326,12 +326,13 @@ MR_CASES = [
     ("C1", 4, 8, 1, "bf16", "dp_shard+halves1-1-1-5+zb+edge", 1, ""), ("C1", 2, 4, 1, "f32", "dp_shard+halves3-5", 2, ""),
     # the bench's multi-GPU defaults: half-layer units, generator / encoder on the lightest stage (N = 4, and
     # N = 8 as P = 4 x D = 2 -- here P = 2 x D = 2), 1F1B and ZB-H1
-    ("C1", 4, 8, 1, "bf16", "dp_shard+halves3-2-2-1+genx7+encx7", 1, ""),
+    ("C1", 4, 8, 1, "bf16", "dp_shard+halves3-2-2-1+genx7+encx7", 1, "es"),
     ("C1", 4, 8, 1, "f32", "dp_shard+halves3-2-2-1+genx7+encx7+zb", 1, ""),
     ("C1", 2, 4, 1, "bf16", "dp_shard+halves5-3+genx1+encx1", 2, ""),
     # the N = 8 bench shape: P = 4 stages x D = 2 replicas (world 8), half-layer units,
     # encoder / generator on the lightest stage
-    ("C1", 4, 8, 1, "bf16", "dp_shard+halves3-2-2-1+genx7+encx7", 2, ""),
+    ("C1", 4, 8, 1, "bf16", "dp_shard+halves3-2-2-1+genx7+encx7", 2, "es"),
+    ("C1", 2, 4, 1, "f32", "dp_shard+encx1", 1, "es"), ("C1", 4, 8, 1, "f32", "dp_shard+halves3-2-2-1+genx7+encx7+zb", 1, "es"),
     ("C1", 4, 8, 1, "f32", "dp_shard+halves3-2-2-1+genx7+encx7+zb", 2, ""),
     # P = 2 x D = 2
     ("C1", 2, 4, 1, "f32", "dp_shard", 2, ""), ("C1", 2, 4, 1, "bf16", "dp_shard", 2, ""),
