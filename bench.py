@@ -733,41 +733,50 @@ def main():
     free_runtime(rt)
     del db
 
-    # ---------------- secondary configuration and the batch sweep
+    # ---------------- secondary configurations and the sweeps (a failing secondary is
+    # reported in its key; the main line above is kept)
     extra = {}
+
+    def secondary(key, fn):
+        try:
+            extra[key] = fn()
+        except Exception as e:   # deterministic failures raise on every rank alike
+            import torch
+            torch.cuda.empty_cache()
+            extra[key] = {"error": repr(e)[:300]}
+
     if not args.no_extra:
         if N == 1:
             # the largest single-GPU workload: C4 (7B-shaped LLM, S = 8192) at P = 1, M = 64
             c4 = get_config("C4", P=1, M=64, V=1)
-            extra["c4_single_gpu"] = run_secondary(args, cx, rank, world, "C4", c4, 1, 1, args.c4_steps, 1)
+            secondary("c4_single_gpu", lambda: run_secondary(args, cx, rank, world, "C4", c4, 1, 1, args.c4_steps, 1))
         elif args.config == "C2" and not args.microbatches:
             # BASELINE.json configs[1]: 16 microbatches per pipeline (global batch 16 D)
             c2 = get_config("C2", P=P, M=16, V=1)
-            extra["c2_m16_per_replica"] = run_secondary(args, cx, rank, world, "C2", c2, P, D, max(3, args.steps // 2), 3)
+            secondary("c2_m16_per_replica",
+                      lambda: run_secondary(args, cx, rank, world, "C2", c2, P, D, max(3, args.steps // 2), 3))
         if N > 1 and args.config == "C2" and not args.microbatches and not args.no_c4_strong:
             # SURVEY §8(d) strong-scaling ladder: the C4 model (7B-shaped LLM, S = 8192) at
             # P = min(N, 4) stages x D replicas over one global batch of 64 microbatches
-            c4 = get_config("C4", P=P, M=64 // D, V=1)
-            extra["c4_strong"] = run_secondary(args, cx, rank, world, "C4", c4, P, D, 2, 2, with_bubble=False)
+            c4s = get_config("C4", P=P, M=64 // D, V=1)
+            secondary("c4_strong", lambda: run_secondary(args, cx, rank, world, "C4", c4s, P, D, 2, 2,
+                                                         with_bubble=False))
         if N > 1 and cfg.V == 1 and cfg.llm_sched != "zb_h1":
             # the same workload on the ZB-H1 zero-bubble base schedule (reading R23)
-            extra["zb_h1"] = run_secondary(args, cx, rank, world, cfg.name, cfg.replace(llm_sched="zb_h1"), P, D,
-                                           max(3, args.steps // 2), 3)
+            secondary("zb_h1", lambda: run_secondary(args, cx, rank, world, cfg.name, cfg.replace(llm_sched="zb_h1"),
+                                                     P, D, max(3, args.steps // 2), 3))
         c5p = args.c5_stages
         if (N >= c5p or args.c5) and N % c5p == 0 and args.config == "C2" and not args.microbatches:
             # BASELINE configs[4] (C5): the C4 model on 8 stages, global batch 8 -> 256
-            try:
-                extra["c5_sweep"] = {"config": f"C5: C4 model (7B-shaped LLM, S = 8192), P = {c5p} x D = {N // c5p}, "
-                                               f"bigmac, 1F1B, 1 timed step per M",
-                                     "points": run_sweep(args, cx, rank, world, c5p,
-                                                         [int(x) for x in args.c5_sweep.split(",") if x], "C4")}
-            except Exception as e:   # the main line must survive a failed secondary
-                extra["c5_sweep"] = {"error": repr(e)[:300]}
+            secondary("c5_sweep", lambda: {
+                "config": f"C5: C4 model (7B-shaped LLM, S = 8192), P = {c5p} x D = {N // c5p}, bigmac, 1F1B, "
+                          f"1 timed step per M",
+                "points": run_sweep(args, cx, rank, world, c5p, [int(x) for x in args.c5_sweep.split(",") if x],
+                                    "C4")})
         if args.sweep:
-            extra["batch_sweep"] = {"config": f"{args.config} model, P = {P} x D = {D}, bigmac, 1 timed step per "
-                                              f"per-replica M",
-                                    "points": run_sweep(args, cx, rank, world, P,
-                                                        [int(x) for x in args.sweep.split(",") if x])}
+            secondary("batch_sweep", lambda: {
+                "config": f"{args.config} model, P = {P} x D = {D}, bigmac, 1 timed step per per-replica M",
+                "points": run_sweep(args, cx, rank, world, P, [int(x) for x in args.sweep.split(",") if x])})
 
     if rank != 0:
         cx.barrier()
