@@ -366,7 +366,8 @@ def run_cp(sched, cfg, weights, batch):
             return out
         if op.kind == LLM_BWD:
             s = vstage(P, r, op.chunk)
-            ent = llm_stash[k].pop((m, op.chunk))
+            zb = sc.llm_sched == "zb_h1"      # B = input gradient; stash kept until W (R23)
+            ent = llm_stash[k][(m, op.chunk)] if zb else llm_stash[k].pop((m, op.chunk))
             if s == P * V - 1:
                 dHn = ent["dHn"].copy()
                 g_lo, g_hi = ent["gen_rows"]
@@ -377,7 +378,9 @@ def run_cp(sched, cfg, weights, batch):
                 dy = local[k].pop(("grad", m, s + 1))
             else:
                 dy = take(k, "grad", m, c * P + (s + 1) % P)
-            dx = om.llm_layers_bwd(W, cfg, om.stage_layers(cfg, s), ent["caches"], dy, G[k])
+            if zb:
+                ent["defer"] = []
+            dx = om.llm_layers_bwd(W, cfg, om.stage_layers(cfg, s), ent["caches"], dy, G[k], ent.get("defer"))
             out = {}
             if s == 0:
                 nm_loc = max(0, min(n_mod, hi) - lo)
@@ -395,6 +398,9 @@ def run_cp(sched, cfg, weights, batch):
                     local[k][("grad", m, s)] = dx
                 out["grad"] = dx
             return out
+        if op.kind == LLM_W:
+            om.llm_wgrad(llm_stash[k].pop((m, op.chunk)).pop("defer"), G[k])
+            return {}
         if op.kind == GEN_FWD:
             X = local[k].pop(("genin", m))
             lo_g, hi_g = llm_stash[k][(m, V - 1)]["gen_rows"]

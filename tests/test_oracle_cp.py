@@ -178,10 +178,12 @@ def test_cp_errors():
         assert e.value.code == S.E_INVALID
 
 
-@pytest.mark.parametrize("P,M,V,lcp,ecp,edge", [(2, 8, 1, 2, 1, False), (2, 8, 1, 2, 2, False), (4, 16, 1, 2, 1, False),
-                                                (2, 8, 1, 4, 2, False), (2, 8, 2, 2, 1, False), (2, 16, 1, 4, 1, False),
-                                                (2, 8, 1, 2, 2, True), (4, 16, 1, 2, 1, True)])
-def test_cp_interpreter_equals_sequential(P, M, V, lcp, ecp, edge):
+@pytest.mark.parametrize("P,M,V,lcp,ecp,edge,zb", [(2, 8, 1, 2, 1, False, False), (2, 8, 1, 2, 2, False, False),
+                                                   (4, 16, 1, 2, 1, False, False), (2, 8, 1, 4, 2, False, False),
+                                                   (2, 8, 2, 2, 1, False, False), (2, 16, 1, 4, 1, False, False),
+                                                   (2, 8, 1, 2, 2, True, False), (4, 16, 1, 2, 1, True, False),
+                                                   (2, 8, 1, 2, 1, False, True), (4, 16, 1, 2, 2, True, True)])
+def test_cp_interpreter_equals_sequential(P, M, V, lcp, ecp, edge, zb):
     """The fp64 interpreter executes the CP schedule with sequence-sharded LLM ranks,
     row-sharded encoder CP groups and the CP-conversion messages carrying the row
     intersections; loss and every gradient equal the sequential reference,
@@ -201,7 +203,9 @@ def test_cp_interpreter_equals_sequential(P, M, V, lcp, ecp, edge):
     else:
         W, B = make_weights(cfg), make_batch(cfg)
     loss, per, G = om.step_fp64(cfg, W, B)
-    s = S.build(cfg_of(P, M, V, llm_cp=lcp, enc_cp=ecp, gen_place="last_stage"))
+    kw = {"llm_sched": "zb_h1"} if zb else {}
+    s = S.build(S.SchedCfg(P, M, V, llm_sched=kw.get("llm_sched", "1f1b" if V == 1 else "interleaved"),
+                           llm_cp=lcp, enc_cp=ecp, gen_place="last_stage"))
     loss2, per2, G2 = interp.run_cp(s, cfg, W, B)
     assert abs(loss2 - loss) <= 1e-12 * abs(loss)
     assert np.allclose(per2, per, rtol=1e-12, atol=1e-15)
